@@ -1,0 +1,814 @@
+"""CPU oracle for the Superfast LSE inner loop -- TEST INFRASTRUCTURE ONLY.
+
+This module is a plain-numpy restatement of the reference algorithm
+(`superlse`, /root/reference/pkg/src/superlse) for the complete-data,
+single-snapshot (G = 1) superfast path.  It exists for three purposes only:
+
+* the checker in ``tests/`` (parity of the CUDA path against it),
+* ``__graft_entry__.smoke()`` (one small check on cuda:0),
+* the ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py``.
+
+The product path (``paper_1705_06073_b200``) never imports it.
+
+Pinning: the oracle is checked against golden vectors produced by the real
+reference (``tests/golden/make_golden.py`` imports /root/reference in the
+build container and writes ``tests/golden/*.npz``); see
+``tests/test_oracle_golden.py``.
+
+Algorithm choices (each equivalent within ~1e-13 to the reference's own
+``auto`` dispatch, as measured in SURVEY.md section 8(c)):
+
+* Toeplitz factor: Levinson-Durbin at every N (reference: LD for N <= 256,
+  divide-and-conquer Schur above; toeplitz.py:263-276).  LD is also the
+  faster of the two in numpy.
+* Off-grid Fourier sums: direct O(NK) sums at every N (reference: direct
+  below N = 512, Gaussian-gridding NUFFT above; nufft.py:118-123).
+
+Every function cites the reference file:line it restates.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from math import comb
+
+import numpy as np
+
+# --- constants (reference values) -------------------------------------------
+PD_EPS = 1e-13                       # toeplitz.py:32
+BETA_FLOOR_SCALE = 1e-12             # model_core.py:36
+DEFAULT_TAU = 5.0                    # smlr.py:28
+EPS_OBJECTIVE = float(np.finfo(np.float64).eps)  # smlr.py:31
+SWEEP_WITHIN_FACTOR = 5.0            # smlr.py:35
+SWEEP_MIN_SPACING_SCALE = 0.05       # smlr.py:36
+GAMMA_BAR_K_INIT = 4                 # smlr.py:40
+MAX_PAIRS = 10                       # lbfgs.py:19
+ARMIJO_C1 = 1e-4                     # lbfgs.py:21
+BACKTRACK_FACTOR = 0.5               # lbfgs.py:22
+MAX_BACKTRACKS = 30                  # lbfgs.py:23
+CURVATURE_EPS = 1e-12                # lbfgs.py:26
+INITIAL_ZETA = 0.2                   # estimator.py:30
+INITIAL_BETA_ENERGY_FRACTION = 0.01  # estimator.py:31
+
+STAGES = ("init", "beta", "activate", "zeta", "refine", "deactivate")
+
+
+class OracleNotPD(Exception):
+    """Mirror of superlse.errors.NotPositiveDefinite (errors.py:8)."""
+
+
+class OracleLineSearchFailed(Exception):
+    """Mirror of superlse.errors.LineSearchFailed (errors.py:28)."""
+
+
+# --- grid size / prior --------------------------------------------------------
+def default_grid_size(n, grid_factor=8):
+    """model_core.py:224-227."""
+    target = max(2 * n, grid_factor * n)
+    return 1 << int(np.ceil(np.log2(target)))
+
+
+def prior_zeta(zeta, k_max):
+    """model_core.py:230-234."""
+    return float(min(max(zeta, 0.5 / k_max), 0.5))
+
+
+def prior_term(k_hat, zeta, k_max):
+    """model_core.py:237-239."""
+    ze = prior_zeta(zeta, k_max)
+    return -(k_hat * np.log(ze) + (k_max - k_hat) * np.log1p(-ze))
+
+
+def wrap_distance(x, y):
+    """simdata.py:50-53."""
+    d = np.abs(np.asarray(x, dtype=np.float64) - np.asarray(y, dtype=np.float64)) % 1.0
+    return np.minimum(d, 1.0 - d)
+
+
+# --- Row 1: Toeplitz column ---------------------------------------------------
+def steer_forward(thetas, coeffs, n):
+    """sum_k coeffs_k e^{j 2 pi m theta_k}, m = 0..n-1 (nufft.py:126-144, direct
+    branch :139-141)."""
+    thetas = np.asarray(thetas, dtype=np.float64)
+    coeffs = np.asarray(coeffs, dtype=np.complex128)
+    if thetas.size == 0:
+        return np.zeros(n, dtype=np.complex128)
+    basis = np.exp(2j * np.pi * np.outer(np.arange(n), thetas))
+    return basis @ coeffs
+
+
+def steer_adjoint(thetas, x):
+    """sum_m x_m e^{-j 2 pi m theta_k} (nufft.py:147-159, direct :156-158)."""
+    thetas = np.asarray(thetas, dtype=np.float64)
+    x = np.asarray(x, dtype=np.complex128)
+    n = x.shape[0]
+    if thetas.size == 0:
+        return np.zeros((0,) + x.shape[1:], dtype=np.complex128)
+    basis = np.exp(-2j * np.pi * np.outer(thetas, np.arange(n)))
+    return basis @ x
+
+
+def fourier_sum_two_sided(thetas, omega):
+    """sum_{i=-(N-1)}^{N-1} omega(i) e^{j 2 pi i theta} (nufft.py:162-181)."""
+    omega = np.asarray(omega, dtype=np.complex128)
+    vec = omega.ndim == 1
+    if vec:
+        omega = omega[:, None]
+    n = (omega.shape[0] + 1) // 2
+    pos = omega[n - 1:]
+    neg = np.zeros_like(pos)
+    neg[1:] = omega[n - 2::-1]
+    out = np.conj(steer_adjoint(thetas, np.conj(pos))) + steer_adjoint(thetas, neg)
+    return out[:, 0] if vec else out
+
+
+def cov_column(thetas, gammas, beta, n):
+    """c_m = beta [m == 0] + sum_k gamma_k e^{j2 pi m theta_k}
+    (model_core.py:242-249 and :264-265; toeplitz.py:55-59 forces c_0 real)."""
+    c = steer_forward(thetas, np.asarray(gammas, dtype=np.complex128), n)
+    c[0] = c[0].real + beta
+    return c
+
+
+def check_column(c):
+    """HermitianToeplitz validation, toeplitz.py:44-64."""
+    c0 = c[0]
+    if abs(c0.imag) > 1e-10 * max(abs(c0.real), 1.0) or c0.real <= 0.0:
+        raise OracleNotPD("diagonal entry c_0 must be real and positive")
+    c = c.copy()
+    c[0] = c0.real
+    return c
+
+
+# --- Row 3: Levinson-Durbin -------------------------------------------------------
+def levinson(c):
+    """Levinson-Durbin recursion giving the Gohberg-Semencul parameters
+    (rho, delta); toeplitz.py:121-145."""
+    c = check_column(np.asarray(c, dtype=np.complex128))
+    n = c.size
+    c0 = c[0].real
+    delta = np.empty(n)
+    delta[0] = c0
+    a = np.zeros(n, dtype=np.complex128)
+    a[0] = 1.0
+    floor = PD_EPS * c0
+    for m in range(1, n):
+        acc = c[m] + np.dot(a[1:m], c[m - 1:0:-1])
+        k = -acc / delta[m - 1]
+        a[1:m + 1] = a[1:m + 1] + k * np.conj(a[m - 1::-1])
+        delta[m] = delta[m - 1] * (1.0 - (k * np.conj(k)).real)
+        if not delta[m] > floor:
+            raise OracleNotPD(f"pivot delta_{m} = {delta[m]:.3e} <= {floor:.3e}")
+    rho = np.conj(a)[::-1]
+    rho = rho / rho[-1]
+    return rho, delta
+
+
+# --- Row 5: GS apply ------------------------------------------------------------
+def _pow2_at_least(n):
+    return 1 << int(np.ceil(np.log2(max(n, 1))))
+
+
+def gs_apply(rho, delta_last, x):
+    """C^{-1} x = delta_{N-1}^{-1} (T1^H T1 x - T0 T0^H x) through four FFT
+    convolutions (toeplitz.py:279-309, plan :93-112).  nfft is any length
+    >= 2N-1 (reference: next_fast_len; the result does not depend on it
+    beyond roundoff)."""
+    n = rho.size
+    x = np.asarray(x, dtype=np.complex128)
+    if n == 1:
+        return x / delta_last
+    nfft = _pow2_at_least(2 * n - 1)
+    v0 = np.concatenate(([0.0], rho[:-1]))
+    f_t1 = np.fft.fft(rho, nfft)
+    f_t1h = np.fft.fft(np.conj(rho)[::-1], nfft)
+    f_t0h = np.fft.fft(np.conj(v0)[::-1], nfft)
+    f_t0 = np.fft.fft(v0, nfft)
+    fx = np.fft.fft(x, nfft)
+    t1x = np.fft.ifft(fx * f_t1)[n - 1:2 * n - 1]
+    t0hx = np.fft.ifft(fx * f_t0h)[n - 1:2 * n - 1]
+    y1 = np.fft.ifft(np.fft.fft(t1x, nfft) * f_t1h)[:n]
+    y0 = np.fft.ifft(np.fft.fft(t0hx, nfft) * f_t0)[:n]
+    return (y1 - y0) / delta_last
+
+
+# --- Row 7: omega diagonal sums -----------------------------------------------------
+def weight_coefficients(kind, n):
+    """Diagonal weights in powers q^a i^b (toeplitz.py:317-354)."""
+    if kind == "s":
+        return {(0, 0): 2.0 - n, (0, 1): 1.0, (1, 0): 2.0}
+    if kind == "t":
+        return {(1, 1): -1.0, (0, 1): n - 1.5, (0, 2): -0.5, (1, 0): n - 1.0,
+                (0, 0): -(n - 1.0) * (n - 2.0) / 2.0}
+    if kind == "v":
+        return {(3, 0): 2.0 / 3.0, (2, 1): 1.0, (1, 2): 1.0, (2, 0): 2.0 - n,
+                (1, 1): 3.0 - 2.0 * n, (1, 0): n * n - 3.0 * n + 7.0 / 3.0,
+                (0, 3): 1.0 / 3.0, (0, 2): 1.5 - n,
+                (0, 1): n * n - 3.0 * n + 13.0 / 6.0,
+                (0, 0): 1.5 * n * n - n ** 3 / 3.0 - 13.0 * n / 6.0 + 1.0}
+    if kind == "x":
+        return {(3, 0): 2.0 / 3.0, (2, 1): 1.0, (2, 0): 2.0 - n, (1, 1): 2.0 - n,
+                (1, 0): n * n - 3.0 * n + 7.0 / 3.0, (0, 3): -1.0 / 6.0,
+                (0, 1): (3.0 * n * n - 9.0 * n + 7.0) / 6.0,
+                (0, 0): -(n ** 3) / 3.0 + 1.5 * n * n - 13.0 * n / 6.0 + 1.0}
+    raise ValueError(kind)
+
+
+def crosscorr_basis(coeffs):
+    """(q, i) -> (q, m = q + i) change of basis (toeplitz.py:357-365)."""
+    out = {}
+    for (a, b), cf in coeffs.items():
+        for j in range(b + 1):
+            key = (a + b - j, j)
+            out[key] = out.get(key, 0.0) + cf * comb(b, j) * (-1.0) ** (b - j)
+    return out
+
+
+OMEGA_SCALE = {"s": 1.0, "t": 2.0 * np.pi, "v": 4.0 * np.pi ** 2, "x": 4.0 * np.pi ** 2}
+
+
+def _fftconv(a, b):
+    nfft = _pow2_at_least(a.size + b.size - 1)
+    return np.fft.ifft(np.fft.fft(a, nfft) * np.fft.fft(b, nfft))[: a.size + b.size - 1]
+
+
+def omegas(rho, delta_last):
+    """All four diagonal-sum vectors over lags -(N-1)..N-1
+    (toeplitz.py:368-432; s and x symmetrised as at :428-430)."""
+    n = rho.size
+    q = np.arange(n, dtype=np.float64)
+    sets = {k: crosscorr_basis(weight_coefficients(k, n)) for k in "stvx"}
+    pairs = sorted({key for cs in sets.values() for key in cs})
+    corr = {}
+    for a, b in pairs:
+        corr[(a, b)] = _fftconv((q ** b) * np.conj(rho), ((q ** a) * rho)[::-1])
+    mid = n - 1
+    out = {}
+    for kind, cs in sets.items():
+        om = np.zeros(2 * n - 1, dtype=np.complex128)
+        for key, cf in cs.items():
+            om += cf * corr[key]
+        om *= OMEGA_SCALE[kind] / delta_last
+        if kind in ("s", "x"):
+            om[:mid] = np.conj(om[mid + 1:][::-1])
+            om[mid] = om[mid].real
+        out[kind] = om
+    return out
+
+
+# --- Bundle: rows 1, 3, 5, 6 (+7, 8, 9 lazily) ------------------------------------------
+class Bundle:
+    """One evaluation of the model at (theta, gamma, beta):
+    _SuperfastBundle, model_core.py:256-313."""
+
+    def __init__(self, y, thetas, gammas, beta):
+        n = y.size
+        self.y = y
+        self.thetas = np.asarray(thetas, dtype=np.float64)
+        self.gammas = np.asarray(gammas, dtype=np.float64)
+        self.beta = beta
+        self.c = cov_column(self.thetas, self.gammas, beta, n)
+        self.rho, self.delta = levinson(self.c)
+        self.w = gs_apply(self.rho, self.delta[-1], y)
+        quad = float(np.sum(np.conj(y) * self.w).real)
+        self.logdet = float(np.sum(np.log(self.delta)))
+        self.data_term = self.logdet + quad
+        self._om = None
+        self._stats = None
+        self._grid = {}
+
+    def omegas(self):
+        if self._om is None:
+            self._om = omegas(self.rho, self.delta[-1])
+        return self._om
+
+    def stats(self):
+        """model_core.py:281-301 (direct sums)."""
+        if self._stats is None:
+            n = self.y.size
+            d = 2.0 * np.pi * np.arange(n)
+            stack = np.stack((self.w, d * self.w, d ** 2 * self.w), axis=1)
+            adj = steer_adjoint(self.thetas, stack)
+            om = self.omegas()
+            omstack = np.stack([om["s"], om["t"], om["v"], om["x"]], axis=1)
+            stvx = fourier_sum_two_sided(self.thetas, omstack)
+            self._stats = dict(q=adj[:, 0].copy(), r=adj[:, 1].copy(), u=adj[:, 2].copy(),
+                               s=stvx[:, 0].real.copy(), t=stvx[:, 1].copy(),
+                               v=stvx[:, 2].copy(), x=stvx[:, 3].real.copy())
+        return self._stats
+
+    def grid(self, length):
+        """model_core.py:303-313."""
+        if length not in self._grid:
+            n = self.y.size
+            q_grid = np.fft.fft(self.w, n=length)
+            buf = np.zeros(length, dtype=np.complex128)
+            buf[np.arange(-(n - 1), n) % length] = self.omegas()["s"]
+            s_grid = (length * np.fft.ifft(buf)).real
+            self._grid[length] = (q_grid, s_grid)
+        return self._grid[length]
+
+
+# --- Row 10: activation -----------------------------------------------------------
+def gamma_bar(active_gamma, energy, m):
+    """smlr.py:53-59."""
+    if active_gamma.size:
+        bar = float(np.mean(active_gamma))
+        if bar > 0.0:
+            return bar
+    return max(energy / (m * GAMMA_BAR_K_INIT), np.finfo(np.float64).tiny)
+
+
+def delta_curve(q_grid, s_grid, gbar, zeta_eff):
+    """smlr.py:62-70 (G = 1)."""
+    sum_q2 = np.abs(q_grid) ** 2
+    log_ratio = np.log((1.0 - zeta_eff) / zeta_eff)
+    delta = np.log1p(gbar * s_grid) + log_ratio - sum_q2 / (1.0 / gbar + s_grid)
+    return delta, sum_q2
+
+
+def gamma_estimate(kappa, s):
+    """smlr.py:73-76."""
+    return (kappa * s - s) / s ** 2 if kappa > 1.0 else 0.0
+
+
+def snr_criterion(kappa, s, gbar, zeta_eff, tau):
+    """smlr.py:79-81."""
+    rhs = (1.0 + 1.0 / (gbar * s)) * np.log((1.0 + gbar * s) * (1.0 - zeta_eff) / zeta_eff)
+    return kappa > rhs + tau
+
+
+# --- Row 12: gradient / diag Hessian -------------------------------------------------
+def gradient(gammas, st):
+    """model_core.py:497-505 (G = 1)."""
+    cross = np.conj(st["q"]) * st["r"]
+    d_theta = 2.0 * gammas * (st["t"] - cross).imag
+    d_gamma = st["s"] - np.abs(st["q"]) ** 2
+    return np.concatenate((d_theta, d_gamma))
+
+
+def diag_hessian(gammas, st, n):
+    """model_core.py:508-536 (G = 1, fallback on)."""
+    ga = gammas
+    q2 = np.abs(st["q"]) ** 2
+    r2 = np.abs(st["r"]) ** 2
+    rqc = st["r"] * np.conj(st["q"])
+    uqc = st["u"] * np.conj(st["q"])
+    s, t, v, x = st["s"], st["t"], st["v"], st["x"]
+    core = (x - v) + ga * (t ** 2 - x * s) + ga * (x * q2 + s * r2 - 2.0 * t * rqc) + uqc - r2
+    d2_theta = 2.0 * ga * core.real
+    d2_gamma = 2.0 * s * q2 - s ** 2
+    d2_theta = np.where(d2_theta <= 0.0, float(50 * n) ** 2, d2_theta)
+    safe = np.where(ga > 0.0, ga, 1.0 / (50.0 * n))
+    d2_gamma = np.where(d2_gamma <= 0.0, safe ** -2, d2_gamma)
+    return np.concatenate((d2_theta, d2_gamma))
+
+
+# --- Row 13: L-BFGS ---------------------------------------------------------------
+@dataclass
+class Memory:
+    """lbfgs.py:29-53."""
+    diag: np.ndarray
+    pairs: list = field(default_factory=list)
+    max_pairs: int = MAX_PAIRS
+
+    @property
+    def dim(self):
+        return self.diag.size
+
+    def push(self, step, gdiff):
+        curv = float(np.dot(step, gdiff))
+        if curv <= CURVATURE_EPS * np.linalg.norm(step) * np.linalg.norm(gdiff):
+            return
+        self.pairs.append((step, gdiff, 1.0 / curv))
+        if len(self.pairs) > self.max_pairs:
+            self.pairs.pop(0)
+
+
+def two_loop(mem, g):
+    """lbfgs.py:63-76."""
+    q = g.copy()
+    alphas = []
+    for s, y, r in reversed(mem.pairs):
+        a = r * np.dot(s, q)
+        alphas.append(a)
+        q -= a * y
+    r_ = q / mem.diag
+    for (s, y, r), a in zip(mem.pairs, reversed(alphas)):
+        b = r * np.dot(y, r_)
+        r_ += s * (a - b)
+    return -r_
+
+
+def lbfgs_step(mem, point, f0, g0, objective_fn, gradient_fn):
+    """lbfgs.py:100-136."""
+    if not np.any(g0):
+        return point, f0, g0, 0.0, 0
+    d = two_loop(mem, g0)
+    slope = float(np.dot(g0, d))
+    dec = -slope
+    if slope >= 0.0:
+        d = -g0 / mem.diag
+        slope = float(np.dot(g0, d))
+        dec = -slope
+    k = point.size // 2
+    dg = d[k:]
+    shrink = dg < 0.0
+    cap = float(np.min(point[k:][shrink] / -dg[shrink])) if np.any(shrink) else np.inf
+    alpha = min(1.0, cap)
+    if alpha <= 0.0:
+        raise OracleLineSearchFailed("pinned")
+    for trial in range(MAX_BACKTRACKS):
+        cand = point + alpha * d
+        cand[:k] = np.mod(cand[:k], 1.0)
+        f_new = objective_fn(cand)
+        if f_new <= f0 + ARMIJO_C1 * alpha * slope:
+            g_new = gradient_fn(cand)
+            mem.push(alpha * d, g_new - g0)
+            return cand, f_new, g_new, dec, trial + 1
+        alpha *= BACKTRACK_FACTOR
+    raise OracleLineSearchFailed("no sufficient decrease")
+
+
+# --- Row 15: the loop -----------------------------------------------------------
+@dataclass
+class OracleOptions:
+    """estimator.py:34-50 (fields used on the superfast path)."""
+    grid_factor: int = 8
+    tau: float = DEFAULT_TAU
+    max_outer_iterations: int = 200
+    convergence_tol_scale: float = 1e-7
+    lbfgs_inner_max: int = 5
+    newton_decrement_tol_scale: float = 1e-8
+    initial_sweep_iterations: int = 3
+    lbfgs_memory: int = 10
+    k_max: int = None
+
+
+class _State:
+    def __init__(self, k_max, beta, zeta):
+        self.z = np.zeros(k_max, dtype=bool)
+        self.theta = np.zeros(k_max)
+        self.gamma = np.zeros(k_max)
+        self.beta = float(beta)
+        self.zeta = float(zeta)
+
+    def copy(self):
+        o = _State.__new__(_State)
+        o.z, o.theta, o.gamma = self.z.copy(), self.theta.copy(), self.gamma.copy()
+        o.beta, o.zeta = self.beta, self.zeta
+        return o
+
+    @property
+    def k_max(self):
+        return self.z.size
+
+    @property
+    def k_hat(self):
+        return int(np.count_nonzero(self.z))
+
+    @property
+    def act(self):
+        return np.flatnonzero(self.z)
+
+
+class _Engine:
+    """LRU(4) bundle cache keyed on the exact state bytes (model_core.py:416-444)."""
+
+    def __init__(self, y, grid_size):
+        self.y = y
+        self.grid_size = grid_size
+        self._b = {}
+        self._order = []
+        self.builds = 0
+
+    def bundle(self, st):
+        th = st.theta[st.z]
+        ga = st.gamma[st.z]
+        key = (th.tobytes(), ga.tobytes(), float(st.beta))
+        hit = self._b.get(key)
+        if hit is not None:
+            return hit
+        b = Bundle(self.y, th, ga, float(st.beta))
+        self.builds += 1
+        self._b[key] = b
+        self._order.append(key)
+        if len(self._order) > 4:
+            self._b.pop(self._order.pop(0), None)
+        return b
+
+    def objective(self, st):
+        return self.bundle(st).data_term + prior_term(st.k_hat, st.zeta, st.k_max)
+
+
+def _activate_slot(st, theta, gamma):
+    """smlr.py:99-104: the lowest free slot."""
+    slot = int(np.flatnonzero(~st.z)[0])
+    st.z[slot] = True
+    st.theta[slot] = theta
+    st.gamma[slot] = gamma
+    return slot
+
+
+def try_activate(st, energy, m, q_grid, s_grid, tau):
+    """smlr.py:84-122. Returns (new_state, slot, grid_index) or None."""
+    if st.k_hat >= st.k_max:
+        return None
+    gbar = gamma_bar(st.gamma[st.z], energy, m)
+    ze = prior_zeta(st.zeta, st.k_max)
+    delta, q2 = delta_curve(q_grid, s_grid, gbar, ze)
+    best = int(np.argmin(delta))
+    kappa = float(q2[best] / s_grid[best])
+    gam = gamma_estimate(kappa, float(s_grid[best]))
+    if float(delta[best]) >= -EPS_OBJECTIVE or gam <= 0.0:
+        return None
+    if not snr_criterion(kappa, float(s_grid[best]), gbar, ze, tau):
+        return None
+    out = st.copy()
+    slot = _activate_slot(out, best / q_grid.size, gam)
+    return out, slot, best
+
+
+def initial_sweep(st, energy, m, n, q_grid, s_grid, tau):
+    """smlr.py:125-171.  Returns (state, [(slot, grid_index), ...])."""
+    gbar = gamma_bar(st.gamma[st.z], energy, m)
+    ze = prior_zeta(st.zeta, st.k_max)
+    delta, q2 = delta_curve(q_grid, s_grid, gbar, ze)
+    length = q_grid.size
+    local_min = (delta <= np.roll(delta, 1)) & (delta <= np.roll(delta, -1))
+    cands = np.flatnonzero(local_min)
+    if cands.size == 0:
+        return st, []
+    cands = cands[np.argsort(delta[cands], kind="stable")]
+    dmin = float(delta[cands[0]])
+    if dmin >= -EPS_OBJECTIVE:
+        return st, []
+    out = st.copy()
+    spacing = SWEEP_MIN_SPACING_SCALE / n
+    added = []
+    for idx in cands:
+        if out.k_hat >= out.k_max:
+            break
+        d = float(delta[idx])
+        if d >= -EPS_OBJECTIVE or d > dmin / SWEEP_WITHIN_FACTOR:
+            continue
+        kappa = float(q2[idx] / s_grid[idx])
+        gnew = gamma_estimate(kappa, float(s_grid[idx]))
+        if gnew <= 0.0:
+            continue
+        tau_eff = tau if out.k_hat == 0 else 0.0
+        if not snr_criterion(kappa, float(s_grid[idx]), gbar, ze, tau_eff):
+            continue
+        th = idx / length
+        if out.k_hat and np.min(wrap_distance(th, out.theta[out.z])) < spacing:
+            continue
+        added.append((_activate_slot(out, th, gnew), int(idx)))
+    return out, added
+
+
+def deactivation_margins(st, stt):
+    """smlr.py:174-200 (G = 1)."""
+    gamma = st.gamma[st.z]
+    ze = prior_zeta(st.zeta, st.k_max)
+    rhs = np.log((1.0 - ze) / ze)
+    denom = 1.0 - gamma * stt["s"]
+    q2 = np.abs(stt["q"]) ** 2
+    out = np.empty(gamma.size)
+    for i in range(gamma.size):
+        if gamma[i] <= 0.0:
+            out[i] = -np.inf if rhs > 0.0 else 0.0
+            continue
+        if denom[i] <= 0.0:
+            out[i] = np.inf
+            continue
+        q2dd = q2[i] / denom[i] ** 2
+        sdd = stt["s"][i] / denom[i]
+        out[i] = q2dd / (1.0 / gamma[i] + sdd) - np.log1p(gamma[i] * sdd) - rhs
+    return out
+
+
+def try_deactivate(st, stt, recompute):
+    """smlr.py:203-225."""
+    removed = []
+    cur = st
+    while cur.k_hat:
+        mg = deactivation_margins(cur, stt)
+        worst = int(np.argmin(mg))
+        if not mg[worst] < 0.0:
+            break
+        slot = int(cur.act[worst])
+        cur = cur.copy() if cur is st else cur
+        cur.z[slot] = False
+        cur.gamma[slot] = 0.0
+        removed.append(slot)
+        if cur.k_hat == 0:
+            break
+        stt = recompute(cur)
+    return cur, removed
+
+
+@dataclass
+class OracleResult:
+    k_hat: int
+    theta_hat: np.ndarray
+    alpha_hat: np.ndarray
+    beta_hat: float
+    gamma_hat: np.ndarray
+    zeta_hat: float
+    objective_trace: np.ndarray
+    trace_stages: list
+    trace_khat: list
+    iterations: int
+    converged: bool
+    warnings: list
+    events: list
+    slots: np.ndarray
+    builds: int = 0
+    wall_time: float = 0.0
+
+
+def estimate(y, opts: OracleOptions = None) -> OracleResult:
+    """estimator.py:117-275 for G = 1, complete data, superfast backend.
+
+    `events` is the active-set history: ("sweep", [(slot, idx)...]),
+    ("activate", slot, idx), ("deactivate", [slots]) in order."""
+    t_start = time.perf_counter()
+    opts = opts or OracleOptions()
+    y = np.asarray(y, dtype=np.complex128).ravel()
+    n = m = y.size
+    if m < 2:
+        raise ValueError("need at least two observed samples")
+    k_max = opts.k_max if opts.k_max is not None else m
+    L = default_grid_size(n, opts.grid_factor)
+    eng = _Engine(y, L)
+    energy = float(np.mean(np.sum(np.abs(y[None, :]) ** 2, axis=1)))
+    floor = BETA_FLOOR_SCALE * energy / m
+    beta0 = max(INITIAL_BETA_ENERGY_FRACTION * energy / m, floor)
+    st = _State(k_max, beta0, INITIAL_ZETA)
+    trace, stages, khat, events, warns = [], [], [], [], []
+
+    def record(stage):
+        trace.append(eng.objective(st))
+        stages.append(stage)
+        khat.append(st.k_hat)
+
+    record("init")
+    st = st.copy()
+    st.beta = max(floor, energy / m)
+    record("beta")
+    previous = trace[-1]
+    mem = None
+    z_dirty = True
+    converged = False
+    iterations = 0
+
+    def stats_of(s):
+        return eng.bundle(s).stats()
+
+    for it in range(1, opts.max_outer_iterations + 1):
+        iterations = it
+        if it <= opts.initial_sweep_iterations:
+            qg, sg = eng.bundle(st).grid(L)
+            new, added = initial_sweep(st, energy, m, n, qg, sg, opts.tau)
+            if new.k_hat != st.k_hat:
+                st, z_dirty = new, True
+                events.append(("sweep", added))
+        else:
+            for _ in range(k_max):
+                qg, sg = eng.bundle(st).grid(L)
+                res = try_activate(st, energy, m, qg, sg, opts.tau)
+                if res is None:
+                    break
+                st, slot, idx = res
+                z_dirty = True
+                events.append(("activate", slot, idx))
+            else:
+                warns.append(f"iteration {it}: activation loop hit the K_max cap")
+        record("activate")
+        st = st.copy()
+        st.zeta = min(0.5, st.k_hat / st.k_max)
+        record("zeta")
+        cand = st.copy()
+        if st.k_hat:
+            stt = stats_of(st)
+            ga = st.gamma[st.z]
+            mu = ga * stt["q"]
+            tr = float(st.beta * np.sum(stt["s"] * ga))
+            fitted = steer_forward(st.theta[st.z], mu, n)
+            resid = y - fitted
+            value = (tr + float(np.sum(np.abs(resid) ** 2))) / m
+        else:
+            value = energy / m
+        cand.beta = max(floor, value)
+        if eng.objective(cand) <= trace[-1]:
+            st = cand
+        record("beta")
+        if st.k_hat:
+            for _ in range(opts.lbfgs_inner_max):
+                stt = stats_of(st)
+                if z_dirty or mem is None or mem.dim != 2 * st.k_hat:
+                    mem = Memory(diag=diag_hessian(st.gamma[st.z], stt, n), max_pairs=opts.lbfgs_memory)
+                    z_dirty = False
+                g0 = gradient(st.gamma[st.z], stt)
+                f0 = eng.objective(st)
+                base = st
+
+                def with_point(p, base=base):
+                    o = base.copy()
+                    a = o.act
+                    k = a.size
+                    o.theta[a] = p[:k]
+                    o.gamma[a] = p[k:]
+                    return o
+
+                point = np.concatenate((st.theta[st.z], st.gamma[st.z]))
+                def grad_at(p):
+                    trial = with_point(p)
+                    return gradient(trial.gamma[trial.z], stats_of(trial))
+
+                try:
+                    newp, _, _, dec, _ = lbfgs_step(
+                        mem, point, f0, g0, lambda p: eng.objective(with_point(p)), grad_at)
+                except OracleLineSearchFailed:
+                    break
+                st = with_point(newp)
+                record("refine")
+                new, removed = try_deactivate(st, stats_of(st), stats_of)
+                if removed:
+                    st, z_dirty = new, True
+                    events.append(("deactivate", removed))
+                    record("deactivate")
+                    if st.k_hat == 0:
+                        break
+                if dec < m * opts.newton_decrement_tol_scale:
+                    break
+        current = trace[-1]
+        if abs(previous - current) < m * opts.convergence_tol_scale:
+            converged = True
+            break
+        previous = current
+
+    if st.k_hat:
+        alpha = (st.gamma[st.z] * stats_of(st)["q"])[None, :]
+    else:
+        alpha = np.zeros((1, 0), dtype=np.complex128)
+    return OracleResult(
+        k_hat=st.k_hat, theta_hat=st.theta[st.z].copy(), alpha_hat=alpha, beta_hat=st.beta,
+        gamma_hat=st.gamma[st.z].copy(), zeta_hat=st.zeta, objective_trace=np.array(trace),
+        trace_stages=stages, trace_khat=khat, iterations=iterations, converged=converged,
+        warnings=warns, events=events, slots=st.act.copy(), builds=eng.builds,
+        wall_time=time.perf_counter() - t_start,
+    )
+
+
+# --- seeded config generator -----------------------------
+CONFIGS = {
+    # cfg: (B, N, K, min_sep_scale, amplitude law, snr_db)
+    1: (1, 64, 4, 2.0, "unit", 20.0),
+    2: (4096, 256, 16, 1.5, "cn", 15.0),
+    3: (1024, 1024, 64, 2.0, "uniform", 20.0),
+    4: (256, 4096, 256, 2.0, "cn", 20.0),
+    5: (64, 16384, 512, 1.0, "loguniform", 10.0),
+}
+
+
+def generate_problem(seed, cfg, b, n=None, k=None):
+    """One seeded problem y (complex128[N]) plus its truth, drawn with
+    rng = default_rng([seed, cfg, b]) (simdata.py:12-14 stream contract).
+    Frequencies: sequential rejection sampling (simdata.py:61-73); noise
+    variance from the paper SNR definition (simdata.py:96-99)."""
+    _, n0, k0, sep, law, snr = CONFIGS[cfg]
+    n = n or n0
+    k = k or k0
+    rng = np.random.default_rng([seed, cfg, b])
+    min_sep = sep / n
+    thetas = []
+    while len(thetas) < k:
+        cand = rng.random()
+        if not thetas or np.min(wrap_distance(cand, np.array(thetas))) > min_sep:
+            thetas.append(cand)
+    thetas = np.array(thetas)
+    phase = np.exp(2j * np.pi * rng.random(k))
+    if law == "unit":
+        mag = np.ones(k)
+    elif law == "cn":
+        a = (rng.standard_normal(k) + 1j * rng.standard_normal(k)) / np.sqrt(2.0)
+        mag, phase = np.abs(a), np.exp(1j * np.angle(a))
+    elif law == "uniform":
+        mag = rng.uniform(0.5, 1.5, k)
+    elif law == "loguniform":
+        # 20 dB power range: |alpha|^2 in [0.01, 1]
+        mag = 10.0 ** rng.uniform(-1.0, 0.0, k)
+    else:
+        raise ValueError(law)
+    alpha = mag * phase
+    clean = steer_forward(thetas, alpha, n)
+    beta = float(np.sum(np.abs(clean) ** 2)) / (n * 10.0 ** (snr / 10.0))
+    noise = np.sqrt(beta / 2.0) * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    return clean + noise, dict(thetas=thetas, alphas=alpha, beta=beta)
+
+
+def generate_batch(seed, cfg, count, n=None, k=None, start=0):
+    ys = [generate_problem(seed, cfg, start + b, n=n, k=k)[0] for b in range(count)]
+    return np.stack(ys)

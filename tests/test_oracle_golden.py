@@ -1,0 +1,126 @@
+"""Pin the CPU oracle (oracle/superlse_oracle.py) against golden vectors
+produced by the real reference (tests/golden/make_golden.py) and against the
+reference test-suite's known-answer tests (pkg/tests/test_toeplitz.py,
+pkg/tests/test_model_core.py)."""
+
+import numpy as np
+import pytest
+
+from golden_util import (AMP_TOL, CALL_TOL, STAGES, THETA_TOL, encode_events, load, rel,
+                         wrap_distance)
+from oracle import superlse_oracle as O
+
+CASES = [(1, b) for b in range(6)] + [(2, b) for b in range(4)] + [(3, 0)]
+
+
+@pytest.mark.parametrize("cfg,b", CASES)
+def test_trajectory_matches_reference(cfg, b):
+    z = load(cfg)
+    p = f"p{b}_"
+    r = O.estimate(z[p + "y"], O.OracleOptions(grid_factor=4))
+    assert r.k_hat == int(z[p + "k_hat"])
+    stages = np.array([STAGES.index(s) for s in r.trace_stages])
+    assert np.array_equal(stages, z[p + "stages"])
+    assert np.array_equal(encode_events(r.events), z[p + "events"])
+    assert r.iterations == int(z[p + "iterations"])
+    assert r.converged == bool(z[p + "converged"])
+    assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
+    assert rel(r.alpha_hat[0], z[p + "alpha_hat"]) < AMP_TOL
+    assert abs(r.beta_hat - float(z[p + "beta_hat"])) / float(z[p + "beta_hat"]) < AMP_TOL
+    assert rel(r.gamma_hat, z[p + "gamma_hat"]) < AMP_TOL
+    assert np.max(np.abs(r.objective_trace - z[p + "trace"]) / np.abs(z[p + "trace"])) < 1e-9
+
+
+CALL_CASES = [(cfg, b, st) for cfg, nb in ((1, 2), (2, 2), (3, 1)) for b in range(nb)
+              for st in ("empty", "truth", "final")]
+
+
+@pytest.mark.parametrize("cfg,b,state", CALL_CASES)
+def test_per_call_matches_reference(cfg, b, state):
+    z = load(cfg)
+    p = f"p{b}_call_{state}_"
+    y = z[f"p{b}_y"]
+    th, ga, be = z[p + "thetas"], z[p + "gammas"], float(z[p + "beta"])
+    n = y.size
+    L = O.default_grid_size(n, 4)
+    c = O.cov_column(th, ga, be, n)
+    assert rel(c, z[p + "c"]) < 1e-12
+    bd = O.Bundle(y, th, ga, be)
+    assert rel(bd.rho, z[p + "rho"]) < CALL_TOL
+    assert rel(bd.delta, z[p + "delta"]) < CALL_TOL
+    assert rel(bd.w, z[p + "w"]) < CALL_TOL
+    assert abs(bd.logdet - float(z[p + "logdet"])) <= CALL_TOL * abs(float(z[p + "logdet"])) + 1e-9
+    assert abs(bd.data_term - float(z[p + "data_term"])) <= CALL_TOL * abs(float(z[p + "data_term"]))
+    om = bd.omegas()
+    for k in "stvx":
+        assert rel(om[k], z[p + "om_" + k]) < CALL_TOL
+    qg, sg = bd.grid(L)
+    assert rel(qg, z[p + "q_grid"]) < CALL_TOL
+    assert rel(sg, z[p + "s_grid"]) < CALL_TOL
+    if th.size:
+        st = bd.stats()
+        for k in "qrustvx":
+            assert rel(st[k], z[p + "st_" + k]) < CALL_TOL, k
+
+
+# --- known-answer tests from the reference suite ---------------------------
+def test_kat_levinson_identity():
+    # pkg/tests/test_toeplitz.py:67-70
+    rho, delta = O.levinson(np.array([1, 0, 0, 0], complex))
+    assert np.allclose(rho, [0, 0, 0, 1]) and np.allclose(delta, 1)
+
+
+def test_kat_levinson_2x2():
+    # pkg/tests/test_toeplitz.py:73-79
+    rho, delta = O.levinson(np.array([2, 1], complex))
+    assert np.allclose(rho, [-0.5, 1]) and np.allclose(delta, [2, 1.5])
+
+
+def test_kat_apply_inverse_2x2():
+    # pkg/tests/test_toeplitz.py:156-159
+    rho, delta = O.levinson(np.array([2, 1], complex))
+    assert np.allclose(O.gs_apply(rho, delta[-1], np.array([1, 0], complex)), [2 / 3, -1 / 3])
+
+
+def test_kat_logdet():
+    # pkg/tests/test_toeplitz.py:184-190
+    _, delta = O.levinson(np.array([2, 1], complex))
+    assert np.isclose(np.sum(np.log(delta)), np.log(3))
+    _, delta = O.levinson(np.array([3.0, 0, 0, 0, 0], complex))
+    assert np.isclose(np.sum(np.log(delta)), 5 * np.log(3.0))
+
+
+def test_kat_identity_omegas():
+    # pkg/tests/test_toeplitz.py:202-212
+    n = 16
+    rho, delta = O.levinson(np.eye(1, n, 0, complex)[0])
+    om = O.omegas(rho, delta[-1])
+    assert np.isclose(om["s"][n - 1], n)
+    assert np.isclose(om["t"][n - 1], 2 * np.pi * n * (n - 1) / 2)
+
+
+def test_kat_sherman_morrison():
+    # pkg/tests/test_model_core.py:132-143: one component, q1 = s1 = N/(beta+N gamma) on y = psi
+    n, th, ga, be = 32, 0.3, 0.7, 0.4
+    y = np.exp(2j * np.pi * th * np.arange(n))
+    st = O.Bundle(y, [th], [ga], be).stats()
+    assert np.isclose(st["s"][0], n / (be + n * ga))
+    assert np.isclose(st["q"][0], n / (be + n * ga))
+
+
+def test_kat_empty_grid():
+    # pkg/tests/test_model_core.py:174-184
+    rng = np.random.default_rng(3)
+    n, be = 32, 0.8
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    qg, sg = O.Bundle(y, [], [], be).grid(4 * n)
+    assert np.allclose(sg, n / be)
+    assert np.allclose(qg, np.fft.fft(y / be, 4 * n))
+
+
+def test_kat_not_pd():
+    # pkg/tests/test_toeplitz.py:95-99
+    with pytest.raises(O.OracleNotPD):
+        O.levinson(np.array([1, 2], complex))
+    with pytest.raises(O.OracleNotPD):
+        O.levinson(np.array([-1, 0], complex))
