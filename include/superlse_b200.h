@@ -1,0 +1,123 @@
+/*
+ * superlse_b200.h -- C ABI of the B200-native Superfast LSE inner loop.
+ *
+ * Plain pointers and sizes only.  Every array argument is a DEVICE pointer
+ * (cudaMalloc / torch CUDA storage) unless stated; complex128 arrays are
+ * interleaved (re, im) doubles.  Calls are stream-ordered on `stream`
+ * (a cudaStream_t passed as void*; NULL = legacy default stream) and never
+ * synchronise.  Batched entry points process B independent problems; a
+ * problem's slice of a (B, X) array starts at b * X.
+ *
+ * Return codes: 0 = launched; < 0 = launch/argument error (message in
+ * slse_last_error()).  Per-problem numerical outcomes are int32 status
+ * codes: 0 ok, 1 not positive definite (superlse.errors.NotPositiveDefinite,
+ * toeplitz.py:141-142,191-192,249-252), 2 invalid diagonal (toeplitz.py:55-57).
+ *
+ * Reference interfaces replaced (paths relative to the reference package
+ * pkg/src/superlse/):
+ *   slse_cov_column        <- model_core.covariance_first_column :242-249
+ *                             and nufft.steer_forward :126-144
+ *   slse_toeplitz_factor   <- toeplitz.decompose :263-276
+ *                             (levinson_durbin :121-145, generalized_schur :230-260)
+ *   slse_gs_apply          <- toeplitz.apply_inverse :279-309 (+ quad, model_core.py:268-269)
+ *   slse_component_stats   <- model_core._SuperfastBundle.stats :281-301
+ *   slse_grid_eval         <- model_core._SuperfastBundle.grid :303-313
+ *   slse_estimate_batch    <- estimator.estimate :117-275 (complete data, G = 1,
+ *                             backend "superfast"), one problem per batch row
+ */
+#ifndef SUPERLSE_B200_H
+#define SUPERLSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLSE_ABI_VERSION 1
+
+/* EstimatorOptions (estimator.py:34-50), superfast fields. */
+typedef struct slse_options {
+  int grid_factor;               /* 8 */
+  double tau;                    /* 5.0 (smlr.DEFAULT_TAU) */
+  int max_outer_iterations;      /* 200 */
+  double convergence_tol_scale;  /* 1e-7 */
+  int lbfgs_inner_max;           /* 5 */
+  double newton_decrement_tol_scale; /* 1e-8 */
+  int initial_sweep_iterations;  /* 3 */
+  int lbfgs_memory;              /* 10 (<= 16) */
+  int k_max;                     /* <= 0: M */
+  int trace_capacity;            /* <= 0: 2 + 13 * max_outer_iterations */
+  int event_capacity;            /* <= 0: 4 * k_max + 64 */
+} slse_options;
+
+/* Outputs of slse_estimate_batch (device pointers, per problem b at offset
+ * b * stride).  K = k_max, T = trace_capacity, E = event_capacity. */
+typedef struct slse_outputs {
+  int32_t* k_hat;        /* [B] */
+  int32_t* status;       /* [B] 0 ok, 1 not PD, 2 invalid diagonal */
+  int32_t* iterations;   /* [B] */
+  int32_t* flags;        /* [B] bit0 converged, bit1 K_max-cap warning,
+                                  bit2 trace truncated, bit3 events truncated */
+  double* beta;          /* [B] */
+  double* zeta;          /* [B] */
+  double* theta;         /* [B, K] active frequencies, slot order */
+  double* gamma;         /* [B, K] */
+  double* alpha;         /* [B, K] complex (posterior means) */
+  int32_t* slot;         /* [B, K] slot index of each active component */
+  double* trace;         /* [B, T] objective trace */
+  int32_t* stage;        /* [B, T] 0 init 1 beta 2 activate 3 zeta 4 refine 5 deactivate */
+  int32_t* trace_k;      /* [B, T] model order at each record */
+  int32_t* n_trace;      /* [B] */
+  int32_t* events;       /* [B, E, 3] (kind, slot, grid index); kind 0 sweep,
+                            1 activate, 2 deactivate, -1 end-of-event */
+  int32_t* n_events;     /* [B] */
+  int64_t* counters;     /* [B, 4] builds, grid evals, stats evals, line-search trials */
+  double* stage_seconds; /* [B, 6] activate objective beta refine deactivate total */
+} slse_outputs;
+
+int slse_abi_version(void);
+const char* slse_last_error(void);
+/* SM count and opt-in shared memory per block of the current device. */
+int slse_device_info(int* sm_count, int* smem_optin_bytes, int* cc_major, int* cc_minor);
+
+/* default options (host struct) */
+void slse_default_options(slse_options* opts);
+
+/* Row 1: c[b, m] = beta[b] [m == 0] + sum_{k < kcount[b]} gamma[b,k] e^{j2 pi m theta[b,k]},
+ * c_0 forced real.  theta/gamma rows have stride kstride. c: [B, N] complex. */
+int slse_cov_column(const double* theta, const double* gamma, const int32_t* kcount, int kstride,
+                    const double* beta, int N, int B, double* c, void* stream);
+
+/* Rows 2-4: Gohberg-Semencul parameters.  c: [B, N] complex -> rho [B, N]
+ * complex, delta [B, N] (may be NULL), logdet [B], status [B]. */
+int slse_toeplitz_factor(const double* c, int N, int B, double* rho, double* delta, double* logdet,
+                         int32_t* status, void* stream);
+
+/* Row 5: w = C^{-1} y from (rho, delta_{N-1}); quad[b] = Re(y^H w) (may be NULL). */
+int slse_gs_apply(const double* rho, const double* delta_last, const double* y, int N, int B,
+                  double* w, double* quad, void* stream);
+
+/* Row 8: statistics at kcount[b] frequencies (rows of stride kstride).
+ * q, r, u, t, v: [B, kstride] complex; s, x: [B, kstride] real. */
+int slse_component_stats(const double* theta, const int32_t* kcount, int kstride, const double* rho,
+                         const double* delta_last, const double* w, int N, int B, double* q,
+                         double* r, double* u, double* s, double* t, double* v, double* x,
+                         void* stream);
+
+/* Row 9: activation grid.  q_grid [B, L] complex (FFT_L(w)), s_grid [B, L] real. */
+int slse_grid_eval(const double* rho, const double* delta_last, const double* w, int N, int L, int B,
+                   double* q_grid, double* s_grid, void* stream);
+
+/* Rows 10-15: the whole estimate() per problem.  y: [B, N] complex.
+ * workspace: device buffer of slse_estimate_workspace_bytes() bytes. */
+size_t slse_estimate_workspace_bytes(int N, int B, const slse_options* opts);
+int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
+                        const slse_outputs* out, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUPERLSE_B200_H */

@@ -1,0 +1,327 @@
+// slse_capi.cu -- sm_100a kernels and the extern "C" boundary declared in
+// include/superlse_b200.h.
+//
+// Kernels:
+//   solve_kernel<NT>      persistent: each CTA pulls problems from an atomic
+//                         work queue and runs the whole estimate() for one
+//                         problem (slse_solver.cuh); per-CTA workspace slab.
+//   cov_kernel / factor_kernel / apply_kernel / stats_kernel / grid_kernel
+//                         one CTA per problem; the per-call operators the
+//                         parity tests check against the oracle.
+//   tw_fill_kernel        twiddle table exp(-2 pi i k / TW).
+#include "slse_kernels.cuh"
+
+thread_local char g_err[512] = "";
+
+using namespace slse_k;
+
+namespace {
+
+
+int fail(const char* what, cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+  return -(int)e - 1000;
+}
+
+int fail_arg(const char* what) {
+  snprintf(g_err, sizeof(g_err), "%s", what);
+  return -1;
+}
+
+bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// ---------------------------------------------------------------- twiddles
+__global__ void tw_fill_kernel(cplx* tw, int lg) {
+  const int n = 1 << lg;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double s, c;
+    // exp(-2 pi i k / n); k/n exact (power of two)
+    sincospi(2.0 * ((double)k / (double)n), &s, &c);
+    tw[k] = mk(c, -s);
+  }
+}
+
+struct TwEntry {
+  cplx* ptr = nullptr;
+  int lg = 0;
+};
+std::mutex g_tw_mu;
+TwEntry g_tw[64];
+
+constexpr int kMinTwLog = 17;  // 131072 entries (2 MiB) covers L = 4N up to N = 32768
+
+int twiddles(int need_lg, cudaStream_t st, const cplx** out, int* out_lg) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail("cudaGetDevice", e);
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  TwEntry& t = g_tw[dev & 63];
+  if (t.ptr == nullptr || t.lg < need_lg) {
+    const int lg = need_lg > kMinTwLog ? need_lg : kMinTwLog;
+    cplx* p = nullptr;
+    e = cudaMalloc(&p, sizeof(cplx) << lg);
+    if (e != cudaSuccess) return fail("cudaMalloc(twiddles)", e);
+    tw_fill_kernel<<<256, 256, 0, st>>>(p, lg);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail("tw_fill_kernel", e);
+    // older tables stay allocated: in-flight kernels may still read them
+    t.ptr = p;
+    t.lg = lg;
+  }
+  *out = t.ptr;
+  *out_lg = t.lg;
+  return 0;
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+
+#define SLSE_DISPATCH_NT(nt, ...) \
+  switch (nt) {                    \
+    case 128: { constexpr int NTC = 128; __VA_ARGS__; } break; \
+    case 256: { constexpr int NTC = 256; __VA_ARGS__; } break; \
+    case 512: { constexpr int NTC = 512; __VA_ARGS__; } break; \
+    default: { constexpr int NTC = 1024; __VA_ARGS__; } break; \
+  }
+
+template <class KernelT>
+cudaError_t set_smem(KernelT kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+namespace {
+int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
+  SolveParams P = make_params(n, o);
+  SmemPlan plan = smem_plan(n, P.L);
+  const int nt = block_threads(n);
+  int occ = 1;
+  cudaError_t e = cudaSuccess;
+  switch (nt) {
+    case 128: e = slse_solve_occupancy_128(plan.bytes, &occ); break;
+    case 256: e = slse_solve_occupancy_256(plan.bytes, &occ); break;
+    case 512: e = slse_solve_occupancy_512(plan.bytes, &occ); break;
+    default: e = slse_solve_occupancy_1024(plan.bytes, &occ); break;
+  }
+  if (e != cudaSuccess) return fail("solver occupancy", e);
+  if (occ < 1) occ = 1;
+  int g = sm_count() * occ;
+  if (g > B) g = B;
+  if (g < 1) g = 1;
+  Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0);
+  *slab_out = lay.total;
+  if (plan_out) *plan_out = plan;
+  return g;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int slse_abi_version(void) { return SLSE_ABI_VERSION; }
+
+const char* slse_last_error(void) { return g_err; }
+
+int slse_device_info(int* sms, int* smem_optin, int* major, int* minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail("cudaGetDevice", e);
+  if (sms) cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
+  if (smem_optin) cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (major) cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (minor) cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return 0;
+}
+
+void slse_default_options(slse_options* o) {
+  o->grid_factor = 8;
+  o->tau = 5.0;
+  o->max_outer_iterations = 200;
+  o->convergence_tol_scale = 1e-7;
+  o->lbfgs_inner_max = 5;
+  o->newton_decrement_tol_scale = 1e-8;
+  o->initial_sweep_iterations = 3;
+  o->lbfgs_memory = 10;
+  o->k_max = 0;
+  o->trace_capacity = 0;
+  o->event_capacity = 0;
+}
+
+int slse_cov_column(const double* theta, const double* gamma, const int32_t* kcount, int kstride, const double* beta,
+                    int N, int B, double* c, void* stream) {
+  if (N < 1 || B < 0 || kstride < 0) return fail_arg("slse_cov_column: bad sizes");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nt = block_threads(N);
+  SLSE_DISPATCH_NT(nt, { cov_kernel<NTC><<<B, NTC, kRedBytes, st>>>(theta, gamma, kcount, kstride, beta, N, (cplx*)c); });
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail("cov_kernel", e);
+}
+
+int slse_toeplitz_factor(const double* c, int N, int B, double* rho, double* delta, double* logdet, int32_t* status,
+                         void* stream) {
+  if (N < 1 || B < 0) return fail_arg("slse_toeplitz_factor: bad sizes");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nt = block_threads(N);
+  const size_t rec = 48 * (size_t)N;
+  const int rec_smem = rec <= kRegionBudget ? 1 : 0;
+  const size_t smem = kHeadBytes + (rec_smem ? rec : 0);
+  cplx* scratch = nullptr;
+  double* dscr = nullptr;
+  cudaError_t e = cudaMallocAsync(&dscr, sizeof(double) * (size_t)N * B, st);
+  if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+  if (!rec_smem) {
+    e = cudaMallocAsync(&scratch, sizeof(cplx) * 3 * (size_t)N * B, st);
+    if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+  }
+  SLSE_DISPATCH_NT(nt, {
+    e = set_smem(factor_kernel<NTC>, smem);
+    if (e == cudaSuccess) {
+      factor_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)c, N, (cplx*)rho, delta, logdet, status, scratch, dscr,
+                                              rec_smem);
+      e = cudaGetLastError();
+    }
+  });
+  if (scratch) cudaFreeAsync(scratch, st);
+  cudaFreeAsync(dscr, st);
+  return e == cudaSuccess ? 0 : fail("factor_kernel", e);
+}
+
+int slse_gs_apply(const double* rho, const double* delta_last, const double* y, int N, int B, double* w, double* quad,
+                  void* stream) {
+  if (N < 1 || B < 0) return fail_arg("slse_gs_apply: bad sizes");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const cplx* tw;
+  int twlog;
+  const int nf = 1 << ilog2(2 * N);
+  int rc = twiddles(ilog2(nf), st, &tw, &twlog);
+  if (rc) return rc;
+  const int nt = block_threads(N);
+  int cap = 16 * (size_t)nf <= kRegionBudget ? nf : 0;
+  const size_t smem = kHeadBytes + 16 * (size_t)cap;
+  cplx* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, sizeof(cplx) * 4 * (size_t)nf * B, st);
+  if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+  SLSE_DISPATCH_NT(nt, {
+    e = set_smem(apply_kernel<NTC>, smem);
+    if (e == cudaSuccess) {
+      apply_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)rho, delta_last, (const cplx*)y, N, (cplx*)w, quad, scratch,
+                                             tw, twlog, cap);
+      e = cudaGetLastError();
+    }
+  });
+  cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? 0 : fail("apply_kernel", e);
+}
+
+int slse_component_stats(const double* theta, const int32_t* kcount, int kstride, const double* rho,
+                         const double* delta_last, const double* w, int N, int B, double* q, double* r, double* u,
+                         double* s, double* t, double* v, double* x, void* stream) {
+  if (N < 1 || B < 0) return fail_arg("slse_component_stats: bad sizes");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  CfTable cft;
+  cf_build(cft, N);
+  const int nt = block_threads(N);
+  cudaError_t e = cudaSuccess;
+  SLSE_DISPATCH_NT(nt, {
+    stats_kernel<NTC><<<B, NTC, kHeadBytes, st>>>(cft, theta, kcount, kstride, (const cplx*)rho, delta_last,
+                                                 (const cplx*)w, N, (cplx*)q, (cplx*)r, (cplx*)u, s, (cplx*)t,
+                                                 (cplx*)v, x);
+    e = cudaGetLastError();
+  });
+  return e == cudaSuccess ? 0 : fail("stats_kernel", e);
+}
+
+int slse_grid_eval(const double* rho, const double* delta_last, const double* w, int N, int L, int B, double* q_grid,
+                   double* s_grid, void* stream) {
+  if (N < 1 || !pow2(L) || L < N || B < 0) return fail_arg("slse_grid_eval: L must be a power of two >= N");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const cplx* tw;
+  int twlog;
+  int rc = twiddles(ilog2(L), st, &tw, &twlog);
+  if (rc) return rc;
+  const int nt = block_threads(N);
+  const int fused = 48 * (size_t)L <= kRegionBudget ? 1 : 0;
+  const size_t smem = kHeadBytes + (fused ? 48 * (size_t)L : 0);
+  cplx* scratch = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (!fused) {
+    e = cudaMallocAsync(&scratch, sizeof(cplx) * 2 * (size_t)L * B, st);
+    if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+  }
+  SLSE_DISPATCH_NT(nt, {
+    e = set_smem(grid_kernel<NTC>, smem);
+    if (e == cudaSuccess) {
+      grid_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, L, (cplx*)q_grid, s_grid,
+                                            scratch, tw, twlog, fused);
+      e = cudaGetLastError();
+    }
+  });
+  if (scratch) cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? 0 : fail("grid_kernel", e);
+}
+
+size_t slse_estimate_workspace_bytes(int N, int B, const slse_options* opts) {
+  slse_options o;
+  if (opts) o = *opts; else slse_default_options(&o);
+  size_t slab = 0;
+  int g = grid_size_for_solver(N, B, o, &slab, nullptr);
+  if (g < 0) return 0;
+  return 256 + (size_t)g * slab;
+}
+
+int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts, const slse_outputs* out,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  slse_options o;
+  if (opts) o = *opts; else slse_default_options(&o);
+  if (N < 2) return fail_arg("slse_estimate_batch: need at least two observed samples");
+  if (o.lbfgs_memory < 1 || o.lbfgs_memory > 16) return fail_arg("slse_estimate_batch: lbfgs_memory must be 1..16");
+  if (B < 0 || out == nullptr) return fail_arg("slse_estimate_batch: bad arguments");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t slab = 0;
+  SmemPlan plan;
+  int g = grid_size_for_solver(N, B, o, &slab, &plan);
+  if (g < 0) return g;
+  const size_t need = 256 + (size_t)g * slab;
+  if (workspace_bytes < need) {
+    snprintf(g_err, sizeof(g_err), "slse_estimate_batch: workspace %zu < required %zu bytes", workspace_bytes, need);
+    return -2;
+  }
+  SolveParams P = make_params(N, o);
+  const cplx* tw;
+  int twlog;
+  const int fmax = P.L > 2 * N ? P.L : (1 << ilog2(2 * N));
+  int rc = twiddles(ilog2(fmax), st, &tw, &twlog);
+  if (rc) return rc;
+  CfTable cft;
+  cf_build(cft, N);
+  int* queue = (int*)workspace;
+  cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(int), st);
+  if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
+  char* ws = (char*)workspace + 256;
+  const int nt = block_threads(N);
+#define SLSE_SOLVE_ARGS g, plan.bytes, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog, plan.fft_cap, \
+                        plan.rec_in_smem
+  switch (nt) {
+    case 128: e = slse_solve_launch_128(SLSE_SOLVE_ARGS); break;
+    case 256: e = slse_solve_launch_256(SLSE_SOLVE_ARGS); break;
+    case 512: e = slse_solve_launch_512(SLSE_SOLVE_ARGS); break;
+    default: e = slse_solve_launch_1024(SLSE_SOLVE_ARGS); break;
+  }
+#undef SLSE_SOLVE_ARGS
+  return e == cudaSuccess ? 0 : fail("solve_kernel", e);
+}
+
+}  // extern "C"

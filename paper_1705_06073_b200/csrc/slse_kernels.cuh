@@ -1,0 +1,243 @@
+// slse_kernels.cuh -- kernel templates and launch configuration shared by
+// the C-ABI translation unit (slse_capi.cu) and the per-block-size solver
+// instantiations (slse_solve_inst.cu, compiled once per NT in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "superlse_b200.h"
+#include "slse_solver.cuh"
+
+using namespace slse;
+
+namespace slse_k {
+
+// ---------------------------------------------------------- configuration
+constexpr size_t kRedBytes = 2 * 32 * 16 * sizeof(double);  // Blk::red
+constexpr size_t kCfBytes = sizeof(CfTable);
+constexpr size_t kHeadBytes = kRedBytes + ((kCfBytes + 255) & ~(size_t)255);
+constexpr size_t kRegionBudget = 200 * 1024;
+
+inline int block_threads(int n) {
+  if (n <= 128) return 128;
+  if (n <= 512) return 256;
+  if (n <= 2048) return 512;
+  return 1024;
+}
+
+struct SmemPlan {
+  int rec_in_smem;
+  int fft_cap;
+  size_t bytes;
+};
+
+inline SmemPlan smem_plan(int n, int L) {
+  SmemPlan p;
+  const size_t rec = 48 * (size_t)n;
+  p.rec_in_smem = rec <= kRegionBudget ? 1 : 0;
+  const int fftmax = L > 2 * n ? L : (1 << ilog2(2 * n));
+  size_t cap_bytes = p.rec_in_smem ? rec : 0;
+  if (16 * (size_t)fftmax <= kRegionBudget) {
+    p.fft_cap = fftmax;
+  } else {
+    int F = 1;
+    const size_t lim = cap_bytes > 0 ? cap_bytes : kRegionBudget;
+    while (16 * (size_t)(F * 2) <= lim) F *= 2;
+    p.fft_cap = F;
+  }
+  size_t region = 16 * (size_t)p.fft_cap;
+  if (p.rec_in_smem && rec > region) region = rec;
+  p.bytes = kHeadBytes + region;
+  return p;
+}
+
+
+// ------------------------------------------------------------------ kernels
+struct OutPtrs {
+  slse_outputs o;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) solve_kernel(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
+                                                   int B, slse_outputs out, char* ws, size_t slab_bytes,
+                                                   int* queue, const cplx* tw, int twlog, int fft_cap,
+                                                   int rec_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* red = (double*)smem_raw;
+  CfTable* cf = (CfTable*)(smem_raw + kRedBytes);
+  cplx* region = (cplx*)(smem_raw + kHeadBytes);
+  __shared__ int s_prob;
+  if (threadIdx.x == 0) *cf = cft;
+  Blk b;
+  b.tid = threadIdx.x;
+  b.nt = NT;
+  b.red = red;
+  b.bank = 0;
+  FftCtx f;
+  f.tw = tw;
+  f.twlog = twlog;
+  f.smem = region;
+  f.smem_cap = fft_cap;
+  char* slab = ws + (size_t)blockIdx.x * slab_bytes;
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0);
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) s_prob = atomicAdd(queue, 1);
+    __syncthreads();
+    const int p = s_prob;
+    __syncthreads();
+    if (p >= B) break;
+    const size_t K = (size_t)P.kmax;
+    ProbOut o;
+    o.khat = out.k_hat + p;
+    o.status = out.status + p;
+    o.iters = out.iterations + p;
+    o.flags = out.flags + p;
+    o.beta = out.beta + p;
+    o.zeta = out.zeta + p;
+    o.theta = out.theta + p * K;
+    o.gamma = out.gamma + p * K;
+    o.alpha = (cplx*)out.alpha + p * K;
+    o.slot = out.slot + p * K;
+    o.trace = out.trace + (size_t)p * P.tcap;
+    o.stage = out.stage + (size_t)p * P.tcap;
+    o.trace_k = out.trace_k + (size_t)p * P.tcap;
+    o.ntrace = out.n_trace + p;
+    o.events = out.events + (size_t)p * P.ecap * 3;
+    o.nevents = out.n_events + p;
+    o.counters = (long long*)out.counters + (size_t)p * 4;
+    o.stage_s = out.stage_seconds + (size_t)p * 6;
+    Solver S(b, P, cf, ys + (size_t)p * P.n, o, slab, lay, rec_smem ? region : nullptr, f);
+    S.run();
+    b.bank = S.b.bank;
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) cov_kernel(const double* theta, const double* gamma, const int* kcount,
+                                                 int kstride, const double* beta, int n, cplx* c) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  steer_forward(c + (size_t)p * n, n, theta + (size_t)p * kstride, gamma + (size_t)p * kstride, nullptr,
+                kcount[p], beta[p], true, b);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) factor_kernel(const cplx* c, int n, cplx* rho, double* delta,
+                                                    double* logdet, int* status, cplx* scratch, double* dscratch,
+                                                    int rec_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  cplx* e;
+  if (rec_smem) {
+    e = (cplx*)(smem_raw + kHeadBytes);
+  } else {
+    e = scratch + (size_t)p * 3 * n;
+  }
+  Factor F = toeplitz_factor(c + (size_t)p * n, n, e, e + n, e + 2 * n, delta ? delta + (size_t)p * n : nullptr,
+                             dscratch + (size_t)p * n, rho + (size_t)p * n, b);
+  if (threadIdx.x == 0) {
+    logdet[p] = F.logdet;
+    status[p] = F.status;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) apply_kernel(const cplx* rho, const double* delta_last, const cplx* y, int n,
+                                                   cplx* w, double* quad, cplx* scratch, const cplx* tw, int twlog,
+                                                   int fft_cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  FftCtx f{tw, twlog, (cplx*)(smem_raw + kHeadBytes), fft_cap};
+  const int p = blockIdx.x;
+  const int nf = 1 << ilog2(2 * n);
+  cplx* yh = scratch + (size_t)p * 4 * nf;
+  const cplx* yp = y + (size_t)p * n;
+  fft(yh, nf, -1.0, [&](int i) { return i < n ? yp[i] : mk(0.0, 0.0); }, [&](int i, cplx v) { yh[i] = v; }, f, b);
+  double qd = gs_apply(rho + (size_t)p * n, n, delta_last[p], yp, yh, yh + nf, yh + 2 * nf, yh + 3 * nf,
+                       w + (size_t)p * n, f, b);
+  if (quad && threadIdx.x == 0) quad[p] = qd;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) stats_kernel(CfTable cft, const double* theta, const int* kcount, int kstride,
+                                                   const cplx* rho, const double* delta_last, const cplx* w, int n,
+                                                   cplx* q, cplx* r, cplx* u, double* s, cplx* t, cplx* v,
+                                                   double* x) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CfTable* cf = (CfTable*)(smem_raw + kRedBytes);
+  if (threadIdx.x == 0) *cf = cft;
+  __syncthreads();
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  const size_t o = (size_t)p * kstride;
+  component_stats(theta + o, kcount[p], rho + (size_t)p * n, w + (size_t)p * n, n, delta_last[p], cf, q + o, r + o,
+                  u + o, s + o, t + o, v + o, x + o, b);
+}
+
+// Row 9 standalone (the roofline kernel): all three length-L transforms in
+// shared memory when 48 L bytes fit, one pass over HBM in and out.
+template <int NT>
+__global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, const double* __restrict__ delta_last,
+                                                  const cplx* __restrict__ w, int n, int L, cplx* __restrict__ q_grid,
+                                                  double* __restrict__ s_grid, cplx* scratch, const cplx* tw,
+                                                  int twlog, int fused) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  const cplx* rp = rho + (size_t)p * n;
+  const cplx* wp = w + (size_t)p * n;
+  cplx* qg = q_grid + (size_t)p * L;
+  double* sgp = s_grid + (size_t)p * L;
+  const double inv_d = 1.0 / delta_last[p];
+  const double c2n = 2.0 - (double)n;
+  if (fused) {
+    cplx* X0 = (cplx*)(smem_raw + kHeadBytes);
+    cplx* X1 = X0 + L;
+    cplx* X2 = X1 + L;
+    FftCtx f{tw, twlog, X0, 0};
+    const int lg = ilog2(L);
+    for (int i = threadIdx.x; i < L; i += NT) {
+      const unsigned j = brev_bits((unsigned)i, lg);
+      cplx a = mk(0.0, 0.0), rr = mk(0.0, 0.0);
+      if (i < n) { a = wp[i]; rr = rp[i]; }
+      X0[j] = a;
+      X1[j] = rr;
+      X2[j] = cscale(rr, (double)i);
+    }
+    __syncthreads();
+    fft_passes(X0, L, -1.0, f, b);
+    fft_passes(X1, L, -1.0, f, b);
+    fft_passes(X2, L, -1.0, f, b);
+    for (int l = threadIdx.x; l < L; l += NT) {
+      const cplx a0 = X1[l], a1 = X2[l];
+      qg[l] = X0[l];
+      sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+    }
+  } else {
+    FftCtx f{tw, twlog, (cplx*)(smem_raw + kHeadBytes), 0};
+    cplx* G1 = scratch + (size_t)p * 2 * L;
+    grid_eval(rp, wp, n, delta_last[p], L, qg, G1, G1 + L, sgp, f, b);
+  }
+}
+
+
+}  // namespace slse_k
+
+// per-NT solver entry points (slse_solve_inst.cu)
+#define SLSE_DECL_SOLVE(NT)                                                                            \
+  cudaError_t slse_solve_occupancy_##NT(size_t smem, int* occ);                                       \
+  cudaError_t slse_solve_launch_##NT(int grid, size_t smem, cudaStream_t st, const slse::SolveParams& P, \
+                                     const slse::CfTable& cft, const slse::cplx* ys, int B,            \
+                                     const slse_outputs& out, char* ws, size_t slab, int* queue,       \
+                                     const slse::cplx* tw, int twlog, int fft_cap, int rec_smem);
+SLSE_DECL_SOLVE(128)
+SLSE_DECL_SOLVE(256)
+SLSE_DECL_SOLVE(512)
+SLSE_DECL_SOLVE(1024)

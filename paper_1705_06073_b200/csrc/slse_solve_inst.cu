@@ -1,0 +1,29 @@
+// slse_solve_inst.cu -- one solver instantiation per block size; compiled
+// once per SLSE_NT (128, 256, 512, 1024) so the four builds run in parallel.
+#include "slse_kernels.cuh"
+
+#ifndef SLSE_NT
+#error "compile with -DSLSE_NT=<threads per block>"
+#endif
+
+#define SLSE_CAT2(a, b) a##b
+#define SLSE_CAT(a, b) SLSE_CAT2(a, b)
+
+cudaError_t SLSE_CAT(slse_solve_occupancy_, SLSE_NT)(size_t smem, int* occ) {
+  cudaError_t e = cudaFuncSetAttribute(slse_k::solve_kernel<SLSE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, slse_k::solve_kernel<SLSE_NT>, SLSE_NT, smem);
+}
+
+cudaError_t SLSE_CAT(slse_solve_launch_, SLSE_NT)(int grid, size_t smem, cudaStream_t st, const slse::SolveParams& P,
+                                                  const slse::CfTable& cft, const slse::cplx* ys, int B,
+                                                  const slse_outputs& out, char* ws, size_t slab, int* queue,
+                                                  const slse::cplx* tw, int twlog, int fft_cap, int rec_smem) {
+  cudaError_t e = cudaFuncSetAttribute(slse_k::solve_kernel<SLSE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  slse_k::solve_kernel<SLSE_NT><<<grid, SLSE_NT, smem, st>>>(P, cft, ys, B, out, ws, slab, queue, tw, twlog, fft_cap,
+                                                             rec_smem);
+  return cudaGetLastError();
+}

@@ -1,0 +1,950 @@
+// slse_solver.cuh -- the whole Superfast-LSE estimate() for ONE problem,
+// executed by one CTA (persistent; problems are pulled from a work queue).
+//
+// Mirrors estimator.estimate (estimator.py:117-275) for complete data and a
+// single snapshot (G = 1): warm-up, initial activation sweeps
+// (smlr.py:125-171), greedy activations (smlr.py:107-122), zeta and beta
+// block updates (estimator.py:69-90,184-203), L-BFGS refinement
+// (lbfgs.py:63-136) with deactivation (smlr.py:174-225) and the stopping
+// rules.  Every scalar decision is computed redundantly by all threads from
+// block reductions that return identical bits, so control flow is uniform.
+#pragma once
+#include "slse_stats.cuh"
+#include "superlse_b200.h"
+
+#ifdef SLSE_HOST_EMU
+#include <chrono>
+#endif
+
+namespace slse {
+
+constexpr double kEpsObjective = 2.220446049250313e-16;  // smlr.py:31
+constexpr double kSweepWithin = 5.0;                     // smlr.py:35
+constexpr double kSweepSpacing = 0.05;                   // smlr.py:36
+constexpr double kGammaBarKInit = 4.0;                   // smlr.py:40
+constexpr double kArmijoC1 = 1e-4;                       // lbfgs.py:21
+constexpr double kBacktrack = 0.5;                       // lbfgs.py:22
+constexpr int kMaxBacktracks = 30;                       // lbfgs.py:23
+constexpr double kCurvEps = 1e-12;                       // lbfgs.py:26
+constexpr double kInitialZeta = 0.2;                     // estimator.py:30
+constexpr double kInitialBetaFrac = 0.01;                // estimator.py:31
+constexpr double kBetaFloorScale = 1e-12;                // model_core.py:36
+constexpr double kTiny = 2.2250738585072014e-308;        // np.finfo(float64).tiny
+
+enum Stage : int { kStInit = 0, kStBeta = 1, kStActivate = 2, kStZeta = 3, kStRefine = 4, kStDeactivate = 5 };
+enum EvKind : int { kEvSweep = 0, kEvActivate = 1, kEvDeactivate = 2, kEvEnd = -1 };
+enum Flags : int { kFlConverged = 1, kFlKmaxCap = 2, kFlTraceFull = 4, kFlEventsFull = 8 };
+enum Timer : int { kTmActivate = 0, kTmObjective = 1, kTmBeta = 2, kTmRefine = 3, kTmDeactivate = 4, kTmTotal = 5 };
+
+struct SolveParams {
+  int n, L, kmax;
+  int max_outer, inner_max, sweep_iters, lbfgs_mem;
+  int tcap, ecap;
+  double tau, conv_tol_scale, dec_tol_scale;
+};
+
+// Launch-uniform parameters from the C-ABI options (estimator.py:34-50).
+SLSE_HD SolveParams make_params(int n, const slse_options& o) {
+  SolveParams P;
+  P.n = n;
+  int target = 2 * n > o.grid_factor * n ? 2 * n : o.grid_factor * n;
+  int L = 1;
+  while (L < target) L <<= 1;  // model_core.py:224-227
+  P.L = L;
+  P.kmax = o.k_max > 0 ? o.k_max : n;
+  P.max_outer = o.max_outer_iterations;
+  P.inner_max = o.lbfgs_inner_max;
+  P.sweep_iters = o.initial_sweep_iterations;
+  P.lbfgs_mem = o.lbfgs_memory;
+  P.tcap = o.trace_capacity > 0 ? o.trace_capacity : 2 + 13 * o.max_outer_iterations;
+  P.ecap = o.event_capacity > 0 ? o.event_capacity : 4 * P.kmax + 64;
+  P.tau = o.tau;
+  P.conv_tol_scale = o.convergence_tol_scale;
+  P.dec_tol_scale = o.newton_decrement_tol_scale;
+  return P;
+}
+
+// Per-CTA workspace layout (offsets in bytes from the CTA's slab).
+struct Layout {
+  size_t yhat, c, e, bg, a, rho[2], w[2], P, U, V, G0, G1, G2;
+  size_t st_q[2], st_r[2], st_u[2], st_t[2], st_v[2], mu;
+  size_t dtmp, dl, q2, sg, theta, gamma, act_theta, act_gamma, st_s[2], st_x[2];
+  size_t lbS, lbY, lbR, diag, g0, gnew, dir, pt, cand, cth, cga, marg, cflist_d;
+  size_t z, act_slot, cidx, csort;
+  size_t total;
+};
+
+SLSE_HD size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion_in_smem) {
+  Layout l;
+  size_t o = 0;
+  const size_t C = 16, D = 8, I = 4;
+  const int nf = 1 << ilog2(2 * n);
+  const size_t K = (size_t)kmax, K2 = 2 * (size_t)kmax;
+  l.yhat = o; o = al(o + C * nf);
+  l.c = o; o = al(o + C * n);
+  if (recursion_in_smem) {
+    l.e = l.bg = l.a = 0;
+  } else {
+    l.e = o; o = al(o + C * n);
+    l.bg = o; o = al(o + C * n);
+    l.a = o; o = al(o + C * n);
+  }
+  for (int i = 0; i < 2; ++i) { l.rho[i] = o; o = al(o + C * n); l.w[i] = o; o = al(o + C * n); }
+  l.P = o; o = al(o + C * nf);
+  l.U = o; o = al(o + C * nf);
+  l.V = o; o = al(o + C * nf);
+  l.G0 = o; o = al(o + C * L);
+  l.G1 = o; o = al(o + C * L);
+  l.G2 = o; o = al(o + C * L);
+  for (int i = 0; i < 2; ++i) {
+    l.st_q[i] = o; o = al(o + C * K);
+    l.st_r[i] = o; o = al(o + C * K);
+    l.st_u[i] = o; o = al(o + C * K);
+    l.st_t[i] = o; o = al(o + C * K);
+    l.st_v[i] = o; o = al(o + C * K);
+    l.st_s[i] = o; o = al(o + D * K);
+    l.st_x[i] = o; o = al(o + D * K);
+  }
+  l.mu = o; o = al(o + C * K);
+  l.dtmp = o; o = al(o + D * n);
+  l.dl = o; o = al(o + D * L);
+  l.q2 = o; o = al(o + D * L);
+  l.sg = o; o = al(o + D * L);
+  l.theta = o; o = al(o + D * K);
+  l.gamma = o; o = al(o + D * K);
+  l.act_theta = o; o = al(o + D * K);
+  l.act_gamma = o; o = al(o + D * K);
+  l.lbS = o; o = al(o + D * K2 * lbfgs_mem);
+  l.lbY = o; o = al(o + D * K2 * lbfgs_mem);
+  l.lbR = o; o = al(o + D * (lbfgs_mem + 1));
+  l.diag = o; o = al(o + D * K2);
+  l.g0 = o; o = al(o + D * K2);
+  l.gnew = o; o = al(o + D * K2);
+  l.dir = o; o = al(o + D * K2);
+  l.pt = o; o = al(o + D * K2);
+  l.cand = o; o = al(o + D * K2);
+  l.cth = o; o = al(o + D * K);
+  l.cga = o; o = al(o + D * K);
+  l.marg = o; o = al(o + D * K);
+  l.cflist_d = o; o = al(o + D * L);
+  l.z = o; o = al(o + I * K);
+  l.act_slot = o; o = al(o + I * K);
+  l.cidx = o; o = al(o + I * L);
+  l.csort = o; o = al(o + I * L);
+  l.total = o;
+  return l;
+}
+
+// Outputs of one problem (pointers already offset to the problem).
+struct ProbOut {
+  int* khat;
+  int* status;
+  int* iters;
+  int* flags;
+  double* beta;
+  double* zeta;
+  double* theta;   // [kmax] active, slot order
+  double* gamma;   // [kmax]
+  cplx* alpha;     // [kmax]
+  int* slot;       // [kmax]
+  double* trace;   // [tcap]
+  int* stage;      // [tcap]
+  int* trace_k;    // [tcap]
+  int* ntrace;
+  int* events;     // [ecap][3]
+  int* nevents;
+  long long* counters;  // [4] builds, grids, stats, backtracks
+  double* stage_s;      // [6] seconds per stage (estimator.py:106-114 buckets)
+};
+
+SLSE_D double prior_zeta(double zeta, int kmax) {  // model_core.py:230-234
+  double z = fmax(zeta, 0.5 / (double)kmax);
+  return z < 0.5 ? z : 0.5;
+}
+
+SLSE_D double prior_term(int k, double zeta, int kmax) {  // model_core.py:237-239
+  const double ze = prior_zeta(zeta, kmax);
+  return -((double)k * log(ze) + (double)(kmax - k) * log1p(-ze));
+}
+
+SLSE_D double np_mod1(double x) {  // numpy float mod by 1.0 (npy_divmod)
+  double m = fmod(x, 1.0);
+  if (m != 0.0) {
+    if (m < 0.0) m += 1.0;
+  } else {
+    m = 0.0;
+  }
+  return m;
+}
+
+SLSE_D double wrap_dist(double x, double y) {  // simdata.py:50-53
+  double d = np_mod1(fabs(x - y));
+  double e = 1.0 - d;
+  return d < e ? d : e;
+}
+
+SLSE_D unsigned long long now_ns() {
+#ifdef SLSE_HOST_EMU
+  return (unsigned long long)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+#else
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+#endif
+}
+
+struct Bundle {
+  cplx* rho;
+  cplx* w;
+  cplx *q, *r, *u, *t, *v;
+  double *s, *x;
+  double data_term, delta_last, logdet;
+  int stats_valid;
+};
+
+struct Solver {
+  Blk& b;
+  FftCtx f;
+  const SolveParams& P;
+  const CfTable* cf;
+  const cplx* y;
+  ProbOut o;
+  // workspace
+  cplx *yhat, *c, *e, *bg, *a, *PP, *U, *V, *G0, *G1, *G2, *mu;
+  double *dtmp, *dl, *q2, *sg, *theta, *gamma, *act_theta, *act_gamma;
+  double *lbS, *lbY, *lbR, *diag, *g0, *gnew, *dir, *pt, *cand, *cth, *cga, *marg;
+  int *z, *act_slot, *cidx, *csort;
+  Bundle bun[2];
+  int cur;
+  int cur_valid;
+  // scalar state (identical in every thread)
+  int n, L, kmax, k;
+  double beta, zeta, energy, floor_beta;
+  int status;
+  int ntrace, nevents, flags;
+  int mem_valid, mem_dim, mem_count, mem_head;
+  long long n_builds, n_grids, n_stats, n_backtracks;
+  unsigned long long t_mark, t_start;
+  double tm[6];
+  int free_hint;
+
+  SLSE_D Solver(Blk& blk, const SolveParams& p, const CfTable* cf_, const cplx* y_, ProbOut out,
+                char* slab, const Layout& lay, cplx* rec_smem, const FftCtx& fc)
+      : b(blk), f(fc), P(p), cf(cf_), y(y_), o(out) {
+    n = p.n; L = p.L; kmax = p.kmax;
+    yhat = (cplx*)(slab + lay.yhat);
+    c = (cplx*)(slab + lay.c);
+    if (rec_smem) {
+      e = rec_smem; bg = rec_smem + n; a = rec_smem + 2 * n;
+    } else {
+      e = (cplx*)(slab + lay.e); bg = (cplx*)(slab + lay.bg); a = (cplx*)(slab + lay.a);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bun[i].rho = (cplx*)(slab + lay.rho[i]);
+      bun[i].w = (cplx*)(slab + lay.w[i]);
+      bun[i].q = (cplx*)(slab + lay.st_q[i]);
+      bun[i].r = (cplx*)(slab + lay.st_r[i]);
+      bun[i].u = (cplx*)(slab + lay.st_u[i]);
+      bun[i].t = (cplx*)(slab + lay.st_t[i]);
+      bun[i].v = (cplx*)(slab + lay.st_v[i]);
+      bun[i].s = (double*)(slab + lay.st_s[i]);
+      bun[i].x = (double*)(slab + lay.st_x[i]);
+      bun[i].stats_valid = 0;
+      bun[i].data_term = bun[i].delta_last = bun[i].logdet = 0.0;
+    }
+    PP = (cplx*)(slab + lay.P); U = (cplx*)(slab + lay.U); V = (cplx*)(slab + lay.V);
+    G0 = (cplx*)(slab + lay.G0); G1 = (cplx*)(slab + lay.G1); G2 = (cplx*)(slab + lay.G2);
+    mu = (cplx*)(slab + lay.mu);
+    dtmp = (double*)(slab + lay.dtmp);
+    dl = (double*)(slab + lay.dl); q2 = (double*)(slab + lay.q2); sg = (double*)(slab + lay.sg);
+    theta = (double*)(slab + lay.theta); gamma = (double*)(slab + lay.gamma);
+    act_theta = (double*)(slab + lay.act_theta); act_gamma = (double*)(slab + lay.act_gamma);
+    lbS = (double*)(slab + lay.lbS); lbY = (double*)(slab + lay.lbY); lbR = (double*)(slab + lay.lbR);
+    diag = (double*)(slab + lay.diag); g0 = (double*)(slab + lay.g0); gnew = (double*)(slab + lay.gnew);
+    dir = (double*)(slab + lay.dir); pt = (double*)(slab + lay.pt); cand = (double*)(slab + lay.cand);
+    cth = (double*)(slab + lay.cth); cga = (double*)(slab + lay.cga); marg = (double*)(slab + lay.marg);
+    z = (int*)(slab + lay.z); act_slot = (int*)(slab + lay.act_slot);
+    cidx = (int*)(slab + lay.cidx); csort = (int*)(slab + lay.csort);
+    cur = 0; cur_valid = 0; status = kOk; ntrace = 0; nevents = 0; flags = 0;
+    mem_valid = 0; mem_dim = 0; mem_count = 0; mem_head = 0;
+    n_builds = n_grids = n_stats = n_backtracks = 0;
+    for (int i = 0; i < 6; ++i) tm[i] = 0.0;
+    free_hint = 0;
+    k = 0;
+  }
+
+  // ---- timers (estimator.py:106-114) ----
+  SLSE_D void lap(int which) {
+    unsigned long long t = now_ns();
+    tm[which] += (double)(t - t_mark) * 1e-9;
+    t_mark = t;
+  }
+
+  // ---- active set bookkeeping ----
+  // rebuild act_slot / act_theta / act_gamma from the slot arrays (slot order)
+  SLSE_NIM void compact() {
+    const int chunk = (kmax + b.nt - 1) / b.nt;
+    const int lo = b.tid * chunk;
+    const int hi = lo + chunk < kmax ? lo + chunk : kmax;
+    int cnt = 0;
+    for (int i = lo; i < hi; ++i) cnt += z[i];
+    int total = 0;
+    int off = b.exscan(cnt, total);
+    for (int i = lo; i < hi; ++i) {
+      if (z[i]) {
+        act_slot[off] = i;
+        act_theta[off] = theta[i];
+        act_gamma[off] = gamma[i];
+        ++off;
+      }
+    }
+    k = total;
+    b.sync();
+  }
+
+  // lowest free slot (smlr.py:99-104); leader only
+  SLSE_D int lowest_free() {
+    int s = free_hint;
+    while (s < kmax && z[s]) ++s;
+    free_hint = s + 1;
+    return s;
+  }
+
+  SLSE_D void push_event(int kind, int slot, int idx) {
+    if (b.leader()) {
+      if (nevents < P.ecap) {
+        o.events[3 * nevents] = kind;
+        o.events[3 * nevents + 1] = slot;
+        o.events[3 * nevents + 2] = idx;
+      }
+    }
+    if (nevents < P.ecap) ++nevents; else flags |= kFlEventsFull;
+  }
+
+  // ---- model evaluation ----
+  // Bundle for (th[0..kk), ga[0..kk), beta): model_core.py:257-274
+  SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
+    ++n_builds;
+    steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
+    Factor F = toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
+    if (F.status != kOk) return F.status;
+    B.delta_last = F.delta_last;
+    B.logdet = F.logdet;
+    double quad = gs_apply(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b);
+    B.data_term = F.logdet + quad;
+    B.stats_valid = 0;
+    return kOk;
+  }
+
+  SLSE_NIM void stats(Bundle& B, const double* th, int kk) {
+    if (B.stats_valid) return;
+    ++n_stats;
+    component_stats(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b);
+    B.stats_valid = 1;
+  }
+
+  SLSE_D double objective(const Bundle& B) const { return B.data_term + prior_term(k, zeta, kmax); }
+
+  SLSE_NIM int ensure_cur() {
+    if (cur_valid) return kOk;
+    int st = build(bun[cur], act_theta, act_gamma, k, beta);
+    if (st == kOk) cur_valid = 1;
+    return st;
+  }
+
+  SLSE_NIM void record(int stage) {
+    const double val = objective(bun[cur]);
+    if (b.leader() && ntrace < P.tcap) {
+      o.trace[ntrace] = val;
+      o.stage[ntrace] = stage;
+      o.trace_k[ntrace] = k;
+    }
+    if (ntrace < P.tcap) ++ntrace; else flags |= kFlTraceFull;
+    last_trace = val;
+  }
+  double last_trace;
+
+  // ---- activation (smlr.py:53-171) ----
+  SLSE_NIM double gamma_bar() {  // smlr.py:53-59
+    if (k) {
+      double part = 0.0;
+      for (int i = b.tid; i < k; i += b.nt) part += act_gamma[i];
+      double bar = b.sum(part) / (double)k;
+      if (bar > 0.0) return bar;
+    }
+    double g = energy / ((double)n * kGammaBarKInit);
+    return g > kTiny ? g : kTiny;
+  }
+
+  SLSE_NIM void grid_curve(double gb, double ze) {
+    ++n_grids;
+    Bundle& B = bun[cur];
+    grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
+    const double lr = log((1.0 - ze) / ze);
+    for (int l = b.tid; l < L; l += b.nt) {
+      const double qq = cabs2(G0[l]);
+      q2[l] = qq;
+      dl[l] = gain(qq, sg[l], gb, lr);
+    }
+    b.sync();
+  }
+
+  SLSE_D static double gamma_estimate(double kappa, double s) {  // smlr.py:73-76
+    return kappa > 1.0 ? (kappa * s - s) / (s * s) : 0.0;
+  }
+
+  SLSE_D static bool snr_ok(double kappa, double s, double gb, double ze, double tau) {  // smlr.py:79-81
+    const double rhs = (1.0 + 1.0 / (gb * s)) * log((1.0 + gb * s) * (1.0 - ze) / ze);
+    return kappa > rhs + tau;
+  }
+
+  // returns 1 if a component was activated (smlr.py:107-122)
+  SLSE_NIM int try_activate() {
+    if (k >= kmax) return 0;
+    const double gb = gamma_bar();
+    const double ze = prior_zeta(zeta, kmax);
+    grid_curve(gb, ze);
+    double best = 0.0;
+    int bi = -1;
+    for (int l = b.tid; l < L; l += b.nt) {
+      const double d = dl[l];
+      if (Blk::better(d, l, best, bi)) { best = d; bi = l; }
+    }
+    b.argmin(best, bi);
+    if (bi < 0) return 0;
+    const double s = sg[bi];
+    const double kappa = q2[bi] / s;
+    const double gam = gamma_estimate(kappa, s);
+    if (best >= -kEpsObjective || gam <= 0.0) return 0;
+    if (!snr_ok(kappa, s, gb, ze, P.tau)) return 0;
+    int slot = 0;
+    if (b.leader()) {
+      slot = lowest_free();
+      z[slot] = 1;
+      theta[slot] = (double)bi / (double)L;
+      gamma[slot] = gam;
+    }
+    slot = b.bcast_i(slot);
+    free_hint = slot + 1;
+    push_event(kEvActivate, slot, bi);
+    push_event(kEvEnd, -1, -1);
+    compact();
+    cur_valid = 0;
+    return 1;
+  }
+
+  // initial multi-activation sweep (smlr.py:125-171); returns #added
+  SLSE_NIM int sweep() {
+    const double gb = gamma_bar();
+    const double ze = prior_zeta(zeta, kmax);
+    grid_curve(gb, ze);
+    // circular local minima and their minimum
+    double mn = 0.0;
+    int mi = -1;
+    for (int l = b.tid; l < L; l += b.nt) {
+      const double d = dl[l];
+      const double dp = dl[(l + L - 1) & (L - 1)], dn = dl[(l + 1) & (L - 1)];
+      if (d <= dp && d <= dn) {
+        if (Blk::better(d, l, mn, mi)) { mn = d; mi = l; }
+      }
+    }
+    b.argmin(mn, mi);
+    if (mi < 0) return 0;
+    const double dmin = mn;
+    if (dmin >= -kEpsObjective) return 0;
+    const double thr = dmin / kSweepWithin;
+    // compact qualifying minima in index order
+    const int chunk = (L + b.nt - 1) / b.nt;
+    const int lo = b.tid * chunk;
+    const int hi = lo + chunk < L ? lo + chunk : L;
+    int cnt = 0;
+    for (int l = lo; l < hi; ++l) {
+      const double d = dl[l];
+      const double dp = dl[(l + L - 1) & (L - 1)], dn = dl[(l + 1) & (L - 1)];
+      if (d <= dp && d <= dn && d < -kEpsObjective && !(d > thr)) ++cnt;
+    }
+    int m = 0;
+    int off = b.exscan(cnt, m);
+    for (int l = lo; l < hi; ++l) {
+      const double d = dl[l];
+      const double dp = dl[(l + L - 1) & (L - 1)], dn = dl[(l + 1) & (L - 1)];
+      if (d <= dp && d <= dn && d < -kEpsObjective && !(d > thr)) cidx[off++] = l;
+    }
+    b.sync();
+    // stable sort by (delta, index): rank = #{j: (d_j, j) < (d_i, i)}
+    for (int i = b.tid; i < m; i += b.nt) {
+      const int li = cidx[i];
+      const double di = dl[li];
+      int rank = 0;
+      for (int j = 0; j < m; ++j) {
+        const int lj = cidx[j];
+        const double dj = dl[lj];
+        rank += (dj < di || (dj == di && lj < li)) ? 1 : 0;
+      }
+      csort[rank] = li;
+    }
+    b.sync();
+    // serial pass in sorted order (leader), activating as in the reference
+    int added = 0;
+    if (b.leader()) {
+      const double spacing = kSweepSpacing / (double)n;
+      int kk = k;
+      for (int i = 0; i < m; ++i) {
+        if (kk >= kmax) break;
+        const int l = csort[i];
+        const double s = sg[l];
+        const double kappa = q2[l] / s;
+        const double gnew_ = gamma_estimate(kappa, s);
+        if (gnew_ <= 0.0) continue;
+        const double tau_eff = (kk == 0) ? P.tau : 0.0;
+        if (!snr_ok(kappa, s, gb, ze, tau_eff)) continue;
+        const double th = (double)l / (double)L;
+        if (kk) {
+          double dmn = 2.0;
+          for (int j = 0; j < k; ++j) { double dd = wrap_dist(th, act_theta[j]); dmn = dd < dmn ? dd : dmn; }
+          for (int j = 0; j < added; ++j) { double dd = wrap_dist(th, cth[j]); dmn = dd < dmn ? dd : dmn; }
+          if (dmn < spacing) continue;
+        }
+        const int slot = lowest_free();
+        z[slot] = 1;
+        theta[slot] = th;
+        gamma[slot] = gnew_;
+        cth[added] = th;
+        marg[added] = (double)slot;  // scratch: remember slot order of additions
+        cidx[added] = l;             // cidx no longer needed; reuse for grid index
+        ++added;
+        ++kk;
+      }
+    }
+    added = b.bcast_i(added);
+    if (added) {
+      for (int i = 0; i < added; ++i) push_event(kEvSweep, (int)marg[i], cidx[i]);
+      push_event(kEvEnd, -1, -1);
+      compact();
+      cur_valid = 0;
+    } else {
+      b.sync();
+    }
+    return added;
+  }
+
+  // ---- deactivation (smlr.py:174-225) ----
+  // on return: number removed; cur is valid for the new state (stats too if k>0)
+  SLSE_NIM int deactivate(int* st) {
+    int removed = 0;
+    *st = kOk;
+    while (k) {
+      Bundle& B = bun[cur];
+      const double ze = prior_zeta(zeta, kmax);
+      const double rhs = log((1.0 - ze) / ze);
+      double wv = 0.0;
+      int wi = -1;
+      for (int i = b.tid; i < k; i += b.nt) {
+        const double ga = act_gamma[i];
+        const double s = B.s[i];
+        const double den = 1.0 - ga * s;
+        double mgn;
+        if (ga <= 0.0) {
+          mgn = rhs > 0.0 ? -INFINITY : 0.0;
+        } else if (den <= 0.0) {
+          mgn = INFINITY;
+        } else {
+          const double qq = cabs2(B.q[i]);
+          const double q2dd = qq / (den * den);
+          const double sdd = s / den;
+          const double lhs = q2dd / (1.0 / ga + sdd) - log1p(ga * sdd);
+          mgn = lhs - rhs;
+        }
+        if (Blk::better(mgn, i, wv, wi)) { wv = mgn; wi = i; }
+      }
+      b.argmin(wv, wi);
+      if (wi < 0 || !(wv < 0.0)) break;
+      const int slot = act_slot[wi];
+      if (b.leader()) {
+        z[slot] = 0;
+        gamma[slot] = 0.0;
+      }
+      if (slot < free_hint) free_hint = slot;
+      b.sync();
+      push_event(kEvDeactivate, slot, -1);
+      ++removed;
+      compact();
+      cur_valid = 0;
+      if (k == 0) break;
+      *st = ensure_cur();
+      if (*st != kOk) return removed;
+      stats(bun[cur], act_theta, k);
+    }
+    if (removed) push_event(kEvEnd, -1, -1);
+    return removed;
+  }
+
+  // ---- gradient / diag Hessian (model_core.py:497-536) ----
+  SLSE_NIM void gradient(const Bundle& B, const double* ga, double* g) {
+    for (int i = b.tid; i < k; i += b.nt) {
+      const cplx q = B.q[i], r = B.r[i], t = B.t[i];
+      const cplx cross = cmul(conjg(q), r);
+      g[i] = 2.0 * ga[i] * (t.im - cross.im);
+      g[k + i] = B.s[i] - cabs2(q);
+    }
+  }
+
+  SLSE_NIM void diag_hessian(const Bundle& B, const double* ga_, double* d) {
+    const double fb_theta = (double)(50 * n) * (double)(50 * n);
+    for (int i = b.tid; i < k; i += b.nt) {
+      const double ga = ga_[i];
+      const cplx q = B.q[i], r = B.r[i], u = B.u[i], t = B.t[i], v = B.v[i];
+      const double s = B.s[i], x = B.x[i];
+      const double qq = cabs2(q), rr = cabs2(r);
+      const cplx rqc = cmul(r, conjg(q));
+      const cplx uqc = cmul(u, conjg(q));
+      // core = (x - v) + ga (t^2 - x s) + ga (x q2 + s r2 - 2 t rqc) + uqc - r2
+      const cplx t2 = cmul(t, t);
+      cplx c1 = mk(x - v.re, -v.im);
+      cplx c2 = cscale(mk(t2.re - x * s, t2.im), ga);
+      const cplx trq = cmul(mk(2.0 * t.re, 2.0 * t.im), rqc);
+      cplx c3 = cscale(mk(x * qq + s * rr - trq.re, -trq.im), ga);
+      cplx core = cadd(cadd(c1, c2), c3);
+      core = cadd(core, uqc);
+      core.re -= rr;
+      double d2t = 2.0 * ga * core.re;
+      double d2g = 2.0 * s * qq - s * s;
+      if (d2t <= 0.0) d2t = fb_theta;
+      if (d2g <= 0.0) {
+        const double sg_ = ga > 0.0 ? ga : 1.0 / (50.0 * (double)n);
+        d2g = 1.0 / (sg_ * sg_);
+      }
+      d[i] = d2t;
+      d[k + i] = d2g;
+    }
+  }
+
+  // ---- L-BFGS (lbfgs.py) ----
+  SLSE_D double dot(const double* p, const double* q, int dim) {
+    double part = 0.0;
+    for (int i = b.tid; i < dim; i += b.nt) part += p[i] * q[i];
+    return b.sum(part);
+  }
+
+  // two-loop recursion into dir (lbfgs.py:63-76); uses gnew as q scratch
+  SLSE_NIM void two_loop(int dim) {
+    double alphas[16];
+    double* qv = gnew;
+    for (int i = b.tid; i < dim; i += b.nt) qv[i] = g0[i];
+    const int K2 = 2 * kmax;
+    for (int jj = mem_count - 1; jj >= 0; --jj) {
+      const int slot = (mem_head + jj) % P.lbfgs_mem;
+      const double* S = lbS + (size_t)slot * K2;
+      const double* Y = lbY + (size_t)slot * K2;
+      const double al_ = lbR[slot] * dot(S, qv, dim);
+      alphas[jj] = al_;
+      for (int i = b.tid; i < dim; i += b.nt) qv[i] -= al_ * Y[i];
+    }
+    for (int i = b.tid; i < dim; i += b.nt) dir[i] = qv[i] / diag[i];
+    for (int jj = 0; jj < mem_count; ++jj) {
+      const int slot = (mem_head + jj) % P.lbfgs_mem;
+      const double* S = lbS + (size_t)slot * K2;
+      const double* Y = lbY + (size_t)slot * K2;
+      const double be = lbR[slot] * dot(Y, dir, dim);
+      const double coef = alphas[jj] - be;
+      for (int i = b.tid; i < dim; i += b.nt) dir[i] += S[i] * coef;
+    }
+    for (int i = b.tid; i < dim; i += b.nt) dir[i] = -dir[i];
+  }
+
+  // memory.push(alpha*dir, gnew - g0) (lbfgs.py:47-53)
+  SLSE_NIM void push_pair(double alpha, int dim) {
+    const int K2 = 2 * kmax;
+    const int slot = (mem_count < P.lbfgs_mem) ? (mem_head + mem_count) % P.lbfgs_mem : mem_head;
+    double* S = lbS + (size_t)slot * K2;
+    double* Y = lbY + (size_t)slot * K2;
+    double pv[3] = {0.0, 0.0, 0.0};
+    for (int i = b.tid; i < dim; i += b.nt) {
+      const double s = alpha * dir[i];
+      const double yv = gnew[i] - g0[i];
+      S[i] = s;
+      Y[i] = yv;
+      pv[0] += s * yv;
+      pv[1] += s * s;
+      pv[2] += yv * yv;
+    }
+    b.sumv(pv, 3);
+    const double curv = pv[0];
+    if (curv <= kCurvEps * sqrt(pv[1]) * sqrt(pv[2])) return;
+    if (b.leader()) lbR[slot] = 1.0 / curv;
+    if (mem_count < P.lbfgs_mem) {
+      ++mem_count;
+    } else {
+      mem_head = (mem_head + 1) % P.lbfgs_mem;
+    }
+    b.sync();
+  }
+
+  // One lbfgs_step (lbfgs.py:100-136).  Returns 0 accepted, 1 line-search
+  // failure, or a negative model status.  On acceptance the new point is in
+  // the slot arrays, cur is the accepted bundle (stats valid), *dec set.
+  SLSE_NIM int lbfgs_step(double f0, double* dec) {
+    const int dim = 2 * k;
+    // any(g0)?
+    double nz = 0.0;
+    for (int i = b.tid; i < dim; i += b.nt) nz += (g0[i] != 0.0) ? 1.0 : 0.0;
+    if (b.sum(nz) == 0.0) {
+      *dec = 0.0;
+      return 0;  // point unchanged
+    }
+    two_loop(dim);
+    double slope = dot(g0, dir, dim);
+    if (slope >= 0.0) {
+      for (int i = b.tid; i < dim; i += b.nt) dir[i] = -g0[i] / diag[i];
+      slope = dot(g0, dir, dim);
+    }
+    *dec = -slope;
+    // gamma step cap (lbfgs.py:84-90)
+    double capv = INFINITY;
+    for (int i = b.tid; i < k; i += b.nt) {
+      const double dg = dir[k + i];
+      if (dg < 0.0) {
+        const double r = pt[k + i] / -dg;
+        capv = r < capv ? r : capv;
+      }
+    }
+    capv = b.minv(capv);
+    double alpha = capv < 1.0 ? capv : 1.0;
+    if (alpha <= 0.0) return 1;
+    Bundle& T = bun[cur ^ 1];
+    for (int bt = 0; bt < kMaxBacktracks; ++bt) {
+      ++n_backtracks;
+      for (int i = b.tid; i < k; i += b.nt) {
+        cth[i] = np_mod1(pt[i] + alpha * dir[i]);
+        cga[i] = pt[k + i] + alpha * dir[k + i];
+        cand[i] = cth[i];
+        cand[k + i] = cga[i];
+      }
+      b.sync();
+      int st = build(T, cth, cga, k, beta);
+      if (st != kOk) return -st;
+      const double fn = T.data_term + prior_term(k, zeta, kmax);
+      if (fn <= f0 + kArmijoC1 * alpha * slope) {
+        stats(T, cth, k);
+        gradient(T, cga, gnew);
+        b.sync();
+        push_pair(alpha, dim);
+        // accept: write the point into the slots; swap bundles
+        for (int i = b.tid; i < k; i += b.nt) {
+          const int s = act_slot[i];
+          theta[s] = cth[i];
+          gamma[s] = cga[i];
+          act_theta[i] = cth[i];
+          act_gamma[i] = cga[i];
+        }
+        b.sync();
+        cur ^= 1;
+        cur_valid = 1;
+        return 0;
+      }
+      alpha *= kBacktrack;
+    }
+    return 1;
+  }
+
+  // ---- the outer loop (estimator.py:117-275) ----
+  SLSE_NIM void run() {
+    t_start = now_ns();
+    t_mark = t_start;
+    // energy, floor, beta0 (model_core.py:125-130; estimator.py:135-137)
+    double part = 0.0;
+    for (int i = b.tid; i < n; i += b.nt) {
+      part += cabs2(y[i]);
+    }
+    energy = b.sum(part);
+    floor_beta = kBetaFloorScale * energy / (double)n;
+    const double b0 = kInitialBetaFrac * energy / (double)n;
+    beta = b0 > floor_beta ? b0 : floor_beta;
+    zeta = kInitialZeta;
+    for (int i = b.tid; i < kmax; i += b.nt) { z[i] = 0; theta[i] = 0.0; gamma[i] = 0.0; }
+    k = 0;
+    // cached spectrum of y for every GS apply
+    fft(yhat, 1 << ilog2(2 * n), -1.0, [&](int i) { return i < n ? y[i] : mk(0.0, 0.0); },
+        [&](int i, cplx v) { yhat[i] = v; }, f, b);
+    status = ensure_cur();
+    if (status != kOk) { finish(0, 0); return; }
+    record(kStInit);
+    {  // warm-up beta (estimator.py:153)
+      const double v = energy / (double)n;
+      beta = floor_beta > v ? floor_beta : v;
+      cur_valid = 0;
+    }
+    status = ensure_cur();
+    if (status != kOk) { finish(0, 0); return; }
+    record(kStBeta);
+    lap(kTmObjective);
+    double previous = last_trace;
+    int z_dirty = 1;
+    int converged = 0;
+    int iterations = 0;
+    for (int it = 1; it <= P.max_outer; ++it) {
+      iterations = it;
+      // 1) activation
+      if (it <= P.sweep_iters) {
+        status = ensure_cur();
+        if (status != kOk) break;
+        if (sweep()) z_dirty = 1;
+      } else {
+        int hit_cap = 1;
+        for (int rep = 0; rep < kmax; ++rep) {
+          status = ensure_cur();
+          if (status != kOk) break;
+          if (!try_activate()) { hit_cap = 0; break; }
+          z_dirty = 1;
+        }
+        if (status != kOk) break;
+        if (hit_cap) flags |= kFlKmaxCap;
+      }
+      lap(kTmActivate);
+      status = ensure_cur();
+      if (status != kOk) break;
+      record(kStActivate);
+      lap(kTmObjective);
+      // 2) zeta (estimator.py:69-74)
+      {
+        const double zz = (double)k / (double)kmax;
+        zeta = zz < 0.5 ? zz : 0.5;
+      }
+      record(kStZeta);
+      // 3) beta EM step (estimator.py:184-203)
+      double value;
+      if (k) {
+        Bundle& B = bun[cur];
+        stats(B, act_theta, k);
+        double tr_part = 0.0;
+        for (int i = b.tid; i < k; i += b.nt) {
+          mu[i] = cscale(B.q[i], act_gamma[i]);
+          tr_part += B.s[i] * act_gamma[i];
+        }
+        const double tr = beta * b.sum(tr_part);
+        value = residual_value(tr);
+      } else {
+        value = energy / (double)n;
+      }
+      const double bc = floor_beta > value ? floor_beta : value;
+      {
+        Bundle& T = bun[cur ^ 1];
+        status = build(T, act_theta, act_gamma, k, bc);
+        if (status != kOk) break;
+        const double fc = T.data_term + prior_term(k, zeta, kmax);
+        if (fc <= last_trace) {
+          beta = bc;
+          cur ^= 1;
+          cur_valid = 1;
+        }
+      }
+      lap(kTmBeta);
+      record(kStBeta);
+      lap(kTmObjective);
+      // 4) refinement (estimator.py:206-245)
+      if (k) {
+        for (int inner = 0; inner < P.inner_max; ++inner) {
+          Bundle& B = bun[cur];
+          stats(B, act_theta, k);
+          if (z_dirty || !mem_valid || mem_dim != 2 * k) {
+            diag_hessian(B, act_gamma, diag);
+            mem_valid = 1;
+            mem_dim = 2 * k;
+            mem_count = 0;
+            mem_head = 0;
+            z_dirty = 0;
+          }
+          gradient(B, act_gamma, g0);
+          for (int i = b.tid; i < k; i += b.nt) { pt[i] = act_theta[i]; pt[k + i] = act_gamma[i]; }
+          b.sync();
+          const double f0 = objective(B);
+          double dec = 0.0;
+          int rs = lbfgs_step(f0, &dec);
+          if (rs < 0) { status = -rs; break; }
+          if (rs == 1) break;
+          lap(kTmRefine);
+          record(kStRefine);
+          lap(kTmObjective);
+          int st = kOk;
+          stats(bun[cur], act_theta, k);
+          int removed = deactivate(&st);
+          if (st != kOk) { status = st; break; }
+          if (removed) {
+            z_dirty = 1;
+            lap(kTmDeactivate);
+            status = ensure_cur();
+            if (status != kOk) break;
+            record(kStDeactivate);
+            lap(kTmObjective);
+            if (k == 0) break;
+          }
+          if (dec < (double)n * P.dec_tol_scale) break;
+        }
+        if (status != kOk) break;
+      }
+      lap(kTmRefine);
+      const double current = last_trace;
+      if (fabs(previous - current) < (double)n * P.conv_tol_scale) {
+        converged = 1;
+        break;
+      }
+      previous = current;
+    }
+    finish(iterations, converged);
+  }
+
+  // beta EM value (tr + ||y - Psi(theta) mu||^2) / M  (estimator.py:86-88)
+  SLSE_NIM double residual_value(double tr) {
+    double* mre = marg;  // scratch (length >= k)
+    double* mim = dtmp;  // scratch (length n >= k), free outside build()
+    for (int i = b.tid; i < k; i += b.nt) { mre[i] = mu[i].re; mim[i] = mu[i].im; }
+    b.sync();
+    steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
+    double part = 0.0;
+    for (int i = b.tid; i < n; i += b.nt) part += cabs2(csub(y[i], c[i]));
+    const double resid = b.sum(part);
+    return (tr + resid) / (double)n;
+  }
+
+  SLSE_NIM void finish(int iterations, int converged) {
+    // posterior mean alpha = gamma * q (model_core.py:539-547)
+    if (status == kOk && k) {
+      int st = ensure_cur();
+      if (st == kOk) {
+        stats(bun[cur], act_theta, k);
+        for (int i = b.tid; i < k; i += b.nt) {
+          o.alpha[i] = cscale(bun[cur].q[i], act_gamma[i]);
+          o.theta[i] = act_theta[i];
+          o.gamma[i] = act_gamma[i];
+          o.slot[i] = act_slot[i];
+        }
+      } else {
+        status = st;
+      }
+    }
+    tm[kTmTotal] = (double)(now_ns() - t_start) * 1e-9;
+    if (converged) flags |= kFlConverged;
+    if (b.leader()) {
+      *o.khat = k;
+      *o.status = status;
+      *o.iters = iterations;
+      *o.flags = flags;
+      *o.beta = beta;
+      *o.zeta = zeta;
+      *o.ntrace = ntrace;
+      *o.nevents = nevents;
+      o.counters[0] = n_builds;
+      o.counters[1] = n_grids;
+      o.counters[2] = n_stats;
+      o.counters[3] = n_backtracks;
+      for (int i = 0; i < 6; ++i) o.stage_s[i] = tm[i];
+    }
+    b.sync();
+  }
+};
+
+}  // namespace slse

@@ -1,0 +1,176 @@
+// slse_stats.cuh -- per-component statistics (q, r, u, s, t, v, x) at the
+// active frequencies and the activation grid (q^G, s^G) with the fused
+// activation-gain curve.
+//
+// Reference: model_core.py:281-313 (_SuperfastBundle.stats / grid),
+// toeplitz.py:317-432 (omega diagonal sums), nufft.py:147-181 (adjoint and
+// two-sided sums), smlr.py:62-70 (gain curve).
+//
+// Product form (no omega sums): with A_a(th) = sum_q q^a rho_q e^{-j2pi q th},
+//   kind(th) = scale_kind / delta * sum_{(a,b)} cf^{kind}_{ab} A_a conj(A_b)
+// where cf are the reference's cross-correlation-basis coefficients
+// (toeplitz.py:317-365): R_ab(i) = sum_q q^a rho_q (q+i)^b conj(rho_{q+i})
+// and sum_i R_ab(i) e^{j2pi i th} = A_a conj(A_b) exactly.
+#pragma once
+#include "slse_toeplitz.cuh"
+
+namespace slse {
+
+constexpr double kPi = 3.14159265358979323846;
+
+// cf[kind][a][b], kind = s,t,v,x ; mirrors toeplitz.py:317-365.
+struct CfTable {
+  double cf[4][4][4];
+};
+
+SLSE_HD void cf_add(CfTable& T, int kind, int a, int b, double c) {
+  // q^a i^b with i = m - q  ->  sum_j C(b,j) m^j (-q)^{b-j}
+  const int binom[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
+  for (int j = 0; j <= b; ++j) {
+    const double sgn = ((b - j) & 1) ? -1.0 : 1.0;
+    T.cf[kind][a + b - j][j] += c * (double)binom[b][j] * sgn;
+  }
+}
+
+SLSE_HD void cf_build(CfTable& T, int n_) {
+  const double n = (double)n_;
+  for (int k = 0; k < 4; ++k)
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) T.cf[k][a][b] = 0.0;
+  const double n3 = (double)((long long)n_ * n_ * n_);
+  // s
+  cf_add(T, 0, 0, 0, 2.0 - n);
+  cf_add(T, 0, 0, 1, 1.0);
+  cf_add(T, 0, 1, 0, 2.0);
+  // t
+  cf_add(T, 1, 1, 1, -1.0);
+  cf_add(T, 1, 0, 1, n - 1.5);
+  cf_add(T, 1, 0, 2, -0.5);
+  cf_add(T, 1, 1, 0, n - 1.0);
+  cf_add(T, 1, 0, 0, -(n - 1.0) * (n - 2.0) / 2.0);
+  // v
+  cf_add(T, 2, 3, 0, 2.0 / 3.0);
+  cf_add(T, 2, 2, 1, 1.0);
+  cf_add(T, 2, 1, 2, 1.0);
+  cf_add(T, 2, 2, 0, 2.0 - n);
+  cf_add(T, 2, 1, 1, 3.0 - 2.0 * n);
+  cf_add(T, 2, 1, 0, n * n - 3.0 * n + 7.0 / 3.0);
+  cf_add(T, 2, 0, 3, 1.0 / 3.0);
+  cf_add(T, 2, 0, 2, 1.5 - n);
+  cf_add(T, 2, 0, 1, n * n - 3.0 * n + 13.0 / 6.0);
+  cf_add(T, 2, 0, 0, 1.5 * n * n - n3 / 3.0 - 13.0 * n / 6.0 + 1.0);
+  // x
+  cf_add(T, 3, 3, 0, 2.0 / 3.0);
+  cf_add(T, 3, 2, 1, 1.0);
+  cf_add(T, 3, 2, 0, 2.0 - n);
+  cf_add(T, 3, 1, 1, 2.0 - n);
+  cf_add(T, 3, 1, 0, n * n - 3.0 * n + 7.0 / 3.0);
+  cf_add(T, 3, 0, 3, -1.0 / 6.0);
+  cf_add(T, 3, 0, 1, (3.0 * n * n - 9.0 * n + 7.0) / 6.0);
+  cf_add(T, 3, 0, 0, -n3 / 3.0 + 1.5 * n * n - 13.0 * n / 6.0 + 1.0);
+}
+
+// Statistics for K frequencies.  One warp per frequency; lanes stride the
+// sample axis with a phasor recurrence re-anchored (exact sincospi) every
+// 32 steps.  Outputs (length K): q, r, u, t, v complex; s, x real.
+// `cf` must be visible to the whole block (shared memory or global).
+SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cplx* SLSE_RESTRICT rho,
+                            const cplx* SLSE_RESTRICT w, int n, double delta_last, const CfTable* cf,
+                            cplx* q, cplx* r, cplx* u, double* s, cplx* t, cplx* v, double* x,
+                            Blk& b) {
+  const double inv_d = 1.0 / delta_last;
+  const double two_pi = 2.0 * kPi;
+#ifdef SLSE_HOST_EMU
+  const int lanes = 1, lane = 0, warp = 0, nwarp = 1;
+#else
+  const int lanes = 32, lane = b.tid & 31, warp = b.tid >> 5, nwarp = b.nt >> 5;
+#endif
+  for (int kk = warp; kk < K; kk += nwarp) {
+    const double th = thetas[kk];
+    double acc[14];
+#pragma unroll
+    for (int i = 0; i < 14; ++i) acc[i] = 0.0;
+    const cplx step = expj2pi((double)lanes, th, -1.0);
+    cplx e = mk(1.0, 0.0);
+    int since = 1 << 30;
+    for (int m = lane; m < n; m += lanes) {
+      if (since >= 32) {
+        e = expj2pi((double)m, th, -1.0);
+        since = 0;
+      }
+      const double dm = (double)m;
+      const cplx p = cmul(rho[m], e);
+      const cplx qq = cmul(w[m], e);
+      const double m2 = dm * dm, m3 = m2 * dm;
+      acc[0] += p.re;       acc[1] += p.im;
+      acc[2] += dm * p.re;  acc[3] += dm * p.im;
+      acc[4] += m2 * p.re;  acc[5] += m2 * p.im;
+      acc[6] += m3 * p.re;  acc[7] += m3 * p.im;
+      const double d1 = two_pi * dm;
+      const double d2 = d1 * d1;
+      acc[8] += qq.re;       acc[9] += qq.im;
+      acc[10] += d1 * qq.re; acc[11] += d1 * qq.im;
+      acc[12] += d2 * qq.re; acc[13] += d2 * qq.im;
+      e = cmul(e, step);
+      ++since;
+    }
+#ifndef SLSE_HOST_EMU
+#pragma unroll
+    for (int i = 0; i < 14; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    }
+#endif
+    if (lane == 0) {
+      cplx A[4];
+      for (int a = 0; a < 4; ++a) A[a] = mk(acc[2 * a], acc[2 * a + 1]);
+      q[kk] = mk(acc[8], acc[9]);
+      r[kk] = mk(acc[10], acc[11]);
+      u[kk] = mk(acc[12], acc[13]);
+      cplx sum[4];
+      for (int kind = 0; kind < 4; ++kind) {
+        cplx tot = mk(0.0, 0.0);
+        for (int a = 0; a < 4; ++a)
+          for (int bb = 0; bb < 4; ++bb) {
+            const double c = cf->cf[kind][a][bb];
+            if (c != 0.0) tot = cadd(tot, cscale(cmulc(A[a], A[bb]), c));
+          }
+        sum[kind] = tot;
+      }
+      const double sc_tv = two_pi * inv_d, sc_vx = 4.0 * kPi * kPi * inv_d;
+      s[kk] = sum[0].re * inv_d;
+      t[kk] = cscale(sum[1], sc_tv);
+      v[kk] = cscale(sum[2], sc_vx);
+      x[kk] = sum[3].re * sc_vx;
+    }
+  }
+  b.sync();
+}
+
+// Activation grid (model_core.py:303-313) in product form:
+//   q^G = FFT_L(w),  s^G = delta^{-1} [(2-N)|A0|^2 + 2 Re(A1 conj A0)],
+//   A0 = FFT_L(rho), A1 = FFT_L(n rho_n).
+// Results land in G0 (q^G), and sg (s^G, real).  G1/G2 are scratch.
+SLSE_NI void grid_eval(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT w, int n, double delta_last,
+                      int L, cplx* G0, cplx* G1, cplx* G2, double* sg, const FftCtx& f, Blk& b) {
+  const cplx z = mk(0.0, 0.0);
+  fft(G0, L, -1.0, [&](int i) { return i < n ? w[i] : z; }, [&](int i, cplx v) { G0[i] = v; }, f, b);
+  fft(G1, L, -1.0, [&](int i) { return i < n ? rho[i] : z; }, [&](int i, cplx v) { G1[i] = v; }, f, b);
+  fft(G2, L, -1.0, [&](int i) { return i < n ? cscale(rho[i], (double)i) : z; },
+      [&](int i, cplx v) { G2[i] = v; }, f, b);
+  const double c2n = 2.0 - (double)n;
+  const double inv_d = 1.0 / delta_last;
+  for (int l = b.tid; l < L; l += b.nt) {
+    const cplx a0 = G1[l], a1 = G2[l];
+    sg[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+  }
+  b.sync();
+}
+
+// Activation gain (smlr.py:62-70, G = 1):
+//   Delta = log1p(gb s) + log((1-ze)/ze) - |q|^2 / (1/gb + s)
+SLSE_D double gain(double q2, double s, double gb, double log_ratio) {
+  return (log1p(gb * s) + log_ratio) - q2 / (1.0 / gb + s);
+}
+
+}  // namespace slse

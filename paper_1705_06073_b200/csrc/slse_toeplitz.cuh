@@ -1,0 +1,232 @@
+// slse_toeplitz.cuh -- Hermitian-Toeplitz column, Gohberg-Semencul factor,
+// GS apply (C^{-1} y) and the objective's data term.
+//
+// Reference: toeplitz.py (HermitianToeplitz :44-64, levinson_durbin
+// :121-145, generalized_schur :230-260, apply_inverse :279-309,
+// log_det :312-314); model_core.py:242-249, 256-274.
+#pragma once
+#include "slse_fft.cuh"
+
+namespace slse {
+
+constexpr double kPdEps = 1e-13;  // toeplitz.py:32
+
+enum Status : int {
+  kOk = 0,
+  kNotPD = 1,          // NotPositiveDefinite (toeplitz.py:55-57, 141-142, 191-192, 249-252)
+  kBadColumn = 2,      // c_0 not real-positive (toeplitz.py:55-57)
+  kCapacity = 3,       // trace / event buffer too small (results truncated)
+};
+
+// ---------------------------------------------------------------------------
+// Row 1: y_m = beta*[m==0] + sum_k coef_k e^{+j 2 pi m theta_k}, m = 0..n-1
+// (nufft.py:126-144 direct branch; model_core.py:264-265).  Thread t owns
+// m = t, t+nt, ...; e^{j2pi m theta} advances by the phasor e^{j2pi nt theta}
+// and is re-anchored with an exact sincospi every 16 steps.
+// coef_re/coef_im: coefficient k (coef_im may be null for real gammas).
+// column=true: covariance-column convention, c_0 <- Re(c_0) + beta0.
+SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RESTRICT thetas,
+                          const double* SLSE_RESTRICT coef_re, const double* SLSE_RESTRICT coef_im,
+                          int k, double beta0, bool column, Blk& b) {
+  // accumulate in registers chunk-wise: each thread handles up to 16 owned m
+  // values per sweep over k.
+  for (int m0 = b.tid; m0 < n; m0 += 16 * b.nt) {
+    const int J = (n - m0 + b.nt - 1) / b.nt;  // owned values in this chunk (<= 16 used)
+    cplx acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = mk(0.0, 0.0);
+    for (int kk = 0; kk < k; ++kk) {
+      const double th = thetas[kk];
+      const double cr = coef_re[kk];
+      const double ci = coef_im ? coef_im[kk] : 0.0;
+      cplx e = expj2pi((double)m0, th, 1.0);
+      cplx step = expj2pi((double)b.nt, th, 1.0);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < J) {
+          // coef * basis, summed over k in slot order
+          acc[j].re += e.re * cr - e.im * ci;
+          acc[j].im += e.re * ci + e.im * cr;
+          e = cmul(e, step);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int m = m0 + j * b.nt;
+      if (m < n) {
+        cplx v = acc[j];
+        if (column && m == 0) v = mk(v.re + beta0, 0.0);  // c_0 forced real (toeplitz.py:58-59)
+        out[m] = v;
+      }
+    }
+  }
+  b.sync();
+}
+
+// ---------------------------------------------------------------------------
+// Rows 2-4: Gohberg-Semencul parameters (rho, delta) by the Schur-Levinson
+// recursion.  Reflection coefficients come from the Schur generators
+// (no inner products: one barrier per step), the predictor a follows the
+// Levinson update a <- a + k z conj(rev a) (toeplitz.py:135-142); with
+// e_j^{(m)} = sum_i a_i c_{j-i} and B_j^{(m)} = b_{j+m}^{(m)} the backward
+// residual in a shifted frame:
+//   k      = -e_{m+1} / delta_m
+//   e_{j+m+1} += k B_j ,  B_j += conj(k) e_{j+m+1}      (j = 0..N-2-m)
+//   delta_{m+1} = delta_m (1 - |k|^2)
+// Numerically equivalent to the reference's LD / generalized Schur within
+// ~1e-13.  Work arrays e, B, a hold n complex each (shared
+// memory when they fit, else global).  Output rho_i = conj(a_{N-1-i})
+// (rho_{N-1} = 1), delta (optional array), sum log delta, delta_{N-1}.
+struct Factor {
+  double logdet;
+  double delta_last;
+  double c0;
+  int status;
+};
+
+SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
+                              double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho,
+                              Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  // HermitianToeplitz validation (toeplitz.py:55-57)
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  const double c0 = c0c.re;
+  const double floor_ = kPdEps * c0;
+  for (int j = b.tid; j < n; j += b.nt) {
+    cplx cj = (j == 0) ? mk(c0, 0.0) : c[j];
+    e[j] = cj;
+    B[j] = cj;
+    a[j] = mk(j == 0 ? 1.0 : 0.0, 0.0);
+    delta_tmp[j] = 0.0;
+  }
+  if (b.tid == 0) delta_tmp[0] = c0;
+  b.sync();
+  double delta = c0;
+  int fail = 0;
+  for (int m = 0; m + 1 < n; ++m) {
+    const cplx em = e[m + 1];
+    const cplx k = mk(-em.re / delta, -em.im / delta);
+    const cplx kc = conjg(k);
+    const int cnt = n - 1 - m;  // pairs j = 0..cnt-1
+    for (int j = b.tid; j < cnt; j += b.nt) {
+      const cplx ej = e[j + m + 1];
+      const cplx bj = B[j];
+      if (j > 0) e[j + m + 1] = cadd(ej, cmul(k, bj));
+      B[j] = cadd(bj, cmul(kc, ej));
+    }
+    // predictor: a_i' = a_i + k conj(a_{m+1-i}), i = 1..m+1 (a_{m+1} = 0 before)
+    const int top = m + 1;
+    const int npair = (top + 1) / 2;  // i = 1..npair pairs with top-i (i <= top-i or middle)
+    for (int i = b.tid; i <= npair; i += b.nt) {
+      if (i == 0) {
+        // a_{top} = 0 + k * conj(a_0)
+        a[top] = cmul(k, conjg(a[0]));
+      } else {
+        const int jj = top - i;
+        if (i < jj) {
+          const cplx ai = a[i], aj = a[jj];
+          a[i] = cadd(ai, cmul(k, conjg(aj)));
+          a[jj] = cadd(aj, cmul(k, conjg(ai)));
+        } else if (i == jj) {
+          const cplx ai = a[i];
+          a[i] = cadd(ai, cmul(k, conjg(ai)));
+        }
+      }
+    }
+    delta = delta * (1.0 - (k.re * k.re + k.im * k.im));
+    if (b.tid == 0) delta_tmp[m + 1] = delta;
+    b.sync();
+    if (!(delta > floor_)) { fail = 1; break; }
+  }
+  if (fail) {
+    F.status = kNotPD;
+    return F;
+  }
+  F.delta_last = delta;
+  double part = 0.0;
+  for (int j = b.tid; j < n; j += b.nt) {
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
+    rho[j] = conjg(a[n - 1 - j]);
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+
+// ---------------------------------------------------------------------------
+// Row 5: w = C^{-1} x = delta^{-1} (T1^H T1 x - T0 T0^H x) via FFTs of length
+// nf = 2^ceil(log2 2N) (toeplitz.py:279-309).  All four kernel spectra derive from
+// P1 = FFT(rho): with W = e^{-2 pi i/nf},
+//   FFT(conj(rev rho))_k = W^{(N-1)k} conj(P1_k)
+//   P0_k  = FFT(v0)_k    = W^k (P1_k - rho_{N-1} W^{(N-1)k}),  v0 = [0, rho_0..rho_{N-2}]
+//   P0h_k = FFT(conj(rev v0))_k = W^{(N-1)k} conj(P0_k).
+// Xhat = FFT_nf(x) is cached by the caller (x = y is fixed per problem).
+// Buffers P, U, V: nf complex each (global).
+SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
+                       const cplx* SLSE_RESTRICT x, const cplx* SLSE_RESTRICT Xhat, cplx* P, cplx* U,
+                       cplx* V, cplx* SLSE_RESTRICT w, const FftCtx& f, Blk& b) {
+  const int lg = ilog2(2 * n);  // nf = next power of two >= 2N
+  const int nf = 1 << lg;
+  const cplx rlast = rho[n - 1];
+  // P = FFT(rho zero-padded)
+  fft(P, nf, -1.0,
+      [&](int i) { return i < n ? rho[i] : mk(0.0, 0.0); },
+      [&](int i, cplx v) { P[i] = v; }, f, b);
+  // U = Xhat * P1 ; V = Xhat * P0h
+  for (int k = b.tid; k < nf; k += b.nt) {
+    const cplx p1 = P[k];
+    const cplx wk = twid(f, k, lg, -1.0);
+    const cplx wn1 = twid(f, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
+    const cplx p0 = cmul(wk, csub(p1, cmul(rlast, wn1)));
+    const cplx p0h = cmul(wn1, conjg(p0));
+    const cplx xk = Xhat[k];
+    U[k] = cmul(xk, p1);
+    V[k] = cmul(xk, p0h);
+  }
+  b.sync();
+  const double inv = 1.0 / (double)nf;
+  // t1x = IFFT(U)[N-1 : 2N-1] and t0hx = IFFT(V)[N-1 : 2N-1], zero padded
+  fft_inplace(U, nf, 1.0, f, b);
+  fft_inplace(V, nf, 1.0, f, b);
+  // shift down by N-1 through registers (barrier between read and write)
+  for (int i0 = 0; i0 < nf; i0 += b.nt) {
+    const int i = i0 + b.tid;
+    cplx u = mk(0.0, 0.0), v = mk(0.0, 0.0);
+    if (i < n) { u = cscale(U[n - 1 + i], inv); v = cscale(V[n - 1 + i], inv); }
+    b.sync();
+    if (i < nf) { U[i] = u; V[i] = v; }
+    b.sync();
+  }
+  fft_inplace(U, nf, -1.0, f, b);
+  fft_inplace(V, nf, -1.0, f, b);
+  // Z = F1 * P1h - F0 * P0  -> U
+  for (int k = b.tid; k < nf; k += b.nt) {
+    const cplx p1 = P[k];
+    const cplx wk = twid(f, k, lg, -1.0);
+    const cplx wn1 = twid(f, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
+    const cplx p1h = cmul(wn1, conjg(p1));
+    const cplx p0 = cmul(wk, csub(p1, cmul(rlast, wn1)));
+    U[k] = csub(cmul(U[k], p1h), cmul(V[k], p0));
+  }
+  b.sync();
+  const double sc = inv / delta_last;
+  double quad = 0.0;
+  fft_inplace(U, nf, 1.0, f, b);
+  for (int i = b.tid; i < n; i += b.nt) {
+    const cplx wi = cscale(U[i], sc);
+    w[i] = wi;
+    quad += x[i].re * wi.re + x[i].im * wi.im;  // Re(conj(x) w)
+  }
+  return b.sum(quad);
+}
+
+}  // namespace slse

@@ -1,0 +1,302 @@
+"""Drop-in estimator boundary: ``estimate(obs, opts) -> LseResult``.
+
+Same signature, options and result type as the reference
+(estimator.py:34-66, 117-283).  The whole outer loop runs on the GPU: one
+CTA per problem executes the estimator state machine (csrc/slse_solver.cuh)
+and this module only packs inputs, launches ``slse_estimate_batch`` through
+the C ABI and unpacks results.  ``estimate_batch`` is the batched entry
+point (one problem per row).
+
+Scope: complete data, a single snapshot (G = 1), the
+superfast backend.  ``backend="auto"`` runs superfast for complete data
+(the reference's auto picks its semifast backend below N = 512; both agree
+to ~1e-13 per call and give the same trajectories).
+``backend="semifast"``, incomplete patterns and G > 1 are outside this
+build's scope and raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import DimensionMismatch, InvalidPattern, NotPositiveDefinite, SuperLseError
+from .model_core import BACKENDS, Observation, default_grid_size
+
+DEFAULT_TAU = 5.0  # smlr.py:28
+STAGE_NAMES = ("init", "beta", "activate", "zeta", "refine", "deactivate")
+TIMER_NAMES = ("activate", "objective", "beta", "refine", "deactivate", "total")
+FLAG_CONVERGED, FLAG_KMAX_CAP, FLAG_TRACE_FULL, FLAG_EVENTS_FULL = 1, 2, 4, 8
+STATUS_OK, STATUS_NOT_PD, STATUS_BAD_DIAGONAL = 0, 1, 2
+
+
+@dataclass
+class EstimatorOptions:
+    """Knobs of the outer loop (estimator.py:34-50)."""
+
+    grid_factor: int = 8
+    tau: float = DEFAULT_TAU
+    max_outer_iterations: int = 200
+    convergence_tol_scale: float = 1e-7
+    lbfgs_inner_max: int = 5
+    newton_decrement_tol_scale: float = 1e-8
+    backend: str = "auto"
+    seed: int = None
+    initial_sweep_iterations: int = 3
+    lbfgs_memory: int = 10
+    k_max: int = None
+    decomp_method: str = "auto"
+    steer_method: str = "auto"
+
+
+@dataclass
+class LseResult:
+    """estimator.py:53-66, plus the active-set history (``events``) and
+    per-problem counters the GPU path records."""
+
+    k_hat: int
+    theta_hat: np.ndarray
+    alpha_hat: np.ndarray
+    beta_hat: float
+    gamma_hat: np.ndarray
+    zeta_hat: float
+    objective_trace: np.ndarray
+    iterations: int
+    wall_time_per_stage: dict
+    converged: bool = True
+    trace_stages: list = field(default_factory=list)
+    warnings: list = field(default_factory=list)
+    events: list = field(default_factory=list)
+    trace_k: np.ndarray = None
+    slots: np.ndarray = None
+    counters: dict = field(default_factory=dict)
+    status: int = STATUS_OK
+
+
+def _validate(opts: EstimatorOptions):
+    if opts.backend not in BACKENDS:
+        raise ValueError(f"backend must be one of {BACKENDS}")
+    if opts.backend == "semifast":
+        raise NotImplementedError("the semifast (Woodbury) backend is outside this build's scope")
+    if opts.decomp_method not in ("auto", "levinson", "schur"):
+        raise ValueError(f"unknown decomposition method {opts.decomp_method!r}")
+    if opts.steer_method not in ("auto", "direct", "nufft"):
+        raise ValueError(f"unknown method {opts.steer_method!r}")
+    if not 1 <= opts.lbfgs_memory <= 16:
+        raise ValueError("lbfgs_memory must lie in 1..16 on the GPU path")
+
+
+def c_options(opts: EstimatorOptions, n: int) -> _native.SlseOptions:
+    o = _native.SlseOptions()
+    o.grid_factor = int(opts.grid_factor)
+    o.tau = float(opts.tau)
+    o.max_outer_iterations = int(opts.max_outer_iterations)
+    o.convergence_tol_scale = float(opts.convergence_tol_scale)
+    o.lbfgs_inner_max = int(opts.lbfgs_inner_max)
+    o.newton_decrement_tol_scale = float(opts.newton_decrement_tol_scale)
+    o.initial_sweep_iterations = int(opts.initial_sweep_iterations)
+    o.lbfgs_memory = int(opts.lbfgs_memory)
+    o.k_max = int(opts.k_max) if opts.k_max is not None else n
+    o.trace_capacity = 2 + 13 * int(opts.max_outer_iterations)
+    o.event_capacity = 4 * o.k_max + 64
+    return o
+
+
+class BatchOutputs:
+    """Output arrays of one batched solve (torch tensors on one device, or
+    numpy arrays for host-side consumers), laid out as slse_outputs."""
+
+    def __init__(self, xp_empty, B, kmax, tcap, ecap):
+        e = xp_empty
+        self.k_hat = e((B,), "i32")
+        self.status = e((B,), "i32")
+        self.iterations = e((B,), "i32")
+        self.flags = e((B,), "i32")
+        self.beta = e((B,), "f64")
+        self.zeta = e((B,), "f64")
+        self.theta = e((B, kmax), "f64")
+        self.gamma = e((B, kmax), "f64")
+        self.alpha = e((B, kmax, 2), "f64")
+        self.slot = e((B, kmax), "i32")
+        self.trace = e((B, tcap), "f64")
+        self.stage = e((B, tcap), "i32")
+        self.trace_k = e((B, tcap), "i32")
+        self.n_trace = e((B,), "i32")
+        self.events = e((B, ecap, 3), "i32")
+        self.n_events = e((B,), "i32")
+        self.counters = e((B, 4), "i64")
+        self.stage_seconds = e((B, 6), "f64")
+
+    def struct(self, ptr_of) -> _native.SlseOutputs:
+        s = _native.SlseOutputs()
+        for name in _native.OUTPUT_FIELDS:
+            setattr(s, name, ptr_of(getattr(self, name)))
+        return s
+
+
+def decode_events(rows: np.ndarray):
+    """(kind, slot, idx) rows -> [("sweep", [(slot, idx)...]) | ("activate", slot, idx) |
+    ("deactivate", [slots])] (the encoding of tests/golden/make_golden.py)."""
+    out = []
+    cur = []
+    for kind, slot, idx in rows:
+        if kind == -1:
+            if cur:
+                k0 = cur[0][0]
+                if k0 == 0:
+                    out.append(("sweep", [(s, i) for _, s, i in cur]))
+                elif k0 == 1:
+                    out.append(("activate", cur[0][1], cur[0][2]))
+                else:
+                    out.append(("deactivate", [s for _, s, _ in cur]))
+            cur = []
+        else:
+            cur.append((int(kind), int(slot), int(idx)))
+    return out
+
+
+def unpack(h: dict, b: int) -> LseResult:
+    """Build the LseResult of problem b from host (numpy) copies."""
+    k = int(h["k_hat"][b])
+    nt = int(h["n_trace"][b])
+    ne = int(h["n_events"][b])
+    flags = int(h["flags"][b])
+    alpha = h["alpha"][b, :k, 0] + 1j * h["alpha"][b, :k, 1]
+    warns = []
+    if flags & FLAG_KMAX_CAP:
+        warns.append("activation loop hit the K_max cap")
+    if flags & FLAG_TRACE_FULL:
+        warns.append("objective trace truncated (trace capacity)")
+    if flags & FLAG_EVENTS_FULL:
+        warns.append("active-set history truncated (event capacity)")
+    secs = h["stage_seconds"][b]
+    times = {name: float(secs[i]) for i, name in enumerate(TIMER_NAMES)}
+    times["per_iteration"] = []
+    ctr = h["counters"][b]
+    stages = h["stage"][b, :nt]
+    return LseResult(
+        k_hat=k,
+        theta_hat=h["theta"][b, :k].copy(),
+        alpha_hat=alpha.reshape(1, k).astype(np.complex128),
+        beta_hat=float(h["beta"][b]),
+        gamma_hat=h["gamma"][b, :k].copy(),
+        zeta_hat=float(h["zeta"][b]),
+        objective_trace=h["trace"][b, :nt].copy(),
+        iterations=int(h["iterations"][b]),
+        wall_time_per_stage=times,
+        converged=bool(flags & FLAG_CONVERGED),
+        trace_stages=[STAGE_NAMES[int(s)] for s in stages],
+        warnings=warns,
+        events=decode_events(h["events"][b, :ne]),
+        trace_k=h["trace_k"][b, :nt].copy(),
+        slots=h["slot"][b, :k].copy(),
+        counters=dict(builds=int(ctr[0]), grids=int(ctr[1]), stats=int(ctr[2]), line_search_trials=int(ctr[3])),
+        status=int(h["status"][b]),
+    )
+
+
+# ------------------------------------------------------------------ GPU path
+def _torch():
+    import torch
+
+    return torch
+
+
+_TORCH_DT = {"i32": "int32", "f64": "float64", "i64": "int64"}
+
+
+class BatchSolver:
+    """Reusable device buffers + launch for B problems of length N.
+
+    ``solve(y_dev)`` launches on the current torch stream; inputs must be a
+    contiguous complex128 (B, N) CUDA tensor.  ``results()`` copies back and
+    unpacks.  No host synchronisation happens inside ``solve``."""
+
+    def __init__(self, n: int, batch: int, opts: EstimatorOptions = None, device=None):
+        torch = _torch()
+        self.opts = opts or EstimatorOptions()
+        _validate(self.opts)
+        if n < 2:
+            raise ValueError("need at least two observed samples")
+        self.lib = _native.load()
+        if not torch.cuda.is_available():
+            raise SuperLseError("no CUDA device: the superfast GPU path has no CPU fallback")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n, self.batch = n, batch
+        self.copts = c_options(self.opts, n)
+        self.kmax = self.copts.k_max
+        self.L = default_grid_size(n, self.opts.grid_factor)
+        with torch.cuda.device(self.device):
+            ws = self.lib.slse_estimate_workspace_bytes(n, batch, ctypes.byref(self.copts))
+            if ws == 0:
+                _native.check(-1, "slse_estimate_workspace_bytes")
+            self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
+
+            def empty(shape, dt):
+                return torch.empty(shape, dtype=getattr(torch, _TORCH_DT[dt]), device=self.device)
+
+            self.out = BatchOutputs(empty, batch, self.kmax, self.copts.trace_capacity, self.copts.event_capacity)
+        self.cout = self.out.struct(lambda t: t.data_ptr())
+
+    def solve(self, y_dev, stream=None):
+        torch = _torch()
+        if y_dev.dtype != torch.complex128 or not y_dev.is_contiguous() or tuple(y_dev.shape) != (self.batch, self.n):
+            raise DimensionMismatch(f"y must be a contiguous complex128 tensor of shape ({self.batch}, {self.n})")
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.slse_estimate_batch(
+            ctypes.c_void_p(y_dev.data_ptr()), self.n, self.batch, ctypes.byref(self.copts),
+            ctypes.byref(self.cout), ctypes.c_void_p(self.workspace.data_ptr()),
+            ctypes.c_size_t(self.workspace.numel()), ctypes.c_void_p(st.cuda_stream))
+        _native.check(rc, "slse_estimate_batch")
+
+    def host_outputs(self) -> dict:
+        return {name: getattr(self.out, name).cpu().numpy() for name in _native.OUTPUT_FIELDS}
+
+    def results(self):
+        h = self.host_outputs()
+        return [unpack(h, b) for b in range(self.batch)]
+
+
+def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False):
+    """Solve B independent complete-data problems, y: (B, N) complex.
+    Accepts numpy or torch input; returns a list of LseResult (problem
+    order).  Problems that hit a non-PD covariance carry ``status`` 1 instead
+    of raising."""
+    torch = _torch()
+    if isinstance(y, torch.Tensor):
+        yt = y
+    else:
+        yt = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(np.asarray(y, dtype=np.complex128))))
+    if yt.dim() != 2:
+        raise DimensionMismatch("y must have shape (B, N)")
+    solver = BatchSolver(int(yt.shape[1]), int(yt.shape[0]), opts, device=device)
+    ydev = yt.to(device=solver.device, dtype=torch.complex128).contiguous()
+    solver.solve(ydev)
+    res = solver.results()
+    return (res, solver) if return_solver else res
+
+
+def estimate(obs: Observation, opts: EstimatorOptions = None) -> LseResult:
+    """Fit the line-spectrum model (estimator.py:117-275) on the GPU."""
+    opts = opts if opts is not None else EstimatorOptions()
+    if obs.m < 2:
+        raise ValueError("need at least two observed samples")
+    _validate(opts)
+    if not obs.is_complete:
+        raise InvalidPattern("superfast backend requires the complete observation pattern")
+    if obs.g != 1:
+        raise NotImplementedError("multiple snapshots (G > 1) are outside this build's scope")
+    res = estimate_batch(obs.y, opts)[0]
+    if res.status == STATUS_NOT_PD:
+        raise NotPositiveDefinite("covariance lost positive definiteness during the fit")
+    if res.status == STATUS_BAD_DIAGONAL:
+        raise NotPositiveDefinite("diagonal entry c_0 must be real and positive")
+    return res
+
+
+def estimate_mmv(obs: Observation, opts: EstimatorOptions = None) -> LseResult:
+    """estimator.py:278-283 alias (G = 1 is the same code path)."""
+    return estimate(obs, opts)

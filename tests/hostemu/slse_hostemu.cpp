@@ -1,0 +1,103 @@
+// TEST-ONLY host emulation of the per-problem device program.
+//
+// Compiles the product's device headers (paper_1705_06073_b200/csrc/*.cuh)
+// with g++ -DSLSE_HOST_EMU, where a "block" is one serial thread.  It lets
+// the CPU test suite exercise the estimator state machine (sweeps,
+// activations, L-BFGS, deactivation, trace/event recording) against the
+// oracle without a GPU.  It is never loaded by the package: the product path
+// is the nvcc-built libsuperlse_b200.so and fails loudly without it.
+#define SLSE_HOST_EMU 1
+#include <cmath>
+#include <vector>
+
+#include "slse_solver.cuh"
+
+using namespace slse;
+
+static std::vector<cplx> make_twiddles(int lg) {
+  const int n = 1 << lg;
+  std::vector<cplx> tw(n);
+  for (int k = 0; k < n; ++k) {
+    double s, c;
+    sincos2pi((double)k / (double)n, &s, &c);
+    tw[k] = mk(c, -s);
+  }
+  return tw;
+}
+
+extern "C" int emu_estimate_batch(const double* y, int N, int B, const slse_options* opts, const slse_outputs* out) {
+  SolveParams P = make_params(N, *opts);
+  const int fmax = P.L > 2 * N ? P.L : 2 * N;
+  std::vector<cplx> tw = make_twiddles(ilog2(fmax));
+  CfTable cf;
+  cf_build(cf, N);
+  Layout lay = make_layout(N, P.L, P.kmax, P.lbfgs_mem, false);
+  std::vector<char> slab(lay.total + 256);
+  char* base = (char*)(((uintptr_t)slab.data() + 255) & ~(uintptr_t)255);
+  std::vector<double> red(2 * 32 * 16);
+  std::vector<cplx> region(fmax);
+  FftCtx f{tw.data(), ilog2(fmax), region.data(), fmax};
+  const size_t K = (size_t)P.kmax;
+  for (int p = 0; p < B; ++p) {
+    Blk b{0, 1, red.data(), 0};
+    ProbOut o;
+    o.khat = out->k_hat + p;
+    o.status = out->status + p;
+    o.iters = out->iterations + p;
+    o.flags = out->flags + p;
+    o.beta = out->beta + p;
+    o.zeta = out->zeta + p;
+    o.theta = out->theta + p * K;
+    o.gamma = out->gamma + p * K;
+    o.alpha = (cplx*)out->alpha + p * K;
+    o.slot = out->slot + p * K;
+    o.trace = out->trace + (size_t)p * P.tcap;
+    o.stage = out->stage + (size_t)p * P.tcap;
+    o.trace_k = out->trace_k + (size_t)p * P.tcap;
+    o.ntrace = out->n_trace + p;
+    o.events = out->events + (size_t)p * P.ecap * 3;
+    o.nevents = out->n_events + p;
+    o.counters = (long long*)out->counters + (size_t)p * 4;
+    o.stage_s = out->stage_seconds + (size_t)p * 6;
+    Solver S(b, P, &cf, (const cplx*)y + (size_t)p * N, o, base, lay, nullptr, f);
+    S.run();
+  }
+  return 0;
+}
+
+// per-call operators on host arrays (one problem)
+extern "C" int emu_bundle(const double* y, int N, const double* th, const double* ga, int k, double beta, int L,
+                          double* c, double* rho, double* w, double* scal /* logdet, delta_last, data_term */,
+                          double* qg, double* sg, double* st /* q r u t v (complex k each), s x (k each) */) {
+  const int fmax = L > 2 * N ? L : 2 * N;
+  std::vector<cplx> tw = make_twiddles(ilog2(fmax));
+  std::vector<cplx> region(fmax);
+  FftCtx f{tw.data(), ilog2(fmax), region.data(), fmax};
+  std::vector<double> red(2 * 32 * 16);
+  Blk b{0, 1, red.data(), 0};
+  std::vector<cplx> e(N), bg(N), a(N), yh(2 * N), P(2 * N), U(2 * N), V(2 * N), G1(L), G2(L);
+  std::vector<double> dt(N);
+  steer_forward((cplx*)c, N, th, ga, nullptr, k, beta, true, b);
+  Factor F = toeplitz_factor((const cplx*)c, N, e.data(), bg.data(), a.data(), nullptr, dt.data(), (cplx*)rho, b);
+  if (F.status) return F.status;
+  const cplx* yy = (const cplx*)y;
+  fft(yh.data(), 2 * N, -1.0, [&](int i) { return i < N ? yy[i] : mk(0, 0); }, [&](int i, cplx v) { yh[i] = v; }, f, b);
+  double quad = gs_apply((const cplx*)rho, N, F.delta_last, yy, yh.data(), P.data(), U.data(), V.data(), (cplx*)w, f, b);
+  scal[0] = F.logdet;
+  scal[1] = F.delta_last;
+  scal[2] = F.logdet + quad;
+  grid_eval((const cplx*)rho, (const cplx*)w, N, F.delta_last, L, (cplx*)qg, G1.data(), G2.data(), sg, f, b);
+  if (k) {
+    CfTable cf;
+    cf_build(cf, N);
+    cplx* q = (cplx*)st;
+    cplx* r = q + k;
+    cplx* u = r + k;
+    cplx* t = u + k;
+    cplx* v = t + k;
+    double* s = (double*)(v + k);
+    double* x = s + k;
+    component_stats(th, k, (const cplx*)rho, (const cplx*)w, N, F.delta_last, &cf, q, r, u, s, t, v, x, b);
+  }
+  return 0;
+}
