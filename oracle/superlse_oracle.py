@@ -401,6 +401,16 @@ def two_loop(mem, g):
     return -r_
 
 
+_MARGINS = None  # list receiving (kind, normalised margin) while estimate() runs
+
+
+def _margin(kind, lhs, rhs, scale):
+    """Record how far a decision lhs <= rhs (or lhs < rhs) was from flipping,
+    in units of `scale` (the decision's roundoff noise)."""
+    if _MARGINS is not None:
+        _MARGINS.append((kind, abs(lhs - rhs) / scale))
+
+
 def lbfgs_step(mem, point, f0, g0, objective_fn, gradient_fn):
     """lbfgs.py:100-136."""
     if not np.any(g0):
@@ -423,6 +433,7 @@ def lbfgs_step(mem, point, f0, g0, objective_fn, gradient_fn):
         cand = point + alpha * d
         cand[:k] = np.mod(cand[:k], 1.0)
         f_new = objective_fn(cand)
+        _margin("armijo", f_new, f0 + ARMIJO_C1 * alpha * slope, 1e-12 * max(1.0, abs(f0)))
         if f_new <= f0 + ARMIJO_C1 * alpha * slope:
             g_new = gradient_fn(cand)
             mem.push(alpha * d, g_new - g0)
@@ -626,6 +637,7 @@ class OracleResult:
     slots: np.ndarray
     builds: int = 0
     wall_time: float = 0.0
+    min_margin: float = float("inf")  # smallest decision margin in roundoff units
 
 
 def estimate(y, opts: OracleOptions = None) -> OracleResult:
@@ -633,8 +645,10 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
 
     `events` is the active-set history: ("sweep", [(slot, idx)...]),
     ("activate", slot, idx), ("deactivate", [slots]) in order."""
+    global _MARGINS
     t_start = time.perf_counter()
     opts = opts or OracleOptions()
+    _MARGINS = []
     y = np.asarray(y, dtype=np.complex128).ravel()
     n = m = y.size
     if m < 2:
@@ -701,6 +715,7 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
         else:
             value = energy / m
         cand.beta = max(floor, value)
+        _margin("beta", eng.objective(cand), trace[-1], 1e-12 * max(1.0, abs(trace[-1])))
         if eng.objective(cand) <= trace[-1]:
             st = cand
         record("beta")
@@ -741,9 +756,13 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
                     record("deactivate")
                     if st.k_hat == 0:
                         break
+                _margin("decrement", dec, m * opts.newton_decrement_tol_scale,
+                        1e-9 * m * opts.newton_decrement_tol_scale + 1e-12 * max(1.0, abs(trace[-1])))
                 if dec < m * opts.newton_decrement_tol_scale:
                     break
         current = trace[-1]
+        _margin("converge", abs(previous - current), m * opts.convergence_tol_scale,
+                1e-12 * max(1.0, abs(current)))
         if abs(previous - current) < m * opts.convergence_tol_scale:
             converged = True
             break
@@ -759,6 +778,7 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
         trace_stages=stages, trace_khat=khat, iterations=iterations, converged=converged,
         warnings=warns, events=events, slots=st.act.copy(), builds=eng.builds,
         wall_time=time.perf_counter() - t_start,
+        min_margin=min((mg for _, mg in _MARGINS), default=float("inf")),
     )
 
 

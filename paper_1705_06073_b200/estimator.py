@@ -253,7 +253,23 @@ class BatchSolver:
         _native.check(rc, "slse_estimate_batch")
 
     def host_outputs(self) -> dict:
-        return {name: getattr(self.out, name).cpu().numpy() for name in _native.OUTPUT_FIELDS}
+        """Host copies, trimmed to the longest trace / history / model order
+        in the batch (one small D2H for the counts, then the used prefixes)."""
+        torch = _torch()
+        small = ("k_hat", "status", "iterations", "flags", "beta", "zeta", "n_trace", "n_events", "counters",
+                 "stage_seconds")
+        h = {name: getattr(self.out, name).cpu().numpy() for name in small}
+        kk = max(1, int(h["k_hat"].max(initial=0)))
+        tt = max(1, int(h["n_trace"].max(initial=0)))
+        ee = max(1, int(h["n_events"].max(initial=0)))
+        o = self.out
+        big = {"theta": o.theta[:, :kk], "gamma": o.gamma[:, :kk], "alpha": o.alpha[:, :kk], "slot": o.slot[:, :kk],
+               "trace": o.trace[:, :tt], "stage": o.stage[:, :tt], "trace_k": o.trace_k[:, :tt],
+               "events": o.events[:, :ee]}
+        for name, t in big.items():
+            h[name] = t.contiguous().cpu().numpy()
+        del torch
+        return h
 
     def results(self):
         h = self.host_outputs()

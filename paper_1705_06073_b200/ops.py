@@ -1,0 +1,103 @@
+"""Per-call batched operators on CUDA tensors (the bundle pieces of
+model_core._SuperfastBundle, model_core.py:256-313), each one launch of an
+sm_100a kernel through the C ABI.  Complex arrays are complex128 tensors;
+every call runs on the current torch stream and does not synchronise.
+
+These are what the parity tests check call-by-call against the oracle; the
+estimator itself runs all of them fused inside the solver kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+from .errors import NotPositiveDefinite
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _c128(t):
+    assert t.dtype == torch.complex128 and t.is_cuda and t.is_contiguous()
+    return t
+
+
+def cov_column(theta, gamma, kcount, beta, n):
+    """Row 1: c[b] = beta[b] e_0 + sum_{k<kcount[b]} gamma[b,k] psi(theta[b,k])
+    (model_core.py:242-249).  theta/gamma: (B, K) float64; kcount: (B,) int32."""
+    lib = _native.load()
+    B, K = theta.shape
+    c = torch.empty((B, n), dtype=torch.complex128, device=theta.device)
+    _native.check(lib.slse_cov_column(_p(theta), _p(gamma), _p(kcount), K, _p(beta), n, B, _p(c), _stream()),
+                  "slse_cov_column")
+    return c
+
+
+def toeplitz_factor(c, with_delta=True, raise_on_error=False):
+    """Rows 2-4: (rho, delta, logdet, status) of the Hermitian Toeplitz
+    matrices with first columns c (B, N) (toeplitz.decompose, :263-276)."""
+    lib = _native.load()
+    _c128(c)
+    B, n = c.shape
+    rho = torch.empty_like(c)
+    delta = torch.empty((B, n), dtype=torch.float64, device=c.device) if with_delta else None
+    logdet = torch.empty(B, dtype=torch.float64, device=c.device)
+    status = torch.empty(B, dtype=torch.int32, device=c.device)
+    _native.check(lib.slse_toeplitz_factor(_p(c), n, B, _p(rho), _p(delta), _p(logdet), _p(status), _stream()),
+                  "slse_toeplitz_factor")
+    if raise_on_error and bool((status != 0).any()):
+        raise NotPositiveDefinite("Toeplitz factorisation hit a non-positive pivot")
+    return rho, delta, logdet, status
+
+
+def gs_apply(rho, delta_last, y):
+    """Row 5: (w = C^{-1} y, Re(y^H w)) (toeplitz.apply_inverse, :279-309)."""
+    lib = _native.load()
+    _c128(rho)
+    _c128(y)
+    B, n = rho.shape
+    w = torch.empty_like(rho)
+    quad = torch.empty(B, dtype=torch.float64, device=rho.device)
+    _native.check(lib.slse_gs_apply(_p(rho), _p(delta_last.contiguous()), _p(y), n, B, _p(w), _p(quad), _stream()),
+                  "slse_gs_apply")
+    return w, quad
+
+
+def component_stats(theta, kcount, rho, delta_last, w):
+    """Row 8: dict of q, r, u, t, v (complex) and s, x (real), each (B, K)
+    (model_core._SuperfastBundle.stats, :281-301)."""
+    lib = _native.load()
+    B, K = theta.shape
+    n = rho.shape[1]
+    dev = rho.device
+    cz = lambda: torch.zeros((B, K), dtype=torch.complex128, device=dev)  # noqa: E731
+    rz = lambda: torch.zeros((B, K), dtype=torch.float64, device=dev)  # noqa: E731
+    q, r, u, t, v = cz(), cz(), cz(), cz(), cz()
+    s, x = rz(), rz()
+    _native.check(lib.slse_component_stats(_p(theta), _p(kcount), K, _p(rho), _p(delta_last.contiguous()), _p(w), n,
+                                           B, _p(q), _p(r), _p(u), _p(s), _p(t), _p(v), _p(x), _stream()),
+                  "slse_component_stats")
+    return dict(q=q, r=r, u=u, s=s, t=t, v=v, x=x)
+
+
+def grid_eval(rho, delta_last, w, L, out=None):
+    """Row 9: (q_grid (B, L) complex, s_grid (B, L) real)
+    (model_core._SuperfastBundle.grid, :303-313)."""
+    lib = _native.load()
+    B, n = rho.shape
+    if out is None:
+        qg = torch.empty((B, L), dtype=torch.complex128, device=rho.device)
+        sg = torch.empty((B, L), dtype=torch.float64, device=rho.device)
+    else:
+        qg, sg = out
+    _native.check(lib.slse_grid_eval(_p(rho), _p(delta_last.contiguous()), _p(w), n, L, B, _p(qg), _p(sg),
+                                     _stream()), "slse_grid_eval")
+    return qg, sg
