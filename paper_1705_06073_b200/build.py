@@ -26,7 +26,7 @@ LIBPATH = os.path.join(LIBDIR, LIBNAME)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--extended-lambda", "-Xcompiler", "-fPIC",
                      "-I" + INCLUDE, "-I" + CSRC]
-SOLVE_NTS = (128, 256, 512, 1024)
+SOLVE_NTS = (32, 64, 128, 256, 512, 1024)
 
 
 def nvcc():

@@ -11,6 +11,8 @@
 //   tw_fill_kernel        twiddle table exp(-2 pi i k / TW).
 #include "slse_kernels.cuh"
 
+#include <cstdlib>
+
 thread_local char g_err[512] = "";
 
 using namespace slse_k;
@@ -97,13 +99,42 @@ cudaError_t set_smem(KernelT kernel, size_t bytes) {
 }  // namespace
 
 namespace {
+// host mirror of slse::stockham_ok (register caps per radix)
+bool stockham_fits(int count, int n, int nt) {
+  const int caps[4][2] = {{16, 1}, {8, 2}, {4, 4}, {2, 8}};
+  for (int Ns = 1; Ns < n;) {
+    int R = 0;
+    for (int q = 0; q < 4 && !R; ++q)
+      if (caps[q][0] <= n / Ns && count * (n / caps[q][0]) <= caps[q][1] * nt) R = caps[q][0];
+    if (!R) return false;
+    Ns *= R;
+  }
+  return true;
+}
+
+// threads per solver CTA: small N run one warp per problem (no block-wide
+// barriers; many problems resident per SM); SLSE_SOLVER_NT overrides.
+int solver_threads(int n) {
+  const char* env = getenv("SLSE_SOLVER_NT");
+  if (env) {
+    int v = atoi(env);
+    if (v == 32 || v == 64 || v == 128 || v == 256 || v == 512 || v == 1024) return v;
+  }
+  if (n <= 512) return 32;    // cfg1-2: measured 68 ms (32) vs 113 ms (256) per 4096 x N=256 batch
+  if (n <= 2048) return 256;  // cfg3: 167 ms (256) vs 205 (128) / 236 (512) per 1024 x N=1024
+  if (n <= 4096) return 512;  // cfg4: 1.44 s (512) vs 1.48 (1024) / 1.78 (256) per 256 x N=4096
+  return 1024;
+}
+
 int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
-  SmemPlan plan = smem_plan(n, P.L);
-  const int nt = block_threads(n);
+  const int nt = solver_threads(n);
+  SmemPlan plan = smem_plan(n, P.L, nt);
   int occ = 1;
   cudaError_t e = cudaSuccess;
   switch (nt) {
+    case 32: e = slse_solve_occupancy_32(plan.bytes, &occ); break;
+    case 64: e = slse_solve_occupancy_64(plan.bytes, &occ); break;
     case 128: e = slse_solve_occupancy_128(plan.bytes, &occ); break;
     case 256: e = slse_solve_occupancy_256(plan.bytes, &occ); break;
     case 512: e = slse_solve_occupancy_512(plan.bytes, &occ); break;
@@ -251,11 +282,27 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   int twlog;
   int rc = twiddles(ilog2(L), st, &tw, &twlog);
   if (rc) return rc;
+  cudaError_t e = cudaSuccess;
+  // register-Stockham path: 3 L-point transforms resident in shared memory
+  int snt = 64;
+  while (snt < 1024 && snt * 16 < 3 * L) snt *= 2;
+  const size_t ssmem = head_bytes(snt) + 48 * (size_t)L;
+  const bool stock = getenv("SLSE_GRID_DIT") == nullptr && ssmem <= 227 * 1024 && stockham_fits(3, L, snt);
+  if (stock) {
+    SLSE_DISPATCH_NT(snt, {
+      e = set_smem(grid_stockham_kernel<NTC>, ssmem);
+      if (e == cudaSuccess) {
+        grid_stockham_kernel<NTC><<<B, NTC, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, L,
+                                                        (cplx*)q_grid, s_grid, tw, twlog);
+        e = cudaGetLastError();
+      }
+    });
+    return e == cudaSuccess ? 0 : fail("grid_stockham_kernel", e);
+  }
   const int nt = block_threads(N);
   const int fused = 48 * (size_t)L <= kRegionBudget ? 1 : 0;
   const size_t smem = kHeadBytes + (fused ? 48 * (size_t)L : 0);
   cplx* scratch = nullptr;
-  cudaError_t e = cudaSuccess;
   if (!fused) {
     e = cudaMallocAsync(&scratch, sizeof(cplx) * 2 * (size_t)L * B, st);
     if (e != cudaSuccess) return fail("cudaMallocAsync", e);
@@ -311,10 +358,12 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
   cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(int), st);
   if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
   char* ws = (char*)workspace + 256;
-  const int nt = block_threads(N);
+  const int nt = solver_threads(N);
 #define SLSE_SOLVE_ARGS g, plan.bytes, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog, plan.fft_cap, \
                         plan.rec_in_smem
   switch (nt) {
+    case 32: e = slse_solve_launch_32(SLSE_SOLVE_ARGS); break;
+    case 64: e = slse_solve_launch_64(SLSE_SOLVE_ARGS); break;
     case 128: e = slse_solve_launch_128(SLSE_SOLVE_ARGS); break;
     case 256: e = slse_solve_launch_256(SLSE_SOLVE_ARGS); break;
     case 512: e = slse_solve_launch_512(SLSE_SOLVE_ARGS); break;

@@ -130,4 +130,170 @@ SLSE_NI void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b
   }
 }
 
+// ===========================================================================
+// Register-resident Stockham autosort FFT (radix 16/8/4/2 passes).
+//
+// Each pass: a thread loads R points of one sub-transform (stride n/R),
+// applies the pass twiddles W_{Ns R}^{(j mod Ns) r}, runs a radix-R DFT in
+// registers (compile-time constants, trivial rotations folded) and, after a
+// barrier, stores them to their autosorted positions -- in place, natural
+// order in and out, no bit reversal.  Requires that every pass's items fit
+// the block's registers (count * n / R <= MAXI(R) * nt).
+namespace fftc {
+// cos / sin of 2 pi k / 16, k = 0..4 (other octants by symmetry)
+constexpr double C16[5] = {1.0, 0.92387953251128673848, 0.70710678118654752440, 0.38268343236508978178, 0.0};
+SLSE_HD constexpr double cos16(int k) {  // cos(2 pi k / 16), k in [0, 16)
+  return k <= 4 ? C16[k] : (k <= 8 ? -C16[8 - k] : (k <= 12 ? -C16[k - 8] : C16[16 - k]));
+}
+SLSE_HD constexpr double sin16(int k) { return cos16((k + 12) & 15); }  // sin x = cos(x - pi/2)
+}  // namespace fftc
+
+// v <- v * exp(sign 2 pi i k / R) for compile-time k, R (R | 16)
+template <int K, int R>
+SLSE_D cplx rot_const(cplx v, double sign) {
+  constexpr int k16 = (K * 16 / R) & 15;
+  if constexpr (k16 == 0) {
+    return v;
+  } else if constexpr (k16 == 4) {  // exp(sign i pi/2) = sign * i
+    return sign < 0 ? mk(v.im, -v.re) : mk(-v.im, v.re);
+  } else if constexpr (k16 == 8) {
+    return mk(-v.re, -v.im);
+  } else if constexpr (k16 == 12) {
+    return sign < 0 ? mk(-v.im, v.re) : mk(v.im, -v.re);
+  } else {
+    constexpr double c = fftc::cos16(k16), s = fftc::sin16(k16);
+    const double ss = sign * s;
+    return mk(v.re * c - v.im * ss, v.re * ss + v.im * c);
+  }
+}
+
+template <int R, int S = 1, int O = 0>
+struct RegDft {
+  // in-place DFT of the R points v[O + S*i], i < R (radix-2 DIT recursion)
+  template <class V>
+  SLSE_D static void run(V& v, double sign) {
+    RegDft<R / 2, 2 * S, O>::run(v, sign);
+    RegDft<R / 2, 2 * S, O + S>::run(v, sign);
+    // combine: even part at O + 2S i, odd part at O + S + 2S i; outputs in
+    // natural order need a permutation: gather into temporaries
+    cplx t[R];
+    combine<0>(v, t, sign);
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[O + S * i] = t[i];
+  }
+  template <int K, class V>
+  SLSE_D static void combine(V& v, cplx* t, double sign) {
+    if constexpr (K < R / 2) {
+      const cplx e = v[O + 2 * S * K];
+      const cplx o = rot_const<K, R>(v[O + S + 2 * S * K], sign);
+      t[K] = cadd(e, o);
+      t[K + R / 2] = csub(e, o);
+      combine<K + 1>(v, t, sign);
+    }
+  }
+};
+template <int S, int O>
+struct RegDft<1, S, O> {
+  template <class V>
+  SLSE_D static void run(V&, double) {}
+};
+
+template <int R, int MAXI>
+SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const FftCtx& f, Blk& b) {
+  const int per = n / R;
+  const int total = count * per;
+  const int lg = ilog2(Ns * R);
+#ifdef SLSE_HOST_EMU
+  // serial emulation: hold every item of the pass (the device holds MAXI per thread)
+  std::vector<std::array<cplx, R>> vv(total);
+  for (int it = 0; it < total; ++it) {
+    const int c = it / per, j = it - c * per;
+    const cplx* xc = x + (size_t)c * n;
+    for (int r = 0; r < R; ++r) vv[it][r] = xc[j + r * per];
+    if (Ns > 1) {
+      const int kk = j & (Ns - 1);
+      for (int r = 1; r < R; ++r) vv[it][r] = cmul(vv[it][r], twid(f, kk * r, lg, sign));
+    }
+    RegDft<R>::run(vv[it], sign);
+  }
+  for (int it = 0; it < total; ++it) {
+    const int c = it / per, j = it - c * per;
+    cplx* xc = x + (size_t)c * n;
+    const int kk = j & (Ns - 1);
+    const int base = (j - kk) * R + kk;
+    for (int r = 0; r < R; ++r) xc[base + r * Ns] = vv[it][r];
+  }
+  (void)b;
+  return;
+#endif
+  cplx v[MAXI][R];
+#pragma unroll
+  for (int i = 0; i < MAXI; ++i) {
+    const int it = b.tid + i * b.nt;
+    if (it < total) {
+      const int c = it / per, j = it - c * per;
+      const cplx* xc = x + (size_t)c * n;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[i][r] = xc[j + r * per];
+      if (Ns > 1) {
+        const int kk = j & (Ns - 1);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twid(f, kk * r, lg, sign));
+      }
+      RegDft<R>::run(v[i], sign);
+    }
+  }
+  b.sync();
+#pragma unroll
+  for (int i = 0; i < MAXI; ++i) {
+    const int it = b.tid + i * b.nt;
+    if (it < total) {
+      const int c = it / per, j = it - c * per;
+      cplx* xc = x + (size_t)c * n;
+      const int kk = j & (Ns - 1);
+      const int base = (j - kk) * R + kk;
+#pragma unroll
+      for (int r = 0; r < R; ++r) xc[base + r * Ns] = v[i][r];
+    }
+  }
+  b.sync();
+}
+
+// radix for the pass with `rem` = n / Ns points per sub-transform left
+SLSE_D int stockham_radix(int rem, int count, int n, int nt) {
+#ifdef SLSE_HOST_EMU
+  nt = 1 << 24;  // no register cap in the serial emulation
+#endif
+  const int caps[4][2] = {{16, 1}, {8, 2}, {4, 4}, {2, 8}};
+  for (int q = 0; q < 4; ++q) {
+    const int R = caps[q][0];
+    if (R <= rem && count * (n / R) <= caps[q][1] * nt) return R;
+  }
+  return 0;
+}
+
+// true if the register Stockham applies to (count, n) with nt threads
+SLSE_D bool stockham_ok(int count, int n, int nt) {
+  for (int Ns = 1; Ns < n;) {
+    const int R = stockham_radix(n / Ns, count, n, nt);
+    if (R == 0) return false;
+    Ns *= R;
+  }
+  return true;
+}
+
+// in-place forward/backward transform of `count` contiguous buffers of n
+SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& f, Blk& b) {
+  for (int Ns = 1; Ns < n;) {
+    const int R = stockham_radix(n / Ns, count, n, b.nt);
+    switch (R) {
+      case 16: stockham_pass<16, 1>(x, count, n, Ns, sign, f, b); break;
+      case 8: stockham_pass<8, 2>(x, count, n, Ns, sign, f, b); break;
+      case 4: stockham_pass<4, 4>(x, count, n, Ns, sign, f, b); break;
+      default: stockham_pass<2, 8>(x, count, n, Ns, sign, f, b); break;
+    }
+    Ns *= R;
+  }
+}
+
 }  // namespace slse

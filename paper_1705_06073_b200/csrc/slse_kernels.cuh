@@ -16,9 +16,12 @@ using namespace slse;
 namespace slse_k {
 
 // ---------------------------------------------------------- configuration
-constexpr size_t kRedBytes = 2 * 32 * 16 * sizeof(double);  // Blk::red
-constexpr size_t kCfBytes = sizeof(CfTable);
-constexpr size_t kHeadBytes = kRedBytes + ((kCfBytes + 255) & ~(size_t)255);
+// shared-memory head: Blk reduction scratch (2 banks x nwarps x 16 doubles)
+// followed by the cf table; the FFT / recursion region starts at head_bytes
+SLSE_HD constexpr size_t red_bytes(int nt) { return (2 * ((nt + 31) / 32) * 16 * sizeof(double) + 255) & ~(size_t)255; }
+SLSE_HD constexpr size_t head_bytes(int nt) { return red_bytes(nt) + ((sizeof(CfTable) + 255) & ~(size_t)255); }
+constexpr size_t kRedBytes = red_bytes(1024);
+constexpr size_t kHeadBytes = head_bytes(1024);
 constexpr size_t kRegionBudget = 200 * 1024;
 
 inline int block_threads(int n) {
@@ -34,7 +37,7 @@ struct SmemPlan {
   size_t bytes;
 };
 
-inline SmemPlan smem_plan(int n, int L) {
+inline SmemPlan smem_plan(int n, int L, int nt) {
   SmemPlan p;
   const size_t rec = 48 * (size_t)n;
   p.rec_in_smem = rec <= kRegionBudget ? 1 : 0;
@@ -50,7 +53,7 @@ inline SmemPlan smem_plan(int n, int L) {
   }
   size_t region = 16 * (size_t)p.fft_cap;
   if (p.rec_in_smem && rec > region) region = rec;
-  p.bytes = kHeadBytes + region;
+  p.bytes = head_bytes(nt) + region;
   return p;
 }
 
@@ -67,8 +70,8 @@ __global__ void __launch_bounds__(NT) solve_kernel(SolveParams P, CfTable cft, c
                                                    int rec_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* red = (double*)smem_raw;
-  CfTable* cf = (CfTable*)(smem_raw + kRedBytes);
-  cplx* region = (cplx*)(smem_raw + kHeadBytes);
+  CfTable* cf = (CfTable*)(smem_raw + red_bytes(NT));
+  cplx* region = (cplx*)(smem_raw + head_bytes(NT));
   __shared__ int s_prob;
   if (threadIdx.x == 0) *cf = cft;
   Blk b;
@@ -228,6 +231,43 @@ __global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, 
 }
 
 
+
+// Row 9 standalone, register-Stockham variant: the three length-L transforms
+// (w, rho, n*rho; zero padded) live in shared memory, run as radix-16/4
+// passes over all three at once, and the combine writes q^G and s^G once.
+template <int NT>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_stockham_kernel(const cplx* __restrict__ rho,
+                                                           const double* __restrict__ delta_last,
+                                                           const cplx* __restrict__ w, int n, int L,
+                                                           cplx* __restrict__ q_grid, double* __restrict__ s_grid,
+                                                           const cplx* tw, int twlog) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  const cplx* rp = rho + (size_t)p * n;
+  const cplx* wp = w + (size_t)p * n;
+  cplx* X = (cplx*)(smem_raw + head_bytes(NT));
+  for (int i = threadIdx.x; i < L; i += NT) {
+    cplx a = mk(0.0, 0.0), rr = mk(0.0, 0.0);
+    if (i < n) { a = wp[i]; rr = rp[i]; }
+    X[i] = a;
+    X[L + i] = rr;
+    X[2 * L + i] = cscale(rr, (double)i);
+  }
+  __syncthreads();
+  FftCtx f{tw, twlog, nullptr, 0};
+  fft_stockham(X, 3, L, -1.0, f, b);
+  const double inv_d = 1.0 / delta_last[p];
+  const double c2n = 2.0 - (double)n;
+  cplx* qg = q_grid + (size_t)p * L;
+  double* sgp = s_grid + (size_t)p * L;
+  for (int l = threadIdx.x; l < L; l += NT) {
+    const cplx a0 = X[L + l], a1 = X[2 * L + l];
+    qg[l] = X[l];
+    sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+  }
+}
+
 }  // namespace slse_k
 
 // per-NT solver entry points (slse_solve_inst.cu)
@@ -237,6 +277,8 @@ __global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, 
                                      const slse::CfTable& cft, const slse::cplx* ys, int B,            \
                                      const slse_outputs& out, char* ws, size_t slab, int* queue,       \
                                      const slse::cplx* tw, int twlog, int fft_cap, int rec_smem);
+SLSE_DECL_SOLVE(32)
+SLSE_DECL_SOLVE(64)
 SLSE_DECL_SOLVE(128)
 SLSE_DECL_SOLVE(256)
 SLSE_DECL_SOLVE(512)

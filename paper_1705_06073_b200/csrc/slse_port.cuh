@@ -12,7 +12,9 @@
 
 #ifdef SLSE_HOST_EMU
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <vector>
 #include <cstring>
 #define SLSE_D inline
 #define SLSE_NI inline
@@ -93,7 +95,7 @@ using std::sqrt; using std::isnan;
 struct Blk {
   int tid;
   int nt;
-  double* red;  // shared scratch: 2 banks x 32 warps x 16 doubles
+  double* red;  // shared scratch: 2 banks x nwarps x 16 doubles
   int bank;     // alternates so one barrier per reduction suffices
 
   SLSE_D void sync() {
@@ -129,7 +131,7 @@ struct Blk {
         v[i] = x;
       }
     }
-    double* r = red + bank * (32 * 16);
+    double* r = red + bank * (nwarps() * 16);
     if (lane == 0) {
       for (int i = 0; i < k; ++i) r[w * 16 + i] = v[i];
     }
@@ -149,7 +151,7 @@ struct Blk {
     const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
-    double* r = red + bank * (32 * 16);
+    double* r = red + bank * (nwarps() * 16);
     if (lane == 0) r[w * 16] = x;
     __syncthreads();
     double acc = r[0];
@@ -166,7 +168,7 @@ struct Blk {
       int oi = __shfl_xor_sync(0xffffffffu, idx, o);
       if (better(ov, oi, v, idx)) { v = ov; idx = oi; }
     }
-    double* r = red + bank * (32 * 16);
+    double* r = red + bank * (nwarps() * 16);
     if (lane == 0) { r[w * 16] = v; r[w * 16 + 1] = (double)idx; }
     __syncthreads();
     v = r[0]; idx = (int)r[1];
@@ -177,7 +179,7 @@ struct Blk {
     bank ^= 1;
   }
   SLSE_D int bcast_i(int x) {  // value of thread 0
-    double* r = red + bank * (32 * 16);
+    double* r = red + bank * (nwarps() * 16);
     if (tid == 0) r[0] = (double)x;
     __syncthreads();
     int out = (int)r[0];
@@ -185,7 +187,7 @@ struct Blk {
     return out;
   }
   SLSE_D double bcast_d(double x) {
-    double* r = red + bank * (32 * 16);
+    double* r = red + bank * (nwarps() * 16);
     if (tid == 0) r[0] = x;
     __syncthreads();
     double out = r[0];
@@ -201,7 +203,7 @@ struct Blk {
       int y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += y;
     }
-    double* r = red + bank * (32 * 16);
+    double* r = red + bank * (nwarps() * 16);
     if (lane == 31) r[w * 16] = (double)inc;
     __syncthreads();
     int before = 0, tot = 0;

@@ -112,10 +112,28 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
   b.sync();
   double delta = c0;
   int fail = 0;
+  // Reflection coefficient of step 0.  Every step uses one reciprocal of
+  // delta (instead of two divisions); a single-warp block also computes the
+  // NEXT coefficient from the pre-update values e_{m+2}, B_1 before its bulk
+  // update (lookahead), taking the reciprocal off the critical path.
+  const bool look = b.nt <= 32;
+  cplx k = mk(0.0, 0.0);
+  if (n > 1) {
+    const cplx e1 = e[1];
+    const double inv = 1.0 / delta;
+    k = mk(-e1.re * inv, -e1.im * inv);
+  }
   for (int m = 0; m + 1 < n; ++m) {
-    const cplx em = e[m + 1];
-    const cplx k = mk(-em.re / delta, -em.im / delta);
     const cplx kc = conjg(k);
+    const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
+    cplx knext = mk(0.0, 0.0);
+    if (look && m + 2 < n) {
+      const cplx e2 = e[m + 2], b1 = B[1];
+      const cplx emn = cadd(e2, cmul(k, b1));
+      const double invn = 1.0 / dnext;
+      knext = mk(-emn.re * invn, -emn.im * invn);
+      b.sync();  // every lane has read e_{m+2}, B_1 before any write below
+    }
     const int cnt = n - 1 - m;  // pairs j = 0..cnt-1
     for (int j = b.tid; j < cnt; j += b.nt) {
       const cplx ej = e[j + m + 1];
@@ -125,10 +143,9 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
     }
     // predictor: a_i' = a_i + k conj(a_{m+1-i}), i = 1..m+1 (a_{m+1} = 0 before)
     const int top = m + 1;
-    const int npair = (top + 1) / 2;  // i = 1..npair pairs with top-i (i <= top-i or middle)
+    const int npair = (top + 1) / 2;
     for (int i = b.tid; i <= npair; i += b.nt) {
       if (i == 0) {
-        // a_{top} = 0 + k * conj(a_0)
         a[top] = cmul(k, conjg(a[0]));
       } else {
         const int jj = top - i;
@@ -142,10 +159,19 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
         }
       }
     }
-    delta = delta * (1.0 - (k.re * k.re + k.im * k.im));
-    if (b.tid == 0) delta_tmp[m + 1] = delta;
+    if (b.tid == 0) delta_tmp[m + 1] = dnext;
     b.sync();
+    delta = dnext;
     if (!(delta > floor_)) { fail = 1; break; }
+    if (m + 2 < n) {
+      if (look) {
+        k = knext;
+      } else {
+        const cplx em = e[m + 2];
+        const double inv = 1.0 / delta;
+        k = mk(-em.re * inv, -em.im * inv);
+      }
+    }
   }
   if (fail) {
     F.status = kNotPD;

@@ -101,3 +101,26 @@ extern "C" int emu_bundle(const double* y, int N, const double* th, const double
   }
   return 0;
 }
+
+// Stockham register FFT (count buffers of n, in place)
+extern "C" int emu_fft_stockham(double* x, int count, int n, int sign) {
+  const int lg = ilog2(n) > 4 ? ilog2(n) : 4;
+  std::vector<cplx> tw = make_twiddles(lg);
+  std::vector<double> red(64);
+  Blk b{0, 1, red.data(), 0};
+  FftCtx f{tw.data(), lg, nullptr, 0};
+  fft_stockham((cplx*)x, count, n, (double)sign, f, b);
+  return 0;
+}
+
+// radix-4 DIT reference path
+extern "C" int emu_fft_dit(double* x, int n, int sign) {
+  const int lg = ilog2(n) > 4 ? ilog2(n) : 4;
+  std::vector<cplx> tw = make_twiddles(lg);
+  std::vector<double> red(64);
+  std::vector<cplx> sm(n);
+  Blk b{0, 1, red.data(), 0};
+  FftCtx f{tw.data(), lg, sm.data(), n};
+  fft_inplace((cplx*)x, n, (double)sign, f, b);
+  return 0;
+}
