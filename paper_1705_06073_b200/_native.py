@@ -12,7 +12,8 @@ import os
 
 from .errors import SuperLseError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsuperlse_b200.so")
+_LIB_PATH = os.environ.get("SLSE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                     "libsuperlse_b200.so")
 ABI_VERSION = 1
 
 c_int_p = ctypes.POINTER(ctypes.c_int32)

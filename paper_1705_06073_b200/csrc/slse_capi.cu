@@ -85,6 +85,8 @@ int sm_count() {
 
 #define SLSE_DISPATCH_NT(nt, ...) \
   switch (nt) {                    \
+    case 32: { constexpr int NTC = 32; __VA_ARGS__; } break; \
+    case 64: { constexpr int NTC = 64; __VA_ARGS__; } break; \
     case 128: { constexpr int NTC = 128; __VA_ARGS__; } break; \
     case 256: { constexpr int NTC = 256; __VA_ARGS__; } break; \
     case 512: { constexpr int NTC = 512; __VA_ARGS__; } break; \
@@ -286,7 +288,7 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   // register-Stockham path: 3 L-point transforms resident in shared memory
   int snt = 64;
   while (snt < 1024 && snt * 16 < 3 * L) snt *= 2;
-  const size_t ssmem = head_bytes(snt) + 48 * (size_t)L;
+  const size_t ssmem = head_bytes(snt) + 48 * (size_t)sk_len(L);
   const bool stock = getenv("SLSE_GRID_DIT") == nullptr && ssmem <= 227 * 1024 && stockham_fits(3, L, snt);
   if (stock) {
     SLSE_DISPATCH_NT(snt, {

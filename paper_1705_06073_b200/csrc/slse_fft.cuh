@@ -95,7 +95,7 @@ SLSE_NI void fft_passes(cplx* x, int n, double sign, const FftCtx& f, Blk& b) {
 // only at its own index i.  sign -1: numpy fft
 // convention; sign +1: unscaled inverse (caller applies 1/n).
 template <class Load, class Store>
-SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
+SLSE_D void fft_dit(cplx* work, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
   const int p = ilog2(n);
   cplx* x = (n <= f.smem_cap) ? f.smem : work;
   for (int i = b.tid; i < n; i += b.nt) x[brev_bits((unsigned)i, p)] = ld(i);
@@ -107,7 +107,7 @@ SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx&
 
 // In-place transform of data[0..n) (global).  Post-processing is the
 // caller's business (one more loop).
-SLSE_NI void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {
+SLSE_NI void fft_inplace_dit(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {
   const int p = ilog2(n);
   if (n <= f.smem_cap) {
     cplx* x = f.smem;
@@ -198,6 +198,11 @@ struct RegDft<1, S, O> {
   SLSE_D static void run(V&, double) {}
 };
 
+// shared-memory skew: one pad slot per 16 points, so the stride-R stores of
+// a pass (and stride-16 anything) spread over all banks
+SLSE_HD int sk(int i) { return i + (i >> 4); }
+SLSE_HD int sk_len(int n) { return n + (n >> 4); }
+
 template <int R, int MAXI>
 SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const FftCtx& f, Blk& b) {
   const int per = n / R;
@@ -208,8 +213,8 @@ SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const 
   std::vector<std::array<cplx, R>> vv(total);
   for (int it = 0; it < total; ++it) {
     const int c = it / per, j = it - c * per;
-    const cplx* xc = x + (size_t)c * n;
-    for (int r = 0; r < R; ++r) vv[it][r] = xc[j + r * per];
+    const cplx* xc = x + (size_t)c * sk_len(n);
+    for (int r = 0; r < R; ++r) vv[it][r] = xc[sk(j + r * per)];
     if (Ns > 1) {
       const int kk = j & (Ns - 1);
       for (int r = 1; r < R; ++r) vv[it][r] = cmul(vv[it][r], twid(f, kk * r, lg, sign));
@@ -218,10 +223,10 @@ SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const 
   }
   for (int it = 0; it < total; ++it) {
     const int c = it / per, j = it - c * per;
-    cplx* xc = x + (size_t)c * n;
+    cplx* xc = x + (size_t)c * sk_len(n);
     const int kk = j & (Ns - 1);
     const int base = (j - kk) * R + kk;
-    for (int r = 0; r < R; ++r) xc[base + r * Ns] = vv[it][r];
+    for (int r = 0; r < R; ++r) xc[sk(base + r * Ns)] = vv[it][r];
   }
   (void)b;
   return;
@@ -232,9 +237,9 @@ SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const 
     const int it = b.tid + i * b.nt;
     if (it < total) {
       const int c = it / per, j = it - c * per;
-      const cplx* xc = x + (size_t)c * n;
+      const cplx* xc = x + (size_t)c * sk_len(n);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[i][r] = xc[j + r * per];
+      for (int r = 0; r < R; ++r) v[i][r] = xc[sk(j + r * per)];
       if (Ns > 1) {
         const int kk = j & (Ns - 1);
 #pragma unroll
@@ -249,11 +254,11 @@ SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const 
     const int it = b.tid + i * b.nt;
     if (it < total) {
       const int c = it / per, j = it - c * per;
-      cplx* xc = x + (size_t)c * n;
+      cplx* xc = x + (size_t)c * sk_len(n);
       const int kk = j & (Ns - 1);
       const int base = (j - kk) * R + kk;
 #pragma unroll
-      for (int r = 0; r < R; ++r) xc[base + r * Ns] = v[i][r];
+      for (int r = 0; r < R; ++r) xc[sk(base + r * Ns)] = v[i][r];
     }
   }
   b.sync();
@@ -282,7 +287,8 @@ SLSE_D bool stockham_ok(int count, int n, int nt) {
   return true;
 }
 
-// in-place forward/backward transform of `count` contiguous buffers of n
+// in-place forward/backward transform of `count` buffers of n points held
+// in the skewed layout (buffer c at x + c * sk_len(n), point i at sk(i))
 SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& f, Blk& b) {
   for (int Ns = 1; Ns < n;) {
     const int R = stockham_radix(n / Ns, count, n, b.nt);
@@ -293,6 +299,37 @@ SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& 
       default: stockham_pass<2, 8>(x, count, n, Ns, sign, f, b); break;
     }
     Ns *= R;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Dispatch: the register Stockham when the transform fits the shared
+// staging area and the block's register caps, else radix-4 DIT.
+template <class Load, class Store>
+SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
+  if (sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
+    cplx* x = f.smem;
+    for (int i = b.tid; i < n; i += b.nt) x[sk(i)] = ld(i);
+    b.sync();
+    fft_stockham(x, 1, n, sign, f, b);
+    for (int i = b.tid; i < n; i += b.nt) st(i, x[sk(i)]);
+    b.sync();
+  } else {
+    fft_dit(work, n, sign, ld, st, f, b);
+  }
+}
+
+SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {
+  if (sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
+    cplx* x = f.smem;
+    for (int i = b.tid; i < n; i += b.nt) x[sk(i)] = data[i];
+    b.sync();
+    fft_stockham(x, 1, n, sign, f, b);
+    for (int i = b.tid; i < n; i += b.nt) data[i] = x[sk(i)];
+    b.sync();
+  } else {
+    fft_inplace_dit(data, n, sign, f, b);
   }
 }
 

@@ -7,11 +7,18 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 
 #include "superlse_b200.h"
 #include "slse_solver.cuh"
 
 using namespace slse;
+
+// min resident CTAs per SM for the one-warp solver (caps registers)
+#ifndef SLSE_SOLVER_MINB32
+#define SLSE_SOLVER_MINB32 16
+#endif
+
 
 namespace slse_k {
 
@@ -39,18 +46,29 @@ struct SmemPlan {
 
 inline SmemPlan smem_plan(int n, int L, int nt) {
   SmemPlan p;
+  // one-warp solvers: keep the region small so more problems stay resident
+  // (only the recursion and the 2N-point transforms are staged; the grid's
+  // L-point transforms then run from L1/L2)
+  size_t budget = kRegionBudget;
+  if (nt <= 32) {
+    const char* env = getenv("SLSE_WARP_REGION_KB");
+    budget = env ? (size_t)atoi(env) * 1024 : 48 * (size_t)n;
+    if (budget < 48 * (size_t)n) budget = 48 * (size_t)n;
+  }
   const size_t rec = 48 * (size_t)n;
-  p.rec_in_smem = rec <= kRegionBudget ? 1 : 0;
+  p.rec_in_smem = rec <= budget ? 1 : 0;
   const int fftmax = L > 2 * n ? L : (1 << ilog2(2 * n));
   size_t cap_bytes = p.rec_in_smem ? rec : 0;
-  if (16 * (size_t)fftmax <= kRegionBudget) {
-    p.fft_cap = fftmax;
+  // staging capacity in complex elements: the largest power-of-two transform
+  // that fits, in the skewed layout (sk_len)
+  int F = 1;
+  if (16 * (size_t)sk_len(fftmax) <= budget) {
+    F = fftmax;
   } else {
-    int F = 1;
-    const size_t lim = cap_bytes > 0 ? cap_bytes : kRegionBudget;
-    while (16 * (size_t)(F * 2) <= lim) F *= 2;
-    p.fft_cap = F;
+    const size_t lim = cap_bytes > 0 ? cap_bytes : budget;
+    while (16 * (size_t)sk_len(F * 2) <= lim) F *= 2;
   }
+  p.fft_cap = sk_len(F);
   size_t region = 16 * (size_t)p.fft_cap;
   if (p.rec_in_smem && rec > region) region = rec;
   p.bytes = head_bytes(nt) + region;
@@ -64,7 +82,7 @@ struct OutPtrs {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(NT) solve_kernel(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
+__global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve_kernel(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
                                                    int B, slse_outputs out, char* ws, size_t slab_bytes,
                                                    int* queue, const cplx* tw, int twlog, int fft_cap,
                                                    int rec_smem) {
@@ -236,7 +254,7 @@ __global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, 
 // (w, rho, n*rho; zero padded) live in shared memory, run as radix-16/4
 // passes over all three at once, and the combine writes q^G and s^G once.
 template <int NT>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_stockham_kernel(const cplx* __restrict__ rho,
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 4 : 1)) grid_stockham_kernel(const cplx* __restrict__ rho,
                                                            const double* __restrict__ delta_last,
                                                            const cplx* __restrict__ w, int n, int L,
                                                            cplx* __restrict__ q_grid, double* __restrict__ s_grid,
@@ -247,12 +265,14 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_stockham_kernel(
   const cplx* rp = rho + (size_t)p * n;
   const cplx* wp = w + (size_t)p * n;
   cplx* X = (cplx*)(smem_raw + head_bytes(NT));
+  const int LS = sk_len(L);
   for (int i = threadIdx.x; i < L; i += NT) {
     cplx a = mk(0.0, 0.0), rr = mk(0.0, 0.0);
     if (i < n) { a = wp[i]; rr = rp[i]; }
-    X[i] = a;
-    X[L + i] = rr;
-    X[2 * L + i] = cscale(rr, (double)i);
+    const int si = sk(i);
+    X[si] = a;
+    X[LS + si] = rr;
+    X[2 * LS + si] = cscale(rr, (double)i);
   }
   __syncthreads();
   FftCtx f{tw, twlog, nullptr, 0};
@@ -262,8 +282,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_stockham_kernel(
   cplx* qg = q_grid + (size_t)p * L;
   double* sgp = s_grid + (size_t)p * L;
   for (int l = threadIdx.x; l < L; l += NT) {
-    const cplx a0 = X[L + l], a1 = X[2 * L + l];
-    qg[l] = X[l];
+    const int sl = sk(l);
+    const cplx a0 = X[LS + sl], a1 = X[2 * LS + sl];
+    qg[l] = X[sl];
     sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
   }
 }

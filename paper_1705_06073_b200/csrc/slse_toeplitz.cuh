@@ -85,9 +85,10 @@ struct Factor {
   int status;
 };
 
-SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
-                              double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho,
-                              Blk& b) {
+template <bool SH>
+SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
+                                   double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho,
+                                   Blk& b) {
   Factor F;
   F.logdet = 0.0;
   F.status = kOk;
@@ -101,6 +102,13 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
   }
   const double c0 = c0c.re;
   const double floor_ = kPdEps * c0;
+#ifndef SLSE_HOST_EMU
+  if (SH) {  // work arrays in shared memory: let the compiler emit LDS/STS
+    __builtin_assume(__isShared(e));
+    __builtin_assume(__isShared(B));
+    __builtin_assume(__isShared(a));
+  }
+#endif
   for (int j = b.tid; j < n; j += b.nt) {
     cplx cj = (j == 0) ? mk(c0, 0.0) : c[j];
     e[j] = cj;
@@ -186,6 +194,14 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
   }
   F.logdet = b.sum(part);
   return F;
+}
+
+SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
+                              double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
+#ifndef SLSE_HOST_EMU
+  if (__isShared(e)) return toeplitz_factor_impl<true>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
+#endif
+  return toeplitz_factor_impl<false>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
 }
 
 // ---------------------------------------------------------------------------

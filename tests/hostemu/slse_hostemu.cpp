@@ -109,7 +109,13 @@ extern "C" int emu_fft_stockham(double* x, int count, int n, int sign) {
   std::vector<double> red(64);
   Blk b{0, 1, red.data(), 0};
   FftCtx f{tw.data(), lg, nullptr, 0};
-  fft_stockham((cplx*)x, count, n, (double)sign, f, b);
+  std::vector<cplx> sx((size_t)count * sk_len(n));
+  cplx* xx = (cplx*)x;
+  for (int c = 0; c < count; ++c)
+    for (int i = 0; i < n; ++i) sx[(size_t)c * sk_len(n) + sk(i)] = xx[(size_t)c * n + i];
+  fft_stockham(sx.data(), count, n, (double)sign, f, b);
+  for (int c = 0; c < count; ++c)
+    for (int i = 0; i < n; ++i) xx[(size_t)c * n + i] = sx[(size_t)c * sk_len(n) + sk(i)];
   return 0;
 }
 
