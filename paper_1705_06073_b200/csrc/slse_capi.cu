@@ -285,21 +285,32 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   int rc = twiddles(ilog2(L), st, &tw, &twlog);
   if (rc) return rc;
   cudaError_t e = cudaSuccess;
-  // register-Stockham path: 3 L-point transforms resident in shared memory
-  int snt = 64;
-  while (snt < 1024 && snt * 16 < 3 * L) snt *= 2;
-  const size_t ssmem = head_bytes(snt) + 48 * (size_t)sk_len(L);
-  const bool stock = getenv("SLSE_GRID_DIT") == nullptr && ssmem <= 227 * 1024 && stockham_fits(3, L, snt);
-  if (stock) {
-    SLSE_DISPATCH_NT(snt, {
-      e = set_smem(grid_stockham_kernel<NTC>, ssmem);
-      if (e == cudaSuccess) {
-        grid_stockham_kernel<NTC><<<B, NTC, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, L,
-                                                        (cplx*)q_grid, s_grid, tw, twlog);
-        e = cudaGetLastError();
-      }
-    });
-    return e == cudaSuccess ? 0 : fail("grid_stockham_kernel", e);
+  // register-Stockham path: 3 L-point transforms resident in shared memory,
+  // compile-time pass schedules for L = 2^6 .. 2^12
+  if (getenv("SLSE_GRID_DIT") == nullptr) {
+    const int lg = ilog2(L);
+#define SLSE_GRID_CASE(LGV, NTV)                                                                          \
+  case LGV: {                                                                                              \
+    const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(L);                                         \
+    e = set_smem(grid_stockham_kernel<NTV, LGV>, ssmem);                                                    \
+    if (e == cudaSuccess) {                                                                                \
+      grid_stockham_kernel<NTV, LGV><<<B, NTV, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, L, \
+                                                           (cplx*)q_grid, s_grid, tw, twlog);             \
+      e = cudaGetLastError();                                                                              \
+    }                                                                                                      \
+    return e == cudaSuccess ? 0 : fail("grid_stockham_kernel", e);                                         \
+  }
+    switch (lg) {
+      SLSE_GRID_CASE(6, 64)
+      SLSE_GRID_CASE(7, 64)
+      SLSE_GRID_CASE(8, 64)
+      SLSE_GRID_CASE(9, 128)
+      SLSE_GRID_CASE(10, 256)
+      SLSE_GRID_CASE(11, 512)
+      SLSE_GRID_CASE(12, 1024)
+      default: break;
+    }
+#undef SLSE_GRID_CASE
   }
   const int nt = block_threads(N);
   const int fused = 48 * (size_t)L <= kRegionBudget ? 1 : 0;

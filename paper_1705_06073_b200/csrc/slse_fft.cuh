@@ -43,7 +43,13 @@ SLSE_D unsigned brev_bits(unsigned i, int p) {
 #endif
 }
 
-// twiddle exp(sign * 2 pi i k / 2^lg)
+// twiddle exp(sign * 2 pi i k / 2^lg) from a table of 2^twlog entries
+SLSE_D cplx twid_tab(const cplx* __restrict__ tw, int twlog, int k, int lg, double sign) {
+  cplx t = tw[(size_t)k << (twlog - lg)];
+  if (sign > 0) t.im = -t.im;
+  return t;
+}
+
 SLSE_D cplx twid(const FftCtx& f, int k, int lg, double sign) {
   cplx t = f.tw[(size_t)k << (f.twlog - lg)];
   if (sign > 0) t.im = -t.im;
@@ -141,70 +147,77 @@ SLSE_NI void fft_inplace_dit(cplx* data, int n, double sign, const FftCtx& f, Bl
 // the block's registers (count * n / R <= MAXI(R) * nt).
 namespace fftc {
 // cos / sin of 2 pi k / 16, k = 0..4 (other octants by symmetry)
-constexpr double C16[5] = {1.0, 0.92387953251128673848, 0.70710678118654752440, 0.38268343236508978178, 0.0};
+SLSE_HD constexpr double c16q(int k) {  // cos(2 pi k / 16), k in [0, 4]
+  return k == 0 ? 1.0
+                : (k == 1 ? 0.92387953251128673848
+                          : (k == 2 ? 0.70710678118654752440 : (k == 3 ? 0.38268343236508978178 : 0.0)));
+}
 SLSE_HD constexpr double cos16(int k) {  // cos(2 pi k / 16), k in [0, 16)
-  return k <= 4 ? C16[k] : (k <= 8 ? -C16[8 - k] : (k <= 12 ? -C16[k - 8] : C16[16 - k]));
+  return k <= 4 ? c16q(k) : (k <= 8 ? -c16q(8 - k) : (k <= 12 ? -c16q(k - 8) : c16q(16 - k)));
 }
 SLSE_HD constexpr double sin16(int k) { return cos16((k + 12) & 15); }  // sin x = cos(x - pi/2)
 }  // namespace fftc
 
-// v <- v * exp(sign 2 pi i k / R) for compile-time k, R (R | 16)
-template <int K, int R>
-SLSE_D cplx rot_const(cplx v, double sign) {
-  constexpr int k16 = (K * 16 / R) & 15;
-  if constexpr (k16 == 0) {
-    return v;
-  } else if constexpr (k16 == 4) {  // exp(sign i pi/2) = sign * i
-    return sign < 0 ? mk(v.im, -v.re) : mk(-v.im, v.re);
-  } else if constexpr (k16 == 8) {
-    return mk(-v.re, -v.im);
-  } else if constexpr (k16 == 12) {
-    return sign < 0 ? mk(-v.im, v.re) : mk(v.im, -v.re);
-  } else {
-    constexpr double c = fftc::cos16(k16), s = fftc::sin16(k16);
-    const double ss = sign * s;
-    return mk(v.re * c - v.im * ss, v.re * ss + v.im * c);
-  }
+// Runtime-indexed constant rotation: with every loop unrolled k16 is a
+// compile-time constant and the branches fold (trivial rotations free).
+SLSE_D cplx rot16(cplx v, int k16, double sign) {
+  if (k16 == 0) return v;
+  if (k16 == 4) return sign < 0 ? mk(v.im, -v.re) : mk(-v.im, v.re);
+  if (k16 == 8) return mk(-v.re, -v.im);
+  if (k16 == 12) return sign < 0 ? mk(-v.im, v.re) : mk(v.im, -v.re);
+  const double c = fftc::cos16(k16), ss = sign * fftc::sin16(k16);
+  return mk(v.re * c - v.im * ss, v.re * ss + v.im * c);
 }
 
-template <int R, int S = 1, int O = 0>
-struct RegDft {
-  // in-place DFT of the R points v[O + S*i], i < R (radix-2 DIT recursion)
-  template <class V>
-  SLSE_D static void run(V& v, double sign) {
-    RegDft<R / 2, 2 * S, O>::run(v, sign);
-    RegDft<R / 2, 2 * S, O + S>::run(v, sign);
-    // combine: even part at O + 2S i, odd part at O + S + 2S i; outputs in
-    // natural order need a permutation: gather into temporaries
-    cplx t[R];
-    combine<0>(v, t, sign);
+SLSE_HD constexpr int brev_const(int r, int R) {
+  int out = 0;
+  for (int m = R >> 1, q = 1; m >= 1; m >>= 1, q <<= 1)
+    if (r & q) out |= m;
+  return out;
+}
+
+// In-place radix-2 DIF DFT of R = 2..16 register points: natural order in,
+// bit-reversed order out (X[k] = v[brev(k)]); no temporaries.  Stages are
+// template-recursive so every index is a compile-time constant.
+template <int R, int SPAN>
+struct DifStage {
+  SLSE_D static void run(cplx* v, double sign) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) v[O + S * i] = t[i];
-  }
-  template <int K, class V>
-  SLSE_D static void combine(V& v, cplx* t, double sign) {
-    if constexpr (K < R / 2) {
-      const cplx e = v[O + 2 * S * K];
-      const cplx o = rot_const<K, R>(v[O + S + 2 * S * K], sign);
-      t[K] = cadd(e, o);
-      t[K + R / 2] = csub(e, o);
-      combine<K + 1>(v, t, sign);
+    for (int g = 0; g < R; g += 2 * SPAN) {
+#pragma unroll
+      for (int p = 0; p < SPAN; ++p) {
+        const cplx a = v[g + p], c = v[g + p + SPAN];
+        v[g + p] = cadd(a, c);
+        v[g + p + SPAN] = rot16(csub(a, c), p * (16 / (2 * SPAN)), sign);
+      }
     }
+    DifStage<R, SPAN / 2>::run(v, sign);
   }
 };
-template <int S, int O>
-struct RegDft<1, S, O> {
-  template <class V>
-  SLSE_D static void run(V&, double) {}
+template <int R>
+struct DifStage<R, 0> {
+  SLSE_D static void run(cplx*, double) {}
 };
+
+template <int R>
+SLSE_D void dft_dif(cplx* v, double sign) {
+  DifStage<R, R / 2>::run(v, sign);
+}
 
 // shared-memory skew: one pad slot per 16 points, so the stride-R stores of
 // a pass (and stride-16 anything) spread over all banks
 SLSE_HD int sk(int i) { return i + (i >> 4); }
 SLSE_HD int sk_len(int n) { return n + (n >> 4); }
 
+SLSE_D void block_barrier() {
+#ifndef SLSE_HOST_EMU
+  __syncthreads();
+#endif
+}
+
 template <int R, int MAXI>
-SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const FftCtx& f, Blk& b) {
+SLSE_D void stockham_pass_inl(cplx* x, int count, int n, int Ns, double sign, const cplx* __restrict__ tw, int twlog,
+                           int tid, int nt) {
   const int per = n / R;
   const int total = count * per;
   const int lg = ilog2(Ns * R);
@@ -217,24 +230,24 @@ SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const 
     for (int r = 0; r < R; ++r) vv[it][r] = xc[sk(j + r * per)];
     if (Ns > 1) {
       const int kk = j & (Ns - 1);
-      for (int r = 1; r < R; ++r) vv[it][r] = cmul(vv[it][r], twid(f, kk * r, lg, sign));
+      for (int r = 1; r < R; ++r) vv[it][r] = cmul(vv[it][r], twid_tab(tw, twlog, kk * r, lg, sign));
     }
-    RegDft<R>::run(vv[it], sign);
+    dft_dif<R>(vv[it].data(), sign);
   }
   for (int it = 0; it < total; ++it) {
     const int c = it / per, j = it - c * per;
     cplx* xc = x + (size_t)c * sk_len(n);
     const int kk = j & (Ns - 1);
     const int base = (j - kk) * R + kk;
-    for (int r = 0; r < R; ++r) xc[sk(base + r * Ns)] = vv[it][r];
+    for (int r = 0; r < R; ++r) xc[sk(base + r * Ns)] = vv[it][brev_const(r, R)];
   }
-  (void)b;
+  (void)tid; (void)nt;
   return;
 #endif
   cplx v[MAXI][R];
 #pragma unroll
   for (int i = 0; i < MAXI; ++i) {
-    const int it = b.tid + i * b.nt;
+    const int it = tid + i * nt;
     if (it < total) {
       const int c = it / per, j = it - c * per;
       const cplx* xc = x + (size_t)c * sk_len(n);
@@ -243,26 +256,51 @@ SLSE_D void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const 
       if (Ns > 1) {
         const int kk = j & (Ns - 1);
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twid(f, kk * r, lg, sign));
+        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twid_tab(tw, twlog, kk * r, lg, sign));
       }
-      RegDft<R>::run(v[i], sign);
+      dft_dif<R>(v[i], sign);
     }
   }
-  b.sync();
+  block_barrier();
 #pragma unroll
   for (int i = 0; i < MAXI; ++i) {
-    const int it = b.tid + i * b.nt;
+    const int it = tid + i * nt;
     if (it < total) {
       const int c = it / per, j = it - c * per;
       cplx* xc = x + (size_t)c * sk_len(n);
       const int kk = j & (Ns - 1);
       const int base = (j - kk) * R + kk;
 #pragma unroll
-      for (int r = 0; r < R; ++r) xc[sk(base + r * Ns)] = v[i][r];
+      for (int r = 0; r < R; ++r) xc[sk(base + r * Ns)] = v[i][brev_const(r, R)];
     }
   }
-  b.sync();
+  block_barrier();
 }
+
+template <int R, int MAXI>
+SLSE_NI void stockham_pass(cplx* x, int count, int n, int Ns, double sign, const cplx* __restrict__ tw, int twlog,
+                           int tid, int nt) {
+  stockham_pass_inl<R, MAXI>(x, count, n, Ns, sign, tw, twlog, tid, nt);
+}
+
+// Compile-time pass schedule for a transform of 2^LG points (radix 16 while
+// at least 16 points per sub-transform remain, then the remainder): fully
+// inlined so the register allocator sees straight-line passes.
+template <int LG, int LGNS>
+struct FixedPlan {
+  SLSE_D static void run(cplx* x, int count, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+    constexpr int rem = LG - LGNS;
+    constexpr int lr = rem >= 4 ? 4 : rem;
+    constexpr int R = 1 << lr;
+    constexpr int MAXI = 16 / R;
+    stockham_pass_inl<R, MAXI>(x, count, 1 << LG, 1 << LGNS, sign, tw, twlog, tid, nt);
+    FixedPlan<LG, LGNS + lr>::run(x, count, sign, tw, twlog, tid, nt);
+  }
+};
+template <int LG>
+struct FixedPlan<LG, LG> {
+  SLSE_D static void run(cplx*, int, double, const cplx* __restrict__, int, int, int) {}
+};
 
 // radix for the pass with `rem` = n / Ns points per sub-transform left
 SLSE_D int stockham_radix(int rem, int count, int n, int nt) {
@@ -289,26 +327,36 @@ SLSE_D bool stockham_ok(int count, int n, int nt) {
 
 // in-place forward/backward transform of `count` buffers of n points held
 // in the skewed layout (buffer c at x + c * sk_len(n), point i at sk(i))
-SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& f, Blk& b) {
+SLSE_D void fft_stockham_inl(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                             Blk& b) {
   for (int Ns = 1; Ns < n;) {
     const int R = stockham_radix(n / Ns, count, n, b.nt);
     switch (R) {
-      case 16: stockham_pass<16, 1>(x, count, n, Ns, sign, f, b); break;
-      case 8: stockham_pass<8, 2>(x, count, n, Ns, sign, f, b); break;
-      case 4: stockham_pass<4, 4>(x, count, n, Ns, sign, f, b); break;
-      default: stockham_pass<2, 8>(x, count, n, Ns, sign, f, b); break;
+      case 16: stockham_pass<16, 1>(x, count, n, Ns, sign, tw, twlog, b.tid, b.nt); break;
+      case 8: stockham_pass<8, 2>(x, count, n, Ns, sign, tw, twlog, b.tid, b.nt); break;
+      case 4: stockham_pass<4, 4>(x, count, n, Ns, sign, tw, twlog, b.tid, b.nt); break;
+      default: stockham_pass<2, 8>(x, count, n, Ns, sign, tw, twlog, b.tid, b.nt); break;
     }
     Ns *= R;
   }
+}
+
+SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& f, Blk& b) {
+  Blk bb = b;
+  fft_stockham_inl(x, count, n, sign, f.tw, f.twlog, bb);
+  b.bank = bb.bank;
 }
 
 
 // ---------------------------------------------------------------------------
 // Dispatch: the register Stockham when the transform fits the shared
 // staging area and the block's register caps, else radix-4 DIT.
+#ifndef SLSE_SOLVER_STOCKHAM
+#define SLSE_SOLVER_STOCKHAM 0
+#endif
 template <class Load, class Store>
 SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
-  if (sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
+  if (SLSE_SOLVER_STOCKHAM && sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
     cplx* x = f.smem;
     for (int i = b.tid; i < n; i += b.nt) x[sk(i)] = ld(i);
     b.sync();
@@ -321,7 +369,7 @@ SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx&
 }
 
 SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {
-  if (sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
+  if (SLSE_SOLVER_STOCKHAM && sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
     cplx* x = f.smem;
     for (int i = b.tid; i < n; i += b.nt) x[sk(i)] = data[i];
     b.sync();

@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, 
 // Row 9 standalone, register-Stockham variant: the three length-L transforms
 // (w, rho, n*rho; zero padded) live in shared memory, run as radix-16/4
 // passes over all three at once, and the combine writes q^G and s^G once.
-template <int NT>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 4 : 1)) grid_stockham_kernel(const cplx* __restrict__ rho,
+template <int NT, int LG>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grid_stockham_kernel(const cplx* __restrict__ rho,
                                                            const double* __restrict__ delta_last,
                                                            const cplx* __restrict__ w, int n, int L,
                                                            cplx* __restrict__ q_grid, double* __restrict__ s_grid,
@@ -275,8 +275,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 4 : 1)) grid_stockham_kernel(
     X[2 * LS + si] = cscale(rr, (double)i);
   }
   __syncthreads();
-  FftCtx f{tw, twlog, nullptr, 0};
-  fft_stockham(X, 3, L, -1.0, f, b);
+  FixedPlan<LG, 0>::run(X, 3, -1.0, tw, twlog, threadIdx.x, NT);
   const double inv_d = 1.0 / delta_last[p];
   const double c2n = 2.0 - (double)n;
   cplx* qg = q_grid + (size_t)p * L;
