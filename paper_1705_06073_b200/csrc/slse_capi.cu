@@ -286,31 +286,40 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   if (rc) return rc;
   cudaError_t e = cudaSuccess;
   // register-Stockham path: 3 L-point transforms resident in shared memory,
-  // compile-time pass schedules for L = 2^6 .. 2^12
+  // compile-time pass schedules for L = 2^6 .. 2^12, pruned first pass
   if (getenv("SLSE_GRID_DIT") == nullptr) {
     const int lg = ilog2(L);
-#define SLSE_GRID_CASE(LGV, NTV)                                                                          \
-  case LGV: {                                                                                              \
-    const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(L);                                         \
-    e = set_smem(grid_stockham_kernel<NTV, LGV>, ssmem);                                                    \
+    int q = 0;
+    while (q < 3 && (N << (q + 1)) <= L) ++q;  // input support n <= L / 2^q
+#define SLSE_GRID_Q(NTV, LGV, QV)                                                                          \
+  case QV: {                                                                                               \
+    const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
+    e = set_smem(grid_stockham_kernel<NTV, LGV, QV>, ssmem);                                               \
     if (e == cudaSuccess) {                                                                                \
-      grid_stockham_kernel<NTV, LGV><<<B, NTV, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, L, \
-                                                           (cplx*)q_grid, s_grid, tw, twlog);             \
+      grid_stockham_kernel<NTV, LGV, QV><<<B, NTV, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, \
+                                                               (cplx*)q_grid, s_grid, tw, twlog);          \
       e = cudaGetLastError();                                                                              \
     }                                                                                                      \
     return e == cudaSuccess ? 0 : fail("grid_stockham_kernel", e);                                         \
   }
+#define SLSE_GRID_CASE(LGV, NTV)                                                \
+  case LGV:                                                                     \
+    switch (q) {                                                                \
+      SLSE_GRID_Q(NTV, LGV, 0) SLSE_GRID_Q(NTV, LGV, 1) SLSE_GRID_Q(NTV, LGV, 2) SLSE_GRID_Q(NTV, LGV, 3) \
+    }                                                                           \
+    break;
     switch (lg) {
-      SLSE_GRID_CASE(6, 64)
-      SLSE_GRID_CASE(7, 64)
+      SLSE_GRID_CASE(6, 32)
+      SLSE_GRID_CASE(7, 32)
       SLSE_GRID_CASE(8, 64)
-      SLSE_GRID_CASE(9, 128)
-      SLSE_GRID_CASE(10, 256)
-      SLSE_GRID_CASE(11, 512)
-      SLSE_GRID_CASE(12, 1024)
+      SLSE_GRID_CASE(9, 96)
+      SLSE_GRID_CASE(10, 192)
+      SLSE_GRID_CASE(11, 384)
+      SLSE_GRID_CASE(12, 768)
       default: break;
     }
 #undef SLSE_GRID_CASE
+#undef SLSE_GRID_Q
   }
   const int nt = block_threads(N);
   const int fused = 48 * (size_t)L <= kRegionBudget ? 1 : 0;

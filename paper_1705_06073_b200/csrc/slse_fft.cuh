@@ -381,4 +381,88 @@ SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Pruned first pass for zero-padded inputs: only the first NZ of the R
+// points of every radix-R sub-transform are nonzero (input support
+// [0, n*NZ/R)).  The DIF stages with span >= NZ reduce to rotations of the
+// nonzero half (no additions), and the zero inputs are never loaded.
+template <int R, int NZ, int SPAN>
+struct DifPrunedStage {
+  SLSE_D static void run(cplx* v, double sign) {
+    if constexpr (SPAN >= NZ) {
+#pragma unroll
+      for (int g = 0; g < R; g += 2 * SPAN) {
+#pragma unroll
+        for (int p = 0; p < NZ; ++p) v[g + p + SPAN] = rot16(v[g + p], p * (16 / (2 * SPAN)), sign);
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < R; g += 2 * SPAN) {
+#pragma unroll
+        for (int p = 0; p < SPAN; ++p) {
+          const cplx a = v[g + p], c = v[g + p + SPAN];
+          v[g + p] = cadd(a, c);
+          v[g + p + SPAN] = rot16(csub(a, c), p * (16 / (2 * SPAN)), sign);
+        }
+      }
+    }
+    DifPrunedStage<R, NZ, SPAN / 2>::run(v, sign);
+  }
+};
+template <int R, int NZ>
+struct DifPrunedStage<R, NZ, 0> {
+  SLSE_D static void run(cplx*, double) {}
+};
+
+template <int R, int NZ>
+SLSE_D void stockham_first_pruned(cplx* x, int count, int n, double sign, int tid, int nt) {
+  const int per = n / R;
+  const int total = count * per;
+#ifdef SLSE_HOST_EMU
+  std::vector<std::array<cplx, R>> vv(total);
+  for (int it = 0; it < total; ++it) {
+    const int c = it / per, j = it - c * per;
+    const cplx* xc = x + (size_t)c * sk_len(n);
+    for (int r = 0; r < NZ; ++r) vv[it][r] = xc[sk(j + r * per)];
+    DifPrunedStage<R, NZ, R / 2>::run(vv[it].data(), sign);
+  }
+  for (int it = 0; it < total; ++it) {
+    const int c = it / per, j = it - c * per;
+    cplx* xc = x + (size_t)c * sk_len(n);
+    for (int r = 0; r < R; ++r) xc[sk(j * R + r)] = vv[it][brev_const(r, R)];
+  }
+  (void)tid; (void)nt;
+  return;
+#endif
+  cplx v[R];
+  const int it = tid;
+  const bool act = it < total;
+  int c = 0, j = 0;
+  if (act) {
+    c = it / per;
+    j = it - c * per;
+    const cplx* xc = x + (size_t)c * sk_len(n);
+#pragma unroll
+    for (int r = 0; r < NZ; ++r) v[r] = xc[sk(j + r * per)];
+    DifPrunedStage<R, NZ, R / 2>::run(v, sign);
+  }
+  block_barrier();
+  if (act) {
+    cplx* xc = x + (size_t)c * sk_len(n);
+#pragma unroll
+    for (int r = 0; r < R; ++r) xc[sk(j * R + r)] = v[brev_const(r, R)];
+  }
+  block_barrier();
+}
+
+// Whole transform for inputs supported on the first 2^-Q of each buffer:
+// pruned radix-16 first pass, then the fixed schedule.  Needs count*n/16 <= nt.
+template <int LG, int Q>
+SLSE_D void fft_fixed_pruned(cplx* x, int count, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+  static_assert(LG >= 4 && Q >= 0 && Q <= 3, "pruned plan: L >= 16, support >= L/8");
+  stockham_first_pruned<16, (16 >> Q)>(x, count, 1 << LG, sign, tid, nt);
+  FixedPlan<LG, 4>::run(x, count, sign, tw, twlog, tid, nt);
+}
+
 }  // namespace slse

@@ -251,22 +251,22 @@ __global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, 
 
 
 // Row 9 standalone, register-Stockham variant: the three length-L transforms
-// (w, rho, n*rho; zero padded) live in shared memory, run as radix-16/4
-// passes over all three at once, and the combine writes q^G and s^G once.
-template <int NT, int LG>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grid_stockham_kernel(const cplx* __restrict__ rho,
-                                                           const double* __restrict__ delta_last,
-                                                           const cplx* __restrict__ w, int n, int L,
-                                                           cplx* __restrict__ q_grid, double* __restrict__ s_grid,
-                                                           const cplx* tw, int twlog) {
+// (w, rho, n*rho) live in shared memory; only their nonzero heads (the
+// first L/2^Q points, n <= L/2^Q) are loaded, the first radix-16 pass is
+// pruned accordingly, and the combine writes q^G and s^G once.
+template <int NT, int LG, int Q>
+__global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) grid_stockham_kernel(
+    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n,
+    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* tw, int twlog) {
+  constexpr int L = 1 << LG;
+  constexpr int LS = L + (L >> 4);
+  constexpr int H = L >> Q;  // loaded head (>= n)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
   const int p = blockIdx.x;
   const cplx* rp = rho + (size_t)p * n;
   const cplx* wp = w + (size_t)p * n;
   cplx* X = (cplx*)(smem_raw + head_bytes(NT));
-  const int LS = sk_len(L);
-  for (int i = threadIdx.x; i < L; i += NT) {
+  for (int i = threadIdx.x; i < H; i += NT) {
     cplx a = mk(0.0, 0.0), rr = mk(0.0, 0.0);
     if (i < n) { a = wp[i]; rr = rp[i]; }
     const int si = sk(i);
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grid_stockham_kernel(
     X[2 * LS + si] = cscale(rr, (double)i);
   }
   __syncthreads();
-  FixedPlan<LG, 0>::run(X, 3, -1.0, tw, twlog, threadIdx.x, NT);
+  fft_fixed_pruned<LG, Q>(X, 3, -1.0, tw, twlog, threadIdx.x, NT);
   const double inv_d = 1.0 / delta_last[p];
   const double c2n = 2.0 - (double)n;
   cplx* qg = q_grid + (size_t)p * L;

@@ -130,3 +130,40 @@ extern "C" int emu_fft_dit(double* x, int n, int sign) {
   fft_inplace((cplx*)x, n, (double)sign, f, b);
   return 0;
 }
+
+// grid kernel pipeline (load head, pruned Stockham over 3 buffers, combine)
+template <int LG, int Q>
+static void grid_pruned_t(const cplx* w, const cplx* rho, int n, double dl, cplx* qg, double* sg) {
+  constexpr int L = 1 << LG;
+  const int LS = sk_len(L);
+  std::vector<cplx> tw = make_twiddles(LG);
+  std::vector<cplx> X(3 * LS, mk(0, 0));
+  for (int i = 0; i < (L >> Q); ++i) {
+    cplx a = mk(0, 0), r = mk(0, 0);
+    if (i < n) { a = w[i]; r = rho[i]; }
+    X[sk(i)] = a; X[LS + sk(i)] = r; X[2 * LS + sk(i)] = cscale(r, (double)i);
+  }
+  fft_fixed_pruned<LG, Q>(X.data(), 3, -1.0, tw.data(), LG, 0, 1);
+  for (int l = 0; l < L; ++l) {
+    const cplx a0 = X[LS + sk(l)], a1 = X[2 * LS + sk(l)];
+    qg[l] = X[sk(l)];
+    sg[l] = ((2.0 - n) * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) / dl;
+  }
+}
+
+extern "C" int emu_grid_pruned(const double* w, const double* rho, int n, double dl, int L, double* qg, double* sg) {
+  int q = 0;
+  while (q < 3 && (n << (q + 1)) <= L) ++q;
+  const cplx* W = (const cplx*)w;
+  const cplx* R = (const cplx*)rho;
+#define C(LGV) \
+  if (L == (1 << LGV)) { \
+    if (q == 0) grid_pruned_t<LGV, 0>(W, R, n, dl, (cplx*)qg, sg); \
+    if (q == 1) grid_pruned_t<LGV, 1>(W, R, n, dl, (cplx*)qg, sg); \
+    if (q == 2) grid_pruned_t<LGV, 2>(W, R, n, dl, (cplx*)qg, sg); \
+    if (q == 3) grid_pruned_t<LGV, 3>(W, R, n, dl, (cplx*)qg, sg); \
+    return q; }
+  C(6) C(7) C(8) C(9) C(10) C(11) C(12)
+#undef C
+  return -1;
+}

@@ -79,3 +79,41 @@ def test_emulated_batch_vs_oracle_cfg2_shape():
         assert res[b].k_hat == o.k_hat
         assert res[b].trace_stages == o.trace_stages
         assert encode_events(res[b].events).tolist() == encode_events(o.events).tolist()
+
+
+@pytest.mark.parametrize("n,L", [(64, 256), (256, 1024), (100, 1024), (1024, 4096), (256, 512), (32, 64),
+                                 (17, 128), (512, 4096)])
+def test_emulated_pruned_stockham_grid(n, L):
+    """The grid kernel's pipeline (head load, pruned radix-16 first pass,
+    fixed Stockham schedule over three buffers, product-form combine)
+    against the oracle's grid (model_core.py:303-313)."""
+    import ctypes
+
+    lib = H.build()
+    rng = np.random.default_rng(n + L)
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    b = O.Bundle(y, [0.1, 0.4], [1.0, 0.5], 0.3)
+    qg = np.zeros(L, complex)
+    sg = np.zeros(L)
+    lib.emu_grid_pruned.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                    ctypes.c_void_p, ctypes.c_void_p]
+    q = lib.emu_grid_pruned(b.w.ctypes.data, b.rho.ctypes.data, n, b.delta[-1], L, qg.ctypes.data, sg.ctypes.data)
+    assert q >= 0
+    q0, s0 = b.grid(L)
+    assert rel(qg, q0) < 1e-13 and rel(sg, s0) < 1e-13
+
+
+@pytest.mark.parametrize("n", [2, 4, 16, 64, 256, 1024, 4096, 8192])
+def test_emulated_stockham_fft(n):
+    import ctypes
+
+    lib = H.build()
+    rng = np.random.default_rng(n)
+    for cnt in (1, 3):
+        x = rng.standard_normal((cnt, n)) + 1j * rng.standard_normal((cnt, n))
+        y = x.copy()
+        lib.emu_fft_stockham(ctypes.c_void_p(y.ctypes.data), cnt, n, -1)
+        assert rel(y, np.fft.fft(x, axis=1)) < 1e-14
+        z = x.copy()
+        lib.emu_fft_stockham(ctypes.c_void_p(z.ctypes.data), cnt, n, 1)
+        assert rel(z, n * np.fft.ifft(x, axis=1)) < 1e-14
