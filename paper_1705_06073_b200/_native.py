@@ -72,6 +72,7 @@ def load():
         "slse_default_options": ([ctypes.POINTER(SlseOptions)], None),
         "slse_cov_column": ([vp, vp, vp, i, vp, i, i, vp, vp], i),
         "slse_toeplitz_factor": ([vp, i, i, vp, vp, vp, vp, vp], i),
+        "slse_toeplitz_factor_ex": ([vp, i, i, vp, vp, vp, vp, i, vp], i),
         "slse_gs_apply": ([vp, vp, vp, i, i, vp, vp, vp], i),
         "slse_component_stats": ([vp, vp, i, vp, vp, vp, i, i, vp, vp, vp, vp, vp, vp, vp, vp], i),
         "slse_grid_eval": ([vp, vp, vp, i, i, i, vp, vp, vp], i),

@@ -130,8 +130,9 @@ int solver_threads(int n) {
 
 int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
+  P.dnc = n >= dnc_min_n() ? 1 : 0;
   const int nt = solver_threads(n);
-  SmemPlan plan = smem_plan(n, P.L, nt);
+  SmemPlan plan = smem_plan(n, P.L, nt, P.dnc != 0);
   int occ = 1;
   cudaError_t e = cudaSuccess;
   switch (nt) {
@@ -147,7 +148,7 @@ int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, 
   int g = sm_count() * occ;
   if (g > B) g = B;
   if (g < 1) g = 1;
-  Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0);
+  Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0, P.dnc != 0);
   *slab_out = lay.total;
   if (plan_out) *plan_out = plan;
   return g;
@@ -200,9 +201,44 @@ int slse_cov_column(const double* theta, const double* gamma, const int32_t* kco
 
 int slse_toeplitz_factor(const double* c, int N, int B, double* rho, double* delta, double* logdet, int32_t* status,
                          void* stream) {
-  if (N < 1 || B < 0) return fail_arg("slse_toeplitz_factor: bad sizes");
+  return slse_toeplitz_factor_ex(c, N, B, rho, delta, logdet, status, 0, stream);
+}
+
+int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* delta, double* logdet,
+                            int32_t* status, int method, void* stream) {
+  if (N < 1 || B < 0 || method < 0 || method > 2) return fail_arg("slse_toeplitz_factor: bad arguments");
   if (B == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  if (method == 2 || (method == 0 && N >= dnc_min_n())) {
+    const cplx* tw;
+    int twlog;
+    const int F = 1 << ilog2(N);
+    int rc = twiddles(ilog2(F > 16 ? F : 16), st, &tw, &twlog);
+    if (rc) return rc;
+    const int nt = N <= 2048 ? 256 : 1024;
+    int cap = 1;
+    while (16 * (size_t)(cap * 2) <= kRegionBudget) cap *= 2;
+    if (cap > F) cap = F;
+    const size_t smem = kHeadBytes + 16 * (size_t)cap;
+    const size_t per = 4 * (size_t)N + dnc_arena_elems(N - 1) + 16;
+    cplx* scratch = nullptr;
+    double* dscr = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, sizeof(cplx) * per * B, st);
+    if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+    e = cudaMallocAsync(&dscr, sizeof(double) * (size_t)N * B, st);
+    if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+    SLSE_DISPATCH_NT(nt, {
+      e = set_smem(factor_dnc_kernel<NTC>, smem);
+      if (e == cudaSuccess) {
+        factor_dnc_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)c, N, (cplx*)rho, delta, logdet, status, scratch, per,
+                                                    dscr, tw, twlog, cap);
+        e = cudaGetLastError();
+      }
+    });
+    cudaFreeAsync(scratch, st);
+    cudaFreeAsync(dscr, st);
+    return e == cudaSuccess ? 0 : fail("factor_dnc_kernel", e);
+  }
   const int nt = block_threads(N);
   const size_t rec = 48 * (size_t)N;
   const int rec_smem = rec <= kRegionBudget ? 1 : 0;
@@ -369,6 +405,7 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
     return -2;
   }
   SolveParams P = make_params(N, o);
+  P.dnc = N >= dnc_min_n() ? 1 : 0;
   const cplx* tw;
   int twlog;
   const int fmax = P.L > 2 * N ? P.L : (1 << ilog2(2 * N));

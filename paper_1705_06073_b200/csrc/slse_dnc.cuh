@@ -1,0 +1,290 @@
+// slse_dnc.cuh -- superfast (divide-and-conquer, FFT-doubling) generalized
+// Schur factorisation of a Hermitian PD Toeplitz matrix.
+//
+// Reference: toeplitz.generalized_schur / _schur_split / _schur_base /
+// _theta_matmul (pkg/src/superlse/toeplitz.py:148-260), O(N log^2 N).
+//
+// Formulation (own; unnormalised steps).  With generator polynomials
+// e(z) = sum e_j z^j, b(z) = sum b_j z^j (e = b = c initially) one Schur
+// step with reflection coefficient k = -e_{m+1} / delta_m is
+//     [e; b] <- M_k [e; b],   M_k = [[1, k z], [conj(k), z]],
+// delta_{m+1} = delta_m (1 - |k|^2), and the Levinson predictor pair
+// (a, conj-reversed a) obeys the same recursion from [1; 1], so after all
+// N-1 steps  a = Theta_11 + Theta_12  for Theta = M_{N-2} ... M_0.
+//
+// split(E, Bw, s): transfer matrix Theta of s steps from the generator
+// window E[j] = e_{m0+j} (j <= s), Bw[j] = b_{m0+j} (j < s):
+//   s <= 32 : leaf -- one warp runs the classical recursion in registers
+//             (shuffles, no block barriers) and accumulates Theta;
+//   else    : Theta1 = split(left half h = s/2); the right half's window is
+//             the middle product [h, s] of Theta1 with (E, Bw); Theta2 =
+//             split(right half); Theta = Theta2 Theta1.  Every product is
+//             a cyclic convolution of length F = 2^ceil(log2(s+1)), done
+//             with the block FFT (shared-memory staged when it fits).
+#pragma once
+#include "slse_toeplitz.cuh"
+
+namespace slse {
+
+constexpr int kDncLeaf = 32;
+
+struct DncCtx {
+  FftCtx f;
+  cplx* arena;        // global scratch (bump allocated along the recursion)
+  double* delta_tmp;  // pivots delta_0..delta_{N-1}
+  double floor_;      // PD floor = PD_EPS * c0
+  double d;           // current pivot (identical in every thread)
+  int step;           // steps done
+  int status;
+};
+
+#ifndef SLSE_HOST_EMU
+SLSE_D cplx shfl_c(cplx v, int src) {
+  return mk(__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src));
+}
+SLSE_D cplx shfl_down_c(cplx v, int d) {
+  return mk(__shfl_down_sync(0xffffffffu, v.re, d), __shfl_down_sync(0xffffffffu, v.im, d));
+}
+SLSE_D cplx shfl_up_c(cplx v, int d) {
+  return mk(__shfl_up_sync(0xffffffffu, v.re, d), __shfl_up_sync(0xffffffffu, v.im, d));
+}
+#endif
+
+// Leaf: s <= 32 steps.  E1[j] = e_{m0+1+j}, Bw[j] = b_{m0+j} (j < s).
+// Writes Theta (4 polys of s+1 coefficients, row-major T11 T12 T21 T22 at
+// stride s+1), pivots, and updates X.d / X.step / X.status (uniform).
+SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T, Blk& b) {
+  const int ld = s + 1;
+#ifdef SLSE_HOST_EMU
+  std::vector<cplx> e(E1, E1 + s), bb(Bw, Bw + s);
+  std::vector<cplx> t11(ld + 1, mk(0, 0)), t12(ld + 1, mk(0, 0)), t21(ld + 1, mk(0, 0)), t22(ld + 1, mk(0, 0));
+  t11[0] = mk(1, 0);
+  t22[0] = mk(1, 0);
+  double d = X.d;
+  int st = 0;
+  for (int t = 0; t < s; ++t) {
+    const double inv = 1.0 / d;
+    const cplx k = mk(-e[t].re * inv, -e[t].im * inv), kc = conjg(k);
+    for (int j = 0; j < s - t; ++j) {
+      const cplx ej = e[t + j], bj = bb[j];
+      e[t + j] = cadd(ej, cmul(k, bj));
+      bb[j] = cadd(bj, cmul(kc, ej));
+    }
+    for (int i = t + 1; i >= 0; --i) {  // degree grows by one per step
+      const cplx a11 = t11[i], a12 = t12[i];
+      const cplx p21 = i ? t21[i - 1] : mk(0, 0), p22 = i ? t22[i - 1] : mk(0, 0);
+      t11[i] = cadd(a11, cmul(k, p21));
+      t12[i] = cadd(a12, cmul(k, p22));
+      t21[i] = cadd(cmul(kc, a11), p21);
+      t22[i] = cadd(cmul(kc, a12), p22);
+    }
+    d = d * (1.0 - (k.re * k.re + k.im * k.im));
+    X.delta_tmp[X.step + t + 1] = d;
+    if (!(d > X.floor_)) { st = kNotPD; break; }
+  }
+  for (int i = 0; i < ld; ++i) {
+    T[i] = t11[i];
+    T[ld + i] = t12[i];
+    T[2 * ld + i] = t21[i];
+    T[3 * ld + i] = t22[i];
+  }
+  X.d = d;
+  X.step += s;
+  if (st) X.status = st;
+  (void)b;
+#else
+  __shared__ double s_out[2];
+  if (b.tid < 32) {
+    const int lane = b.tid;
+    // generator pairs in the shifted frame: lane j holds (e_{m0+t+1+j}, b_{m0+t+j})
+    cplx ej = lane < s ? E1[lane] : mk(0.0, 0.0);
+    cplx bj = lane < s ? Bw[lane] : mk(0.0, 0.0);
+    // Theta coefficients i = lane (and i = 32 kept redundantly in x*)
+    cplx t11 = mk(lane == 0 ? 1.0 : 0.0, 0.0), t12 = mk(0.0, 0.0), t21 = mk(0.0, 0.0);
+    cplx t22 = mk(lane == 0 ? 1.0 : 0.0, 0.0);
+    cplx x11 = mk(0.0, 0.0), x12 = mk(0.0, 0.0), x21 = mk(0.0, 0.0), x22 = mk(0.0, 0.0);
+    double d = X.d;
+    int st = 0;
+    for (int t = 0; t < s; ++t) {
+      const cplx e0 = shfl_c(ej, 0);
+      const double inv = 1.0 / d;
+      const cplx k = mk(-e0.re * inv, -e0.im * inv), kc = conjg(k);
+      const cplx en = cadd(ej, cmul(k, bj));
+      const cplx bn = cadd(bj, cmul(kc, ej));
+      ej = shfl_down_c(en, 1);
+      bj = bn;
+      // Theta <- M_k Theta : T1x[i] += k T2x[i-1] ; T2x[i] = conj(k) T1x[i] + T2x[i-1]
+      const cplx p21 = shfl_up_c(t21, 1), p22 = shfl_up_c(t22, 1);
+      const cplx l21 = shfl_c(t21, 31), l22 = shfl_c(t22, 31);  // coefficient 31 feeds 32
+      const cplx q21 = lane ? p21 : mk(0.0, 0.0), q22 = lane ? p22 : mk(0.0, 0.0);
+      const cplx n11 = cadd(t11, cmul(k, q21)), n12 = cadd(t12, cmul(k, q22));
+      const cplx n21 = cadd(cmul(kc, t11), q21), n22 = cadd(cmul(kc, t12), q22);
+      const cplx m11 = cadd(x11, cmul(k, l21)), m12 = cadd(x12, cmul(k, l22));
+      const cplx m21 = cadd(cmul(kc, x11), l21), m22 = cadd(cmul(kc, x12), l22);
+      t11 = n11; t12 = n12; t21 = n21; t22 = n22;
+      x11 = m11; x12 = m12; x21 = m21; x22 = m22;
+      d = d * (1.0 - (k.re * k.re + k.im * k.im));
+      if (lane == 0) X.delta_tmp[X.step + t + 1] = d;
+      if (!(d > X.floor_)) { st = kNotPD; break; }
+    }
+    if (lane < ld) {
+      T[lane] = t11;
+      T[ld + lane] = t12;
+      T[2 * ld + lane] = t21;
+      T[3 * ld + lane] = t22;
+    }
+    if (lane == 31 && ld > 32) {
+      T[32] = x11;
+      T[ld + 32] = x12;
+      T[2 * ld + 32] = x21;
+      T[3 * ld + 32] = x22;
+    }
+    if (lane == 0) {
+      s_out[0] = d;
+      s_out[1] = (double)st;
+    }
+  }
+  b.sync();
+  X.d = s_out[0];
+  X.step += s;
+  if (s_out[1] != 0.0) X.status = (int)s_out[1];
+  b.sync();
+#endif
+}
+
+// forward transform of src[0..len) zero padded to F -> dst[0..F)
+SLSE_D void dnc_fwd(cplx* dst, const cplx* src, int len, int F, cplx* work, const FftCtx& f, Blk& b) {
+  fft(work, F, -1.0, [&](int i) { return i < len ? src[i] : mk(0.0, 0.0); },
+      [&](int i, cplx v) { dst[i] = v; }, f, b);
+}
+
+SLSE_NI void dnc_split(DncCtx& X, const cplx* E, const cplx* Bw, int s, cplx* T, Blk& b) {
+  if (X.status) return;
+  if (s <= kDncLeaf) {
+    dnc_leaf(X, E + 1, Bw, s, T, b);
+    return;
+  }
+  const int h = s / 2;
+  const int F = 1 << ilog2(s + 1);
+  const double invF = 1.0 / (double)F;
+  cplx* base = X.arena;
+  cplx* T1 = base;                       // 4 (h+1)
+  cplx* S = T1 + 4 * (h + 1);            // 4 F : spectra of T1 (kept for the product)
+  cplx* SE = S + 4 * (size_t)F;          // F
+  cplx* SB = SE + F;                     // F
+  cplx* work = SB + F;                   // F  (global fallback buffer)
+  cplx* E2 = work + F;                   // s - h + 1
+  cplx* B2 = E2 + (s - h + 1);           // s - h
+  cplx* T2 = B2 + (s - h);               // 4 (s - h + 1)
+  X.arena = T2 + 4 * (s - h + 1);
+  // ---- left half
+  dnc_split(X, E, Bw, h, T1, b);
+  if (X.status) { X.arena = base; return; }
+  const int l1 = h + 1;
+  for (int q = 0; q < 4; ++q) dnc_fwd(S + (size_t)q * F, T1 + q * l1, l1, F, work, X.f, b);
+  dnc_fwd(SE, E, s + 1, F, work, X.f, b);
+  dnc_fwd(SB, Bw, s, F, work, X.f, b);
+  // ---- middle products: E2 = (T11 E + T12 Bw)[h..s], B2 = (T21 E + T22 Bw)[h..s-1]
+  fft(work, F, 1.0,
+      [&](int k) { return cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k])); },
+      [&](int i, cplx v) { if (i >= h && i <= s) E2[i - h] = cscale(v, invF); }, X.f, b);
+  fft(work, F, 1.0,
+      [&](int k) { return cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k])); },
+      [&](int i, cplx v) { if (i >= h && i < s) B2[i - h] = cscale(v, invF); }, X.f, b);
+  // ---- right half
+  dnc_split(X, E2, B2, s - h, T2, b);
+  if (X.status) { X.arena = base; return; }
+  // ---- Theta = T2 T1  (degree s, s+1 coefficients; F >= s+1 so no wrap)
+  const int l2 = s - h + 1;
+  cplx* S2 = SE;  // reuse: spectra of T2 need 4F -> SE, SB, work, and a fresh F
+  cplx* S2b = X.arena;
+  X.arena = S2b + 2 * (size_t)F;
+  dnc_fwd(SE, T2, l2, F, S2b + F, X.f, b);           // T2_11
+  dnc_fwd(SB, T2 + l2, l2, F, S2b + F, X.f, b);      // T2_12
+  dnc_fwd(work, T2 + 2 * l2, l2, F, S2b + F, X.f, b);  // T2_21
+  dnc_fwd(S2b, T2 + 3 * l2, l2, F, S2b + F, X.f, b);   // T2_22
+  (void)S2;
+  cplx* scratch = S2b + F;
+  const int ld = s + 1;
+  // T11 = A11 B11 + A12 B21 ; T12 = A11 B12 + A12 B22 ; T21 = A21 B11 + A22 B21 ; T22 = A21 B12 + A22 B22
+  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(SE[k], S[k]), cmul(SB[k], S[2 * F + k])); },
+      [&](int i, cplx v) { if (i < ld) T[i] = cscale(v, invF); }, X.f, b);
+  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(SE[k], S[F + k]), cmul(SB[k], S[3 * F + k])); },
+      [&](int i, cplx v) { if (i < ld) T[ld + i] = cscale(v, invF); }, X.f, b);
+  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(work[k], S[k]), cmul(S2b[k], S[2 * F + k])); },
+      [&](int i, cplx v) { if (i < ld) T[2 * ld + i] = cscale(v, invF); }, X.f, b);
+  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(work[k], S[F + k]), cmul(S2b[k], S[3 * F + k])); },
+      [&](int i, cplx v) { if (i < ld) T[3 * ld + i] = cscale(v, invF); }, X.f, b);
+  X.arena = base;
+}
+
+// arena size (complex elements) needed by dnc_split for s steps: own
+// buffers plus the larger of the (right, i.e. larger) child's need and the
+// product stage's 2F; iterative along the chain of larger children.
+SLSE_HD size_t dnc_arena_elems(int s) {
+  int chain[48];
+  int cnt = 0;
+  for (int t = s; t > kDncLeaf && cnt < 48; t -= t / 2) chain[cnt++] = t;
+  size_t below = 0;
+  for (int i = cnt - 1; i >= 0; --i) {
+    const int t = chain[i];
+    const int h = t / 2;
+    const size_t F = (size_t)1 << ilog2(t + 1);
+    const size_t own = 4 * (size_t)(h + 1) + 7 * F + 2 * (size_t)(t - h) + 1 + 4 * (size_t)(t - h + 1);
+    below = own + (below > 2 * F ? below : 2 * F);
+  }
+  return below;
+}
+
+// Superfast factorisation: same outputs as toeplitz_factor.  T is the root
+// transfer matrix storage (4 N complex), arena from dnc_arena_elems(N-1).
+SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, cplx* arena, double* delta_out,
+                                   double* delta_tmp, cplx* SLSE_RESTRICT rho, const FftCtx& f, Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  const double c0 = c0c.re;
+  if (b.tid == 0) delta_tmp[0] = c0;
+  DncCtx X;
+  X.f = f;
+  X.arena = arena;
+  X.delta_tmp = delta_tmp;
+  X.floor_ = kPdEps * c0;
+  X.d = c0;
+  X.step = 0;
+  X.status = 0;
+  b.sync();
+  // the root window is the column itself: e = b = c (c_0 forced real)
+  // (E[0] and Bw[0] are c_0; E[j] = Bw[j] = c_j)
+  if (n > 1) dnc_split(X, c, c, n - 1, T, b);
+  b.sync();
+  if (X.status) {
+    F.status = X.status;
+    return F;
+  }
+  F.delta_last = X.d;
+  // a = Theta_11 + Theta_12 (first n coefficients), rho_i = conj(a_{n-1-i}) / conj(a_0)
+  const int ld = n;  // root Theta has s + 1 = n coefficients
+  const cplx a0 = cadd(T[0], T[ld]);
+  double part = 0.0;
+  for (int j = b.tid; j < n; j += b.nt) {
+    const cplx aj = cadd(T[n - 1 - j], T[ld + n - 1 - j]);
+    // conj(aj) / conj(a0)
+    const double den = cabs2(a0);
+    const cplx num = cmul(conjg(aj), a0);
+    rho[j] = (n == 1) ? mk(1.0, 0.0) : mk(num.re / den, num.im / den);
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+
+}  // namespace slse

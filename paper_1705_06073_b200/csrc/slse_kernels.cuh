@@ -44,7 +44,7 @@ struct SmemPlan {
   size_t bytes;
 };
 
-inline SmemPlan smem_plan(int n, int L, int nt) {
+inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false) {
   SmemPlan p;
   // one-warp solvers: keep the region small so more problems stay resident
   // (only the recursion and the 2N-point transforms are staged; the grid's
@@ -55,8 +55,8 @@ inline SmemPlan smem_plan(int n, int L, int nt) {
     budget = env ? (size_t)atoi(env) * 1024 : 48 * (size_t)n;
     if (budget < 48 * (size_t)n) budget = 48 * (size_t)n;
   }
-  const size_t rec = 48 * (size_t)n;
-  p.rec_in_smem = rec <= budget ? 1 : 0;
+  const size_t rec = dnc ? 0 : 48 * (size_t)n;
+  p.rec_in_smem = (!dnc && rec <= budget) ? 1 : 0;
   const int fftmax = L > 2 * n ? L : (1 << ilog2(2 * n));
   size_t cap_bytes = p.rec_in_smem ? rec : 0;
   // staging capacity in complex elements: the largest power-of-two transform
@@ -75,6 +75,12 @@ inline SmemPlan smem_plan(int n, int L, int nt) {
   return p;
 }
 
+
+// superfast (D&C) factorisation from this N up; SLSE_DNC_MIN overrides
+inline int dnc_min_n() {
+  const char* env = getenv("SLSE_DNC_MIN");
+  return env ? atoi(env) : 1024;
+}
 
 // ------------------------------------------------------------------ kernels
 struct OutPtrs {
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve
   f.smem = region;
   f.smem_cap = fft_cap;
   char* slab = ws + (size_t)blockIdx.x * slab_bytes;
-  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0);
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0, P.dnc != 0);
   __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) s_prob = atomicAdd(queue, 1);
@@ -249,6 +255,23 @@ __global__ void __launch_bounds__(NT) grid_kernel(const cplx* __restrict__ rho, 
 }
 
 
+
+template <int NT>
+__global__ void __launch_bounds__(NT) factor_dnc_kernel(const cplx* c, int n, cplx* rho, double* delta, double* logdet,
+                                                        int* status, cplx* scratch, size_t per_problem,
+                                                        double* dscratch, const cplx* tw, int twlog, int fft_cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  FftCtx f{tw, twlog, (cplx*)(smem_raw + kHeadBytes), fft_cap};
+  const int p = blockIdx.x;
+  cplx* T = scratch + (size_t)p * per_problem;
+  Factor F = toeplitz_factor_dnc(c + (size_t)p * n, n, T, T + 4 * (size_t)n, delta ? delta + (size_t)p * n : nullptr,
+                                 dscratch + (size_t)p * n, rho + (size_t)p * n, f, b);
+  if (threadIdx.x == 0) {
+    logdet[p] = F.logdet;
+    status[p] = F.status;
+  }
+}
 
 // Row 9 standalone, register-Stockham variant: the three length-L transforms
 // (w, rho, n*rho) live in shared memory; only their nonzero heads (the

@@ -10,6 +10,7 @@
 // block reductions that return identical bits, so control flow is uniform.
 #pragma once
 #include "slse_stats.cuh"
+#include "slse_dnc.cuh"
 #include "superlse_b200.h"
 
 #ifdef SLSE_HOST_EMU
@@ -41,6 +42,7 @@ struct SolveParams {
   int max_outer, inner_max, sweep_iters, lbfgs_mem;
   int tcap, ecap;
   double tau, conv_tol_scale, dec_tol_scale;
+  int dnc;  // 1: superfast divide-and-conquer Schur (slse_dnc.cuh), 0: Schur-Levinson
 };
 
 // Launch-uniform parameters from the C-ABI options (estimator.py:34-50).
@@ -61,12 +63,13 @@ SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   P.tau = o.tau;
   P.conv_tol_scale = o.convergence_tol_scale;
   P.dec_tol_scale = o.newton_decrement_tol_scale;
+  P.dnc = 0;
   return P;
 }
 
 // Per-CTA workspace layout (offsets in bytes from the CTA's slab).
 struct Layout {
-  size_t yhat, c, e, bg, a, rho[2], w[2], P, U, V, G0, G1, G2;
+  size_t yhat, c, e, bg, a, dT, darena, rho[2], w[2], P, U, V, G0, G1, G2;
   size_t st_q[2], st_r[2], st_u[2], st_t[2], st_v[2], mu;
   size_t dtmp, dl, q2, sg, theta, gamma, act_theta, act_gamma, st_s[2], st_x[2];
   size_t lbS, lbY, lbR, diag, g0, gnew, dir, pt, cand, cth, cga, marg, cflist_d;
@@ -76,7 +79,7 @@ struct Layout {
 
 SLSE_HD size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion_in_smem) {
+SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion_in_smem, bool dnc = false) {
   Layout l;
   size_t o = 0;
   const size_t C = 16, D = 8, I = 4;
@@ -84,7 +87,12 @@ SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion
   const size_t K = (size_t)kmax, K2 = 2 * (size_t)kmax;
   l.yhat = o; o = al(o + C * nf);
   l.c = o; o = al(o + C * n);
-  if (recursion_in_smem) {
+  l.dT = l.darena = 0;
+  if (dnc) {
+    l.e = l.bg = l.a = 0;
+    l.dT = o; o = al(o + C * 4 * (size_t)n);
+    l.darena = o; o = al(o + C * (dnc_arena_elems(n - 1) + 16));
+  } else if (recursion_in_smem) {
     l.e = l.bg = l.a = 0;
   } else {
     l.e = o; o = al(o + C * n);
@@ -214,7 +222,7 @@ struct Solver {
   const cplx* y;
   ProbOut o;
   // workspace
-  cplx *yhat, *c, *e, *bg, *a, *PP, *U, *V, *G0, *G1, *G2, *mu;
+  cplx *yhat, *c, *e, *bg, *a, *dT, *darena, *PP, *U, *V, *G0, *G1, *G2, *mu;
   double *dtmp, *dl, *q2, *sg, *theta, *gamma, *act_theta, *act_gamma;
   double *lbS, *lbY, *lbR, *diag, *g0, *gnew, *dir, *pt, *cand, *cth, *cga, *marg;
   int *z, *act_slot, *cidx, *csort;
@@ -243,6 +251,8 @@ struct Solver {
     } else {
       e = (cplx*)(slab + lay.e); bg = (cplx*)(slab + lay.bg); a = (cplx*)(slab + lay.a);
     }
+    dT = (cplx*)(slab + lay.dT);
+    darena = (cplx*)(slab + lay.darena);
     for (int i = 0; i < 2; ++i) {
       bun[i].rho = (cplx*)(slab + lay.rho[i]);
       bun[i].w = (cplx*)(slab + lay.w[i]);
@@ -330,7 +340,8 @@ struct Solver {
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
     steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
-    Factor F = toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
+    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b)
+                     : toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
     if (F.status != kOk) return F.status;
     B.delta_last = F.delta_last;
     B.logdet = F.logdet;

@@ -143,43 +143,27 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
       b.sync();  // every lane has read e_{m+2}, B_1 before any write below
     }
     const int cnt = n - 1 - m;  // pairs j = 0..cnt-1
-    // batches of 4 independent pairs per thread: all loads issue before the
-    // dependent multiply-adds (ILP for the one-warp solver)
-    for (int j0 = b.tid; j0 < cnt; j0 += 4 * b.nt) {
-      cplx ej[4], bj[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u * b.nt;
-        if (j < cnt) { ej[u] = e[j + m + 1]; bj[u] = B[j]; }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u * b.nt;
-        if (j < cnt) {
-          if (j > 0) e[j + m + 1] = cadd(ej[u], cmul(k, bj[u]));
-          B[j] = cadd(bj[u], cmul(kc, ej[u]));
-        }
-      }
+    for (int j = b.tid; j < cnt; j += b.nt) {
+      const cplx ej = e[j + m + 1];
+      const cplx bj = B[j];
+      if (j > 0) e[j + m + 1] = cadd(ej, cmul(k, bj));
+      B[j] = cadd(bj, cmul(kc, ej));
     }
     // predictor: a_i' = a_i + k conj(a_{m+1-i}), i = 1..m+1 (a_{m+1} = 0 before)
     const int top = m + 1;
     const int npair = (top + 1) / 2;
-    if (b.tid == 0) a[top] = cmul(k, conjg(a[0]));
-    for (int i0 = 1 + b.tid; i0 <= npair; i0 += 4 * b.nt) {
-      cplx ai[4], aj[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * b.nt;
-        if (i <= npair) { ai[u] = a[i]; aj[u] = a[top - i]; }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * b.nt, jj = top - i;
+    for (int i = b.tid; i <= npair; i += b.nt) {
+      if (i == 0) {
+        a[top] = cmul(k, conjg(a[0]));
+      } else {
+        const int jj = top - i;
         if (i < jj) {
-          a[i] = cadd(ai[u], cmul(k, conjg(aj[u])));
-          a[jj] = cadd(aj[u], cmul(k, conjg(ai[u])));
+          const cplx ai = a[i], aj = a[jj];
+          a[i] = cadd(ai, cmul(k, conjg(aj)));
+          a[jj] = cadd(aj, cmul(k, conjg(ai)));
         } else if (i == jj) {
-          a[i] = cadd(ai[u], cmul(k, conjg(ai[u])));
+          const cplx ai = a[i];
+          a[i] = cadd(ai, cmul(k, conjg(ai)));
         }
       }
     }

@@ -41,9 +41,14 @@ def cov_column(theta, gamma, kcount, beta, n):
     return c
 
 
-def toeplitz_factor(c, with_delta=True, raise_on_error=False):
+METHODS = {"auto": 0, "levinson": 1, "schur": 2}
+
+
+def toeplitz_factor(c, with_delta=True, raise_on_error=False, method="auto"):
     """Rows 2-4: (rho, delta, logdet, status) of the Hermitian Toeplitz
-    matrices with first columns c (B, N) (toeplitz.decompose, :263-276)."""
+    matrices with first columns c (B, N) (toeplitz.decompose, :263-276).
+    method: "levinson" (Schur-Levinson, O(N^2)), "schur" (superfast
+    divide-and-conquer, O(N log^2 N)) or "auto" (superfast from N >= 1024)."""
     lib = _native.load()
     _c128(c)
     B, n = c.shape
@@ -51,8 +56,8 @@ def toeplitz_factor(c, with_delta=True, raise_on_error=False):
     delta = torch.empty((B, n), dtype=torch.float64, device=c.device) if with_delta else None
     logdet = torch.empty(B, dtype=torch.float64, device=c.device)
     status = torch.empty(B, dtype=torch.int32, device=c.device)
-    _native.check(lib.slse_toeplitz_factor(_p(c), n, B, _p(rho), _p(delta), _p(logdet), _p(status), _stream()),
-                  "slse_toeplitz_factor")
+    _native.check(lib.slse_toeplitz_factor_ex(_p(c), n, B, _p(rho), _p(delta), _p(logdet), _p(status),
+                                              METHODS[method], _stream()), "slse_toeplitz_factor_ex")
     if raise_on_error and bool((status != 0).any()):
         raise NotPositiveDefinite("Toeplitz factorisation hit a non-positive pivot")
     return rho, delta, logdet, status

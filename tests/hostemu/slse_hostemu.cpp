@@ -8,9 +8,11 @@
 // is the nvcc-built libsuperlse_b200.so and fails loudly without it.
 #define SLSE_HOST_EMU 1
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "slse_solver.cuh"
+#include "slse_dnc.cuh"
 
 using namespace slse;
 
@@ -27,11 +29,13 @@ static std::vector<cplx> make_twiddles(int lg) {
 
 extern "C" int emu_estimate_batch(const double* y, int N, int B, const slse_options* opts, const slse_outputs* out) {
   SolveParams P = make_params(N, *opts);
+  const char* dm = getenv("SLSE_DNC_MIN");
+  P.dnc = (dm && N >= atoi(dm)) ? 1 : 0;
   const int fmax = P.L > 2 * N ? P.L : 2 * N;
   std::vector<cplx> tw = make_twiddles(ilog2(fmax));
   CfTable cf;
   cf_build(cf, N);
-  Layout lay = make_layout(N, P.L, P.kmax, P.lbfgs_mem, false);
+  Layout lay = make_layout(N, P.L, P.kmax, P.lbfgs_mem, false, P.dnc != 0);
   std::vector<char> slab(lay.total + 256);
   char* base = (char*)(((uintptr_t)slab.data() + 255) & ~(uintptr_t)255);
   std::vector<double> red(2 * 32 * 16);
@@ -166,4 +170,20 @@ extern "C" int emu_grid_pruned(const double* w, const double* rho, int n, double
   C(6) C(7) C(8) C(9) C(10) C(11) C(12)
 #undef C
   return -1;
+}
+
+#include "slse_dnc.cuh"
+// superfast D&C factorisation
+extern "C" int emu_factor_dnc(const double* c, int n, double* rho, double* delta, double* logdet) {
+  const int F = 1 << ilog2(2 * n);
+  std::vector<cplx> tw = make_twiddles(ilog2(F) > 4 ? ilog2(F) : 4);
+  std::vector<cplx> region(sk_len(F));
+  std::vector<double> red(64);
+  Blk b{0, 1, red.data(), 0};
+  FftCtx f{tw.data(), ilog2(F) > 4 ? ilog2(F) : 4, region.data(), (int)region.size()};
+  std::vector<cplx> T(4 * (size_t)n + 4), arena(dnc_arena_elems(n - 1) + 16);
+  std::vector<double> dt(n);
+  Factor Fa = toeplitz_factor_dnc((const cplx*)c, n, T.data(), arena.data(), delta, dt.data(), (cplx*)rho, f, b);
+  *logdet = Fa.logdet;
+  return Fa.status;
 }

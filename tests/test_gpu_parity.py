@@ -25,8 +25,9 @@ CALL_CASES = [(cfg, b, st) for cfg, nb in ((1, 2), (2, 2), (3, 1)) for b in rang
               for st in ("empty", "truth", "final")]
 
 
+@pytest.mark.parametrize("method", ["levinson", "schur"])
 @pytest.mark.parametrize("cfg,b,state", CALL_CASES)
-def test_per_call_against_reference(cfg, b, state):
+def test_per_call_against_reference(cfg, b, state, method):
     from paper_1705_06073_b200 import ops
 
     z = load(cfg)
@@ -42,7 +43,7 @@ def test_per_call_against_reference(cfg, b, state):
     kc = _dev(np.array([k]), np.int32)
     c = ops.cov_column(tht, gat, kc, _dev(np.array([be])), n)
     assert rel(c.cpu().numpy()[0], z[p + "c"]) < 1e-12
-    rho, delta, logdet, status = ops.toeplitz_factor(c)
+    rho, delta, logdet, status = ops.toeplitz_factor(c, method=method)
     assert int(status.item()) == 0
     assert rel(rho.cpu().numpy()[0], z[p + "rho"]) < CALL_TOL
     assert rel(delta.cpu().numpy()[0], z[p + "delta"]) < CALL_TOL
@@ -153,3 +154,18 @@ def test_pure_noise_and_zero_signal():
     # all-zero data: beta0 = 0 -> c_0 = 0 -> NotPositiveDefinite (toeplitz.py:55-57)
     with pytest.raises(NotPositiveDefinite):
         estimate(Observation.complete(np.zeros(32, complex)), EstimatorOptions(grid_factor=4))
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_trajectories_superfast_forced(cfg, monkeypatch):
+    """Golden histories with the superfast (divide-and-conquer) factorisation
+    forced on inside the solver kernel."""
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
+
+    monkeypatch.setenv("SLSE_DNC_MIN", "64")
+    z = load(cfg)
+    count = int(z["count"])
+    Y = np.stack([z[f"p{b}_y"] for b in range(count)])
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    for b in range(count):
+        _check_traj(res[b], z, f"p{b}_")

@@ -117,3 +117,37 @@ def test_emulated_stockham_fft(n):
         z = x.copy()
         lib.emu_fft_stockham(ctypes.c_void_p(z.ctypes.data), cnt, n, 1)
         assert rel(z, n * np.fft.ifft(x, axis=1)) < 1e-14
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_emulated_superfast_factor(cfg):
+    """Divide-and-conquer (superfast) Schur vs the oracle's Levinson on the
+    config-shaped covariance at the true state (toeplitz.py:230-260 role)."""
+    import ctypes
+
+    lib = H.build()
+    lib.emu_factor_dnc.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    y, tr = O.generate_problem(1, cfg, 0)
+    n = y.size
+    c = O.cov_column(tr["thetas"], np.abs(tr["alphas"]) ** 2, tr["beta"], n)
+    r0, d0 = O.levinson(c)
+    rho = np.zeros(n, complex)
+    dl = np.zeros(n)
+    ld = np.zeros(1)
+    assert lib.emu_factor_dnc(c.ctypes.data, n, rho.ctypes.data, dl.ctypes.data, ld.ctypes.data) == 0
+    assert rel(rho, r0) < CALL_TOL and rel(dl, d0) < CALL_TOL
+    assert abs(ld[0] - np.sum(np.log(d0))) < 1e-9 * max(1.0, abs(np.sum(np.log(d0))))
+
+
+@pytest.mark.parametrize("cfg,b", [(1, 0), (2, 0), (2, 2), (3, 0)])
+def test_emulated_trajectory_superfast(cfg, b, monkeypatch):
+    """Whole estimator with the superfast factorisation forced on."""
+    monkeypatch.setenv("SLSE_DNC_MIN", "32")
+    z = load(cfg)
+    p = f"p{b}_"
+    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4))[0]
+    assert r.k_hat == int(z[p + "k_hat"])
+    assert np.array_equal(np.array([STAGES.index(s) for s in r.trace_stages]), z[p + "stages"])
+    assert np.array_equal(encode_events(r.events), z[p + "events"])
+    assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
+    assert rel(r.alpha_hat[0], z[p + "alpha_hat"]) < AMP_TOL
