@@ -158,64 +158,104 @@ SLSE_D void dnc_fwd(cplx* dst, const cplx* src, int len, int F, cplx* work, cons
       [&](int i, cplx v) { dst[i] = v; }, f, b);
 }
 
-SLSE_NI void dnc_split(DncCtx& X, const cplx* E, const cplx* Bw, int s, cplx* T, Blk& b) {
-  if (X.status) return;
-  if (s <= kDncLeaf) {
-    dnc_leaf(X, E + 1, Bw, s, T, b);
-    return;
+// One internal node's buffers, all carved from `base` (see dnc_arena_elems).
+struct DncNode {
+  int h, F;
+  cplx *T1, *S, *SE, *SB, *work, *E2, *B2, *T2, *above;
+};
+
+SLSE_D DncNode dnc_node(cplx* base, int s) {
+  DncNode d;
+  d.h = s / 2;
+  d.F = 1 << ilog2(s + 1);
+  d.T1 = base;                         // 4 (h+1)
+  d.S = d.T1 + 4 * (d.h + 1);          // 4 F : spectra of T1 (kept for the product)
+  d.SE = d.S + 4 * (size_t)d.F;        // F
+  d.SB = d.SE + d.F;                   // F
+  d.work = d.SB + d.F;                 // F   (global fallback buffer of the FFT)
+  d.E2 = d.work + d.F;                 // s - h + 1
+  d.B2 = d.E2 + (s - d.h + 1);         // s - h
+  d.T2 = d.B2 + (s - d.h);             // 4 (s - h + 1)
+  d.above = d.T2 + 4 * (s - d.h + 1);  // children / product scratch start here
+  return d;
+}
+
+struct DncFrame {
+  const cplx* E;
+  const cplx* Bw;
+  cplx* T;
+  cplx* base;
+  int s;
+  int phase;
+};
+
+// Transfer matrix of s steps (iterative post-order traversal; an explicit
+// frame stack instead of device recursion keeps the stack statically sized).
+SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx* T0, Blk& b) {
+  DncFrame fr[40];
+  int sp = 0;
+  fr[sp++] = DncFrame{E0, Bw0, T0, X.arena, s0, 0};
+  while (sp > 0 && !X.status) {
+    DncFrame& cf = fr[sp - 1];
+    const int s = cf.s;
+    if (s <= kDncLeaf) {
+      dnc_leaf(X, cf.E + 1, cf.Bw, s, cf.T, b);
+      --sp;
+      continue;
+    }
+    const DncNode d = dnc_node(cf.base, s);
+    const int h = d.h, F = d.F;
+    const double invF = 1.0 / (double)F;
+    if (cf.phase == 0) {  // descend into the left half
+      cf.phase = 1;
+      fr[sp++] = DncFrame{cf.E, cf.Bw, d.T1, d.above, h, 0};
+      continue;
+    }
+    if (cf.phase == 1) {  // left done: middle products give the right window
+      const int l1 = h + 1;
+      for (int q = 0; q < 4; ++q) dnc_fwd(d.S + (size_t)q * F, d.T1 + q * l1, l1, F, d.work, X.f, b);
+      dnc_fwd(d.SE, cf.E, s + 1, F, d.work, X.f, b);
+      dnc_fwd(d.SB, cf.Bw, s, F, d.work, X.f, b);
+      const cplx* S = d.S;
+      const cplx* SE = d.SE;
+      const cplx* SB = d.SB;
+      cplx* E2 = d.E2;
+      cplx* B2 = d.B2;
+      // E2 = (T11 E + T12 Bw)[h..s], B2 = (T21 E + T22 Bw)[h..s-1]
+      fft(d.work, F, 1.0, [&](int k) { return cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k])); },
+          [&](int i, cplx v) { if (i >= h && i <= s) E2[i - h] = cscale(v, invF); }, X.f, b);
+      fft(d.work, F, 1.0, [&](int k) { return cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k])); },
+          [&](int i, cplx v) { if (i >= h && i < s) B2[i - h] = cscale(v, invF); }, X.f, b);
+      cf.phase = 2;
+      fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
+      continue;
+    }
+    // phase 2: Theta = T2 T1 (degree s; F >= s + 1 so no wrap)
+    {
+      const int l2 = s - h + 1;
+      cplx* A11 = d.SE;  // spectra of T2 reuse SE, SB, work and one fresh F
+      cplx* A12 = d.SB;
+      cplx* A21 = d.work;
+      cplx* A22 = d.above;
+      cplx* scratch = d.above + F;
+      dnc_fwd(A11, d.T2, l2, F, scratch, X.f, b);
+      dnc_fwd(A12, d.T2 + l2, l2, F, scratch, X.f, b);
+      dnc_fwd(A21, d.T2 + 2 * l2, l2, F, scratch, X.f, b);
+      dnc_fwd(A22, d.T2 + 3 * l2, l2, F, scratch, X.f, b);
+      const cplx* S = d.S;
+      cplx* T = cf.T;
+      const int ld = s + 1;
+      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A11[k], S[k]), cmul(A12[k], S[2 * F + k])); },
+          [&](int i, cplx v) { if (i < ld) T[i] = cscale(v, invF); }, X.f, b);
+      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A11[k], S[F + k]), cmul(A12[k], S[3 * F + k])); },
+          [&](int i, cplx v) { if (i < ld) T[ld + i] = cscale(v, invF); }, X.f, b);
+      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A21[k], S[k]), cmul(A22[k], S[2 * F + k])); },
+          [&](int i, cplx v) { if (i < ld) T[2 * ld + i] = cscale(v, invF); }, X.f, b);
+      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A21[k], S[F + k]), cmul(A22[k], S[3 * F + k])); },
+          [&](int i, cplx v) { if (i < ld) T[3 * ld + i] = cscale(v, invF); }, X.f, b);
+      --sp;
+    }
   }
-  const int h = s / 2;
-  const int F = 1 << ilog2(s + 1);
-  const double invF = 1.0 / (double)F;
-  cplx* base = X.arena;
-  cplx* T1 = base;                       // 4 (h+1)
-  cplx* S = T1 + 4 * (h + 1);            // 4 F : spectra of T1 (kept for the product)
-  cplx* SE = S + 4 * (size_t)F;          // F
-  cplx* SB = SE + F;                     // F
-  cplx* work = SB + F;                   // F  (global fallback buffer)
-  cplx* E2 = work + F;                   // s - h + 1
-  cplx* B2 = E2 + (s - h + 1);           // s - h
-  cplx* T2 = B2 + (s - h);               // 4 (s - h + 1)
-  X.arena = T2 + 4 * (s - h + 1);
-  // ---- left half
-  dnc_split(X, E, Bw, h, T1, b);
-  if (X.status) { X.arena = base; return; }
-  const int l1 = h + 1;
-  for (int q = 0; q < 4; ++q) dnc_fwd(S + (size_t)q * F, T1 + q * l1, l1, F, work, X.f, b);
-  dnc_fwd(SE, E, s + 1, F, work, X.f, b);
-  dnc_fwd(SB, Bw, s, F, work, X.f, b);
-  // ---- middle products: E2 = (T11 E + T12 Bw)[h..s], B2 = (T21 E + T22 Bw)[h..s-1]
-  fft(work, F, 1.0,
-      [&](int k) { return cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k])); },
-      [&](int i, cplx v) { if (i >= h && i <= s) E2[i - h] = cscale(v, invF); }, X.f, b);
-  fft(work, F, 1.0,
-      [&](int k) { return cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k])); },
-      [&](int i, cplx v) { if (i >= h && i < s) B2[i - h] = cscale(v, invF); }, X.f, b);
-  // ---- right half
-  dnc_split(X, E2, B2, s - h, T2, b);
-  if (X.status) { X.arena = base; return; }
-  // ---- Theta = T2 T1  (degree s, s+1 coefficients; F >= s+1 so no wrap)
-  const int l2 = s - h + 1;
-  cplx* S2 = SE;  // reuse: spectra of T2 need 4F -> SE, SB, work, and a fresh F
-  cplx* S2b = X.arena;
-  X.arena = S2b + 2 * (size_t)F;
-  dnc_fwd(SE, T2, l2, F, S2b + F, X.f, b);           // T2_11
-  dnc_fwd(SB, T2 + l2, l2, F, S2b + F, X.f, b);      // T2_12
-  dnc_fwd(work, T2 + 2 * l2, l2, F, S2b + F, X.f, b);  // T2_21
-  dnc_fwd(S2b, T2 + 3 * l2, l2, F, S2b + F, X.f, b);   // T2_22
-  (void)S2;
-  cplx* scratch = S2b + F;
-  const int ld = s + 1;
-  // T11 = A11 B11 + A12 B21 ; T12 = A11 B12 + A12 B22 ; T21 = A21 B11 + A22 B21 ; T22 = A21 B12 + A22 B22
-  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(SE[k], S[k]), cmul(SB[k], S[2 * F + k])); },
-      [&](int i, cplx v) { if (i < ld) T[i] = cscale(v, invF); }, X.f, b);
-  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(SE[k], S[F + k]), cmul(SB[k], S[3 * F + k])); },
-      [&](int i, cplx v) { if (i < ld) T[ld + i] = cscale(v, invF); }, X.f, b);
-  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(work[k], S[k]), cmul(S2b[k], S[2 * F + k])); },
-      [&](int i, cplx v) { if (i < ld) T[2 * ld + i] = cscale(v, invF); }, X.f, b);
-  fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(work[k], S[F + k]), cmul(S2b[k], S[3 * F + k])); },
-      [&](int i, cplx v) { if (i < ld) T[3 * ld + i] = cscale(v, invF); }, X.f, b);
-  X.arena = base;
 }
 
 // arena size (complex elements) needed by dnc_split for s steps: own

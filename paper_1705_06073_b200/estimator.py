@@ -142,7 +142,8 @@ def decode_events(rows: np.ndarray):
     ("deactivate", [slots])] (the encoding of tests/golden/make_golden.py)."""
     out = []
     cur = []
-    for kind, slot, idx in rows:
+    for row in rows:
+        kind, slot, idx = row
         if kind == -1:
             if cur:
                 k0 = cur[0][0]
@@ -158,44 +159,67 @@ def decode_events(rows: np.ndarray):
     return out
 
 
+_STAGE_ARR = np.array(STAGE_NAMES, dtype=object)
+
+
+def unpack_all(h: dict):
+    """LseResult per problem from host (numpy) copies of the batch outputs.
+    Per-batch vectorised preparation; per-problem arrays are views."""
+    B = h["k_hat"].shape[0]
+    khat = h["k_hat"].tolist()
+    ntr = h["n_trace"].tolist()
+    nev = h["n_events"].tolist()
+    flags = h["flags"].tolist()
+    status = h["status"].tolist()
+    iters = h["iterations"].tolist()
+    beta = h["beta"].tolist()
+    zeta = h["zeta"].tolist()
+    alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]  # (B, K)
+    names = _STAGE_ARR[np.clip(h["stage"], 0, len(STAGE_NAMES) - 1)]
+    secs = h["stage_seconds"].tolist()
+    ctr = h["counters"].tolist()
+    theta, gamma, slot, trace, trace_k, events = (h["theta"], h["gamma"], h["slot"], h["trace"], h["trace_k"],
+                                                  h["events"])
+    out = []
+    for b in range(B):
+        k, nt, fl = khat[b], ntr[b], flags[b]
+        warns = []
+        if fl & (FLAG_KMAX_CAP | FLAG_TRACE_FULL | FLAG_EVENTS_FULL):
+            if fl & FLAG_KMAX_CAP:
+                warns.append("activation loop hit the K_max cap")
+            if fl & FLAG_TRACE_FULL:
+                warns.append("objective trace truncated (trace capacity)")
+            if fl & FLAG_EVENTS_FULL:
+                warns.append("active-set history truncated (event capacity)")
+        times = dict(zip(TIMER_NAMES, secs[b]))
+        times["per_iteration"] = []
+        c = ctr[b]
+        out.append(LseResult(
+            k_hat=k,
+            theta_hat=theta[b, :k],
+            alpha_hat=alpha[b, :k].reshape(1, k),
+            beta_hat=beta[b],
+            gamma_hat=gamma[b, :k],
+            zeta_hat=zeta[b],
+            objective_trace=trace[b, :nt],
+            iterations=iters[b],
+            wall_time_per_stage=times,
+            converged=bool(fl & FLAG_CONVERGED),
+            trace_stages=names[b, :nt].tolist(),
+            warnings=warns,
+            events=decode_events(events[b, :nev[b]].tolist()),
+            trace_k=trace_k[b, :nt],
+            slots=slot[b, :k],
+            counters=dict(builds=c[0], grids=c[1], stats=c[2], line_search_trials=c[3]),
+            status=status[b],
+        ))
+    return out
+
+
 def unpack(h: dict, b: int) -> LseResult:
-    """Build the LseResult of problem b from host (numpy) copies."""
-    k = int(h["k_hat"][b])
-    nt = int(h["n_trace"][b])
-    ne = int(h["n_events"][b])
-    flags = int(h["flags"][b])
-    alpha = h["alpha"][b, :k, 0] + 1j * h["alpha"][b, :k, 1]
-    warns = []
-    if flags & FLAG_KMAX_CAP:
-        warns.append("activation loop hit the K_max cap")
-    if flags & FLAG_TRACE_FULL:
-        warns.append("objective trace truncated (trace capacity)")
-    if flags & FLAG_EVENTS_FULL:
-        warns.append("active-set history truncated (event capacity)")
-    secs = h["stage_seconds"][b]
-    times = {name: float(secs[i]) for i, name in enumerate(TIMER_NAMES)}
-    times["per_iteration"] = []
-    ctr = h["counters"][b]
-    stages = h["stage"][b, :nt]
-    return LseResult(
-        k_hat=k,
-        theta_hat=h["theta"][b, :k].copy(),
-        alpha_hat=alpha.reshape(1, k).astype(np.complex128),
-        beta_hat=float(h["beta"][b]),
-        gamma_hat=h["gamma"][b, :k].copy(),
-        zeta_hat=float(h["zeta"][b]),
-        objective_trace=h["trace"][b, :nt].copy(),
-        iterations=int(h["iterations"][b]),
-        wall_time_per_stage=times,
-        converged=bool(flags & FLAG_CONVERGED),
-        trace_stages=[STAGE_NAMES[int(s)] for s in stages],
-        warnings=warns,
-        events=decode_events(h["events"][b, :ne]),
-        trace_k=h["trace_k"][b, :nt].copy(),
-        slots=h["slot"][b, :k].copy(),
-        counters=dict(builds=int(ctr[0]), grids=int(ctr[1]), stats=int(ctr[2]), line_search_trials=int(ctr[3])),
-        status=int(h["status"][b]),
-    )
+    """LseResult of problem b alone (see unpack_all)."""
+    sub = {k: v[b:b + 1] for k, v in h.items()}
+    return unpack_all(sub)[0]
 
 
 # ------------------------------------------------------------------ GPU path
@@ -272,8 +296,7 @@ class BatchSolver:
         return h
 
     def results(self):
-        h = self.host_outputs()
-        return [unpack(h, b) for b in range(self.batch)]
+        return unpack_all(self.host_outputs())
 
 
 def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False):
