@@ -101,19 +101,6 @@ cudaError_t set_smem(KernelT kernel, size_t bytes) {
 }  // namespace
 
 namespace {
-// host mirror of slse::stockham_ok (register caps per radix)
-bool stockham_fits(int count, int n, int nt) {
-  const int caps[4][2] = {{16, 1}, {8, 2}, {4, 4}, {2, 8}};
-  for (int Ns = 1; Ns < n;) {
-    int R = 0;
-    for (int q = 0; q < 4 && !R; ++q)
-      if (caps[q][0] <= n / Ns && count * (n / caps[q][0]) <= caps[q][1] * nt) R = caps[q][0];
-    if (!R) return false;
-    Ns *= R;
-  }
-  return true;
-}
-
 // threads per solver CTA: small N run one warp per problem (no block-wide
 // barriers; many problems resident per SM); SLSE_SOLVER_NT overrides.
 int solver_threads(int n) {
