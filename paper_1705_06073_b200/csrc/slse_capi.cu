@@ -204,8 +204,9 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
     if (rc) return rc;
     const int nt = N <= 2048 ? 256 : 1024;
     int cap = 1;
-    while (16 * (size_t)(cap * 2) <= kRegionBudget) cap *= 2;
+    while (16 * (size_t)sk_len(cap * 2) <= kRegionBudget) cap *= 2;
     if (cap > F) cap = F;
+    cap = sk_len(cap);  // staging capacity in the skewed layout
     const size_t smem = kHeadBytes + 16 * (size_t)cap;
     const size_t per = 4 * (size_t)N + dnc_arena_elems(N - 1) + 16;
     cplx* scratch = nullptr;

@@ -294,6 +294,7 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   if (b.tid == 0) delta_tmp[0] = c0;
   DncCtx X;
   X.f = f;
+  X.f.stockham = 1;  // radix-16 register passes for the product transforms
   X.arena = arena;
   X.delta_tmp = delta_tmp;
   X.floor_ = kPdEps * c0;

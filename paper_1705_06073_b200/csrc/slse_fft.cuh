@@ -24,6 +24,7 @@ struct FftCtx {
   int twlog;        // log2(TW)
   cplx* smem;       // shared scratch for staging
   int smem_cap;     // capacity in complex elements
+  int stockham = 0; // 1: prefer the register Stockham passes when they fit
 };
 
 SLSE_HD int ilog2(int n) {
@@ -57,32 +58,38 @@ SLSE_D cplx twid(const FftCtx& f, int k, int lg, double sign) {
 }
 
 // In-place DIT passes on bit-reversed data x[0..n).
-SLSE_NI void fft_passes(cplx* x, int n, double sign, const FftCtx& f, Blk& b) {
+SLSE_D void fft_barrier() {
+#ifndef SLSE_HOST_EMU
+  __syncthreads();
+#endif
+}
+
+SLSE_NI void fft_passes_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
   const int p = ilog2(n);
   int lgh = 0;  // log2 of current half-span
   if (p & 1) {
-    for (int t = b.tid; t < (n >> 1); t += b.nt) {
+    for (int t = tid; t < (n >> 1); t += nt) {
       cplx x0 = x[2 * t], x1 = x[2 * t + 1];
       x[2 * t] = cadd(x0, x1);
       x[2 * t + 1] = csub(x0, x1);
     }
-    b.sync();
+    fft_barrier();
     lgh = 1;
   }
   for (; lgh + 2 <= p; lgh += 2) {
     const int h = 1 << lgh;
-    for (int t = b.tid; t < (n >> 2); t += b.nt) {
+    for (int t = tid; t < (n >> 2); t += nt) {
       const int pos = t & (h - 1);
       const int base = ((t >> lgh) << (lgh + 2)) + pos;
       cplx x0 = x[base], x1 = x[base + h], x2 = x[base + 2 * h], x3 = x[base + 3 * h];
       // stage span 2h
-      cplx w1 = twid(f, pos, lgh + 1, sign);
+      cplx w1 = twid_tab(tw, twlog, pos, lgh + 1, sign);
       cplx t1 = cmul(w1, x1);
       cplx a0 = cadd(x0, t1), a1 = csub(x0, t1);
       cplx t3 = cmul(w1, x3);
       cplx a2 = cadd(x2, t3), a3 = csub(x2, t3);
       // stage span 4h: W^{pos} and W^{pos+h} = (-+ i) W^{pos}
-      cplx w2 = twid(f, pos, lgh + 2, sign);
+      cplx w2 = twid_tab(tw, twlog, pos, lgh + 2, sign);
       cplx u2 = cmul(w2, a2);
       cplx u3 = cmul(w2, a3);
       u3 = (sign < 0) ? mk(u3.im, -u3.re) : mk(-u3.im, u3.re);
@@ -91,8 +98,12 @@ SLSE_NI void fft_passes(cplx* x, int n, double sign, const FftCtx& f, Blk& b) {
       x[base + h] = cadd(a1, u3);
       x[base + 3 * h] = csub(a1, u3);
     }
-    b.sync();
+    fft_barrier();
   }
+}
+
+SLSE_D void fft_passes(cplx* x, int n, double sign, const FftCtx& f, Blk& b) {
+  fft_passes_v(x, n, sign, f.tw, f.twlog, b.tid, b.nt);
 }
 
 // out = FFT_n(load) ; store(i, out_i).  `work` (global, n elements) is used
@@ -132,7 +143,7 @@ SLSE_NI void fft_inplace_dit(cplx* data, int n, double sign, const FftCtx& f, Bl
       }
     }
     b.sync();
-    fft_passes(data, n, sign, f, b);
+    fft_passes_v(data, n, sign, f.tw, f.twlog, b.tid, b.nt);
   }
 }
 
@@ -255,8 +266,30 @@ SLSE_D void stockham_pass_inl(cplx* x, int count, int n, int Ns, double sign, co
       for (int r = 0; r < R; ++r) v[i][r] = xc[sk(j + r * per)];
       if (Ns > 1) {
         const int kk = j & (Ns - 1);
+        if constexpr (R >= 8) {
+          // two table loads (W^kk, W^4kk); the rest by short products
+          const cplx w1 = twid_tab(tw, twlog, kk, lg, sign);
+          const cplx w4 = twid_tab(tw, twlog, 4 * kk, lg, sign);
+          const cplx w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+          cplx wq = w4;
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twid_tab(tw, twlog, kk * r, lg, sign));
+          for (int q = 0; q < R / 4; ++q) {
+            if (q >= 2) wq = cmul(wq, w4);
+            if (q == 0) {
+              v[i][1] = cmul(v[i][1], w1);
+              v[i][2] = cmul(v[i][2], w2);
+              v[i][3] = cmul(v[i][3], w3);
+            } else {
+              v[i][4 * q] = cmul(v[i][4 * q], wq);
+              v[i][4 * q + 1] = cmul(v[i][4 * q + 1], cmul(wq, w1));
+              v[i][4 * q + 2] = cmul(v[i][4 * q + 2], cmul(wq, w2));
+              v[i][4 * q + 3] = cmul(v[i][4 * q + 3], cmul(wq, w3));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twid_tab(tw, twlog, kk * r, lg, sign));
+        }
       }
       dft_dif<R>(v[i], sign);
     }
@@ -354,33 +387,58 @@ SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& 
 #ifndef SLSE_SOLVER_STOCKHAM
 #define SLSE_SOLVER_STOCKHAM 0
 #endif
+// Stockham (by value: table, thread index/count) on skewed shared staging
+SLSE_NI void fft_stockham_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+  for (int Ns = 1; Ns < n;) {
+    const int R = stockham_radix(n / Ns, 1, n, nt);
+    switch (R) {
+      case 16: stockham_pass_inl<16, 1>(x, 1, n, Ns, sign, tw, twlog, tid, nt); break;
+      case 8: stockham_pass_inl<8, 2>(x, 1, n, Ns, sign, tw, twlog, tid, nt); break;
+      case 4: stockham_pass_inl<4, 4>(x, 1, n, Ns, sign, tw, twlog, tid, nt); break;
+      default: stockham_pass_inl<2, 8>(x, 1, n, Ns, sign, tw, twlog, tid, nt); break;
+    }
+    Ns *= R;
+  }
+}
+
+SLSE_D bool use_stockham(const FftCtx& f, int n, int nt) {
+  return (SLSE_SOLVER_STOCKHAM || f.stockham) && n >= 4 && sk_len(n) <= f.smem_cap && stockham_ok(1, n, nt);
+}
+
 template <class Load, class Store>
 SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
-  if (SLSE_SOLVER_STOCKHAM && sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
+  const int tid = b.tid, nt = b.nt;
+  if (use_stockham(f, n, nt)) {
     cplx* x = f.smem;
-    for (int i = b.tid; i < n; i += b.nt) x[sk(i)] = ld(i);
-    b.sync();
-    fft_stockham(x, 1, n, sign, f, b);
-    for (int i = b.tid; i < n; i += b.nt) st(i, x[sk(i)]);
-    b.sync();
+    for (int i = tid; i < n; i += nt) x[sk(i)] = ld(i);
+    fft_barrier();
+    fft_stockham_v(x, n, sign, f.tw, f.twlog, tid, nt);
+    for (int i = tid; i < n; i += nt) st(i, x[sk(i)]);
+    fft_barrier();
   } else {
-    fft_dit(work, n, sign, ld, st, f, b);
+    const int p = ilog2(n);
+    cplx* x = (n <= f.smem_cap) ? f.smem : work;
+    for (int i = tid; i < n; i += nt) x[brev_bits((unsigned)i, p)] = ld(i);
+    fft_barrier();
+    fft_passes_v(x, n, sign, f.tw, f.twlog, tid, nt);
+    for (int i = tid; i < n; i += nt) st(i, x[i]);
+    fft_barrier();
   }
 }
 
 SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {
-  if (SLSE_SOLVER_STOCKHAM && sk_len(n) <= f.smem_cap && n >= 4 && stockham_ok(1, n, b.nt)) {
+  const int tid = b.tid, nt = b.nt;
+  if (use_stockham(f, n, nt)) {
     cplx* x = f.smem;
-    for (int i = b.tid; i < n; i += b.nt) x[sk(i)] = data[i];
-    b.sync();
-    fft_stockham(x, 1, n, sign, f, b);
-    for (int i = b.tid; i < n; i += b.nt) data[i] = x[sk(i)];
-    b.sync();
+    for (int i = tid; i < n; i += nt) x[sk(i)] = data[i];
+    fft_barrier();
+    fft_stockham_v(x, n, sign, f.tw, f.twlog, tid, nt);
+    for (int i = tid; i < n; i += nt) data[i] = x[sk(i)];
+    fft_barrier();
   } else {
     fft_inplace_dit(data, n, sign, f, b);
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // Pruned first pass for zero-padded inputs: only the first NZ of the R
