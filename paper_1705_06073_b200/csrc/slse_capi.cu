@@ -118,6 +118,7 @@ int solver_threads(int n) {
 int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
   P.dnc = n >= dnc_min_n() ? 1 : 0;
+  P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
   const int nt = solver_threads(n);
   SmemPlan plan = smem_plan(n, P.L, nt, P.dnc != 0);
   int occ = 1;
@@ -317,6 +318,21 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
     while (q < 3 && (N << (q + 1)) <= L) ++q;  // input support n <= L / 2^q
 #define SLSE_GRID_Q(NTV, LGV, QV)                                                                          \
   case QV: {                                                                                               \
+    if (getenv("SLSE_GRID_NOPERSIST") == nullptr && (N % 1) == 0) {                                        \
+      const size_t psmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV) + 64 * (size_t)N;             \
+      e = set_smem(grid_persist_kernel<NTV, LGV, QV>, psmem);                                              \
+      int occ = 0;                                                                                         \
+      if (e == cudaSuccess)                                                                                \
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_persist_kernel<NTV, LGV, QV>, NTV, psmem); \
+      if (e == cudaSuccess && occ > 0) {                                                                   \
+        int g = sm_count() * occ;                                                                          \
+        if (g > B) g = B;                                                                                  \
+        grid_persist_kernel<NTV, LGV, QV><<<g, NTV, psmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, \
+                                                                 B, (cplx*)q_grid, s_grid, tw, twlog);     \
+        e = cudaGetLastError();                                                                            \
+        return e == cudaSuccess ? 0 : fail("grid_persist_kernel", e);                                      \
+      }                                                                                                    \
+    }                                                                                                      \
     const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
     e = set_smem(grid_stockham_kernel<NTV, LGV, QV>, ssmem);                                               \
     if (e == cudaSuccess) {                                                                                \
@@ -394,6 +410,7 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
   }
   SolveParams P = make_params(N, o);
   P.dnc = N >= dnc_min_n() ? 1 : 0;
+  P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
   const cplx* tw;
   int twlog;
   const int fmax = P.L > 2 * N ? P.L : (1 << ilog2(2 * N));

@@ -279,7 +279,8 @@ SLSE_HD size_t dnc_arena_elems(int s) {
 // Superfast factorisation: same outputs as toeplitz_factor.  T is the root
 // transfer matrix storage (4 N complex), arena from dnc_arena_elems(N-1).
 SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, cplx* arena, double* delta_out,
-                                   double* delta_tmp, cplx* SLSE_RESTRICT rho, const FftCtx& f, Blk& b) {
+                                   double* delta_tmp, cplx* SLSE_RESTRICT rho, const FftCtx& f, Blk& b,
+                                   int dnc_stockham = 0) {
   Factor F;
   F.logdet = 0.0;
   F.status = kOk;
@@ -294,7 +295,7 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   if (b.tid == 0) delta_tmp[0] = c0;
   DncCtx X;
   X.f = f;
-  X.f.stockham = 1;  // radix-16 register passes for the product transforms
+  X.f.stockham = dnc_stockham;  // register Stockham passes for the product transforms
   X.arena = arena;
   X.delta_tmp = delta_tmp;
   X.floor_ = kPdEps * c0;

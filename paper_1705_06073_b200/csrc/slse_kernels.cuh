@@ -50,10 +50,14 @@ inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false) {
   // (only the recursion and the 2N-point transforms are staged; the grid's
   // L-point transforms then run from L1/L2)
   size_t budget = kRegionBudget;
-  if (nt <= 32) {
+  if (nt <= 32 && !dnc) {
     const char* env = getenv("SLSE_WARP_REGION_KB");
     budget = env ? (size_t)atoi(env) * 1024 : 48 * (size_t)n;
     if (budget < 48 * (size_t)n) budget = 48 * (size_t)n;
+  }
+  if (const char* env = getenv("SLSE_REGION_KB")) {  // experiment override
+    const size_t v = (size_t)atoi(env) * 1024;
+    if (dnc || v >= 48 * (size_t)n) budget = v;
   }
   const size_t rec = dnc ? 0 : 48 * (size_t)n;
   p.rec_in_smem = (!dnc && rec <= budget) ? 1 : 0;
@@ -308,6 +312,77 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) gri
     const cplx a0 = X[LS + sl], a1 = X[2 * LS + sl];
     qg[l] = X[sl];
     sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+  }
+}
+
+
+// cp.async (16 B, L2-only) helpers for the persistent grid kernel
+SLSE_D void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+SLSE_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+SLSE_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
+
+// Persistent variant of grid_stockham_kernel: each CTA walks problems
+// p = blockIdx.x, + gridDim.x, ...; the next problem's (w, rho) are
+// prefetched with cp.async into a double-buffered stage while the current
+// one is transformed, hiding the HBM latency behind the FFT passes.
+template <int NT, int LG, int Q>
+__global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) grid_persist_kernel(
+    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int B,
+    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* tw, int twlog) {
+  constexpr int L = 1 << LG;
+  constexpr int LS = L + (L >> 4);
+  constexpr int H = L >> Q;  // transformed head (>= n)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* X = (cplx*)(smem_raw + head_bytes(NT));
+  cplx* stage = X + 3 * LS;  // [2][2][n] : buffer, (w, rho), point
+  const int tid = threadIdx.x;
+  auto prefetch = [&](int prob, int buf) {
+    const cplx* wp = w + (size_t)prob * n;
+    const cplx* rp = rho + (size_t)prob * n;
+    cplx* sw = stage + (size_t)buf * 2 * n;
+    for (int i = tid; i < n; i += NT) {
+      cp_async16(sw + i, wp + i);
+      cp_async16(sw + n + i, rp + i);
+    }
+    cp_async_commit();
+  };
+  int p = blockIdx.x;
+  if (p < B) prefetch(p, 0);
+  for (int it = 0; p < B; ++it, p += gridDim.x) {
+    const int nxt = p + gridDim.x;
+    if (nxt < B) {
+      prefetch(nxt, (it + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const cplx* sw = stage + (size_t)(it & 1) * 2 * n;
+    for (int i = tid; i < H; i += NT) {
+      cplx a = mk(0.0, 0.0), rr = mk(0.0, 0.0);
+      if (i < n) { a = sw[i]; rr = sw[n + i]; }
+      const int si = sk(i);
+      X[si] = a;
+      X[LS + si] = rr;
+      X[2 * LS + si] = cscale(rr, (double)i);
+    }
+    __syncthreads();
+    fft_fixed_pruned<LG, Q>(X, 3, -1.0, tw, twlog, tid, NT);
+    const double inv_d = 1.0 / delta_last[p];
+    const double c2n = 2.0 - (double)n;
+    cplx* qg = q_grid + (size_t)p * L;
+    double* sgp = s_grid + (size_t)p * L;
+    for (int l = tid; l < L; l += NT) {
+      const int sl = sk(l);
+      const cplx a0 = X[LS + sl], a1 = X[2 * LS + sl];
+      qg[l] = X[sl];
+      sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+    }
+    __syncthreads();
   }
 }
 

@@ -43,6 +43,7 @@ struct SolveParams {
   int tcap, ecap;
   double tau, conv_tol_scale, dec_tol_scale;
   int dnc;  // 1: superfast divide-and-conquer Schur (slse_dnc.cuh), 0: Schur-Levinson
+  int dnc_stockham;  // product transforms with the register Stockham passes
 };
 
 // Launch-uniform parameters from the C-ABI options (estimator.py:34-50).
@@ -64,6 +65,7 @@ SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   P.conv_tol_scale = o.convergence_tol_scale;
   P.dec_tol_scale = o.newton_decrement_tol_scale;
   P.dnc = 0;
+  P.dnc_stockham = 0;
   return P;
 }
 
@@ -297,8 +299,9 @@ struct Solver {
   // ---- active set bookkeeping ----
   // rebuild act_slot / act_theta / act_gamma from the slot arrays (slot order)
   SLSE_NIM void compact() {
-    const int chunk = (kmax + b.nt - 1) / b.nt;
-    const int lo = b.tid * chunk;
+    const int tid_ = b.tid, nt_ = b.nt;
+    const int chunk = (kmax + nt_ - 1) / nt_;
+    const int lo = tid_ * chunk;
     const int hi = lo + chunk < kmax ? lo + chunk : kmax;
     int cnt = 0;
     for (int i = lo; i < hi; ++i) cnt += z[i];
@@ -340,7 +343,7 @@ struct Solver {
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
     steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
-    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b)
+    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham)
                      : toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
     if (F.status != kOk) return F.status;
     B.delta_last = F.delta_last;
@@ -380,10 +383,11 @@ struct Solver {
   double last_trace;
 
   // ---- activation (smlr.py:53-171) ----
-  SLSE_NIM double gamma_bar() {  // smlr.py:53-59
+  SLSE_NIM double gamma_bar() {
+    const int tid_ = b.tid, nt_ = b.nt;  // smlr.py:53-59
     if (k) {
       double part = 0.0;
-      for (int i = b.tid; i < k; i += b.nt) part += act_gamma[i];
+      for (int i = tid_; i < k; i += nt_) part += act_gamma[i];
       double bar = b.sum(part) / (double)k;
       if (bar > 0.0) return bar;
     }
@@ -392,11 +396,12 @@ struct Solver {
   }
 
   SLSE_NIM void grid_curve(double gb, double ze) {
+    const int tid_ = b.tid, nt_ = b.nt;
     ++n_grids;
     Bundle& B = bun[cur];
     grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
     const double lr = log((1.0 - ze) / ze);
-    for (int l = b.tid; l < L; l += b.nt) {
+    for (int l = tid_; l < L; l += nt_) {
       const double qq = cabs2(G0[l]);
       q2[l] = qq;
       dl[l] = gain(qq, sg[l], gb, lr);
@@ -415,13 +420,14 @@ struct Solver {
 
   // returns 1 if a component was activated (smlr.py:107-122)
   SLSE_NIM int try_activate() {
+    const int tid_ = b.tid, nt_ = b.nt;
     if (k >= kmax) return 0;
     const double gb = gamma_bar();
     const double ze = prior_zeta(zeta, kmax);
     grid_curve(gb, ze);
     double best = 0.0;
     int bi = -1;
-    for (int l = b.tid; l < L; l += b.nt) {
+    for (int l = tid_; l < L; l += nt_) {
       const double d = dl[l];
       if (Blk::better(d, l, best, bi)) { best = d; bi = l; }
     }
@@ -450,13 +456,14 @@ struct Solver {
 
   // initial multi-activation sweep (smlr.py:125-171); returns #added
   SLSE_NIM int sweep() {
+    const int tid_ = b.tid, nt_ = b.nt;
     const double gb = gamma_bar();
     const double ze = prior_zeta(zeta, kmax);
     grid_curve(gb, ze);
     // circular local minima and their minimum
     double mn = 0.0;
     int mi = -1;
-    for (int l = b.tid; l < L; l += b.nt) {
+    for (int l = tid_; l < L; l += nt_) {
       const double d = dl[l];
       const double dp = dl[(l + L - 1) & (L - 1)], dn = dl[(l + 1) & (L - 1)];
       if (d <= dp && d <= dn) {
@@ -469,8 +476,8 @@ struct Solver {
     if (dmin >= -kEpsObjective) return 0;
     const double thr = dmin / kSweepWithin;
     // compact qualifying minima in index order
-    const int chunk = (L + b.nt - 1) / b.nt;
-    const int lo = b.tid * chunk;
+    const int chunk = (L + nt_ - 1) / nt_;
+    const int lo = tid_ * chunk;
     const int hi = lo + chunk < L ? lo + chunk : L;
     int cnt = 0;
     for (int l = lo; l < hi; ++l) {
@@ -487,7 +494,7 @@ struct Solver {
     }
     b.sync();
     // stable sort by (delta, index): rank = #{j: (d_j, j) < (d_i, i)}
-    for (int i = b.tid; i < m; i += b.nt) {
+    for (int i = tid_; i < m; i += nt_) {
       const int li = cidx[i];
       const double di = dl[li];
       int rank = 0;
@@ -546,6 +553,7 @@ struct Solver {
   // ---- deactivation (smlr.py:174-225) ----
   // on return: number removed; cur is valid for the new state (stats too if k>0)
   SLSE_NIM int deactivate(int* st) {
+    const int tid_ = b.tid, nt_ = b.nt;
     int removed = 0;
     *st = kOk;
     while (k) {
@@ -554,7 +562,7 @@ struct Solver {
       const double rhs = log((1.0 - ze) / ze);
       double wv = 0.0;
       int wi = -1;
-      for (int i = b.tid; i < k; i += b.nt) {
+      for (int i = tid_; i < k; i += nt_) {
         const double ga = act_gamma[i];
         const double s = B.s[i];
         const double den = 1.0 - ga * s;
@@ -596,7 +604,8 @@ struct Solver {
 
   // ---- gradient / diag Hessian (model_core.py:497-536) ----
   SLSE_NIM void gradient(const Bundle& B, const double* ga, double* g) {
-    for (int i = b.tid; i < k; i += b.nt) {
+    const int tid_ = b.tid, nt_ = b.nt;
+    for (int i = tid_; i < k; i += nt_) {
       const cplx q = B.q[i], r = B.r[i], t = B.t[i];
       const cplx cross = cmul(conjg(q), r);
       g[i] = 2.0 * ga[i] * (t.im - cross.im);
@@ -605,8 +614,9 @@ struct Solver {
   }
 
   SLSE_NIM void diag_hessian(const Bundle& B, const double* ga_, double* d) {
+    const int tid_ = b.tid, nt_ = b.nt;
     const double fb_theta = (double)(50 * n) * (double)(50 * n);
-    for (int i = b.tid; i < k; i += b.nt) {
+    for (int i = tid_; i < k; i += nt_) {
       const double ga = ga_[i];
       const cplx q = B.q[i], r = B.r[i], u = B.u[i], t = B.t[i], v = B.v[i];
       const double s = B.s[i], x = B.x[i];
@@ -636,16 +646,18 @@ struct Solver {
 
   // ---- L-BFGS (lbfgs.py) ----
   SLSE_D double dot(const double* p, const double* q, int dim) {
+    const int tid_ = b.tid, nt_ = b.nt;
     double part = 0.0;
-    for (int i = b.tid; i < dim; i += b.nt) part += p[i] * q[i];
+    for (int i = tid_; i < dim; i += nt_) part += p[i] * q[i];
     return b.sum(part);
   }
 
   // two-loop recursion into dir (lbfgs.py:63-76); uses gnew as q scratch
   SLSE_NIM void two_loop(int dim) {
+    const int tid_ = b.tid, nt_ = b.nt;
     double alphas[16];
     double* qv = gnew;
-    for (int i = b.tid; i < dim; i += b.nt) qv[i] = g0[i];
+    for (int i = tid_; i < dim; i += nt_) qv[i] = g0[i];
     const int K2 = 2 * kmax;
     for (int jj = mem_count - 1; jj >= 0; --jj) {
       const int slot = (mem_head + jj) % P.lbfgs_mem;
@@ -653,28 +665,29 @@ struct Solver {
       const double* Y = lbY + (size_t)slot * K2;
       const double al_ = lbR[slot] * dot(S, qv, dim);
       alphas[jj] = al_;
-      for (int i = b.tid; i < dim; i += b.nt) qv[i] -= al_ * Y[i];
+      for (int i = tid_; i < dim; i += nt_) qv[i] -= al_ * Y[i];
     }
-    for (int i = b.tid; i < dim; i += b.nt) dir[i] = qv[i] / diag[i];
+    for (int i = tid_; i < dim; i += nt_) dir[i] = qv[i] / diag[i];
     for (int jj = 0; jj < mem_count; ++jj) {
       const int slot = (mem_head + jj) % P.lbfgs_mem;
       const double* S = lbS + (size_t)slot * K2;
       const double* Y = lbY + (size_t)slot * K2;
       const double be = lbR[slot] * dot(Y, dir, dim);
       const double coef = alphas[jj] - be;
-      for (int i = b.tid; i < dim; i += b.nt) dir[i] += S[i] * coef;
+      for (int i = tid_; i < dim; i += nt_) dir[i] += S[i] * coef;
     }
-    for (int i = b.tid; i < dim; i += b.nt) dir[i] = -dir[i];
+    for (int i = tid_; i < dim; i += nt_) dir[i] = -dir[i];
   }
 
   // memory.push(alpha*dir, gnew - g0) (lbfgs.py:47-53)
   SLSE_NIM void push_pair(double alpha, int dim) {
+    const int tid_ = b.tid, nt_ = b.nt;
     const int K2 = 2 * kmax;
     const int slot = (mem_count < P.lbfgs_mem) ? (mem_head + mem_count) % P.lbfgs_mem : mem_head;
     double* S = lbS + (size_t)slot * K2;
     double* Y = lbY + (size_t)slot * K2;
     double pv[3] = {0.0, 0.0, 0.0};
-    for (int i = b.tid; i < dim; i += b.nt) {
+    for (int i = tid_; i < dim; i += nt_) {
       const double s = alpha * dir[i];
       const double yv = gnew[i] - g0[i];
       S[i] = s;
@@ -699,10 +712,11 @@ struct Solver {
   // failure, or a negative model status.  On acceptance the new point is in
   // the slot arrays, cur is the accepted bundle (stats valid), *dec set.
   SLSE_NIM int lbfgs_step(double f0, double* dec) {
+    const int tid_ = b.tid, nt_ = b.nt;
     const int dim = 2 * k;
     // any(g0)?
     double nz = 0.0;
-    for (int i = b.tid; i < dim; i += b.nt) nz += (g0[i] != 0.0) ? 1.0 : 0.0;
+    for (int i = tid_; i < dim; i += nt_) nz += (g0[i] != 0.0) ? 1.0 : 0.0;
     if (b.sum(nz) == 0.0) {
       *dec = 0.0;
       return 0;  // point unchanged
@@ -710,13 +724,13 @@ struct Solver {
     two_loop(dim);
     double slope = dot(g0, dir, dim);
     if (slope >= 0.0) {
-      for (int i = b.tid; i < dim; i += b.nt) dir[i] = -g0[i] / diag[i];
+      for (int i = tid_; i < dim; i += nt_) dir[i] = -g0[i] / diag[i];
       slope = dot(g0, dir, dim);
     }
     *dec = -slope;
     // gamma step cap (lbfgs.py:84-90)
     double capv = INFINITY;
-    for (int i = b.tid; i < k; i += b.nt) {
+    for (int i = tid_; i < k; i += nt_) {
       const double dg = dir[k + i];
       if (dg < 0.0) {
         const double r = pt[k + i] / -dg;
@@ -729,7 +743,7 @@ struct Solver {
     Bundle& T = bun[cur ^ 1];
     for (int bt = 0; bt < kMaxBacktracks; ++bt) {
       ++n_backtracks;
-      for (int i = b.tid; i < k; i += b.nt) {
+      for (int i = tid_; i < k; i += nt_) {
         cth[i] = np_mod1(pt[i] + alpha * dir[i]);
         cga[i] = pt[k + i] + alpha * dir[k + i];
         cand[i] = cth[i];
@@ -745,7 +759,7 @@ struct Solver {
         b.sync();
         push_pair(alpha, dim);
         // accept: write the point into the slots; swap bundles
-        for (int i = b.tid; i < k; i += b.nt) {
+        for (int i = tid_; i < k; i += nt_) {
           const int s = act_slot[i];
           theta[s] = cth[i];
           gamma[s] = cga[i];
@@ -910,24 +924,26 @@ struct Solver {
 
   // beta EM value (tr + ||y - Psi(theta) mu||^2) / M  (estimator.py:86-88)
   SLSE_NIM double residual_value(double tr) {
+    const int tid_ = b.tid, nt_ = b.nt;
     double* mre = marg;  // scratch (length >= k)
     double* mim = dtmp;  // scratch (length n >= k), free outside build()
-    for (int i = b.tid; i < k; i += b.nt) { mre[i] = mu[i].re; mim[i] = mu[i].im; }
+    for (int i = tid_; i < k; i += nt_) { mre[i] = mu[i].re; mim[i] = mu[i].im; }
     b.sync();
     steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
     double part = 0.0;
-    for (int i = b.tid; i < n; i += b.nt) part += cabs2(csub(y[i], c[i]));
+    for (int i = tid_; i < n; i += nt_) part += cabs2(csub(y[i], c[i]));
     const double resid = b.sum(part);
     return (tr + resid) / (double)n;
   }
 
   SLSE_NIM void finish(int iterations, int converged) {
+    const int tid_ = b.tid, nt_ = b.nt;
     // posterior mean alpha = gamma * q (model_core.py:539-547)
     if (status == kOk && k) {
       int st = ensure_cur();
       if (st == kOk) {
         stats(bun[cur], act_theta, k);
-        for (int i = b.tid; i < k; i += b.nt) {
+        for (int i = tid_; i < k; i += nt_) {
           o.alpha[i] = cscale(bun[cur].q[i], act_gamma[i]);
           o.theta[i] = act_theta[i];
           o.gamma[i] = act_gamma[i];

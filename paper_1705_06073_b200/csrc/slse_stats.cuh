@@ -78,12 +78,13 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
                             const cplx* SLSE_RESTRICT w, int n, double delta_last, const CfTable* cf,
                             cplx* q, cplx* r, cplx* u, double* s, cplx* t, cplx* v, double* x,
                             Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
   const double inv_d = 1.0 / delta_last;
   const double two_pi = 2.0 * kPi;
 #ifdef SLSE_HOST_EMU
   const int lanes = 1, lane = 0, warp = 0, nwarp = 1;
 #else
-  const int lanes = 32, lane = b.tid & 31, warp = b.tid >> 5, nwarp = b.nt >> 5;
+  const int lanes = 32, lane = tid_ & 31, warp = tid_ >> 5, nwarp = nt_ >> 5;
 #endif
   for (int kk = warp; kk < K; kk += nwarp) {
     const double th = thetas[kk];
@@ -153,6 +154,7 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
 // Results land in G0 (q^G), and sg (s^G, real).  G1/G2 are scratch.
 SLSE_NI void grid_eval(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT w, int n, double delta_last,
                       int L, cplx* G0, cplx* G1, cplx* G2, double* sg, const FftCtx& f, Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
   const cplx z = mk(0.0, 0.0);
   fft(G0, L, -1.0, [&](int i) { return i < n ? w[i] : z; }, [&](int i, cplx v) { G0[i] = v; }, f, b);
   fft(G1, L, -1.0, [&](int i) { return i < n ? rho[i] : z; }, [&](int i, cplx v) { G1[i] = v; }, f, b);
@@ -160,7 +162,7 @@ SLSE_NI void grid_eval(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT 
       [&](int i, cplx v) { G2[i] = v; }, f, b);
   const double c2n = 2.0 - (double)n;
   const double inv_d = 1.0 / delta_last;
-  for (int l = b.tid; l < L; l += b.nt) {
+  for (int l = tid_; l < L; l += nt_) {
     const cplx a0 = G1[l], a1 = G2[l];
     sg[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
   }

@@ -28,10 +28,11 @@ enum Status : int {
 SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RESTRICT thetas,
                           const double* SLSE_RESTRICT coef_re, const double* SLSE_RESTRICT coef_im,
                           int k, double beta0, bool column, Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
   // accumulate in registers chunk-wise: each thread handles up to 16 owned m
   // values per sweep over k.
-  for (int m0 = b.tid; m0 < n; m0 += 16 * b.nt) {
-    const int J = (n - m0 + b.nt - 1) / b.nt;  // owned values in this chunk (<= 16 used)
+  for (int m0 = tid_; m0 < n; m0 += 16 * nt_) {
+    const int J = (n - m0 + nt_ - 1) / nt_;  // owned values in this chunk (<= 16 used)
     cplx acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = mk(0.0, 0.0);
@@ -40,7 +41,7 @@ SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RE
       const double cr = coef_re[kk];
       const double ci = coef_im ? coef_im[kk] : 0.0;
       cplx e = expj2pi((double)m0, th, 1.0);
-      cplx step = expj2pi((double)b.nt, th, 1.0);
+      cplx step = expj2pi((double)nt_, th, 1.0);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (j < J) {
@@ -53,7 +54,7 @@ SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RE
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int m = m0 + j * b.nt;
+      const int m = m0 + j * nt_;
       if (m < n) {
         cplx v = acc[j];
         if (column && m == 0) v = mk(v.re + beta0, 0.0);  // c_0 forced real (toeplitz.py:58-59)
@@ -89,6 +90,7 @@ template <bool SH>
 SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
                                    double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho,
                                    Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
   Factor F;
   F.logdet = 0.0;
   F.status = kOk;
@@ -109,14 +111,14 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     __builtin_assume(__isShared(a));
   }
 #endif
-  for (int j = b.tid; j < n; j += b.nt) {
+  for (int j = tid_; j < n; j += nt_) {
     cplx cj = (j == 0) ? mk(c0, 0.0) : c[j];
     e[j] = cj;
     B[j] = cj;
     a[j] = mk(j == 0 ? 1.0 : 0.0, 0.0);
     delta_tmp[j] = 0.0;
   }
-  if (b.tid == 0) delta_tmp[0] = c0;
+  if (tid_ == 0) delta_tmp[0] = c0;
   b.sync();
   double delta = c0;
   int fail = 0;
@@ -124,7 +126,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
   // delta (instead of two divisions); a single-warp block also computes the
   // NEXT coefficient from the pre-update values e_{m+2}, B_1 before its bulk
   // update (lookahead), taking the reciprocal off the critical path.
-  const bool look = b.nt <= 32;
+  const bool look = nt_ <= 32;
   cplx k = mk(0.0, 0.0);
   if (n > 1) {
     const cplx e1 = e[1];
@@ -143,7 +145,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
       b.sync();  // every lane has read e_{m+2}, B_1 before any write below
     }
     const int cnt = n - 1 - m;  // pairs j = 0..cnt-1
-    for (int j = b.tid; j < cnt; j += b.nt) {
+    for (int j = tid_; j < cnt; j += nt_) {
       const cplx ej = e[j + m + 1];
       const cplx bj = B[j];
       if (j > 0) e[j + m + 1] = cadd(ej, cmul(k, bj));
@@ -152,7 +154,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     // predictor: a_i' = a_i + k conj(a_{m+1-i}), i = 1..m+1 (a_{m+1} = 0 before)
     const int top = m + 1;
     const int npair = (top + 1) / 2;
-    for (int i = b.tid; i <= npair; i += b.nt) {
+    for (int i = tid_; i <= npair; i += nt_) {
       if (i == 0) {
         a[top] = cmul(k, conjg(a[0]));
       } else {
@@ -167,7 +169,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
         }
       }
     }
-    if (b.tid == 0) delta_tmp[m + 1] = dnext;
+    if (tid_ == 0) delta_tmp[m + 1] = dnext;
     b.sync();
     delta = dnext;
     if (!(delta > floor_)) { fail = 1; break; }
@@ -187,7 +189,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
   }
   F.delta_last = delta;
   double part = 0.0;
-  for (int j = b.tid; j < n; j += b.nt) {
+  for (int j = tid_; j < n; j += nt_) {
     part += log(delta_tmp[j]);
     if (delta_out) delta_out[j] = delta_tmp[j];
     rho[j] = conjg(a[n - 1 - j]);
@@ -216,6 +218,7 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
 SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
                        const cplx* SLSE_RESTRICT x, const cplx* SLSE_RESTRICT Xhat, cplx* P, cplx* U,
                        cplx* V, cplx* SLSE_RESTRICT w, const FftCtx& f, Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
   const int lg = ilog2(2 * n);  // nf = next power of two >= 2N
   const int nf = 1 << lg;
   const cplx rlast = rho[n - 1];
@@ -224,7 +227,7 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
       [&](int i) { return i < n ? rho[i] : mk(0.0, 0.0); },
       [&](int i, cplx v) { P[i] = v; }, f, b);
   // U = Xhat * P1 ; V = Xhat * P0h
-  for (int k = b.tid; k < nf; k += b.nt) {
+  for (int k = tid_; k < nf; k += nt_) {
     const cplx p1 = P[k];
     const cplx wk = twid(f, k, lg, -1.0);
     const cplx wn1 = twid(f, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
@@ -240,8 +243,8 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
   fft_inplace(U, nf, 1.0, f, b);
   fft_inplace(V, nf, 1.0, f, b);
   // shift down by N-1 through registers (barrier between read and write)
-  for (int i0 = 0; i0 < nf; i0 += b.nt) {
-    const int i = i0 + b.tid;
+  for (int i0 = 0; i0 < nf; i0 += nt_) {
+    const int i = i0 + tid_;
     cplx u = mk(0.0, 0.0), v = mk(0.0, 0.0);
     if (i < n) { u = cscale(U[n - 1 + i], inv); v = cscale(V[n - 1 + i], inv); }
     b.sync();
@@ -251,7 +254,7 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
   fft_inplace(U, nf, -1.0, f, b);
   fft_inplace(V, nf, -1.0, f, b);
   // Z = F1 * P1h - F0 * P0  -> U
-  for (int k = b.tid; k < nf; k += b.nt) {
+  for (int k = tid_; k < nf; k += nt_) {
     const cplx p1 = P[k];
     const cplx wk = twid(f, k, lg, -1.0);
     const cplx wn1 = twid(f, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
@@ -263,7 +266,7 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
   const double sc = inv / delta_last;
   double quad = 0.0;
   fft_inplace(U, nf, 1.0, f, b);
-  for (int i = b.tid; i < n; i += b.nt) {
+  for (int i = tid_; i < n; i += nt_) {
     const cplx wi = cscale(U[i], sc);
     w[i] = wi;
     quad += x[i].re * wi.re + x[i].im * wi.im;  // Re(conj(x) w)
