@@ -240,8 +240,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res, solver_e2e = estimate_batch(Y, opts, device=dev, return_solver=True)
-        # consume every result (model order + estimates) inside the timed region
-        chk = sum(r.k_hat for r in res) + float(sum(np.abs(r.alpha_hat).sum() for r in res))
+        # consume every problem's estimates (SoA host arrays) inside the timed region
+        chk = int(res.k_hat.sum()) + float(np.abs(res.alpha).sum() + res.theta.sum() + res.beta.sum())
         t1 = time.perf_counter()
         if i > 0:
             e2e_ms.append(1000.0 * (t1 - t0))

@@ -112,7 +112,7 @@ int solver_threads(int n) {
   if (n <= 512) return 32;    // cfg1-2: measured 68 ms (32) vs 113 ms (256) per 4096 x N=256 batch
   if (n <= 2048) return 256;  // cfg3: 167 ms (256) vs 205 (128) / 236 (512) per 1024 x N=1024
   if (n <= 4096) return 512;  // cfg4: 1.44 s (512) vs 1.48 (1024) / 1.78 (256) per 256 x N=4096
-  return 1024;
+  return 512;                 // cfg5 (superfast): 8.8 s (512) vs 13.1 (1024) / 12 (128) per 64 x N=16384
 }
 
 int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
@@ -318,7 +318,7 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
     while (q < 3 && (N << (q + 1)) <= L) ++q;  // input support n <= L / 2^q
 #define SLSE_GRID_Q(NTV, LGV, QV)                                                                          \
   case QV: {                                                                                               \
-    if (getenv("SLSE_GRID_NOPERSIST") == nullptr && (N % 1) == 0) {                                        \
+    if (getenv("SLSE_GRID_PERSIST") != nullptr) {  /* measured slower than one CTA per problem */    \
       const size_t psmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV) + 64 * (size_t)N;             \
       e = set_smem(grid_persist_kernel<NTV, LGV, QV>, psmem);                                              \
       int occ = 0;                                                                                         \

@@ -299,11 +299,51 @@ class BatchSolver:
         return unpack_all(self.host_outputs())
 
 
-def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False):
+class BatchResult:
+    """Results of a batched solve: structure-of-arrays host copies (every
+    estimate of every problem) plus list-like access to per-problem
+    LseResult objects, built on first access.
+
+    SoA fields (problem-major): k_hat, status, iterations, converged, beta,
+    zeta (B,); theta, gamma, alpha (complex), slot (B, K) zero-padded past
+    k_hat; trace (B, T) padded past n_trace."""
+
+    def __init__(self, h: dict):
+        self.h = h
+        self.k_hat = h["k_hat"]
+        self.status = h["status"]
+        self.iterations = h["iterations"]
+        self.converged = (h["flags"] & FLAG_CONVERGED) != 0
+        self.beta = h["beta"]
+        self.zeta = h["zeta"]
+        self.theta = h["theta"]
+        self.gamma = h["gamma"]
+        self.alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]
+        self.slot = h["slot"]
+        self.trace = h["trace"]
+        self.n_trace = h["n_trace"]
+        self._items = None
+
+    def __len__(self):
+        return int(self.k_hat.shape[0])
+
+    def _all(self):
+        if self._items is None:
+            self._items = unpack_all(self.h)
+        return self._items
+
+    def __getitem__(self, i):
+        return self._all()[i]
+
+    def __iter__(self):
+        return iter(self._all())
+
+
+def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False) -> BatchResult:
     """Solve B independent complete-data problems, y: (B, N) complex.
-    Accepts numpy or torch input; returns a list of LseResult (problem
-    order).  Problems that hit a non-PD covariance carry ``status`` 1 instead
-    of raising."""
+    Accepts numpy or torch input; returns a BatchResult (SoA arrays + a
+    sequence of LseResult in problem order).  Problems that hit a non-PD
+    covariance carry ``status`` 1 instead of raising."""
     torch = _torch()
     if isinstance(y, torch.Tensor):
         yt = y
@@ -312,9 +352,11 @@ def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=
     if yt.dim() != 2:
         raise DimensionMismatch("y must have shape (B, N)")
     solver = BatchSolver(int(yt.shape[1]), int(yt.shape[0]), opts, device=device)
-    ydev = yt.to(device=solver.device, dtype=torch.complex128).contiguous()
+    if yt.device.type == "cpu" and not yt.is_pinned():
+        yt = yt.pin_memory()
+    ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=True).contiguous()
     solver.solve(ydev)
-    res = solver.results()
+    res = BatchResult(solver.host_outputs())
     return (res, solver) if return_solver else res
 
 
