@@ -158,10 +158,11 @@ SLSE_D void dnc_fwd(cplx* dst, const cplx* src, int len, int F, cplx* work, cons
       [&](int i, cplx v) { dst[i] = v; }, f, b);
 }
 
-// One internal node's buffers, all carved from `base` (see dnc_arena_elems).
+// One internal node's buffers, all carved from `base` (see dnc_arena_elems);
+// the product stage uses 8 F above them.
 struct DncNode {
   int h, F;
-  cplx *T1, *S, *SE, *SB, *work, *E2, *B2, *T2, *above;
+  cplx *T1, *S, *SE, *SB, *work_multi, *E2, *B2, *T2, *above;
 };
 
 SLSE_D DncNode dnc_node(cplx* base, int s) {
@@ -172,8 +173,8 @@ SLSE_D DncNode dnc_node(cplx* base, int s) {
   d.S = d.T1 + 4 * (d.h + 1);          // 4 F : spectra of T1 (kept for the product)
   d.SE = d.S + 4 * (size_t)d.F;        // F
   d.SB = d.SE + d.F;                   // F
-  d.work = d.SB + d.F;                 // F   (global fallback buffer of the FFT)
-  d.E2 = d.work + d.F;                 // s - h + 1
+  d.work_multi = d.SB + d.F;           // 6 F (global fallback buffer of the batched FFTs)
+  d.E2 = d.work_multi + 6 * (size_t)d.F;  // s - h + 1
   d.B2 = d.E2 + (s - d.h + 1);         // s - h
   d.T2 = d.B2 + (s - d.h);             // 4 (s - h + 1)
   d.above = d.T2 + 4 * (s - d.h + 1);  // children / product scratch start here
@@ -213,19 +214,36 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
     }
     if (cf.phase == 1) {  // left done: middle products give the right window
       const int l1 = h + 1;
-      for (int q = 0; q < 4; ++q) dnc_fwd(d.S + (size_t)q * F, d.T1 + q * l1, l1, F, d.work, X.f, b);
-      dnc_fwd(d.SE, cf.E, s + 1, F, d.work, X.f, b);
-      dnc_fwd(d.SB, cf.Bw, s, F, d.work, X.f, b);
-      const cplx* S = d.S;
+      const cplx* T1 = d.T1;
+      const cplx* E = cf.E;
+      const cplx* Bw = cf.Bw;
+      cplx* S = d.S;  // S[0..3] = spectra of T1, S[4] = E, S[5] = Bw (contiguous: S, SE, SB)
+      // six forward transforms in one batch (SE, SB follow S contiguously)
+      fft_multi(d.work_multi, 6, F, -1.0,
+                [&](int q, int i) {
+                  if (q < 4) return i < l1 ? T1[q * l1 + i] : mk(0.0, 0.0);
+                  if (q == 4) return i <= s ? E[i] : mk(0.0, 0.0);
+                  return i < s ? Bw[i] : mk(0.0, 0.0);
+                },
+                [&](int q, int i, cplx v) { S[(size_t)q * F + i] = v; }, X.f, b);
       const cplx* SE = d.SE;
       const cplx* SB = d.SB;
       cplx* E2 = d.E2;
       cplx* B2 = d.B2;
       // E2 = (T11 E + T12 Bw)[h..s], B2 = (T21 E + T22 Bw)[h..s-1]
-      fft(d.work, F, 1.0, [&](int k) { return cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k])); },
-          [&](int i, cplx v) { if (i >= h && i <= s) E2[i - h] = cscale(v, invF); }, X.f, b);
-      fft(d.work, F, 1.0, [&](int k) { return cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k])); },
-          [&](int i, cplx v) { if (i >= h && i < s) B2[i - h] = cscale(v, invF); }, X.f, b);
+      fft_multi(d.work_multi, 2, F, 1.0,
+                [&](int q, int k) {
+                  return q == 0 ? cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k]))
+                                : cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k]));
+                },
+                [&](int q, int i, cplx v) {
+                  if (q == 0) {
+                    if (i >= h && i <= s) E2[i - h] = cscale(v, invF);
+                  } else if (i >= h && i < s) {
+                    B2[i - h] = cscale(v, invF);
+                  }
+                },
+                X.f, b);
       cf.phase = 2;
       fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
       continue;
@@ -233,26 +251,22 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
     // phase 2: Theta = T2 T1 (degree s; F >= s + 1 so no wrap)
     {
       const int l2 = s - h + 1;
-      cplx* A11 = d.SE;  // spectra of T2 reuse SE, SB, work and one fresh F
-      cplx* A12 = d.SB;
-      cplx* A21 = d.work;
-      cplx* A22 = d.above;
-      cplx* scratch = d.above + F;
-      dnc_fwd(A11, d.T2, l2, F, scratch, X.f, b);
-      dnc_fwd(A12, d.T2 + l2, l2, F, scratch, X.f, b);
-      dnc_fwd(A21, d.T2 + 2 * l2, l2, F, scratch, X.f, b);
-      dnc_fwd(A22, d.T2 + 3 * l2, l2, F, scratch, X.f, b);
+      const cplx* T2 = d.T2;
+      cplx* A = d.above;            // 4 F : spectra of T2
+      cplx* wk = d.above + 4 * (size_t)F;  // 4 F global work
+      fft_multi(wk, 4, F, -1.0, [&](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
+                [&](int q, int i, cplx v) { A[(size_t)q * F + i] = v; }, X.f, b);
       const cplx* S = d.S;
       cplx* T = cf.T;
       const int ld = s + 1;
-      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A11[k], S[k]), cmul(A12[k], S[2 * F + k])); },
-          [&](int i, cplx v) { if (i < ld) T[i] = cscale(v, invF); }, X.f, b);
-      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A11[k], S[F + k]), cmul(A12[k], S[3 * F + k])); },
-          [&](int i, cplx v) { if (i < ld) T[ld + i] = cscale(v, invF); }, X.f, b);
-      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A21[k], S[k]), cmul(A22[k], S[2 * F + k])); },
-          [&](int i, cplx v) { if (i < ld) T[2 * ld + i] = cscale(v, invF); }, X.f, b);
-      fft(scratch, F, 1.0, [&](int k) { return cadd(cmul(A21[k], S[F + k]), cmul(A22[k], S[3 * F + k])); },
-          [&](int i, cplx v) { if (i < ld) T[3 * ld + i] = cscale(v, invF); }, X.f, b);
+      // T_rc = A_r1 S_1c + A_r2 S_2c ; output q = 2 r + c
+      fft_multi(wk, 4, F, 1.0,
+                [&](int q, int k) {
+                  const int r = q >> 1, c = q & 1;
+                  return cadd(cmul(A[(size_t)(2 * r) * F + k], S[(size_t)c * F + k]),
+                              cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
+                },
+                [&](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
       --sp;
     }
   }
@@ -270,8 +284,8 @@ SLSE_HD size_t dnc_arena_elems(int s) {
     const int t = chain[i];
     const int h = t / 2;
     const size_t F = (size_t)1 << ilog2(t + 1);
-    const size_t own = 4 * (size_t)(h + 1) + 7 * F + 2 * (size_t)(t - h) + 1 + 4 * (size_t)(t - h + 1);
-    below = own + (below > 2 * F ? below : 2 * F);
+    const size_t own = 4 * (size_t)(h + 1) + 12 * F + 2 * (size_t)(t - h) + 1 + 4 * (size_t)(t - h + 1);
+    below = own + (below > 8 * F ? below : 8 * F);
   }
   return below;
 }

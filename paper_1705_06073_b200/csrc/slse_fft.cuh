@@ -64,24 +64,33 @@ SLSE_D void fft_barrier() {
 #endif
 }
 
-SLSE_NI void fft_passes_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+// DIT passes over `count` contiguous bit-reversed buffers of n points
+// (one barrier per pass for all of them).
+SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                              int tid, int nt) {
   const int p = ilog2(n);
   int lgh = 0;  // log2 of current half-span
   if (p & 1) {
-    for (int t = tid; t < (n >> 1); t += nt) {
-      cplx x0 = x[2 * t], x1 = x[2 * t + 1];
-      x[2 * t] = cadd(x0, x1);
-      x[2 * t + 1] = csub(x0, x1);
+    const int per = n >> 1;
+    for (int t = tid; t < count * per; t += nt) {
+      const int c = t / per, u = t - c * per;
+      cplx* xc = x + (size_t)c * n;
+      cplx x0 = xc[2 * u], x1 = xc[2 * u + 1];
+      xc[2 * u] = cadd(x0, x1);
+      xc[2 * u + 1] = csub(x0, x1);
     }
     fft_barrier();
     lgh = 1;
   }
+  const int per = n >> 2;
   for (; lgh + 2 <= p; lgh += 2) {
     const int h = 1 << lgh;
-    for (int t = tid; t < (n >> 2); t += nt) {
-      const int pos = t & (h - 1);
-      const int base = ((t >> lgh) << (lgh + 2)) + pos;
-      cplx x0 = x[base], x1 = x[base + h], x2 = x[base + 2 * h], x3 = x[base + 3 * h];
+    for (int t = tid; t < count * per; t += nt) {
+      const int c = t / per, u = t - c * per;
+      cplx* xc = x + (size_t)c * n;
+      const int pos = u & (h - 1);
+      const int base = ((u >> lgh) << (lgh + 2)) + pos;
+      cplx x0 = xc[base], x1 = xc[base + h], x2 = xc[base + 2 * h], x3 = xc[base + 3 * h];
       // stage span 2h
       cplx w1 = twid_tab(tw, twlog, pos, lgh + 1, sign);
       cplx t1 = cmul(w1, x1);
@@ -93,13 +102,17 @@ SLSE_NI void fft_passes_v(cplx* x, int n, double sign, const cplx* __restrict__ 
       cplx u2 = cmul(w2, a2);
       cplx u3 = cmul(w2, a3);
       u3 = (sign < 0) ? mk(u3.im, -u3.re) : mk(-u3.im, u3.re);
-      x[base] = cadd(a0, u2);
-      x[base + 2 * h] = csub(a0, u2);
-      x[base + h] = cadd(a1, u3);
-      x[base + 3 * h] = csub(a1, u3);
+      xc[base] = cadd(a0, u2);
+      xc[base + 2 * h] = csub(a0, u2);
+      xc[base + h] = cadd(a1, u3);
+      xc[base + 3 * h] = csub(a1, u3);
     }
     fft_barrier();
   }
+}
+
+SLSE_D void fft_passes_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+  fft_passes_multi(x, 1, n, sign, tw, twlog, tid, nt);
 }
 
 SLSE_D void fft_passes(cplx* x, int n, double sign, const FftCtx& f, Blk& b) {
@@ -424,6 +437,27 @@ SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx&
     for (int i = tid; i < n; i += nt) st(i, x[i]);
     fft_barrier();
   }
+}
+
+// `count` transforms of n points at once: ld(c, i) -> FFT -> st(c, i, v).
+// Staged in shared memory when count*n fits, else in `work` (count*n,
+// global; the loader must not read `work`).
+template <class Load, class Store>
+SLSE_D void fft_multi(cplx* work, int count, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
+  const int tid = b.tid, nt = b.nt;
+  const int p = ilog2(n);
+  cplx* x = (count * n <= f.smem_cap) ? f.smem : work;
+  for (int t = tid; t < count * n; t += nt) {
+    const int c = t >> p, i = t & (n - 1);
+    x[(size_t)c * n + brev_bits((unsigned)i, p)] = ld(c, i);
+  }
+  fft_barrier();
+  fft_passes_multi(x, count, n, sign, f.tw, f.twlog, tid, nt);
+  for (int t = tid; t < count * n; t += nt) {
+    const int c = t >> p, i = t & (n - 1);
+    st(c, i, x[(size_t)c * n + i]);
+  }
+  fft_barrier();
 }
 
 SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {
