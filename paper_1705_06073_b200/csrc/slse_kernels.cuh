@@ -75,6 +75,7 @@ inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false) {
   p.fft_cap = sk_len(F);
   size_t region = 16 * (size_t)p.fft_cap;
   if (p.rec_in_smem && rec > region) region = rec;
+  p.fft_cap = (int)(region / 16);  // staging capacity = the whole region (recursion and FFTs alternate)
   p.bytes = head_bytes(nt) + region;
   return p;
 }

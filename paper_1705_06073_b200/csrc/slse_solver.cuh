@@ -399,8 +399,9 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     ++n_grids;
     Bundle& B = bun[cur];
-    grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
     const double lr = log((1.0 - ze) / ze);
+    if (grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) return;
+    grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
     for (int l = tid_; l < L; l += nt_) {
       const double qq = cabs2(G0[l]);
       q2[l] = qq;

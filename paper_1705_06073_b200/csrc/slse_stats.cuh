@@ -169,6 +169,53 @@ SLSE_NI void grid_eval(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT 
   b.sync();
 }
 
+// Activation grid fused with the gain curve, exploiting the zero padding:
+// with M = 2^ceil(log2 N) and R = L / M, grid point l = m R + r is
+//   X[m R + r] = sum_{i<N} (x_i W_L^{i r}) W_M^{i m},
+// so the three length-L transforms (w, rho, i rho) become R batches of three
+// length-M transforms -- no work on the zero tail, each batch staged in
+// shared memory (needs 3 M <= f.smem_cap) -- and every output is combined
+// straight into s^G, |q^G|^2 and the gain curve (no L-sized complex
+// buffers).  Returns false when the staging does not fit (caller falls
+// back to grid_eval).
+SLSE_NI bool grid_gain_fused(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT w, int n, double delta_last,
+                             int L, double gb, double log_ratio, double* dl, double* q2, double* sg,
+                             const FftCtx& f, Blk& b) {
+  const int M = 1 << ilog2(n);
+  if (3 * M > f.smem_cap || M > L) return false;
+  const int tid = b.tid, nt = b.nt;
+  const int R = L / M;
+  const int lgL = ilog2(L), p = ilog2(M);
+  const double c2n = 2.0 - (double)n;
+  const double inv_d = 1.0 / delta_last;
+  cplx* x = f.smem;
+  for (int r = 0; r < R; ++r) {
+    for (int t = tid; t < 3 * M; t += nt) {
+      const int c = t >> p, i = t & (M - 1);
+      cplx v = mk(0.0, 0.0);
+      if (i < n) {
+        const cplx tw = twid_tab(f.tw, f.twlog, (int)(((long long)i * r) & (L - 1)), lgL, -1.0);
+        const cplx src = c == 0 ? w[i] : (c == 1 ? rho[i] : cscale(rho[i], (double)i));
+        v = r ? cmul(src, tw) : src;
+      }
+      x[(size_t)c * M + brev_bits((unsigned)i, p)] = v;
+    }
+    fft_barrier();
+    fft_passes_multi(x, 3, M, -1.0, f.tw, f.twlog, tid, nt);
+    for (int m = tid; m < M; m += nt) {
+      const int l = m * R + r;
+      const cplx q = x[m], a0 = x[M + m], a1 = x[2 * M + m];
+      const double s = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+      const double qq = cabs2(q);
+      sg[l] = s;
+      q2[l] = qq;
+      dl[l] = (log1p(gb * s) + log_ratio) - qq / (1.0 / gb + s);
+    }
+    fft_barrier();
+  }
+  return true;
+}
+
 // Activation gain (smlr.py:62-70, G = 1):
 //   Delta = log1p(gb s) + log((1-ze)/ze) - |q|^2 / (1/gb + s)
 SLSE_D double gain(double q2, double s, double gb, double log_ratio) {
