@@ -411,6 +411,7 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
   SolveParams P = make_params(N, o);
   P.dnc = N >= dnc_min_n() ? 1 : 0;
   P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
+  P.grid_fused = getenv("SLSE_GRID_UNFUSED") ? 0 : 1;
   const cplx* tw;
   int twlog;
   const int fmax = P.L > 2 * N ? P.L : (1 << ilog2(2 * N));

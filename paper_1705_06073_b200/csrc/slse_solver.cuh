@@ -44,6 +44,7 @@ struct SolveParams {
   double tau, conv_tol_scale, dec_tol_scale;
   int dnc;  // 1: superfast divide-and-conquer Schur (slse_dnc.cuh), 0: Schur-Levinson
   int dnc_stockham;  // product transforms with the register Stockham passes
+  int grid_fused;    // activation grid via the zero-padding-aware R x M decomposition
 };
 
 // Launch-uniform parameters from the C-ABI options (estimator.py:34-50).
@@ -66,6 +67,7 @@ SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   P.dec_tol_scale = o.newton_decrement_tol_scale;
   P.dnc = 0;
   P.dnc_stockham = 0;
+  P.grid_fused = 1;
   return P;
 }
 
@@ -400,7 +402,7 @@ struct Solver {
     ++n_grids;
     Bundle& B = bun[cur];
     const double lr = log((1.0 - ze) / ze);
-    if (grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) return;
+    if (P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) return;
     grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
     for (int l = tid_; l < L; l += nt_) {
       const double qq = cabs2(G0[l]);

@@ -198,9 +198,118 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
   return F;
 }
 
+#ifndef SLSE_HOST_EMU
+// One-warp Schur-Levinson (the N <= 512 solver path): the backward generator
+// B_j of pair j = lane + 32 q stays in registers for the whole recursion
+// (its pair never changes lanes in the shifted frame), only e and the
+// predictor a live in shared memory; warp barriers only.
+template <int Q>
+SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* a, double* delta_out,
+                                   double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  __builtin_assume(__isShared(e));
+  __builtin_assume(__isShared(a));
+  const int lane = b.tid;
+  const double c0 = c0c.re;
+  const double floor_ = kPdEps * c0;
+  cplx Breg[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int j = lane + 32 * q;
+    cplx cj = mk(0.0, 0.0);
+    if (j < n) cj = (j == 0) ? mk(c0, 0.0) : c[j];
+    Breg[q] = cj;
+    if (j < n) {
+      e[j] = cj;
+      a[j] = mk(j == 0 ? 1.0 : 0.0, 0.0);
+      delta_tmp[j] = 0.0;
+    }
+  }
+  if (lane == 0) delta_tmp[0] = c0;
+  __syncwarp();
+  double delta = c0;
+  int fail = 0;
+  cplx k = mk(0.0, 0.0);
+  if (n > 1) {
+    const cplx e1 = e[1];
+    const double inv = 1.0 / delta;
+    k = mk(-e1.re * inv, -e1.im * inv);
+  }
+  for (int m = 0; m + 1 < n; ++m) {
+    const cplx kc = conjg(k);
+    const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
+    cplx knext = mk(0.0, 0.0);
+    if (m + 2 < n) {  // lookahead from pre-update values
+      const cplx e2 = e[m + 2];
+      const cplx b1 = mk(__shfl_sync(0xffffffffu, Breg[0].re, 1), __shfl_sync(0xffffffffu, Breg[0].im, 1));
+      const cplx emn = cadd(e2, cmul(k, b1));
+      const double invn = 1.0 / dnext;
+      knext = mk(-emn.re * invn, -emn.im * invn);
+      __syncwarp();
+    }
+    const int cnt = n - 1 - m;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = lane + 32 * q;
+      if (j < cnt) {
+        const cplx ej = e[j + m + 1];
+        const cplx bj = Breg[q];
+        if (j > 0) e[j + m + 1] = cadd(ej, cmul(k, bj));
+        Breg[q] = cadd(bj, cmul(kc, ej));
+      }
+    }
+    const int top = m + 1;
+    const int npair = (top + 1) / 2;
+    if (lane == 0) a[top] = k;  // k * conj(a_0), a_0 = 1
+    for (int i = 1 + lane; i <= npair; i += 32) {
+      const int jj = top - i;
+      if (i < jj) {
+        const cplx ai = a[i], aj = a[jj];
+        a[i] = cadd(ai, cmul(k, conjg(aj)));
+        a[jj] = cadd(aj, cmul(k, conjg(ai)));
+      } else if (i == jj) {
+        const cplx ai = a[i];
+        a[i] = cadd(ai, cmul(k, conjg(ai)));
+      }
+    }
+    if (lane == 0) delta_tmp[m + 1] = dnext;
+    __syncwarp();
+    delta = dnext;
+    if (!(delta > floor_)) { fail = 1; break; }
+    k = knext;
+  }
+  if (fail) {
+    F.status = kNotPD;
+    return F;
+  }
+  F.delta_last = delta;
+  double part = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
+    rho[j] = conjg(a[n - 1 - j]);
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+#endif
+
 SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
                               double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
 #ifndef SLSE_HOST_EMU
+  if (b.nt == 32 && __isShared(e) && __isShared(a)) {
+    if (n <= 256) return toeplitz_factor_warp<8>(c, n, e, a, delta_out, delta_tmp, rho, b);
+    if (n <= 512) return toeplitz_factor_warp<16>(c, n, e, a, delta_out, delta_tmp, rho, b);
+  }
   if (__isShared(e)) return toeplitz_factor_impl<true>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
 #endif
   return toeplitz_factor_impl<false>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
