@@ -348,6 +348,26 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
       SLSE_GRID_Q(NTV, LGV, 0) SLSE_GRID_Q(NTV, LGV, 1) SLSE_GRID_Q(NTV, LGV, 2) SLSE_GRID_Q(NTV, LGV, 3) \
     }                                                                           \
     break;
+    // v3 (fused last pass) where the plan allows: L = 2^10 (NT 256), 2^11 (256), 2^7 (16: too small -> skip)
+    if (getenv("SLSE_GRID_V2") == nullptr && (lg == 10 || lg == 11)) {
+#define SLSE_GRID3_Q(NTV, LGV, QV)                                                                        \
+  case QV: {                                                                                               \
+    const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
+    e = set_smem(grid_fused_kernel<NTV, LGV, QV>, ssmem);                                                  \
+    if (e == cudaSuccess) {                                                                                \
+      grid_fused_kernel<NTV, LGV, QV><<<B, NTV, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N,   \
+                                                            (cplx*)q_grid, s_grid, tw, twlog);             \
+      e = cudaGetLastError();                                                                              \
+    }                                                                                                      \
+    return e == cudaSuccess ? 0 : fail("grid_fused_kernel", e);                                            \
+  }
+      if (lg == 10) {
+        switch (q) { SLSE_GRID3_Q(256, 10, 0) SLSE_GRID3_Q(256, 10, 1) SLSE_GRID3_Q(256, 10, 2) SLSE_GRID3_Q(256, 10, 3) }
+      } else {
+        switch (q) { SLSE_GRID3_Q(256, 11, 0) SLSE_GRID3_Q(256, 11, 1) SLSE_GRID3_Q(256, 11, 2) SLSE_GRID3_Q(256, 11, 3) }
+      }
+#undef SLSE_GRID3_Q
+    }
     switch (lg) {
       SLSE_GRID_CASE(6, 32)
       SLSE_GRID_CASE(7, 32)

@@ -348,6 +348,19 @@ struct FixedPlan<LG, LG> {
   SLSE_D static void run(cplx*, int, double, const cplx* __restrict__, int, int, int) {}
 };
 
+
+// Fixed-schedule radix-16 passes from log2(Ns) = LGNS up to LGEND (the
+// caller runs the remaining pass itself).
+template <int LG, int LGNS, int LGEND>
+struct FixedPlanMid {
+  SLSE_D static void run(cplx* x, int count, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+    if constexpr (LGNS + 4 <= LGEND) {
+      stockham_pass_inl<16, 1>(x, count, 1 << LG, 1 << LGNS, sign, tw, twlog, tid, nt);
+      FixedPlanMid<LG, LGNS + 4, LGEND>::run(x, count, sign, tw, twlog, tid, nt);
+    }
+  }
+};
+
 // radix for the pass with `rem` = n / Ns points per sub-transform left
 SLSE_D int stockham_radix(int rem, int count, int n, int nt) {
 #ifdef SLSE_HOST_EMU

@@ -387,6 +387,87 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) gri
   }
 }
 
+
+// Row 9 standalone, v3: pass 1 (pruned radix-16) reads w / rho straight from
+// HBM (no staging copy), the middle passes run in skewed shared memory, and
+// the last radix-RL pass is fused with the product-form combine: thread j
+// transforms item j of all three buffers and writes q^G and s^G at
+// l = j + r L/RL directly (coalesced), so the final spectra never touch
+// shared memory.  Requires RL = 2^(LG - 4 - 4k) in {2, 4, 8}.
+template <int NT, int LG, int Q>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_fused_kernel(
+    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n,
+    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* tw, int twlog) {
+  constexpr int L = 1 << LG;
+  constexpr int LS = L + (L >> 4);
+  constexpr int LGRL = (LG - 4) % 4;  // last radix (1 <= LGRL <= 3)
+  constexpr int RL = 1 << LGRL;
+  constexpr int PER = L / RL;         // last-pass items per buffer (== NT)
+  constexpr int NZ = 16 >> Q;
+  constexpr int P1 = L / 16;          // first-pass items per buffer
+  static_assert(LGRL >= 1 && PER == NT, "grid_fused_kernel: plan needs NT = L / RL");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x;
+  const cplx* rp = rho + (size_t)p * n;
+  const cplx* wp = w + (size_t)p * n;
+  cplx* X = (cplx*)(smem_raw + head_bytes(NT));
+  // ---- pass 1: pruned radix-16 straight from global
+  for (int it = tid; it < 3 * P1; it += NT) {
+    const int c = it / P1, j = it - c * P1;
+    cplx v[16];
+#pragma unroll
+    for (int r = 0; r < NZ; ++r) {
+      const int i = j + r * P1;
+      cplx x = mk(0.0, 0.0);
+      if (i < n) {
+        if (c == 0) x = wp[i];
+        else if (c == 1) x = rp[i];
+        else x = cscale(rp[i], (double)i);
+      }
+      v[r] = x;
+    }
+    DifPrunedStage<16, NZ, 8>::run(v, -1.0);
+    cplx* xc = X + (size_t)c * LS;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) xc[sk(j * 16 + r)] = v[brev_const(r, 16)];
+  }
+  __syncthreads();
+  // ---- middle radix-16 passes
+  FixedPlanMid<LG, 4, LG - LGRL>::run(X, 3, -1.0, tw, twlog, tid, NT);
+  // ---- last pass fused with the combine
+  const int j = tid;
+  constexpr int NS = L / RL;
+  cplx v0[RL], v1[RL], v2[RL];
+#pragma unroll
+  for (int r = 0; r < RL; ++r) {
+    v0[r] = X[sk(j + r * PER)];
+    v1[r] = X[LS + sk(j + r * PER)];
+    v2[r] = X[2 * LS + sk(j + r * PER)];
+  }
+#pragma unroll
+  for (int r = 1; r < RL; ++r) {
+    const cplx t = twid_tab(tw, twlog, j * r, LG, -1.0);
+    v0[r] = cmul(v0[r], t);
+    v1[r] = cmul(v1[r], t);
+    v2[r] = cmul(v2[r], t);
+  }
+  dft_dif<RL>(v0, -1.0);
+  dft_dif<RL>(v1, -1.0);
+  dft_dif<RL>(v2, -1.0);
+  const double inv_d = 1.0 / delta_last[p];
+  const double c2n = 2.0 - (double)n;
+  cplx* qg = q_grid + (size_t)p * L;
+  double* sgp = s_grid + (size_t)p * L;
+#pragma unroll
+  for (int r = 0; r < RL; ++r) {
+    const int l = j + r * NS;
+    const cplx a0 = v1[brev_const(r, RL)], a1 = v2[brev_const(r, RL)];
+    qg[l] = v0[brev_const(r, RL)];
+    sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+  }
+}
+
 }  // namespace slse_k
 
 // per-NT solver entry points (slse_solve_inst.cu)
