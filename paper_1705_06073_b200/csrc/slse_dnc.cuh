@@ -27,6 +27,12 @@
 namespace slse {
 
 constexpr int kDncLeaf = 32;
+// nodes up to this many steps multiply their polynomials directly (one
+// output coefficient per thread, two barriers per node) instead of through
+// batched FFTs, whose fixed barrier cost dominates at small sizes
+#ifndef SLSE_DNC_DIRECT
+#define SLSE_DNC_DIRECT 256
+#endif
 
 struct DncCtx {
   FftCtx f;
@@ -36,6 +42,7 @@ struct DncCtx {
   double d;           // current pivot (identical in every thread)
   int step;           // steps done
   int status;
+  int direct_max;     // nodes with s <= direct_max use direct products
 };
 
 #ifndef SLSE_HOST_EMU
@@ -212,6 +219,57 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       fr[sp++] = DncFrame{cf.E, cf.Bw, d.T1, d.above, h, 0};
       continue;
     }
+    if (s <= X.direct_max) {  // small node: direct products
+      const int tid = b.tid, nt = b.nt;
+      const int l1 = h + 1;
+      const cplx* T1 = d.T1;
+      if (cf.phase == 1) {
+        const cplx* E = cf.E;
+        const cplx* Bw = cf.Bw;
+        cplx* E2 = d.E2;
+        cplx* B2 = d.B2;
+        const int ne = s - h + 1, nb = s - h;
+        for (int t = tid; t < ne + nb; t += nt) {
+          const bool isE = t < ne;
+          const int j = isE ? t : t - ne;
+          const cplx* A = T1 + (isE ? 0 : 2 * l1);  // T11,T12 or T21,T22
+          cplx acc = mk(0.0, 0.0);
+          for (int i = 0; i < l1; ++i) {
+            const int k = h + j - i;  // 0 <= k <= s
+            acc = cadd(acc, cmul(A[i], E[k]));
+            if (k < s) acc = cadd(acc, cmul(A[l1 + i], Bw[k]));
+          }
+          if (isE) E2[j] = acc; else B2[j] = acc;
+        }
+        fft_barrier();
+        cf.phase = 2;
+        fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
+        continue;
+      }
+      // Theta = T2 T1 ; T_rc[k] = sum_i T2_r1[i] T1_1c[k-i] + T2_r2[i] T1_2c[k-i]
+      const int l2 = s - h + 1, ld = s + 1;
+      const cplx* T2 = d.T2;
+      cplx* T = cf.T;
+      for (int t = tid; t < 4 * ld; t += nt) {
+        const int q = t / ld, k = t - q * ld;
+        const int r = q >> 1, c = q & 1;
+        const cplx* A1 = T2 + (2 * r) * l2;
+        const cplx* A2 = T2 + (2 * r + 1) * l2;
+        const cplx* B1 = T1 + c * l1;
+        const cplx* B2p = T1 + (2 + c) * l1;
+        const int lo = k - h > 0 ? k - h : 0;
+        const int hi = k < l2 - 1 ? k : l2 - 1;
+        cplx acc = mk(0.0, 0.0);
+        for (int i = lo; i <= hi; ++i) {
+          acc = cadd(acc, cmul(A1[i], B1[k - i]));
+          acc = cadd(acc, cmul(A2[i], B2p[k - i]));
+        }
+        T[t] = acc;
+      }
+      fft_barrier();
+      --sp;
+      continue;
+    }
     if (cf.phase == 1) {  // left done: middle products give the right window
       const int l1 = h + 1;
       const cplx* T1 = d.T1;
@@ -316,6 +374,7 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   X.d = c0;
   X.step = 0;
   X.status = 0;
+  X.direct_max = SLSE_DNC_DIRECT;
   b.sync();
   // the root window is the column itself: e = b = c (c_0 forced real)
   // (E[0] and Bw[0] are c_0; E[j] = Bw[j] = c_j)
