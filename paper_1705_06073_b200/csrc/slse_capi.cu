@@ -432,6 +432,7 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
   P.dnc = N >= dnc_min_n() ? 1 : 0;
   P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
   P.grid_fused = getenv("SLSE_GRID_UNFUSED") ? 0 : 1;
+  if (const char* dd = getenv("SLSE_DNC_DIRECT_MAX")) P.dnc_direct = atoi(dd);
   const cplx* tw;
   int twlog;
   const int fmax = P.L > 2 * N ? P.L : (1 << ilog2(2 * N));

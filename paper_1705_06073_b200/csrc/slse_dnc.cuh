@@ -352,7 +352,7 @@ SLSE_HD size_t dnc_arena_elems(int s) {
 // transfer matrix storage (4 N complex), arena from dnc_arena_elems(N-1).
 SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, cplx* arena, double* delta_out,
                                    double* delta_tmp, cplx* SLSE_RESTRICT rho, const FftCtx& f, Blk& b,
-                                   int dnc_stockham = 0) {
+                                   int dnc_stockham = 0, int direct_max = SLSE_DNC_DIRECT) {
   Factor F;
   F.logdet = 0.0;
   F.status = kOk;
@@ -374,7 +374,7 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   X.d = c0;
   X.step = 0;
   X.status = 0;
-  X.direct_max = SLSE_DNC_DIRECT;
+  X.direct_max = direct_max;
   b.sync();
   // the root window is the column itself: e = b = c (c_0 forced real)
   // (E[0] and Bw[0] are c_0; E[j] = Bw[j] = c_j)

@@ -459,18 +459,25 @@ template <class Load, class Store>
 SLSE_D void fft_multi(cplx* work, int count, int n, double sign, Load ld, Store st, const FftCtx& f, Blk& b) {
   const int tid = b.tid, nt = b.nt;
   const int p = ilog2(n);
-  cplx* x = (count * n <= f.smem_cap) ? f.smem : work;
-  for (int t = tid; t < count * n; t += nt) {
-    const int c = t >> p, i = t & (n - 1);
-    x[(size_t)c * n + brev_bits((unsigned)i, p)] = ld(c, i);
+  // as many buffers per group as the shared staging holds (all of them in
+  // one group when possible); only a transform larger than the staging
+  // runs in the global work buffer
+  const int g = n <= f.smem_cap ? (f.smem_cap / n < count ? f.smem_cap / n : count) : count;
+  cplx* x = n <= f.smem_cap ? f.smem : work;
+  for (int c0 = 0; c0 < count; c0 += g) {
+    const int gc = count - c0 < g ? count - c0 : g;
+    for (int t = tid; t < gc * n; t += nt) {
+      const int c = t >> p, i = t & (n - 1);
+      x[(size_t)c * n + brev_bits((unsigned)i, p)] = ld(c0 + c, i);
+    }
+    fft_barrier();
+    fft_passes_multi(x, gc, n, sign, f.tw, f.twlog, tid, nt);
+    for (int t = tid; t < gc * n; t += nt) {
+      const int c = t >> p, i = t & (n - 1);
+      st(c0 + c, i, x[(size_t)c * n + i]);
+    }
+    fft_barrier();
   }
-  fft_barrier();
-  fft_passes_multi(x, count, n, sign, f.tw, f.twlog, tid, nt);
-  for (int t = tid; t < count * n; t += nt) {
-    const int c = t >> p, i = t & (n - 1);
-    st(c, i, x[(size_t)c * n + i]);
-  }
-  fft_barrier();
 }
 
 SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b) {

@@ -45,6 +45,7 @@ struct SolveParams {
   int dnc;  // 1: superfast divide-and-conquer Schur (slse_dnc.cuh), 0: Schur-Levinson
   int dnc_stockham;  // product transforms with the register Stockham passes
   int grid_fused;    // activation grid via the zero-padding-aware R x M decomposition
+  int dnc_direct;    // superfast nodes up to this many steps use direct products
 };
 
 // Launch-uniform parameters from the C-ABI options (estimator.py:34-50).
@@ -68,6 +69,7 @@ SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   P.dnc = 0;
   P.dnc_stockham = 0;
   P.grid_fused = 1;
+  P.dnc_direct = SLSE_DNC_DIRECT;
   return P;
 }
 
@@ -345,7 +347,7 @@ struct Solver {
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
     steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
-    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham)
+    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham, P.dnc_direct)
                      : toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
     if (F.status != kOk) return F.status;
     B.delta_last = F.delta_last;
