@@ -161,8 +161,8 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
 
 // forward transform of src[0..len) zero padded to F -> dst[0..F)
 SLSE_D void dnc_fwd(cplx* dst, const cplx* src, int len, int F, cplx* work, const FftCtx& f, Blk& b) {
-  fft(work, F, -1.0, [&](int i) { return i < len ? src[i] : mk(0.0, 0.0); },
-      [&](int i, cplx v) { dst[i] = v; }, f, b);
+  fft(work, F, -1.0, [=](int i) { return i < len ? src[i] : mk(0.0, 0.0); },
+      [=](int i, cplx v) { dst[i] = v; }, f, b);
 }
 
 // One internal node's buffers, all carved from `base` (see dnc_arena_elems);
@@ -278,23 +278,23 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       cplx* S = d.S;  // S[0..3] = spectra of T1, S[4] = E, S[5] = Bw (contiguous: S, SE, SB)
       // six forward transforms in one batch (SE, SB follow S contiguously)
       fft_multi(d.work_multi, 6, F, -1.0,
-                [&](int q, int i) {
+                [=](int q, int i) {
                   if (q < 4) return i < l1 ? T1[q * l1 + i] : mk(0.0, 0.0);
                   if (q == 4) return i <= s ? E[i] : mk(0.0, 0.0);
                   return i < s ? Bw[i] : mk(0.0, 0.0);
                 },
-                [&](int q, int i, cplx v) { S[(size_t)q * F + i] = v; }, X.f, b);
+                [=](int q, int i, cplx v) { S[(size_t)q * F + i] = v; }, X.f, b);
       const cplx* SE = d.SE;
       const cplx* SB = d.SB;
       cplx* E2 = d.E2;
       cplx* B2 = d.B2;
       // E2 = (T11 E + T12 Bw)[h..s], B2 = (T21 E + T22 Bw)[h..s-1]
       fft_multi(d.work_multi, 2, F, 1.0,
-                [&](int q, int k) {
+                [=](int q, int k) {
                   return q == 0 ? cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k]))
                                 : cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k]));
                 },
-                [&](int q, int i, cplx v) {
+                [=](int q, int i, cplx v) {
                   if (q == 0) {
                     if (i >= h && i <= s) E2[i - h] = cscale(v, invF);
                   } else if (i >= h && i < s) {
@@ -312,19 +312,19 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       const cplx* T2 = d.T2;
       cplx* A = d.above;            // 4 F : spectra of T2
       cplx* wk = d.above + 4 * (size_t)F;  // 4 F global work
-      fft_multi(wk, 4, F, -1.0, [&](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
-                [&](int q, int i, cplx v) { A[(size_t)q * F + i] = v; }, X.f, b);
+      fft_multi(wk, 4, F, -1.0, [=](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
+                [=](int q, int i, cplx v) { A[(size_t)q * F + i] = v; }, X.f, b);
       const cplx* S = d.S;
       cplx* T = cf.T;
       const int ld = s + 1;
       // T_rc = A_r1 S_1c + A_r2 S_2c ; output q = 2 r + c
       fft_multi(wk, 4, F, 1.0,
-                [&](int q, int k) {
+                [=](int q, int k) {
                   const int r = q >> 1, c = q & 1;
                   return cadd(cmul(A[(size_t)(2 * r) * F + k], S[(size_t)c * F + k]),
                               cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
                 },
-                [&](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
+                [=](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
       --sp;
     }
   }

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NT) apply_kernel(const cplx* rho, const double
   const int nf = 1 << ilog2(2 * n);
   cplx* yh = scratch + (size_t)p * 4 * nf;
   const cplx* yp = y + (size_t)p * n;
-  fft(yh, nf, -1.0, [&](int i) { return i < n ? yp[i] : mk(0.0, 0.0); }, [&](int i, cplx v) { yh[i] = v; }, f, b);
+  fft(yh, nf, -1.0, [=](int i) { return i < n ? yp[i] : mk(0.0, 0.0); }, [=](int i, cplx v) { yh[i] = v; }, f, b);
   double qd = gs_apply(rho + (size_t)p * n, n, delta_last[p], yp, yh, yh + nf, yh + 2 * nf, yh + 3 * nf,
                        w + (size_t)p * n, f, b);
   if (quad && threadIdx.x == 0) quad[p] = qd;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) gri
   cplx* X = (cplx*)(smem_raw + head_bytes(NT));
   cplx* stage = X + 3 * LS;  // [2][2][n] : buffer, (w, rho), point
   const int tid = threadIdx.x;
-  auto prefetch = [&](int prob, int buf) {
+  auto prefetch = [=](int prob, int buf) {
     const cplx* wp = w + (size_t)prob * n;
     const cplx* rp = rho + (size_t)prob * n;
     cplx* sw = stage + (size_t)buf * 2 * n;

@@ -798,8 +798,8 @@ struct Solver {
     for (int i = b.tid; i < kmax; i += b.nt) { z[i] = 0; theta[i] = 0.0; gamma[i] = 0.0; }
     k = 0;
     // cached spectrum of y for every GS apply
-    fft(yhat, 1 << ilog2(2 * n), -1.0, [&](int i) { return i < n ? y[i] : mk(0.0, 0.0); },
-        [&](int i, cplx v) { yhat[i] = v; }, f, b);
+    fft(yhat, 1 << ilog2(2 * n), -1.0, [=](int i) { return i < n ? y[i] : mk(0.0, 0.0); },
+        [=](int i, cplx v) { yhat[i] = v; }, f, b);
     status = ensure_cur();
     if (status != kOk) { finish(0, 0); return; }
     record(kStInit);

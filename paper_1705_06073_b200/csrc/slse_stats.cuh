@@ -156,10 +156,10 @@ SLSE_NI void grid_eval(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT 
                       int L, cplx* G0, cplx* G1, cplx* G2, double* sg, const FftCtx& f, Blk& b) {
   const int tid_ = b.tid, nt_ = b.nt;
   const cplx z = mk(0.0, 0.0);
-  fft(G0, L, -1.0, [&](int i) { return i < n ? w[i] : z; }, [&](int i, cplx v) { G0[i] = v; }, f, b);
-  fft(G1, L, -1.0, [&](int i) { return i < n ? rho[i] : z; }, [&](int i, cplx v) { G1[i] = v; }, f, b);
-  fft(G2, L, -1.0, [&](int i) { return i < n ? cscale(rho[i], (double)i) : z; },
-      [&](int i, cplx v) { G2[i] = v; }, f, b);
+  fft(G0, L, -1.0, [=](int i) { return i < n ? w[i] : z; }, [=](int i, cplx v) { G0[i] = v; }, f, b);
+  fft(G1, L, -1.0, [=](int i) { return i < n ? rho[i] : z; }, [=](int i, cplx v) { G1[i] = v; }, f, b);
+  fft(G2, L, -1.0, [=](int i) { return i < n ? cscale(rho[i], (double)i) : z; },
+      [=](int i, cplx v) { G2[i] = v; }, f, b);
   const double c2n = 2.0 - (double)n;
   const double inv_d = 1.0 / delta_last;
   for (int l = tid_; l < L; l += nt_) {

@@ -333,8 +333,8 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
   const cplx rlast = rho[n - 1];
   // P = FFT(rho zero-padded)
   fft(P, nf, -1.0,
-      [&](int i) { return i < n ? rho[i] : mk(0.0, 0.0); },
-      [&](int i, cplx v) { P[i] = v; }, f, b);
+      [=](int i) { return i < n ? rho[i] : mk(0.0, 0.0); },
+      [=](int i, cplx v) { P[i] = v; }, f, b);
   // U = Xhat * P1 ; V = Xhat * P0h
   for (int k = tid_; k < nf; k += nt_) {
     const cplx p1 = P[k];
