@@ -219,8 +219,9 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
     SLSE_DISPATCH_NT(nt, {
       e = set_smem(factor_dnc_kernel<NTC>, smem);
       if (e == cudaSuccess) {
+        const char* dd = getenv("SLSE_DNC_DIRECT_MAX");
         factor_dnc_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)c, N, (cplx*)rho, delta, logdet, status, scratch, per,
-                                                    dscr, tw, twlog, cap);
+                                                    dscr, tw, twlog, cap, dd ? atoi(dd) : SLSE_DNC_DIRECT);
         e = cudaGetLastError();
       }
     });

@@ -27,10 +27,14 @@ struct FftCtx {
   int stockham = 0; // 1: prefer the register Stockham passes when they fit
 };
 
-SLSE_HD int ilog2(int n) {
+SLSE_HD int ilog2(int n) {  // ceil(log2 n), n >= 1
+#if defined(__CUDA_ARCH__)
+  return n <= 1 ? 0 : 32 - __clz(n - 1);
+#else
   int p = 0;
   while ((1 << p) < n) ++p;
   return p;
+#endif
 }
 
 SLSE_D unsigned brev_bits(unsigned i, int p) {
@@ -73,7 +77,7 @@ SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx
   if (p & 1) {
     const int per = n >> 1;
     for (int t = tid; t < count * per; t += nt) {
-      const int c = t / per, u = t - c * per;
+      const int c = t >> (p - 1), u = t & (per - 1);
       cplx* xc = x + (size_t)c * n;
       cplx x0 = xc[2 * u], x1 = xc[2 * u + 1];
       xc[2 * u] = cadd(x0, x1);
@@ -86,7 +90,7 @@ SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx
   for (; lgh + 2 <= p; lgh += 2) {
     const int h = 1 << lgh;
     for (int t = tid; t < count * per; t += nt) {
-      const int c = t / per, u = t - c * per;
+      const int c = t >> (p - 2), u = t & (per - 1);
       cplx* xc = x + (size_t)c * n;
       const int pos = u & (h - 1);
       const int base = ((u >> lgh) << (lgh + 2)) + pos;
