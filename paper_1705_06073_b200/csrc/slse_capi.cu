@@ -220,8 +220,21 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
       e = set_smem(factor_dnc_kernel<NTC>, smem);
       if (e == cudaSuccess) {
         const char* dd = getenv("SLSE_DNC_DIRECT_MAX");
+        long long* prof = nullptr;
+        if (getenv("SLSE_DNC_PROF")) {  // debug: phase clocks of problem 0, printed to stderr
+          cudaMalloc(&prof, 8 * sizeof(long long));
+          cudaMemsetAsync(prof, 0, 8 * sizeof(long long), st);
+        }
         factor_dnc_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)c, N, (cplx*)rho, delta, logdet, status, scratch, per,
-                                                    dscr, tw, twlog, cap, dd ? atoi(dd) : SLSE_DNC_DIRECT);
+                                                    dscr, tw, twlog, cap, dd ? atoi(dd) : SLSE_DNC_DIRECT, prof);
+        if (prof) {
+          long long h[8];
+          cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fprintf(stderr, "[dnc prof N=%d] leaf %lld direct1 %lld direct2 %lld fft1 %lld fft2 %lld total %lld cycles\n",
+                  N, h[0], h[1], h[2], h[3], h[4], h[5]);
+          cudaFree(prof);
+        }
         e = cudaGetLastError();
       }
     });

@@ -43,7 +43,16 @@ struct DncCtx {
   int step;           // steps done
   int status;
   int direct_max;     // nodes with s <= direct_max use direct products
+  long long* prof;    // optional: clock64 per phase (leaf, direct1, direct2, fft1, fft2, total)
 };
+
+SLSE_D long long dnc_clock() {
+#ifdef SLSE_HOST_EMU
+  return 0;
+#else
+  return clock64();
+#endif
+}
 
 #ifndef SLSE_HOST_EMU
 SLSE_D cplx shfl_c(cplx v, int src) {
@@ -111,11 +120,24 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
     cplx t22 = mk(lane == 0 ? 1.0 : 0.0, 0.0);
     cplx x11 = mk(0.0, 0.0), x12 = mk(0.0, 0.0), x21 = mk(0.0, 0.0), x22 = mk(0.0, 0.0);
     double d = X.d;
+    double* dtmp = X.delta_tmp + X.step;
+    const double floor_ = X.floor_;
     int st = 0;
-    for (int t = 0; t < s; ++t) {
+    cplx k;
+    {
       const cplx e0 = shfl_c(ej, 0);
       const double inv = 1.0 / d;
-      const cplx k = mk(-e0.re * inv, -e0.im * inv), kc = conjg(k);
+      k = mk(-e0.re * inv, -e0.im * inv);
+    }
+    for (int t = 0; t < s; ++t) {
+      // next coefficient straight from lane 1's pre-update pair: off the
+      // shift/broadcast path, so one step costs ~ a reciprocal, not shuffles
+      const cplx ej1 = shfl_c(ej, 1), bj1 = shfl_c(bj, 1);
+      const cplx kc = conjg(k);
+      const double dn = d * (1.0 - (k.re * k.re + k.im * k.im));
+      const double invn = 1.0 / dn;
+      const cplx enext = cadd(ej1, cmul(k, bj1));
+      const cplx knext = mk(-enext.re * invn, -enext.im * invn);
       const cplx en = cadd(ej, cmul(k, bj));
       const cplx bn = cadd(bj, cmul(kc, ej));
       ej = shfl_down_c(en, 1);
@@ -130,9 +152,10 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
       const cplx m21 = cadd(cmul(kc, x11), l21), m22 = cadd(cmul(kc, x12), l22);
       t11 = n11; t12 = n12; t21 = n21; t22 = n22;
       x11 = m11; x12 = m12; x21 = m21; x22 = m22;
-      d = d * (1.0 - (k.re * k.re + k.im * k.im));
-      if (lane == 0) X.delta_tmp[X.step + t + 1] = d;
-      if (!(d > X.floor_)) { st = kNotPD; break; }
+      d = dn;
+      if (lane == 0) dtmp[t + 1] = d;
+      if (!(d > floor_)) { st = kNotPD; break; }
+      k = knext;
     }
     if (lane < ld) {
       T[lane] = t11;
@@ -203,11 +226,15 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
   DncFrame fr[40];
   int sp = 0;
   fr[sp++] = DncFrame{E0, Bw0, T0, X.arena, s0, 0};
+  const bool prof = X.prof != nullptr && b.tid == 0;
+  const long long tstart = dnc_clock();
   while (sp > 0 && !X.status) {
     DncFrame& cf = fr[sp - 1];
     const int s = cf.s;
+    const long long t0 = prof ? dnc_clock() : 0;
     if (s <= kDncLeaf) {
       dnc_leaf(X, cf.E + 1, cf.Bw, s, cf.T, b);
+      if (prof) X.prof[0] += dnc_clock() - t0;
       --sp;
       continue;
     }
@@ -229,6 +256,18 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         cplx* E2 = d.E2;
         cplx* B2 = d.B2;
         const int ne = s - h + 1, nb = s - h;
+        if (4 * l1 + 2 * s + 1 <= X.f.smem_cap) {  // operands to shared memory (latency)
+          cplx* sT = X.f.smem;
+          cplx* sE = sT + 4 * l1;
+          cplx* sB = sE + (s + 1);
+          for (int i = tid; i < 4 * l1; i += nt) sT[i] = T1[i];
+          for (int i = tid; i <= s; i += nt) sE[i] = E[i];
+          for (int i = tid; i < s; i += nt) sB[i] = Bw[i];
+          fft_barrier();
+          T1 = sT;
+          E = sE;
+          Bw = sB;
+        }
         for (int t = tid; t < ne + nb; t += nt) {
           const bool isE = t < ne;
           const int j = isE ? t : t - ne;
@@ -242,6 +281,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
           if (isE) E2[j] = acc; else B2[j] = acc;
         }
         fft_barrier();
+        if (prof) X.prof[1] += dnc_clock() - t0;
         cf.phase = 2;
         fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
         continue;
@@ -250,6 +290,15 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       const int l2 = s - h + 1, ld = s + 1;
       const cplx* T2 = d.T2;
       cplx* T = cf.T;
+      if (4 * (l1 + l2) <= X.f.smem_cap) {
+        cplx* s1 = X.f.smem;
+        cplx* s2 = s1 + 4 * l1;
+        for (int i = tid; i < 4 * l1; i += nt) s1[i] = T1[i];
+        for (int i = tid; i < 4 * l2; i += nt) s2[i] = T2[i];
+        fft_barrier();
+        T1 = s1;
+        T2 = s2;
+      }
       for (int t = tid; t < 4 * ld; t += nt) {
         const int q = t / ld, k = t - q * ld;
         const int r = q >> 1, c = q & 1;
@@ -267,6 +316,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         T[t] = acc;
       }
       fft_barrier();
+      if (prof) X.prof[2] += dnc_clock() - t0;
       --sp;
       continue;
     }
@@ -302,6 +352,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
                   }
                 },
                 X.f, b);
+      if (prof) X.prof[3] += dnc_clock() - t0;
       cf.phase = 2;
       fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
       continue;
@@ -325,9 +376,11 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
                               cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
                 },
                 [=](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
+      if (prof) X.prof[4] += dnc_clock() - t0;
       --sp;
     }
   }
+  if (prof) X.prof[5] += dnc_clock() - tstart;
 }
 
 // arena size (complex elements) needed by dnc_split for s steps: own
@@ -352,7 +405,8 @@ SLSE_HD size_t dnc_arena_elems(int s) {
 // transfer matrix storage (4 N complex), arena from dnc_arena_elems(N-1).
 SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, cplx* arena, double* delta_out,
                                    double* delta_tmp, cplx* SLSE_RESTRICT rho, const FftCtx& f, Blk& b,
-                                   int dnc_stockham = 0, int direct_max = SLSE_DNC_DIRECT) {
+                                   int dnc_stockham = 0, int direct_max = SLSE_DNC_DIRECT,
+                                   long long* prof = nullptr) {
   Factor F;
   F.logdet = 0.0;
   F.status = kOk;
@@ -375,6 +429,7 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   X.step = 0;
   X.status = 0;
   X.direct_max = direct_max;
+  X.prof = prof;
   b.sync();
   // the root window is the column itself: e = b = c (c_0 forced real)
   // (E[0] and Bw[0] are c_0; E[j] = Bw[j] = c_j)

@@ -265,14 +265,15 @@ template <int NT>
 __global__ void __launch_bounds__(NT) factor_dnc_kernel(const cplx* c, int n, cplx* rho, double* delta, double* logdet,
                                                         int* status, cplx* scratch, size_t per_problem,
                                                         double* dscratch, const cplx* tw, int twlog, int fft_cap,
-                                                        int direct_max) {
+                                                        int direct_max, long long* prof) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
   FftCtx f{tw, twlog, (cplx*)(smem_raw + kHeadBytes), fft_cap};
   const int p = blockIdx.x;
   cplx* T = scratch + (size_t)p * per_problem;
   Factor F = toeplitz_factor_dnc(c + (size_t)p * n, n, T, T + 4 * (size_t)n, delta ? delta + (size_t)p * n : nullptr,
-                                 dscratch + (size_t)p * n, rho + (size_t)p * n, f, b, 0, direct_max);
+                                 dscratch + (size_t)p * n, rho + (size_t)p * n, f, b, 0, direct_max,
+                                 (prof && p == 0) ? prof : nullptr);
   if (threadIdx.x == 0) {
     logdet[p] = F.logdet;
     status[p] = F.status;
