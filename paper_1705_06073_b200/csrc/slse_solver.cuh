@@ -346,6 +346,7 @@ struct Solver {
   // Bundle for (th[0..kk), ga[0..kk), beta): model_core.py:257-274
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
+    if (kk == 0) return build_white(B, be);
     steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
     Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham, P.dnc_direct)
                      : toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
@@ -354,6 +355,29 @@ struct Solver {
     B.logdet = F.logdet;
     double quad = gs_apply(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b);
     B.data_term = F.logdet + quad;
+    B.stats_valid = 0;
+    return kOk;
+  }
+
+  // Empty active set: C = beta I.  The recursion's reflection coefficients
+  // are all exactly zero, so rho = e_{N-1}, every pivot is beta and
+  // C^{-1} y = y / beta (exact; the reference's LD produces the same rho and
+  // pivots bit for bit, toeplitz.py:135-142).
+  SLSE_NIM int build_white(Bundle& B, double be) {
+    if (!(be > 0.0)) return kBadColumn;  // c_0 must be real positive (toeplitz.py:55-57)
+    const int tid_ = b.tid, nt_ = b.nt;
+    const double inv = 1.0 / be;
+    double qp = 0.0;
+    for (int i = tid_; i < n; i += nt_) {
+      B.rho[i] = mk(i == n - 1 ? 1.0 : 0.0, 0.0);
+      const cplx wi = cscale(y[i], inv);
+      B.w[i] = wi;
+      qp += y[i].re * wi.re + y[i].im * wi.im;
+    }
+    const double quad = b.sum(qp);
+    B.delta_last = be;
+    B.logdet = (double)n * log(be);
+    B.data_term = B.logdet + quad;
     B.stats_valid = 0;
     return kOk;
   }

@@ -42,16 +42,27 @@ def main():
     src = list(csv.reader(io.StringIO(ncu([a.report, "--page", "source", "--csv", "--print-source=cuda,sass"]))))
     fp = None
     res = []
+    ins = []
+    hdr = None
     for r in src:
         if not r:
             continue
         if r[0] == "File Path":
             fp = r[1].split("/")[-1]
             continue
-        if r[0] in ("Function Name", "Line No"):
+        if r[0] == "Line No":
+            hdr = r
+            continue
+        if r[0] == "Function Name":
             continue
         if len(r) > 4 and r[2] == "-" and r[0].isdigit() and r[4].isdigit():
             res.append((int(r[4]), fp, int(r[0]), r[1].strip()[:90]))
+            if hdr and "Instructions Executed" in hdr:
+                v = r[hdr.index("Instructions Executed")].replace(",", "")
+                try:
+                    ins.append((float(v), fp, int(r[0]), r[1].strip()[:90]))
+                except ValueError:
+                    pass
     tot = sum(x[0] for x in res) or 1
     per_file = defaultdict(int)
     for s, f, _, _ in res:
@@ -60,6 +71,11 @@ def main():
     print(f"\ntop {a.top} source lines by warp-stall samples:")
     for s, f, ln, text in sorted(res, reverse=True)[: a.top]:
         print(f"  {100 * s / tot:5.1f}%  {f}:{ln}  {text}")
+    if ins:
+        itot = sum(x[0] for x in ins) or 1
+        print(f"\ntop {a.top} source lines by warp instructions executed (total {itot:.3g}):")
+        for s, f, ln, text in sorted(ins, reverse=True)[: a.top]:
+            print(f"  {100 * s / itot:5.1f}%  {f}:{ln}  {text}")
 
 
 if __name__ == "__main__":
