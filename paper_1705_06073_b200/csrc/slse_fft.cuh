@@ -431,8 +431,11 @@ SLSE_NI void fft_stockham_v(cplx* x, int n, double sign, const cplx* __restrict_
   }
 }
 
+// Stockham wins for wide blocks (cfg3: 187 vs 195 ms), DIT for one-warp
+// solvers (cfg2: 49 vs 69 ms), measured on B200.
 SLSE_D bool use_stockham(const FftCtx& f, int n, int nt) {
-  return (SLSE_SOLVER_STOCKHAM || f.stockham) && n >= 4 && sk_len(n) <= f.smem_cap && stockham_ok(1, n, nt);
+  return (SLSE_SOLVER_STOCKHAM || f.stockham || nt >= 256) && n >= 4 && sk_len(n) <= f.smem_cap &&
+         stockham_ok(1, n, nt);
 }
 
 template <class Load, class Store>
