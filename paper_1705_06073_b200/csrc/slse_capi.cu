@@ -203,7 +203,7 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
     const int F = 1 << ilog2(N);
     int rc = twiddles(ilog2(F > 16 ? F : 16), st, &tw, &twlog);
     if (rc) return rc;
-    const int nt = N <= 2048 ? 256 : 1024;
+    const int nt = N <= 2048 ? 256 : 512;  // 1024 threads cap registers at 64 and the leaves spill
     int cap = 1;
     while (16 * (size_t)sk_len(cap * 2) <= kRegionBudget) cap *= 2;
     if (cap > F) cap = F;

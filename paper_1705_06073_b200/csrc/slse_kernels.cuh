@@ -390,6 +390,9 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) gri
 }
 
 
+#ifndef SLSE_GRID_MINB
+#define SLSE_GRID_MINB 3
+#endif
 // Row 9 standalone, v3: pass 1 (pruned radix-16) reads w / rho straight from
 // HBM (no staging copy), the middle passes run in skewed shared memory, and
 // the last radix-RL pass is fused with the product-form combine: thread j
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) gri
 // l = j + r L/RL directly (coalesced), so the final spectra never touch
 // shared memory.  Requires RL = 2^(LG - 4 - 4k) in {2, 4, 8}.
 template <int NT, int LG, int Q>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_fused_kernel(
+__global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fused_kernel(
     const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n,
     cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* tw, int twlog) {
   constexpr int L = 1 << LG;
@@ -437,36 +440,42 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1)) grid_fused_kernel(
   __syncthreads();
   // ---- middle radix-16 passes
   FixedPlanMid<LG, 4, LG - LGRL>::run(X, 3, -1.0, tw, twlog, tid, NT);
-  // ---- last pass fused with the combine
+  // ---- last pass fused with the combine (q^G first, then the (A0, A1)
+  // pair, keeping at most 2 RL complex values live)
   const int j = tid;
   constexpr int NS = L / RL;
-  cplx v0[RL], v1[RL], v2[RL];
+  cplx* qg = q_grid + (size_t)p * L;
+  double* sgp = s_grid + (size_t)p * L;
+  {
+    cplx v0[RL];
+#pragma unroll
+    for (int r = 0; r < RL; ++r) v0[r] = X[sk(j + r * PER)];
+#pragma unroll
+    for (int r = 1; r < RL; ++r) v0[r] = cmul(v0[r], twid_tab(tw, twlog, j * r, LG, -1.0));
+    dft_dif<RL>(v0, -1.0);
+#pragma unroll
+    for (int r = 0; r < RL; ++r) qg[j + r * NS] = v0[brev_const(r, RL)];
+  }
+  const double inv_d = 1.0 / delta_last[p];
+  const double c2n = 2.0 - (double)n;
+  cplx v1[RL], v2[RL];
 #pragma unroll
   for (int r = 0; r < RL; ++r) {
-    v0[r] = X[sk(j + r * PER)];
     v1[r] = X[LS + sk(j + r * PER)];
     v2[r] = X[2 * LS + sk(j + r * PER)];
   }
 #pragma unroll
   for (int r = 1; r < RL; ++r) {
     const cplx t = twid_tab(tw, twlog, j * r, LG, -1.0);
-    v0[r] = cmul(v0[r], t);
     v1[r] = cmul(v1[r], t);
     v2[r] = cmul(v2[r], t);
   }
-  dft_dif<RL>(v0, -1.0);
   dft_dif<RL>(v1, -1.0);
   dft_dif<RL>(v2, -1.0);
-  const double inv_d = 1.0 / delta_last[p];
-  const double c2n = 2.0 - (double)n;
-  cplx* qg = q_grid + (size_t)p * L;
-  double* sgp = s_grid + (size_t)p * L;
 #pragma unroll
   for (int r = 0; r < RL; ++r) {
-    const int l = j + r * NS;
     const cplx a0 = v1[brev_const(r, RL)], a1 = v2[brev_const(r, RL)];
-    qg[l] = v0[brev_const(r, RL)];
-    sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+    sgp[j + r * NS] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
   }
 }
 
