@@ -222,17 +222,18 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
         const char* dd = getenv("SLSE_DNC_DIRECT_MAX");
         long long* prof = nullptr;
         if (getenv("SLSE_DNC_PROF")) {  // debug: phase clocks of problem 0, printed to stderr
-          cudaMalloc(&prof, 8 * sizeof(long long));
-          cudaMemsetAsync(prof, 0, 8 * sizeof(long long), st);
+          cudaMalloc(&prof, 16 * sizeof(long long));
+          cudaMemsetAsync(prof, 0, 16 * sizeof(long long), st);
         }
         factor_dnc_kernel<NTC><<<B, NTC, smem, st>>>((const cplx*)c, N, (cplx*)rho, delta, logdet, status, scratch, per,
                                                     dscr, tw, twlog, cap, dd ? atoi(dd) : SLSE_DNC_DIRECT, prof);
         if (prof) {
-          long long h[8];
+          long long h[16];
           cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
           cudaStreamSynchronize(st);
-          fprintf(stderr, "[dnc prof N=%d] leaf %lld direct1 %lld direct2 %lld fft1 %lld fft2 %lld total %lld cycles\n",
-                  N, h[0], h[1], h[2], h[3], h[4], h[5]);
+          fprintf(stderr, "[dnc prof N=%d] leaf %lld direct1 %lld direct2 %lld fft1 %lld fft2 %lld total %lld cycles;"
+                          " fft by F=512..: %lld %lld %lld %lld %lld %lld\n",
+                  N, h[0], h[1], h[2], h[3], h[4], h[5], h[8], h[9], h[10], h[11], h[12], h[13]);
           cudaFree(prof);
         }
         e = cudaGetLastError();

@@ -352,7 +352,12 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
                   }
                 },
                 X.f, b);
-      if (prof) X.prof[3] += dnc_clock() - t0;
+      if (prof) {
+        const long long dt = dnc_clock() - t0;
+        X.prof[3] += dt;
+        const int lv = ilog2(F) - 9;
+        if (lv >= 0 && lv < 8) X.prof[8 + lv] += dt;
+      }
       cf.phase = 2;
       fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
       continue;
@@ -376,7 +381,12 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
                               cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
                 },
                 [=](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
-      if (prof) X.prof[4] += dnc_clock() - t0;
+      if (prof) {
+        const long long dt = dnc_clock() - t0;
+        X.prof[4] += dt;
+        const int lv = ilog2(F) - 9;
+        if (lv >= 0 && lv < 8) X.prof[8 + lv] += dt;
+      }
       --sp;
     }
   }
