@@ -257,19 +257,11 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
       __syncwarp();
     }
     const int cnt = n - 1 - m;
-    // all loads first (clamped in-bounds indices, results masked) so the
-    // eight shared-memory reads are in flight together
-    cplx ev[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int idx = lane + 32 * q + m + 1;
-      ev[q] = e[idx < n ? idx : n - 1];
-    }
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int j = lane + 32 * q;
       if (j < cnt) {
-        const cplx ej = ev[q];
+        const cplx ej = e[j + m + 1];
         const cplx bj = Breg[q];
         if (j > 0) e[j + m + 1] = cadd(ej, cmul(k, bj));
         Breg[q] = cadd(bj, cmul(kc, ej));
@@ -278,25 +270,15 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     const int top = m + 1;
     const int npair = (top + 1) / 2;
     if (lane == 0) a[top] = k;  // k * conj(a_0), a_0 = 1
-    constexpr int U = (Q + 1) / 2;  // pairs per lane: npair <= n / 2 <= 16 Q
-    cplx ai[U], aj[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int i = 1 + lane + 32 * u;
-      i = i <= npair ? i : npair;
-      ai[u] = a[i];
-      aj[u] = a[top - i];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = 1 + lane + 32 * u, jj = top - i;
-      if (i <= npair) {
-        if (i < jj) {
-          a[i] = cadd(ai[u], cmul(k, conjg(aj[u])));
-          a[jj] = cadd(aj[u], cmul(k, conjg(ai[u])));
-        } else if (i == jj) {
-          a[i] = cadd(ai[u], cmul(k, conjg(ai[u])));
-        }
+    for (int i = 1 + lane; i <= npair; i += 32) {
+      const int jj = top - i;
+      if (i < jj) {
+        const cplx ai = a[i], aj = a[jj];
+        a[i] = cadd(ai, cmul(k, conjg(aj)));
+        a[jj] = cadd(aj, cmul(k, conjg(ai)));
+      } else if (i == jj) {
+        const cplx ai = a[i];
+        a[i] = cadd(ai, cmul(k, conjg(ai)));
       }
     }
     if (lane == 0) delta_tmp[m + 1] = dnext;
