@@ -218,6 +218,7 @@ struct DncFrame {
   cplx* base;
   int s;
   int phase;
+  int row1;  // only Theta_11, Theta_12 are needed (the root and its right spine)
 };
 
 // Transfer matrix of s steps (iterative post-order traversal; an explicit
@@ -225,7 +226,7 @@ struct DncFrame {
 SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx* T0, Blk& b) {
   DncFrame fr[40];
   int sp = 0;
-  fr[sp++] = DncFrame{E0, Bw0, T0, X.arena, s0, 0};
+  fr[sp++] = DncFrame{E0, Bw0, T0, X.arena, s0, 0, 1};
   const bool prof = X.prof != nullptr && b.tid == 0;
   const long long tstart = dnc_clock();
   while (sp > 0 && !X.status) {
@@ -243,7 +244,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
     const double invF = 1.0 / (double)F;
     if (cf.phase == 0) {  // descend into the left half
       cf.phase = 1;
-      fr[sp++] = DncFrame{cf.E, cf.Bw, d.T1, d.above, h, 0};
+      fr[sp++] = DncFrame{cf.E, cf.Bw, d.T1, d.above, h, 0, 0};
       continue;
     }
     if (s <= X.direct_max) {  // small node: direct products
@@ -283,7 +284,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         fft_barrier();
         if (prof) X.prof[1] += dnc_clock() - t0;
         cf.phase = 2;
-        fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
+        fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0, cf.row1};
         continue;
       }
       // Theta = T2 T1 ; T_rc[k] = sum_i T2_r1[i] T1_1c[k-i] + T2_r2[i] T1_2c[k-i]
@@ -299,7 +300,8 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         T1 = s1;
         T2 = s2;
       }
-      for (int t = tid; t < 4 * ld; t += nt) {
+      const int nrow = cf.row1 ? 2 : 4;  // output blocks (row 1 only on the right spine)
+      for (int t = tid; t < nrow * ld; t += nt) {
         const int q = t / ld, k = t - q * ld;
         const int r = q >> 1, c = q & 1;
         const cplx* A1 = T2 + (2 * r) * l2;
@@ -359,7 +361,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         if (lv >= 0 && lv < 8) X.prof[8 + lv] += dt;
       }
       cf.phase = 2;
-      fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0};
+      fr[sp++] = DncFrame{d.E2, d.B2, d.T2, d.above, s - h, 0, cf.row1};
       continue;
     }
     // phase 2: Theta = T2 T1 (degree s; F >= s + 1 so no wrap)
@@ -368,13 +370,16 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       const cplx* T2 = d.T2;
       cplx* A = d.above;            // 4 F : spectra of T2
       cplx* wk = d.above + 4 * (size_t)F;  // 4 F global work
-      fft_multi(wk, 4, F, -1.0, [=](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
+      // row-1 nodes (root and right spine) only need Theta_11, Theta_12,
+      // hence only T2's first row: 2 + 2 transforms instead of 4 + 4
+      const int nq = cf.row1 ? 2 : 4;
+      fft_multi(wk, nq, F, -1.0, [=](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
                 [=](int q, int i, cplx v) { A[(size_t)q * F + i] = v; }, X.f, b);
       const cplx* S = d.S;
       cplx* T = cf.T;
       const int ld = s + 1;
       // T_rc = A_r1 S_1c + A_r2 S_2c ; output q = 2 r + c
-      fft_multi(wk, 4, F, 1.0,
+      fft_multi(wk, nq, F, 1.0,
                 [=](int q, int k) {
                   const int r = q >> 1, c = q & 1;
                   return cadd(cmul(A[(size_t)(2 * r) * F + k], S[(size_t)c * F + k]),

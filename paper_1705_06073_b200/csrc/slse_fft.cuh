@@ -469,6 +469,47 @@ SLSE_D void fft_multi(cplx* work, int count, int n, double sign, Load ld, Store 
   // as many buffers per group as the shared staging holds (all of them in
   // one group when possible); only a transform larger than the staging
   // runs in the global work buffer
+  if (n > f.smem_cap && n >= 64 && (1 << (p - (p >> 1))) <= f.smem_cap) {
+    // four-step: n = n1 n2, column transforms of n1 then rows of n2, both
+    // staged in shared memory in groups; `work` holds the intermediate.
+    const int p1 = p >> 1, p2 = p - p1;
+    const int n1 = 1 << p1, n2 = 1 << p2;
+    int G = 1;
+    while (2 * G * (n1 > n2 ? n1 : n2) <= f.smem_cap && 2 * G <= n2 && 2 * G <= n1) G *= 2;
+    cplx* x = f.smem;
+    for (int c = 0; c < count; ++c) {
+      cplx* wc = work + (size_t)c * n;
+      for (int j0 = 0; j0 < n2; j0 += G) {  // columns j2 = j0 .. j0+G-1
+        for (int t = tid; t < G * n1; t += nt) {
+          const int j1 = t / G, g = t - j1 * G;  // consecutive threads -> consecutive j2 (coalesced)
+          x[(size_t)g * n1 + brev_bits((unsigned)j1, p1)] = ld(c, (j0 + g) + n2 * j1);
+        }
+        fft_barrier();
+        fft_passes_multi(x, G, n1, sign, f.tw, f.twlog, tid, nt);
+        for (int t = tid; t < G * n1; t += nt) {
+          const int k1 = t / G, g = t - k1 * G;
+          const int j2 = j0 + g;
+          const cplx v = cmul(x[(size_t)g * n1 + k1], twid_tab(f.tw, f.twlog, (j2 * k1) & (n - 1), p, sign));
+          wc[(size_t)k1 * n2 + j2] = v;
+        }
+        fft_barrier();
+      }
+      for (int k0 = 0; k0 < n1; k0 += G) {  // rows k1 = k0 .. k0+G-1
+        for (int t = tid; t < G * n2; t += nt) {
+          const int g = t >> p2, j2 = t & (n2 - 1);
+          x[(size_t)g * n2 + brev_bits((unsigned)j2, p2)] = wc[(size_t)(k0 + g) * n2 + j2];
+        }
+        fft_barrier();
+        fft_passes_multi(x, G, n2, sign, f.tw, f.twlog, tid, nt);
+        for (int t = tid; t < G * n2; t += nt) {
+          const int k2 = t / G, g = t - k2 * G;  // consecutive threads -> consecutive k1 (coalesced)
+          st(c, (k0 + g) + n1 * k2, x[(size_t)g * n2 + k2]);
+        }
+        fft_barrier();
+      }
+    }
+    return;
+  }
   const int g = n <= f.smem_cap ? (f.smem_cap / n < count ? f.smem_cap / n : count) : count;
   cplx* x = n <= f.smem_cap ? f.smem : work;
   for (int c0 = 0; c0 < count; c0 += g) {

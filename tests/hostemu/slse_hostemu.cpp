@@ -187,3 +187,18 @@ extern "C" int emu_factor_dnc(const double* c, int n, double* rho, double* delta
   *logdet = Fa.logdet;
   return Fa.status;
 }
+
+// batched transform through fft_multi with a small staging cap (exercises the four-step path)
+extern "C" int emu_fft_multi(double* x, int count, int n, int sign, int cap) {
+  const int lg = ilog2(n) > 4 ? ilog2(n) : 4;
+  std::vector<cplx> tw = make_twiddles(lg);
+  std::vector<double> red(64);
+  std::vector<cplx> sm(cap > 0 ? cap : 1), work((size_t)count * n), out((size_t)count * n);
+  Blk b{0, 1, red.data(), 0};
+  FftCtx f{tw.data(), lg, sm.data(), cap};
+  cplx* xx = (cplx*)x;
+  fft_multi(work.data(), count, n, (double)sign, [=](int c, int i) { return xx[(size_t)c * n + i]; },
+            [&](int c, int i, cplx v) { out[(size_t)c * n + i] = v; }, f, b);
+  for (size_t i = 0; i < out.size(); ++i) xx[i] = out[i];
+  return 0;
+}
