@@ -95,7 +95,7 @@ int slse_cov_column(const double* theta, const double* gamma, const int32_t* kco
 int slse_toeplitz_factor(const double* c, int N, int B, double* rho, double* delta, double* logdet,
                          int32_t* status, void* stream);
 
-/* Same with an explicit algorithm: 0 auto (superfast from N >= 8192),
+/* Same with an explicit algorithm: 0 auto (superfast from N >= 4096),
  * 1 Schur-Levinson O(N^2) (toeplitz.levinson_durbin role),
  * 2 superfast divide-and-conquer Schur O(N log^2 N) (toeplitz.generalized_schur). */
 int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* delta, double* logdet,

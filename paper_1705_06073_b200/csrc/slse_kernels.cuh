@@ -84,7 +84,7 @@ inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false) {
 // superfast (D&C) factorisation from this N up; SLSE_DNC_MIN overrides
 inline int dnc_min_n() {
   const char* env = getenv("SLSE_DNC_MIN");
-  return env ? atoi(env) : 8192;
+  return env ? atoi(env) : 4096;
 }
 
 // ------------------------------------------------------------------ kernels

@@ -48,7 +48,7 @@ def toeplitz_factor(c, with_delta=True, raise_on_error=False, method="auto"):
     """Rows 2-4: (rho, delta, logdet, status) of the Hermitian Toeplitz
     matrices with first columns c (B, N) (toeplitz.decompose, :263-276).
     method: "levinson" (Schur-Levinson, O(N^2)), "schur" (superfast
-    divide-and-conquer, O(N log^2 N)) or "auto" (superfast from N >= 8192)."""
+    divide-and-conquer, O(N log^2 N)) or "auto" (superfast from N >= 4096)."""
     lib = _native.load()
     _c128(c)
     B, n = c.shape

@@ -151,3 +151,19 @@ def test_emulated_trajectory_superfast(cfg, b, monkeypatch):
     assert np.array_equal(encode_events(r.events), z[p + "events"])
     assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
     assert rel(r.alpha_hat[0], z[p + "alpha_hat"]) < AMP_TOL
+
+
+@pytest.mark.parametrize("n,count,cap", [(64, 3, 32), (256, 2, 64), (1024, 4, 256), (16384, 2, 8704), (8192, 1, 1024),
+                                         (128, 6, 1024)])
+def test_emulated_batched_fft(n, count, cap):
+    """fft_multi: shared-memory groups and the four-step path for transforms
+    larger than the staging capacity."""
+    import ctypes
+
+    lib = H.build()
+    rng = np.random.default_rng(n + count)
+    x = rng.standard_normal((count, n)) + 1j * rng.standard_normal((count, n))
+    for sign, ref in ((-1, np.fft.fft(x, axis=1)), (1, n * np.fft.ifft(x, axis=1))):
+        y = x.copy()
+        lib.emu_fft_multi(ctypes.c_void_p(y.ctypes.data), count, n, sign, cap)
+        assert rel(y, ref) < 1e-14
