@@ -401,14 +401,16 @@ def two_loop(mem, g):
     return -r_
 
 
-_MARGINS = None  # list receiving (kind, normalised margin) while estimate() runs
+_MARGINS = None  # list receiving (kind, normalised margin, trace length) while estimate() runs
+_TRACE = None    # the running estimate()'s objective trace (for the decision's position)
 
 
 def _margin(kind, lhs, rhs, scale):
     """Record how far a decision lhs <= rhs (or lhs < rhs) was from flipping,
-    in units of `scale` (the decision's roundoff noise)."""
+    in units of `scale` (the decision's roundoff noise), and the length of
+    the objective trace when it was taken (the trace entry it first affects)."""
     if _MARGINS is not None:
-        _MARGINS.append((kind, abs(lhs - rhs) / scale))
+        _MARGINS.append((kind, abs(lhs - rhs) / scale, len(_TRACE) if _TRACE is not None else -1))
 
 
 def lbfgs_step(mem, point, f0, g0, objective_fn, gradient_fn):
@@ -638,6 +640,7 @@ class OracleResult:
     builds: int = 0
     wall_time: float = 0.0
     min_margin: float = float("inf")  # smallest decision margin in roundoff units
+    margins: list = None  # every decision: (kind, margin, trace position)
 
 
 def estimate(y, opts: OracleOptions = None) -> OracleResult:
@@ -645,7 +648,7 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
 
     `events` is the active-set history: ("sweep", [(slot, idx)...]),
     ("activate", slot, idx), ("deactivate", [slots]) in order."""
-    global _MARGINS
+    global _MARGINS, _TRACE
     t_start = time.perf_counter()
     opts = opts or OracleOptions()
     _MARGINS = []
@@ -661,6 +664,7 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
     beta0 = max(INITIAL_BETA_ENERGY_FRACTION * energy / m, floor)
     st = _State(k_max, beta0, INITIAL_ZETA)
     trace, stages, khat, events, warns = [], [], [], [], []
+    _TRACE = trace
 
     def record(stage):
         trace.append(eng.objective(st))
@@ -778,7 +782,8 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
         trace_stages=stages, trace_khat=khat, iterations=iterations, converged=converged,
         warnings=warns, events=events, slots=st.act.copy(), builds=eng.builds,
         wall_time=time.perf_counter() - t_start,
-        min_margin=min((mg for _, mg in _MARGINS), default=float("inf")),
+        min_margin=min((mg for _, mg, _ in _MARGINS), default=float("inf")),
+        margins=list(_MARGINS),
     )
 
 

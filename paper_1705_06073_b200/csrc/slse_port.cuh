@@ -88,6 +88,27 @@ using std::fabs; using std::floor; using std::fma; using std::fmod; using std::l
 using std::sqrt; using std::isnan;
 #endif
 
+#ifndef SLSE_HOST_EMU
+// Transposed warp sum of V (power of two, <= 16) per-lane values over groups
+// of 2V lanes: each xor stage sends half of the remaining values and keeps
+// the other half, so it takes V shuffles instead of 5 V.  Sum v ends in lanes
+// 2v and 2v+1 of each group (value bit i <-> lane bit i+1).  Clobbers v.
+template <int V>
+SLSE_D double warp_tsum(double* v, int lane) {
+#pragma unroll
+  for (int h = V / 2; h >= 1; h >>= 1) {
+    const bool up = (lane & (2 * h)) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? v[i] : v[i + h];
+      const double keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // Block context.  All reductions return the SAME bits to every thread (warp
 // xor-butterflies are symmetric; the cross-warp stage is a fixed sequential

@@ -88,9 +88,9 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
 #endif
   for (int kk = warp; kk < K; kk += nwarp) {
     const double th = thetas[kk];
-    double acc[14];
+    double acc[16];
 #pragma unroll
-    for (int i = 0; i < 14; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
     const cplx step = expj2pi((double)lanes, th, -1.0);
     cplx e = mk(1.0, 0.0);
     int since = 1 << 30;
@@ -116,12 +116,50 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
       ++since;
     }
 #ifndef SLSE_HOST_EMU
-#pragma unroll
-    for (int i = 0; i < 14; ++i) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    // Transposed warp reduction: 16 shuffles for the 14 sums (vs 70), sum v
+    // ends in lanes 2v, 2v+1.
+    acc[14] = acc[15] = 0.0;
+    const double red = warp_tsum<16>(acc, lane);
+    const auto from = [&](int v) { return __shfl_sync(0xffffffffu, red, 2 * v); };
+    // Lanes 0..15 each form one product A_a conj(A_b) (a = lane/4, b = lane%4)
+    // and its four cf-weighted terms; a second transposed reduction over the
+    // 16 lanes leaves s, t, v, x in lanes 0, 2..4, 6..8, 10.
+    const int pa = (lane >> 2) & 3, pb = lane & 3;
+    const cplx Aa = mk(from(2 * pa), from(2 * pa + 1));
+    const cplx Ab = mk(from(2 * pb), from(2 * pb + 1));
+    const cplx P = cmulc(Aa, Ab);
+    double term[8];
+    const double* c = &cf->cf[0][pa][pb];
+    const double c0 = lane < 16 ? c[0] : 0.0, c1 = lane < 16 ? c[16] : 0.0;
+    const double c2 = lane < 16 ? c[32] : 0.0, c3 = lane < 16 ? c[48] : 0.0;
+    term[0] = c0 * P.re;
+    term[1] = c1 * P.re; term[2] = c1 * P.im;
+    term[3] = c2 * P.re; term[4] = c2 * P.im;
+    term[5] = c3 * P.re;
+    term[6] = term[7] = 0.0;
+    const double tot = warp_tsum<8>(term, lane);
+    const double sc_tv = two_pi * inv_d, sc_vx = 4.0 * kPi * kPi * inv_d;
+    double* qd = (double*)&q[kk];
+    double* rd = (double*)&r[kk];
+    double* ud = (double*)&u[kk];
+    double* td = (double*)&t[kk];
+    double* vd = (double*)&v[kk];
+    switch (lane) {
+      case 0: s[kk] = tot * inv_d; break;
+      case 2: td[0] = tot * sc_tv; break;
+      case 4: td[1] = tot * sc_tv; break;
+      case 6: vd[0] = tot * sc_vx; break;
+      case 8: vd[1] = tot * sc_vx; break;
+      case 10: x[kk] = tot * sc_vx; break;
+      case 16: qd[0] = red; break;
+      case 18: qd[1] = red; break;
+      case 20: rd[0] = red; break;
+      case 22: rd[1] = red; break;
+      case 24: ud[0] = red; break;
+      case 26: ud[1] = red; break;
+      default: break;
     }
-#endif
+#else
     if (lane == 0) {
       cplx A[4];
       for (int a = 0; a < 4; ++a) A[a] = mk(acc[2 * a], acc[2 * a + 1]);
@@ -144,6 +182,7 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
       v[kk] = cscale(sum[2], sc_vx);
       x[kk] = sum[3].re * sc_vx;
     }
+#endif
   }
   b.sync();
 }

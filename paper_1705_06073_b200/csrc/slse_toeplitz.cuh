@@ -199,12 +199,19 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
 }
 
 #ifndef SLSE_HOST_EMU
-// One-warp Schur-Levinson (the N <= 512 solver path): the backward generator
-// B_j of pair j = lane + 32 q stays in registers for the whole recursion
-// (its pair never changes lanes in the shifted frame), only e and the
-// predictor a live in shared memory; warp barriers only.
+// One-warp Schur-Levinson (the N <= 512 solver path).  Register slot
+// r = lane + 32 q holds, in a shifted frame where it never changes lanes,
+// either the backward generator B_r (r < n-1-m at step m) or the backward
+// predictor coefficient b_m[r - n + 1 + m] (r >= n-1-m).  The two ranges tile
+// [0, n) exactly, and both updates read and write E[r + m + 1], where
+// E[0, n) is the forward generator e and E[n-1+j] the forward predictor a_j:
+//   E <- E + k B,   B <- B + conj(k) E,
+// so each step is one uniform pass over the Q register slots (no separate
+// predictor loop).  The slot that retires from the generator range at step
+// m becomes the new predictor coefficient b_{m+1}[0] = conj(k).  Needs E of
+// 2n elements (e and the adjacent generator buffer); warp barriers only.
 template <int Q>
-SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* a, double* delta_out,
+SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* E, double* delta_out,
                                    double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
   Factor F;
   F.logdet = 0.0;
@@ -216,8 +223,7 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     F.status = kBadColumn;
     return F;
   }
-  __builtin_assume(__isShared(e));
-  __builtin_assume(__isShared(a));
+  __builtin_assume(__isShared(E));
   const int lane = b.tid;
   const double c0 = c0c.re;
   const double floor_ = kPdEps * c0;
@@ -227,10 +233,10 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     const int j = lane + 32 * q;
     cplx cj = mk(0.0, 0.0);
     if (j < n) cj = (j == 0) ? mk(c0, 0.0) : c[j];
-    Breg[q] = cj;
+    Breg[q] = (j == n - 1) ? mk(1.0, 0.0) : cj;  // b_0 = 1 sits in slot n-1
     if (j < n) {
-      e[j] = cj;
-      a[j] = mk(j == 0 ? 1.0 : 0.0, 0.0);
+      E[j] = cj;
+      E[n + j] = mk(0.0, 0.0);
       delta_tmp[j] = 0.0;
     }
   }
@@ -240,7 +246,7 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
   int fail = 0;
   cplx k = mk(0.0, 0.0);
   if (n > 1) {
-    const cplx e1 = e[1];
+    const cplx e1 = E[1];
     const double inv = 1.0 / delta;
     k = mk(-e1.re * inv, -e1.im * inv);
   }
@@ -249,36 +255,22 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
     cplx knext = mk(0.0, 0.0);
     if (m + 2 < n) {  // lookahead from pre-update values
-      const cplx e2 = e[m + 2];
+      const cplx e2 = E[m + 2];
       const cplx b1 = mk(__shfl_sync(0xffffffffu, Breg[0].re, 1), __shfl_sync(0xffffffffu, Breg[0].im, 1));
       const cplx emn = cadd(e2, cmul(k, b1));
       const double invn = 1.0 / dnext;
       knext = mk(-emn.re * invn, -emn.im * invn);
       __syncwarp();
     }
-    const int cnt = n - 1 - m;
+    const int top = n - 2 - m;  // generator slot retiring at this step
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const int j = lane + 32 * q;
-      if (j < cnt) {
-        const cplx ej = e[j + m + 1];
+      const int r = lane + 32 * q;
+      if (r < n) {
+        const cplx ej = E[r + m + 1];
         const cplx bj = Breg[q];
-        if (j > 0) e[j + m + 1] = cadd(ej, cmul(k, bj));
-        Breg[q] = cadd(bj, cmul(kc, ej));
-      }
-    }
-    const int top = m + 1;
-    const int npair = (top + 1) / 2;
-    if (lane == 0) a[top] = k;  // k * conj(a_0), a_0 = 1
-    for (int i = 1 + lane; i <= npair; i += 32) {
-      const int jj = top - i;
-      if (i < jj) {
-        const cplx ai = a[i], aj = a[jj];
-        a[i] = cadd(ai, cmul(k, conjg(aj)));
-        a[jj] = cadd(aj, cmul(k, conjg(ai)));
-      } else if (i == jj) {
-        const cplx ai = a[i];
-        a[i] = cadd(ai, cmul(k, conjg(ai)));
+        if (r > 0) E[r + m + 1] = cadd(ej, cmul(k, bj));
+        Breg[q] = (r == top) ? kc : cadd(bj, cmul(kc, ej));
       }
     }
     if (lane == 0) delta_tmp[m + 1] = dnext;
@@ -296,7 +288,153 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
   for (int j = lane; j < n; j += 32) {
     part += log(delta_tmp[j]);
     if (delta_out) delta_out[j] = delta_tmp[j];
-    rho[j] = conjg(a[n - 1 - j]);
+    rho[j] = (j == n - 1) ? mk(1.0, 0.0) : conjg(E[2 * n - 2 - j]);  // conj(a_{n-1-j}), a_0 = 1
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+#endif
+
+#ifndef SLSE_HOST_EMU
+// Register-resident one-warp Schur-Levinson for N <= 32 Q.  Same slot scheme
+// as toeplitz_factor_warp, but lane L owns the CONTIGUOUS slots
+// r = Q L + i and keeps both E[r + m + 1] and B_r in registers: after each
+// step E moves down one slot, which is a static register rotation (the m
+// loop is unrolled Q times) plus one shuffle from lane L+1.  No shared
+// memory traffic; lane 0 owns slot 1, so it forms the next reflection
+// coefficient from its own update and broadcasts it.  Slots r >= n hold
+// zeros and stay zero.
+//
+// The n-1 steps are aligned so that they END on a block boundary: the first
+// block starts at sub-step t0 = (-(n-1)) mod Q.  Then at sub-step t the
+// retiring generator slot n-2-m always sits in register Q-1-t (only its
+// lane varies), and the final rotation is the identity.
+template <int Q, int T>
+SLSE_D void lev_regs_step(cplx (&Er)[Q], cplx (&Br)[Q], cplx& k, double& delta, int m, int n, int lane,
+                          double* delta_tmp) {
+  const double kr = k.re, ki = k.im;
+  const double dnext = delta * (1.0 - (kr * kr + ki * ki));
+  const double inv = __drcp_rn(dnext);
+  const int top = n - 2 - m;
+  const bool mine = (top - (Q - 1 - T)) == Q * lane;  // this lane owns the retiring slot
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int p = (i + T) % Q;  // physical E register of logical slot i (B does not move)
+    const cplx ej = Er[p], bj = Br[i];
+    // E <- E + k B ;  B <- B + conj(k) E
+    Er[p] = mk(fma(kr, bj.re, fma(-ki, bj.im, ej.re)), fma(kr, bj.im, fma(ki, bj.re, ej.im)));
+    cplx bn = mk(fma(kr, ej.re, fma(ki, ej.im, bj.re)), fma(kr, ej.im, fma(-ki, ej.re, bj.im)));
+    if (i == Q - 1 - T) bn = mine ? mk(kr, -ki) : bn;  // b_{m+1}[0] = conj(k)
+    Br[i] = bn;
+  }
+  // lane 0 holds slot 1, i.e. the updated e_{m+2}: the next pivot
+  const cplx e2 = Er[(1 + T) % Q];
+  const double nr = __shfl_sync(0xffffffffu, -e2.re * inv, 0);
+  const double ni = __shfl_sync(0xffffffffu, -e2.im * inv, 0);
+  // shift E down one slot: logical slot 0 of lane L+1 becomes logical slot
+  // Q-1 of lane L (the same physical register under the rotation)
+  constexpr int p0 = T % Q;
+  const double sr = __shfl_down_sync(0xffffffffu, Er[p0].re, 1);
+  const double si = __shfl_down_sync(0xffffffffu, Er[p0].im, 1);
+  Er[p0] = (lane == 31) ? mk(0.0, 0.0) : mk(sr, si);
+  if (lane == 0) delta_tmp[m + 1] = dnext;
+  delta = dnext;
+  k = mk(nr, ni);
+}
+
+template <int Q, int T>
+SLSE_D void lev_regs_block(cplx (&Er)[Q], cplx (&Br)[Q], cplx& k, double& delta, int& m, int n, int lane,
+                           double* delta_tmp, int t0) {
+  if constexpr (T < Q) {
+    if (T >= t0) {
+      lev_regs_step<Q, T>(Er, Br, k, delta, m, n, lane, delta_tmp);
+      ++m;
+    }
+    lev_regs_block<Q, T + 1>(Er, Br, k, delta, m, n, lane, delta_tmp, t0);
+  }
+}
+
+template <int Q, int T>
+SLSE_D void lev_regs_full(cplx (&Er)[Q], cplx (&Br)[Q], cplx& k, double& delta, int m, int n, int lane,
+                          double* delta_tmp) {
+  if constexpr (T < Q) {
+    lev_regs_step<Q, T>(Er, Br, k, delta, m + T, n, lane, delta_tmp);
+    lev_regs_full<Q, T + 1>(Er, Br, k, delta, m, n, lane, delta_tmp);
+  }
+}
+
+template <int Q>
+SLSE_D Factor toeplitz_factor_regs(const cplx* SLSE_RESTRICT c, int n, double* delta_out, double* delta_tmp,
+                                   cplx* SLSE_RESTRICT rho, Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  const int lane = b.tid;
+  const int base = Q * lane;
+  const double c0 = c0c.re;
+  const double floor_ = kPdEps * c0;
+  const int t0 = (Q - (n - 1) % Q) % Q;  // first block runs sub-steps t0..Q-1
+  cplx Er[Q], Br[Q];
+#pragma unroll
+  for (int p = 0; p < Q; ++p) {
+    const int i = (p - t0 + Q) % Q;  // logical slot held by physical register p at the start
+    const int r = base + i;
+    Er[p] = (r + 1 < n) ? c[r + 1] : mk(0.0, 0.0);
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int r = base + i;
+    Br[i] = (r + 1 < n) ? (r == 0 ? mk(c0, 0.0) : c[r]) : mk(r == n - 1 ? 1.0 : 0.0, 0.0);
+    if (r < n) delta_tmp[r] = 0.0;
+  }
+  __syncwarp();
+  if (lane == 0) delta_tmp[0] = c0;
+  double delta = c0;
+  cplx k = mk(0.0, 0.0);
+  if (n > 1) {
+    const double e1r = __shfl_sync(0xffffffffu, c[1].re, 0), e1i = __shfl_sync(0xffffffffu, c[1].im, 0);
+    const double inv = 1.0 / delta;
+    k = mk(-e1r * inv, -e1i * inv);
+  }
+  int fail = 0;
+  if (n > 1) {
+    int m = 0;
+    lev_regs_block<Q, 0>(Er, Br, k, delta, m, n, lane, delta_tmp, t0);
+    fail = !(delta > floor_);
+    for (; m + 1 < n && !fail; m += Q) {
+      lev_regs_full<Q, 0>(Er, Br, k, delta, m, n, lane, delta_tmp);
+      fail = !(delta > floor_);
+    }
+  }
+  __syncwarp();
+  if (!fail) {  // a pivot below the floor anywhere inside a block
+    for (int j = lane + 1; j < n; j += 32) fail |= !(delta_tmp[j] > floor_);
+    fail = __any_sync(0xffffffffu, fail);
+  }
+  if (fail) {
+    F.status = kNotPD;
+    return F;
+  }
+  // after n-1 steps (rotation back to identity) logical slot i of lane L
+  // holds a_{QL+i+1}; rho_j = conj(a_{n-1-j})
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int j = base + i + 1;
+    if (j <= n - 1) rho[n - 1 - j] = conjg(Er[i]);
+  }
+  if (lane == 0) rho[n - 1] = mk(1.0, 0.0);
+  F.delta_last = delta;
+  double part = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
   }
   F.logdet = b.sum(part);
   return F;
@@ -306,9 +444,13 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
 SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
                               double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
 #ifndef SLSE_HOST_EMU
+#ifndef SLSE_LEV_SMEM
+  if (b.nt == 32 && n <= 256) return toeplitz_factor_regs<8>(c, n, delta_out, delta_tmp, rho, b);
+#endif
   if (b.nt == 32 && __isShared(e) && __isShared(a)) {
-    if (n <= 256) return toeplitz_factor_warp<8>(c, n, e, a, delta_out, delta_tmp, rho, b);
-    if (n <= 512) return toeplitz_factor_warp<16>(c, n, e, a, delta_out, delta_tmp, rho, b);
+    // e and B are adjacent (B == e + n) in every caller's shared-memory plan
+    if (B == e + n && n <= 256) return toeplitz_factor_warp<8>(c, n, e, delta_out, delta_tmp, rho, b);
+    if (B == e + n && n <= 512) return toeplitz_factor_warp<16>(c, n, e, delta_out, delta_tmp, rho, b);
   }
   if (__isShared(e)) return toeplitz_factor_impl<true>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
 #endif

@@ -44,3 +44,13 @@ def rel(a, b):
 THETA_TOL = 1e-8      # wrap-around distance
 AMP_TOL = 1e-6        # amplitudes and noise variance, relative
 CALL_TOL = 1e-9       # per-call quantities, relative (inf-norm / inf-norm)
+# A decision closer than this to flipping, in units of its roundoff scale
+# (1e-12 relative for objective comparisons), is a near tie (make_margins.py).
+NEAR_TIE = 1.0
+
+
+def near_ties(cfg, b):
+    """Near-tie decisions of golden trajectory (cfg, b): [[trace_pos, kind, margin], ...]."""
+    import json
+    with open(os.path.join(GOLDEN_DIR, "margins.json")) as f:
+        return json.load(f)[f"cfg{cfg}_p{b}"]["near_ties"]
