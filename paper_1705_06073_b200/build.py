@@ -18,8 +18,12 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(REPO, "include")
-LIBDIR = os.path.join(PKG, "_lib")
-OBJDIR = os.path.join(REPO, "build", "obj")
+# Variant builds (tools/): SLSE_BUILD_DEFS adds -D flags, SLSE_BUILD_OUT
+# redirects objects and the .so (the default build ignores both).
+_OUT = os.environ.get("SLSE_BUILD_OUT")
+LIBDIR = os.path.abspath(_OUT) if _OUT else os.path.join(PKG, "_lib")
+OBJDIR = os.path.join(LIBDIR, "obj") if _OUT else os.path.join(REPO, "build", "obj")
+EXTRA_DEFS = os.environ.get("SLSE_BUILD_DEFS", "").split() if _OUT else []
 LIBNAME = "libsuperlse_b200.so"
 LIBPATH = os.path.join(LIBDIR, LIBNAME)
 
@@ -63,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
         obj = os.path.join(OBJDIR, name + ".o")
         if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(hdr_time, os.path.getmtime(src)):
             return obj, ""
-        cmd = [exe] + NVCC_FLAGS + extra + defs + ["-c", src, "-o", obj]
+        cmd = [exe] + NVCC_FLAGS + extra + EXTRA_DEFS + defs + ["-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {name}:\n{res.stderr[-6000:]}")

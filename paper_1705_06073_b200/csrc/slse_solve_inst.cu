@@ -27,3 +27,16 @@ cudaError_t SLSE_CAT(slse_solve_launch_, SLSE_NT)(int grid, size_t smem, cudaStr
                                                              rec_smem);
   return cudaGetLastError();
 }
+
+#ifdef SLSE_SOLVER_PROF
+// Read (and optionally reset) the solver phase-cycle accumulators of this
+// instantiation (see slse_solver.cuh, SLSE_SOLVER_PROF).
+extern "C" int SLSE_CAT(slse_solver_prof_, SLSE_NT)(unsigned long long* out, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, slse::slse_prof_cycles, sizeof(unsigned long long) * 6);
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(slse::slse_prof_cycles, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif

@@ -37,6 +37,19 @@ enum EvKind : int { kEvSweep = 0, kEvActivate = 1, kEvDeactivate = 2, kEvEnd = -
 enum Flags : int { kFlConverged = 1, kFlKmaxCap = 2, kFlTraceFull = 4, kFlEventsFull = 8 };
 enum Timer : int { kTmActivate = 0, kTmObjective = 1, kTmBeta = 2, kTmRefine = 3, kTmDeactivate = 4, kTmTotal = 5 };
 
+// Optional per-phase cycle profile of the solver (build with
+// -DSLSE_SOLVER_PROF; tools/solver_prof.py).  Leader-thread clock64 deltas,
+// accumulated per problem and added to slse_prof_cycles at finish():
+// 0 covariance column, 1 factor, 2 GS apply, 3 stats, 4 grid, 5 whole run.
+#ifdef SLSE_SOLVER_PROF
+__device__ unsigned long long slse_prof_cycles[6];
+#define SLSE_PROF_T0(v) const long long v = clock64()
+#define SLSE_PROF_ADD(i, v) (prof_acc[i] += clock64() - (v))
+#else
+#define SLSE_PROF_T0(v)
+#define SLSE_PROF_ADD(i, v)
+#endif
+
 struct SolveParams {
   int n, L, kmax;
   int max_outer, inner_max, sweep_iters, lbfgs_mem;
@@ -242,6 +255,9 @@ struct Solver {
   int ntrace, nevents, flags;
   int mem_valid, mem_dim, mem_count, mem_head;
   long long n_builds, n_grids, n_stats, n_backtracks;
+#ifdef SLSE_SOLVER_PROF
+  long long prof_acc[6], prof_run0;
+#endif
   unsigned long long t_mark, t_start;
   double tm[6];
   int free_hint;
@@ -288,6 +304,9 @@ struct Solver {
     cur = 0; cur_valid = 0; status = kOk; ntrace = 0; nevents = 0; flags = 0;
     mem_valid = 0; mem_dim = 0; mem_count = 0; mem_head = 0;
     n_builds = n_grids = n_stats = n_backtracks = 0;
+#ifdef SLSE_SOLVER_PROF
+    for (int i = 0; i < 6; ++i) prof_acc[i] = 0;
+#endif
     for (int i = 0; i < 6; ++i) tm[i] = 0.0;
     free_hint = 0;
     k = 0;
@@ -347,13 +366,19 @@ struct Solver {
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
     if (kk == 0) return build_white(B, be);
+    SLSE_PROF_T0(t0);
     steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
+    SLSE_PROF_ADD(0, t0);
+    SLSE_PROF_T0(t1);
     Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham, P.dnc_direct)
                      : toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
+    SLSE_PROF_ADD(1, t1);
     if (F.status != kOk) return F.status;
     B.delta_last = F.delta_last;
     B.logdet = F.logdet;
-    double quad = gs_apply(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b);
+    SLSE_PROF_T0(t2);
+    double quad = gs_apply_any(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b);
+    SLSE_PROF_ADD(2, t2);
     B.data_term = F.logdet + quad;
     B.stats_valid = 0;
     return kOk;
@@ -385,7 +410,9 @@ struct Solver {
   SLSE_NIM void stats(Bundle& B, const double* th, int kk) {
     if (B.stats_valid) return;
     ++n_stats;
+    SLSE_PROF_T0(t0);
     component_stats(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b);
+    SLSE_PROF_ADD(3, t0);
     B.stats_valid = 1;
   }
 
@@ -428,7 +455,11 @@ struct Solver {
     ++n_grids;
     Bundle& B = bun[cur];
     const double lr = log((1.0 - ze) / ze);
-    if (P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) return;
+    SLSE_PROF_T0(t0);
+    if (P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) {
+      SLSE_PROF_ADD(4, t0);
+      return;
+    }
     grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
     for (int l = tid_; l < L; l += nt_) {
       const double qq = cabs2(G0[l]);
@@ -808,6 +839,9 @@ struct Solver {
   // ---- the outer loop (estimator.py:117-275) ----
   SLSE_NIM void run() {
     t_start = now_ns();
+#ifdef SLSE_SOLVER_PROF
+    prof_run0 = clock64();
+#endif
     t_mark = t_start;
     // energy, floor, beta0 (model_core.py:125-130; estimator.py:135-137)
     double part = 0.0;
@@ -983,6 +1017,11 @@ struct Solver {
       }
     }
     tm[kTmTotal] = (double)(now_ns() - t_start) * 1e-9;
+#ifdef SLSE_SOLVER_PROF
+    prof_acc[5] = clock64() - prof_run0;
+    if (b.leader())
+      for (int i = 0; i < 6; ++i) atomicAdd(&slse_prof_cycles[i], (unsigned long long)prof_acc[i]);
+#endif
     if (converged) flags |= kFlConverged;
     if (b.leader()) {
       *o.khat = k;

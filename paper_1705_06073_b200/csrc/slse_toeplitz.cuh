@@ -441,11 +441,106 @@ SLSE_D Factor toeplitz_factor_regs(const cplx* SLSE_RESTRICT c, int n, double* d
 }
 #endif
 
+#ifndef SLSE_HOST_EMU
+// Compact form of toeplitz_factor_regs (the default): the same register
+// slots, but a rolled step loop -- E moves down one slot by register moves
+// and the retiring slot is found by compare -- so the whole recursion is a
+// ~2.5 KB loop body instead of a 30 KB unrolled one.  The persistent solver
+// interleaves every phase on an SM, so instruction-cache footprint matters
+// more than the ~40 % extra ALU instructions (measured on B200).
+template <int Q>
+SLSE_D Factor toeplitz_factor_regs_c(const cplx* SLSE_RESTRICT c, int n, double* delta_out, double* delta_tmp,
+                                     cplx* SLSE_RESTRICT rho, Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  const int lane = b.tid;
+  const int base = Q * lane;
+  const double c0 = c0c.re;
+  const double floor_ = kPdEps * c0;
+  cplx Er[Q], Br[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int r = base + i;
+    Er[i] = (r + 1 < n) ? c[r + 1] : mk(0.0, 0.0);
+    Br[i] = (r + 1 < n) ? (r == 0 ? mk(c0, 0.0) : c[r]) : mk(r == n - 1 ? 1.0 : 0.0, 0.0);
+    if (r < n) delta_tmp[r] = 0.0;
+  }
+  __syncwarp();
+  if (lane == 0) delta_tmp[0] = c0;
+  double delta = c0;
+  double kr = 0.0, ki = 0.0;
+  if (n > 1) {
+    const double e1r = __shfl_sync(0xffffffffu, Er[0].re, 0), e1i = __shfl_sync(0xffffffffu, Er[0].im, 0);
+    const double inv = 1.0 / delta;
+    kr = -e1r * inv;
+    ki = -e1i * inv;
+  }
+  int fail = 0;
+#pragma unroll 1
+  for (int m = 0; m + 1 < n; ++m) {
+    const double dnext = delta * (1.0 - (kr * kr + ki * ki));
+    const double inv = __drcp_rn(dnext);
+    const int toff = n - 2 - m - base;  // retiring generator slot, if this lane owns it
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const cplx ej = Er[i], bj = Br[i];
+      Er[i] = mk(fma(kr, bj.re, fma(-ki, bj.im, ej.re)), fma(kr, bj.im, fma(ki, bj.re, ej.im)));
+      const cplx bn = mk(fma(kr, ej.re, fma(ki, ej.im, bj.re)), fma(kr, ej.im, fma(-ki, ej.re, bj.im)));
+      Br[i] = (i == toff) ? mk(kr, -ki) : bn;  // b_{m+1}[0] = conj(k)
+    }
+    // lane 0 holds slot 1 = the updated e_{m+2}: the next pivot
+    const double nr = __shfl_sync(0xffffffffu, -Er[1].re * inv, 0);
+    const double ni = __shfl_sync(0xffffffffu, -Er[1].im * inv, 0);
+    const double sr = __shfl_down_sync(0xffffffffu, Er[0].re, 1);
+    const double si = __shfl_down_sync(0xffffffffu, Er[0].im, 1);
+#pragma unroll
+    for (int i = 0; i + 1 < Q; ++i) Er[i] = Er[i + 1];
+    Er[Q - 1] = (lane == 31) ? mk(0.0, 0.0) : mk(sr, si);
+    if (lane == 0) delta_tmp[m + 1] = dnext;
+    delta = dnext;
+    if (!(delta > floor_)) { fail = 1; break; }
+    kr = nr;
+    ki = ni;
+  }
+  if (fail) {
+    F.status = kNotPD;
+    return F;
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int j = base + i + 1;
+    if (j <= n - 1) rho[n - 1 - j] = conjg(Er[i]);
+  }
+  if (lane == 0) rho[n - 1] = mk(1.0, 0.0);
+  F.delta_last = delta;
+  __syncwarp();
+  double part = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+#endif
+
 SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
                               double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
 #ifndef SLSE_HOST_EMU
 #ifndef SLSE_LEV_SMEM
+#ifdef SLSE_LEV_UNROLLED
   if (b.nt == 32 && n <= 256) return toeplitz_factor_regs<8>(c, n, delta_out, delta_tmp, rho, b);
+#else
+  if (b.nt == 32 && n <= 256) return toeplitz_factor_regs_c<8>(c, n, delta_out, delta_tmp, rho, b);
+#endif
 #endif
   if (b.nt == 32 && __isShared(e) && __isShared(a)) {
     // e and B are adjacent (B == e + n) in every caller's shared-memory plan
@@ -523,6 +618,181 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
     quad += x[i].re * wi.re + x[i].im * wi.im;  // Re(conj(x) w)
   }
   return b.sum(quad);
+}
+
+#ifndef SLSE_HOST_EMU
+// Runtime-size one-warp Stockham pass of radix R over 2^lg <= 512 points
+// (MAXI = 16 / R groups per lane held across the warp barrier, in place).
+template <int R>
+SLSE_D void warp_pass_rt(cplx* S, int lg, int lgns, double sign, const cplx* __restrict__ tw, int twlog,
+                         unsigned lane) {
+  constexpr int MAXI = 16 / R;
+  const unsigned per = (1u << lg) / R, NS = 1u << lgns;
+  const int lgt = lgns + ilog2(R);
+  cplx v[MAXI][R];
+#pragma unroll
+  for (int i = 0; i < MAXI; ++i) {
+    const unsigned j = lane + 32u * i;
+    if (j < per) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[i][r] = S[sk(j + r * per)];
+      if (NS > 1) {
+        const unsigned kk = j & (NS - 1);
+        const cplx w1 = twid_tab(tw, twlog, kk, lgt, sign);
+        v[i][1] = cmul(v[i][1], w1);
+        if constexpr (R >= 4) {
+          const cplx w2 = cmul(w1, w1);
+          v[i][2] = cmul(v[i][2], w2);
+          const cplx w3 = cmul(w2, w1);
+          v[i][3] = cmul(v[i][3], w3);
+          if constexpr (R == 8) {
+            const cplx w4 = cmul(w2, w2);
+            v[i][4] = cmul(v[i][4], w4);
+            v[i][5] = cmul(v[i][5], cmul(w4, w1));
+            v[i][6] = cmul(v[i][6], cmul(w4, w2));
+            v[i][7] = cmul(v[i][7], cmul(w4, w3));
+          }
+        }
+      }
+      dft_dif<R>(v[i], sign);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < MAXI; ++i) {
+    const unsigned j = lane + 32u * i;
+    if (j < per) {
+      const unsigned kk = j & (NS - 1);
+      const unsigned base = (j - kk) * R + kk;
+#pragma unroll
+      for (int r = 0; r < R; ++r) S[sk(base + r * NS)] = v[i][brev_const(r, R)];
+    }
+  }
+  __syncwarp();
+}
+
+// One-warp in-place transform of 2^lg (<= 512) points on the skewed shared
+// buffer S: radix-8 passes, then one radix-4 or radix-2 pass.  One compact
+// out-of-line body for every size and direction.
+static __device__ __noinline__ void warp_fft_rt(cplx* S, int lg, double sign, const cplx* __restrict__ tw, int twlog,
+                                         int lane_) {
+  __builtin_assume(__isShared(S));
+  const unsigned lane = (unsigned)lane_ & 31u;
+  int lgns = 0;
+#pragma unroll 1
+  for (; lg - lgns >= 3; lgns += 3) warp_pass_rt<8>(S, lg, lgns, sign, tw, twlog, lane);
+  if (lg - lgns == 2) warp_pass_rt<4>(S, lg, lgns, sign, tw, twlog, lane);
+  else if (lg - lgns == 1) warp_pass_rt<2>(S, lg, lgns, sign, tw, twlog, lane);
+}
+
+// IFFT, keep [N-1, 2N-1) scaled by 1/nf, zero pad, FFT (the middle of a GS
+// product), in place on S.
+static __device__ __noinline__ void warp_gs_middle(cplx* S, int n, int lg, const cplx* __restrict__ tw, int twlog,
+                                            int lane) {
+  __builtin_assume(__isShared(S));
+  const int nf = 1 << lg;
+  warp_fft_rt(S, lg, 1.0, tw, twlog, lane);
+  const double inv = 1.0 / (double)nf;
+  cplx hold[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int i = lane + 32 * t;
+    hold[t] = i < n ? cscale(S[sk(n - 1 + i)], inv) : mk(0.0, 0.0);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int i = lane + 32 * t;
+    if (i < nf) S[sk(i)] = hold[t];
+  }
+  __syncwarp();
+  warp_fft_rt(S, lg, -1.0, tw, twlog, lane);
+}
+
+// One-warp GS apply (N <= 256 solver path): the same six transforms as
+// gs_apply, each an in-place warp Stockham on ONE skewed shared-memory
+// buffer S; the spectra that must survive a transform (P = FFT(rho), the
+// V chain input, the partial Z) go to the global work arrays P, V, U in
+// coalesced passes.
+static __device__ __noinline__ double gs_apply_warp(const cplx* SLSE_RESTRICT rho, int n, int lg, double delta_last,
+                                             const cplx* SLSE_RESTRICT x, const cplx* SLSE_RESTRICT Xhat,
+                                             cplx* SLSE_RESTRICT P, cplx* SLSE_RESTRICT U, cplx* SLSE_RESTRICT V,
+                                             cplx* SLSE_RESTRICT w, cplx* S, const cplx* __restrict__ tw, int twlog,
+                                             int lane) {
+  const int nf = 1 << lg;
+  __builtin_assume(__isShared(S));
+  const cplx z = mk(0.0, 0.0);
+  const cplx rlast = rho[n - 1];
+  // P = FFT(rho zero-padded)
+#pragma unroll 1
+  for (int i = lane; i < nf; i += 32) S[sk(i)] = i < n ? rho[i] : z;
+  __syncwarp();
+  warp_fft_rt(S, lg, -1.0, tw, twlog, lane);
+  // P -> global; U = Xhat P1 -> S; V = Xhat P0h -> global
+#pragma unroll 1
+  for (int k = lane; k < nf; k += 32) {
+    const cplx p1 = S[sk(k)];
+    const cplx wk = twid_tab(tw, twlog, k, lg, -1.0);
+    const cplx wn1 = twid_tab(tw, twlog, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
+    const cplx p0 = cmul(wk, csub(p1, cmul(rlast, wn1)));
+    const cplx p0h = cmul(wn1, conjg(p0));
+    const cplx xk = Xhat[k];
+    P[k] = p1;
+    S[sk(k)] = cmul(xk, p1);
+    V[k] = cmul(xk, p0h);
+  }
+  __syncwarp();
+  // U chain; Z = U'' P1h -> global U; V -> S
+  warp_gs_middle(S, n, lg, tw, twlog, lane);
+#pragma unroll 1
+  for (int k = lane; k < nf; k += 32) {
+    const cplx wn1 = twid_tab(tw, twlog, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
+    const cplx p1h = cmul(wn1, conjg(P[k]));
+    U[k] = cmul(S[sk(k)], p1h);
+    S[sk(k)] = V[k];
+  }
+  __syncwarp();
+  // V chain, then Z = U'' P1h - V'' P0 -> S, IFFT
+  warp_gs_middle(S, n, lg, tw, twlog, lane);
+#pragma unroll 1
+  for (int k = lane; k < nf; k += 32) {
+    const cplx p1 = P[k];
+    const cplx wk = twid_tab(tw, twlog, k, lg, -1.0);
+    const cplx wn1 = twid_tab(tw, twlog, (int)(((long long)(n - 1) * k) & (nf - 1)), lg, -1.0);
+    const cplx p0 = cmul(wk, csub(p1, cmul(rlast, wn1)));
+    S[sk(k)] = csub(U[k], cmul(S[sk(k)], p0));
+  }
+  __syncwarp();
+  warp_fft_rt(S, lg, 1.0, tw, twlog, lane);
+  const double sc = 1.0 / ((double)nf * delta_last);
+  double quad = 0.0;
+#pragma unroll 1
+  for (int i = lane; i < n; i += 32) {
+    const cplx wi = cscale(S[sk(i)], sc);
+    w[i] = wi;
+    quad += x[i].re * wi.re + x[i].im * wi.im;  // Re(conj(x) w)
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) quad += __shfl_xor_sync(0xffffffffu, quad, o);
+  __syncwarp();
+  return quad;
+}
+#endif
+
+// GS apply dispatch: the one-warp shared-memory version for 2N in [64, 512]
+// when the staging fits, else the general block version.
+SLSE_NI double gs_apply_any(const cplx* SLSE_RESTRICT rho, int n, double delta_last, const cplx* SLSE_RESTRICT x,
+                           const cplx* SLSE_RESTRICT Xhat, cplx* P, cplx* U, cplx* V, cplx* SLSE_RESTRICT w,
+                           const FftCtx& f, Blk& b) {
+#if !defined(SLSE_HOST_EMU) && !defined(SLSE_GS_BLOCK)
+  if (b.nt == 32 && __isShared(f.smem)) {
+    const int lg = ilog2(2 * n);
+    if (sk_len(1 << lg) <= f.smem_cap) {
+      if (lg >= 5 && lg <= 9) return gs_apply_warp(rho, n, lg, delta_last, x, Xhat, P, U, V, w, f.smem, f.tw, f.twlog, b.tid);
+    }
+  }
+#endif
+  return gs_apply(rho, n, delta_last, x, Xhat, P, U, V, w, f, b);
 }
 
 }  // namespace slse
