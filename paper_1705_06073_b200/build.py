@@ -46,6 +46,7 @@ def _sources():
     units = [("slse_capi", os.path.join(CSRC, "slse_capi.cu"), [])]
     for nt in SOLVE_NTS:
         units.append((f"slse_solve_{nt}", os.path.join(CSRC, "slse_solve_inst.cu"), [f"-DSLSE_NT={nt}"]))
+    units.append(("slse_solve_warps", os.path.join(CSRC, "slse_solve_warps.cu"), ["-DSLSE_WARP_MODE"]))
     return hdrs, units
 
 

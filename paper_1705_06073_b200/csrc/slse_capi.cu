@@ -115,12 +115,38 @@ int solver_threads(int n) {
   return 512;                 // cfg5 (superfast): 8.8 s (512) vs 13.1 (1024) / 12 (128) per 64 x N=16384
 }
 
+// Warp mode: the one-warp solvers run W per CTA (one CTA per SM) with a
+// CTA-wide rendezvous per heavy operation (slse_solve_warps.cu).  Returns
+// W (16, 8 or 4 -- as many as the per-warp shared memory allows), or 0 when
+// the classic one-problem-per-CTA kernel is used (nt > 32, SLSE_NO_WARPS).
+int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem) {
+  if (nt != 32 || dnc || getenv("SLSE_NO_WARPS")) return 0;  // (the superfast factor keeps CTA-static scratch)
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t ws = red_bytes(32) + (plan.bytes - head_bytes(32));
+  *warp_smem = (int)ws;
+  for (int W = 16; W >= 4; W >>= 1)
+    if (kCfBytes + (size_t)W * ws <= (size_t)optin) return W;
+  return 0;
+}
+
 int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
   P.dnc = n >= dnc_min_n() ? 1 : 0;
   P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
   const int nt = solver_threads(n);
   SmemPlan plan = smem_plan(n, P.L, nt, P.dnc != 0);
+  int wsm = 0;
+  if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {  // one slab per warp of every CTA
+    int ctas = (B + W - 1) / W;
+    if (ctas > sm_count()) ctas = sm_count();
+    if (ctas < 1) ctas = 1;
+    Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0, P.dnc != 0);
+    *slab_out = lay.total;
+    if (plan_out) *plan_out = plan;
+    return ctas * W;
+  }
   int occ = 1;
   cudaError_t e = cudaSuccess;
   switch (nt) {
@@ -460,6 +486,12 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
   if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
   char* ws = (char*)workspace + 256;
   const int nt = solver_threads(N);
+  int wsm = 0;
+  if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {
+    e = slse_solve_warps_launch(W, g / W, kCfBytes + (size_t)W * wsm, st, P, cft, (const cplx*)y, B, *out, ws, slab,
+                                queue, tw, twlog, plan.fft_cap, plan.rec_in_smem, wsm);
+    return e == cudaSuccess ? 0 : fail("solve_kernel_warps", e);
+  }
 #define SLSE_SOLVE_ARGS g, plan.bytes, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog, plan.fft_cap, \
                         plan.rec_in_smem
   switch (nt) {

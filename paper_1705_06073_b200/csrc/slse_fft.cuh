@@ -62,11 +62,7 @@ SLSE_D cplx twid(const FftCtx& f, int k, int lg, double sign) {
 }
 
 // In-place DIT passes on bit-reversed data x[0..n).
-SLSE_D void fft_barrier() {
-#ifndef SLSE_HOST_EMU
-  __syncthreads();
-#endif
-}
+SLSE_D void fft_barrier() { SLSE_GROUP_SYNC(); }
 
 // DIT passes over `count` contiguous bit-reversed buffers of n points
 // (one barrier per pass for all of them).
@@ -237,11 +233,7 @@ SLSE_D void dft_dif(cplx* v, double sign) {
 SLSE_HD int sk(int i) { return i + (i >> 4); }
 SLSE_HD int sk_len(int n) { return n + (n >> 4); }
 
-SLSE_D void block_barrier() {
-#ifndef SLSE_HOST_EMU
-  __syncthreads();
-#endif
-}
+SLSE_D void block_barrier() { SLSE_GROUP_SYNC(); }
 
 template <int R, int MAXI>
 SLSE_D void stockham_pass_inl(cplx* x, int count, int n, int Ns, double sign, const cplx* __restrict__ tw, int twlog,

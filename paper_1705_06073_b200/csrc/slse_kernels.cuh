@@ -28,6 +28,7 @@ namespace slse_k {
 SLSE_HD constexpr size_t red_bytes(int nt) { return (2 * ((nt + 31) / 32) * 16 * sizeof(double) + 255) & ~(size_t)255; }
 SLSE_HD constexpr size_t head_bytes(int nt) { return red_bytes(nt) + ((sizeof(CfTable) + 255) & ~(size_t)255); }
 constexpr size_t kRedBytes = red_bytes(1024);
+constexpr size_t kCfBytes = (sizeof(CfTable) + 255) & ~(size_t)255;
 constexpr size_t kHeadBytes = head_bytes(1024);
 constexpr size_t kRegionBudget = 200 * 1024;
 
@@ -92,6 +93,31 @@ struct OutPtrs {
   slse_outputs o;
 };
 
+// output views of problem p
+SLSE_D ProbOut prob_out(const slse_outputs& out, const SolveParams& P, int p) {
+  const size_t K = (size_t)P.kmax;
+  ProbOut o;
+  o.khat = out.k_hat + p;
+  o.status = out.status + p;
+  o.iters = out.iterations + p;
+  o.flags = out.flags + p;
+  o.beta = out.beta + p;
+  o.zeta = out.zeta + p;
+  o.theta = out.theta + p * K;
+  o.gamma = out.gamma + p * K;
+  o.alpha = (cplx*)out.alpha + p * K;
+  o.slot = out.slot + p * K;
+  o.trace = out.trace + (size_t)p * P.tcap;
+  o.stage = out.stage + (size_t)p * P.tcap;
+  o.trace_k = out.trace_k + (size_t)p * P.tcap;
+  o.ntrace = out.n_trace + p;
+  o.events = out.events + (size_t)p * P.ecap * 3;
+  o.nevents = out.n_events + p;
+  o.counters = (long long*)out.counters + (size_t)p * 4;
+  o.stage_s = out.stage_seconds + (size_t)p * 6;
+  return o;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve_kernel(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
                                                    int B, slse_outputs out, char* ws, size_t slab_bytes,
@@ -122,32 +148,58 @@ __global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve
     const int p = s_prob;
     __syncthreads();
     if (p >= B) break;
-    const size_t K = (size_t)P.kmax;
-    ProbOut o;
-    o.khat = out.k_hat + p;
-    o.status = out.status + p;
-    o.iters = out.iterations + p;
-    o.flags = out.flags + p;
-    o.beta = out.beta + p;
-    o.zeta = out.zeta + p;
-    o.theta = out.theta + p * K;
-    o.gamma = out.gamma + p * K;
-    o.alpha = (cplx*)out.alpha + p * K;
-    o.slot = out.slot + p * K;
-    o.trace = out.trace + (size_t)p * P.tcap;
-    o.stage = out.stage + (size_t)p * P.tcap;
-    o.trace_k = out.trace_k + (size_t)p * P.tcap;
-    o.ntrace = out.n_trace + p;
-    o.events = out.events + (size_t)p * P.ecap * 3;
-    o.nevents = out.n_events + p;
-    o.counters = (long long*)out.counters + (size_t)p * 4;
-    o.stage_s = out.stage_seconds + (size_t)p * 6;
+    const ProbOut o = prob_out(out, P, p);
     Solver S(b, P, cf, ys + (size_t)p * P.n, o, slab, lay, rec_smem ? region : nullptr, f);
     S.run();
     b.bank = S.b.bank;
     __syncthreads();
   }
 }
+
+#ifdef SLSE_WARP_MODE
+// W independent one-warp solvers per CTA (one CTA per SM), meeting at a
+// CTA-wide rendezvous for every heavy operation (Solver::build / stats /
+// grid_curve in warp mode).  Shared memory: the cf table, then per warp its
+// reduction scratch and its FFT / recursion region (warp_smem bytes).
+template <int W>
+__global__ void __launch_bounds__(32 * W, 16 / W) solve_kernel_warps(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
+                                                                    int B, slse_outputs out, char* ws, size_t slab_bytes,
+                                                                    int* queue, const cplx* tw, int twlog, int fft_cap,
+                                                                    int rec_smem, int warp_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CfTable* cf = (CfTable*)smem_raw;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* mine = smem_raw + kCfBytes + (size_t)warp * warp_smem;
+  if (threadIdx.x == 0) *cf = cft;
+  __syncthreads();
+  Blk b;
+  b.tid = lane;
+  b.nt = 32;
+  b.red = (double*)mine;
+  b.bank = 0;
+  FftCtx f;
+  f.tw = tw;
+  f.twlog = twlog;
+  f.smem = (cplx*)(mine + red_bytes(32));
+  f.smem_cap = fft_cap;
+  cplx* region = f.smem;
+  char* slab = ws + ((size_t)blockIdx.x * W + warp) * slab_bytes;
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0, P.dnc != 0);
+  for (;;) {
+    int p = 0;
+    if (lane == 0) p = atomicAdd(queue, 1);
+    p = __shfl_sync(0xffffffffu, p, 0);
+    if (p >= B) break;
+    const ProbOut o = prob_out(out, P, p);
+    Solver S(b, P, cf, ys + (size_t)p * P.n, o, slab, lay, rec_smem ? region : nullptr, f);
+    S.run();
+    b.bank = S.b.bank;
+    __syncwarp();
+  }
+  // no problem left: answer the other warps' rendezvous until all are idle
+  while (!rv_arrive(1)) rv_depart();
+}
+#endif
 
 template <int NT>
 __global__ void __launch_bounds__(NT) cov_kernel(const double* theta, const double* gamma, const int* kcount,
@@ -494,3 +546,9 @@ SLSE_DECL_SOLVE(128)
 SLSE_DECL_SOLVE(256)
 SLSE_DECL_SOLVE(512)
 SLSE_DECL_SOLVE(1024)
+
+// warp-mode solver (slse_solve_warps.cu): W one-warp solvers per CTA
+cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t st, const slse::SolveParams& P,
+                                    const slse::CfTable& cft, const slse::cplx* ys, int B, const slse_outputs& out,
+                                    char* ws, size_t slab, int* queue, const slse::cplx* tw, int twlog, int fft_cap,
+                                    int rec_smem, int warp_smem);

@@ -109,21 +109,78 @@ SLSE_D double warp_tsum(double* v, int lane) {
 }
 #endif
 
+// Barrier of one cooperative group ("block").  In warp mode
+// (SLSE_WARP_MODE: several independent one-warp solvers share a CTA) a
+// group is one warp, so every group barrier is a warp barrier.
+#ifdef SLSE_HOST_EMU
+#define SLSE_GROUP_SYNC()
+#elif defined(SLSE_WARP_MODE)
+#define SLSE_GROUP_SYNC() __syncwarp()
+#else
+#define SLSE_GROUP_SYNC() __syncthreads()
+#endif
+
+#if defined(SLSE_WARP_MODE) && !defined(SLSE_HOST_EMU)
+// CTA-wide rendezvous of the warp-mode solver (see Solver::build).  Heavy
+// operations run between rv_arrive (barrier 0, with an all-idle vote) and
+// rv_depart (barrier 1); control code runs between rv_depart and the next
+// rv_arrive.  A long operation yields at rv_slice points, ending the current
+// operation window and waiting out the control window, so short operations
+// of the other warps do not wait for it to finish.
+#ifndef SLSE_RV_GROUPS
+#define SLSE_RV_GROUPS 4  // rendezvous groups per CTA: warps w with equal w % GROUPS (one per SM sub-partition)
+#endif
+SLSE_D bool rv_arrive(int idle) {
+#if SLSE_RV_GROUPS == 1
+  return __syncthreads_and(idle) != 0;
+#else
+  const unsigned g = (threadIdx.x >> 5) % SLSE_RV_GROUPS, cnt = blockDim.x / SLSE_RV_GROUPS;
+  unsigned r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, %2, %3, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((unsigned)idle), "r"(1 + g), "r"(cnt)
+      : "memory");
+  return r != 0;
+#endif
+}
+SLSE_D void rv_depart() {
+#if SLSE_RV_GROUPS == 1
+  asm volatile("bar.sync 1;" ::: "memory");
+#else
+  const unsigned g = (threadIdx.x >> 5) % SLSE_RV_GROUPS, cnt = blockDim.x / SLSE_RV_GROUPS;
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + SLSE_RV_GROUPS + g), "r"(cnt) : "memory");
+#endif
+}
+SLSE_D void rv_slice() {
+  rv_depart();
+  (void)rv_arrive(0);
+}
+#define SLSE_RV_SLICE() rv_slice()
+#else
+#define SLSE_RV_SLICE()
+#endif
+
 // ---------------------------------------------------------------------------
 // Block context.  All reductions return the SAME bits to every thread (warp
 // xor-butterflies are symmetric; the cross-warp stage is a fixed sequential
 // order), so scalar control flow derived from them stays uniform.
+// Block reductions are out of line on the device: one shared copy instead of
+// an inlined shuffle tree (plus the compiler's divergent fallback) at every
+// call site of the control code -- instruction-cache footprint.
+#ifdef SLSE_HOST_EMU
+#define SLSE_BLK_NI SLSE_D
+#else
+#define SLSE_BLK_NI __device__ __noinline__
+#endif
+
 struct Blk {
   int tid;
   int nt;
   double* red;  // shared scratch: 2 banks x nwarps x 16 doubles
   int bank;     // alternates so one barrier per reduction suffices
 
-  SLSE_D void sync() {
-#ifndef SLSE_HOST_EMU
-    __syncthreads();
-#endif
-  }
+  SLSE_D void sync() { SLSE_GROUP_SYNC(); }
   SLSE_D bool leader() const { return tid == 0; }
 
 #ifdef SLSE_HOST_EMU
@@ -141,7 +198,7 @@ struct Blk {
 #else
   SLSE_D int nwarps() const { return (nt + 31) >> 5; }
   // k <= 16 doubles reduced at once
-  SLSE_D void sumv(double* v, int k) {
+  SLSE_BLK_NI void sumv(double* v, int k) {
     const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -156,7 +213,7 @@ struct Blk {
     if (lane == 0) {
       for (int i = 0; i < k; ++i) r[w * 16 + i] = v[i];
     }
-    __syncthreads();
+    SLSE_GROUP_SYNC();
     const int nw = nwarps();
     for (int i = 0; i < k; ++i) {
       double acc = r[i];
@@ -168,20 +225,20 @@ struct Blk {
   SLSE_D double sum(double x) { double v[1] = {x}; sumv(v, 1); return v[0]; }
   SLSE_D cplx sum(cplx x) { double v[2] = {x.re, x.im}; sumv(v, 2); return mk(v[0], v[1]); }
   SLSE_D int sumi(int x) { return (int)sum((double)x); }
-  SLSE_D double minv(double x) {
+  SLSE_BLK_NI double minv(double x) {
     const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
     double* r = red + bank * (nwarps() * 16);
     if (lane == 0) r[w * 16] = x;
-    __syncthreads();
+    SLSE_GROUP_SYNC();
     double acc = r[0];
     for (int j = 1; j < nwarps(); ++j) acc = fmin(acc, r[j * 16]);
     bank ^= 1;
     return acc;
   }
   SLSE_D double maxv(double x) { return -minv(-x); }
-  SLSE_D void argmin(double& v, int& idx) {
+  SLSE_BLK_NI void argmin(double& v, int& idx) {
     const int lane = tid & 31, w = tid >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -191,7 +248,7 @@ struct Blk {
     }
     double* r = red + bank * (nwarps() * 16);
     if (lane == 0) { r[w * 16] = v; r[w * 16 + 1] = (double)idx; }
-    __syncthreads();
+    SLSE_GROUP_SYNC();
     v = r[0]; idx = (int)r[1];
     for (int j = 1; j < nwarps(); ++j) {
       double ov = r[j * 16]; int oi = (int)r[j * 16 + 1];
@@ -199,24 +256,24 @@ struct Blk {
     }
     bank ^= 1;
   }
-  SLSE_D int bcast_i(int x) {  // value of thread 0
+  SLSE_BLK_NI int bcast_i(int x) {  // value of thread 0
     double* r = red + bank * (nwarps() * 16);
     if (tid == 0) r[0] = (double)x;
-    __syncthreads();
+    SLSE_GROUP_SYNC();
     int out = (int)r[0];
     bank ^= 1;
     return out;
   }
-  SLSE_D double bcast_d(double x) {
+  SLSE_BLK_NI double bcast_d(double x) {
     double* r = red + bank * (nwarps() * 16);
     if (tid == 0) r[0] = x;
-    __syncthreads();
+    SLSE_GROUP_SYNC();
     double out = r[0];
     bank ^= 1;
     return out;
   }
   // exclusive prefix sum over threads in tid order; total to everyone
-  SLSE_D int exscan(int x, int& total) {
+  SLSE_BLK_NI int exscan(int x, int& total) {
     const int lane = tid & 31, w = tid >> 5;
     int inc = x;
 #pragma unroll
@@ -226,7 +283,7 @@ struct Blk {
     }
     double* r = red + bank * (nwarps() * 16);
     if (lane == 31) r[w * 16] = (double)inc;
-    __syncthreads();
+    SLSE_GROUP_SYNC();
     int before = 0, tot = 0;
     for (int j = 0; j < nwarps(); ++j) {
       int c = (int)r[j * 16];

@@ -40,14 +40,25 @@ enum Timer : int { kTmActivate = 0, kTmObjective = 1, kTmBeta = 2, kTmRefine = 3
 // Optional per-phase cycle profile of the solver (build with
 // -DSLSE_SOLVER_PROF; tools/solver_prof.py).  Leader-thread clock64 deltas,
 // accumulated per problem and added to slse_prof_cycles at finish():
-// 0 covariance column, 1 factor, 2 GS apply, 3 stats, 4 grid, 5 whole run.
+// 0 covariance column, 1 factor, 2 GS apply, 3 stats, 4 grid, 5 whole run,
+// 6 waiting to enter an operation window, 7 waiting for it to close (warp mode).
 #ifdef SLSE_SOLVER_PROF
-__device__ unsigned long long slse_prof_cycles[6];
+__device__ unsigned long long slse_prof_cycles[8];
 #define SLSE_PROF_T0(v) const long long v = clock64()
 #define SLSE_PROF_ADD(i, v) (prof_acc[i] += clock64() - (v))
 #else
 #define SLSE_PROF_T0(v)
 #define SLSE_PROF_ADD(i, v)
+#endif
+
+// Control-code loops (thread-strided over k, dim, L): kept rolled -- the
+// solver's control code is executed rarely per instruction but its size
+// sets the instruction-cache footprint (SLSE_CTRL_UNROLL=1 restores the
+// compiler's unrolling).
+#ifdef SLSE_CTRL_UNROLL
+#define SLSE_CTRL_LOOP
+#else
+#define SLSE_CTRL_LOOP _Pragma("unroll 1")
 #endif
 
 struct SolveParams {
@@ -256,7 +267,7 @@ struct Solver {
   int mem_valid, mem_dim, mem_count, mem_head;
   long long n_builds, n_grids, n_stats, n_backtracks;
 #ifdef SLSE_SOLVER_PROF
-  long long prof_acc[6], prof_run0;
+  long long prof_acc[8], prof_run0;
 #endif
   unsigned long long t_mark, t_start;
   double tm[6];
@@ -305,7 +316,7 @@ struct Solver {
     mem_valid = 0; mem_dim = 0; mem_count = 0; mem_head = 0;
     n_builds = n_grids = n_stats = n_backtracks = 0;
 #ifdef SLSE_SOLVER_PROF
-    for (int i = 0; i < 6; ++i) prof_acc[i] = 0;
+    for (int i = 0; i < 8; ++i) prof_acc[i] = 0;
 #endif
     for (int i = 0; i < 6; ++i) tm[i] = 0.0;
     free_hint = 0;
@@ -363,11 +374,40 @@ struct Solver {
 
   // ---- model evaluation ----
   // Bundle for (th[0..kk), ga[0..kk), beta): model_core.py:257-274
+  // Warp mode (several one-warp solvers per CTA, SLSE_WARP_MODE): every heavy
+  // operation runs inside a CTA-wide operation window (rv_arrive ..
+  // rv_depart, slse_port.cuh) and all control code between operations in
+  // the complementary control window, so the SM never interleaves the
+  // solver's large control code with the operations' hot loops
+  // (instruction-cache locality; measured no-instruction stalls drop from
+  // ~45 % of samples to ~1 %).  Long operations yield at rv_slice points.
+  // A warp with no problem left keeps answering with an idle vote until the
+  // whole CTA is idle (solve_kernel_warps).
+
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
     if (kk == 0) return build_white(B, be);
+#ifdef SLSE_WARP_MODE
+    SLSE_PROF_T0(w0);
+    rv_arrive(0);
+    SLSE_PROF_ADD(6, w0);
+    const int st = build_impl(B, th, ga, kk, be);
+    SLSE_PROF_T0(w1);
+    rv_depart();
+    SLSE_PROF_ADD(7, w1);
+    return st;
+#else
+    return build_impl(B, th, ga, kk, be);
+#endif
+  }
+
+  SLSE_NIM int build_impl(Bundle& B, const double* th, const double* ga, int kk, double be) {
     SLSE_PROF_T0(t0);
-    steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
+#ifndef SLSE_HOST_EMU
+    if (b.nt == 32 && n <= 512) steer_forward_warp(c, n, th, ga, nullptr, kk, be, true, b.tid);
+    else
+#endif
+      steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
     SLSE_PROF_ADD(0, t0);
     SLSE_PROF_T0(t1);
     Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham, P.dnc_direct)
@@ -393,6 +433,7 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     const double inv = 1.0 / be;
     double qp = 0.0;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < n; i += nt_) {
       B.rho[i] = mk(i == n - 1 ? 1.0 : 0.0, 0.0);
       const cplx wi = cscale(y[i], inv);
@@ -410,8 +451,27 @@ struct Solver {
   SLSE_NIM void stats(Bundle& B, const double* th, int kk) {
     if (B.stats_valid) return;
     ++n_stats;
+#ifdef SLSE_WARP_MODE
+    SLSE_PROF_T0(w0);
+    rv_arrive(0);
+    SLSE_PROF_ADD(6, w0);
+    stats_impl(B, th, kk);
+    SLSE_PROF_T0(w1);
+    rv_depart();
+    SLSE_PROF_ADD(7, w1);
+#else
+    stats_impl(B, th, kk);
+#endif
+  }
+
+  SLSE_NIM void stats_impl(Bundle& B, const double* th, int kk) {
     SLSE_PROF_T0(t0);
-    component_stats(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b);
+#ifndef SLSE_HOST_EMU
+    if (b.nt == 32 && n <= 512)
+      component_stats_warp(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b.tid);
+    else
+#endif
+      component_stats(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b);
     SLSE_PROF_ADD(3, t0);
     B.stats_valid = 1;
   }
@@ -442,6 +502,7 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;  // smlr.py:53-59
     if (k) {
       double part = 0.0;
+      SLSE_CTRL_LOOP
       for (int i = tid_; i < k; i += nt_) part += act_gamma[i];
       double bar = b.sum(part) / (double)k;
       if (bar > 0.0) return bar;
@@ -451,8 +512,22 @@ struct Solver {
   }
 
   SLSE_NIM void grid_curve(double gb, double ze) {
-    const int tid_ = b.tid, nt_ = b.nt;
     ++n_grids;
+#ifdef SLSE_WARP_MODE
+    SLSE_PROF_T0(w0);
+    rv_arrive(0);
+    SLSE_PROF_ADD(6, w0);
+    grid_impl(gb, ze);
+    SLSE_PROF_T0(w1);
+    rv_depart();
+    SLSE_PROF_ADD(7, w1);
+#else
+    grid_impl(gb, ze);
+#endif
+  }
+
+  SLSE_NIM void grid_impl(double gb, double ze) {
+    const int tid_ = b.tid, nt_ = b.nt;
     Bundle& B = bun[cur];
     const double lr = log((1.0 - ze) / ze);
     SLSE_PROF_T0(t0);
@@ -461,6 +536,7 @@ struct Solver {
       return;
     }
     grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
+    SLSE_CTRL_LOOP
     for (int l = tid_; l < L; l += nt_) {
       const double qq = cabs2(G0[l]);
       q2[l] = qq;
@@ -487,6 +563,7 @@ struct Solver {
     grid_curve(gb, ze);
     double best = 0.0;
     int bi = -1;
+    SLSE_CTRL_LOOP
     for (int l = tid_; l < L; l += nt_) {
       const double d = dl[l];
       if (Blk::better(d, l, best, bi)) { best = d; bi = l; }
@@ -523,6 +600,7 @@ struct Solver {
     // circular local minima and their minimum
     double mn = 0.0;
     int mi = -1;
+    SLSE_CTRL_LOOP
     for (int l = tid_; l < L; l += nt_) {
       const double d = dl[l];
       const double dp = dl[(l + L - 1) & (L - 1)], dn = dl[(l + 1) & (L - 1)];
@@ -554,6 +632,7 @@ struct Solver {
     }
     b.sync();
     // stable sort by (delta, index): rank = #{j: (d_j, j) < (d_i, i)}
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < m; i += nt_) {
       const int li = cidx[i];
       const double di = dl[li];
@@ -622,6 +701,7 @@ struct Solver {
       const double rhs = log((1.0 - ze) / ze);
       double wv = 0.0;
       int wi = -1;
+      SLSE_CTRL_LOOP
       for (int i = tid_; i < k; i += nt_) {
         const double ga = act_gamma[i];
         const double s = B.s[i];
@@ -665,6 +745,7 @@ struct Solver {
   // ---- gradient / diag Hessian (model_core.py:497-536) ----
   SLSE_NIM void gradient(const Bundle& B, const double* ga, double* g) {
     const int tid_ = b.tid, nt_ = b.nt;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) {
       const cplx q = B.q[i], r = B.r[i], t = B.t[i];
       const cplx cross = cmul(conjg(q), r);
@@ -676,6 +757,7 @@ struct Solver {
   SLSE_NIM void diag_hessian(const Bundle& B, const double* ga_, double* d) {
     const int tid_ = b.tid, nt_ = b.nt;
     const double fb_theta = (double)(50 * n) * (double)(50 * n);
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) {
       const double ga = ga_[i];
       const cplx q = B.q[i], r = B.r[i], u = B.u[i], t = B.t[i], v = B.v[i];
@@ -708,6 +790,7 @@ struct Solver {
   SLSE_D double dot(const double* p, const double* q, int dim) {
     const int tid_ = b.tid, nt_ = b.nt;
     double part = 0.0;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < dim; i += nt_) part += p[i] * q[i];
     return b.sum(part);
   }
@@ -717,6 +800,7 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     double alphas[16];
     double* qv = gnew;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < dim; i += nt_) qv[i] = g0[i];
     const int K2 = 2 * kmax;
     for (int jj = mem_count - 1; jj >= 0; --jj) {
@@ -725,8 +809,10 @@ struct Solver {
       const double* Y = lbY + (size_t)slot * K2;
       const double al_ = lbR[slot] * dot(S, qv, dim);
       alphas[jj] = al_;
+      SLSE_CTRL_LOOP
       for (int i = tid_; i < dim; i += nt_) qv[i] -= al_ * Y[i];
     }
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < dim; i += nt_) dir[i] = qv[i] / diag[i];
     for (int jj = 0; jj < mem_count; ++jj) {
       const int slot = (mem_head + jj) % P.lbfgs_mem;
@@ -734,8 +820,10 @@ struct Solver {
       const double* Y = lbY + (size_t)slot * K2;
       const double be = lbR[slot] * dot(Y, dir, dim);
       const double coef = alphas[jj] - be;
+      SLSE_CTRL_LOOP
       for (int i = tid_; i < dim; i += nt_) dir[i] += S[i] * coef;
     }
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < dim; i += nt_) dir[i] = -dir[i];
   }
 
@@ -747,6 +835,7 @@ struct Solver {
     double* S = lbS + (size_t)slot * K2;
     double* Y = lbY + (size_t)slot * K2;
     double pv[3] = {0.0, 0.0, 0.0};
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < dim; i += nt_) {
       const double s = alpha * dir[i];
       const double yv = gnew[i] - g0[i];
@@ -776,6 +865,7 @@ struct Solver {
     const int dim = 2 * k;
     // any(g0)?
     double nz = 0.0;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < dim; i += nt_) nz += (g0[i] != 0.0) ? 1.0 : 0.0;
     if (b.sum(nz) == 0.0) {
       *dec = 0.0;
@@ -784,12 +874,14 @@ struct Solver {
     two_loop(dim);
     double slope = dot(g0, dir, dim);
     if (slope >= 0.0) {
+      SLSE_CTRL_LOOP
       for (int i = tid_; i < dim; i += nt_) dir[i] = -g0[i] / diag[i];
       slope = dot(g0, dir, dim);
     }
     *dec = -slope;
     // gamma step cap (lbfgs.py:84-90)
     double capv = INFINITY;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) {
       const double dg = dir[k + i];
       if (dg < 0.0) {
@@ -803,6 +895,7 @@ struct Solver {
     Bundle& T = bun[cur ^ 1];
     for (int bt = 0; bt < kMaxBacktracks; ++bt) {
       ++n_backtracks;
+      SLSE_CTRL_LOOP
       for (int i = tid_; i < k; i += nt_) {
         cth[i] = np_mod1(pt[i] + alpha * dir[i]);
         cga[i] = pt[k + i] + alpha * dir[k + i];
@@ -819,6 +912,7 @@ struct Solver {
         b.sync();
         push_pair(alpha, dim);
         // accept: write the point into the slots; swap bundles
+        SLSE_CTRL_LOOP
         for (int i = tid_; i < k; i += nt_) {
           const int s = act_slot[i];
           theta[s] = cth[i];
@@ -990,10 +1084,16 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     double* mre = marg;  // scratch (length >= k)
     double* mim = dtmp;  // scratch (length n >= k), free outside build()
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) { mre[i] = mu[i].re; mim[i] = mu[i].im; }
     b.sync();
-    steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
+#ifndef SLSE_HOST_EMU
+    if (b.nt == 32 && n <= 512) steer_forward_warp(c, n, act_theta, mre, mim, k, 0.0, false, b.tid);
+    else
+#endif
+      steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
     double part = 0.0;
+    SLSE_CTRL_LOOP
     for (int i = tid_; i < n; i += nt_) part += cabs2(csub(y[i], c[i]));
     const double resid = b.sum(part);
     return (tr + resid) / (double)n;
@@ -1006,6 +1106,7 @@ struct Solver {
       int st = ensure_cur();
       if (st == kOk) {
         stats(bun[cur], act_theta, k);
+        SLSE_CTRL_LOOP
         for (int i = tid_; i < k; i += nt_) {
           o.alpha[i] = cscale(bun[cur].q[i], act_gamma[i]);
           o.theta[i] = act_theta[i];
@@ -1020,7 +1121,7 @@ struct Solver {
 #ifdef SLSE_SOLVER_PROF
     prof_acc[5] = clock64() - prof_run0;
     if (b.leader())
-      for (int i = 0; i < 6; ++i) atomicAdd(&slse_prof_cycles[i], (unsigned long long)prof_acc[i]);
+      for (int i = 0; i < 8; ++i) atomicAdd(&slse_prof_cycles[i], (unsigned long long)prof_acc[i]);
 #endif
     if (converged) flags |= kFlConverged;
     if (b.leader()) {

@@ -187,6 +187,76 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
   b.sync();
 }
 
+#ifndef SLSE_HOST_EMU
+// One-warp form of component_stats (N <= 512 solver path): same sums and
+// epilogue, rolled loops, one phasor recurrence per frequency.
+static __device__ __noinline__ void component_stats_warp(const double* SLSE_RESTRICT thetas, int K,
+                                                         const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT w,
+                                                         int n, double delta_last, const CfTable* cf, cplx* q,
+                                                         cplx* r, cplx* u, double* s, cplx* t, cplx* v, double* x,
+                                                         int lane) {
+  const double inv_d = 1.0 / delta_last;
+  const double two_pi = 2.0 * kPi;
+  const double sc_tv = two_pi * inv_d, sc_vx = 4.0 * kPi * kPi * inv_d;
+  const int pa = (lane >> 2) & 3, pb = lane & 3;
+  const double* cfp = &cf->cf[0][pa][pb];
+  const double c0 = lane < 16 ? cfp[0] : 0.0, c1 = lane < 16 ? cfp[16] : 0.0;
+  const double c2 = lane < 16 ? cfp[32] : 0.0, c3 = lane < 16 ? cfp[48] : 0.0;
+#pragma unroll 1
+  for (int kk = 0; kk < K; ++kk) {
+    const double th = thetas[kk];
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    cplx e = expj2pi((double)lane, th, -1.0);
+    const cplx step = expj2pi(32.0, th, -1.0);
+#pragma unroll 1
+    for (int m = lane; m < n; m += 32) {
+      const double dm = (double)m;
+      const cplx p = cmul(rho[m], e);
+      const cplx qq = cmul(w[m], e);
+      const double m2 = dm * dm, m3 = m2 * dm;
+      acc[0] += p.re;       acc[1] += p.im;
+      acc[2] += dm * p.re;  acc[3] += dm * p.im;
+      acc[4] += m2 * p.re;  acc[5] += m2 * p.im;
+      acc[6] += m3 * p.re;  acc[7] += m3 * p.im;
+      const double d1 = two_pi * dm;
+      const double d2 = d1 * d1;
+      acc[8] += qq.re;       acc[9] += qq.im;
+      acc[10] += d1 * qq.re; acc[11] += d1 * qq.im;
+      acc[12] += d2 * qq.re; acc[13] += d2 * qq.im;
+      e = cmul(e, step);
+    }
+    const double red = warp_tsum<16>(acc, lane);  // sum v in lanes 2v, 2v+1
+    const double a_re = __shfl_sync(0xffffffffu, red, 4 * pa), a_im = __shfl_sync(0xffffffffu, red, 4 * pa + 2);
+    const double b_re = __shfl_sync(0xffffffffu, red, 4 * pb), b_im = __shfl_sync(0xffffffffu, red, 4 * pb + 2);
+    const cplx P = cmulc(mk(a_re, a_im), mk(b_re, b_im));
+    double term[8];
+    term[0] = c0 * P.re;
+    term[1] = c1 * P.re; term[2] = c1 * P.im;
+    term[3] = c2 * P.re; term[4] = c2 * P.im;
+    term[5] = c3 * P.re;
+    term[6] = term[7] = 0.0;
+    const double tot = warp_tsum<8>(term, lane);
+    // lane -> output: 0 s, 2/4 t, 6/8 v, 10 x (from tot); 16..26 q, r, u (from red)
+    double* dst = nullptr;
+    double val = 0.0;
+    if (lane < 12 && !(lane & 1)) {
+      const int o = lane >> 1;
+      val = tot * (o == 0 ? inv_d : (o <= 2 ? sc_tv : sc_vx));
+      dst = o == 0 ? &s[kk] : (o <= 2 ? (double*)&t[kk] + (o - 1) : (o <= 4 ? (double*)&v[kk] + (o - 3) : &x[kk]));
+    } else if (lane >= 16 && lane < 28 && !(lane & 1)) {
+      const int o = (lane - 16) >> 1;
+      val = red;
+      cplx* arr = o < 2 ? q : (o < 4 ? r : u);
+      dst = (double*)&arr[kk] + (o & 1);
+    }
+    if (dst) *dst = val;
+  }
+  __syncwarp();
+}
+#endif
+
 // Activation grid (model_core.py:303-313) in product form:
 //   q^G = FFT_L(w),  s^G = delta^{-1} [(2-N)|A0|^2 + 2 Re(A1 conj A0)],
 //   A0 = FFT_L(rho), A1 = FFT_L(n rho_n).

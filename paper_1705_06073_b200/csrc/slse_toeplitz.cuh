@@ -65,6 +65,44 @@ SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RE
   b.sync();
 }
 
+#ifndef SLSE_HOST_EMU
+// One-warp form of steer_forward (N <= 512 solver path): lane owns
+// m = lane + 32 j in chunks of 8, phasor recurrence anchored by an exact
+// sincospi per chunk; small rolled body (instruction-cache footprint).
+static __device__ __noinline__ void steer_forward_warp(cplx* SLSE_RESTRICT out, int n,
+                                                       const double* SLSE_RESTRICT thetas,
+                                                       const double* SLSE_RESTRICT coef_re,
+                                                       const double* SLSE_RESTRICT coef_im, int k, double beta0,
+                                                       bool column, int lane) {
+#pragma unroll 1
+  for (int m0 = lane; m0 < n; m0 += 256) {
+    cplx acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = mk(0.0, 0.0);
+#pragma unroll 1
+    for (int kk = 0; kk < k; ++kk) {
+      const double th = thetas[kk];
+      const double cr = coef_re[kk];
+      const double ci = coef_im ? coef_im[kk] : 0.0;
+      cplx e = expj2pi((double)m0, th, 1.0);
+      const cplx step = expj2pi(32.0, th, 1.0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[j].re += e.re * cr - e.im * ci;
+        acc[j].im += e.re * ci + e.im * cr;
+        e = cmul(e, step);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int m = m0 + 32 * j;
+      if (m < n) out[m] = (column && m == 0) ? mk(acc[j].re + beta0, 0.0) : acc[j];
+    }
+  }
+  __syncwarp();
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // Rows 2-4: Gohberg-Semencul parameters (rho, delta) by the Schur-Levinson
 // recursion.  Reflection coefficients come from the Schur generators
@@ -448,6 +486,9 @@ SLSE_D Factor toeplitz_factor_regs(const cplx* SLSE_RESTRICT c, int n, double* d
 // ~2.5 KB loop body instead of a 30 KB unrolled one.  The persistent solver
 // interleaves every phase on an SM, so instruction-cache footprint matters
 // more than the ~40 % extra ALU instructions (measured on B200).
+#ifndef SLSE_LEV_SLICE
+#define SLSE_LEV_SLICE 0  // warp mode: yield the operation window every this many steps (0: never)
+#endif
 template <int Q>
 SLSE_D Factor toeplitz_factor_regs_c(const cplx* SLSE_RESTRICT c, int n, double* delta_out, double* delta_tmp,
                                      cplx* SLSE_RESTRICT rho, Blk& b) {
@@ -509,6 +550,9 @@ SLSE_D Factor toeplitz_factor_regs_c(const cplx* SLSE_RESTRICT c, int n, double*
     if (!(delta > floor_)) { fail = 1; break; }
     kr = nr;
     ki = ni;
+#if SLSE_LEV_SLICE > 0
+    if ((m & (SLSE_LEV_SLICE - 1)) == SLSE_LEV_SLICE - 1) SLSE_RV_SLICE();
+#endif
   }
   if (fail) {
     F.status = kNotPD;
@@ -672,17 +716,17 @@ SLSE_D void warp_pass_rt(cplx* S, int lg, int lgns, double sign, const cplx* __r
 }
 
 // One-warp in-place transform of 2^lg (<= 512) points on the skewed shared
-// buffer S: radix-8 passes, then one radix-4 or radix-2 pass.  One compact
-// out-of-line body for every size and direction.
+// buffer S: radix-4 passes, then one radix-2 pass when lg is odd.  One
+// compact out-of-line body for every size and direction (radix 8 runs fewer
+// passes but its 3x larger body costs more in instruction fetch).
 static __device__ __noinline__ void warp_fft_rt(cplx* S, int lg, double sign, const cplx* __restrict__ tw, int twlog,
                                          int lane_) {
   __builtin_assume(__isShared(S));
   const unsigned lane = (unsigned)lane_ & 31u;
   int lgns = 0;
 #pragma unroll 1
-  for (; lg - lgns >= 3; lgns += 3) warp_pass_rt<8>(S, lg, lgns, sign, tw, twlog, lane);
-  if (lg - lgns == 2) warp_pass_rt<4>(S, lg, lgns, sign, tw, twlog, lane);
-  else if (lg - lgns == 1) warp_pass_rt<2>(S, lg, lgns, sign, tw, twlog, lane);
+  for (; lg - lgns >= 2; lgns += 2) warp_pass_rt<4>(S, lg, lgns, sign, tw, twlog, lane);
+  if (lg - lgns == 1) warp_pass_rt<2>(S, lg, lgns, sign, tw, twlog, lane);
 }
 
 // IFFT, keep [N-1, 2N-1) scaled by 1/nf, zero pad, FFT (the middle of a GS
