@@ -488,8 +488,14 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
   const int nt = solver_threads(N);
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {
-    e = slse_solve_warps_launch(W, g / W, kCfBytes + (size_t)W * wsm, st, P, cft, (const cplx*)y, B, *out, ws, slab,
-                                queue, tw, twlog, plan.fft_cap, plan.rec_in_smem, wsm);
+    // twiddle table in shared memory when it fits next to the W regions
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t base = kCfBytes + (size_t)W * wsm, twb = sizeof(cplx) << twlog;
+    const int tw_smem = (!getenv("SLSE_TW_GLOBAL") && base + twb <= (size_t)optin) ? 1 : 0;
+    e = slse_solve_warps_launch(W, g / W, base + (tw_smem ? twb : 0), st, P, cft, (const cplx*)y, B, *out, ws, slab,
+                                queue, tw, twlog, plan.fft_cap, plan.rec_in_smem, wsm, tw_smem);
     return e == cudaSuccess ? 0 : fail("solve_kernel_warps", e);
   }
 #define SLSE_SOLVE_ARGS g, plan.bytes, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog, plan.fft_cap, \

@@ -165,13 +165,19 @@ template <int W>
 __global__ void __launch_bounds__(32 * W, 16 / W) solve_kernel_warps(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
                                                                     int B, slse_outputs out, char* ws, size_t slab_bytes,
                                                                     int* queue, const cplx* tw, int twlog, int fft_cap,
-                                                                    int rec_smem, int warp_smem) {
+                                                                    int rec_smem, int warp_smem, int tw_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CfTable* cf = (CfTable*)smem_raw;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* mine = smem_raw + kCfBytes + (size_t)warp * warp_smem;
+  // optional CTA-shared copy of the twiddle table (tw_smem: 1 = 2^twlog entries)
+  cplx* tws = (cplx*)(smem_raw + kCfBytes);
+  const size_t tw_bytes = tw_smem ? ((sizeof(cplx) << twlog)) : 0;
+  unsigned char* mine = smem_raw + kCfBytes + tw_bytes + (size_t)warp * warp_smem;
   if (threadIdx.x == 0) *cf = cft;
+  if (tw_smem)
+    for (int i = threadIdx.x; i < (1 << twlog); i += blockDim.x) tws[i] = tw[i];
   __syncthreads();
+  if (tw_smem) tw = tws;
   Blk b;
   b.tid = lane;
   b.nt = 32;
@@ -551,4 +557,4 @@ SLSE_DECL_SOLVE(1024)
 cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t st, const slse::SolveParams& P,
                                     const slse::CfTable& cft, const slse::cplx* ys, int B, const slse_outputs& out,
                                     char* ws, size_t slab, int* queue, const slse::cplx* tw, int twlog, int fft_cap,
-                                    int rec_smem, int warp_smem);
+                                    int rec_smem, int warp_smem, int tw_smem);

@@ -39,7 +39,7 @@ def main():
         m = re.search(r"/\*([0-9a-f]{4,})\*/", line)
         if m and label is not None:
             name = label.split("$")[-1]
-            name = re.sub(r"_ZN49_INTERNAL_\w+?4slse", "", name)
+            name = re.sub(r"_ZN\d+_INTERNAL_\w+?_cu_[0-9a-f]+4slse", "", name)
             starts.append((int(m.group(1), 16), name[:60]))
             label = None
     starts.sort()
