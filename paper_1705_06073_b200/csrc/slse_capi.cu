@@ -389,10 +389,35 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
       SLSE_GRID_Q(NTV, LGV, 0) SLSE_GRID_Q(NTV, LGV, 1) SLSE_GRID_Q(NTV, LGV, 2) SLSE_GRID_Q(NTV, LGV, 3) \
     }                                                                           \
     break;
+    // v4 (one warp per residue, registers + 4.6 KB shared per warp) for 2^ceil(log2 N) = 256:
+    // opt-in (SLSE_GRID_V4); measured 80 us vs v3's 70 us on cfg2 (latency-bound at 16 warps/SM)
+    if (getenv("SLSE_GRID_V4") != nullptr && ilog2(N) == 8 && (lg == 10 || lg == 9)) {
+      if (lg == 9)
+        grid_warp_kernel<9><<<B, 64, 0, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, (cplx*)q_grid, s_grid, tw, twlog);
+      else
+        grid_warp_kernel<10><<<B, 128, 0, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, (cplx*)q_grid, s_grid, tw, twlog);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? 0 : fail("grid_warp_kernel", e);
+    }
     // v3 (fused last pass) where the plan allows: L = 2^10 (NT 256), 2^11 (256), 2^7 (16: too small -> skip)
     if (getenv("SLSE_GRID_V2") == nullptr && (lg == 10 || lg == 11)) {
 #define SLSE_GRID3_Q(NTV, LGV, QV)                                                                        \
   case QV: {                                                                                               \
+    if (getenv("SLSE_GRID_PERSIST3") != nullptr) {  /* persistent v3 + cp.async: measured slower (100 vs 70 us) */ \
+      const size_t psmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV) + 64 * (size_t)N;             \
+      e = set_smem(grid_fused_persist_kernel<NTV, LGV, QV>, psmem);                                        \
+      int occ = 0;                                                                                         \
+      if (e == cudaSuccess)                                                                                \
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_fused_persist_kernel<NTV, LGV, QV>, NTV, psmem); \
+      if (e == cudaSuccess && occ > 0) {                                                                   \
+        int g = sm_count() * occ;                                                                          \
+        if (g > B) g = B;                                                                                  \
+        grid_fused_persist_kernel<NTV, LGV, QV><<<g, NTV, psmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, \
+                                                                       N, B, (cplx*)q_grid, s_grid, tw, twlog); \
+        e = cudaGetLastError();                                                                            \
+        return e == cudaSuccess ? 0 : fail("grid_fused_persist_kernel", e);                                \
+      }                                                                                                    \
+    }                                                                                                      \
     const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
     e = set_smem(grid_fused_kernel<NTV, LGV, QV>, ssmem);                                                  \
     if (e == cudaSuccess) {                                                                                \
