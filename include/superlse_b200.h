@@ -20,8 +20,12 @@
  *   slse_toeplitz_factor   <- toeplitz.decompose :263-276
  *                             (levinson_durbin :121-145, generalized_schur :230-260)
  *   slse_gs_apply          <- toeplitz.apply_inverse :279-309 (+ quad, model_core.py:268-269)
+ *   slse_omegas            <- toeplitz.all_diagonal_sums :415-432 (model_core.omegas :276-279)
  *   slse_component_stats   <- model_core._SuperfastBundle.stats :281-301
  *   slse_grid_eval         <- model_core._SuperfastBundle.grid :303-313
+ *   slse_activation_curve  <- smlr._delta_objective_curve :62-70 + best_candidate argmin :84-96
+ *   slse_deactivation_margins <- smlr.deactivation_margins :174-200 (+ try_deactivate argmin :203-225)
+ *   slse_gradient_hessian  <- model_core.gradient :497-505, diag_hessian :508-536
  *   slse_estimate_batch    <- estimator.estimate :117-275 (complete data, G = 1,
  *                             backend "superfast"), one problem per batch row
  */
@@ -105,6 +109,12 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
 int slse_gs_apply(const double* rho, const double* delta_last, const double* y, int N, int B,
                   double* w, double* quad, void* stream);
 
+/* Row 7: diagonal sums omega_kind(i), i = -(N-1)..N-1 (index i + N - 1) for
+ * kind = s, t, v, x; each [B, 2N-1] complex (s and x Hermitian-symmetrised
+ * as toeplitz.py:428-430). */
+int slse_omegas(const double* rho, const double* delta_last, int N, int B, double* om_s, double* om_t,
+                double* om_v, double* om_x, void* stream);
+
 /* Row 8: statistics at kcount[b] frequencies (rows of stride kstride).
  * q, r, u, t, v: [B, kstride] complex; s, x: [B, kstride] real. */
 int slse_component_stats(const double* theta, const int32_t* kcount, int kstride, const double* rho,
@@ -115,6 +125,30 @@ int slse_component_stats(const double* theta, const int32_t* kcount, int kstride
 /* Row 9: activation grid.  q_grid [B, L] complex (FFT_L(w)), s_grid [B, L] real. */
 int slse_grid_eval(const double* rho, const double* delta_last, const double* w, int N, int L, int B,
                    double* q_grid, double* s_grid, void* stream);
+
+/* Row 10: activation curve Delta L_l = log1p(gbar s_l) + ln((1-ze)/ze)
+ * - |q_l|^2 / (1/gbar + s_l) over the grid (G = 1; ze = clamp(zeta[b],
+ * 1/(2 kmax), 1/2)) and its argmin, lowest index on ties.  curve [B, L]
+ * (may be NULL), argmin [B]. */
+int slse_activation_curve(const double* q_grid, const double* s_grid, const double* gamma_bar,
+                          const double* zeta, int kmax, int L, int B, double* curve, int32_t* argmin,
+                          void* stream);
+
+/* Row 11: deactivation margins of the kcount[b] active components (rows of
+ * stride kstride: q complex, s and gamma real) and their argmin (lowest
+ * index on ties; -1 when kcount[b] = 0).  margin [B, kstride] (may be NULL). */
+int slse_deactivation_margins(const double* q, const double* s, const double* gamma, const int32_t* kcount,
+                              int kstride, const double* zeta, int kmax, int B, double* margin,
+                              int32_t* argmin, void* stream);
+
+/* Row 12: gradient and diagonal Hessian in (theta, gamma) of the kcount[b]
+ * components from their statistics (layout of slse_component_stats) and
+ * gamma [B, kstride].  g, d: [B, 2 kstride]; row b holds the theta block
+ * in [0, k) and the gamma block in [k, 2k), k = kcount[b]. */
+int slse_gradient_hessian(const double* q, const double* r, const double* u, const double* s,
+                          const double* t, const double* v, const double* x, const double* gamma,
+                          const int32_t* kcount, int kstride, int N, int B, double* g, double* d,
+                          void* stream);
 
 /* Rows 10-15: the whole estimate() per problem.  y: [B, N] complex.
  * workspace: device buffer of slse_estimate_workspace_bytes() bytes. */

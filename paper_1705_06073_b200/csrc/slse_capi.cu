@@ -322,6 +322,70 @@ int slse_gs_apply(const double* rho, const double* delta_last, const double* y, 
   return e == cudaSuccess ? 0 : fail("apply_kernel", e);
 }
 
+int slse_omegas(const double* rho, const double* delta_last, int N, int B, double* om_s, double* om_t, double* om_v,
+                double* om_x, void* stream) {
+  if (N < 2 || B < 0) return fail_arg("slse_omegas: need N >= 2");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nf = 1 << ilog2(2 * N - 1);
+  const cplx* tw;
+  int twlog;
+  int rc = twiddles(ilog2(nf), st, &tw, &twlog);
+  if (rc) return rc;
+  CfTable cft;
+  cf_build(cft, N);
+  const int nt = block_threads(N);
+  const int cap = 16 * (size_t)sk_len(nf) <= kRegionBudget ? sk_len(nf) : 0;
+  const size_t smem = kHeadBytes + 16 * (size_t)cap;
+  cplx* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, sizeof(cplx) * 9 * (size_t)nf * B, st);
+  if (e != cudaSuccess) return fail("cudaMallocAsync", e);
+  SLSE_DISPATCH_NT(nt, {
+    e = set_smem(omegas_kernel<NTC>, smem);
+    if (e == cudaSuccess) {
+      omegas_kernel<NTC><<<B, NTC, smem, st>>>(cft, (const cplx*)rho, delta_last, N, (cplx*)om_s, (cplx*)om_t,
+                                              (cplx*)om_v, (cplx*)om_x, scratch, tw, twlog, cap);
+      e = cudaGetLastError();
+    }
+  });
+  cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? 0 : fail("omegas_kernel", e);
+}
+
+int slse_activation_curve(const double* q_grid, const double* s_grid, const double* gamma_bar, const double* zeta,
+                          int kmax, int L, int B, double* curve, int32_t* argmin, void* stream) {
+  if (L < 1 || B < 0 || kmax < 1 || argmin == nullptr) return fail_arg("slse_activation_curve: bad arguments");
+  if (B == 0) return 0;
+  act_curve_kernel<256><<<B, 256, kHeadBytes, (cudaStream_t)stream>>>((const cplx*)q_grid, s_grid, gamma_bar, zeta,
+                                                                       kmax, L, curve, argmin);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail("act_curve_kernel", e);
+}
+
+int slse_deactivation_margins(const double* q, const double* s, const double* gamma, const int32_t* kcount,
+                              int kstride, const double* zeta, int kmax, int B, double* margin, int32_t* argmin,
+                              void* stream) {
+  if (kstride < 1 || B < 0 || kmax < 1 || argmin == nullptr) return fail_arg("slse_deactivation_margins: bad arguments");
+  if (B == 0) return 0;
+  deact_kernel<128><<<B, 128, kHeadBytes, (cudaStream_t)stream>>>((const cplx*)q, s, gamma, kcount, kstride, zeta,
+                                                                  kmax, margin, argmin);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail("deact_kernel", e);
+}
+
+int slse_gradient_hessian(const double* q, const double* r, const double* u, const double* s, const double* t,
+                          const double* v, const double* x, const double* gamma, const int32_t* kcount, int kstride,
+                          int N, int B, double* g, double* d, void* stream) {
+  if (kstride < 1 || B < 0 || N < 1) return fail_arg("slse_gradient_hessian: bad arguments");
+  if (B == 0) return 0;
+  const long long tot = (long long)B * kstride;
+  grad_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const cplx*)q, (const cplx*)r, (const cplx*)u, s, (const cplx*)t, (const cplx*)v, x, gamma, kcount, kstride, B,
+      N, g, d);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : fail("grad_kernel", e);
+}
+
 int slse_component_stats(const double* theta, const int32_t* kcount, int kstride, const double* rho,
                          const double* delta_last, const double* w, int N, int B, double* q, double* r, double* u,
                          double* s, double* t, double* v, double* x, void* stream) {

@@ -255,6 +255,141 @@ __global__ void __launch_bounds__(NT) apply_kernel(const cplx* rho, const double
   if (quad && threadIdx.x == 0) quad[p] = qd;
 }
 
+// Row 7: the four diagonal-sum vectors omega_kind(i), i = -(N-1)..N-1
+// (toeplitz.py:415-432) from the same cf table as the product-form stats:
+//   omega_kind(i) = scale / delta  sum_ab cf[kind][a][b] R_ab(i),
+//   R_ab(i) = sum_q q^a rho_q (q+i)^b conj(rho_{q+i})
+//           = IFFT( P_a . Y_b )(i) / nf,  P_a = sum_q q^a rho_q e^{+j..},
+//             Y_b = FFT(q^b conj(rho)),  nf >= 2N - 1  (no wrap),
+// so 4 + 4 + 4 transforms of nf per problem; s and x are symmetrised as
+// the reference does (:428-430).  Scratch: 9 nf complex per problem.
+template <int NT>
+__global__ void __launch_bounds__(NT) omegas_kernel(CfTable cft, const cplx* rho, const double* delta_last, int n,
+                                                    cplx* om_s, cplx* om_t, cplx* om_v, cplx* om_x, cplx* scratch,
+                                                    const cplx* tw, int twlog, int fft_cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  FftCtx f{tw, twlog, (cplx*)(smem_raw + kHeadBytes), fft_cap};
+  const int p = blockIdx.x;
+  const int lg = ilog2(2 * n - 1);
+  const int nf = 1 << lg;
+  cplx* P = scratch + (size_t)p * 9 * nf;
+  cplx* Y = P + 4 * (size_t)nf;
+  cplx* W = Y + 4 * (size_t)nf;
+  const cplx* rp = rho + (size_t)p * n;
+  const cplx z = mk(0.0, 0.0);
+  for (int a = 0; a < 4; ++a) {
+    cplx* Pa = P + (size_t)a * nf;
+    fft(W, nf, 1.0, [=](int i) { return i < n ? cscale(rp[i], a == 0 ? 1.0 : pow((double)i, (double)a)) : z; },
+        [=](int i, cplx v) { Pa[i] = v; }, f, b);
+    cplx* Yb = Y + (size_t)a * nf;
+    fft(W, nf, -1.0, [=](int i) { return i < n ? cscale(conjg(rp[i]), a == 0 ? 1.0 : pow((double)i, (double)a)) : z; },
+        [=](int i, cplx v) { Yb[i] = v; }, f, b);
+  }
+  const double dl = delta_last[p];
+  const double scales[4] = {1.0, 2.0 * kPi, 4.0 * kPi * kPi, 4.0 * kPi * kPi};
+  cplx* outs[4] = {om_s, om_t, om_v, om_x};
+  const int len = 2 * n - 1;
+  for (int kind = 0; kind < 4; ++kind) {
+    cplx* om = outs[kind] + (size_t)p * len;
+    const double sc = scales[kind] / (dl * (double)nf);
+    const CfTable T = cft;
+    const cplx* Pc = P;
+    const cplx* Yc = Y;
+    fft(W, nf, 1.0,
+        [=](int fi) {
+          cplx acc = z;
+          for (int a = 0; a < 4; ++a)
+            for (int bb = 0; bb < 4; ++bb) {
+              const double c = T.cf[kind][a][bb];
+              if (c != 0.0) acc = cadd(acc, cscale(cmul(Pc[(size_t)a * nf + fi], Yc[(size_t)bb * nf + fi]), c));
+            }
+          return acc;
+        },
+        [=](int i, cplx v) {
+          int d = -1;
+          if (i <= n - 1) d = i + n - 1;             // lag i >= 0
+          else if (i >= nf - (n - 1)) d = i - nf + n - 1;  // lag i - nf < 0
+          if (d >= 0) om[d] = cscale(v, sc);
+        },
+        f, b);
+    if (kind == 0 || kind == 3) {  // Hermitian symmetrisation (s, x)
+      b.sync();
+      for (int d = threadIdx.x; d < n - 1; d += NT) om[d] = conjg(om[len - 1 - d]);
+      if (threadIdx.x == 0) om[n - 1].im = 0.0;
+      b.sync();
+    }
+  }
+}
+
+// Row 10: Delta-L curve over the grid and its argmin (lowest index on ties),
+// one CTA per problem.  gbar, zeta per problem; zeta is clamped as the
+// prior does (prior_zeta).
+template <int NT>
+__global__ void __launch_bounds__(NT) act_curve_kernel(const cplx* q_grid, const double* s_grid, const double* gbar,
+                                                       const double* zeta, int kmax, int L, double* curve,
+                                                       int* argmin_idx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  const double gb = gbar[p];
+  const double ze = prior_zeta(zeta[p], kmax);
+  const double lr = log((1.0 - ze) / ze);
+  double bv = 0.0;
+  int bi = -1;
+  for (int l = threadIdx.x; l < L; l += NT) {
+    const double dv = gain(cabs2(q_grid[(size_t)p * L + l]), s_grid[(size_t)p * L + l], gb, lr);
+    if (curve) curve[(size_t)p * L + l] = dv;
+    if (Blk::better(dv, l, bv, bi)) { bv = dv; bi = l; }
+  }
+  b.argmin(bv, bi);
+  if (threadIdx.x == 0) argmin_idx[p] = bi;
+}
+
+// Row 11: deactivation margins of the kcount[p] components (smlr.py:174-200)
+// and their argmin (lowest index on ties).
+template <int NT>
+__global__ void __launch_bounds__(NT) deact_kernel(const cplx* q, const double* s, const double* gamma,
+                                                   const int* kcount, int kstride, const double* zeta, int kmax,
+                                                   double* margin, int* argmin_idx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b{(int)threadIdx.x, NT, (double*)smem_raw, 0};
+  const int p = blockIdx.x;
+  const int k = kcount[p];
+  const double ze = prior_zeta(zeta[p], kmax);
+  const double rhs = log((1.0 - ze) / ze);
+  double bv = 0.0;
+  int bi = -1;
+  for (int i = threadIdx.x; i < k; i += NT) {
+    const size_t o = (size_t)p * kstride + i;
+    const double mg = deact_margin(gamma[o], s[o], cabs2(q[o]), rhs);
+    if (margin) margin[o] = mg;
+    if (Blk::better(mg, i, bv, bi)) { bv = mg; bi = i; }
+  }
+  b.argmin(bv, bi);
+  if (threadIdx.x == 0) argmin_idx[p] = bi;
+}
+
+// Row 12: gradient and diagonal Hessian (model_core.py:497-536), one thread
+// per component; g and d are [B, 2 kstride] (theta block, then gamma block).
+static __global__ void grad_kernel(const cplx* q, const cplx* r, const cplx* u, const double* s, const cplx* t, const cplx* v,
+                            const double* x, const double* gamma, const int* kcount, int kstride, int B, int n,
+                            double* g, double* d) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * kstride) return;
+  const int p = (int)(idx / kstride), i = (int)(idx - (long long)p * kstride);
+  if (i >= kcount[p]) return;
+  const int k = kcount[p];
+  double gth, gga, dth, dga;
+  grad_diag_comp(gamma[idx], q[idx], r[idx], u[idx], s[idx], t[idx], v[idx], x[idx], n, &gth, &gga, &dth, &dga);
+  double* gp = g + (size_t)p * 2 * kstride;
+  double* dp = d + (size_t)p * 2 * kstride;
+  gp[i] = gth;
+  gp[k + i] = gga;
+  dp[i] = dth;
+  dp[k + i] = dga;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) stats_kernel(CfTable cft, const double* theta, const int* kcount, int kstride,
                                                    const cplx* rho, const double* delta_last, const cplx* w, int n,

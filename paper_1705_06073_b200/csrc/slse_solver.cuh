@@ -202,6 +202,46 @@ SLSE_D double prior_zeta(double zeta, int kmax) {  // model_core.py:230-234
   return z < 0.5 ? z : 0.5;
 }
 
+// Row 11: one deactivation margin (smlr.py:174-200); rhs = ln((1-ze)/ze).
+SLSE_HD double deact_margin(double ga, double s, double qq, double rhs) {
+  const double den = 1.0 - ga * s;
+  if (ga <= 0.0) return rhs > 0.0 ? -INFINITY : 0.0;
+  if (den <= 0.0) return INFINITY;
+  const double q2dd = qq / (den * den);
+  const double sdd = s / den;
+  return (q2dd / (1.0 / ga + sdd) - log1p(ga * sdd)) - rhs;
+}
+
+// Row 12: gradient and diagonal Hessian of one component
+// (model_core.py:497-536).
+SLSE_HD void grad_diag_comp(double ga, cplx q, cplx r, cplx u, double s, cplx t, cplx v, double x, int n,
+                            double* gth, double* gga, double* dth, double* dga) {
+  const cplx cross = cmul(conjg(q), r);
+  *gth = 2.0 * ga * (t.im - cross.im);
+  *gga = s - cabs2(q);
+  const double qq = cabs2(q), rr = cabs2(r);
+  const cplx rqc = cmul(r, conjg(q));
+  const cplx uqc = cmul(u, conjg(q));
+  const cplx t2 = cmul(t, t);
+  const cplx c1 = mk(x - v.re, -v.im);
+  const cplx c2 = cscale(mk(t2.re - x * s, t2.im), ga);
+  const cplx trq = cmul(mk(2.0 * t.re, 2.0 * t.im), rqc);
+  const cplx c3 = cscale(mk(x * qq + s * rr - trq.re, -trq.im), ga);
+  cplx core = cadd(cadd(c1, c2), c3);
+  core = cadd(core, uqc);
+  core.re -= rr;
+  double d2t = 2.0 * ga * core.re;
+  double d2g = 2.0 * s * qq - s * s;
+  if (d2t <= 0.0) d2t = (double)(50 * n) * (double)(50 * n);
+  if (d2g <= 0.0) {
+    const double sg_ = ga > 0.0 ? ga : 1.0 / (50.0 * (double)n);
+    d2g = 1.0 / (sg_ * sg_);
+  }
+  *dth = d2t;
+  *dga = d2g;
+}
+
+
 SLSE_D double prior_term(int k, double zeta, int kmax) {  // model_core.py:237-239
   const double ze = prior_zeta(zeta, kmax);
   return -((double)k * log(ze) + (double)(kmax - k) * log1p(-ze));
@@ -703,21 +743,7 @@ struct Solver {
       int wi = -1;
       SLSE_CTRL_LOOP
       for (int i = tid_; i < k; i += nt_) {
-        const double ga = act_gamma[i];
-        const double s = B.s[i];
-        const double den = 1.0 - ga * s;
-        double mgn;
-        if (ga <= 0.0) {
-          mgn = rhs > 0.0 ? -INFINITY : 0.0;
-        } else if (den <= 0.0) {
-          mgn = INFINITY;
-        } else {
-          const double qq = cabs2(B.q[i]);
-          const double q2dd = qq / (den * den);
-          const double sdd = s / den;
-          const double lhs = q2dd / (1.0 / ga + sdd) - log1p(ga * sdd);
-          mgn = lhs - rhs;
-        }
+        const double mgn = deact_margin(act_gamma[i], B.s[i], cabs2(B.q[i]), rhs);
         if (Blk::better(mgn, i, wv, wi)) { wv = mgn; wi = i; }
       }
       b.argmin(wv, wi);
@@ -756,33 +782,10 @@ struct Solver {
 
   SLSE_NIM void diag_hessian(const Bundle& B, const double* ga_, double* d) {
     const int tid_ = b.tid, nt_ = b.nt;
-    const double fb_theta = (double)(50 * n) * (double)(50 * n);
     SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) {
-      const double ga = ga_[i];
-      const cplx q = B.q[i], r = B.r[i], u = B.u[i], t = B.t[i], v = B.v[i];
-      const double s = B.s[i], x = B.x[i];
-      const double qq = cabs2(q), rr = cabs2(r);
-      const cplx rqc = cmul(r, conjg(q));
-      const cplx uqc = cmul(u, conjg(q));
-      // core = (x - v) + ga (t^2 - x s) + ga (x q2 + s r2 - 2 t rqc) + uqc - r2
-      const cplx t2 = cmul(t, t);
-      cplx c1 = mk(x - v.re, -v.im);
-      cplx c2 = cscale(mk(t2.re - x * s, t2.im), ga);
-      const cplx trq = cmul(mk(2.0 * t.re, 2.0 * t.im), rqc);
-      cplx c3 = cscale(mk(x * qq + s * rr - trq.re, -trq.im), ga);
-      cplx core = cadd(cadd(c1, c2), c3);
-      core = cadd(core, uqc);
-      core.re -= rr;
-      double d2t = 2.0 * ga * core.re;
-      double d2g = 2.0 * s * qq - s * s;
-      if (d2t <= 0.0) d2t = fb_theta;
-      if (d2g <= 0.0) {
-        const double sg_ = ga > 0.0 ? ga : 1.0 / (50.0 * (double)n);
-        d2g = 1.0 / (sg_ * sg_);
-      }
-      d[i] = d2t;
-      d[k + i] = d2g;
+      double gth, gga;
+      grad_diag_comp(ga_[i], B.q[i], B.r[i], B.u[i], B.s[i], B.t[i], B.v[i], B.x[i], n, &gth, &gga, &d[i], &d[k + i]);
     }
   }
 

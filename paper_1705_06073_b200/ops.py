@@ -106,3 +106,53 @@ def grid_eval(rho, delta_last, w, L, out=None):
     _native.check(lib.slse_grid_eval(_p(rho), _p(delta_last.contiguous()), _p(w), n, L, B, _p(qg), _p(sg),
                                      _stream()), "slse_grid_eval")
     return qg, sg
+
+
+def omegas(rho, delta_last):
+    """Row 7: dict s, t, v, x of the diagonal sums omega(i), i = -(N-1)..N-1,
+    each (B, 2N-1) complex (toeplitz.all_diagonal_sums, :415-432)."""
+    lib = _native.load()
+    B, n = rho.shape
+    out = {k: torch.empty((B, 2 * n - 1), dtype=torch.complex128, device=rho.device) for k in "stvx"}
+    _native.check(lib.slse_omegas(_p(rho), _p(delta_last.contiguous()), n, B, _p(out["s"]), _p(out["t"]),
+                                  _p(out["v"]), _p(out["x"]), _stream()), "slse_omegas")
+    return out
+
+
+def activation_curve(q_grid, s_grid, gamma_bar, zeta, kmax, with_curve=True):
+    """Row 10: (curve (B, L) float64 or None, argmin (B,) int32) of
+    smlr._delta_objective_curve / best_candidate (:62-70, :84-96), G = 1."""
+    lib = _native.load()
+    B, L = s_grid.shape
+    curve = torch.empty((B, L), dtype=torch.float64, device=s_grid.device) if with_curve else None
+    idx = torch.empty(B, dtype=torch.int32, device=s_grid.device)
+    _native.check(lib.slse_activation_curve(_p(q_grid), _p(s_grid), _p(gamma_bar.contiguous()), _p(zeta.contiguous()),
+                                            kmax, L, B, _p(curve), _p(idx), _stream()), "slse_activation_curve")
+    return curve, idx
+
+
+def deactivation_margins(q, s, gamma, kcount, zeta, kmax):
+    """Row 11: (margins (B, K) float64, argmin (B,) int32) of
+    smlr.deactivation_margins (:174-200); entries past kcount[b] untouched."""
+    lib = _native.load()
+    B, K = s.shape
+    margin = torch.zeros((B, K), dtype=torch.float64, device=s.device)
+    idx = torch.empty(B, dtype=torch.int32, device=s.device)
+    _native.check(lib.slse_deactivation_margins(_p(q), _p(s), _p(gamma), _p(kcount), K, _p(zeta.contiguous()), kmax,
+                                                B, _p(margin), _p(idx), _stream()), "slse_deactivation_margins")
+    return margin, idx
+
+
+def gradient_hessian(stats, gamma, kcount, n):
+    """Row 12: (g, d), each (B, 2K) float64: row b holds the theta block in
+    [0, k) and the gamma block in [k, 2k), k = kcount[b]
+    (model_core.gradient :497-505, diag_hessian :508-536)."""
+    lib = _native.load()
+    B, K = gamma.shape
+    g = torch.zeros((B, 2 * K), dtype=torch.float64, device=gamma.device)
+    d = torch.zeros((B, 2 * K), dtype=torch.float64, device=gamma.device)
+    st = {k: v.contiguous() for k, v in stats.items()}
+    _native.check(lib.slse_gradient_hessian(_p(st["q"]), _p(st["r"]), _p(st["u"]), _p(st["s"]), _p(st["t"]),
+                                            _p(st["v"]), _p(st["x"]), _p(gamma), _p(kcount), K, n, B, _p(g), _p(d),
+                                            _stream()), "slse_gradient_hessian")
+    return g, d

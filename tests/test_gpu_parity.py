@@ -194,3 +194,78 @@ def test_trajectories_superfast_forced(cfg, monkeypatch):
         assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
         assert rel(r.alpha_hat[0], z[p + "alpha_hat"]) < AMP_TOL
         assert abs(r.beta_hat - float(z[p + "beta_hat"])) / float(z[p + "beta_hat"]) < AMP_TOL
+
+
+# ---- rows 7, 10, 11, 12 as separate operators (the solver runs them fused)
+ROW_CASES = [(cfg, b, st) for cfg, nb in ((1, 2), (2, 2), (3, 1)) for b in range(nb)
+             for st in ("empty", "truth", "final")]
+
+
+@pytest.mark.parametrize("cfg,b,state", ROW_CASES)
+def test_omegas_against_reference(cfg, b, state):
+    """Row 7: the four diagonal-sum vectors against the reference's
+    all_diagonal_sums (toeplitz.py:415-432) on the golden states."""
+    from paper_1705_06073_b200 import ops
+
+    z = load(cfg)
+    p = f"p{b}_call_{state}_"
+    rho = _dev(z[p + "rho"][None, :])
+    dl = _dev(np.array([z[p + "delta"][-1]]))
+    om = ops.omegas(rho, dl)
+    for kind in "stvx":
+        assert rel(om[kind].cpu().numpy()[0], z[p + "om_" + kind]) < CALL_TOL, kind
+
+
+def _stats_of(z, p, k):
+    return {key: z[p + "st_" + key][:k] for key in "qrustvx"}
+
+
+@pytest.mark.parametrize("cfg,b,state", [c for c in ROW_CASES if c[2] != "empty"])
+def test_activation_deactivation_gradient_against_oracle(cfg, b, state):
+    """Rows 10-12 on the golden states: Delta-L curve + argmin, deactivation
+    margins + argmin, gradient and diagonal Hessian, each against the oracle
+    restatement of smlr.py / model_core.py."""
+    from paper_1705_06073_b200 import ops
+
+    z = load(cfg)
+    p = f"p{b}_call_{state}_"
+    n = z[f"p{b}_y"].size
+    L = O.default_grid_size(n, 4)
+    kmax = n
+    ga = z[p + "gammas"]
+    k = ga.size
+    # row 10 on the golden grid
+    qg, sg = z[p + "q_grid"], z[p + "s_grid"]
+    for gbar, zeta in ((float(np.mean(ga)), 0.2), (1e-3, k / kmax)):
+        ze = O.prior_zeta(zeta, kmax)
+        want, _ = O.delta_curve(qg, sg, gbar, ze)
+        curve, idx = ops.activation_curve(_dev(qg[None, :]), _dev(sg[None, :]), _dev(np.array([gbar])),
+                                          _dev(np.array([zeta])), kmax)
+        got = curve.cpu().numpy()[0]
+        assert rel(got, want) < CALL_TOL
+        i = int(idx.item())
+        assert i == int(np.argmin(got))  # lowest index on ties, as best_candidate
+        assert want[i] - want.min() <= 1e-12 * max(1.0, abs(want.min()))
+    # rows 11-12 on the golden statistics
+    st = _stats_of(z, p, k)
+    K = k + 3  # padded rows: entries past kcount must be ignored
+    pad = lambda a, dt: _dev(np.pad(a, (0, K - k))[None, :], dt)  # noqa: E731
+    dstats = {key: pad(st[key], np.complex128 if key in "qrutv" else np.float64) for key in "qrustvx"}
+    gam = pad(ga, np.float64)
+    kc = _dev(np.array([k]), np.int32)
+    for zeta in (0.2, k / kmax, 1e-6):
+        class _S:  # minimal EstimationState view for the oracle
+            pass
+        sv = _S()
+        sv.gamma, sv.z, sv.zeta, sv.k_max = ga, np.ones(k, bool), zeta, kmax
+        want = O.deactivation_margins(sv, st)
+        marg, idx = ops.deactivation_margins(dstats["q"], dstats["s"], gam, kc, _dev(np.array([zeta])), kmax)
+        got = marg.cpu().numpy()[0, :k]
+        fin = np.isfinite(want)
+        assert np.array_equal(np.isfinite(got), fin) and np.array_equal(got[~fin], want[~fin])
+        if fin.any():
+            assert rel(got[fin], want[fin]) < CALL_TOL
+        assert int(idx.item()) == int(np.argmin(want))
+    g, d = ops.gradient_hessian(dstats, gam, kc, n)
+    assert rel(g.cpu().numpy()[0, :2 * k], O.gradient(ga, st)) < CALL_TOL
+    assert rel(d.cpu().numpy()[0, :2 * k], O.diag_hessian(ga, st, n)) < CALL_TOL
