@@ -271,10 +271,18 @@ def run_ours(args):
     alg_bytes = B * (32 * n + 24 * L)
     achieved = alg_bytes / (grid_ms / 1000.0) / 1e9
     peaks, peak_kind = measured_peaks()
-    roof = {"bound": "hbm", "kernel": "grid_kernel (activation grid, SURVEY 8(a) row 9)",
+    flops = B * 15 * L * int(np.log2(L))  # 3 complex FFTs of L at 5 L log2 L
+    fp64_tf = flops / (grid_ms / 1000.0) / 1e12
+    # FP64 DFMA peak measured on this pool's B200 (tools/micro/fp64_peak.cu, profiles/r1_fp64_peak.txt)
+    fp64_peak = 34.09
+    attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg_bytes, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
+    roof = {"bound": "hbm", "kernel": "grid_fused_kernel (activation grid, SURVEY 8(a) row 9)",
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
             "traffic": None, "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
-            "launch_ms": grid_ms, "flops_per_launch": B * 15 * L * int(np.log2(L))}
+            "launch_ms": grid_ms, "flops_per_launch": flops,
+            "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "peak_source": "measured DFMA loop",
+                     "frac": fp64_tf / fp64_peak, "attainable_tflops": attainable,
+                     "frac_of_min_roofline": fp64_tf / attainable}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
