@@ -263,17 +263,21 @@ class Bundle:
     _SuperfastBundle, model_core.py:256-313."""
 
     def __init__(self, y, thetas, gammas, beta):
-        n = y.size
+        # y: (N,) for one snapshot or (G, N) for G snapshots (model_core.py:266-270)
+        y2 = np.atleast_2d(y)
+        n = y2.shape[1]
         self.y = y
+        self.g = y2.shape[0]
         self.thetas = np.asarray(thetas, dtype=np.float64)
         self.gammas = np.asarray(gammas, dtype=np.float64)
         self.beta = beta
         self.c = cov_column(self.thetas, self.gammas, beta, n)
         self.rho, self.delta = levinson(self.c)
-        self.w = gs_apply(self.rho, self.delta[-1], y)
-        quad = float(np.sum(np.conj(y) * self.w).real)
+        w2 = np.stack([gs_apply(self.rho, self.delta[-1], yg) for yg in y2])
+        self.w = w2 if y.ndim == 2 else w2[0]
+        quad = float(np.sum(np.conj(y2) * w2).real)
         self.logdet = float(np.sum(np.log(self.delta)))
-        self.data_term = self.logdet + quad
+        self.data_term = self.g * self.logdet + quad
         self._om = None
         self._stats = None
         self._grid = {}
@@ -284,25 +288,34 @@ class Bundle:
         return self._om
 
     def stats(self):
-        """model_core.py:281-301 (direct sums)."""
+        """model_core.py:281-301 (direct sums); q, r, u are (G, K) for a
+        (G, N) observation, (K,) for a single snapshot."""
         if self._stats is None:
-            n = self.y.size
+            w2 = np.atleast_2d(self.w)
+            n = w2.shape[1]
             d = 2.0 * np.pi * np.arange(n)
-            stack = np.stack((self.w, d * self.w, d ** 2 * self.w), axis=1)
-            adj = steer_adjoint(self.thetas, stack)
+            qs, rs, us = [], [], []
+            for wg in w2:
+                stack = np.stack((wg, d * wg, d ** 2 * wg), axis=1)
+                adj = steer_adjoint(self.thetas, stack)
+                qs.append(adj[:, 0].copy())
+                rs.append(adj[:, 1].copy())
+                us.append(adj[:, 2].copy())
             om = self.omegas()
             omstack = np.stack([om["s"], om["t"], om["v"], om["x"]], axis=1)
             stvx = fourier_sum_two_sided(self.thetas, omstack)
-            self._stats = dict(q=adj[:, 0].copy(), r=adj[:, 1].copy(), u=adj[:, 2].copy(),
+            one = np.ndim(self.w) == 1
+            pick = (lambda a: a[0]) if one else np.stack
+            self._stats = dict(q=pick(qs), r=pick(rs), u=pick(us),
                                s=stvx[:, 0].real.copy(), t=stvx[:, 1].copy(),
                                v=stvx[:, 2].copy(), x=stvx[:, 3].real.copy())
         return self._stats
 
     def grid(self, length):
-        """model_core.py:303-313."""
+        """model_core.py:303-313; q_grid is (G, L) for a (G, N) observation."""
         if length not in self._grid:
-            n = self.y.size
-            q_grid = np.fft.fft(self.w, n=length)
+            n = self.rho.size
+            q_grid = np.fft.fft(self.w, n=length, axis=-1)
             buf = np.zeros(length, dtype=np.complex128)
             buf[np.arange(-(n - 1), n) % length] = self.omegas()["s"]
             s_grid = (length * np.fft.ifft(buf)).real
@@ -321,11 +334,13 @@ def gamma_bar(active_gamma, energy, m):
 
 
 def delta_curve(q_grid, s_grid, gbar, zeta_eff):
-    """smlr.py:62-70 (G = 1)."""
-    sum_q2 = np.abs(q_grid) ** 2
+    """smlr.py:62-70; q_grid (L,) or (G, L).  Returns (delta, mean_g |q|^2)."""
+    q2 = np.atleast_2d(q_grid)
+    g = q2.shape[0]
+    sum_q2 = np.sum(np.abs(q2) ** 2, axis=0)
     log_ratio = np.log((1.0 - zeta_eff) / zeta_eff)
-    delta = np.log1p(gbar * s_grid) + log_ratio - sum_q2 / (1.0 / gbar + s_grid)
-    return delta, sum_q2
+    delta = g * np.log1p(gbar * s_grid) + log_ratio - sum_q2 / (1.0 / gbar + s_grid)
+    return delta, sum_q2 / g
 
 
 def gamma_estimate(kappa, s):
@@ -341,24 +356,28 @@ def snr_criterion(kappa, s, gbar, zeta_eff, tau):
 
 # --- Row 12: gradient / diag Hessian -------------------------------------------------
 def gradient(gammas, st):
-    """model_core.py:497-505 (G = 1)."""
-    cross = np.conj(st["q"]) * st["r"]
-    d_theta = 2.0 * gammas * (st["t"] - cross).imag
-    d_gamma = st["s"] - np.abs(st["q"]) ** 2
+    """model_core.py:497-505 (sums over snapshots; q, r may be (G, K))."""
+    q, r = np.atleast_2d(st["q"]), np.atleast_2d(st["r"])
+    g = q.shape[0]
+    cross = np.sum(np.conj(q) * r, axis=0)
+    d_theta = 2.0 * gammas * (g * st["t"] - cross).imag
+    d_gamma = g * st["s"] - np.sum(np.abs(q) ** 2, axis=0)
     return np.concatenate((d_theta, d_gamma))
 
 
 def diag_hessian(gammas, st, n):
-    """model_core.py:508-536 (G = 1, fallback on)."""
+    """model_core.py:508-536 (fallback on; q, r, u may be (G, K))."""
     ga = gammas
-    q2 = np.abs(st["q"]) ** 2
-    r2 = np.abs(st["r"]) ** 2
-    rqc = st["r"] * np.conj(st["q"])
-    uqc = st["u"] * np.conj(st["q"])
+    q, r, u = np.atleast_2d(st["q"]), np.atleast_2d(st["r"]), np.atleast_2d(st["u"])
+    g = q.shape[0]
+    q2 = np.sum(np.abs(q) ** 2, axis=0)
+    r2 = np.sum(np.abs(r) ** 2, axis=0)
+    rqc = np.sum(r * np.conj(q), axis=0)
+    uqc = np.sum(u * np.conj(q), axis=0)
     s, t, v, x = st["s"], st["t"], st["v"], st["x"]
-    core = (x - v) + ga * (t ** 2 - x * s) + ga * (x * q2 + s * r2 - 2.0 * t * rqc) + uqc - r2
+    core = g * (x - v) + ga * g * (t ** 2 - x * s) + ga * (x * q2 + s * r2 - 2.0 * t * rqc) + uqc - r2
     d2_theta = 2.0 * ga * core.real
-    d2_gamma = 2.0 * s * q2 - s ** 2
+    d2_gamma = 2.0 * s * q2 - g * s ** 2
     d2_theta = np.where(d2_theta <= 0.0, float(50 * n) ** 2, d2_theta)
     safe = np.where(ga > 0.0, ga, 1.0 / (50.0 * n))
     d2_gamma = np.where(d2_gamma <= 0.0, safe ** -2, d2_gamma)
@@ -539,7 +558,7 @@ def try_activate(st, energy, m, q_grid, s_grid, tau):
     if not snr_criterion(kappa, float(s_grid[best]), gbar, ze, tau):
         return None
     out = st.copy()
-    slot = _activate_slot(out, best / q_grid.size, gam)
+    slot = _activate_slot(out, best / s_grid.size, gam)
     return out, slot, best
 
 
@@ -548,7 +567,7 @@ def initial_sweep(st, energy, m, n, q_grid, s_grid, tau):
     gbar = gamma_bar(st.gamma[st.z], energy, m)
     ze = prior_zeta(st.zeta, st.k_max)
     delta, q2 = delta_curve(q_grid, s_grid, gbar, ze)
-    length = q_grid.size
+    length = s_grid.size
     local_min = (delta <= np.roll(delta, 1)) & (delta <= np.roll(delta, -1))
     cands = np.flatnonzero(local_min)
     if cands.size == 0:
@@ -581,12 +600,14 @@ def initial_sweep(st, energy, m, n, q_grid, s_grid, tau):
 
 
 def deactivation_margins(st, stt):
-    """smlr.py:174-200 (G = 1)."""
+    """smlr.py:174-200 (q may be (G, K))."""
     gamma = st.gamma[st.z]
     ze = prior_zeta(st.zeta, st.k_max)
     rhs = np.log((1.0 - ze) / ze)
     denom = 1.0 - gamma * stt["s"]
-    q2 = np.abs(stt["q"]) ** 2
+    qa = np.atleast_2d(stt["q"])
+    g = qa.shape[0]
+    q2 = np.sum(np.abs(qa) ** 2, axis=0)
     out = np.empty(gamma.size)
     for i in range(gamma.size):
         if gamma[i] <= 0.0:
@@ -597,7 +618,7 @@ def deactivation_margins(st, stt):
             continue
         q2dd = q2[i] / denom[i] ** 2
         sdd = stt["s"][i] / denom[i]
-        out[i] = q2dd / (1.0 / gamma[i] + sdd) - np.log1p(gamma[i] * sdd) - rhs
+        out[i] = q2dd / (1.0 / gamma[i] + sdd) - g * np.log1p(gamma[i] * sdd) - rhs
     return out
 
 
@@ -644,7 +665,8 @@ class OracleResult:
 
 
 def estimate(y, opts: OracleOptions = None) -> OracleResult:
-    """estimator.py:117-275 for G = 1, complete data, superfast backend.
+    """estimator.py:117-275, complete data, superfast backend; y is one
+    snapshot (N,) or G snapshots (G, N) sharing the frequencies (MMV).
 
     `events` is the active-set history: ("sweep", [(slot, idx)...]),
     ("activate", slot, idx), ("deactivate", [slots]) in order."""
@@ -652,14 +674,17 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
     t_start = time.perf_counter()
     opts = opts or OracleOptions()
     _MARGINS = []
-    y = np.asarray(y, dtype=np.complex128).ravel()
-    n = m = y.size
+    y = np.asarray(y, dtype=np.complex128)
+    if y.ndim != 2:
+        y = y.ravel()
+    g = 1 if y.ndim == 1 else y.shape[0]
+    n = m = y.shape[-1]
     if m < 2:
         raise ValueError("need at least two observed samples")
     k_max = opts.k_max if opts.k_max is not None else m
     L = default_grid_size(n, opts.grid_factor)
     eng = _Engine(y, L)
-    energy = float(np.mean(np.sum(np.abs(y[None, :]) ** 2, axis=1)))
+    energy = float(np.mean(np.sum(np.abs(np.atleast_2d(y)) ** 2, axis=1)))
     floor = BETA_FLOOR_SCALE * energy / m
     beta0 = max(INITIAL_BETA_ENERGY_FRACTION * energy / m, floor)
     st = _State(k_max, beta0, INITIAL_ZETA)
@@ -711,11 +736,11 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
         if st.k_hat:
             stt = stats_of(st)
             ga = st.gamma[st.z]
-            mu = ga * stt["q"]
+            mu = ga * stt["q"]  # (K,) or (G, K)
             tr = float(st.beta * np.sum(stt["s"] * ga))
-            fitted = steer_forward(st.theta[st.z], mu, n)
-            resid = y - fitted
-            value = (tr + float(np.sum(np.abs(resid) ** 2))) / m
+            fitted = steer_forward(st.theta[st.z], mu if g == 1 else mu.T, n)
+            resid = y - fitted if g == 1 else y.T - fitted
+            value = (tr + float(np.sum(np.abs(resid) ** 2)) / g) / m
         else:
             value = energy / m
         cand.beta = max(floor, value)
@@ -773,7 +798,7 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
         previous = current
 
     if st.k_hat:
-        alpha = (st.gamma[st.z] * stats_of(st)["q"])[None, :]
+        alpha = np.atleast_2d(st.gamma[st.z] * stats_of(st)["q"])
     else:
         alpha = np.zeros((1, 0), dtype=np.complex128)
     return OracleResult(
@@ -837,3 +862,38 @@ def generate_problem(seed, cfg, b, n=None, k=None):
 def generate_batch(seed, cfg, count, n=None, k=None, start=0):
     ys = [generate_problem(seed, cfg, start + b, n=n, k=k)[0] for b in range(count)]
     return np.stack(ys)
+
+
+def generate_problem_mmv(seed, cfg, b, g, n=None, k=None):
+    """G snapshots sharing the frequencies (MMV, estimator.py:278-283):
+    y (G, N).  rng = default_rng([seed, cfg, 1000 + g, b]); frequencies as
+    generate_problem; amplitudes drawn per snapshot with the config's law;
+    one noise variance from the mean clean power and the config's SNR."""
+    _, n0, k0, sep, law, snr = CONFIGS[cfg]
+    n = n or n0
+    k = k or k0
+    rng = np.random.default_rng([seed, cfg, 1000 + g, b])
+    min_sep = sep / n
+    thetas = []
+    while len(thetas) < k:
+        cand = rng.random()
+        if not thetas or np.min(wrap_distance(cand, np.array(thetas))) > min_sep:
+            thetas.append(cand)
+    thetas = np.array(thetas)
+    alphas = np.empty((g, k), dtype=np.complex128)
+    for gi in range(g):
+        phase = np.exp(2j * np.pi * rng.random(k))
+        if law == "unit":
+            mag = np.ones(k)
+        elif law == "cn":
+            a = (rng.standard_normal(k) + 1j * rng.standard_normal(k)) / np.sqrt(2.0)
+            mag, phase = np.abs(a), np.exp(1j * np.angle(a))
+        elif law == "uniform":
+            mag = rng.uniform(0.5, 1.5, k)
+        else:
+            mag = 10.0 ** rng.uniform(-1.0, 0.0, k)
+        alphas[gi] = mag * phase
+    clean = np.stack([steer_forward(thetas, alphas[gi], n) for gi in range(g)])
+    beta = float(np.mean(np.sum(np.abs(clean) ** 2, axis=1))) / (n * 10.0 ** (snr / 10.0))
+    noise = np.sqrt(beta / 2.0) * (rng.standard_normal((g, n)) + 1j * rng.standard_normal((g, n)))
+    return clean + noise, dict(thetas=thetas, alphas=alphas, beta=beta)

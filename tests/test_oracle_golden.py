@@ -3,6 +3,8 @@ produced by the real reference (tests/golden/make_golden.py) and against the
 reference test-suite's known-answer tests (pkg/tests/test_toeplitz.py,
 pkg/tests/test_model_core.py)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -124,3 +126,42 @@ def test_kat_not_pd():
         O.levinson(np.array([1, 2], complex))
     with pytest.raises(O.OracleNotPD):
         O.levinson(np.array([-1, 0], complex))
+
+
+# ---- MMV (G > 1 snapshots), SURVEY 8(f) item 1 -------------------------------------
+def _mmv_keys():
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_mmv.npz"))
+    out = []
+    for cfg, g, count in z["cases"]:
+        out += [(int(cfg), int(g), b) for b in range(int(count))]
+    return out
+
+
+@pytest.mark.parametrize("cfg,g,b", _mmv_keys())
+def test_oracle_mmv_against_reference(cfg, g, b):
+    """The oracle's G-snapshot restatement reproduces the reference's MMV
+    trajectory and one per-call bundle (estimator.py:117-283)."""
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_mmv.npz"))
+    p = f"c{cfg}g{g}_p{b}_"
+    y = z[p + "y"]
+    assert y.shape == (g, y.shape[1])
+    r = O.estimate(y, O.OracleOptions(grid_factor=4))
+    assert r.k_hat == int(z[p + "k_hat"])
+    assert np.array_equal(np.array([STAGES.index(s) for s in r.trace_stages]), z[p + "stages"])
+    assert np.array_equal(encode_events(r.events), z[p + "events"])
+    assert np.max(np.abs(r.objective_trace - z[p + "trace"]) / np.abs(z[p + "trace"])) < 1e-9
+    assert np.max(O.wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
+    assert r.alpha_hat.shape == z[p + "alpha_hat"].shape
+    assert rel(r.alpha_hat, z[p + "alpha_hat"]) < AMP_TOL
+    assert abs(r.beta_hat - float(z[p + "beta_hat"])) / float(z[p + "beta_hat"]) < AMP_TOL
+    q = "call_"
+    bd = O.Bundle(y, z[p + q + "thetas"], z[p + q + "gammas"], float(z[p + q + "beta"]))
+    assert rel(bd.w, z[p + q + "w"]) < CALL_TOL
+    assert abs(bd.data_term - float(z[p + q + "data_term"])) <= CALL_TOL * abs(float(z[p + q + "data_term"]))
+    st = bd.stats()
+    for key in "qrustvx":
+        assert rel(st[key], z[p + q + "st_" + key]) < CALL_TOL, key
+    L = O.default_grid_size(y.shape[1], 4)
+    qg, sg = bd.grid(L)
+    assert rel(qg, z[p + q + "q_grid"]) < CALL_TOL
+    assert rel(sg, z[p + q + "s_grid"]) < CALL_TOL
