@@ -28,6 +28,7 @@
  *   slse_gradient_hessian  <- model_core.gradient :497-505, diag_hessian :508-536
  *   slse_estimate_batch    <- estimator.estimate :117-275 (complete data, G = 1,
  *                             backend "superfast"), one problem per batch row
+ *   slse_estimate_batch_mmv <- estimator.estimate_mmv :278-283 (G >= 1 snapshots)
  */
 #ifndef SUPERLSE_B200_H
 #define SUPERLSE_B200_H
@@ -156,6 +157,15 @@ size_t slse_estimate_workspace_bytes(int N, int B, const slse_options* opts);
 int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
                         const slse_outputs* out, void* workspace, size_t workspace_bytes,
                         void* stream);
+
+/* MMV (G >= 1 snapshots sharing the frequencies; estimator.estimate_mmv
+ * :278-283, all data sums over snapshots): y is [B, G, N] complex, and the
+ * outputs' alpha is [B, G, kmax] (row g = snapshot g); every other output as
+ * slse_estimate_batch.  G = 1 is slse_estimate_batch. */
+size_t slse_estimate_workspace_bytes_mmv(int N, int G, int B, const slse_options* opts);
+int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_options* opts,
+                            const slse_outputs* out, void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 #ifdef __cplusplus
 }

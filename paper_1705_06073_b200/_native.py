@@ -82,6 +82,9 @@ def load():
         "slse_gradient_hessian": ([vp, vp, vp, vp, vp, vp, vp, vp, vp, i, i, i, vp, vp, vp], i),
         "slse_estimate_workspace_bytes": ([i, i, ctypes.POINTER(SlseOptions)], sz),
         "slse_estimate_batch": ([vp, i, i, ctypes.POINTER(SlseOptions), ctypes.POINTER(SlseOutputs), vp, sz, vp], i),
+        "slse_estimate_workspace_bytes_mmv": ([i, i, i, ctypes.POINTER(SlseOptions)], sz),
+        "slse_estimate_batch_mmv": ([vp, i, i, i, ctypes.POINTER(SlseOptions), ctypes.POINTER(SlseOutputs), vp, sz,
+                                     vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -131,7 +131,7 @@ int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem) {
   return 0;
 }
 
-int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
+int grid_size_for_solver(int n, int G, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
   P.dnc = n >= dnc_min_n() ? 1 : 0;
   P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
@@ -142,7 +142,7 @@ int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, 
     int ctas = (B + W - 1) / W;
     if (ctas > sm_count()) ctas = sm_count();
     if (ctas < 1) ctas = 1;
-    Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0, P.dnc != 0);
+    Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0, P.dnc != 0, G);
     *slab_out = lay.total;
     if (plan_out) *plan_out = plan;
     return ctas * W;
@@ -162,7 +162,7 @@ int grid_size_for_solver(int n, int B, const slse_options& o, size_t* slab_out, 
   int g = sm_count() * occ;
   if (g > B) g = B;
   if (g < 1) g = 1;
-  Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0, P.dnc != 0);
+  Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, plan.rec_in_smem != 0, P.dnc != 0, G);
   *slab_out = lay.total;
   if (plan_out) *plan_out = plan;
   return g;
@@ -531,27 +531,38 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   return e == cudaSuccess ? 0 : fail("grid_kernel", e);
 }
 
-size_t slse_estimate_workspace_bytes(int N, int B, const slse_options* opts) {
+size_t slse_estimate_workspace_bytes_mmv(int N, int G, int B, const slse_options* opts) {
   slse_options o;
   if (opts) o = *opts; else slse_default_options(&o);
+  if (G < 1) return 0;
   size_t slab = 0;
-  int g = grid_size_for_solver(N, B, o, &slab, nullptr);
+  int g = grid_size_for_solver(N, G, B, o, &slab, nullptr);
   if (g < 0) return 0;
   return 256 + (size_t)g * slab;
 }
 
+size_t slse_estimate_workspace_bytes(int N, int B, const slse_options* opts) {
+  return slse_estimate_workspace_bytes_mmv(N, 1, B, opts);
+}
+
 int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts, const slse_outputs* out,
                         void* workspace, size_t workspace_bytes, void* stream) {
+  return slse_estimate_batch_mmv(y, N, 1, B, opts, out, workspace, workspace_bytes, stream);
+}
+
+int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_options* opts, const slse_outputs* out,
+                            void* workspace, size_t workspace_bytes, void* stream) {
   slse_options o;
   if (opts) o = *opts; else slse_default_options(&o);
   if (N < 2) return fail_arg("slse_estimate_batch: need at least two observed samples");
+  if (G < 1) return fail_arg("slse_estimate_batch_mmv: need at least one snapshot");
   if (o.lbfgs_memory < 1 || o.lbfgs_memory > 16) return fail_arg("slse_estimate_batch: lbfgs_memory must be 1..16");
   if (B < 0 || out == nullptr) return fail_arg("slse_estimate_batch: bad arguments");
   if (B == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   size_t slab = 0;
   SmemPlan plan;
-  int g = grid_size_for_solver(N, B, o, &slab, &plan);
+  int g = grid_size_for_solver(N, G, B, o, &slab, &plan);
   if (g < 0) return g;
   const size_t need = 256 + (size_t)g * slab;
   if (workspace_bytes < need) {
@@ -559,6 +570,7 @@ int slse_estimate_batch(const double* y, int N, int B, const slse_options* opts,
     return -2;
   }
   SolveParams P = make_params(N, o);
+  P.g = G;
   P.dnc = N >= dnc_min_n() ? 1 : 0;
   P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
   P.grid_fused = getenv("SLSE_GRID_UNFUSED") ? 0 : 1;

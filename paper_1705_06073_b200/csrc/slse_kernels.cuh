@@ -105,7 +105,7 @@ SLSE_D ProbOut prob_out(const slse_outputs& out, const SolveParams& P, int p) {
   o.zeta = out.zeta + p;
   o.theta = out.theta + p * K;
   o.gamma = out.gamma + p * K;
-  o.alpha = (cplx*)out.alpha + p * K;
+  o.alpha = (cplx*)out.alpha + (size_t)p * K * P.g;  // [B, G, kmax]
   o.slot = out.slot + p * K;
   o.trace = out.trace + (size_t)p * P.tcap;
   o.stage = out.stage + (size_t)p * P.tcap;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve
   f.smem = region;
   f.smem_cap = fft_cap;
   char* slab = ws + (size_t)blockIdx.x * slab_bytes;
-  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0, P.dnc != 0);
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0, P.dnc != 0, P.g);
   __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) s_prob = atomicAdd(queue, 1);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve
     __syncthreads();
     if (p >= B) break;
     const ProbOut o = prob_out(out, P, p);
-    Solver S(b, P, cf, ys + (size_t)p * P.n, o, slab, lay, rec_smem ? region : nullptr, f);
+    Solver S(b, P, cf, ys + (size_t)p * P.n * P.g, o, slab, lay, rec_smem ? region : nullptr, f);
     S.run();
     b.bank = S.b.bank;
     __syncthreads();
@@ -190,14 +190,14 @@ __global__ void __launch_bounds__(32 * W, 16 / W) solve_kernel_warps(SolveParams
   f.smem_cap = fft_cap;
   cplx* region = f.smem;
   char* slab = ws + ((size_t)blockIdx.x * W + warp) * slab_bytes;
-  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0, P.dnc != 0);
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, rec_smem != 0, P.dnc != 0, P.g);
   for (;;) {
     int p = 0;
     if (lane == 0) p = atomicAdd(queue, 1);
     p = __shfl_sync(0xffffffffu, p, 0);
     if (p >= B) break;
     const ProbOut o = prob_out(out, P, p);
-    Solver S(b, P, cf, ys + (size_t)p * P.n, o, slab, lay, rec_smem ? region : nullptr, f);
+    Solver S(b, P, cf, ys + (size_t)p * P.n * P.g, o, slab, lay, rec_smem ? region : nullptr, f);
     S.run();
     b.bank = S.b.bank;
     __syncwarp();
@@ -381,7 +381,8 @@ static __global__ void grad_kernel(const cplx* q, const cplx* r, const cplx* u, 
   if (i >= kcount[p]) return;
   const int k = kcount[p];
   double gth, gga, dth, dga;
-  grad_diag_comp(gamma[idx], q[idx], r[idx], u[idx], s[idx], t[idx], v[idx], x[idx], n, &gth, &gga, &dth, &dga);
+  grad_diag_comp(gamma[idx], q + idx, r + idx, u + idx, 0, 1, s[idx], t[idx], v[idx], x[idx], n, &gth, &gga, &dth,
+                 &dga);
   double* gp = g + (size_t)p * 2 * kstride;
   double* dp = d + (size_t)p * 2 * kstride;
   gp[i] = gth;

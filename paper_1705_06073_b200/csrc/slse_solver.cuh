@@ -63,6 +63,7 @@ __device__ unsigned long long slse_prof_cycles[8];
 
 struct SolveParams {
   int n, L, kmax;
+  int g;  // snapshots sharing the frequencies (MMV, estimator.py:278-283); 1 = single snapshot
   int max_outer, inner_max, sweep_iters, lbfgs_mem;
   int tcap, ecap;
   double tau, conv_tol_scale, dec_tol_scale;
@@ -76,6 +77,7 @@ struct SolveParams {
 SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   SolveParams P;
   P.n = n;
+  P.g = 1;
   int target = 2 * n > o.grid_factor * n ? 2 * n : o.grid_factor * n;
   int L = 1;
   while (L < target) L <<= 1;  // model_core.py:224-227
@@ -109,13 +111,15 @@ struct Layout {
 
 SLSE_HD size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion_in_smem, bool dnc = false) {
+SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion_in_smem, bool dnc = false,
+                           int g = 1) {
   Layout l;
   size_t o = 0;
   const size_t C = 16, D = 8, I = 4;
   const int nf = 1 << ilog2(2 * n);
   const size_t K = (size_t)kmax, K2 = 2 * (size_t)kmax;
-  l.yhat = o; o = al(o + C * nf);
+  const size_t G = (size_t)g;
+  l.yhat = o; o = al(o + C * nf * G);
   l.c = o; o = al(o + C * n);
   l.dT = l.darena = 0;
   if (dnc) {
@@ -129,7 +133,7 @@ SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion
     l.bg = o; o = al(o + C * n);
     l.a = o; o = al(o + C * n);
   }
-  for (int i = 0; i < 2; ++i) { l.rho[i] = o; o = al(o + C * n); l.w[i] = o; o = al(o + C * n); }
+  for (int i = 0; i < 2; ++i) { l.rho[i] = o; o = al(o + C * n); l.w[i] = o; o = al(o + C * n * G); }
   l.P = o; o = al(o + C * nf);
   l.U = o; o = al(o + C * nf);
   l.V = o; o = al(o + C * nf);
@@ -137,15 +141,15 @@ SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion
   l.G1 = o; o = al(o + C * L);
   l.G2 = o; o = al(o + C * L);
   for (int i = 0; i < 2; ++i) {
-    l.st_q[i] = o; o = al(o + C * K);
-    l.st_r[i] = o; o = al(o + C * K);
-    l.st_u[i] = o; o = al(o + C * K);
+    l.st_q[i] = o; o = al(o + C * K * G);  // row g at g * kmax
+    l.st_r[i] = o; o = al(o + C * K * G);
+    l.st_u[i] = o; o = al(o + C * K * G);
     l.st_t[i] = o; o = al(o + C * K);
     l.st_v[i] = o; o = al(o + C * K);
     l.st_s[i] = o; o = al(o + D * K);
     l.st_x[i] = o; o = al(o + D * K);
   }
-  l.mu = o; o = al(o + C * K);
+  l.mu = o; o = al(o + C * K * G);
   l.dtmp = o; o = al(o + D * n);
   l.dl = o; o = al(o + D * L);
   l.q2 = o; o = al(o + D * L);
@@ -203,35 +207,52 @@ SLSE_D double prior_zeta(double zeta, int kmax) {  // model_core.py:230-234
 }
 
 // Row 11: one deactivation margin (smlr.py:174-200); rhs = ln((1-ze)/ze).
-SLSE_HD double deact_margin(double ga, double s, double qq, double rhs) {
+// qq = sum over snapshots of |q_g|^2; G snapshots (the log1p term carries G).
+SLSE_HD double deact_margin(double ga, double s, double qq, double rhs, int G = 1) {
   const double den = 1.0 - ga * s;
   if (ga <= 0.0) return rhs > 0.0 ? -INFINITY : 0.0;
   if (den <= 0.0) return INFINITY;
   const double q2dd = qq / (den * den);
   const double sdd = s / den;
-  return (q2dd / (1.0 / ga + sdd) - log1p(ga * sdd)) - rhs;
+  const double lg = log1p(ga * sdd);
+  return (q2dd / (1.0 / ga + sdd) - (G == 1 ? lg : (double)G * lg)) - rhs;
 }
 
 // Row 12: gradient and diagonal Hessian of one component
-// (model_core.py:497-536).
-SLSE_HD void grad_diag_comp(double ga, cplx q, cplx r, cplx u, double s, cplx t, cplx v, double x, int n,
-                            double* gth, double* gga, double* dth, double* dga) {
-  const cplx cross = cmul(conjg(q), r);
-  *gth = 2.0 * ga * (t.im - cross.im);
-  *gga = s - cabs2(q);
-  const double qq = cabs2(q), rr = cabs2(r);
-  const cplx rqc = cmul(r, conjg(q));
-  const cplx uqc = cmul(u, conjg(q));
+// (model_core.py:497-536).  q, r, u point at snapshot 0 of this component,
+// rows `stride` apart; G snapshots (sums over g, G factors as the reference).
+SLSE_HD void grad_diag_comp(double ga, const cplx* q, const cplx* r, const cplx* u, size_t stride, int G, double s,
+                            cplx t, cplx v, double x, int n, double* gth, double* gga, double* dth, double* dga) {
+  cplx cross = cmul(conjg(q[0]), r[0]);
+  double qq = cabs2(q[0]), rr = cabs2(r[0]);
+  cplx rqc = cmul(r[0], conjg(q[0]));
+  cplx uqc = cmul(u[0], conjg(q[0]));
+  for (int g = 1; g < G; ++g) {
+    const cplx qg = q[g * stride], rg = r[g * stride], ug = u[g * stride];
+    cross = cadd(cross, cmul(conjg(qg), rg));
+    qq += cabs2(qg);
+    rr += cabs2(rg);
+    rqc = cadd(rqc, cmul(rg, conjg(qg)));
+    uqc = cadd(uqc, cmul(ug, conjg(qg)));
+  }
+  const double Gd = (double)G;
+  *gth = 2.0 * ga * ((G == 1 ? t.im : Gd * t.im) - cross.im);
+  *gga = (G == 1 ? s : Gd * s) - qq;
+  // core = G (x - v) + ga G (t^2 - x s) + ga (x q2 + s r2 - 2 t rqc) + uqc - r2
   const cplx t2 = cmul(t, t);
-  const cplx c1 = mk(x - v.re, -v.im);
-  const cplx c2 = cscale(mk(t2.re - x * s, t2.im), ga);
+  cplx c1 = mk(x - v.re, -v.im);
+  cplx c2 = cscale(mk(t2.re - x * s, t2.im), ga);
+  if (G != 1) {
+    c1 = cscale(c1, Gd);
+    c2 = cscale(mk(t2.re - x * s, t2.im), ga * Gd);
+  }
   const cplx trq = cmul(mk(2.0 * t.re, 2.0 * t.im), rqc);
   const cplx c3 = cscale(mk(x * qq + s * rr - trq.re, -trq.im), ga);
   cplx core = cadd(cadd(c1, c2), c3);
   core = cadd(core, uqc);
   core.re -= rr;
   double d2t = 2.0 * ga * core.re;
-  double d2g = 2.0 * s * qq - s * s;
+  double d2g = 2.0 * s * qq - (G == 1 ? s * s : Gd * (s * s));
   if (d2t <= 0.0) d2t = (double)(50 * n) * (double)(50 * n);
   if (d2g <= 0.0) {
     const double sg_ = ga > 0.0 ? ga : 1.0 / (50.0 * (double)n);
@@ -301,6 +322,7 @@ struct Solver {
   int cur_valid;
   // scalar state (identical in every thread)
   int n, L, kmax, k;
+  int G;  // snapshots (P.g): y, yhat and w hold G rows of n / nf; q, r, u, mu G rows of kmax
   double beta, zeta, energy, floor_beta;
   int status;
   int ntrace, nevents, flags;
@@ -316,7 +338,7 @@ struct Solver {
   SLSE_D Solver(Blk& blk, const SolveParams& p, const CfTable* cf_, const cplx* y_, ProbOut out,
                 char* slab, const Layout& lay, cplx* rec_smem, const FftCtx& fc)
       : b(blk), f(fc), P(p), cf(cf_), y(y_), o(out) {
-    n = p.n; L = p.L; kmax = p.kmax;
+    n = p.n; L = p.L; kmax = p.kmax; G = p.g;
     yhat = (cplx*)(slab + lay.yhat);
     c = (cplx*)(slab + lay.c);
     if (rec_smem) {
@@ -457,9 +479,13 @@ struct Solver {
     B.delta_last = F.delta_last;
     B.logdet = F.logdet;
     SLSE_PROF_T0(t2);
+    const int nf = 1 << ilog2(2 * n);
     double quad = gs_apply_any(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b);
+    for (int g = 1; g < G; ++g)  // MMV: one C^{-1} y_g per snapshot (model_core.py:267-269)
+      quad += gs_apply_any(B.rho, n, F.delta_last, y + (size_t)g * n, yhat + (size_t)g * nf, PP, U, V,
+                           B.w + (size_t)g * n, f, b);
     SLSE_PROF_ADD(2, t2);
-    B.data_term = F.logdet + quad;
+    B.data_term = (G == 1 ? F.logdet : (double)G * F.logdet) + quad;
     B.stats_valid = 0;
     return kOk;
   }
@@ -474,8 +500,9 @@ struct Solver {
     const double inv = 1.0 / be;
     double qp = 0.0;
     SLSE_CTRL_LOOP
-    for (int i = tid_; i < n; i += nt_) {
-      B.rho[i] = mk(i == n - 1 ? 1.0 : 0.0, 0.0);
+    for (int i = tid_; i < n; i += nt_) B.rho[i] = mk(i == n - 1 ? 1.0 : 0.0, 0.0);
+    SLSE_CTRL_LOOP
+    for (int i = tid_; i < n * G; i += nt_) {
       const cplx wi = cscale(y[i], inv);
       B.w[i] = wi;
       qp += y[i].re * wi.re + y[i].im * wi.im;
@@ -483,7 +510,7 @@ struct Solver {
     const double quad = b.sum(qp);
     B.delta_last = be;
     B.logdet = (double)n * log(be);
-    B.data_term = B.logdet + quad;
+    B.data_term = (G == 1 ? B.logdet : (double)G * B.logdet) + quad;
     B.stats_valid = 0;
     return kOk;
   }
@@ -506,12 +533,16 @@ struct Solver {
 
   SLSE_NIM void stats_impl(Bundle& B, const double* th, int kk) {
     SLSE_PROF_T0(t0);
+    for (int g = 0; g < G; ++g) {  // s, t, v, x do not depend on g (recomputed identically)
+      const cplx* wg = B.w + (size_t)g * n;
+      cplx *qg = B.q + (size_t)g * kmax, *rg = B.r + (size_t)g * kmax, *ug = B.u + (size_t)g * kmax;
 #ifndef SLSE_HOST_EMU
-    if (b.nt == 32 && n <= 512)
-      component_stats_warp(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b.tid);
-    else
+      if (b.nt == 32 && n <= 512)
+        component_stats_warp(th, kk, B.rho, wg, n, B.delta_last, cf, qg, rg, ug, B.s, B.t, B.v, B.x, b.tid);
+      else
 #endif
-      component_stats(th, kk, B.rho, B.w, n, B.delta_last, cf, B.q, B.r, B.u, B.s, B.t, B.v, B.x, b);
+        component_stats(th, kk, B.rho, wg, n, B.delta_last, cf, qg, rg, ug, B.s, B.t, B.v, B.x, b);
+    }
     SLSE_PROF_ADD(3, t0);
     B.stats_valid = 1;
   }
@@ -571,17 +602,19 @@ struct Solver {
     Bundle& B = bun[cur];
     const double lr = log((1.0 - ze) / ze);
     SLSE_PROF_T0(t0);
-    if (P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) {
+    if (G == 1 && P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) {
       SLSE_PROF_ADD(4, t0);
       return;
     }
-    grid_eval(B.rho, B.w, n, B.delta_last, L, G0, G1, G2, sg, f, b);
-    SLSE_CTRL_LOOP
-    for (int l = tid_; l < L; l += nt_) {
-      const double qq = cabs2(G0[l]);
-      q2[l] = qq;
-      dl[l] = gain(qq, sg[l], gb, lr);
+    // q2 = sum_g |q^G_g|^2, gain with the G log1p term (smlr.py:62-70)
+    for (int g = 0; g < G; ++g) {
+      grid_eval(B.rho, B.w + (size_t)g * n, n, B.delta_last, L, G0, G1, G2, sg, f, b);
+      SLSE_CTRL_LOOP
+      for (int l = tid_; l < L; l += nt_) q2[l] = (g == 0 ? 0.0 : q2[l]) + cabs2(G0[l]);
+      b.sync();
     }
+    SLSE_CTRL_LOOP
+    for (int l = tid_; l < L; l += nt_) dl[l] = gain_g(q2[l], sg[l], gb, lr, G);
     b.sync();
   }
 
@@ -611,7 +644,7 @@ struct Solver {
     b.argmin(best, bi);
     if (bi < 0) return 0;
     const double s = sg[bi];
-    const double kappa = q2[bi] / s;
+    const double kappa = (G == 1 ? q2[bi] : q2[bi] / (double)G) / s;
     const double gam = gamma_estimate(kappa, s);
     if (best >= -kEpsObjective || gam <= 0.0) return 0;
     if (!snr_ok(kappa, s, gb, ze, P.tau)) return 0;
@@ -694,7 +727,7 @@ struct Solver {
         if (kk >= kmax) break;
         const int l = csort[i];
         const double s = sg[l];
-        const double kappa = q2[l] / s;
+        const double kappa = (G == 1 ? q2[l] : q2[l] / (double)G) / s;
         const double gnew_ = gamma_estimate(kappa, s);
         if (gnew_ <= 0.0) continue;
         const double tau_eff = (kk == 0) ? P.tau : 0.0;
@@ -743,7 +776,9 @@ struct Solver {
       int wi = -1;
       SLSE_CTRL_LOOP
       for (int i = tid_; i < k; i += nt_) {
-        const double mgn = deact_margin(act_gamma[i], B.s[i], cabs2(B.q[i]), rhs);
+        double qq = cabs2(B.q[i]);
+        for (int g = 1; g < G; ++g) qq += cabs2(B.q[(size_t)g * kmax + i]);
+        const double mgn = deact_margin(act_gamma[i], B.s[i], qq, rhs, G);
         if (Blk::better(mgn, i, wv, wi)) { wv = mgn; wi = i; }
       }
       b.argmin(wv, wi);
@@ -773,10 +808,9 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) {
-      const cplx q = B.q[i], r = B.r[i], t = B.t[i];
-      const cplx cross = cmul(conjg(q), r);
-      g[i] = 2.0 * ga[i] * (t.im - cross.im);
-      g[k + i] = B.s[i] - cabs2(q);
+      double dth, dga;
+      grad_diag_comp(ga[i], B.q + i, B.r + i, B.u + i, (size_t)kmax, G, B.s[i], B.t[i], B.v[i], B.x[i], n, &g[i],
+                     &g[k + i], &dth, &dga);
     }
   }
 
@@ -785,7 +819,8 @@ struct Solver {
     SLSE_CTRL_LOOP
     for (int i = tid_; i < k; i += nt_) {
       double gth, gga;
-      grad_diag_comp(ga_[i], B.q[i], B.r[i], B.u[i], B.s[i], B.t[i], B.v[i], B.x[i], n, &gth, &gga, &d[i], &d[k + i]);
+      grad_diag_comp(ga_[i], B.q + i, B.r + i, B.u + i, (size_t)kmax, G, B.s[i], B.t[i], B.v[i], B.x[i], n, &gth,
+                     &gga, &d[i], &d[k + i]);
     }
   }
 
@@ -942,10 +977,11 @@ struct Solver {
     t_mark = t_start;
     // energy, floor, beta0 (model_core.py:125-130; estimator.py:135-137)
     double part = 0.0;
-    for (int i = b.tid; i < n; i += b.nt) {
+    for (int i = b.tid; i < n * G; i += b.nt) {
       part += cabs2(y[i]);
     }
     energy = b.sum(part);
+    if (G != 1) energy /= (double)G;  // mean per-snapshot energy (model_core.py:125-127)
     floor_beta = kBetaFloorScale * energy / (double)n;
     const double b0 = kInitialBetaFrac * energy / (double)n;
     beta = b0 > floor_beta ? b0 : floor_beta;
@@ -953,8 +989,12 @@ struct Solver {
     for (int i = b.tid; i < kmax; i += b.nt) { z[i] = 0; theta[i] = 0.0; gamma[i] = 0.0; }
     k = 0;
     // cached spectrum of y for every GS apply
-    fft(yhat, 1 << ilog2(2 * n), -1.0, [=](int i) { return i < n ? y[i] : mk(0.0, 0.0); },
-        [=](int i, cplx v) { yhat[i] = v; }, f, b);
+    for (int g = 0; g < G; ++g) {
+      const cplx* yg = y + (size_t)g * n;
+      cplx* yh = yhat + ((size_t)g << ilog2(2 * n));
+      fft(yh, 1 << ilog2(2 * n), -1.0, [=](int i) { return i < n ? yg[i] : mk(0.0, 0.0); },
+          [=](int i, cplx v) { yh[i] = v; }, f, b);
+    }
     status = ensure_cur();
     if (status != kOk) { finish(0, 0); return; }
     record(kStInit);
@@ -1007,7 +1047,7 @@ struct Solver {
         stats(B, act_theta, k);
         double tr_part = 0.0;
         for (int i = b.tid; i < k; i += b.nt) {
-          mu[i] = cscale(B.q[i], act_gamma[i]);
+          for (int g = 0; g < G; ++g) mu[(size_t)g * kmax + i] = cscale(B.q[(size_t)g * kmax + i], act_gamma[i]);
           tr_part += B.s[i] * act_gamma[i];
         }
         const double tr = beta * b.sum(tr_part);
@@ -1087,19 +1127,24 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     double* mre = marg;  // scratch (length >= k)
     double* mim = dtmp;  // scratch (length n >= k), free outside build()
-    SLSE_CTRL_LOOP
-    for (int i = tid_; i < k; i += nt_) { mre[i] = mu[i].re; mim[i] = mu[i].im; }
-    b.sync();
-#ifndef SLSE_HOST_EMU
-    if (b.nt == 32 && n <= 512) steer_forward_warp(c, n, act_theta, mre, mim, k, 0.0, false, b.tid);
-    else
-#endif
-      steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
     double part = 0.0;
-    SLSE_CTRL_LOOP
-    for (int i = tid_; i < n; i += nt_) part += cabs2(csub(y[i], c[i]));
+    for (int g = 0; g < G; ++g) {  // sum_g ||y_g - Psi mu_g||^2 (estimator.py:86-88)
+      const cplx* mg = mu + (size_t)g * kmax;
+      SLSE_CTRL_LOOP
+      for (int i = tid_; i < k; i += nt_) { mre[i] = mg[i].re; mim[i] = mg[i].im; }
+      b.sync();
+#ifndef SLSE_HOST_EMU
+      if (b.nt == 32 && n <= 512) steer_forward_warp(c, n, act_theta, mre, mim, k, 0.0, false, b.tid);
+      else
+#endif
+        steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
+      const cplx* yg = y + (size_t)g * n;
+      SLSE_CTRL_LOOP
+      for (int i = tid_; i < n; i += nt_) part += cabs2(csub(yg[i], c[i]));
+      b.sync();
+    }
     const double resid = b.sum(part);
-    return (tr + resid) / (double)n;
+    return (tr + (G == 1 ? resid : resid / (double)G)) / (double)n;
   }
 
   SLSE_NIM void finish(int iterations, int converged) {
@@ -1111,7 +1156,8 @@ struct Solver {
         stats(bun[cur], act_theta, k);
         SLSE_CTRL_LOOP
         for (int i = tid_; i < k; i += nt_) {
-          o.alpha[i] = cscale(bun[cur].q[i], act_gamma[i]);
+          for (int g = 0; g < G; ++g)  // alpha_hat (G, k): gamma * q_g (model_core.py:539-547)
+            o.alpha[(size_t)g * kmax + i] = cscale(bun[cur].q[(size_t)g * kmax + i], act_gamma[i]);
           o.theta[i] = act_theta[i];
           o.gamma[i] = act_gamma[i];
           o.slot[i] = act_slot[i];

@@ -331,4 +331,10 @@ SLSE_D double gain(double q2, double s, double gb, double log_ratio) {
   return (log1p(gb * s) + log_ratio) - q2 / (1.0 / gb + s);
 }
 
+// G snapshots: q2 = sum_g |q^G_g|^2 and the log1p term carries G (smlr.py:66-69)
+SLSE_D double gain_g(double q2, double s, double gb, double log_ratio, int G) {
+  const double lg = log1p(gb * s);
+  return ((G == 1 ? lg : (double)G * lg) + log_ratio) - q2 / (1.0 / gb + s);
+}
+
 }  // namespace slse

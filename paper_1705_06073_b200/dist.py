@@ -40,7 +40,12 @@ def pack_results(h: dict, kmax: int) -> np.ndarray:
         v = h[name][:, :kmax]
         out[:, o:o + v.shape[1]] = v
         o += kmax
-    a = h["alpha"][:, :kmax]
+    a = h["alpha"]
+    if a.ndim == 4:  # (B, G, K, 2) from BatchSolver.host_outputs
+        if a.shape[1] != 1:
+            raise NotImplementedError("pack_results gathers single-snapshot results (G = 1)")
+        a = a[:, 0]
+    a = a[:, :kmax]
     out[:, o:o + a.shape[1]] = a[..., 0]
     o += kmax
     out[:, o:o + a.shape[1]] = a[..., 1]

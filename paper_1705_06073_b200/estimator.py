@@ -7,11 +7,11 @@ and this module only packs inputs, launches ``slse_estimate_batch`` through
 the C ABI and unpacks results.  ``estimate_batch`` is the batched entry
 point (one problem per row).
 
-Scope: complete data, a single snapshot (G = 1), the
+Scope: complete data, G >= 1 snapshots (MMV), the
 superfast backend.  ``backend="auto"`` runs superfast for complete data
 (the reference's auto picks its semifast backend below N = 512; both agree
 to ~1e-13 per call and give the same trajectories).
-``backend="semifast"``, incomplete patterns and G > 1 are outside this
+``backend="semifast"`` and incomplete patterns are outside this
 build's scope and raise.
 """
 
@@ -109,7 +109,7 @@ class BatchOutputs:
     """Output arrays of one batched solve (torch tensors on one device, or
     numpy arrays for host-side consumers), laid out as slse_outputs."""
 
-    def __init__(self, xp_empty, B, kmax, tcap, ecap):
+    def __init__(self, xp_empty, B, kmax, tcap, ecap, g=1):
         e = xp_empty
         self.k_hat = e((B,), "i32")
         self.status = e((B,), "i32")
@@ -119,7 +119,7 @@ class BatchOutputs:
         self.zeta = e((B,), "f64")
         self.theta = e((B, kmax), "f64")
         self.gamma = e((B, kmax), "f64")
-        self.alpha = e((B, kmax, 2), "f64")
+        self.alpha = e((B, g, kmax, 2), "f64")  # [B, G, kmax] complex
         self.slot = e((B, kmax), "i32")
         self.trace = e((B, tcap), "f64")
         self.stage = e((B, tcap), "i32")
@@ -174,7 +174,7 @@ def unpack_all(h: dict):
     iters = h["iterations"].tolist()
     beta = h["beta"].tolist()
     zeta = h["zeta"].tolist()
-    alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]  # (B, K)
+    alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]  # (B, G, K)
     names = _STAGE_ARR[np.clip(h["stage"], 0, len(STAGE_NAMES) - 1)]
     secs = h["stage_seconds"].tolist()
     ctr = h["counters"].tolist()
@@ -197,7 +197,7 @@ def unpack_all(h: dict):
         out.append(LseResult(
             k_hat=k,
             theta_hat=theta[b, :k],
-            alpha_hat=alpha[b, :k].reshape(1, k),
+            alpha_hat=alpha[b, :, :k].copy(),
             beta_hat=beta[b],
             gamma_hat=gamma[b, :k],
             zeta_hat=zeta[b],
@@ -239,7 +239,7 @@ class BatchSolver:
     contiguous complex128 (B, N) CUDA tensor.  ``results()`` copies back and
     unpacks.  No host synchronisation happens inside ``solve``."""
 
-    def __init__(self, n: int, batch: int, opts: EstimatorOptions = None, device=None):
+    def __init__(self, n: int, batch: int, opts: EstimatorOptions = None, device=None, g: int = 1):
         torch = _torch()
         self.opts = opts or EstimatorOptions()
         _validate(self.opts)
@@ -249,32 +249,36 @@ class BatchSolver:
         if not torch.cuda.is_available():
             raise SuperLseError("no CUDA device: the superfast GPU path has no CPU fallback")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.n, self.batch = n, batch
+        self.n, self.batch, self.g = n, batch, int(g)
+        if self.g < 1:
+            raise ValueError("need at least one snapshot")
         self.copts = c_options(self.opts, n)
         self.kmax = self.copts.k_max
         self.L = default_grid_size(n, self.opts.grid_factor)
         with torch.cuda.device(self.device):
-            ws = self.lib.slse_estimate_workspace_bytes(n, batch, ctypes.byref(self.copts))
+            ws = self.lib.slse_estimate_workspace_bytes_mmv(n, self.g, batch, ctypes.byref(self.copts))
             if ws == 0:
-                _native.check(-1, "slse_estimate_workspace_bytes")
+                _native.check(-1, "slse_estimate_workspace_bytes_mmv")
             self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
 
             def empty(shape, dt):
                 return torch.empty(shape, dtype=getattr(torch, _TORCH_DT[dt]), device=self.device)
 
-            self.out = BatchOutputs(empty, batch, self.kmax, self.copts.trace_capacity, self.copts.event_capacity)
+            self.out = BatchOutputs(empty, batch, self.kmax, self.copts.trace_capacity, self.copts.event_capacity,
+                                    g=self.g)
         self.cout = self.out.struct(lambda t: t.data_ptr())
 
     def solve(self, y_dev, stream=None):
         torch = _torch()
-        if y_dev.dtype != torch.complex128 or not y_dev.is_contiguous() or tuple(y_dev.shape) != (self.batch, self.n):
-            raise DimensionMismatch(f"y must be a contiguous complex128 tensor of shape ({self.batch}, {self.n})")
+        want = (self.batch, self.n) if self.g == 1 else (self.batch, self.g, self.n)
+        if y_dev.dtype != torch.complex128 or not y_dev.is_contiguous() or tuple(y_dev.shape) != want:
+            raise DimensionMismatch(f"y must be a contiguous complex128 tensor of shape {want}")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        rc = self.lib.slse_estimate_batch(
-            ctypes.c_void_p(y_dev.data_ptr()), self.n, self.batch, ctypes.byref(self.copts),
+        rc = self.lib.slse_estimate_batch_mmv(
+            ctypes.c_void_p(y_dev.data_ptr()), self.n, self.g, self.batch, ctypes.byref(self.copts),
             ctypes.byref(self.cout), ctypes.c_void_p(self.workspace.data_ptr()),
             ctypes.c_size_t(self.workspace.numel()), ctypes.c_void_p(st.cuda_stream))
-        _native.check(rc, "slse_estimate_batch")
+        _native.check(rc, "slse_estimate_batch_mmv")
 
     def host_outputs(self) -> dict:
         """Host copies, trimmed to the longest trace / history / model order
@@ -287,7 +291,7 @@ class BatchSolver:
         tt = max(1, int(h["n_trace"].max(initial=0)))
         ee = max(1, int(h["n_events"].max(initial=0)))
         o = self.out
-        big = {"theta": o.theta[:, :kk], "gamma": o.gamma[:, :kk], "alpha": o.alpha[:, :kk], "slot": o.slot[:, :kk],
+        big = {"theta": o.theta[:, :kk], "gamma": o.gamma[:, :kk], "alpha": o.alpha[:, :, :kk], "slot": o.slot[:, :kk],
                "trace": o.trace[:, :tt], "stage": o.stage[:, :tt], "trace_k": o.trace_k[:, :tt],
                "events": o.events[:, :ee]}
         for name, t in big.items():
@@ -305,8 +309,9 @@ class BatchResult:
     LseResult objects, built on first access.
 
     SoA fields (problem-major): k_hat, status, iterations, converged, beta,
-    zeta (B,); theta, gamma, alpha (complex), slot (B, K) zero-padded past
-    k_hat; trace (B, T) padded past n_trace."""
+    zeta (B,); theta, gamma, slot (B, K) zero-padded past k_hat; alpha
+    complex (B, K), or (B, G, K) with G > 1 snapshots; trace (B, T) padded
+    past n_trace."""
 
     def __init__(self, h: dict):
         self.h = h
@@ -318,7 +323,8 @@ class BatchResult:
         self.zeta = h["zeta"]
         self.theta = h["theta"]
         self.gamma = h["gamma"]
-        self.alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]
+        alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]  # (B, G, K)
+        self.alpha = alpha[:, 0] if alpha.shape[1] == 1 else alpha
         self.slot = h["slot"]
         self.trace = h["trace"]
         self.n_trace = h["n_trace"]
@@ -340,7 +346,8 @@ class BatchResult:
 
 
 def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False) -> BatchResult:
-    """Solve B independent complete-data problems, y: (B, N) complex.
+    """Solve B independent complete-data problems, y: (B, N) complex, or
+    (B, G, N) for G snapshots per problem sharing the frequencies (MMV).
     Accepts numpy or torch input; returns a BatchResult (SoA arrays + a
     sequence of LseResult in problem order).  Problems that hit a non-PD
     covariance carry ``status`` 1 instead of raising."""
@@ -349,9 +356,12 @@ def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=
         yt = y
     else:
         yt = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(np.asarray(y, dtype=np.complex128))))
-    if yt.dim() != 2:
-        raise DimensionMismatch("y must have shape (B, N)")
-    solver = BatchSolver(int(yt.shape[1]), int(yt.shape[0]), opts, device=device)
+    if yt.dim() not in (2, 3):
+        raise DimensionMismatch("y must have shape (B, N) or (B, G, N)")
+    g = 1 if yt.dim() == 2 else int(yt.shape[1])
+    if yt.dim() == 3 and g == 1:
+        yt = yt[:, 0]
+    solver = BatchSolver(int(yt.shape[-1]), int(yt.shape[0]), opts, device=device, g=g)
     if yt.device.type == "cpu" and not yt.is_pinned():
         yt = yt.pin_memory()
     ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=True).contiguous()
@@ -368,9 +378,8 @@ def estimate(obs: Observation, opts: EstimatorOptions = None) -> LseResult:
     _validate(opts)
     if not obs.is_complete:
         raise InvalidPattern("superfast backend requires the complete observation pattern")
-    if obs.g != 1:
-        raise NotImplementedError("multiple snapshots (G > 1) are outside this build's scope")
-    res = estimate_batch(obs.y, opts)[0]
+    y = np.asarray(obs.y, dtype=np.complex128)
+    res = estimate_batch(y if obs.g == 1 else y[None], opts)[0]
     if res.status == STATUS_NOT_PD:
         raise NotPositiveDefinite("covariance lost positive definiteness during the fit")
     if res.status == STATUS_BAD_DIAGONAL:
@@ -379,5 +388,6 @@ def estimate(obs: Observation, opts: EstimatorOptions = None) -> LseResult:
 
 
 def estimate_mmv(obs: Observation, opts: EstimatorOptions = None) -> LseResult:
-    """estimator.py:278-283 alias (G = 1 is the same code path)."""
+    """estimator.py:278-283: snapshots share the frequencies; same path as
+    estimate() (G = 1 included)."""
     return estimate(obs, opts)
