@@ -32,9 +32,9 @@ cudaError_t SLSE_CAT(slse_solve_launch_, SLSE_NT)(int grid, size_t smem, cudaStr
 // Read (and optionally reset) the solver phase-cycle accumulators of this
 // instantiation (see slse_solver.cuh, SLSE_SOLVER_PROF).
 extern "C" int SLSE_CAT(slse_solver_prof_, SLSE_NT)(unsigned long long* out, int reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(out, slse::slse_prof_cycles, sizeof(unsigned long long) * 8);
+  cudaError_t e = cudaMemcpyFromSymbol(out, slse::slse_prof_cycles, sizeof(unsigned long long) * 16);
   if (e == cudaSuccess && reset) {
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long z[16] = {};
     e = cudaMemcpyToSymbol(slse::slse_prof_cycles, z, sizeof(z));
   }
   return (int)e;

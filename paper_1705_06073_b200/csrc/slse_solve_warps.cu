@@ -39,9 +39,9 @@ cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t s
 
 #ifdef SLSE_SOLVER_PROF
 extern "C" int slse_solver_prof_warps(unsigned long long* out, int reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(out, slse::slse_prof_cycles, sizeof(unsigned long long) * 8);
+  cudaError_t e = cudaMemcpyFromSymbol(out, slse::slse_prof_cycles, sizeof(unsigned long long) * 16);
   if (e == cudaSuccess && reset) {
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long z[16] = {};
     e = cudaMemcpyToSymbol(slse::slse_prof_cycles, z, sizeof(z));
   }
   return (int)e;

@@ -41,14 +41,23 @@ enum Timer : int { kTmActivate = 0, kTmObjective = 1, kTmBeta = 2, kTmRefine = 3
 // -DSLSE_SOLVER_PROF; tools/solver_prof.py).  Leader-thread clock64 deltas,
 // accumulated per problem and added to slse_prof_cycles at finish():
 // 0 covariance column, 1 factor, 2 GS apply, 3 stats, 4 grid, 5 whole run,
-// 6 waiting to enter an operation window, 7 waiting for it to close (warp mode).
+// 6 waiting to enter an operation window, 7 waiting for it to close (warp mode),
+// control code (exclusive of the operations inside): 8 sweep, 9 try_activate,
+// 10 deactivate, 11 lbfgs_step, 12 record, 13 beta EM (residual_value);
+// inside lbfgs_step: 14 the accepted point's stats call (inclusive),
+// 15 gradient + memory push + slot update.
 #ifdef SLSE_SOLVER_PROF
-__device__ unsigned long long slse_prof_cycles[8];
+__device__ unsigned long long slse_prof_cycles[16];
 #define SLSE_PROF_T0(v) const long long v = clock64()
 #define SLSE_PROF_ADD(i, v) (prof_acc[i] += clock64() - (v))
+// control-code slots: time inside the function minus the operations it ran
+#define SLSE_PROF_C0(v) const long long v##_t = clock64(), v##_o = prof_ops()
+#define SLSE_PROF_CADD(i, v) (prof_acc[i] += (clock64() - v##_t) - (prof_ops() - v##_o))
 #else
 #define SLSE_PROF_T0(v)
 #define SLSE_PROF_ADD(i, v)
+#define SLSE_PROF_C0(v)
+#define SLSE_PROF_CADD(i, v)
 #endif
 
 // Control-code loops (thread-strided over k, dim, L): kept rolled -- the
@@ -329,7 +338,10 @@ struct Solver {
   int mem_valid, mem_dim, mem_count, mem_head;
   long long n_builds, n_grids, n_stats, n_backtracks;
 #ifdef SLSE_SOLVER_PROF
-  long long prof_acc[8], prof_run0;
+  long long prof_acc[16], prof_run0;
+  SLSE_D long long prof_ops() const {
+    return prof_acc[0] + prof_acc[1] + prof_acc[2] + prof_acc[3] + prof_acc[4] + prof_acc[6] + prof_acc[7];
+  }
 #endif
   unsigned long long t_mark, t_start;
   double tm[6];
@@ -378,7 +390,7 @@ struct Solver {
     mem_valid = 0; mem_dim = 0; mem_count = 0; mem_head = 0;
     n_builds = n_grids = n_stats = n_backtracks = 0;
 #ifdef SLSE_SOLVER_PROF
-    for (int i = 0; i < 8; ++i) prof_acc[i] = 0;
+    for (int i = 0; i < 16; ++i) prof_acc[i] = 0;
 #endif
     for (int i = 0; i < 6; ++i) tm[i] = 0.0;
     free_hint = 0;
@@ -518,7 +530,7 @@ struct Solver {
   SLSE_NIM void stats(Bundle& B, const double* th, int kk) {
     if (B.stats_valid) return;
     ++n_stats;
-#ifdef SLSE_WARP_MODE
+#if defined(SLSE_WARP_MODE) && defined(SLSE_STATS_RV)
     SLSE_PROF_T0(w0);
     rv_arrive(0);
     SLSE_PROF_ADD(6, w0);
@@ -557,6 +569,12 @@ struct Solver {
   }
 
   SLSE_NIM void record(int stage) {
+    SLSE_PROF_C0(pc);
+    record_body(stage);
+    SLSE_PROF_CADD(12, pc);
+  }
+
+  SLSE_NIM void record_body(int stage) {
     const double val = objective(bun[cur]);
     if (b.leader() && ntrace < P.tcap) {
       o.trace[ntrace] = val;
@@ -584,7 +602,7 @@ struct Solver {
 
   SLSE_NIM void grid_curve(double gb, double ze) {
     ++n_grids;
-#ifdef SLSE_WARP_MODE
+#if defined(SLSE_WARP_MODE) && defined(SLSE_GRID_RV)
     SLSE_PROF_T0(w0);
     rv_arrive(0);
     SLSE_PROF_ADD(6, w0);
@@ -629,6 +647,13 @@ struct Solver {
 
   // returns 1 if a component was activated (smlr.py:107-122)
   SLSE_NIM int try_activate() {
+    SLSE_PROF_C0(pc);
+    const int rv_ = try_activate_body();
+    SLSE_PROF_CADD(9, pc);
+    return rv_;
+  }
+
+  SLSE_NIM int try_activate_body() {
     const int tid_ = b.tid, nt_ = b.nt;
     if (k >= kmax) return 0;
     const double gb = gamma_bar();
@@ -666,6 +691,13 @@ struct Solver {
 
   // initial multi-activation sweep (smlr.py:125-171); returns #added
   SLSE_NIM int sweep() {
+    SLSE_PROF_C0(pc);
+    const int rv_ = sweep_body();
+    SLSE_PROF_CADD(8, pc);
+    return rv_;
+  }
+
+  SLSE_NIM int sweep_body() {
     const int tid_ = b.tid, nt_ = b.nt;
     const double gb = gamma_bar();
     const double ze = prior_zeta(zeta, kmax);
@@ -765,6 +797,13 @@ struct Solver {
   // ---- deactivation (smlr.py:174-225) ----
   // on return: number removed; cur is valid for the new state (stats too if k>0)
   SLSE_NIM int deactivate(int* st) {
+    SLSE_PROF_C0(pc);
+    const int rv_ = deactivate_body(st);
+    SLSE_PROF_CADD(10, pc);
+    return rv_;
+  }
+
+  SLSE_NIM int deactivate_body(int* st) {
     const int tid_ = b.tid, nt_ = b.nt;
     int removed = 0;
     *st = kOk;
@@ -834,7 +873,68 @@ struct Solver {
   }
 
   // two-loop recursion into dir (lbfgs.py:63-76); uses gnew as q scratch
+#ifndef SLSE_HOST_EMU
+  // One-warp two-loop recursion for dim <= 64 (two entries per lane): q and
+  // the direction stay in registers, the memory pairs are read once, the
+  // dot products are warp xor-sums (the same bits as Blk::sum for one warp),
+  // and the loop over pairs is unrolled with predicates so the alphas stay in
+  // registers.  Same arithmetic as two_loop.
+  SLSE_NIM void two_loop_warp(int dim) {
+    const int lane = b.tid;
+    const bool in0 = lane < dim, in1 = lane + 32 < dim;
+    double q0 = in0 ? g0[lane] : 0.0, q1 = in1 ? g0[lane + 32] : 0.0;
+    const int K2 = 2 * kmax;
+    const int mc = mem_count;
+    double alphas[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {  // jj = mc - 1 - t, descending
+      alphas[t] = 0.0;
+      if (t < mc) {
+        const int slot = (mem_head + (mc - 1 - t)) % P.lbfgs_mem;
+        const double* S = lbS + (size_t)slot * K2;
+        const double* Y = lbY + (size_t)slot * K2;
+        double part = 0.0;
+        if (in0) part += S[lane] * q0;
+        if (in1) part += S[lane + 32] * q1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const double al_ = lbR[slot] * part;
+        alphas[t] = al_;
+        if (in0) q0 -= al_ * Y[lane];
+        if (in1) q1 -= al_ * Y[lane + 32];
+      }
+    }
+    double d0 = in0 ? q0 / diag[lane] : 0.0, d1 = in1 ? q1 / diag[lane + 32] : 0.0;
+#pragma unroll
+    for (int t = 15; t >= 0; --t) {  // jj = mc - 1 - t, ascending
+      if (t < mc) {
+        const int slot = (mem_head + (mc - 1 - t)) % P.lbfgs_mem;
+        const double* S = lbS + (size_t)slot * K2;
+        const double* Y = lbY + (size_t)slot * K2;
+        double part = 0.0;
+        if (in0) part += Y[lane] * d0;
+        if (in1) part += Y[lane + 32] * d1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const double be = lbR[slot] * part;
+        const double coef = alphas[t] - be;
+        if (in0) d0 += S[lane] * coef;
+        if (in1) d1 += S[lane + 32] * coef;
+      }
+    }
+    if (in0) dir[lane] = -d0;
+    if (in1) dir[lane + 32] = -d1;
+    __syncwarp();
+  }
+#endif
+
   SLSE_NIM void two_loop(int dim) {
+#ifndef SLSE_HOST_EMU
+    if (b.nt == 32 && dim <= 64 && P.lbfgs_mem <= 16) {
+      two_loop_warp(dim);
+      return;
+    }
+#endif
     const int tid_ = b.tid, nt_ = b.nt;
     double alphas[16];
     double* qv = gnew;
@@ -899,6 +999,13 @@ struct Solver {
   // failure, or a negative model status.  On acceptance the new point is in
   // the slot arrays, cur is the accepted bundle (stats valid), *dec set.
   SLSE_NIM int lbfgs_step(double f0, double* dec) {
+    SLSE_PROF_C0(pc);
+    const int rv_ = lbfgs_step_body(f0, dec);
+    SLSE_PROF_CADD(11, pc);
+    return rv_;
+  }
+
+  SLSE_NIM int lbfgs_step_body(double f0, double* dec) {
     const int tid_ = b.tid, nt_ = b.nt;
     const int dim = 2 * k;
     // any(g0)?
@@ -931,6 +1038,7 @@ struct Solver {
     double alpha = capv < 1.0 ? capv : 1.0;
     if (alpha <= 0.0) return 1;
     Bundle& T = bun[cur ^ 1];
+    SLSE_PROF_C0(pl);
     for (int bt = 0; bt < kMaxBacktracks; ++bt) {
       ++n_backtracks;
       SLSE_CTRL_LOOP
@@ -945,7 +1053,10 @@ struct Solver {
       if (st != kOk) return -st;
       const double fn = T.data_term + prior_term(k, zeta, kmax);
       if (fn <= f0 + kArmijoC1 * alpha * slope) {
+        SLSE_PROF_T0(ps);
         stats(T, cth, k);
+        SLSE_PROF_ADD(14, ps);
+        SLSE_PROF_T0(pa);
         gradient(T, cga, gnew);
         b.sync();
         push_pair(alpha, dim);
@@ -961,6 +1072,7 @@ struct Solver {
         b.sync();
         cur ^= 1;
         cur_valid = 1;
+        SLSE_PROF_ADD(15, pa);
         return 0;
       }
       alpha *= kBacktrack;
@@ -1124,6 +1236,13 @@ struct Solver {
 
   // beta EM value (tr + ||y - Psi(theta) mu||^2) / M  (estimator.py:86-88)
   SLSE_NIM double residual_value(double tr) {
+    SLSE_PROF_C0(pc);
+    const double rv_ = residual_value_body(tr);
+    SLSE_PROF_CADD(13, pc);
+    return rv_;
+  }
+
+  SLSE_NIM double residual_value_body(double tr) {
     const int tid_ = b.tid, nt_ = b.nt;
     double* mre = marg;  // scratch (length >= k)
     double* mim = dtmp;  // scratch (length n >= k), free outside build()
@@ -1170,7 +1289,7 @@ struct Solver {
 #ifdef SLSE_SOLVER_PROF
     prof_acc[5] = clock64() - prof_run0;
     if (b.leader())
-      for (int i = 0; i < 8; ++i) atomicAdd(&slse_prof_cycles[i], (unsigned long long)prof_acc[i]);
+      for (int i = 0; i < 16; ++i) atomicAdd(&slse_prof_cycles[i], (unsigned long long)prof_acc[i]);
 #endif
     if (converged) flags |= kFlConverged;
     if (b.leader()) {

@@ -20,7 +20,9 @@ from paper_1705_06073_b200 import EstimatorOptions, simdata  # noqa: E402
 from paper_1705_06073_b200 import _native  # noqa: E402
 from paper_1705_06073_b200.estimator import BatchSolver  # noqa: E402
 
-PHASES = ["covariance column", "factor", "GS apply", "stats", "grid", "whole run", "rv wait (arrive)", "rv wait (depart)"]
+PHASES = ["covariance column", "factor", "GS apply", "stats", "grid", "whole run", "rv wait (arrive)",
+          "rv wait (depart)", "ctl: sweep", "ctl: try_activate", "ctl: deactivate", "ctl: lbfgs_step", "ctl: record",
+          "ctl: beta EM", " (accept: stats incl)", " (accept: grad+push)"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -32,7 +34,7 @@ Y = torch.from_numpy(simdata.batch(20261019, a.config, B)).cuda()
 s = BatchSolver(n, B, EstimatorOptions(grid_factor=4))
 s.solve(Y)  # warm-up
 lib = _native.load()
-out = (ctypes.c_ulonglong * 8)()
+out = (ctypes.c_ulonglong * 16)()
 fns = {nt: getattr(lib, f"slse_solver_prof_{nt}") for nt in (32, 64, 128, 256, 512, 1024)}
 fns["warps"] = lib.slse_solver_prof_warps
 for fn in fns.values():
@@ -50,6 +52,6 @@ for nt, fn in fns.items():
     if v[5] == 0:
         continue
     print(f"solver NT={nt}: total {v[5] / 1e9:.3f} G leader-cycles")
-    for name, x in zip(PHASES[:5] + PHASES[6:], v[:5] + v[6:]):
-        print(f"  {name:18s} {100.0 * x / v[5]:6.1f} %")
-    print(f"  {'other':18s} {100.0 * (v[5] - sum(v[:5]) - sum(v[6:])) / v[5]:6.1f} %")
+    for name, x in zip(PHASES[:5] + PHASES[6:16], v[:5] + v[6:16]):
+        print(f"  {name:20s} {100.0 * x / v[5]:6.1f} %")
+    print(f"  {'other':20s} {100.0 * (v[5] - sum(v[:5]) - sum(v[6:14])) / v[5]:6.1f} %")
