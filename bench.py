@@ -276,7 +276,9 @@ def run_ours(args):
     # FP64 DFMA peak measured on this pool's B200 (tools/micro/fp64_peak.cu, profiles/r1_fp64_peak.txt)
     fp64_peak = 34.09
     attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg_bytes, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
-    roof = {"bound": "hbm", "kernel": "grid_fused_kernel (activation grid, SURVEY 8(a) row 9)",
+    kname = ("grid_tma_kernel" if (L == 1024 and 128 < n <= 256) else "grid_fused_kernel") + \
+        " (activation grid, SURVEY 8(a) row 9)"
+    roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
             "traffic": None, "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
             "launch_ms": grid_ms, "flops_per_launch": flops,

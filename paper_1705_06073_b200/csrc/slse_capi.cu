@@ -10,6 +10,7 @@
 //                         parity tests check against the oracle.
 //   tw_fill_kernel        twiddle table exp(-2 pi i k / TW).
 #include "slse_kernels.cuh"
+#include "slse_grid.cuh"
 
 #include <cstdlib>
 
@@ -417,6 +418,25 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   cudaError_t e = cudaSuccess;
   // register-Stockham path: 3 L-point transforms resident in shared memory,
   // compile-time pass schedules for L = 2^6 .. 2^12, pruned first pass
+  // v5 (slse_grid.cuh): two-pass transform, TMA bulk input prefetch, persistent
+  if (L == 1024 && N > 128 && N <= 256 && getenv("SLSE_GRID_V3") == nullptr && getenv("SLSE_GRID_DIT") == nullptr) {
+    const size_t smem = g5_smem_bytes(N);
+    e = set_smem(grid_tma_kernel, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_tma_kernel, kG5Threads, smem);
+    if (e == cudaSuccess && occ > 0) {
+      int g = sm_count() * occ;
+      if (g > B) g = B;
+      grid_tma_kernel<<<g, kG5Threads, smem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, B, (cplx*)q_grid,
+                                                  s_grid, tw, twlog);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? 0 : fail("grid_tma_kernel", e);
+    }
+    if (e != cudaSuccess) return fail("grid_tma_kernel setup", e);
+  }
   if (getenv("SLSE_GRID_DIT") == nullptr) {
     const int lg = ilog2(L);
     int q = 0;

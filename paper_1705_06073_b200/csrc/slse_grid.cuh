@@ -1,0 +1,237 @@
+// slse_grid.cuh -- Row 9 standalone activation grid, v5 ("two-pass, TMA in").
+//
+// Reference: _SuperfastBundle.grid (pkg/src/superlse/model_core.py:303-313):
+//   q^G = FFT_L(w),  s^G = delta^-1 [(2 - N)|A0|^2 + 2 Re(A1 conj A0)],
+//   A0 = FFT_L(rho), A1 = FFT_L(n rho_n)   (product form).
+//
+// Shape this kernel serves: L = 1024, 128 < N <= 256 (BASELINE cfg2).  The
+// three zero-padded 1024-point transforms run as ONE shared-memory exchange:
+//   n = t + 16 s  (t < 16, s < 64, nonzero only for s < 16 since N <= 256)
+//   l = a + 64 b  (a < 64, b < 16)
+//   X[a + 64 b] = sum_t W16^{t b} W1024^{t a} Y(t, a),
+//   Y(t, a)     = sum_{s<16} x_{t+16s} W64^{s a}.
+// With a = r + 4 a' the inner sum is a 16-point DFT over s of the
+// pre-twiddled x_{t+16s} W64^{s r} (r = 0..3 residues), so
+//   inner pass: thread (signal c, t, r) -> one DFT16, 16 values Y(t, r+4a');
+//   exchange:   Y to shared memory at [a][t] (row stride 17: conflict-free);
+//   outer pass: thread (c, a) -> W1024^{t a} twiddles, one DFT16 over t,
+//               bins l = a + 64 b, b = 0..15 -> consecutive lanes write
+//               consecutive l: q^G and s^G leave coalesced from registers.
+// vs v3 (pruned radix-16, radix-16, radix-4 through two exchanges): half the
+// shared-memory round trips, the only traffic that competes with FP64.
+//
+// Inputs arrive by TMA bulk copy (cp.async.bulk + mbarrier complete_tx):
+// the CTA is persistent, and one thread issues the copy of its NEXT problem's
+// (w, rho) rows as soon as every warp has pulled the current ones into
+// registers, so HBM reads overlap the whole transform.  192 threads:
+//   inner: warp w -> c = w / 2 (0: w, 1: rho, 2: n rho), r = 2 (w % 2) + lane / 16
+//   outer: warps 0-1 -> q^G for a = tid; warps 2-5 -> (a, e) pairs, e = 0: A0,
+//          e = 1: A1; the pair swaps half of its bins by shuffle and each
+//          lane finishes s^G for 8 bins.
+#pragma once
+#include "slse_fft.cuh"
+
+namespace slse_k {
+using namespace slse;
+
+// ------------------------------------------------------------ TMA / mbarrier
+SLSE_D unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+SLSE_D void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+SLSE_D void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+SLSE_D void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+SLSE_D void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
+SLSE_D void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+#ifndef SLSE_G5_MAXREG
+#define SLSE_G5_MAXREG 96
+#endif
+#define SLSE_G5_BOUNDS __maxnreg__(SLSE_G5_MAXREG)
+
+// cos(2 pi k / 64), k = 0..16 (correctly rounded); other k by symmetry
+SLSE_HD constexpr double g5_c64q(int k) {
+  constexpr double c[17] = {1.0, 0.9951847266721969, 0.9807852804032304, 0.9569403357322088, 0.9238795325112867,
+                            0.881921264348355, 0.8314696123025452, 0.773010453362737, 0.7071067811865476,
+                            0.6343932841636455, 0.5555702330196022, 0.47139673682599764, 0.3826834323650898,
+                            0.2902846772544624, 0.19509032201612828, 0.0980171403295606, 0.0};
+  return c[k];
+}
+SLSE_HD constexpr double g5_cos64(int k) {
+  k &= 63;
+  return k <= 16 ? g5_c64q(k) : (k <= 32 ? -g5_c64q(32 - k) : (k <= 48 ? -g5_c64q(k - 32) : g5_c64q(64 - k)));
+}
+SLSE_HD constexpr double g5_sin64(int k) { return g5_cos64(k + 48); }  // sin x = cos(x - pi/2)
+
+// v[s] *= W64^{s r}, r = 2 RP + h: the two candidate twiddles are
+// compile-time constants, picked per half-warp by selects (no table loads)
+template <int RP>
+SLSE_D void g5_pretwiddle(cplx* v, int h) {
+#pragma unroll
+  for (int s = 1; s < 16; ++s) {
+    const int k0 = (s * 2 * RP) & 63, k1 = (s * (2 * RP + 1)) & 63;
+    const double cr = h ? g5_cos64(k1) : g5_cos64(k0);
+    const double ci = h ? -g5_sin64(k1) : -g5_sin64(k0);
+    v[s] = cmul(v[s], mk(cr, ci));
+  }
+}
+
+constexpr int kG5Threads = 192;
+constexpr int kG5Warps = kG5Threads / 32;
+constexpr int kG5Row = 17;                    // exchange row stride (complex) per a
+constexpr int kG5Buf = 64 * kG5Row;           // one signal's exchange buffer
+SLSE_HD constexpr size_t g5_smem_bytes(int n) {
+  // mbarriers (128 B) | 2 stages of (w, rho) (2 x 2 n cplx) | X (3 buffers)
+  return 128 + 2 * 2 * 16 * (size_t)n + 3 * 16 * (size_t)kG5Buf;
+}
+
+SLSE_D void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Synchronisation per problem k (stage k & 1):
+//   full[k & 1]   TMA complete_tx: (w, rho) of problem k landed;
+//   __syncthreads every warp stored its inner spectra to X (the one true
+//                 barrier); it also proves stage k & 1 fully read, so thread
+//                 0 then refills it with problem k + 2;
+//   xfree         one arrival per warp once it has pulled its outer inputs
+//                 from X; a warp waits on it (previous phase) only right
+//                 before its next inner stores, long after everyone arrived.
+__global__ void SLSE_G5_BOUNDS grid_tma_kernel(
+    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int B,
+    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* __restrict__ tw, int twlog) {
+  constexpr int L = 1024;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* full = (uint64_t*)smem_raw;  // [2]
+  uint64_t* xfree = full + 2;
+  cplx* stage = (cplx*)(smem_raw + 128);  // [2][w | rho], n each
+  cplx* X = stage + 4 * n;                // 3 exchange buffers
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const unsigned row_bytes = 16u * (unsigned)n;
+  const int G = gridDim.x;
+
+  const auto issue = [&](int prob, int st) {
+    mbar_expect_tx(&full[st], 2 * row_bytes);
+    tma_load_1d(stage + st * 2 * n, w + (size_t)prob * n, row_bytes, &full[st]);
+    tma_load_1d(stage + st * 2 * n + n, rho + (size_t)prob * n, row_bytes, &full[st]);
+  };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(xfree, kG5Warps);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if ((int)blockIdx.x < B) issue(blockIdx.x, 0);
+    if ((int)blockIdx.x + G < B) issue(blockIdx.x + G, 1);
+  }
+  // inner-pass role (fixed for the kernel's lifetime)
+  const int ic = warp >> 1;                          // 0: w, 1: rho, 2: n rho
+  const int t = lane & 15;
+  const int r = 2 * (warp & 1) + (lane >> 4);         // residue 0..3
+  cplx* Xi = X + ic * kG5Buf;
+  // outer-pass role
+  const bool oq = warp < 2;
+  const int oa = oq ? tid : (tid - 64) >> 1;          // a = 0..63
+  const int oe = oq ? 0 : ((tid - 64) & 1);           // A-pair member: 0 -> A0, 1 -> A1
+  const cplx* Xo = X + (oq ? 0 : 1 + oe) * kG5Buf + oa * kG5Row;
+  // middle twiddles W1024^{t a}, t = 0..15: fixed per thread, recomputed per
+  // problem from two table entries (keeps registers for the transform)
+  const cplx wa = twid_tab(tw, twlog, oa, 10, -1.0);
+  const cplx wa2 = twid_tab(tw, twlog, 2 * oa, 10, -1.0);
+  const double c2n = 2.0 - (double)n;
+
+  int p = blockIdx.x;
+  for (unsigned k = 0; p < B; ++k, p += G) {
+    const unsigned st = k & 1;
+    const double dl = oq ? 1.0 : delta_last[p];  // issued early, used by the outer pass
+    mbar_wait(&full[st], (k >> 1) & 1);
+    // ---- inner pass: load x_{t + 16 s}, s < 16 (zero beyond n)
+    const cplx* src = stage + st * 2 * n + (ic == 0 ? 0 : n);
+    cplx v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int i = t + 16 * s;
+      v[s] = i < n ? src[i] : mk(0.0, 0.0);
+    }
+    if (ic == 2) {
+#pragma unroll
+      for (int s = 0; s < 16; ++s) v[s] = cscale(v[s], (double)(t + 16 * s));
+    }
+    if (warp & 1) g5_pretwiddle<1>(v, lane >> 4);
+    else g5_pretwiddle<0>(v, lane >> 4);
+    dft_dif<16>(v, -1.0);  // Y(t, r + 4 a') = v[brev(a')]
+    if (k) mbar_wait(xfree, (k - 1) & 1);  // everyone has read problem k-1's X
+#pragma unroll
+    for (int a2 = 0; a2 < 16; ++a2) Xi[(r + 4 * a2) * kG5Row + t] = v[brev_const(a2, 16)];
+    __syncthreads();
+    if (tid == 0 && p + 2 * G < B) issue(p + 2 * G, st);
+    // ---- outer pass: Y(t, a) W1024^{t a}, DFT16 over t
+#pragma unroll
+    for (int tt = 0; tt < 16; ++tt) v[tt] = Xo[tt];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xfree);
+    {
+      // W1024^{t a} by two interleaved chains (even / odd t): 3 live values
+      cplx pe = wa2, po = wa;
+      v[1] = cmul(v[1], wa);
+#pragma unroll
+      for (int tt = 2; tt < 16; tt += 2) {
+        if (tt > 2) pe = cmul(pe, wa2);
+        po = cmul(po, wa2);
+        v[tt] = cmul(v[tt], pe);
+        v[tt + 1] = cmul(v[tt + 1], po);
+      }
+    }
+    dft_dif<16>(v, -1.0);  // bin l = a + 64 b is v[brev(b)]
+    if (oq) {
+      double2* qg = (double2*)(q_grid + (size_t)p * L);
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const cplx o = v[brev_const(b, 16)];
+        __stcs(&qg[oa + 64 * b], make_double2(o.re, o.im));
+      }
+    } else {
+      // lane pair (e = 0: A0, e = 1: A1): e keeps bins b in [8e, 8e + 8) and
+      // receives the partner's spectrum there
+      const double inv_d = 1.0 / dl;
+      double* sg = s_grid + (size_t)p * L;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const cplx lo = v[brev_const(j, 16)], hi = v[brev_const(j + 8, 16)];
+        const cplx mine = oe ? hi : lo, give = oe ? lo : hi;
+        cplx got;
+        got.re = __shfl_xor_sync(0xffffffffu, give.re, 1);
+        got.im = __shfl_xor_sync(0xffffffffu, give.im, 1);
+        const cplx a0 = oe ? got : mine, a1 = oe ? mine : got;
+        const double sv = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+        __stcs(&sg[oa + 64 * (j + 8 * oe)], sv);
+      }
+    }
+  }
+}
+
+}  // namespace slse_k
