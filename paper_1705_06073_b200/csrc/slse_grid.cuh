@@ -24,8 +24,9 @@
 // the CTA is persistent, and one thread issues the copy of its NEXT problem's
 // (w, rho) rows as soon as every warp has pulled the current ones into
 // registers, so HBM reads overlap the whole transform.  192 threads:
-//   inner: warp w -> c = w / 2 (0: w, 1: rho, 2: n rho), r = 2 (w % 2) + lane / 16
-//   outer: warps 0-1 -> q^G for a = tid; warps 2-5 -> (a, e) pairs, e = 0: A0,
+//   inner: warps 0-3 -> residue r = warp of w (lanes 0-15) and rho (lanes 16-31),
+//          warps 4-5 -> n rho at r = 2 (warp - 4) + lane / 16
+//   outer: warps 4-5 -> q^G for a = tid - 128; warps 0-3 -> (a, e) pairs, e = 0: A0,
 //          e = 1: A1; the pair swaps half of its bins by shuffle and each
 //          lane finishes s^G for 8 bins.
 #pragma once
@@ -97,10 +98,89 @@ SLSE_D void g5_pretwiddle(cplx* v, int h) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// DFT16 as radix-4 x radix-4 with the twiddles in "scaled" form, so a
+// twiddled butterfly input costs one FMA per component instead of a full
+// complex multiply (the tangent method):
+//   W64^e z = sigma * q,  tangent:   sigma = cos, q = (x + T y, y - T x), T = tan
+//                         cotangent: sigma = sin, q = (K x + y, K y - x), K = cot
+// (whichever keeps |T|, |K| <= 1), exact swaps for e = 16, 32, 48.  A radix-4
+// butterfly with scaled inputs b, c, d then folds the scales into its FMAs:
+// 22 ops for three general twiddles vs 28 (3 cmul + 16 adds).
+// dft16_t<R>: X[k] = sum_s x[s] W64^{s R} W16^{s k}, i.e. a DFT16 of the
+// input pre-twiddled by W64^{s R}; the pre-twiddle splits as W64^{4 n2 R}
+// (stage-1 twiddles) times W64^{n1 R}, which merges into the stage-2
+// twiddles W64^{n1 (4 k2 + R)} at no cost (s = n1 + 4 n2, k = 4 k1 + k2).
+enum { G5_ID = 0, G5_ROT = 1, G5_TAN = 2, G5_COT = 3 };
+SLSE_HD constexpr double g5_abs(double x) { return x < 0 ? -x : x; }
+SLSE_HD constexpr int g5_kind(int e) {
+  return (e & 63) == 0 ? G5_ID
+                       : ((e & 15) == 0 ? G5_ROT : (g5_abs(g5_cos64(e)) >= g5_abs(g5_sin64(e)) ? G5_TAN : G5_COT));
+}
+SLSE_HD constexpr double g5_sigma(int e) {
+  return g5_kind(e) == G5_TAN ? g5_cos64(e) : (g5_kind(e) == G5_COT ? g5_sin64(e) : 1.0);
+}
+template <int E>
+SLSE_D cplx g5_q(cplx z) {
+  constexpr int k = g5_kind(E);
+  if constexpr (k == G5_ID) {
+    return z;
+  } else if constexpr (k == G5_ROT) {
+    constexpr int e = E & 63;
+    if constexpr (e == 16) return mk(z.im, -z.re);    // -i z
+    else if constexpr (e == 32) return mk(-z.re, -z.im);
+    else return mk(-z.im, z.re);                      // +i z
+  } else if constexpr (k == G5_TAN) {
+    constexpr double T = g5_sin64(E) / g5_cos64(E);
+    return mk(fma(T, z.im, z.re), fma(-T, z.re, z.im));
+  } else {
+    constexpr double K = g5_cos64(E) / g5_sin64(E);
+    return mk(fma(K, z.re, z.im), fma(K, z.im, -z.re));
+  }
+}
+// k * x + y, folding k = +-1 to an add / subtract
+SLSE_D cplx g5_fmac(double k, cplx x, cplx y) {
+  if (k == 1.0) return cadd(y, x);
+  if (k == -1.0) return csub(y, x);
+  return mk(fma(k, x.re, y.re), fma(k, x.im, y.im));
+}
+SLSE_D double g5_fmar(double k, double x, double y) {
+  if (k == 1.0) return y + x;
+  if (k == -1.0) return y - x;
+  return fma(k, x, y);
+}
+// radix-4 (forward) of (a, W^EB b, W^EC c, W^ED d); results y0..y3 in a..d
+template <int EB, int EC, int ED>
+SLSE_D void g5_r4(cplx& a, cplx& b, cplx& c, cplx& d) {
+  constexpr double sb = g5_sigma(EB), sc = g5_sigma(EC), sd = g5_sigma(ED);
+  constexpr double rr = sd / sb;
+  const cplx qb = g5_q<EB>(b), qc = g5_q<EC>(c), qd = g5_q<ED>(d);
+  const cplx s0 = g5_fmac(sc, qc, a), d0 = g5_fmac(-sc, qc, a);
+  const cplx s1 = g5_fmac(rr, qd, qb), d1 = g5_fmac(-rr, qd, qb);
+  a = g5_fmac(sb, s1, s0);
+  c = g5_fmac(-sb, s1, s0);
+  b = mk(g5_fmar(sb, d1.im, d0.re), g5_fmar(-sb, d1.re, d0.im));  // d0 - i sb d1
+  d = mk(g5_fmar(-sb, d1.im, d0.re), g5_fmar(sb, d1.re, d0.im));  // d0 + i sb d1
+}
+template <int R>
+SLSE_D void dft16_t(cplx* v) {
+  // stage 1: radix-4 over n2 for each n1 (inputs v[n1 + 4 n2]), twiddles W64^{4 n2 R}
+#pragma unroll
+  for (int n1 = 0; n1 < 4; ++n1) g5_r4<4 * R, 8 * R, 12 * R>(v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]);
+  // now v[n1 + 4 k2] = Z[n1][k2]; stage 2: radix-4 over n1 for each k2
+  g5_r4<1 * (0 + R), 2 * (0 + R), 3 * (0 + R)>(v[0], v[1], v[2], v[3]);
+  g5_r4<1 * (4 + R), 2 * (4 + R), 3 * (4 + R)>(v[4], v[5], v[6], v[7]);
+  g5_r4<1 * (8 + R), 2 * (8 + R), 3 * (8 + R)>(v[8], v[9], v[10], v[11]);
+  g5_r4<1 * (12 + R), 2 * (12 + R), 3 * (12 + R)>(v[12], v[13], v[14], v[15]);
+  // v[4 k2 + k1] = X[4 k1 + k2]
+}
+// output index of bin k after dft16_t
+SLSE_HD constexpr int g5_pos(int k) { return 4 * (k & 3) + (k >> 2); }
+
 constexpr int kG5Threads = 192;
 constexpr int kG5Warps = kG5Threads / 32;
 constexpr int kG5Row = 17;                    // exchange row stride (complex) per a
-constexpr int kG5Buf = 64 * kG5Row;           // one signal's exchange buffer
+constexpr int kG5Buf = 64 * kG5Row + 4;       // one signal's exchange buffer (+4: A0 / A1 rows of one a land in different bank groups)
 SLSE_HD constexpr size_t g5_smem_bytes(int n) {
   // mbarriers (128 B) | 2 stages of (w, rho) (2 x 2 n cplx) | X (3 buffers)
   return 128 + 2 * 2 * 16 * (size_t)n + 3 * 16 * (size_t)kG5Buf;
@@ -148,15 +228,22 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
     if ((int)blockIdx.x < B) issue(blockIdx.x, 0);
     if ((int)blockIdx.x + G < B) issue(blockIdx.x + G, 1);
   }
-  // inner-pass role (fixed for the kernel's lifetime)
-  const int ic = warp >> 1;                          // 0: w, 1: rho, 2: n rho
-  const int t = lane & 15;
-  const int r = 2 * (warp & 1) + (lane >> 4);         // residue 0..3
+  // inner-pass role (fixed for the kernel's lifetime): warps 0-3 run residue
+  // r = warp for w (lanes 0-15) and rho (lanes 16-31), warp-uniform so the
+  // pre-twiddles fold into the DFT's compile-time twiddles; warps 4-5 run
+  // n rho with r = 2 (warp - 4) + lane / 16 (selected constants)
+  const bool ia1 = warp >= 4;
+  const int h = lane >> 4, t = lane & 15;
+  const int r = ia1 ? 2 * (warp - 4) + h : warp;
+  const int ic = ia1 ? 2 : h;                        // 0: w, 1: rho (A0), 2: n rho (A1)
   cplx* Xi = X + ic * kG5Buf;
+  const double dt = (double)t;
   // outer-pass role
-  const bool oq = warp < 2;
-  const int oa = oq ? tid : (tid - 64) >> 1;          // a = 0..63
-  const int oe = oq ? 0 : ((tid - 64) & 1);           // A-pair member: 0 -> A0, 1 -> A1
+  // (q^G goes to warps 4-5, whose inner pass is the heaviest: balances the
+  // per-problem work of the six warps between barriers to within ~3 %)
+  const bool oq = warp >= 4;
+  const int oa = oq ? tid - 128 : tid >> 1;           // a = 0..63
+  const int oe = oq ? 0 : (tid & 1);                  // A-pair member: 0 -> A0, 1 -> A1
   const cplx* Xo = X + (oq ? 0 : 1 + oe) * kG5Buf + oa * kG5Row;
   // middle twiddles W1024^{t a}, t = 0..15: fixed per thread, recomputed per
   // problem from two table entries (keeps registers for the transform)
@@ -177,16 +264,23 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
       const int i = t + 16 * s;
       v[s] = i < n ? src[i] : mk(0.0, 0.0);
     }
-    if (ic == 2) {
+    if (ia1) {
 #pragma unroll
-      for (int s = 0; s < 16; ++s) v[s] = cscale(v[s], (double)(t + 16 * s));
+      for (int s = 0; s < 16; ++s) v[s] = cscale(v[s], dt + (double)(16 * s));
+      if (warp == 4) g5_pretwiddle<0>(v, h);
+      else g5_pretwiddle<1>(v, h);
+      dft16_t<0>(v);
+    } else {
+      switch (warp) {  // Y(t, r + 4 a') = v[g5_pos(a')]
+        case 0: dft16_t<0>(v); break;
+        case 1: dft16_t<1>(v); break;
+        case 2: dft16_t<2>(v); break;
+        default: dft16_t<3>(v); break;
+      }
     }
-    if (warp & 1) g5_pretwiddle<1>(v, lane >> 4);
-    else g5_pretwiddle<0>(v, lane >> 4);
-    dft_dif<16>(v, -1.0);  // Y(t, r + 4 a') = v[brev(a')]
     if (k) mbar_wait(xfree, (k - 1) & 1);  // everyone has read problem k-1's X
 #pragma unroll
-    for (int a2 = 0; a2 < 16; ++a2) Xi[(r + 4 * a2) * kG5Row + t] = v[brev_const(a2, 16)];
+    for (int a2 = 0; a2 < 16; ++a2) Xi[(r + 4 * a2) * kG5Row + t] = v[g5_pos(a2)];
     __syncthreads();
     if (tid == 0 && p + 2 * G < B) issue(p + 2 * G, st);
     // ---- outer pass: Y(t, a) W1024^{t a}, DFT16 over t
@@ -206,12 +300,12 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
         v[tt + 1] = cmul(v[tt + 1], po);
       }
     }
-    dft_dif<16>(v, -1.0);  // bin l = a + 64 b is v[brev(b)]
+    dft16_t<0>(v);  // bin l = a + 64 b is v[g5_pos(b)]
     if (oq) {
       double2* qg = (double2*)(q_grid + (size_t)p * L);
 #pragma unroll
       for (int b = 0; b < 16; ++b) {
-        const cplx o = v[brev_const(b, 16)];
+        const cplx o = v[g5_pos(b)];
         __stcs(&qg[oa + 64 * b], make_double2(o.re, o.im));
       }
     } else {
@@ -221,7 +315,7 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
       double* sg = s_grid + (size_t)p * L;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const cplx lo = v[brev_const(j, 16)], hi = v[brev_const(j + 8, 16)];
+        const cplx lo = v[g5_pos(j)], hi = v[g5_pos(j + 8)];
         const cplx mine = oe ? hi : lo, give = oe ? lo : hi;
         cplx got;
         got.re = __shfl_xor_sync(0xffffffffu, give.re, 1);
