@@ -104,16 +104,28 @@ cudaError_t set_smem(KernelT kernel, size_t bytes) {
 namespace {
 // threads per solver CTA: small N run one warp per problem (no block-wide
 // barriers; many problems resident per SM); SLSE_SOLVER_NT overrides.
-int solver_threads(int n) {
+// Two 256-thread solver CTAs per SM ("paired") when the batch has more
+// problems than SMs and the per-problem shared region fits in half an SM:
+// measured on B200 (tools/occ_exp.sh) cfg3 181 -> 130 ms, cfg4 1.00 -> 0.82 s;
+// with B <= SMs (cfg5) one 512-thread CTA per problem stays faster.
+constexpr size_t kPairRegion = 100 * 1024;
+bool solver_paired(int n, int B) {
+  if (getenv("SLSE_NO_PAIR")) return false;
+  const bool dnc = n >= dnc_min_n();
+  if (n <= 512 || B <= sm_count()) return false;
+  return dnc || 48 * (size_t)n <= kPairRegion;
+}
+
+int solver_threads(int n, int B) {
   const char* env = getenv("SLSE_SOLVER_NT");
   if (env) {
     int v = atoi(env);
     if (v == 32 || v == 64 || v == 128 || v == 256 || v == 512 || v == 1024) return v;
   }
   if (n <= 512) return 32;    // cfg1-2: measured 68 ms (32) vs 113 ms (256) per 4096 x N=256 batch
+  if (solver_paired(n, B)) return 256;
   if (n <= 2048) return 256;  // cfg3: 167 ms (256) vs 205 (128) / 236 (512) per 1024 x N=1024
-  if (n <= 4096) return 512;  // cfg4: 1.44 s (512) vs 1.48 (1024) / 1.78 (256) per 256 x N=4096
-  return 512;                 // cfg5 (superfast): 8.8 s (512) vs 13.1 (1024) / 12 (128) per 64 x N=16384
+  return 512;                 // cfg4/5 with B <= SMs (superfast): 8.8 s (512) vs 13.1 (1024) / 12 (128) at cfg5
 }
 
 // Warp mode: the one-warp solvers run W per CTA (one CTA per SM) with a
@@ -136,8 +148,8 @@ int grid_size_for_solver(int n, int G, int B, const slse_options& o, size_t* sla
   SolveParams P = make_params(n, o);
   P.dnc = n >= dnc_min_n() ? 1 : 0;
   P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
-  const int nt = solver_threads(n);
-  SmemPlan plan = smem_plan(n, P.L, nt, P.dnc != 0);
+  const int nt = solver_threads(n, B);
+  SmemPlan plan = smem_plan(n, P.L, nt, P.dnc != 0, (nt == 256 && solver_paired(n, B)) ? kPairRegion : 0);
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {  // one slab per warp of every CTA
     int ctas = (B + W - 1) / W;
@@ -606,7 +618,7 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
   cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(int), st);
   if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
   char* ws = (char*)workspace + 256;
-  const int nt = solver_threads(N);
+  const int nt = solver_threads(N, B);
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {
     // twiddle table in shared memory when it fits next to the W regions

@@ -15,6 +15,9 @@
 using namespace slse;
 
 // min resident CTAs per SM for the one-warp solver (caps registers)
+#ifndef SLSE_SOLVER_MINB_WIDE
+#define SLSE_SOLVER_MINB_WIDE (NT == 256 ? 2 : 1)  // NT = 256 runs two CTAs per SM (solver_paired)
+#endif
 #ifndef SLSE_SOLVER_MINB32
 #define SLSE_SOLVER_MINB32 16
 #endif
@@ -45,12 +48,13 @@ struct SmemPlan {
   size_t bytes;
 };
 
-inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false) {
+inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false, size_t region_budget = 0) {
   SmemPlan p;
   // one-warp solvers: keep the region small so more problems stay resident
   // (only the recursion and the 2N-point transforms are staged; the grid's
-  // L-point transforms then run from L1/L2)
-  size_t budget = kRegionBudget;
+  // L-point transforms then run from L1/L2); paired 256-thread solvers get
+  // half an SM (region_budget)
+  size_t budget = region_budget ? region_budget : kRegionBudget;
   if (nt <= 32 && !dnc) {
     const char* env = getenv("SLSE_WARP_REGION_KB");
     budget = env ? (size_t)atoi(env) * 1024 : 48 * (size_t)n;
@@ -119,7 +123,7 @@ SLSE_D ProbOut prob_out(const slse_outputs& out, const SolveParams& P, int p) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : 1)) solve_kernel(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
+__global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : SLSE_SOLVER_MINB_WIDE)) solve_kernel(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
                                                    int B, slse_outputs out, char* ws, size_t slab_bytes,
                                                    int* queue, const cplx* tw, int twlog, int fft_cap,
                                                    int rec_smem) {
