@@ -34,13 +34,20 @@ int fail_arg(const char* what) {
 bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
 // ---------------------------------------------------------------- twiddles
+// level-major table (slse_fft.cuh tw_index): entry 2^l + k = exp(-2 pi i k / 2^l)
 __global__ void tw_fill_kernel(cplx* tw, int lg) {
-  const int n = 1 << lg;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+  const int n = (int)tw_entries(lg);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (i == 0) {
+      tw[0] = mk(1.0, 0.0);  // unused slot
+      continue;
+    }
+    const int l = 31 - __clz(i);
+    const int k = i - (1 << l);
     double s, c;
-    // exp(-2 pi i k / n); k/n exact (power of two)
-    sincospi(2.0 * ((double)k / (double)n), &s, &c);
-    tw[k] = mk(c, -s);
+    // k / 2^l exact (power of two)
+    sincospi(2.0 * ((double)k / (double)(1 << l)), &s, &c);
+    tw[i] = mk(c, -s);
   }
 }
 
@@ -62,7 +69,7 @@ int twiddles(int need_lg, cudaStream_t st, const cplx** out, int* out_lg) {
   if (t.ptr == nullptr || t.lg < need_lg) {
     const int lg = need_lg > kMinTwLog ? need_lg : kMinTwLog;
     cplx* p = nullptr;
-    e = cudaMalloc(&p, sizeof(cplx) << lg);
+    e = cudaMalloc(&p, sizeof(cplx) * tw_entries(lg));
     if (e != cudaSuccess) return fail("cudaMalloc(twiddles)", e);
     tw_fill_kernel<<<256, 256, 0, st>>>(p, lg);
     e = cudaGetLastError();
@@ -625,7 +632,7 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const size_t base = kCfBytes + (size_t)W * wsm, twb = sizeof(cplx) << twlog;
+    const size_t base = kCfBytes + (size_t)W * wsm, twb = sizeof(cplx) * tw_entries(twlog);
     const int tw_smem = (!getenv("SLSE_TW_GLOBAL") && base + twb <= (size_t)optin) ? 1 : 0;
     e = slse_solve_warps_launch(W, g / W, base + (tw_smem ? twb : 0), st, P, cft, (const cplx*)y, B, *out, ws, slab,
                                 queue, tw, twlog, plan.fft_cap, plan.rec_in_smem, wsm, tw_smem);

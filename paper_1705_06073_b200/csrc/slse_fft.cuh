@@ -12,8 +12,8 @@
 // passes run there; otherwise they run in place in a global work buffer
 // (L2-resident at these sizes).
 //
-// Twiddles come from a device table tw[k] = exp(-2 pi i k / TW), TW = 2^twlog,
-// filled once per launch with sincospi (exact at the quarter points).
+// Twiddles come from a level-major device table (tw_index below), filled
+// once per device with sincospi (exact at the quarter points).
 #pragma once
 #include "slse_port.cuh"
 
@@ -48,15 +48,24 @@ SLSE_D unsigned brev_bits(unsigned i, int p) {
 #endif
 }
 
-// twiddle exp(sign * 2 pi i k / 2^lg) from a table of 2^twlog entries
+// Level-major twiddle table (levels lg = 0..twlog, 2^(twlog+1) entries):
+// entry 2^lg + k holds exp(-2 pi i k / 2^lg), k < 2^lg.  The twiddles of one
+// transform size are contiguous, so a pass's lookups stay within a few L1
+// lines (a single full-circle table at stride 2^(twlog - lg) puts every
+// twiddle of a large pass in its own line).
+SLSE_HD size_t tw_index(int k, int lg) { return ((size_t)1 << lg) + (size_t)k; }
+SLSE_HD size_t tw_entries(int twlog) { return (size_t)2 << twlog; }
+
+// twiddle exp(sign * 2 pi i k / 2^lg), k < 2^lg <= 2^twlog
 SLSE_D cplx twid_tab(const cplx* __restrict__ tw, int twlog, int k, int lg, double sign) {
-  cplx t = tw[(size_t)k << (twlog - lg)];
+  (void)twlog;
+  cplx t = tw[tw_index(k, lg)];
   if (sign > 0) t.im = -t.im;
   return t;
 }
 
 SLSE_D cplx twid(const FftCtx& f, int k, int lg, double sign) {
-  cplx t = f.tw[(size_t)k << (f.twlog - lg)];
+  cplx t = f.tw[tw_index(k, lg)];
   if (sign > 0) t.im = -t.im;
   return t;
 }

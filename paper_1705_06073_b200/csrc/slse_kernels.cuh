@@ -173,13 +173,13 @@ __global__ void __launch_bounds__(32 * W, 16 / W) solve_kernel_warps(SolveParams
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CfTable* cf = (CfTable*)smem_raw;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // optional CTA-shared copy of the twiddle table (tw_smem: 1 = 2^twlog entries)
+  // optional CTA-shared copy of the twiddle table (tw_smem: 1 = all tw_entries(twlog))
   cplx* tws = (cplx*)(smem_raw + kCfBytes);
-  const size_t tw_bytes = tw_smem ? ((sizeof(cplx) << twlog)) : 0;
+  const size_t tw_bytes = tw_smem ? sizeof(cplx) * tw_entries(twlog) : 0;
   unsigned char* mine = smem_raw + kCfBytes + tw_bytes + (size_t)warp * warp_smem;
   if (threadIdx.x == 0) *cf = cft;
   if (tw_smem)
-    for (int i = threadIdx.x; i < (1 << twlog); i += blockDim.x) tws[i] = tw[i];
+    for (int i = threadIdx.x; i < (int)tw_entries(twlog); i += blockDim.x) tws[i] = tw[i];
   __syncthreads();
   if (tw_smem) tw = tws;
   Blk b;
@@ -802,7 +802,8 @@ SLSE_D cplx ldg_c(const cplx* p) {
   return mk(d.x, d.y);
 }
 SLSE_D cplx twl(const cplx* __restrict__ tw, int twlog, int k, int lg) {
-  return ldg_c(&tw[(size_t)k << (twlog - lg)]);
+  (void)twlog;
+  return ldg_c(&tw[tw_index(k, lg)]);
 }
 
 // in: v[t] = x[lane + 32 t]; out: v[4 j + k1b] = X[k2 + 8 (q + 4 j) + 64 k1b],

@@ -16,14 +16,15 @@
 
 using namespace slse;
 
+// level-major layout, as the device table (slse_fft.cuh tw_index)
 static std::vector<cplx> make_twiddles(int lg) {
-  const int n = 1 << lg;
-  std::vector<cplx> tw(n);
-  for (int k = 0; k < n; ++k) {
-    double s, c;
-    sincos2pi((double)k / (double)n, &s, &c);
-    tw[k] = mk(c, -s);
-  }
+  std::vector<cplx> tw(tw_entries(lg), mk(1.0, 0.0));
+  for (int l = 0; l <= lg; ++l)
+    for (int k = 0; k < (1 << l); ++k) {
+      double s, c;
+      sincos2pi((double)k / (double)(1 << l), &s, &c);
+      tw[tw_index(k, l)] = mk(c, -s);
+    }
   return tw;
 }
 

@@ -43,12 +43,14 @@ __global__ void __launch_bounds__(512, 1) micro_kernel(const cplx* rho_all, cons
   if (lane == 0) out[prob] = acc;
 }
 
+// level-major table (slse_fft.cuh tw_index), T = tw_entries(twlog) entries
 __global__ void tw_fill(cplx* tw, int T) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < T) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > 0 && i < T) {
+    const int l = 31 - __clz(i), k = i - (1 << l);
     double s, c;
-    sincospi(-2.0 * k / T, &s, &c);
-    tw[k] = mk(c, s);
+    sincospi(-2.0 * k / (double)(1 << l), &s, &c);
+    tw[i] = mk(c, s);
   }
 }
 
@@ -58,7 +60,7 @@ int main(int argc, char** argv) {
   const int reps = argc > 3 ? atoi(argv[3]) : 8;
   const int ctas = 148 * 16 / W, B = ctas * W;
   const int nf = 1 << ilog2(2 * n);
-  const int twlog = 10, T = 1 << twlog;
+  const int twlog = 10, T = (int)tw_entries(twlog);
   std::vector<cplx> h((size_t)B * nf);
   srand(1);
   for (auto& v : h) v = mk(rand() / (double)RAND_MAX - 0.5, rand() / (double)RAND_MAX - 0.5);
