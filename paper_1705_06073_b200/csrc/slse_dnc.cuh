@@ -211,6 +211,20 @@ SLSE_D DncNode dnc_node(cplx* base, int s) {
   return d;
 }
 
+// Theta is J-para-unitary: every factor M_k = [[1, k z], [conj(k), z]]
+// satisfies Theta_21 = Theta_12^# and Theta_22 = Theta_11^#, where
+// p^#(z) = z^s conj(p(1 / conj z)) reverses and conjugates the s + 1
+// coefficients (s steps, degree s).  So only row 1 of a product is
+// computed; row 2 is this O(s) reversal (and, for spectra, W^{s k} conj).
+SLSE_D void dnc_fill_row2(cplx* T, int s, Blk& b) {
+  const int ld = s + 1;
+  for (int i = b.tid; i < ld; i += b.nt) {
+    T[2 * ld + i] = conjg(T[ld + (s - i)]);
+    T[3 * ld + i] = conjg(T[s - i]);
+  }
+  fft_barrier();
+}
+
 struct DncFrame {
   const cplx* E;
   const cplx* Bw;
@@ -257,29 +271,50 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         cplx* E2 = d.E2;
         cplx* B2 = d.B2;
         const int ne = s - h + 1, nb = s - h;
-        if (4 * l1 + 2 * s + 1 <= X.f.smem_cap) {  // operands to shared memory (latency)
+        if (4 * l1 + 2 * s + 2 <= X.f.smem_cap) {  // operands to shared memory (latency)
           cplx* sT = X.f.smem;
           cplx* sE = sT + 4 * l1;
           cplx* sB = sE + (s + 1);
           for (int i = tid; i < 4 * l1; i += nt) sT[i] = T1[i];
           for (int i = tid; i <= s; i += nt) sE[i] = E[i];
-          for (int i = tid; i < s; i += nt) sB[i] = Bw[i];
+          for (int i = tid; i <= s; i += nt) sB[i] = i < s ? Bw[i] : mk(0.0, 0.0);  // b_s := 0 (no bound test)
           fft_barrier();
-          T1 = sT;
-          E = sE;
-          Bw = sB;
-        }
-        for (int t = tid; t < ne + nb; t += nt) {
-          const bool isE = t < ne;
-          const int j = isE ? t : t - ne;
-          const cplx* A = T1 + (isE ? 0 : 2 * l1);  // T11,T12 or T21,T22
-          cplx acc = mk(0.0, 0.0);
-          for (int i = 0; i < l1; ++i) {
-            const int k = h + j - i;  // 0 <= k <= s
-            acc = cadd(acc, cmul(A[i], E[k]));
-            if (k < s) acc = cadd(acc, cmul(A[l1 + i], Bw[k]));
+          // four interleaved partial sums: the FMA chain is a quarter as deep
+          for (int t = tid; t < ne + nb; t += nt) {
+            const bool isE = t < ne;
+            const int j = isE ? t : t - ne;
+            const cplx* A = sT + (isE ? 0 : 2 * l1);  // T11,T12 or T21,T22
+            const cplx* Ek = sE + h + j;              // Ek[-i] = e_{h+j-i}
+            const cplx* Bk = sB + h + j;
+            cplx acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+            int i = 0;
+            for (; i + 4 <= l1; i += 4) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                acc[u] = cadd(acc[u], cmul(A[i + u], Ek[-(i + u)]));
+                acc[u] = cadd(acc[u], cmul(A[l1 + i + u], Bk[-(i + u)]));
+              }
+            }
+            for (; i < l1; ++i) {
+              acc[0] = cadd(acc[0], cmul(A[i], Ek[-i]));
+              acc[0] = cadd(acc[0], cmul(A[l1 + i], Bk[-i]));
+            }
+            const cplx r = cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3]));
+            if (isE) E2[j] = r; else B2[j] = r;
           }
-          if (isE) E2[j] = acc; else B2[j] = acc;
+        } else {
+          for (int t = tid; t < ne + nb; t += nt) {
+            const bool isE = t < ne;
+            const int j = isE ? t : t - ne;
+            const cplx* A = T1 + (isE ? 0 : 2 * l1);  // T11,T12 or T21,T22
+            cplx acc = mk(0.0, 0.0);
+            for (int i = 0; i < l1; ++i) {
+              const int k = h + j - i;  // 0 <= k <= s
+              acc = cadd(acc, cmul(A[i], E[k]));
+              if (k < s) acc = cadd(acc, cmul(A[l1 + i], Bw[k]));
+            }
+            if (isE) E2[j] = acc; else B2[j] = acc;
+          }
         }
         fft_barrier();
         if (prof) X.prof[1] += dnc_clock() - t0;
@@ -300,7 +335,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         T1 = s1;
         T2 = s2;
       }
-      const int nrow = cf.row1 ? 2 : 4;  // output blocks (row 1 only on the right spine)
+      const int nrow = 2;  // row 1 only; row 2 by dnc_fill_row2 (not needed on the right spine)
       for (int t = tid; t < nrow * ld; t += nt) {
         const int q = t / ld, k = t - q * ld;
         const int r = q >> 1, c = q & 1;
@@ -310,14 +345,24 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         const cplx* B2p = T1 + (2 + c) * l1;
         const int lo = k - h > 0 ? k - h : 0;
         const int hi = k < l2 - 1 ? k : l2 - 1;
-        cplx acc = mk(0.0, 0.0);
-        for (int i = lo; i <= hi; ++i) {
-          acc = cadd(acc, cmul(A1[i], B1[k - i]));
-          acc = cadd(acc, cmul(A2[i], B2p[k - i]));
+        cplx acc4[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+        int i = lo;
+        for (; i + 4 <= hi + 1; i += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc4[u] = cadd(acc4[u], cmul(A1[i + u], B1[k - i - u]));
+            acc4[u] = cadd(acc4[u], cmul(A2[i + u], B2p[k - i - u]));
+          }
         }
+        for (; i <= hi; ++i) {
+          acc4[0] = cadd(acc4[0], cmul(A1[i], B1[k - i]));
+          acc4[0] = cadd(acc4[0], cmul(A2[i], B2p[k - i]));
+        }
+        const cplx acc = cadd(cadd(acc4[0], acc4[1]), cadd(acc4[2], acc4[3]));
         T[t] = acc;
       }
       fft_barrier();
+      if (!cf.row1) dnc_fill_row2(T, s, b);
       if (prof) X.prof[2] += dnc_clock() - t0;
       --sp;
       continue;
@@ -328,14 +373,26 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       const cplx* E = cf.E;
       const cplx* Bw = cf.Bw;
       cplx* S = d.S;  // S[0..3] = spectra of T1, S[4] = E, S[5] = Bw (contiguous: S, SE, SB)
-      // six forward transforms in one batch (SE, SB follow S contiguously)
-      fft_multi(d.work_multi, 6, F, -1.0,
+      // four forward transforms in one batch (T11, T12, E, Bw); the spectra
+      // of T21 = T12^#, T22 = T11^# (degree h) follow as W^{h k} conj(.)
+      const cplx* SEw = d.SE;
+      fft_multi(d.work_multi, 4, F, -1.0,
                 [=](int q, int i) {
-                  if (q < 4) return i < l1 ? T1[q * l1 + i] : mk(0.0, 0.0);
-                  if (q == 4) return i <= s ? E[i] : mk(0.0, 0.0);
+                  if (q < 2) return i < l1 ? T1[q * l1 + i] : mk(0.0, 0.0);
+                  if (q == 2) return i <= s ? E[i] : mk(0.0, 0.0);
                   return i < s ? Bw[i] : mk(0.0, 0.0);
                 },
-                [=](int q, int i, cplx v) { S[(size_t)q * F + i] = v; }, X.f, b);
+                [=](int q, int i, cplx v) { (q < 2 ? S + (size_t)q * F : (cplx*)SEw + (size_t)(q - 2) * F)[i] = v; },
+                X.f, b);
+      {
+        const int lgF = ilog2(F);
+        for (int k = b.tid; k < F; k += b.nt) {
+          const cplx wk = twid_tab(X.f.tw, X.f.twlog, (int)(((long long)h * k) & (F - 1)), lgF, -1.0);
+          S[2 * (size_t)F + k] = cmul(wk, conjg(S[(size_t)F + k]));
+          S[3 * (size_t)F + k] = cmul(wk, conjg(S[k]));
+        }
+        fft_barrier();
+      }
       const cplx* SE = d.SE;
       const cplx* SB = d.SB;
       cplx* E2 = d.E2;
@@ -370,9 +427,9 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       const cplx* T2 = d.T2;
       cplx* A = d.above;            // 4 F : spectra of T2
       cplx* wk = d.above + 4 * (size_t)F;  // 4 F global work
-      // row-1 nodes (root and right spine) only need Theta_11, Theta_12,
-      // hence only T2's first row: 2 + 2 transforms instead of 4 + 4
-      const int nq = cf.row1 ? 2 : 4;
+      // only row 1 of the product is transformed (2 + 2 transforms instead
+      // of 4 + 4); row 2 follows by symmetry, skipped on the right spine
+      const int nq = 2;  // row 1 of T2 and of the product; row 2 by dnc_fill_row2
       fft_multi(wk, nq, F, -1.0, [=](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
                 [=](int q, int i, cplx v) { A[(size_t)q * F + i] = v; }, X.f, b);
       const cplx* S = d.S;
@@ -386,6 +443,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
                               cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
                 },
                 [=](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
+      if (!cf.row1) dnc_fill_row2(T, s, b);
       if (prof) {
         const long long dt = dnc_clock() - t0;
         X.prof[4] += dt;
