@@ -135,7 +135,7 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
       const cplx ej1 = shfl_c(ej, 1), bj1 = shfl_c(bj, 1);
       const cplx kc = conjg(k);
       const double dn = d * (1.0 - (k.re * k.re + k.im * k.im));
-      const double invn = 1.0 / dn;
+      const double invn = __drcp_rn(dn);  // == 1.0 / dn (both correctly rounded)
       const cplx enext = cadd(ej1, cmul(k, bj1));
       const cplx knext = mk(-enext.re * invn, -enext.im * invn);
       const cplx en = cadd(ej, cmul(k, bj));
@@ -143,15 +143,17 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
       ej = shfl_down_c(en, 1);
       bj = bn;
       // Theta <- M_k Theta : T1x[i] += k T2x[i-1] ; T2x[i] = conj(k) T1x[i] + T2x[i-1]
+      if (t == 31) {  // coefficient 32 (x*) is zero until the 32nd step: only then does 31 feed it
+        const cplx l21 = shfl_c(t21, 31), l22 = shfl_c(t22, 31);
+        const cplx m11 = cadd(x11, cmul(k, l21)), m12 = cadd(x12, cmul(k, l22));
+        const cplx m21 = cadd(cmul(kc, x11), l21), m22 = cadd(cmul(kc, x12), l22);
+        x11 = m11; x12 = m12; x21 = m21; x22 = m22;
+      }
       const cplx p21 = shfl_up_c(t21, 1), p22 = shfl_up_c(t22, 1);
-      const cplx l21 = shfl_c(t21, 31), l22 = shfl_c(t22, 31);  // coefficient 31 feeds 32
       const cplx q21 = lane ? p21 : mk(0.0, 0.0), q22 = lane ? p22 : mk(0.0, 0.0);
       const cplx n11 = cadd(t11, cmul(k, q21)), n12 = cadd(t12, cmul(k, q22));
       const cplx n21 = cadd(cmul(kc, t11), q21), n22 = cadd(cmul(kc, t12), q22);
-      const cplx m11 = cadd(x11, cmul(k, l21)), m12 = cadd(x12, cmul(k, l22));
-      const cplx m21 = cadd(cmul(kc, x11), l21), m22 = cadd(cmul(kc, x12), l22);
       t11 = n11; t12 = n12; t21 = n21; t22 = n22;
-      x11 = m11; x12 = m12; x21 = m21; x22 = m22;
       d = dn;
       if (lane == 0) dtmp[t + 1] = d;
       if (!(d > floor_)) { st = kNotPD; break; }
