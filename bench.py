@@ -278,9 +278,14 @@ def run_ours(args):
     attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg_bytes, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
     kname = ("grid_tma_kernel" if (L == 1024 and 128 < n <= 256) else "grid_fused_kernel") + \
         " (activation grid, SURVEY 8(a) row 9)"
+    traffic = None  # DRAM bytes per launch from the committed ncu capture of this kernel and shape
+    tf = os.path.join(REPO, "profiles", "r1_grid_tma_cfg2.json")
+    if kname.startswith("grid_tma_kernel") and cfg == 2 and os.path.exists(tf):
+        with open(tf) as fh:
+            traffic = json.load(fh)["traffic_bytes_per_launch"] * B // 4096
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-            "traffic": None, "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
+            "traffic": traffic, "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
             "launch_ms": grid_ms, "flops_per_launch": flops,
             "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "peak_source": "measured DFMA loop",
                      "frac": fp64_tf / fp64_peak, "attainable_tflops": attainable,
