@@ -18,6 +18,8 @@ build's scope and raise.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -280,13 +282,34 @@ class BatchSolver:
             ctypes.c_size_t(self.workspace.numel()), ctypes.c_void_p(st.cuda_stream))
         _native.check(rc, "slse_estimate_batch_mmv")
 
+    def _d2h(self, tensors: dict) -> dict:
+        """Asynchronous copies into this solver's pinned staging (allocated
+        once, sized for every output), one stream sync, then host copies the
+        caller owns (the staging is reused by the next call)."""
+        torch = _torch()
+        st = torch.cuda.current_stream(self.device)
+        if getattr(self, "_pinned", None) is None:
+            total = sum(t.numel() * t.element_size() for t in vars(self.out).values() if isinstance(t, torch.Tensor))
+            self._pinned = torch.empty(total + 64 * 32, dtype=torch.uint8, pin_memory=True)
+        off = 0
+        host = {}
+        for name, t in tensors.items():
+            t = t.contiguous()
+            nb = t.numel() * t.element_size()
+            hb = self._pinned[off:off + nb].view(t.dtype).view(t.shape)
+            hb.copy_(t, non_blocking=True)
+            host[name] = hb
+            off += (nb + 63) // 64 * 64
+        st.synchronize()
+        return {name: hb.numpy().copy() for name, hb in host.items()}
+
     def host_outputs(self) -> dict:
         """Host copies, trimmed to the longest trace / history / model order
-        in the batch (one small D2H for the counts, then the used prefixes)."""
-        torch = _torch()
+        in the batch (one small D2H for the counts, then the used prefixes;
+        two stream syncs in all)."""
         small = ("k_hat", "status", "iterations", "flags", "beta", "zeta", "n_trace", "n_events", "counters",
                  "stage_seconds")
-        h = {name: getattr(self.out, name).cpu().numpy() for name in small}
+        h = self._d2h({name: getattr(self.out, name) for name in small})
         kk = max(1, int(h["k_hat"].max(initial=0)))
         tt = max(1, int(h["n_trace"].max(initial=0)))
         ee = max(1, int(h["n_events"].max(initial=0)))
@@ -294,9 +317,7 @@ class BatchSolver:
         big = {"theta": o.theta[:, :kk], "gamma": o.gamma[:, :kk], "alpha": o.alpha[:, :, :kk], "slot": o.slot[:, :kk],
                "trace": o.trace[:, :tt], "stage": o.stage[:, :tt], "trace_k": o.trace_k[:, :tt],
                "events": o.events[:, :ee]}
-        for name, t in big.items():
-            h[name] = t.contiguous().cpu().numpy()
-        del torch
+        h.update(self._d2h(big))
         return h
 
     def results(self):
@@ -345,6 +366,28 @@ class BatchResult:
         return iter(self._all())
 
 
+_SOLVERS = threading.local()
+
+
+def _cached_solver(n, batch, opts, device, g):
+    """BatchSolver reuse across calls of one thread (device buffers and the
+    workspace are sized by (N, B, G, options, device)); results are host
+    copies, so reuse by sequential calls is safe."""
+    torch = _torch()
+    opts = opts or EstimatorOptions()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (n, batch, g, dataclasses.astuple(opts), str(dev))
+    cache = getattr(_SOLVERS, "cache", None)
+    if cache is None:
+        cache = _SOLVERS.cache = {}
+    s = cache.get(key)
+    if s is None:
+        if len(cache) >= 4:
+            cache.pop(next(iter(cache)))
+        s = cache[key] = BatchSolver(n, batch, opts, device=dev, g=g)
+    return s
+
+
 def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False) -> BatchResult:
     """Solve B independent complete-data problems, y: (B, N) complex, or
     (B, G, N) for G snapshots per problem sharing the frequencies (MMV).
@@ -361,10 +404,12 @@ def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=
     g = 1 if yt.dim() == 2 else int(yt.shape[1])
     if yt.dim() == 3 and g == 1:
         yt = yt[:, 0]
-    solver = BatchSolver(int(yt.shape[-1]), int(yt.shape[0]), opts, device=device, g=g)
-    if yt.device.type == "cpu" and not yt.is_pinned():
-        yt = yt.pin_memory()
-    ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=True).contiguous()
+    solver = _cached_solver(int(yt.shape[-1]), int(yt.shape[0]), opts, device, g)
+    # pinned input (e.g. a torch.Tensor from pin_memory()) goes up
+    # asynchronously; pageable numpy memory is copied by the driver directly
+    # (cheaper than page-locking it for one transfer)
+    pinned = yt.device.type == "cpu" and yt.is_pinned()
+    ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=pinned).contiguous()
     solver.solve(ydev)
     res = BatchResult(solver.host_outputs())
     return (res, solver) if return_solver else res
