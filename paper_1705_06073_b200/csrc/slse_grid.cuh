@@ -247,9 +247,9 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
   const cplx* Xo = X + (oq ? 0 : 1 + oe) * kG5Buf + oa * kG5Row;
   // middle twiddles W1024^{t a}, t = 0..15: fixed per thread, recomputed per
   // problem from two table entries (keeps registers for the transform)
-  const cplx wa = twid_tab(tw, twlog, oa, 10, -1.0);
-  const cplx wa2 = twid_tab(tw, twlog, 2 * oa, 10, -1.0);
-  const double c2n = 2.0 - (double)n;
+  // (W1024^a, W1024^2a are re-read from the L1-resident table every problem
+  // rather than held in registers across the loop: 96 registers, no spills)
+  const cplx* twa = tw + tw_index(oa, 10);
 
   int p = blockIdx.x;
   for (unsigned k = 0; p < B; ++k, p += G) {
@@ -290,6 +290,7 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
     if (lane == 0) mbar_arrive(xfree);
     {
       // W1024^{t a} by two interleaved chains (even / odd t): 3 live values
+      const cplx wa = ldg_c(twa), wa2 = ldg_c(twa + oa);
       cplx pe = wa2, po = wa;
       v[1] = cmul(v[1], wa);
 #pragma unroll
@@ -321,7 +322,7 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
         got.re = __shfl_xor_sync(0xffffffffu, give.re, 1);
         got.im = __shfl_xor_sync(0xffffffffu, give.im, 1);
         const cplx a0 = oe ? got : mine, a1 = oe ? mine : got;
-        const double sv = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+        const double sv = ((2.0 - (double)n) * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
         __stcs(&sg[oa + 64 * (j + 8 * oe)], sv);
       }
     }

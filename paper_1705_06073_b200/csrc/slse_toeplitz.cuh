@@ -664,6 +664,9 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
   return b.sum(quad);
 }
 
+#ifndef SLSE_WARP_FFT_R8
+#define SLSE_WARP_FFT_R8 1  // radix-8 passes (cfg2 36.5 -> 32.2 ms: the warp-mode FFTs are shared-memory bound)
+#endif
 #ifndef SLSE_HOST_EMU
 // Runtime-size one-warp Stockham pass of radix R over 2^lg <= 512 points
 // (MAXI = 16 / R groups per lane held across the warp barrier, in place).
@@ -716,14 +719,23 @@ SLSE_D void warp_pass_rt(cplx* S, int lg, int lgns, double sign, const cplx* __r
 }
 
 // One-warp in-place transform of 2^lg (<= 512) points on the skewed shared
-// buffer S: radix-4 passes, then one radix-2 pass when lg is odd.  One
-// compact out-of-line body for every size and direction (radix 8 runs fewer
-// passes but its 3x larger body costs more in instruction fetch).
+// buffer S: radix-8 passes, then radix-4 / radix-2 for the remainder.  One
+// compact out-of-line body for every size and direction.  In warp mode the
+// sixteen warps of an SM run their transforms together, so the passes are
+// bound by shared-memory bandwidth (every pass moves every point twice):
+// 3 radix-8 passes for 512 points beat 5 radix-4 ones (cfg2 36.5 -> 32.2 ms,
+// tools/r8_exp.sh), although the body is larger (the free-running solver
+// once measured the opposite, from instruction fetch).
 static __device__ __noinline__ void warp_fft_rt(cplx* S, int lg, double sign, const cplx* __restrict__ tw, int twlog,
                                          int lane_) {
   __builtin_assume(__isShared(S));
   const unsigned lane = (unsigned)lane_ & 31u;
   int lgns = 0;
+#if SLSE_WARP_FFT_R8
+  // radix-8 passes first: 3 shared-memory round trips for 512 points instead of 5
+#pragma unroll 1
+  for (; lg - lgns >= 3; lgns += 3) warp_pass_rt<8>(S, lg, lgns, sign, tw, twlog, lane);
+#endif
 #pragma unroll 1
   for (; lg - lgns >= 2; lgns += 2) warp_pass_rt<4>(S, lg, lgns, sign, tw, twlog, lane);
   if (lg - lgns == 1) warp_pass_rt<2>(S, lg, lgns, sign, tw, twlog, lane);
