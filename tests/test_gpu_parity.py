@@ -310,3 +310,25 @@ def test_mmv_drop_in_estimate():
         r = fn(Observation.complete(y), EstimatorOptions(grid_factor=4))
         _check_traj(r, z, p, [])
         assert r.alpha_hat.shape == (3, r.k_hat)
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_paired_residency_batch(cfg):
+    """Batches larger than the SM count run two 256-thread solver CTAs per
+    SM (solver_paired: 128 registers, half-SM shared region).  The golden
+    problem replicated across such a batch must reproduce the reference
+    history in every slot, wherever the dynamic queue placed it."""
+    import torch
+
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
+
+    z = load(cfg)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    B = sms + 12
+    Y = np.repeat(z["p0_y"][None, :], B, axis=0)
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    for b in (0, B // 2, B - 1):
+        _check_traj(res[b], z, "p0_", near_ties(cfg, 0))
+    assert np.all(res.status == 0)
+    assert np.all(res.k_hat == res.k_hat[0])
+    assert np.max(np.abs(res.theta - res.theta[0])) == 0.0  # same problem, same program: same bits
