@@ -27,6 +27,9 @@
 namespace slse {
 
 constexpr int kDncLeaf = 32;
+#ifndef SLSE_DNC_BLOCK_LEAF
+#define SLSE_DNC_BLOCK_LEAF 256  // CTA-wide leaves up to this many steps (0 / 32: one-warp leaves only)
+#endif
 // nodes up to this many steps multiply their polynomials directly (one
 // output coefficient per thread, two barriers per node) instead of through
 // batched FFTs, whose fixed barrier cost dominates at small sizes
@@ -43,6 +46,7 @@ struct DncCtx {
   int step;           // steps done
   int status;
   int direct_max;     // nodes with s <= direct_max use direct products
+  int leaf_max;       // subtrees with s <= leaf_max run as one leaf (dnc_leaf_block above 32)
   long long* prof;    // optional: clock64 per phase (leaf, direct1, direct2, fft1, fft2, total)
 };
 
@@ -184,6 +188,92 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
 #endif
 }
 
+// Block leaf: s <= nt - 2 steps with the whole CTA, one barrier per step.
+// The same recursion as dnc_leaf, laid out in the shared staging region:
+// thread j < s - t updates the generator pair (e_{t+j}, b_j) in place and
+// thread 1 forms the next reflection coefficient from its fresh e_{t+1};
+// thread nt-1-i updates Theta coefficient i <= t + 1 (Theta_11 / Theta_12
+// in place, Theta_21 / Theta_22 ping-pong because coefficient i reads
+// i - 1).  Replaces the 32-step one-warp leaves and the small product nodes
+// above them, whose per-node latency (barriers, global round trips)
+// dominated the superfast factorisation.
+SLSE_NI void dnc_leaf_block(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T, Blk& b) {
+#ifdef SLSE_HOST_EMU
+  dnc_leaf(X, E1, Bw, s, T, b);
+#else
+  const int tid = b.tid, nt = b.nt;
+  const int ld = s + 1, lp = s + 2;  // Theta_2x ping-pong rows: offset i + 1 holds coefficient i
+  cplx* e = X.f.smem;                 // s
+  cplx* bb = e + s;                   // s
+  cplx* t1 = bb + s;                  // Theta_11 | Theta_12 : 2 ld
+  cplx* t2 = t1 + 2 * ld;             // [2][Theta_21 | Theta_22] : 4 lp
+  cplx* kb = t2 + 4 * lp;             // [2] reflection coefficients (double-buffered)
+  const cplx z = mk(0.0, 0.0);
+  for (int i = tid; i < s; i += nt) {
+    e[i] = E1[i];
+    bb[i] = Bw[i];
+  }
+  for (int i = tid; i < 2 * ld; i += nt) t1[i] = (i == 0) ? mk(1.0, 0.0) : z;
+  for (int i = tid; i < 4 * lp; i += nt) t2[i] = (i == lp + 1) ? mk(1.0, 0.0) : z;  // buffer 0: Theta_22[0] = 1
+  b.sync();
+  double d = X.d;
+  double* dtmp = X.delta_tmp + X.step;
+  const double floor_ = X.floor_;
+  if (tid == 0) {
+    const double inv = 1.0 / d;
+    kb[0] = mk(-e[0].re * inv, -e[0].im * inv);
+  }
+  b.sync();
+  int st = 0;
+  const int ci = nt - 1 - tid;  // Theta coefficient of this thread
+  for (int t = 0; t < s; ++t) {
+    const cplx k = kb[t & 1], kc = conjg(k);
+    const double dn = d * (1.0 - (k.re * k.re + k.im * k.im));
+    if (tid < s - t) {
+      const cplx ej = e[t + tid], bj = bb[tid];
+      const cplx en = cadd(ej, cmul(k, bj));
+      e[t + tid] = en;
+      bb[tid] = cadd(bj, cmul(kc, ej));
+      if (tid == 1) {
+        const double invn = __drcp_rn(dn);
+        kb[(t + 1) & 1] = mk(-en.re * invn, -en.im * invn);
+      }
+    }
+    if (ci <= t + 1) {
+      const cplx* r2 = t2 + (t & 1) * 2 * lp;
+      cplx* w2 = t2 + ((t + 1) & 1) * 2 * lp;
+      const cplx a11 = t1[ci], a12 = t1[ld + ci];
+      const cplx p21 = r2[ci], p22 = r2[lp + ci];  // coefficient ci - 1 (zero slot for ci = 0)
+      t1[ci] = cadd(a11, cmul(k, p21));
+      t1[ld + ci] = cadd(a12, cmul(k, p22));
+      w2[ci + 1] = cadd(cmul(kc, a11), p21);
+      w2[lp + ci + 1] = cadd(cmul(kc, a12), p22);
+    }
+    d = dn;
+    if (tid == 0) dtmp[t + 1] = d;
+    if (!(d > floor_)) {  // uniform: every thread holds the same d
+      st = kNotPD;
+      break;
+    }
+    b.sync();
+  }
+  b.sync();
+  if (!st) {
+    const cplx* r2 = t2 + (s & 1) * 2 * lp;
+    for (int i = tid; i < ld; i += nt) {
+      T[i] = t1[i];
+      T[ld + i] = t1[ld + i];
+      T[2 * ld + i] = r2[i + 1];
+      T[3 * ld + i] = r2[lp + i + 1];
+    }
+  }
+  b.sync();
+  X.d = d;
+  X.step += s;
+  if (st) X.status = st;
+#endif
+}
+
 // forward transform of src[0..len) zero padded to F -> dst[0..F)
 SLSE_D void dnc_fwd(cplx* dst, const cplx* src, int len, int F, cplx* work, const FftCtx& f, Blk& b) {
   fft(work, F, -1.0, [=](int i) { return i < len ? src[i] : mk(0.0, 0.0); },
@@ -249,8 +339,9 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
     DncFrame& cf = fr[sp - 1];
     const int s = cf.s;
     const long long t0 = prof ? dnc_clock() : 0;
-    if (s <= kDncLeaf) {
-      dnc_leaf(X, cf.E + 1, cf.Bw, s, cf.T, b);
+    if (s <= X.leaf_max) {
+      if (s <= kDncLeaf && X.leaf_max <= kDncLeaf) dnc_leaf(X, cf.E + 1, cf.Bw, s, cf.T, b);
+      else dnc_leaf_block(X, cf.E + 1, cf.Bw, s, cf.T, b);
       if (prof) X.prof[0] += dnc_clock() - t0;
       --sp;
       continue;
@@ -504,6 +595,15 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   X.step = 0;
   X.status = 0;
   X.direct_max = direct_max;
+  // block leaves need s + 2 <= nt threads and 8 s + 14 staging elements
+  X.leaf_max = kDncLeaf;
+#ifndef SLSE_HOST_EMU
+  {
+    int lm = SLSE_DNC_BLOCK_LEAF;
+    while (lm > kDncLeaf && (lm + 2 > b.nt || 8 * lm + 14 > f.smem_cap)) lm >>= 1;
+    if (lm > kDncLeaf) X.leaf_max = lm;
+  }
+#endif
   X.prof = prof;
   b.sync();
   // the root window is the column itself: e = b = c (c_0 forced real)
