@@ -502,8 +502,9 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
       e = cudaGetLastError();
       return e == cudaSuccess ? 0 : fail("grid_warp_kernel", e);
     }
-    // v3 (fused last pass) where the plan allows: L = 2^10 (NT 256), 2^11 (256), 2^7 (16: too small -> skip)
-    if (getenv("SLSE_GRID_V2") == nullptr && (lg == 10 || lg == 11)) {
+    // v3 (fused last pass) for L = 2^10 outside v5's N range; at L = 2^11 the
+    // Stockham kernel measured faster (49 vs 68 us for 1024 x N = 512)
+    if (getenv("SLSE_GRID_V2") == nullptr && (lg == 10 || (lg == 11 && getenv("SLSE_GRID_V3_2048")))) {
 #define SLSE_GRID3_Q(NTV, LGV, QV)                                                                        \
   case QV: {                                                                                               \
     if (getenv("SLSE_GRID_PERSIST3") != nullptr) {  /* persistent v3 + cp.async: measured slower (100 vs 70 us) */ \

@@ -355,13 +355,14 @@ struct FixedPlan<LG, LG> {
 
 
 // Fixed-schedule radix-16 passes from log2(Ns) = LGNS up to LGEND (the
-// caller runs the remaining pass itself).
-template <int LG, int LGNS, int LGEND>
+// caller runs the remaining pass itself).  MAXI: radix-16 items per thread,
+// ceil(count * 2^LG / 16 / nt) -- every item of every buffer must be covered.
+template <int LG, int LGNS, int LGEND, int MAXI = 1>
 struct FixedPlanMid {
   SLSE_D static void run(cplx* x, int count, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
     if constexpr (LGNS + 4 <= LGEND) {
-      stockham_pass_inl<16, 1>(x, count, 1 << LG, 1 << LGNS, sign, tw, twlog, tid, nt);
-      FixedPlanMid<LG, LGNS + 4, LGEND>::run(x, count, sign, tw, twlog, tid, nt);
+      stockham_pass_inl<16, MAXI>(x, count, 1 << LG, 1 << LGNS, sign, tw, twlog, tid, nt);
+      FixedPlanMid<LG, LGNS + 4, LGEND, MAXI>::run(x, count, sign, tw, twlog, tid, nt);
     }
   }
 };

@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fus
   }
   __syncthreads();
   // ---- middle radix-16 passes
-  FixedPlanMid<LG, 4, LG - LGRL>::run(X, 3, -1.0, tw, twlog, tid, NT);
+  FixedPlanMid<LG, 4, LG - LGRL, (3 * (L / 16) + NT - 1) / NT>::run(X, 3, -1.0, tw, twlog, tid, NT);
   // ---- last pass fused with the combine (q^G first, then the (A0, A1)
   // pair, keeping at most 2 RL complex values live)
   const int j = tid;
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fus
       for (int r = 0; r < 16; ++r) xc[sk(j * 16 + r)] = v[brev_const(r, 16)];
     }
     __syncthreads();
-    FixedPlanMid<LG, 4, LG - LGRL>::run(X, 3, -1.0, tw, twlog, tid, NT);
+    FixedPlanMid<LG, 4, LG - LGRL, (3 * (L / 16) + NT - 1) / NT>::run(X, 3, -1.0, tw, twlog, tid, NT);
     const int j = tid;
     constexpr int NS = L / RL;
     cplx* qg = q_grid + (size_t)p * L;

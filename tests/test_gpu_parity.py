@@ -332,3 +332,27 @@ def test_paired_residency_batch(cfg):
     assert np.all(res.status == 0)
     assert np.all(res.k_hat == res.k_hat[0])
     assert np.max(np.abs(res.theta - res.theta[0])) == 0.0  # same problem, same program: same bits
+
+
+@pytest.mark.parametrize("n,L,B", [(256, 1024, 300), (200, 1024, 37), (129, 1024, 5), (256, 2048, 7), (64, 256, 9),
+                                   (1000, 4096, 3)])
+def test_grid_eval_shapes_against_fft(n, L, B):
+    """Row 9 on every kernel family (the TMA two-pass kernel serves L = 1024,
+    128 < N <= 256, including ragged N and batches that are not a multiple
+    of the persistent grid): q^G = FFT_L(w), s^G from the product form, vs
+    numpy's FFT of the same seeded inputs (per-call bar 1e-9)."""
+    from paper_1705_06073_b200 import ops
+
+    rng = np.random.default_rng(n * 7 + L + B)
+    rho = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    w = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    dl = rng.uniform(0.5, 2.0, B)
+    qg, sg = ops.grid_eval(_dev(rho), _dev(dl), _dev(w), L)
+    Q = np.fft.fft(w, L, axis=1)
+    A0 = np.fft.fft(rho, L, axis=1)
+    A1 = np.fft.fft(rho * np.arange(n), L, axis=1)
+    S = ((2 - n) * np.abs(A0) ** 2 + 2 * np.real(A1 * np.conj(A0))) / dl[:, None]
+    q, s = qg.cpu().numpy(), sg.cpu().numpy()
+    for b in range(B):
+        assert rel(q[b], Q[b]) < CALL_TOL, b
+        assert rel(s[b], S[b]) < CALL_TOL, b
