@@ -356,3 +356,61 @@ def test_grid_eval_shapes_against_fft(n, L, B):
     for b in range(B):
         assert rel(q[b], Q[b]) < CALL_TOL, b
         assert rel(s[b], S[b]) < CALL_TOL, b
+
+
+SWEEP_N = [2, 3, 17, 64, 100, 255, 256, 257, 300, 512, 513, 1000, 2048, 3000, 4096]
+
+
+@pytest.mark.parametrize("n", SWEEP_N)
+def test_per_call_size_sweep(n, monkeypatch):
+    """Every per-call operator (rows 1, 3-5, 7-9) at ragged and power-of-two
+    sizes around each kernel-family boundary (one-warp / block / paired /
+    superfast factorisations, warp / block GS apply, grid kernels), each on
+    the SAME inputs as the oracle's direct restatement (its own column, rho,
+    w), so the bar (1e-9) measures the operator, not the conditioning of a
+    random state (chained, the column's 1e-12 already grows to 1e-9 in C^-1 y
+    at N = 4096 through cond(C) ~ 1e4; tools/acc_diag.py).  The oracle's
+    off-grid sums use exactly reduced phases here (O.EXACT_PHASE): its
+    reference-faithful direct sums carry ~1e-8 phase rounding at N = 4096."""
+    from paper_1705_06073_b200 import ops
+
+    monkeypatch.setattr(O, "EXACT_PHASE", True)
+
+    rng = np.random.default_rng(1000 + n)
+    B, K = 2, max(1, min(8, n // 4))
+    th = rng.uniform(0, 1, (B, K))
+    ga = rng.uniform(0.2, 2.0, (B, K))
+    be = rng.uniform(0.05, 0.5, B)
+    y = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    kc = _dev(np.full(B, K), np.int32)
+    c = ops.cov_column(_dev(th), _dev(ga), kc, _dev(be), n)
+    bundles = [O.Bundle(y[b], th[b], ga[b], float(be[b])) for b in range(B)]
+    for b in range(B):
+        assert rel(c.cpu().numpy()[b], bundles[b].c) < CALL_TOL
+    c_or = _dev(np.stack([o.c for o in bundles]))
+    methods = ["levinson", "schur"] if n >= 4 else ["levinson"]
+    for method in methods:
+        rho, delta, logdet, status = ops.toeplitz_factor(c_or, method=method)
+        assert int(status.abs().sum()) == 0
+        for b in range(B):
+            assert rel(rho.cpu().numpy()[b], bundles[b].rho) < CALL_TOL, method
+            assert rel(delta.cpu().numpy()[b], bundles[b].delta) < CALL_TOL, method
+    rho_or = _dev(np.stack([o.rho for o in bundles]))
+    dl_or = _dev(np.array([o.delta[-1] for o in bundles]))
+    w, quad = ops.gs_apply(rho_or, dl_or, _dev(y))
+    w_or = _dev(np.stack([o.w for o in bundles]))
+    st = ops.component_stats(_dev(th), kc, rho_or, dl_or, w_or)
+    om = ops.omegas(rho_or, dl_or)
+    L = 1 << int(np.ceil(np.log2(4 * n)))
+    qg, sg = ops.grid_eval(rho_or, dl_or, w_or, L)
+    for b in range(B):
+        o = bundles[b]
+        assert rel(w.cpu().numpy()[b], o.w) < CALL_TOL
+        ost = o.stats()
+        for key in "qrustvx":
+            assert rel(st[key].cpu().numpy()[b, :K], ost[key]) < CALL_TOL, key
+        for key in "stvx":
+            assert rel(om[key].cpu().numpy()[b], o.omegas()[key]) < CALL_TOL, key
+        q_ref, s_ref = o.grid(L)
+        assert rel(qg.cpu().numpy()[b], q_ref) < CALL_TOL
+        assert rel(sg.cpu().numpy()[b], s_ref) < CALL_TOL
