@@ -46,6 +46,14 @@ SLSE_HD cplx cmulc(cplx a, cplx b) {  // a * conj(b)
 SLSE_HD cplx conjg(cplx a) { return mk(a.re, -a.im); }
 SLSE_HD cplx cscale(cplx a, double s) { return mk(a.re * s, a.im * s); }
 SLSE_HD double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
+// correctly rounded reciprocal (== 1.0 / x on both sides)
+SLSE_HD double rcp_rn(double x) {
+#if defined(__CUDA_ARCH__)
+  return __drcp_rn(x);
+#else
+  return 1.0 / x;
+#endif
+}
 // a / b for complex b (Smith-free plain formula is fine: |b| ~ pivot scale)
 SLSE_HD cplx cdiv_real(cplx a, double b) { return mk(a.re / b, a.im / b); }
 

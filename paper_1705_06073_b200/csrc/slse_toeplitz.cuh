@@ -174,6 +174,9 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
   for (int m = 0; m + 1 < n; ++m) {
     const cplx kc = conjg(k);
     const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
+    // 1 / delta_{m+1}, formed before the step's updates so the next
+    // coefficient after the barrier is a load and a multiply
+    const double inv_next = rcp_rn(dnext);
     cplx knext = mk(0.0, 0.0);
     if (look && m + 2 < n) {
       const cplx e2 = e[m + 2], b1 = B[1];
@@ -216,8 +219,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
         k = knext;
       } else {
         const cplx em = e[m + 2];
-        const double inv = 1.0 / delta;
-        k = mk(-em.re * inv, -em.im * inv);
+        k = mk(-em.re * inv_next, -em.im * inv_next);
       }
     }
   }
@@ -291,6 +293,9 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* E, 
   for (int m = 0; m + 1 < n; ++m) {
     const cplx kc = conjg(k);
     const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
+    // 1 / delta_{m+1}, formed before the step's updates so the next
+    // coefficient after the barrier is a load and a multiply
+    const double inv_next = __drcp_rn(dnext);  // == 1.0 / dnext
     cplx knext = mk(0.0, 0.0);
     if (m + 2 < n) {  // lookahead from pre-update values
       const cplx e2 = E[m + 2];
