@@ -581,6 +581,109 @@ SLSE_D Factor toeplitz_factor_regs_c(const cplx* SLSE_RESTRICT c, int n, double*
 }
 #endif
 
+#ifndef SLSE_HOST_EMU
+// Block form of toeplitz_factor_regs_c: the same register slots across a
+// whole CTA -- slot r = Q tid + i holds (E_r, B_r) -- so a step touches no
+// shared memory except the next reflection coefficient (thread 0 forms it
+// from its own update) and one boundary value per warp for the one-slot
+// shift of E (lane 31 takes warp w+1's first slot); both double-buffered,
+// one barrier per step.  Replaces the shared-memory Schur-Levinson loops
+// (LDS -> FMA -> STS chains per item) for 512 < N <= Q nt.
+template <int Q>
+SLSE_D Factor toeplitz_factor_regs_blk(const cplx* SLSE_RESTRICT c, int n, cplx* scratch, double* delta_out,
+                                       double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  const int tid = b.tid, nt = b.nt;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int base = Q * tid;
+  const double c0 = c0c.re;
+  const double floor_ = kPdEps * c0;
+  cplx* kbuf = scratch;     // [2] next reflection coefficient
+  cplx* bnd = scratch + 2;  // [2][nw] first E slot of each warp (post-update)
+  cplx Er[Q], Br[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int r = base + i;
+    Er[i] = (r + 1 < n) ? c[r + 1] : mk(0.0, 0.0);
+    Br[i] = (r + 1 < n) ? (r == 0 ? mk(c0, 0.0) : c[r]) : mk(r == n - 1 ? 1.0 : 0.0, 0.0);
+    if (r < n) delta_tmp[r] = 0.0;
+  }
+  b.sync();
+  if (tid == 0) delta_tmp[0] = c0;
+  double delta = c0;
+  double kr = 0.0, ki = 0.0;
+  if (n > 1) {
+    const cplx e1 = c[1];
+    const double inv = 1.0 / delta;
+    kr = -e1.re * inv;
+    ki = -e1.im * inv;
+  }
+  int fail = 0;
+#pragma unroll 1
+  for (int m = 0; m + 1 < n; ++m) {
+    const double dnext = delta * (1.0 - (kr * kr + ki * ki));
+    const double inv = __drcp_rn(dnext);
+    const int toff = n - 2 - m - base;  // retiring generator slot, if this thread owns it
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const cplx ej = Er[i], bj = Br[i];
+      Er[i] = mk(fma(kr, bj.re, fma(-ki, bj.im, ej.re)), fma(kr, bj.im, fma(ki, bj.re, ej.im)));
+      const cplx bn = mk(fma(kr, ej.re, fma(ki, ej.im, bj.re)), fma(kr, ej.im, fma(-ki, ej.re, bj.im)));
+      Br[i] = (i == toff) ? mk(kr, -ki) : bn;  // b_{m+1}[0] = conj(k)
+    }
+    // thread 0 holds slot 1 = the updated e_{m+2}: the next pivot
+    if (tid == 0) kbuf[(m + 1) & 1] = mk(-Er[1].re * inv, -Er[1].im * inv);
+    if (lane == 0 && warp > 0) bnd[(m & 1) * nw + warp] = Er[0];
+    const double sr = __shfl_down_sync(0xffffffffu, Er[0].re, 1);
+    const double si = __shfl_down_sync(0xffffffffu, Er[0].im, 1);
+    b.sync();
+    cplx nx = mk(sr, si);
+    if (lane == 31) nx = (warp + 1 < nw) ? bnd[(m & 1) * nw + warp + 1] : mk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i + 1 < Q; ++i) Er[i] = Er[i + 1];
+    Er[Q - 1] = nx;
+    if (tid == 0) delta_tmp[m + 1] = dnext;
+    delta = dnext;
+    if (!(delta > floor_)) { fail = 1; break; }  // uniform
+    const cplx kn = kbuf[(m + 1) & 1];
+    kr = kn.re;
+    ki = kn.im;
+  }
+  if (fail) {
+    F.status = kNotPD;
+    return F;
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int j = base + i + 1;
+    if (j <= n - 1) rho[n - 1 - j] = conjg(Er[i]);
+  }
+  if (tid == 0) rho[n - 1] = mk(1.0, 0.0);
+  F.delta_last = delta;
+  b.sync();
+  double part = 0.0;
+  for (int j = tid; j < n; j += nt) {
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+#endif
+
+#ifndef SLSE_LEV_BLK
+#define SLSE_LEV_BLK 1  // register block Schur-Levinson for wide CTAs
+#endif
+
 SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx* B, cplx* a,
                               double* delta_out, double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
 #ifndef SLSE_HOST_EMU
@@ -596,6 +699,12 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
     if (B == e + n && n <= 256) return toeplitz_factor_warp<8>(c, n, e, delta_out, delta_tmp, rho, b);
     if (B == e + n && n <= 512) return toeplitz_factor_warp<16>(c, n, e, delta_out, delta_tmp, rho, b);
   }
+#if SLSE_LEV_BLK
+  if (b.nt >= 64 && (b.nt & 31) == 0 && n >= 64) {  // (scratch: 2 + 2 nt / 32 elements of e)
+    if (n <= 4 * b.nt) return toeplitz_factor_regs_blk<4>(c, n, e, delta_out, delta_tmp, rho, b);
+    if (n <= 8 * b.nt) return toeplitz_factor_regs_blk<8>(c, n, e, delta_out, delta_tmp, rho, b);
+  }
+#endif
   if (__isShared(e)) return toeplitz_factor_impl<true>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
 #endif
   return toeplitz_factor_impl<false>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
