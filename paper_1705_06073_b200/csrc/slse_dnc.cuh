@@ -206,6 +206,7 @@ SLSE_NI void dnc_leaf_block(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cp
 #else
   const int tid = b.tid, nt = b.nt;
   const int ld = s + 1, lp = s + 2;  // Theta_2x ping-pong rows: offset i + 1 holds coefficient i
+  __builtin_assume(__isShared(X.f.smem));  // shared-memory instructions, not generic LD / ST
   cplx* e = X.f.smem;                 // s
   cplx* bb = e + s;                   // s
   cplx* t1 = bb + s;                  // Theta_11 | Theta_12 : 2 ld
@@ -297,6 +298,7 @@ SLSE_NI void dnc_leaf_regs(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cpl
   const int j = gen ? tid : tid - G;  // generator slot / Theta coefficient
   const int wh = gen ? warp : warp - nwg;  // warp index within the half
   const int ld = s + 1;
+  __builtin_assume(__isShared(X.f.smem));
   cplx* kb = X.f.smem;        // [2]
   cplx* bnd = kb + 2;         // [2][nwg] generator boundary (first slot of warp w, post-update)
   cplx* bth = bnd + 2 * nwg;  // [2][nwg][2] Theta_21 / Theta_22 of each warp's lane 31

@@ -75,8 +75,12 @@ SLSE_D void fft_barrier() { SLSE_GROUP_SYNC(); }
 
 // DIT passes over `count` contiguous bit-reversed buffers of n points
 // (one barrier per pass for all of them).
-SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
-                              int tid, int nt) {
+template <bool SH>
+SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                                  int tid, int nt) {
+#ifndef SLSE_HOST_EMU
+  if constexpr (SH) __builtin_assume(__isShared(x));  // LDS / STS instead of generic LD / ST
+#endif
   const int p = ilog2(n);
   int lgh = 0;  // log2 of current half-span
   if (p & 1) {
@@ -118,6 +122,19 @@ SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx
     }
     fft_barrier();
   }
+}
+
+// x is either the shared staging area or a global work buffer: dispatch so
+// the staged case compiles to shared-memory instructions
+SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                              int tid, int nt) {
+#ifndef SLSE_HOST_EMU
+  if (__isShared(x)) {
+    fft_passes_multi_impl<true>(x, count, n, sign, tw, twlog, tid, nt);
+    return;
+  }
+#endif
+  fft_passes_multi_impl<false>(x, count, n, sign, tw, twlog, tid, nt);
 }
 
 SLSE_D void fft_passes_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
@@ -421,6 +438,9 @@ SLSE_NI void fft_stockham(cplx* x, int count, int n, double sign, const FftCtx& 
 #endif
 // Stockham (by value: table, thread index/count) on skewed shared staging
 SLSE_NI void fft_stockham_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
+#ifndef SLSE_HOST_EMU
+  __builtin_assume(__isShared(x));  // always the shared staging area
+#endif
   for (int Ns = 1; Ns < n;) {
     const int R = stockham_radix(n / Ns, 1, n, nt);
     switch (R) {
