@@ -1,0 +1,4 @@
+# cfg2 solve time per library build (regression bisect)
+for lib in build/variants/bis_72ec20e build/variants/bis_23aa0b4 build/variants/bis_7cbf127 paper_1705_06073_b200/_lib; do
+  echo "== $lib"; for i in 1 2; do SLSE_LIB=$lib/libsuperlse_b200.so python tools/bench_configs.py --configs 2 --no-cpu; done
+done
