@@ -680,6 +680,145 @@ SLSE_D Factor toeplitz_factor_regs_blk(const cplx* SLSE_RESTRICT c, int n, cplx*
 }
 #endif
 
+#ifndef SLSE_HOST_EMU
+// Unrolled form of toeplitz_factor_regs_blk (static register renaming, as
+// toeplitz_factor_regs does for one warp): Q sub-steps per loop iteration,
+// E's one-slot shift is a renaming, and only the one register that can hold
+// the retiring slot carries a select -- no per-slot moves or selects.
+template <int Q, int T>
+SLSE_D void lev_blk_step(cplx (&Er)[Q], cplx (&Br)[Q], double& kr, double& ki, double& delta, int m, int n, int tid,
+                         int lane, int warp, int nw, cplx* kbuf, cplx* bnd, double* delta_tmp, Blk& b) {
+  const double dnext = delta * (1.0 - (kr * kr + ki * ki));
+  const double inv = __drcp_rn(dnext);
+  const int top = n - 2 - m;
+  const bool mine = (top - (Q - 1 - T)) == Q * tid;  // this thread owns the retiring slot
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int p = (i + T) % Q;  // physical E register of logical slot i (B does not move)
+    const cplx ej = Er[p], bj = Br[i];
+    Er[p] = mk(fma(kr, bj.re, fma(-ki, bj.im, ej.re)), fma(kr, bj.im, fma(ki, bj.re, ej.im)));
+    cplx bn = mk(fma(kr, ej.re, fma(ki, ej.im, bj.re)), fma(kr, ej.im, fma(-ki, ej.re, bj.im)));
+    if (i == Q - 1 - T) bn = mine ? mk(kr, -ki) : bn;  // b_{m+1}[0] = conj(k)
+    Br[i] = bn;
+  }
+  if (tid == 0) {  // slot 1 = the updated e_{m+2}: the next pivot
+    const cplx e2 = Er[(1 + T) % Q];
+    kbuf[(m + 1) & 1] = mk(-e2.re * inv, -e2.im * inv);
+  }
+  constexpr int p0 = T % Q;
+  if (lane == 0 && warp > 0) bnd[(m & 1) * nw + warp] = Er[p0];
+  const double sr = __shfl_down_sync(0xffffffffu, Er[p0].re, 1);
+  const double si = __shfl_down_sync(0xffffffffu, Er[p0].im, 1);
+  if (tid == 0) delta_tmp[m + 1] = dnext;
+  b.sync();
+  Er[p0] = (lane == 31) ? ((warp + 1 < nw) ? bnd[(m & 1) * nw + warp + 1] : mk(0.0, 0.0)) : mk(sr, si);
+  delta = dnext;
+  const cplx kn = kbuf[(m + 1) & 1];
+  kr = kn.re;
+  ki = kn.im;
+}
+
+template <int Q, int T>
+SLSE_D void lev_blk_block(cplx (&Er)[Q], cplx (&Br)[Q], double& kr, double& ki, double& delta, int& m, int n, int tid,
+                          int lane, int warp, int nw, cplx* kbuf, cplx* bnd, double* delta_tmp, Blk& b, int t0) {
+  if constexpr (T < Q) {
+    if (T >= t0) {
+      lev_blk_step<Q, T>(Er, Br, kr, ki, delta, m, n, tid, lane, warp, nw, kbuf, bnd, delta_tmp, b);
+      ++m;
+    }
+    lev_blk_block<Q, T + 1>(Er, Br, kr, ki, delta, m, n, tid, lane, warp, nw, kbuf, bnd, delta_tmp, b, t0);
+  }
+}
+
+template <int Q>
+SLSE_D Factor toeplitz_factor_regs_blk_u(const cplx* SLSE_RESTRICT c, int n, cplx* scratch, double* delta_out,
+                                         double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
+  Factor F;
+  F.logdet = 0.0;
+  F.status = kOk;
+  const cplx c0c = c[0];
+  F.c0 = c0c.re;
+  F.delta_last = c0c.re;
+  if (fabs(c0c.im) > 1e-10 * fmax(fabs(c0c.re), 1.0) || !(c0c.re > 0.0)) {
+    F.status = kBadColumn;
+    return F;
+  }
+  const int tid = b.tid, nt = b.nt;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int base = Q * tid;
+  const double c0 = c0c.re;
+  const double floor_ = kPdEps * c0;
+  cplx* kbuf = scratch;
+  cplx* bnd = scratch + 2;
+  const int t0 = (Q - (n - 1) % Q) % Q;  // first block runs sub-steps t0..Q-1 (steps end on a block boundary)
+  cplx Er[Q], Br[Q];
+#pragma unroll
+  for (int p = 0; p < Q; ++p) {
+    const int i = (p - t0 + Q) % Q;  // logical slot held by physical register p at the start
+    const int r = base + i;
+    Er[p] = (r + 1 < n) ? c[r + 1] : mk(0.0, 0.0);
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int r = base + i;
+    Br[i] = (r + 1 < n) ? (r == 0 ? mk(c0, 0.0) : c[r]) : mk(r == n - 1 ? 1.0 : 0.0, 0.0);
+    if (r < n) delta_tmp[r] = 0.0;
+  }
+  b.sync();
+  if (tid == 0) delta_tmp[0] = c0;
+  double delta = c0;
+  double kr = 0.0, ki = 0.0;
+  if (n > 1) {
+    const cplx e1 = c[1];
+    const double inv = 1.0 / delta;
+    kr = -e1.re * inv;
+    ki = -e1.im * inv;
+  }
+  int fail = 0;
+  if (n > 1) {
+    int m = 0;
+    lev_blk_block<Q, 0>(Er, Br, kr, ki, delta, m, n, tid, lane, warp, nw, kbuf, bnd, delta_tmp, b, t0);
+    fail = !(delta > floor_);
+#pragma unroll 1
+    for (; m + 1 < n && !fail; m += Q) {
+      lev_blk_block<Q, 0>(Er, Br, kr, ki, delta, m, n, tid, lane, warp, nw, kbuf, bnd, delta_tmp, b, 0);
+      m -= Q;  // (lev_blk_block advanced m by Q)
+      fail = !(delta > floor_);
+    }
+  }
+  b.sync();
+  if (!fail) {  // a pivot below the floor anywhere inside a block
+    int bad = 0;
+    for (int j = tid + 1; j < n; j += nt) bad |= !(delta_tmp[j] > floor_);
+    fail = b.sumi(bad) != 0;
+  }
+  if (fail) {
+    F.status = kNotPD;
+    return F;
+  }
+  // after n-1 steps (rotation back to identity) logical slot i holds a_{Q tid + i + 1}
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const int j = base + i + 1;
+    if (j <= n - 1) rho[n - 1 - j] = conjg(Er[i]);
+  }
+  if (tid == 0) rho[n - 1] = mk(1.0, 0.0);
+  F.delta_last = delta;
+  b.sync();
+  double part = 0.0;
+  for (int j = tid; j < n; j += nt) {
+    part += log(delta_tmp[j]);
+    if (delta_out) delta_out[j] = delta_tmp[j];
+  }
+  F.logdet = b.sum(part);
+  return F;
+}
+#endif
+
+#ifndef SLSE_LEV_BLK_UNROLL
+#define SLSE_LEV_BLK_UNROLL 1
+#endif
+
 #ifndef SLSE_LEV_BLK
 #define SLSE_LEV_BLK 1  // register block Schur-Levinson for wide CTAs
 #endif
@@ -701,6 +840,9 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
   }
 #if SLSE_LEV_BLK
   if (b.nt >= 64 && (b.nt & 31) == 0 && n >= 64) {  // (scratch: 2 + 2 nt / 32 elements of e)
+#if SLSE_LEV_BLK_UNROLL
+    if (n <= 4 * b.nt) return toeplitz_factor_regs_blk_u<4>(c, n, e, delta_out, delta_tmp, rho, b);
+#endif
     if (n <= 4 * b.nt) return toeplitz_factor_regs_blk<4>(c, n, e, delta_out, delta_tmp, rho, b);
     if (n <= 8 * b.nt) return toeplitz_factor_regs_blk<8>(c, n, e, delta_out, delta_tmp, rho, b);
   }
