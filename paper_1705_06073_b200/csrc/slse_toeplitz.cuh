@@ -819,6 +819,18 @@ SLSE_D Factor toeplitz_factor_regs_blk_u(const cplx* SLSE_RESTRICT c, int n, cpl
 #define SLSE_LEV_BLK_UNROLL 1
 #endif
 
+#ifndef SLSE_HOST_EMU
+// Out-of-line entry points: each variant gets its own register allocation,
+// so the unrolled bodies (which need the 128-register budget) do not push
+// the 1024-thread instantiations of toeplitz_factor into spills.
+template <int Q, bool U>
+SLSE_NI Factor factor_regs_blk_ni(const cplx* SLSE_RESTRICT c, int n, cplx* scratch, double* delta_out,
+                                  double* delta_tmp, cplx* SLSE_RESTRICT rho, Blk& b) {
+  if constexpr (U) return toeplitz_factor_regs_blk_u<Q>(c, n, scratch, delta_out, delta_tmp, rho, b);
+  else return toeplitz_factor_regs_blk<Q>(c, n, scratch, delta_out, delta_tmp, rho, b);
+}
+#endif
+
 #ifndef SLSE_LEV_BLK
 #define SLSE_LEV_BLK 1  // register block Schur-Levinson for wide CTAs
 #endif
@@ -840,11 +852,12 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
   }
 #if SLSE_LEV_BLK
   if (b.nt >= 64 && (b.nt & 31) == 0 && n >= 64) {  // (scratch: 2 + 2 nt / 32 elements of e)
-#if SLSE_LEV_BLK_UNROLL
-    if (n <= 4 * b.nt) return toeplitz_factor_regs_blk_u<4>(c, n, e, delta_out, delta_tmp, rho, b);
-#endif
-    if (n <= 4 * b.nt) return toeplitz_factor_regs_blk<4>(c, n, e, delta_out, delta_tmp, rho, b);
-    if (n <= 8 * b.nt) return toeplitz_factor_regs_blk<8>(c, n, e, delta_out, delta_tmp, rho, b);
+    // the unrolled body needs the 128-register budget: not at 1024 threads
+    const bool u = SLSE_LEV_BLK_UNROLL && b.nt <= 512;
+    if (n <= 4 * b.nt) return u ? factor_regs_blk_ni<4, true>(c, n, e, delta_out, delta_tmp, rho, b)
+                                : factor_regs_blk_ni<4, false>(c, n, e, delta_out, delta_tmp, rho, b);
+    if (n <= 8 * b.nt) return u ? factor_regs_blk_ni<8, true>(c, n, e, delta_out, delta_tmp, rho, b)
+                                : factor_regs_blk_ni<8, false>(c, n, e, delta_out, delta_tmp, rho, b);
   }
 #endif
   if (__isShared(e)) return toeplitz_factor_impl<true>(c, n, e, B, a, delta_out, delta_tmp, rho, b);
