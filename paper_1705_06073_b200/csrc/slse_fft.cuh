@@ -465,6 +465,9 @@ SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx&
   const int tid = b.tid, nt = b.nt;
   if (use_stockham(f, n, nt)) {
     cplx* x = f.smem;
+#ifndef SLSE_HOST_EMU
+    __builtin_assume(__isShared(x));  // the staging area: LDS / STS
+#endif
     for (int i = tid; i < n; i += nt) x[sk(i)] = ld(i);
     fft_barrier();
     fft_stockham_v(x, n, sign, f.tw, f.twlog, tid, nt);
@@ -554,6 +557,9 @@ SLSE_D void fft_inplace(cplx* data, int n, double sign, const FftCtx& f, Blk& b)
   const int tid = b.tid, nt = b.nt;
   if (use_stockham(f, n, nt)) {
     cplx* x = f.smem;
+#ifndef SLSE_HOST_EMU
+    __builtin_assume(__isShared(x));
+#endif
     for (int i = tid; i < n; i += nt) x[sk(i)] = data[i];
     fft_barrier();
     fft_stockham_v(x, n, sign, f.tw, f.twlog, tid, nt);
