@@ -27,6 +27,9 @@
 namespace slse {
 
 constexpr int kDncLeaf = 32;
+#ifndef SLSE_DNC_LEAF2
+#define SLSE_DNC_LEAF2 1  // block leaves take two Schur steps per barrier (dnc_leaf_block2)
+#endif
 #ifndef SLSE_DNC_REG_LEAF
 #define SLSE_DNC_REG_LEAF 0  // 1: leaves of s <= nt / 2 steps in registers (dnc_leaf_regs; measured 11.9 M vs 10.4 M cycles at N = 16384: off)
 #endif
@@ -278,6 +281,158 @@ SLSE_NI void dnc_leaf_block(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cp
 #endif
 }
 
+// Block leaf, two Schur steps per barrier.  The same recursion as
+// dnc_leaf_block (identical arithmetic), but each item also computes the
+// step-t value of its right-hand neighbour (generator slot j + 1, or Theta
+// coefficient i - 1 of row 2) from the pre-pair state, so it can apply step
+// t + 1 without waiting for that neighbour.  All state is ping-ponged
+// between two buffers per pair; thread 1 additionally carries slot 2 so it
+// can form k_{t+2} and k_{t+3} for the next pair.  Needs s + 3 <= nt.
+SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T, Blk& b) {
+#ifdef SLSE_HOST_EMU
+  dnc_leaf(X, E1, Bw, s, T, b);
+#else
+  const int tid = b.tid, nt = b.nt;
+  const int ld = s + 1;
+  const int le = s + 4, l1 = ld + 2, l2 = ld + 3;  // row strides (zero prefixes: 1 for row 1, 2 for row 2)
+  __builtin_assume(__isShared(X.f.smem));
+  cplx* eb = X.f.smem;        // [2][le]
+  cplx* bbuf = eb + 2 * le;   // [2][le]
+  cplx* r1 = bbuf + 2 * le;   // [2][Theta_11 | Theta_12][l1], coefficient i at i + 1
+  cplx* r2 = r1 + 4 * l1;     // [2][Theta_21 | Theta_22][l2], coefficient i at i + 2
+  cplx* kb = r2 + 4 * l2;     // [2][2] (k_t, k_{t+1}) of the pair
+  const cplx z = mk(0.0, 0.0);
+  for (int i = tid; i < 2 * le; i += nt) {
+    const int q = i % le;
+    eb[i] = (i < le && q < s) ? E1[q] : z;
+    bbuf[i] = (i < le && q < s) ? Bw[q] : z;
+  }
+  for (int i = tid; i < 4 * l1; i += nt) r1[i] = (i == 1) ? mk(1.0, 0.0) : z;           // Theta_11[0] = 1
+  for (int i = tid; i < 4 * l2; i += nt) r2[i] = (i == l2 + 2) ? mk(1.0, 0.0) : z;      // Theta_22[0] = 1
+  double d = X.d;
+  double* dtmp = X.delta_tmp + X.step;
+  const double floor_ = X.floor_;
+  if (tid == 0) {  // k_0, and k_1 from the pre-update pair (e_1, b_1)
+    const double inv = 1.0 / d;
+    const cplx e0 = E1[0];
+    const cplx k0 = mk(-e0.re * inv, -e0.im * inv);
+    kb[0] = k0;
+    if (s > 1) {
+      const double d1 = d * (1.0 - (k0.re * k0.re + k0.im * k0.im));
+      const cplx en = cadd(E1[1], cmul(k0, Bw[1]));
+      const double inv1 = __drcp_rn(d1);
+      kb[1] = mk(-en.re * inv1, -en.im * inv1);
+    }
+  }
+  b.sync();
+  int st = 0;
+  const int ci = nt - 1 - tid;  // Theta coefficient of this thread
+  int P = 0;
+  int t = 0;
+  for (; t + 1 < s; t += 2, P ^= 1) {
+    const int Q = P ^ 1;
+    const cplx ka = kb[2 * P], kk = kb[2 * P + 1];
+    const cplx kac = conjg(ka), kkc = conjg(kk);
+    const double d1 = d * (1.0 - (ka.re * ka.re + ka.im * ka.im));
+    const double d2 = d1 * (1.0 - (kk.re * kk.re + kk.im * kk.im));
+    const cplx* ec = eb + P * le;
+    const cplx* bc = bbuf + P * le;
+    cplx* en_ = eb + Q * le;
+    cplx* bn_ = bbuf + Q * le;
+    const int j = tid;
+    if (j < s - t) {
+      const cplx ej = ec[t + j], bj = bc[j];
+      const cplx e1 = cadd(ej, cmul(ka, bj));  // step t, own slot (index t + j; superseded)
+      const cplx b1 = cadd(bj, cmul(kac, ej));
+      (void)e1;
+      if (j < s - t - 1) {
+        const cplx ej1 = ec[t + 1 + j], bj1 = bc[j + 1];
+        const cplx e1h = cadd(ej1, cmul(ka, bj1));  // step t, slot j + 1 (index t + 1 + j)
+        const cplx e2 = cadd(e1h, cmul(kk, b1));    // step t + 1, own slot
+        const cplx b2 = cadd(b1, cmul(kkc, e1h));
+        en_[t + 1 + j] = e2;
+        bn_[j] = b2;
+        if (j == 1 && t + 2 < s) {  // next pair's coefficients
+          const cplx e2s = ec[t + 2], e3s = ec[t + 3], b2s = bc[2], b3s = bc[3];
+          const cplx b1_2 = cadd(b2s, cmul(kac, e2s));
+          const cplx e1h_3 = cadd(e3s, cmul(ka, b3s));
+          const cplx e2_2 = cadd(e1h_3, cmul(kk, b1_2));  // e^{(t+2)}_{t+3}
+          const double inv2 = __drcp_rn(d2);
+          const cplx kn0 = mk(-e2.re * inv2, -e2.im * inv2);
+          const double d3 = d2 * (1.0 - (kn0.re * kn0.re + kn0.im * kn0.im));
+          const cplx e3n = cadd(e2_2, cmul(kn0, b2));  // e^{(t+3)}_{t+3}
+          const double inv3 = __drcp_rn(d3);
+          kb[2 * Q] = kn0;
+          kb[2 * Q + 1] = mk(-e3n.re * inv3, -e3n.im * inv3);
+        }
+      }
+    }
+    if (ci <= t + 2) {
+      const cplx* r1c = r1 + P * 2 * l1;
+      const cplx* r2c = r2 + P * 2 * l2;
+      cplx* r1n = r1 + Q * 2 * l1;
+      cplx* r2n = r2 + Q * 2 * l2;
+      const cplx a11 = r1c[ci + 1], a12 = r1c[l1 + ci + 1];
+      const cplx h11 = r1c[ci], h12 = r1c[l1 + ci];            // coefficient ci - 1, row 1
+      const cplx p21 = r2c[ci + 1], p22 = r2c[l2 + ci + 1];    // coefficient ci - 1, row 2
+      const cplx q21 = r2c[ci], q22 = r2c[l2 + ci];            // coefficient ci - 2, row 2
+      const cplx A1 = cadd(a11, cmul(ka, p21)), A2 = cadd(a12, cmul(ka, p22));
+      const cplx H1 = cadd(cmul(kac, h11), q21), H2 = cadd(cmul(kac, h12), q22);
+      r1n[ci + 1] = cadd(A1, cmul(kk, H1));
+      r1n[l1 + ci + 1] = cadd(A2, cmul(kk, H2));
+      r2n[ci + 2] = cadd(cmul(kkc, A1), H1);
+      r2n[l2 + ci + 2] = cadd(cmul(kkc, A2), H2);
+    }
+    if (tid == 0) {
+      dtmp[t + 1] = d1;
+      dtmp[t + 2] = d2;
+    }
+    d = d2;
+    if (!(d1 > floor_) || !(d2 > floor_)) {  // uniform
+      st = kNotPD;
+      break;
+    }
+    b.sync();
+  }
+  if (!st && t < s) {  // odd s: one last single step with k_{s-1}
+    const int Q = P ^ 1;
+    const cplx ka = kb[2 * P], kac = conjg(ka);
+    const double d1 = d * (1.0 - (ka.re * ka.re + ka.im * ka.im));
+    if (ci <= t + 1) {
+      const cplx* r1c = r1 + P * 2 * l1;
+      const cplx* r2c = r2 + P * 2 * l2;
+      cplx* r1n = r1 + Q * 2 * l1;
+      cplx* r2n = r2 + Q * 2 * l2;
+      const cplx a11 = r1c[ci + 1], a12 = r1c[l1 + ci + 1];
+      const cplx p21 = r2c[ci + 1], p22 = r2c[l2 + ci + 1];
+      r1n[ci + 1] = cadd(a11, cmul(ka, p21));
+      r1n[l1 + ci + 1] = cadd(a12, cmul(ka, p22));
+      r2n[ci + 2] = cadd(cmul(kac, a11), p21);
+      r2n[l2 + ci + 2] = cadd(cmul(kac, a12), p22);
+    }
+    if (tid == 0) dtmp[t + 1] = d1;
+    d = d1;
+    if (!(d1 > floor_)) st = kNotPD;
+    P ^= 1;
+  }
+  b.sync();
+  if (!st) {
+    const cplx* r1c = r1 + P * 2 * l1;
+    const cplx* r2c = r2 + P * 2 * l2;
+    for (int i = tid; i < ld; i += nt) {
+      T[i] = r1c[i + 1];
+      T[ld + i] = r1c[l1 + i + 1];
+      T[2 * ld + i] = r2c[i + 2];
+      T[3 * ld + i] = r2c[l2 + i + 2];
+    }
+  }
+  b.sync();
+  X.d = d;
+  X.step += s;
+  if (st) X.status = st;
+#endif
+}
+
 // Register leaf: s <= nt / 2 steps, the block-leaf recursion with every
 // value in registers.  Threads [0, G), G = nt / 2, hold one generator slot
 // each in the shifted frame (thread j: e_{t+j}, b_j; E moves down one slot
@@ -474,6 +629,9 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       if (s <= kDncLeaf && X.leaf_max <= kDncLeaf) dnc_leaf(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #if SLSE_DNC_REG_LEAF
       else if (2 * s <= b.nt) dnc_leaf_regs(X, cf.E + 1, cf.Bw, s, cf.T, b);
+#endif
+#if SLSE_DNC_LEAF2
+      else if (s + 3 <= b.nt && 12 * s + 48 <= X.f.smem_cap) dnc_leaf_block2(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #endif
       else dnc_leaf_block(X, cf.E + 1, cf.Bw, s, cf.T, b);
       if (prof) X.prof[0] += dnc_clock() - t0;
