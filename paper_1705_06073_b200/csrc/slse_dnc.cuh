@@ -287,7 +287,8 @@ SLSE_NI void dnc_leaf_block(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cp
 // coefficient i - 1 of row 2) from the pre-pair state, so it can apply step
 // t + 1 without waiting for that neighbour.  All state is ping-ponged
 // between two buffers per pair; thread 1 additionally carries slot 2 so it
-// can form k_{t+2} and k_{t+3} for the next pair.  Needs s + 3 <= nt.
+// can form k_{t+2} and k_{t+3} for the next pair.  Needs s <= nt (a few
+// threads then also hold the top Theta coefficients, s + 3 > nt).
 SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T, Blk& b) {
 #ifdef SLSE_HOST_EMU
   dnc_leaf(X, E1, Bw, s, T, b);
@@ -367,21 +368,22 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
         }
       }
     }
-    if (ci <= t + 2) {
+    // Theta coefficient ci (and ci + nt when s >= nt: only the top one)
+    for (int cq = ci; cq <= t + 2; cq += nt) {
       const cplx* r1c = r1 + P * 2 * l1;
       const cplx* r2c = r2 + P * 2 * l2;
       cplx* r1n = r1 + Q * 2 * l1;
       cplx* r2n = r2 + Q * 2 * l2;
-      const cplx a11 = r1c[ci + 1], a12 = r1c[l1 + ci + 1];
-      const cplx h11 = r1c[ci], h12 = r1c[l1 + ci];            // coefficient ci - 1, row 1
-      const cplx p21 = r2c[ci + 1], p22 = r2c[l2 + ci + 1];    // coefficient ci - 1, row 2
-      const cplx q21 = r2c[ci], q22 = r2c[l2 + ci];            // coefficient ci - 2, row 2
+      const cplx a11 = r1c[cq + 1], a12 = r1c[l1 + cq + 1];
+      const cplx h11 = r1c[cq], h12 = r1c[l1 + cq];            // coefficient cq - 1, row 1
+      const cplx p21 = r2c[cq + 1], p22 = r2c[l2 + cq + 1];    // coefficient cq - 1, row 2
+      const cplx q21 = r2c[cq], q22 = r2c[l2 + cq];            // coefficient cq - 2, row 2
       const cplx A1 = cadd(a11, cmul(ka, p21)), A2 = cadd(a12, cmul(ka, p22));
       const cplx H1 = cadd(cmul(kac, h11), q21), H2 = cadd(cmul(kac, h12), q22);
-      r1n[ci + 1] = cadd(A1, cmul(kk, H1));
-      r1n[l1 + ci + 1] = cadd(A2, cmul(kk, H2));
-      r2n[ci + 2] = cadd(cmul(kkc, A1), H1);
-      r2n[l2 + ci + 2] = cadd(cmul(kkc, A2), H2);
+      r1n[cq + 1] = cadd(A1, cmul(kk, H1));
+      r1n[l1 + cq + 1] = cadd(A2, cmul(kk, H2));
+      r2n[cq + 2] = cadd(cmul(kkc, A1), H1);
+      r2n[l2 + cq + 2] = cadd(cmul(kkc, A2), H2);
     }
     if (tid == 0) {
       dtmp[t + 1] = d1;
@@ -398,17 +400,17 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
     const int Q = P ^ 1;
     const cplx ka = kb[2 * P], kac = conjg(ka);
     const double d1 = d * (1.0 - (ka.re * ka.re + ka.im * ka.im));
-    if (ci <= t + 1) {
+    for (int cq = ci; cq <= t + 1; cq += nt) {
       const cplx* r1c = r1 + P * 2 * l1;
       const cplx* r2c = r2 + P * 2 * l2;
       cplx* r1n = r1 + Q * 2 * l1;
       cplx* r2n = r2 + Q * 2 * l2;
-      const cplx a11 = r1c[ci + 1], a12 = r1c[l1 + ci + 1];
-      const cplx p21 = r2c[ci + 1], p22 = r2c[l2 + ci + 1];
-      r1n[ci + 1] = cadd(a11, cmul(ka, p21));
-      r1n[l1 + ci + 1] = cadd(a12, cmul(ka, p22));
-      r2n[ci + 2] = cadd(cmul(kac, a11), p21);
-      r2n[l2 + ci + 2] = cadd(cmul(kac, a12), p22);
+      const cplx a11 = r1c[cq + 1], a12 = r1c[l1 + cq + 1];
+      const cplx p21 = r2c[cq + 1], p22 = r2c[l2 + cq + 1];
+      r1n[cq + 1] = cadd(a11, cmul(ka, p21));
+      r1n[l1 + cq + 1] = cadd(a12, cmul(ka, p22));
+      r2n[cq + 2] = cadd(cmul(kac, a11), p21);
+      r2n[l2 + cq + 2] = cadd(cmul(kac, a12), p22);
     }
     if (tid == 0) dtmp[t + 1] = d1;
     d = d1;
@@ -631,7 +633,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       else if (2 * s <= b.nt) dnc_leaf_regs(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #endif
 #if SLSE_DNC_LEAF2
-      else if (s + 3 <= b.nt && 12 * s + 48 <= X.f.smem_cap) dnc_leaf_block2(X, cf.E + 1, cf.Bw, s, cf.T, b);
+      else if (s <= b.nt && 12 * s + 48 <= X.f.smem_cap) dnc_leaf_block2(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #endif
       else dnc_leaf_block(X, cf.E + 1, cf.Bw, s, cf.T, b);
       if (prof) X.prof[0] += dnc_clock() - t0;
@@ -892,7 +894,11 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
 #ifndef SLSE_HOST_EMU
   {
     int lm = SLSE_DNC_BLOCK_LEAF;
+#if SLSE_DNC_LEAF2
+    while (lm > kDncLeaf && (lm > b.nt || 12 * lm + 48 > f.smem_cap)) lm >>= 1;
+#else
     while (lm > kDncLeaf && (lm + 2 > b.nt || 8 * lm + 14 > f.smem_cap)) lm >>= 1;
+#endif
     if (lm > kDncLeaf) X.leaf_max = lm;
   }
 #endif
