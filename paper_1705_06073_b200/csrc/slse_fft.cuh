@@ -105,13 +105,16 @@ SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const 
       const int base = ((u >> lgh) << (lgh + 2)) + pos;
       cplx x0 = xc[base], x1 = xc[base + h], x2 = xc[base + 2 * h], x3 = xc[base + 3 * h];
       // stage span 2h
-      cplx w1 = twid_tab(tw, twlog, pos, lgh + 1, sign);
+      // one table load per butterfly: W_{4h}^{pos}, and W_{2h}^{pos} as its square
+      // (the tables of large passes do not stay in the small L1 beside a big
+      // shared-memory carve-out)
+      cplx w2 = twid_tab(tw, twlog, pos, lgh + 2, sign);
+      cplx w1 = cmul(w2, w2);
       cplx t1 = cmul(w1, x1);
       cplx a0 = cadd(x0, t1), a1 = csub(x0, t1);
       cplx t3 = cmul(w1, x3);
       cplx a2 = cadd(x2, t3), a3 = csub(x2, t3);
       // stage span 4h: W^{pos} and W^{pos+h} = (-+ i) W^{pos}
-      cplx w2 = twid_tab(tw, twlog, pos, lgh + 2, sign);
       cplx u2 = cmul(w2, a2);
       cplx u3 = cmul(w2, a3);
       u3 = (sign < 0) ? mk(u3.im, -u3.re) : mk(-u3.im, u3.re);
