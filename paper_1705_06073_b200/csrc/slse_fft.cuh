@@ -75,22 +75,30 @@ SLSE_D void fft_barrier() { SLSE_GROUP_SYNC(); }
 
 // DIT passes over `count` contiguous bit-reversed buffers of n points
 // (one barrier per pass for all of them).
-template <bool SH>
+// Swizzled staging layout (fft_multi's staged path): point idx of a 2^p
+// buffer lives at idx ^ (top 3 bits of idx), so the bit-reversed scatter of
+// 8 consecutive points lands in 8 different 16-byte bank groups instead of
+// one (a 32-way serialisation otherwise).
+SLSE_HD int fswz(int idx, int p) { return p >= 3 ? (idx ^ ((idx >> (p - 3)) & 7)) : idx; }
+
+template <bool SH, bool SWZ = false>
 SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
                                   int tid, int nt) {
 #ifndef SLSE_HOST_EMU
   if constexpr (SH) __builtin_assume(__isShared(x));  // LDS / STS instead of generic LD / ST
 #endif
   const int p = ilog2(n);
+  const auto at = [p](int i) { return SWZ ? fswz(i, p) : i; };
   int lgh = 0;  // log2 of current half-span
   if (p & 1) {
     const int per = n >> 1;
     for (int t = tid; t < count * per; t += nt) {
       const int c = t >> (p - 1), u = t & (per - 1);
       cplx* xc = x + (size_t)c * n;
-      cplx x0 = xc[2 * u], x1 = xc[2 * u + 1];
-      xc[2 * u] = cadd(x0, x1);
-      xc[2 * u + 1] = csub(x0, x1);
+      const int i0 = at(2 * u), i1 = at(2 * u + 1);
+      cplx x0 = xc[i0], x1 = xc[i1];
+      xc[i0] = cadd(x0, x1);
+      xc[i1] = csub(x0, x1);
     }
     fft_barrier();
     lgh = 1;
@@ -103,7 +111,8 @@ SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const 
       cplx* xc = x + (size_t)c * n;
       const int pos = u & (h - 1);
       const int base = ((u >> lgh) << (lgh + 2)) + pos;
-      cplx x0 = xc[base], x1 = xc[base + h], x2 = xc[base + 2 * h], x3 = xc[base + 3 * h];
+      const int j0 = at(base), j1 = at(base + h), j2 = at(base + 2 * h), j3 = at(base + 3 * h);
+      cplx x0 = xc[j0], x1 = xc[j1], x2 = xc[j2], x3 = xc[j3];
       // stage span 2h
       // one table load per butterfly: W_{4h}^{pos}, and W_{2h}^{pos} as its square
       // (the tables of large passes do not stay in the small L1 beside a big
@@ -118,10 +127,10 @@ SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const 
       cplx u2 = cmul(w2, a2);
       cplx u3 = cmul(w2, a3);
       u3 = (sign < 0) ? mk(u3.im, -u3.re) : mk(-u3.im, u3.re);
-      xc[base] = cadd(a0, u2);
-      xc[base + 2 * h] = csub(a0, u2);
-      xc[base + h] = cadd(a1, u3);
-      xc[base + 3 * h] = csub(a1, u3);
+      xc[j0] = cadd(a0, u2);
+      xc[j2] = csub(a0, u2);
+      xc[j1] = cadd(a1, u3);
+      xc[j3] = csub(a1, u3);
     }
     fft_barrier();
   }
@@ -139,6 +148,14 @@ SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx
 #endif
   fft_passes_multi_impl<false>(x, count, n, sign, tw, twlog, tid, nt);
 }
+
+#ifndef SLSE_HOST_EMU
+// passes over shared staging in the swizzled layout (fswz)
+SLSE_NI void fft_passes_multi_swz(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                                  int tid, int nt) {
+  fft_passes_multi_impl<true, true>(x, count, n, sign, tw, twlog, tid, nt);
+}
+#endif
 
 SLSE_D void fft_passes_v(cplx* x, int n, double sign, const cplx* __restrict__ tw, int twlog, int tid, int nt) {
   fft_passes_multi(x, 1, n, sign, tw, twlog, tid, nt);
@@ -487,6 +504,9 @@ SLSE_D void fft(cplx* work, int n, double sign, Load ld, Store st, const FftCtx&
   }
 }
 
+#ifndef SLSE_MULTI_SWZ
+#define SLSE_MULTI_SWZ 1
+#endif
 // `count` transforms of n points at once: ld(c, i) -> FFT -> st(c, i, v).
 // Staged in shared memory when count*n fits, else in `work` (count*n,
 // global; the loader must not read `work`).
@@ -539,18 +559,28 @@ SLSE_D void fft_multi(cplx* work, int count, int n, double sign, Load ld, Store 
     return;
   }
   const int g = n <= f.smem_cap ? (f.smem_cap / n < count ? f.smem_cap / n : count) : count;
+#if SLSE_MULTI_SWZ && !defined(SLSE_HOST_EMU)
+  const bool swz = n <= f.smem_cap;  // staged in shared memory: swizzled layout
+#else
+  const bool swz = false;
+#endif
   cplx* x = n <= f.smem_cap ? f.smem : work;
   for (int c0 = 0; c0 < count; c0 += g) {
     const int gc = count - c0 < g ? count - c0 : g;
     for (int t = tid; t < gc * n; t += nt) {
       const int c = t >> p, i = t & (n - 1);
-      x[(size_t)c * n + brev_bits((unsigned)i, p)] = ld(c0 + c, i);
+      const int j = (int)brev_bits((unsigned)i, p);
+      x[(size_t)c * n + (swz ? fswz(j, p) : j)] = ld(c0 + c, i);
     }
     fft_barrier();
+#if SLSE_MULTI_SWZ && !defined(SLSE_HOST_EMU)
+    if (swz) fft_passes_multi_swz(x, gc, n, sign, f.tw, f.twlog, tid, nt);
+    else
+#endif
     fft_passes_multi(x, gc, n, sign, f.tw, f.twlog, tid, nt);
     for (int t = tid; t < gc * n; t += nt) {
       const int c = t >> p, i = t & (n - 1);
-      st(c0 + c, i, x[(size_t)c * n + i]);
+      st(c0 + c, i, x[(size_t)c * n + (swz ? fswz(i, p) : i)]);
     }
     fft_barrier();
   }
