@@ -81,20 +81,29 @@ SLSE_D void fft_barrier() { SLSE_GROUP_SYNC(); }
 // one (a 32-way serialisation otherwise).
 SLSE_HD int fswz(int idx, int p) { return p >= 3 ? (idx ^ ((idx >> (p - 3)) & 7)) : idx; }
 
-template <bool SH, bool SWZ = false>
+// SWZ: 0 natural, 1 fswz within each buffer, 2 XOR with the buffer index
+// (the four-step path's column groups, whose scatter strides by a buffer)
+template <bool SH, int SWZ = 0>
 SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
                                   int tid, int nt) {
 #ifndef SLSE_HOST_EMU
   if constexpr (SH) __builtin_assume(__isShared(x));  // LDS / STS instead of generic LD / ST
 #endif
   const int p = ilog2(n);
-  const auto at = [p](int i) { return SWZ ? fswz(i, p) : i; };
+  int cur_c = 0;
+  const auto at = [p, &cur_c](int i) {
+    if (SWZ == 1) return fswz(i, p);
+    if (SWZ == 2) return p >= 3 ? (i ^ (cur_c & 7)) : i;
+    if (SWZ == 3) return p >= 3 ? (fswz(i, p) ^ (cur_c & 7)) : i;
+    return i;
+  };
   int lgh = 0;  // log2 of current half-span
   if (p & 1) {
     const int per = n >> 1;
     for (int t = tid; t < count * per; t += nt) {
       const int c = t >> (p - 1), u = t & (per - 1);
       cplx* xc = x + (size_t)c * n;
+      cur_c = c;
       const int i0 = at(2 * u), i1 = at(2 * u + 1);
       cplx x0 = xc[i0], x1 = xc[i1];
       xc[i0] = cadd(x0, x1);
@@ -109,6 +118,7 @@ SLSE_D void fft_passes_multi_impl(cplx* x, int count, int n, double sign, const 
     for (int t = tid; t < count * per; t += nt) {
       const int c = t >> (p - 2), u = t & (per - 1);
       cplx* xc = x + (size_t)c * n;
+      cur_c = c;
       const int pos = u & (h - 1);
       const int base = ((u >> lgh) << (lgh + 2)) + pos;
       const int j0 = at(base), j1 = at(base + h), j2 = at(base + 2 * h), j3 = at(base + 3 * h);
@@ -153,7 +163,17 @@ SLSE_NI void fft_passes_multi(cplx* x, int count, int n, double sign, const cplx
 // passes over shared staging in the swizzled layout (fswz)
 SLSE_NI void fft_passes_multi_swz(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
                                   int tid, int nt) {
-  fft_passes_multi_impl<true, true>(x, count, n, sign, tw, twlog, tid, nt);
+  fft_passes_multi_impl<true, 1>(x, count, n, sign, tw, twlog, tid, nt);
+}
+// both: fswz within the buffer, then XOR by (c & 7) (the four-step rows)
+SLSE_NI void fft_passes_multi_rswz(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                                   int tid, int nt) {
+  fft_passes_multi_impl<true, 3>(x, count, n, sign, tw, twlog, tid, nt);
+}
+// passes over shared staging with buffer c's points XORed by (c & 7) (n >= 8)
+SLSE_NI void fft_passes_multi_bswz(cplx* x, int count, int n, double sign, const cplx* __restrict__ tw, int twlog,
+                                   int tid, int nt) {
+  fft_passes_multi_impl<true, 2>(x, count, n, sign, tw, twlog, tid, nt);
 }
 #endif
 
@@ -528,30 +548,50 @@ SLSE_D void fft_multi(cplx* work, int count, int n, double sign, Load ld, Store 
     for (int c = 0; c < count; ++c) {
       cplx* wc = work + (size_t)c * n;
       for (int j0 = 0; j0 < n2; j0 += G) {  // columns j2 = j0 .. j0+G-1
+        // column g's points XORed by (g & 7): the strided scatter / gather
+        // over consecutive g then spreads over the shared-memory banks
+#ifndef SLSE_HOST_EMU
+        const auto bx = [](int g, int i) { return i ^ (g & 7); };
+#else
+        const auto bx = [](int, int i) { return i; };  // (the emulation's passes are unswizzled)
+#endif
         for (int t = tid; t < G * n1; t += nt) {
           const int j1 = t / G, g = t - j1 * G;  // consecutive threads -> consecutive j2 (coalesced)
-          x[(size_t)g * n1 + brev_bits((unsigned)j1, p1)] = ld(c, (j0 + g) + n2 * j1);
+          x[(size_t)g * n1 + bx(g, (int)brev_bits((unsigned)j1, p1))] = ld(c, (j0 + g) + n2 * j1);
         }
         fft_barrier();
+#ifndef SLSE_HOST_EMU
+        fft_passes_multi_bswz(x, G, n1, sign, f.tw, f.twlog, tid, nt);
+#else
         fft_passes_multi(x, G, n1, sign, f.tw, f.twlog, tid, nt);
+#endif
         for (int t = tid; t < G * n1; t += nt) {
           const int k1 = t / G, g = t - k1 * G;
           const int j2 = j0 + g;
-          const cplx v = cmul(x[(size_t)g * n1 + k1], twid_tab(f.tw, f.twlog, (j2 * k1) & (n - 1), p, sign));
+          const cplx v = cmul(x[(size_t)g * n1 + bx(g, k1)], twid_tab(f.tw, f.twlog, (j2 * k1) & (n - 1), p, sign));
           wc[(size_t)k1 * n2 + j2] = v;
         }
         fft_barrier();
       }
       for (int k0 = 0; k0 < n1; k0 += G) {  // rows k1 = k0 .. k0+G-1
+#ifndef SLSE_HOST_EMU
+        const auto rx = [p2](int g, int i) { return p2 >= 3 ? (fswz(i, p2) ^ (g & 7)) : i; };
+#else
+        const auto rx = [](int, int i) { return i; };
+#endif
         for (int t = tid; t < G * n2; t += nt) {
           const int g = t >> p2, j2 = t & (n2 - 1);
-          x[(size_t)g * n2 + brev_bits((unsigned)j2, p2)] = wc[(size_t)(k0 + g) * n2 + j2];
+          x[(size_t)g * n2 + rx(g, (int)brev_bits((unsigned)j2, p2))] = wc[(size_t)(k0 + g) * n2 + j2];
         }
         fft_barrier();
+#ifndef SLSE_HOST_EMU
+        fft_passes_multi_rswz(x, G, n2, sign, f.tw, f.twlog, tid, nt);
+#else
         fft_passes_multi(x, G, n2, sign, f.tw, f.twlog, tid, nt);
+#endif
         for (int t = tid; t < G * n2; t += nt) {
           const int k2 = t / G, g = t - k2 * G;  // consecutive threads -> consecutive k1 (coalesced)
-          st(c, (k0 + g) + n1 * k2, x[(size_t)g * n2 + k2]);
+          st(c, (k0 + g) + n1 * k2, x[(size_t)g * n2 + rx(g, k2)]);
         }
         fft_barrier();
       }
