@@ -76,10 +76,16 @@ SLSE_D void fft_barrier() { SLSE_GROUP_SYNC(); }
 // DIT passes over `count` contiguous bit-reversed buffers of n points
 // (one barrier per pass for all of them).
 // Swizzled staging layout (fft_multi's staged path): point idx of a 2^p
-// buffer lives at idx ^ (top 3 bits of idx), so the bit-reversed scatter of
-// 8 consecutive points lands in 8 different 16-byte bank groups instead of
-// one (a 32-way serialisation otherwise).
-SLSE_HD int fswz(int idx, int p) { return p >= 3 ? (idx ^ ((idx >> (p - 3)) & 7)) : idx; }
+// buffer lives at idx ^ ((bits 2..4) ^ (top 3 bits)), so the bit-reversed
+// scatter of 8 consecutive points lands in 8 different 16-byte bank groups
+// instead of one (a 32-way serialisation otherwise).
+// The XOR also takes bits 2..4, which spreads the strided
+// accesses of the first radix-4 passes (half-spans 1 and 4) too; the map
+// stays a bijection because only bits >= 2 feed the low three.
+SLSE_HD int fswz(int idx, int p) {
+  // (below 2^6 points the top bits overlap the low three: no swizzle)
+  return p >= 6 ? (idx ^ (((idx >> 2) ^ (idx >> (p - 3))) & 7)) : idx;
+}
 
 // SWZ: 0 natural, 1 fswz within each buffer, 2 XOR with the buffer index
 // (the four-step path's column groups, whose scatter strides by a buffer)
