@@ -145,7 +145,7 @@ SLSE_NI void dnc_leaf(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T,
       const cplx ej1 = shfl_c(ej, 1), bj1 = shfl_c(bj, 1);
       const cplx kc = conjg(k);
       const double dn = d * (1.0 - (k.re * k.re + k.im * k.im));
-      const double invn = __drcp_rn(dn);  // == 1.0 / dn (both correctly rounded)
+      const double invn = rcp_pos(dn);
       const cplx enext = cadd(ej1, cmul(k, bj1));
       const cplx knext = mk(-enext.re * invn, -enext.im * invn);
       const cplx en = cadd(ej, cmul(k, bj));
@@ -242,7 +242,7 @@ SLSE_NI void dnc_leaf_block(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cp
       e[t + tid] = en;
       bb[tid] = cadd(bj, cmul(kc, ej));
       if (tid == 1) {
-        const double invn = __drcp_rn(dn);
+        const double invn = rcp_pos(dn);
         kb[(t + 1) & 1] = mk(-en.re * invn, -en.im * invn);
       }
     }
@@ -321,7 +321,7 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
     if (s > 1) {
       const double d1 = d * (1.0 - (k0.re * k0.re + k0.im * k0.im));
       const cplx en = cadd(E1[1], cmul(k0, Bw[1]));
-      const double inv1 = __drcp_rn(d1);
+      const double inv1 = rcp_pos(d1);
       kb[1] = mk(-en.re * inv1, -en.im * inv1);
     }
   }
@@ -358,11 +358,11 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
           const cplx b1_2 = cadd(b2s, cmul(kac, e2s));
           const cplx e1h_3 = cadd(e3s, cmul(ka, b3s));
           const cplx e2_2 = cadd(e1h_3, cmul(kk, b1_2));  // e^{(t+2)}_{t+3}
-          const double inv2 = __drcp_rn(d2);
+          const double inv2 = rcp_pos(d2);
           const cplx kn0 = mk(-e2.re * inv2, -e2.im * inv2);
           const double d3 = d2 * (1.0 - (kn0.re * kn0.re + kn0.im * kn0.im));
           const cplx e3n = cadd(e2_2, cmul(kn0, b2));  // e^{(t+3)}_{t+3}
-          const double inv3 = __drcp_rn(d3);
+          const double inv3 = rcp_pos(d3);
           kb[2 * Q] = kn0;
           kb[2 * Q + 1] = mk(-e3n.re * inv3, -e3n.im * inv3);
         }
@@ -494,7 +494,7 @@ SLSE_NI void dnc_leaf_regs(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cpl
       const cplx en = mk(fma(kr, bj.re, fma(-ki, bj.im, ej.re)), fma(kr, bj.im, fma(ki, bj.re, ej.im)));
       bj = mk(fma(kr, ej.re, fma(ki, ej.im, bj.re)), fma(kr, ej.im, fma(-ki, ej.re, bj.im)));
       if (tid == 1) {
-        const double invn = __drcp_rn(dn);
+        const double invn = rcp_pos(dn);
         kb[(t + 1) & 1] = mk(-en.re * invn, -en.im * invn);
       }
       if (lane == 0 && wh > 0) bnd[q * nwg + wh] = en;

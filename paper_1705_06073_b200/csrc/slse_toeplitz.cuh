@@ -176,7 +176,7 @@ SLSE_D Factor toeplitz_factor_impl(const cplx* SLSE_RESTRICT c, int n, cplx* e, 
     const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
     // 1 / delta_{m+1}, formed before the step's updates so the next
     // coefficient after the barrier is a load and a multiply
-    const double inv_next = rcp_rn(dnext);
+    const double inv_next = rcp_pos(dnext);
     cplx knext = mk(0.0, 0.0);
     if (look && m + 2 < n) {
       const cplx e2 = e[m + 2], b1 = B[1];
@@ -295,7 +295,7 @@ SLSE_D Factor toeplitz_factor_warp(const cplx* SLSE_RESTRICT c, int n, cplx* E, 
     const double dnext = delta * (1.0 - (k.re * k.re + k.im * k.im));
     // 1 / delta_{m+1}, formed before the step's updates so the next
     // coefficient after the barrier is a load and a multiply
-    const double inv_next = __drcp_rn(dnext);  // == 1.0 / dnext
+    const double inv_next = rcp_pos(dnext);
     cplx knext = mk(0.0, 0.0);
     if (m + 2 < n) {  // lookahead from pre-update values
       const cplx e2 = E[m + 2];
@@ -357,7 +357,7 @@ SLSE_D void lev_regs_step(cplx (&Er)[Q], cplx (&Br)[Q], cplx& k, double& delta, 
                           double* delta_tmp) {
   const double kr = k.re, ki = k.im;
   const double dnext = delta * (1.0 - (kr * kr + ki * ki));
-  const double inv = __drcp_rn(dnext);
+  const double inv = rcp_pos(dnext);
   const int top = n - 2 - m;
   const bool mine = (top - (Q - 1 - T)) == Q * lane;  // this lane owns the retiring slot
 #pragma unroll
@@ -533,7 +533,7 @@ SLSE_D Factor toeplitz_factor_regs_c(const cplx* SLSE_RESTRICT c, int n, double*
 #pragma unroll 1
   for (int m = 0; m + 1 < n; ++m) {
     const double dnext = delta * (1.0 - (kr * kr + ki * ki));
-    const double inv = __drcp_rn(dnext);
+    const double inv = rcp_pos(dnext);
     const int toff = n - 2 - m - base;  // retiring generator slot, if this lane owns it
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
@@ -631,7 +631,7 @@ SLSE_D Factor toeplitz_factor_regs_blk(const cplx* SLSE_RESTRICT c, int n, cplx*
 #pragma unroll 1
   for (int m = 0; m + 1 < n; ++m) {
     const double dnext = delta * (1.0 - (kr * kr + ki * ki));
-    const double inv = __drcp_rn(dnext);
+    const double inv = rcp_pos(dnext);
     const int toff = n - 2 - m - base;  // retiring generator slot, if this thread owns it
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
@@ -689,7 +689,7 @@ template <int Q, int T>
 SLSE_D void lev_blk_step(cplx (&Er)[Q], cplx (&Br)[Q], double& kr, double& ki, double& delta, int m, int n, int tid,
                          int lane, int warp, int nw, cplx* kbuf, cplx* bnd, double* delta_tmp, Blk& b) {
   const double dnext = delta * (1.0 - (kr * kr + ki * ki));
-  const double inv = __drcp_rn(dnext);
+  const double inv = rcp_pos(dnext);
   const int top = n - 2 - m;
   const bool mine = (top - (Q - 1 - T)) == Q * tid;  // this thread owns the retiring slot
 #pragma unroll
