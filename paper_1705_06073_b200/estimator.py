@@ -283,25 +283,26 @@ class BatchSolver:
         _native.check(rc, "slse_estimate_batch_mmv")
 
     def _d2h(self, tensors: dict) -> dict:
-        """Asynchronous copies into this solver's pinned staging (allocated
-        once, sized for every output), one stream sync, then host copies the
-        caller owns (the staging is reused by the next call)."""
+        """Asynchronous copies into one fresh pinned block and one stream
+        sync.  The returned arrays are views of that block and keep it alive;
+        once the caller drops them, torch's caching host allocator hands the
+        block to the next call, so steady-state calls neither pin new memory
+        nor copy (or page-fault) the outputs a second time on the host."""
         torch = _torch()
         st = torch.cuda.current_stream(self.device)
-        if getattr(self, "_pinned", None) is None:
-            total = sum(t.numel() * t.element_size() for t in vars(self.out).values() if isinstance(t, torch.Tensor))
-            self._pinned = torch.empty(total + 64 * 32, dtype=torch.uint8, pin_memory=True)
+        ts = {name: t.contiguous() for name, t in tensors.items()}
+        span = {name: (t.numel() * t.element_size() + 63) // 64 * 64 for name, t in ts.items()}
+        buf = torch.empty(max(64, sum(span.values())), dtype=torch.uint8, pin_memory=True)
         off = 0
         host = {}
-        for name, t in tensors.items():
-            t = t.contiguous()
+        for name, t in ts.items():
             nb = t.numel() * t.element_size()
-            hb = self._pinned[off:off + nb].view(t.dtype).view(t.shape)
+            hb = buf[off:off + nb].view(t.dtype).view(t.shape)
             hb.copy_(t, non_blocking=True)
             host[name] = hb
-            off += (nb + 63) // 64 * 64
+            off += span[name]
         st.synchronize()
-        return {name: hb.numpy().copy() for name, hb in host.items()}
+        return {name: hb.numpy() for name, hb in host.items()}
 
     def host_outputs(self) -> dict:
         """Host copies, trimmed to the longest trace / history / model order
