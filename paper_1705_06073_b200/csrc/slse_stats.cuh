@@ -298,6 +298,14 @@ SLSE_NI bool grid_gain_fused(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RES
   const double c2n = 2.0 - (double)n;
   const double inv_d = 1.0 / delta_last;
   cplx* x = f.smem;
+#ifndef SLSE_HOST_EMU
+  // shared staging in the swizzled layout (fswz): the bit-reversed scatter
+  // is otherwise a 32-way bank conflict, and the first radix-4 passes 2-way
+  __builtin_assume(__isShared(x));
+  const auto gz = [p](int i) { return fswz(i, p); };
+#else
+  const auto gz = [](int i) { return i; };
+#endif
   for (int r = 0; r < R; ++r) {
     for (int t = tid; t < 3 * M; t += nt) {
       const int c = t >> p, i = t & (M - 1);
@@ -307,13 +315,18 @@ SLSE_NI bool grid_gain_fused(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RES
         const cplx src = c == 0 ? w[i] : (c == 1 ? rho[i] : cscale(rho[i], (double)i));
         v = r ? cmul(src, tw) : src;
       }
-      x[(size_t)c * M + brev_bits((unsigned)i, p)] = v;
+      x[(size_t)c * M + gz(brev_bits((unsigned)i, p))] = v;
     }
     fft_barrier();
+#ifndef SLSE_HOST_EMU
+    fft_passes_multi_swz(x, 3, M, -1.0, f.tw, f.twlog, tid, nt);
+#else
     fft_passes_multi(x, 3, M, -1.0, f.tw, f.twlog, tid, nt);
+#endif
     for (int m = tid; m < M; m += nt) {
       const int l = m * R + r;
-      const cplx q = x[m], a0 = x[M + m], a1 = x[2 * M + m];
+      const int ms = gz(m);
+      const cplx q = x[ms], a0 = x[M + ms], a1 = x[2 * M + ms];
       const double s = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
       const double qq = cabs2(q);
       sg[l] = s;
