@@ -641,7 +641,7 @@ SLSE_D Factor toeplitz_factor_regs_blk(const cplx* SLSE_RESTRICT c, int n, cplx*
       Br[i] = (i == toff) ? mk(kr, -ki) : bn;  // b_{m+1}[0] = conj(k)
     }
     // thread 0 holds slot 1 = the updated e_{m+2}: the next pivot
-    if (tid == 0) kbuf[(m + 1) & 1] = mk(-Er[1].re * inv, -Er[1].im * inv);
+    if (tid == 0) kbuf[(m + 1) & 1] = Er[1];  // raw: scaled by 1/delta after the barrier
     if (lane == 0 && warp > 0) bnd[(m & 1) * nw + warp] = Er[0];
     const double sr = __shfl_down_sync(0xffffffffu, Er[0].re, 1);
     const double si = __shfl_down_sync(0xffffffffu, Er[0].im, 1);
@@ -655,8 +655,8 @@ SLSE_D Factor toeplitz_factor_regs_blk(const cplx* SLSE_RESTRICT c, int n, cplx*
     delta = dnext;
     if (!(delta > floor_)) { fail = 1; break; }  // uniform
     const cplx kn = kbuf[(m + 1) & 1];
-    kr = kn.re;
-    ki = kn.im;
+    kr = -kn.re * inv;
+    ki = -kn.im * inv;
   }
   if (fail) {
     F.status = kNotPD;
@@ -703,7 +703,7 @@ SLSE_D void lev_blk_step(cplx (&Er)[Q], cplx (&Br)[Q], double& kr, double& ki, d
   }
   if (tid == 0) {  // slot 1 = the updated e_{m+2}: the next pivot
     const cplx e2 = Er[(1 + T) % Q];
-    kbuf[(m + 1) & 1] = mk(-e2.re * inv, -e2.im * inv);
+    kbuf[(m + 1) & 1] = e2;  // raw: every thread scales it by its own 1/delta after the barrier
   }
   constexpr int p0 = T % Q;
   if (lane == 0 && warp > 0) bnd[(m & 1) * nw + warp] = Er[p0];
@@ -714,8 +714,8 @@ SLSE_D void lev_blk_step(cplx (&Er)[Q], cplx (&Br)[Q], double& kr, double& ki, d
   Er[p0] = (lane == 31) ? ((warp + 1 < nw) ? bnd[(m & 1) * nw + warp + 1] : mk(0.0, 0.0)) : mk(sr, si);
   delta = dnext;
   const cplx kn = kbuf[(m + 1) & 1];
-  kr = kn.re;
-  ki = kn.im;
+  kr = -kn.re * inv;
+  ki = -kn.im * inv;
 }
 
 template <int Q, int T>
