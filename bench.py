@@ -6,16 +6,28 @@ independent problems, N = 256 complex128 samples, K = 16 sinusoids,
 min separation 1.5/N, CN(0,1) amplitudes, SNR 15 dB, grid 4N.
 
 One "step" = one full solve of the batch (every problem to convergence)
-by the persistent solver kernel, inputs resident in HBM.  The JSON line
-also carries:
-  e2e          the same metric through the public API estimate_batch() with
-               host numpy input/outputs (H2D + solve + D2H + unpack);
+by the persistent solver kernel, inputs resident in HBM, L2 flushed
+between steps.  The JSON line also carries:
+
+  e2e          the same metric through the public API: estimate_batch() on
+               a pinned host tensor (H2D of y + solve + D2H of every
+               estimate into the SoA BatchResult), and ``e2e_numpy``: a
+               pageable numpy batch in and one LseResult per problem out;
+               at N > 1 GPUs the public multi-GPU entry
+               dist.estimate_batch_distributed (shard, solve, all-gather);
   roofline     the activation-grid kernel (BASELINE metric "grid-eval HBM
-               GB/s vs peak"), timed live over the same batch;
-  cpu_baseline the CPU oracle port (oracle/) on a bounded sample, on this
-               host's cores (rank 0, N = 1 only).
-Multi-GPU (torchrun): each rank solves its own 4096 problems (weak scaling,
-no data-path collective); time = max over ranks.
+               GB/s vs peak") timed live at the config's shape, on a batch
+               whose outputs exceed L2 (so DRAM traffic = algorithmic bytes);
+  per_config   every BASELINE config (cfg1-5) solved in full on this GPU:
+               problems/s, ms per batch, its grid roofline, and the real
+               reference's CPU rate on a bounded sample (N = 1 only);
+  cpu_baseline the REAL reference (baseline/_ref, installed by
+               tools/install_reference.sh) on a bounded sample on this
+               host's cores (rank 0, N = 1 only); the oracle port if absent.
+
+Multi-GPU (torchrun): weak scaling -- the job is world x 4096 problems,
+rank r solves its own slice (no data-path collective); time = max over
+ranks.  ``strong`` adds the fixed 4096-problem batch sharded over the ranks.
 """
 
 from __future__ import annotations
@@ -33,8 +45,13 @@ import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
 
 SEED = 20261019
+METRIC = "LSE problems solved/sec to convergence"
+# per_config (warmup, timed steps): one step = one full config batch
+CONFIG_STEPS = {1: (3, 10), 2: (2, 5), 3: (2, 5), 4: (1, 3), 5: (1, 2)}
+L2_BYTES = 126 * 1024 * 1024
 
 
 def parse():
@@ -45,8 +62,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--batch", type=int, default=None, help="override problems per GPU")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU legs")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the per_config block")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--per-config-cpu", default="1,2,3",
+                    help="configs whose real-reference CPU rate goes into per_config (cfg4/5 take minutes)")
     return ap.parse_args()
 
 
@@ -57,42 +77,86 @@ def dist_env():
     return rank, world, local
 
 
-# ------------------------------------------------------------------ CPU leg
+def config_dict(cfg, world, batch):
+    """Identical in both arms (the driver compares them)."""
+    from paper_1705_06073_b200 import simdata
+
+    _, n, k, sep, law, snr = simdata.CONFIGS[cfg]
+    return {"workload": f"cfg{cfg}", "batch": batch, "N": n, "K": k, "min_sep": f"{sep}/N", "amplitudes": law,
+            "snr_db": snr, "grid": "4N", "parallelism": f"dp{world} (independent problems)",
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+# ------------------------------------------------------------------ CPU legs
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "superlse"))
+
+
 def _cpu_worker(args):
-    seed, cfg, b = args
+    """One problem through the CPU reference path: the REAL reference
+    (baseline/_ref: superlse.estimate(Observation.complete(y),
+    EstimatorOptions(backend="superfast", grid_factor=4)), estimator.py:117)
+    or, without it, the oracle port."""
+    seed, cfg, b, kind = args
     from threadpoolctl import threadpool_limits
 
     threadpool_limits(1)  # one BLAS thread per worker process
-    from oracle import superlse_oracle as O
     from paper_1705_06073_b200 import simdata
 
     y, _ = simdata.problem(seed, cfg, b)
+    if kind == "reference":
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import superlse
+
+        t = time.perf_counter()
+        r = superlse.estimate(superlse.Observation.complete(y),
+                              superlse.EstimatorOptions(backend="superfast", grid_factor=4))
+        return time.perf_counter() - t, r.k_hat
+    from oracle import superlse_oracle as O
+
     t = time.perf_counter()
     r = O.estimate(y, O.OracleOptions(grid_factor=4))
     return time.perf_counter() - t, r.k_hat
 
 
-def cpu_baseline(cfg, seconds, start=0):
-    """Oracle port (numpy restatement of the reference loop) over a pool of
-    all host cores; the sample size is chosen for ~`seconds` of wall time."""
-    import multiprocessing as mp
+class CpuPool:
+    """multiprocessing pool of all host cores, single-thread workers."""
 
-    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ[v] = "1"
-    cores = os.cpu_count() or 1
-    t1, _ = _cpu_worker((SEED, cfg, start))  # warm + size the sample
-    per_core = max(1, int(seconds / max(t1, 1e-3)))
-    count = max(cores, per_core * cores)
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, [(SEED, cfg, start + i) for i in range(cores)])  # one warm-up per worker
+    def __init__(self, kind):
+        import multiprocessing as mp
+
+        for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[v] = "1"
+        self.kind = kind
+        self.cores = os.cpu_count() or 1
+        self.pool = mp.get_context("fork").Pool(self.cores)
+
+    def run(self, cfg, idx):
         t = time.perf_counter()
-        out = pool.map(_cpu_worker, [(SEED, cfg, start + i) for i in range(count)], chunksize=1)
-        wall = time.perf_counter() - t
+        out = self.pool.map(_cpu_worker, [(SEED, cfg, int(b), self.kind) for b in idx], chunksize=1)
+        return time.perf_counter() - t, out
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_sample(pool, cfg, seconds, batch):
+    """Rate of the CPU path on a bounded sample of cfg's batch (problems
+    0.., the same indices the GPU solves), ~`seconds` of wall time."""
+    pool.run(cfg, range(pool.cores))  # warm every worker (imports, FFT plans)
+    t1 = pool.run(cfg, [0])[0]
+    rounds = max(1, int(seconds / max(t1, 1e-3)))
+    count = min(batch, max(pool.cores, rounds * pool.cores)) if batch >= pool.cores else batch
+    wall, out = pool.run(cfg, range(count))
     mean_s = float(np.mean([o[0] for o in out]))
-    return dict(value=count / wall, unit="problems/s", cores=cores, kind="port",
-                sample=f"{count} cfg{cfg} problems (seeded, problems {start}..{start + count - 1}), "
-                       f"multiprocessing pool of {cores} single-thread workers, mean {mean_s:.3f} s/problem")
+    what = "real reference superlse (baseline/_ref)" if pool.kind == "reference" else "oracle port"
+    return dict(value=count / wall, unit="problems/s", cores=pool.cores, kind=pool.kind,
+                sample=f"{count} of the {batch} cfg{cfg} problems (indices 0..{count - 1}), {what}, "
+                       f"multiprocessing pool of {pool.cores} single-thread workers, "
+                       f"wall {wall:.2f} s, mean {mean_s:.3f} s/problem/core",
+                ms_wall=1000.0 * wall, count=count)
 
 
 # ------------------------------------------------------------------ clocks
@@ -144,37 +208,144 @@ class ClockSampler:
 def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
-# ------------------------------------------------------------------ main arms
+# FP64 DFMA peak measured on this pool's B200 (tools/micro/fp64_peak.cu -> profiles/r1_fp64_peak.txt)
+def fp64_peak_tflops():
+    with open(os.path.join(REPO, "profiles", "r1_fp64_peak.txt")) as f:
+        return float(json.loads(f.readline())["fp64_dfma_tflops"]), "measured DFMA loop (profiles/r1_fp64_peak.txt)"
+
+
+# ------------------------------------------------------------------ helpers
+def time_steps(torch, stream, fn, steps, warmup, flush):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        ev[i][0].record(stream)
+        fn()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def grid_roofline(torch, dev, stream, flush, n, launches=10):
+    """Row 9 (model_core.py:303-313) standalone at the config's shape, on a
+    batch whose q^G / s^G outputs (24 L bytes per problem) exceed 2x the L2,
+    so every byte reaches DRAM inside the launch; CUDA events on the
+    launching stream, L2 flushed before each launch."""
+    from paper_1705_06073_b200 import ops
+
+    L = 4 * n
+    per = 32 * n + 24 * L  # SURVEY 8(d): 16N (w) + 16N (rho) in, 16L (q^G) + 8L (s^G) out
+    B = max(1, -(-2 * L2_BYTES // (24 * L)))
+    B = max(B, 148)  # at least one problem per SM
+    g = torch.Generator(device=dev).manual_seed(1)
+    rho = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
+    w = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
+    dl = torch.rand(B, dtype=torch.float64, device=dev, generator=g) + 0.5
+    qg = torch.empty((B, L), dtype=torch.complex128, device=dev)
+    sg = torch.empty((B, L), dtype=torch.float64, device=dev)
+    ms = time_steps(torch, stream, lambda: ops.grid_eval(rho, dl, w, L, out=(qg, sg)), launches, 3, flush)
+    del rho, w, qg, sg
+    grid_ms = float(np.mean(ms))
+    alg = B * per
+    achieved = alg / (grid_ms / 1000.0) / 1e9
+    peaks, peak_src = measured_peaks()
+    flops = B * 15 * L * int(np.log2(L))  # SURVEY 8(d): 3 complex FFTs of L at 5 L log2 L
+    fp64_tf = flops / (grid_ms / 1000.0) / 1e12
+    fp64_peak, fp64_src = fp64_peak_tflops()
+    attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
+    if L == 1024 and 128 < n <= 256:
+        kname = "grid_tma_kernel"
+    elif L == 1024:
+        kname = "grid_fused_kernel"
+    elif L <= 4096:
+        kname = "grid_stockham_kernel"
+    else:
+        kname = "grid_kernel"
+    traffic = None
+    tf = os.path.join(REPO, "profiles", f"r2_{kname}_n{n}.json")
+    if os.path.exists(tf):  # DRAM bytes per launch from the committed ncu --set full capture of this shape
+        with open(tf) as fh:
+            t = json.load(fh)
+        if int(t.get("batch", -1)) == B:
+            traffic = int(t["traffic_bytes_per_launch"])
+    return {"bound": "hbm", "kernel": f"{kname} (activation grid, SURVEY 8(a) row 9)",
+            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "traffic": traffic, "peak_source": peak_src, "batch": B, "alg_bytes_per_problem": per,
+            "alg_bytes_per_launch": alg, "launch_ms": grid_ms, "flops_per_launch": flops,
+            "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "peak_source": fp64_src,
+                     "frac": fp64_tf / fp64_peak, "attainable_tflops": attainable,
+                     "frac_of_min_roofline": fp64_tf / attainable}}
+
+
+# ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The reference's own CPU implementation (baseline/_ref, its public
+    superlse.estimate) on this host's cores, rank 0 only, on the same config,
+    metric and problem indices as our arm; each step a bounded sample of the
+    config batch, its real wall time reported."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from paper_1705_06073_b200 import simdata
 
-    B, n = simdata.CONFIGS[args.config][0], simdata.CONFIGS[args.config][1]
-    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args.config, per_step, start=i * 1000)
-        if i >= args.warmup:
-            vals.append(r["value"])
-            info = r
-    v = float(np.mean(vals))
-    line = {"metric": "LSE problems solved/sec to convergence", "value": v, "unit": "problems/s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * B / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{args.config}", "batch": B, "N": n, "grid": "4N"},
-            "cpu_baseline": {"value": v, "unit": "problems/s", "cores": info["cores"], "kind": "port",
-                             "sample": info["sample"]},
-            "e2e": {"value": v, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    cfg = args.config
+    B = simdata.CONFIGS[cfg][0]
+    kind = "reference" if reference_available() else "port"
+    pool = CpuPool(kind)
+    budget = 150.0  # seconds for the whole --steps/--warmup run
+    pool.run(cfg, range(pool.cores))  # warm every worker
+    t1 = pool.run(cfg, [0])[0]
+    per_step = max(2.0, budget / max(1, args.steps))
+    count = max(pool.cores, int(per_step / max(t1, 1e-3)) * pool.cores)
+    count = min(count, B)
+    for i in range(args.warmup):  # untimed warm-up steps: one problem per worker
+        pool.run(cfg, range(pool.cores))
+    walls = []
+    for i in range(args.steps):
+        lo = (i * count) % B
+        idx = [(lo + j) % B for j in range(count)]
+        wall, _ = pool.run(cfg, idx)
+        walls.append(wall)
+    pool.close()
+    ms = [1000.0 * w for w in walls]
+    v = count * len(walls) / sum(walls)
+    what = "real reference superlse (baseline/_ref)" if kind == "reference" else "oracle port (reference not installed)"
+    line = {"metric": METRIC, "value": v, "unit": "problems/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(ms)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE configs generator, SURVEY 8(d))",
+            "config": config_dict(cfg, world, B),
+            "step_sample": f"each step = {count} of the {B} problems (indices cycle through 0..{B - 1}), "
+                           f"ms_per_step = that sample's wall time",
+            "cpu_baseline": {"value": v, "unit": "problems/s", "cores": pool.cores, "kind": kind,
+                             "sample": f"{args.steps} steps x {count} cfg{cfg} problems, {what}, multiprocessing "
+                                       f"pool of {pool.cores} single-thread workers"},
+            "e2e": {"value": v, "unit": "problems/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "step_ms": ms}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def solve_rate(torch, dev, stream, flush, cfg, steps, warmup, B=None, start=0):
+    from paper_1705_06073_b200 import EstimatorOptions, simdata
+    from paper_1705_06073_b200.estimator import BatchSolver
+
+    B = B or simdata.CONFIGS[cfg][0]
+    n = simdata.CONFIGS[cfg][1]
+    Y = simdata.batch(SEED, cfg, B, start=start)
+    ydev = torch.from_numpy(Y).to(dev)
+    solver = BatchSolver(n, B, EstimatorOptions(grid_factor=4), device=dev)
+    ms = time_steps(torch, stream, lambda: solver.solve(ydev), steps, warmup, flush)
+    h = solver.host_outputs()
+    return Y, solver, ms, h
 
 
 def run_ours(args):
@@ -187,132 +358,152 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch, ops, simdata
-    from paper_1705_06073_b200.estimator import BatchSolver
+    from paper_1705_06073_b200 import EstimatorOptions, dist as D, estimate_batch, simdata
 
     cfg = args.config
     B = args.batch or simdata.CONFIGS[cfg][0]
     n = simdata.CONFIGS[cfg][1]
     opts = EstimatorOptions(grid_factor=4)
-    L = 4 * n
-    Y = simdata.batch(SEED, cfg, B, start=rank * B)  # weak scaling: each rank its own problems
-    ydev = torch.from_numpy(Y).to(dev)
-    solver = BatchSolver(n, B, opts, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > L2
-
     stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
-        solver.solve(ydev)
-    torch.cuda.synchronize()
+
+    # ---- value: weak scaling, rank r solves problems [r B, (r + 1) B) of the world x B job
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     if world > 1:
         torch.distributed.barrier()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        ev[i][0].record(stream)
-        solver.solve(ydev)
-        ev[i][1].record(stream)
-    torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(sum(step_ms))
+    Y, solver, step_ms, h = solve_rate(torch, dev, stream, flush, cfg, args.steps, args.warmup, B=B, start=rank * B)
     clk = clocks.stop()
+    total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = world * B / (ms_per_step / 1000.0)
-
-    # correctness spot check of the timed launches (k_hat distribution)
-    h = solver.host_outputs()
     status_bad = int(np.count_nonzero(h["status"]))
     khat_mean = float(np.mean(h["k_hat"]))
     counters = h["counters"].sum(axis=0).tolist()
+    del solver
 
-    # ---- e2e through the public API (host numpy in, LseResult list out)
+    # ---- strong scaling (N > 1): the fixed B-problem batch sharded over the ranks
+    strong = None
+    if world > 1:
+        lo, hi = D.shard_range(B, rank, world)
+        _, s2, sms, _ = solve_rate(torch, dev, stream, flush, cfg, args.steps, 1, B=hi - lo, start=lo)
+        t = torch.tensor([float(sum(sms))], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        sms_step = float(t.item()) / args.steps
+        strong = {"value": B / (sms_step / 1000.0), "ms_per_step": sms_step, "batch": B,
+                  "per_rank": f"shard_range({B}, rank, {world})"}
+        del s2
+
+    # ---- e2e through the public API, every step: H2D of y from pinned host
+    # memory, the solve, D2H of every estimate into the SoA result
+    Yall = np.ascontiguousarray(simdata.batch(SEED, cfg, world * B)) if world > 1 else Y
+    Yp = torch.from_numpy(Yall).pin_memory()  # the job's input, pinned once (outside the timing)
+
+    def e2e_call():
+        if world > 1:
+            return D.estimate_batch_distributed(Yp, opts)
+        return estimate_batch(Yp, opts, device=dev)
+
     e2e_ms = []
-    h2d = Y.nbytes
-    import torch as _t
-    Yp = _t.from_numpy(Y).pin_memory()  # the step's input sits in pinned host memory (allocated once, untimed)
     n_e2e = max(3, args.steps)
     for i in range(n_e2e + 2):  # two untimed calls: first-use allocations (solver, pinned staging)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        res, solver_e2e = estimate_batch(Yp, opts, device=dev, return_solver=True)
-        # consume every problem's estimates (SoA host arrays) inside the timed region
+        res = e2e_call()
         chk = int(res.k_hat.sum()) + float(np.abs(res.alpha).sum() + res.theta.sum() + res.beta.sum())
         t1 = time.perf_counter()
         if i > 1:
             e2e_ms.append(1000.0 * (t1 - t0))
-    e2e_val = world * B / (float(np.mean(e2e_ms)) / 1000.0)
-    d2h = int(sum(v.nbytes for v in solver_e2e.host_outputs().values()))
+    e2e_t = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = world * B / (e2e_t / 1000.0)
+    h2d = Yall.nbytes // world
+    if world == 1:
+        d2h = int(sum(np.asarray(v).nbytes for v in res.h.values()))
+    else:
+        d2h = int(res._m.nbytes // world)
     del chk
 
-    # ---- roofline: grid-eval kernel over the same batch
-    g = torch.Generator(device=dev).manual_seed(1)
-    rho = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
-    w = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
-    dl = torch.rand(B, dtype=torch.float64, device=dev, generator=g) + 0.5
-    qg = torch.empty((B, L), dtype=torch.complex128, device=dev)
-    sg = torch.empty((B, L), dtype=torch.float64, device=dev)
-    for _ in range(3):
-        ops.grid_eval(rho, dl, w, L, out=(qg, sg))
-    gms = []
-    for _ in range(10):
-        flush.zero_()
-        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        ops.grid_eval(rho, dl, w, L, out=(qg, sg))
-        b_.record(stream)
-        torch.cuda.synchronize()
-        gms.append(a.elapsed_time(b_))
-    grid_ms = float(np.mean(gms))
-    alg_bytes = B * (32 * n + 24 * L)
-    achieved = alg_bytes / (grid_ms / 1000.0) / 1e9
-    peaks, peak_kind = measured_peaks()
-    flops = B * 15 * L * int(np.log2(L))  # 3 complex FFTs of L at 5 L log2 L
-    fp64_tf = flops / (grid_ms / 1000.0) / 1e12
-    # FP64 DFMA peak measured on this pool's B200 (tools/micro/fp64_peak.cu, profiles/r1_fp64_peak.txt)
-    fp64_peak = 34.09
-    attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg_bytes, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
-    kname = ("grid_tma_kernel" if (L == 1024 and 128 < n <= 256) else "grid_fused_kernel") + \
-        " (activation grid, SURVEY 8(a) row 9)"
-    traffic = None  # DRAM bytes per launch from the committed ncu capture of this kernel and shape
-    tf = os.path.join(REPO, "profiles", "r1_grid_tma_cfg2.json")
-    if kname.startswith("grid_tma_kernel") and cfg == 2 and os.path.exists(tf):
-        with open(tf) as fh:
-            traffic = json.load(fh)["traffic_bytes_per_launch"] * B // 4096
-    roof = {"bound": "hbm", "kernel": kname,
-            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-            "traffic": traffic, "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
-            "launch_ms": grid_ms, "flops_per_launch": flops,
-            "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "peak_source": "measured DFMA loop",
-                     "frac": fp64_tf / fp64_peak, "attainable_tflops": attainable,
-                     "frac_of_min_roofline": fp64_tf / attainable}}
+    # e2e_numpy: a pageable numpy batch in, one LseResult object per problem out
+    e2e_np = None
+    if world == 1:
+        tnp = []
+        for i in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rs = estimate_batch(Y, opts, device=dev)
+            items = list(rs)
+            t1 = time.perf_counter()
+            if i > 0:
+                tnp.append(1000.0 * (t1 - t0))
+        e2e_np = {"value": B / (float(np.mean(tnp)) / 1000.0), "unit": "problems/s", "ms_per_step": float(np.mean(tnp)),
+                  "api": "estimate_batch(numpy complex128 (B, N), pageable) -> list of LseResult (every problem)",
+                  "h2d_bytes_per_step": Y.nbytes}
+        del items
 
+    roof = grid_roofline(torch, dev, stream, flush, n) if rank == 0 else None
+
+    # ---- every config in full (N = 1)
+    per_config = None
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, args.cpu_seconds)
+    if rank == 0 and world == 1:
+        pool = None
+        if not args.no_cpu:
+            pool = CpuPool("reference" if reference_available() else "port")
+            cpu = cpu_sample(pool, cfg, args.cpu_seconds, B)
+        if not args.no_per_config:
+            per_config = {}
+            cpu_cfgs = {int(c) for c in args.per_config_cpu.split(",") if c.strip()}
+            for c in sorted(simdata.CONFIGS):
+                if c == cfg:
+                    pc = {"value": value, "ms_per_step": ms_per_step, "steps": args.steps, "roofline": roof}
+                else:
+                    w_, s_ = CONFIG_STEPS[c]
+                    _, s, ms, hc = solve_rate(torch, dev, stream, flush, c, s_, w_)
+                    del s
+                    bc = simdata.CONFIGS[c][0]
+                    mps = float(np.mean(ms))
+                    pc = {"value": bc / (mps / 1000.0), "ms_per_step": mps, "steps": s_, "step_ms": ms,
+                          "status_nonzero": int(np.count_nonzero(hc["status"])),
+                          "k_hat_mean": float(np.mean(hc["k_hat"])),
+                          "roofline": grid_roofline(torch, dev, stream, flush, simdata.CONFIGS[c][1])}
+                pc["config"] = config_dict(c, 1, simdata.CONFIGS[c][0])
+                if pool is not None and c in cpu_cfgs:
+                    pc["cpu_baseline"] = cpu if c == cfg else cpu_sample(pool, c, args.cpu_seconds,
+                                                                          simdata.CONFIGS[c][0])
+                per_config[f"cfg{c}"] = pc
+        if pool is not None:
+            pool.close()
+
     if world > 1:
         torch.distributed.barrier()
     if rank == 0:
-        line = {"metric": "LSE problems solved/sec to convergence", "value": value, "unit": "problems/s",
+        line = {"metric": METRIC, "value": value, "unit": "problems/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded BASELINE configs[1] generator, SURVEY 8(d))",
-                "config": {"workload": f"cfg{cfg}", "batch_per_gpu": B, "N": n, "K": simdata.CONFIGS[cfg][2],
-                           "grid": "4N", "parallelism": f"dp{world} (independent problems)",
-                           "l2": "flushed (256 MiB write) between timed steps"},
+                "data": "synthetic (seeded BASELINE configs generator, SURVEY 8(d))",
+                "config": config_dict(cfg, world, B),
                 "e2e": {"value": e2e_val, "unit": "problems/s", "h2d_bytes_per_step": h2d,
-                        "d2h_bytes_per_step": d2h, "api": "paper_1705_06073_b200.estimate_batch(numpy)"},
-                "roofline": roof, "cpu_baseline": cpu, "gpu_launches": args.steps,
+                        "d2h_bytes_per_step": d2h,
+                        "api": ("paper_1705_06073_b200.estimate_batch(pinned torch (B, N) complex128) -> "
+                                "BatchResult (SoA host arrays of every estimate)") if world == 1 else
+                        "paper_1705_06073_b200.dist.estimate_batch_distributed(pinned (world*B, N)) -> "
+                        "GatheredResult (all-gathered estimates)"},
+                "e2e_numpy": e2e_np, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": args.steps,
+                "gpu_launches_note": "one persistent solve_kernel launch per step (the whole estimate() loop)",
                 "clocks": clk, "status_nonzero": status_bad, "k_hat_mean": khat_mean,
                 "counters_total": dict(zip(["builds", "grids", "stats", "ls_trials"], counters)),
-                "step_ms": step_ms}
+                "step_ms": step_ms, "strong": strong, "per_config": per_config}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

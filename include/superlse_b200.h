@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SLSE_ABI_VERSION 1
+#define SLSE_ABI_VERSION 2
 
 /* EstimatorOptions (estimator.py:34-50), superfast fields. */
 typedef struct slse_options {
@@ -55,6 +55,10 @@ typedef struct slse_options {
   int k_max;                     /* <= 0: M */
   int trace_capacity;            /* <= 0: 2 + 13 * max_outer_iterations */
   int event_capacity;            /* <= 0: 4 * k_max + 64 */
+  int decomp_method;             /* EstimatorOptions.decomp_method (toeplitz.decompose :263-276):
+                                    0 "auto" (superfast from N >= 4096), 1 "levinson"
+                                    (Schur-Levinson, O(N^2)), 2 "schur" (superfast
+                                    divide-and-conquer generalized Schur, O(N log^2 N)) */
 } slse_options;
 
 /* Outputs of slse_estimate_batch (device pointers, per problem b at offset
@@ -80,6 +84,9 @@ typedef struct slse_outputs {
   int32_t* n_events;     /* [B] */
   int64_t* counters;     /* [B, 4] builds, grid evals, stats evals, line-search trials */
   double* stage_seconds; /* [B, 6] activate objective beta refine deactivate total */
+  double* iter_seconds;  /* [B, max_outer_iterations] wall seconds of each outer iteration
+                            (LseResult.wall_time_per_stage["per_iteration"], estimator.py:165,247);
+                            may be NULL */
 } slse_outputs;
 
 int slse_abi_version(void);

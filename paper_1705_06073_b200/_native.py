@@ -14,7 +14,7 @@ from .errors import SuperLseError
 
 _LIB_PATH = os.environ.get("SLSE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                                                      "libsuperlse_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 c_int_p = ctypes.POINTER(ctypes.c_int32)
 
@@ -34,11 +34,12 @@ class SlseOptions(ctypes.Structure):
         ("k_max", ctypes.c_int),
         ("trace_capacity", ctypes.c_int),
         ("event_capacity", ctypes.c_int),
+        ("decomp_method", ctypes.c_int),
     ]
 
 
 OUTPUT_FIELDS = ("k_hat", "status", "iterations", "flags", "beta", "zeta", "theta", "gamma", "alpha", "slot",
-                 "trace", "stage", "trace_k", "n_trace", "events", "n_events", "counters", "stage_seconds")
+                 "trace", "stage", "trace_k", "n_trace", "events", "n_events", "counters", "stage_seconds", "iter_seconds")
 
 
 class SlseOutputs(ctypes.Structure):

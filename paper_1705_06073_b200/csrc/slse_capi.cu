@@ -74,6 +74,10 @@ int twiddles(int need_lg, cudaStream_t st, const cplx** out, int* out_lg) {
     tw_fill_kernel<<<256, 256, 0, st>>>(p, lg);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail("tw_fill_kernel", e);
+    // the table is shared by every later caller, whatever stream it uses: wait
+    // for the fill once before publishing it (a one-time cost per device/size)
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail("tw_fill_kernel (sync)", e);
     // older tables stay allocated: in-flight kernels may still read them
     t.ptr = p;
     t.lg = lg;
@@ -116,21 +120,20 @@ namespace {
 // measured on B200 (tools/occ_exp.sh) cfg3 181 -> 130 ms, cfg4 1.00 -> 0.82 s;
 // with B <= SMs (cfg5) one 512-thread CTA per problem stays faster.
 constexpr size_t kPairRegion = 100 * 1024;
-bool solver_paired(int n, int B) {
-  if (getenv("SLSE_NO_PAIR")) return false;
-  const bool dnc = n >= dnc_min_n();
+bool solver_paired(int n, int B, bool dnc) {
+  if (slse_knob("SLSE_NO_PAIR")) return false;
   if (n <= 512 || B <= sm_count()) return false;
   return dnc || 48 * (size_t)n <= kPairRegion;
 }
 
-int solver_threads(int n, int B) {
-  const char* env = getenv("SLSE_SOLVER_NT");
+int solver_threads(int n, int B, bool dnc) {
+  const char* env = slse_knob("SLSE_SOLVER_NT");
   if (env) {
     int v = atoi(env);
     if (v == 32 || v == 64 || v == 128 || v == 256 || v == 512 || v == 1024) return v;
   }
   if (n <= 512) return 32;    // cfg1-2: measured 68 ms (32) vs 113 ms (256) per 4096 x N=256 batch
-  if (solver_paired(n, B)) return 256;
+  if (solver_paired(n, B, dnc)) return 256;
   if (n <= 2048) return 256;  // cfg3: 167 ms (256) vs 205 (128) / 236 (512) per 1024 x N=1024
   return 512;                 // cfg4/5 with B <= SMs (superfast): 8.8 s (512) vs 13.1 (1024) / 12 (128) at cfg5
 }
@@ -140,7 +143,7 @@ int solver_threads(int n, int B) {
 // W (16, 8 or 4 -- as many as the per-warp shared memory allows), or 0 when
 // the classic one-problem-per-CTA kernel is used (nt > 32, SLSE_NO_WARPS).
 int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem) {
-  if (nt != 32 || dnc || getenv("SLSE_NO_WARPS")) return 0;  // (the superfast factor keeps CTA-static scratch)
+  if (nt != 32 || dnc || slse_knob("SLSE_NO_WARPS")) return 0;  // (the superfast factor keeps CTA-static scratch)
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -153,10 +156,9 @@ int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem) {
 
 int grid_size_for_solver(int n, int G, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
-  P.dnc = n >= dnc_min_n() ? 1 : 0;
-  P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
-  const int nt = solver_threads(n, B);
-  SmemPlan plan = smem_plan(n, P.L, nt, P.dnc != 0, (nt == 256 && solver_paired(n, B)) ? kPairRegion : 0);
+  const bool dnc = P.dnc != 0;
+  const int nt = solver_threads(n, B, dnc);
+  SmemPlan plan = smem_plan(n, P.L, nt, dnc, (nt == 256 && solver_paired(n, B, dnc)) ? kPairRegion : 0);
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {  // one slab per warp of every CTA
     int ctas = (B + W - 1) / W;
@@ -220,6 +222,7 @@ void slse_default_options(slse_options* o) {
   o->k_max = 0;
   o->trace_capacity = 0;
   o->event_capacity = 0;
+  o->decomp_method = 0;
 }
 
 int slse_cov_column(const double* theta, const double* gamma, const int32_t* kcount, int kstride, const double* beta,
@@ -243,7 +246,7 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
   if (N < 1 || B < 0 || method < 0 || method > 2) return fail_arg("slse_toeplitz_factor: bad arguments");
   if (B == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (method == 2 || (method == 0 && N >= dnc_min_n())) {
+  if (use_dnc(N, method)) {
     const cplx* tw;
     int twlog;
     const int F = 1 << ilog2(N);
@@ -265,9 +268,9 @@ int slse_toeplitz_factor_ex(const double* c, int N, int B, double* rho, double* 
     SLSE_DISPATCH_NT(nt, {
       e = set_smem(factor_dnc_kernel<NTC>, smem);
       if (e == cudaSuccess) {
-        const char* dd = getenv("SLSE_DNC_DIRECT_MAX");
+        const char* dd = slse_knob("SLSE_DNC_DIRECT_MAX");
         long long* prof = nullptr;
-        if (getenv("SLSE_DNC_PROF")) {  // debug: phase clocks of problem 0, printed to stderr
+        if (slse_knob("SLSE_DNC_PROF")) {  // debug: phase clocks of problem 0, printed to stderr
           cudaMalloc(&prof, 16 * sizeof(long long));
           cudaMemsetAsync(prof, 0, 16 * sizeof(long long), st);
         }
@@ -435,10 +438,9 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   int rc = twiddles(ilog2(L), st, &tw, &twlog);
   if (rc) return rc;
   cudaError_t e = cudaSuccess;
-  // register-Stockham path: 3 L-point transforms resident in shared memory,
-  // compile-time pass schedules for L = 2^6 .. 2^12, pruned first pass
-  // v5 (slse_grid.cuh): two-pass transform, TMA bulk input prefetch, persistent
-  if (L == 1024 && N > 128 && N <= 256 && getenv("SLSE_GRID_V3") == nullptr && getenv("SLSE_GRID_DIT") == nullptr) {
+  // L = 1024, 128 < N <= 256 (cfg2): v5 (slse_grid.cuh), two-pass transform,
+  // TMA bulk input prefetch, persistent CTAs
+  if (L == 1024 && N > 128 && N <= 256) {
     const size_t smem = g5_smem_bytes(N);
     e = set_smem(grid_tma_kernel, smem);
     if (e == cudaSuccess)
@@ -456,27 +458,30 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
     }
     if (e != cudaSuccess) return fail("grid_tma_kernel setup", e);
   }
-  if (getenv("SLSE_GRID_DIT") == nullptr) {
+  {
     const int lg = ilog2(L);
     int q = 0;
     while (q < 3 && (N << (q + 1)) <= L) ++q;  // input support n <= L / 2^q
+    // v3 (fused last pass) for the other L = 2^10 shapes
+    if (lg == 10) {
+#define SLSE_GRID3_Q(NTV, LGV, QV)                                                                         \
+  case QV: {                                                                                               \
+    const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
+    e = set_smem(grid_fused_kernel<NTV, LGV, QV>, ssmem);                                                  \
+    if (e == cudaSuccess) {                                                                                \
+      grid_fused_kernel<NTV, LGV, QV><<<B, NTV, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N,   \
+                                                            (cplx*)q_grid, s_grid, tw, twlog);             \
+      e = cudaGetLastError();                                                                              \
+    }                                                                                                      \
+    return e == cudaSuccess ? 0 : fail("grid_fused_kernel", e);                                            \
+  }
+      switch (q) { SLSE_GRID3_Q(256, 10, 0) SLSE_GRID3_Q(256, 10, 1) SLSE_GRID3_Q(256, 10, 2) SLSE_GRID3_Q(256, 10, 3) }
+#undef SLSE_GRID3_Q
+    }
+    // register-Stockham kernel: 3 L-point transforms resident in shared
+    // memory, compile-time pass schedules for L = 2^6 .. 2^12, pruned first pass
 #define SLSE_GRID_Q(NTV, LGV, QV)                                                                          \
   case QV: {                                                                                               \
-    if (getenv("SLSE_GRID_PERSIST") != nullptr) {  /* measured slower than one CTA per problem */    \
-      const size_t psmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV) + 64 * (size_t)N;             \
-      e = set_smem(grid_persist_kernel<NTV, LGV, QV>, psmem);                                              \
-      int occ = 0;                                                                                         \
-      if (e == cudaSuccess)                                                                                \
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_persist_kernel<NTV, LGV, QV>, NTV, psmem); \
-      if (e == cudaSuccess && occ > 0) {                                                                   \
-        int g = sm_count() * occ;                                                                          \
-        if (g > B) g = B;                                                                                  \
-        grid_persist_kernel<NTV, LGV, QV><<<g, NTV, psmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, \
-                                                                 B, (cplx*)q_grid, s_grid, tw, twlog);     \
-        e = cudaGetLastError();                                                                            \
-        return e == cudaSuccess ? 0 : fail("grid_persist_kernel", e);                                      \
-      }                                                                                                    \
-    }                                                                                                      \
     const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
     e = set_smem(grid_stockham_kernel<NTV, LGV, QV>, ssmem);                                               \
     if (e == cudaSuccess) {                                                                                \
@@ -492,58 +497,11 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
       SLSE_GRID_Q(NTV, LGV, 0) SLSE_GRID_Q(NTV, LGV, 1) SLSE_GRID_Q(NTV, LGV, 2) SLSE_GRID_Q(NTV, LGV, 3) \
     }                                                                           \
     break;
-    // v4 (one warp per residue, registers + 4.6 KB shared per warp) for 2^ceil(log2 N) = 256:
-    // opt-in (SLSE_GRID_V4); measured 80 us vs v3's 70 us on cfg2 (latency-bound at 16 warps/SM)
-    if (getenv("SLSE_GRID_V4") != nullptr && ilog2(N) == 8 && (lg == 10 || lg == 9)) {
-      if (lg == 9)
-        grid_warp_kernel<9><<<B, 64, 0, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, (cplx*)q_grid, s_grid, tw, twlog);
-      else
-        grid_warp_kernel<10><<<B, 128, 0, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N, (cplx*)q_grid, s_grid, tw, twlog);
-      e = cudaGetLastError();
-      return e == cudaSuccess ? 0 : fail("grid_warp_kernel", e);
-    }
-    // v3 (fused last pass) for L = 2^10 outside v5's N range; at L = 2^11 the
-    // Stockham kernel measured faster (49 vs 68 us for 1024 x N = 512)
-    if (getenv("SLSE_GRID_V2") == nullptr && (lg == 10 || (lg == 11 && getenv("SLSE_GRID_V3_2048")))) {
-#define SLSE_GRID3_Q(NTV, LGV, QV)                                                                        \
-  case QV: {                                                                                               \
-    if (getenv("SLSE_GRID_PERSIST3") != nullptr) {  /* persistent v3 + cp.async: measured slower (100 vs 70 us) */ \
-      const size_t psmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV) + 64 * (size_t)N;             \
-      e = set_smem(grid_fused_persist_kernel<NTV, LGV, QV>, psmem);                                        \
-      int occ = 0;                                                                                         \
-      if (e == cudaSuccess)                                                                                \
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_fused_persist_kernel<NTV, LGV, QV>, NTV, psmem); \
-      if (e == cudaSuccess && occ > 0) {                                                                   \
-        int g = sm_count() * occ;                                                                          \
-        if (g > B) g = B;                                                                                  \
-        grid_fused_persist_kernel<NTV, LGV, QV><<<g, NTV, psmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, \
-                                                                       N, B, (cplx*)q_grid, s_grid, tw, twlog); \
-        e = cudaGetLastError();                                                                            \
-        return e == cudaSuccess ? 0 : fail("grid_fused_persist_kernel", e);                                \
-      }                                                                                                    \
-    }                                                                                                      \
-    const size_t ssmem = head_bytes(NTV) + 48 * (size_t)sk_len(1 << LGV);                                  \
-    e = set_smem(grid_fused_kernel<NTV, LGV, QV>, ssmem);                                                  \
-    if (e == cudaSuccess) {                                                                                \
-      grid_fused_kernel<NTV, LGV, QV><<<B, NTV, ssmem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N,   \
-                                                            (cplx*)q_grid, s_grid, tw, twlog);             \
-      e = cudaGetLastError();                                                                              \
-    }                                                                                                      \
-    return e == cudaSuccess ? 0 : fail("grid_fused_kernel", e);                                            \
-  }
-      if (lg == 10) {
-        switch (q) { SLSE_GRID3_Q(256, 10, 0) SLSE_GRID3_Q(256, 10, 1) SLSE_GRID3_Q(256, 10, 2) SLSE_GRID3_Q(256, 10, 3) }
-      } else {
-        switch (q) { SLSE_GRID3_Q(256, 11, 0) SLSE_GRID3_Q(256, 11, 1) SLSE_GRID3_Q(256, 11, 2) SLSE_GRID3_Q(256, 11, 3) }
-      }
-#undef SLSE_GRID3_Q
-    }
     switch (lg) {
       SLSE_GRID_CASE(6, 32)
       SLSE_GRID_CASE(7, 32)
       SLSE_GRID_CASE(8, 64)
       SLSE_GRID_CASE(9, 96)
-      SLSE_GRID_CASE(10, 192)
       SLSE_GRID_CASE(11, 384)
       SLSE_GRID_CASE(12, 768)
       default: break;
@@ -551,6 +509,8 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
 #undef SLSE_GRID_CASE
 #undef SLSE_GRID_Q
   }
+  // L > 4096 (and L < 64): one CTA per problem, radix-2/4 passes over the
+  // three transforms in shared memory when they fit, else through global scratch
   const int nt = block_threads(N);
   const int fused = 48 * (size_t)L <= kRegionBudget ? 1 : 0;
   const size_t smem = kHeadBytes + (fused ? 48 * (size_t)L : 0);
@@ -611,10 +571,9 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
   }
   SolveParams P = make_params(N, o);
   P.g = G;
-  P.dnc = N >= dnc_min_n() ? 1 : 0;
-  P.dnc_stockham = getenv("SLSE_DNC_STOCKHAM") ? 1 : 0;
-  P.grid_fused = getenv("SLSE_GRID_UNFUSED") ? 0 : 1;
-  if (const char* dd = getenv("SLSE_DNC_DIRECT_MAX")) P.dnc_direct = atoi(dd);
+  P.dnc_stockham = slse_knob("SLSE_DNC_STOCKHAM") ? 1 : 0;
+  P.grid_fused = slse_knob("SLSE_GRID_UNFUSED") ? 0 : 1;
+  if (const char* dd = slse_knob("SLSE_DNC_DIRECT_MAX")) P.dnc_direct = atoi(dd);
   const cplx* tw;
   int twlog;
   const int fmax = P.L > 2 * N ? P.L : (1 << ilog2(2 * N));
@@ -626,17 +585,12 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
   cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(int), st);
   if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
   char* ws = (char*)workspace + 256;
-  const int nt = solver_threads(N, B);
+  const int nt = solver_threads(N, B, P.dnc != 0);
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {
-    // twiddle table in shared memory when it fits next to the W regions
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const size_t base = kCfBytes + (size_t)W * wsm, twb = sizeof(cplx) * tw_entries(twlog);
-    const int tw_smem = (!getenv("SLSE_TW_GLOBAL") && base + twb <= (size_t)optin) ? 1 : 0;
-    e = slse_solve_warps_launch(W, g / W, base + (tw_smem ? twb : 0), st, P, cft, (const cplx*)y, B, *out, ws, slab,
-                                queue, tw, twlog, plan.fft_cap, plan.rec_in_smem, wsm, tw_smem);
+    const size_t smem = kCfBytes + (size_t)W * wsm;
+    e = slse_solve_warps_launch(W, g / W, smem, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog,
+                                plan.fft_cap, plan.rec_in_smem, wsm);
     return e == cudaSuccess ? 0 : fail("solve_kernel_warps", e);
   }
 #define SLSE_SOLVE_ARGS g, plan.bytes, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog, plan.fft_cap, \

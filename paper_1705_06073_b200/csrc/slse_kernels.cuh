@@ -35,6 +35,18 @@ constexpr size_t kCfBytes = (sizeof(CfTable) + 255) & ~(size_t)255;
 constexpr size_t kHeadBytes = head_bytes(1024);
 constexpr size_t kRegionBudget = 200 * 1024;
 
+// Experiment overrides used by tools/ (environment variables) exist only in
+// builds compiled with -DSLSE_DEBUG_KNOBS; the product library reads no
+// environment.
+inline const char* slse_knob(const char* name) {
+#ifdef SLSE_DEBUG_KNOBS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 inline int block_threads(int n) {
   if (n <= 128) return 128;
   if (n <= 512) return 256;
@@ -56,11 +68,11 @@ inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false, size_t region_
   // half an SM (region_budget)
   size_t budget = region_budget ? region_budget : kRegionBudget;
   if (nt <= 32 && !dnc) {
-    const char* env = getenv("SLSE_WARP_REGION_KB");
+    const char* env = slse_knob("SLSE_WARP_REGION_KB");
     budget = env ? (size_t)atoi(env) * 1024 : 48 * (size_t)n;
     if (budget < 48 * (size_t)n) budget = 48 * (size_t)n;
   }
-  if (const char* env = getenv("SLSE_REGION_KB")) {  // experiment override
+  if (const char* env = slse_knob("SLSE_REGION_KB")) {  // experiment override
     const size_t v = (size_t)atoi(env) * 1024;
     if (dnc || v >= 48 * (size_t)n) budget = v;
   }
@@ -86,11 +98,6 @@ inline SmemPlan smem_plan(int n, int L, int nt, bool dnc = false, size_t region_
 }
 
 
-// superfast (D&C) factorisation from this N up; SLSE_DNC_MIN overrides
-inline int dnc_min_n() {
-  const char* env = getenv("SLSE_DNC_MIN");
-  return env ? atoi(env) : 4096;
-}
 
 // ------------------------------------------------------------------ kernels
 struct OutPtrs {
@@ -119,6 +126,7 @@ SLSE_D ProbOut prob_out(const slse_outputs& out, const SolveParams& P, int p) {
   o.nevents = out.n_events + p;
   o.counters = (long long*)out.counters + (size_t)p * 4;
   o.stage_s = out.stage_seconds + (size_t)p * 6;
+  o.iter_s = out.iter_seconds ? out.iter_seconds + (size_t)p * P.max_outer : nullptr;
   return o;
 }
 
@@ -169,19 +177,13 @@ template <int W>
 __global__ void __launch_bounds__(32 * W, 16 / W) solve_kernel_warps(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
                                                                     int B, slse_outputs out, char* ws, size_t slab_bytes,
                                                                     int* queue, const cplx* tw, int twlog, int fft_cap,
-                                                                    int rec_smem, int warp_smem, int tw_smem) {
+                                                                    int rec_smem, int warp_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CfTable* cf = (CfTable*)smem_raw;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // optional CTA-shared copy of the twiddle table (tw_smem: 1 = all tw_entries(twlog))
-  cplx* tws = (cplx*)(smem_raw + kCfBytes);
-  const size_t tw_bytes = tw_smem ? sizeof(cplx) * tw_entries(twlog) : 0;
-  unsigned char* mine = smem_raw + kCfBytes + tw_bytes + (size_t)warp * warp_smem;
+  unsigned char* mine = smem_raw + kCfBytes + (size_t)warp * warp_smem;
   if (threadIdx.x == 0) *cf = cft;
-  if (tw_smem)
-    for (int i = threadIdx.x; i < (int)tw_entries(twlog); i += blockDim.x) tws[i] = tw[i];
   __syncthreads();
-  if (tw_smem) tw = tws;
   Blk b;
   b.tid = lane;
   b.nt = 32;
@@ -517,76 +519,6 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) gri
 }
 
 
-// cp.async (16 B, L2-only) helpers for the persistent grid kernel
-SLSE_D void cp_async16(void* smem_dst, const void* gmem_src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
-}
-SLSE_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int NPEND>
-SLSE_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
-
-// Persistent variant of grid_stockham_kernel: each CTA walks problems
-// p = blockIdx.x, + gridDim.x, ...; the next problem's (w, rho) are
-// prefetched with cp.async into a double-buffered stage while the current
-// one is transformed, hiding the HBM latency behind the FFT passes.
-template <int NT, int LG, int Q>
-__global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : (NT <= 256 ? 2 : 1))) grid_persist_kernel(
-    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int B,
-    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* tw, int twlog) {
-  constexpr int L = 1 << LG;
-  constexpr int LS = L + (L >> 4);
-  constexpr int H = L >> Q;  // transformed head (>= n)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* X = (cplx*)(smem_raw + head_bytes(NT));
-  cplx* stage = X + 3 * LS;  // [2][2][n] : buffer, (w, rho), point
-  const int tid = threadIdx.x;
-  auto prefetch = [=](int prob, int buf) {
-    const cplx* wp = w + (size_t)prob * n;
-    const cplx* rp = rho + (size_t)prob * n;
-    cplx* sw = stage + (size_t)buf * 2 * n;
-    for (int i = tid; i < n; i += NT) {
-      cp_async16(sw + i, wp + i);
-      cp_async16(sw + n + i, rp + i);
-    }
-    cp_async_commit();
-  };
-  int p = blockIdx.x;
-  if (p < B) prefetch(p, 0);
-  for (int it = 0; p < B; ++it, p += gridDim.x) {
-    const int nxt = p + gridDim.x;
-    if (nxt < B) {
-      prefetch(nxt, (it + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const cplx* sw = stage + (size_t)(it & 1) * 2 * n;
-    for (int i = tid; i < H; i += NT) {
-      cplx a = mk(0.0, 0.0), rr = mk(0.0, 0.0);
-      if (i < n) { a = sw[i]; rr = sw[n + i]; }
-      const int si = sk(i);
-      X[si] = a;
-      X[LS + si] = rr;
-      X[2 * LS + si] = cscale(rr, (double)i);
-    }
-    __syncthreads();
-    fft_fixed_pruned<LG, Q>(X, 3, -1.0, tw, twlog, tid, NT);
-    const double inv_d = 1.0 / delta_last[p];
-    const double c2n = 2.0 - (double)n;
-    cplx* qg = q_grid + (size_t)p * L;
-    double* sgp = s_grid + (size_t)p * L;
-    for (int l = tid; l < L; l += NT) {
-      const int sl = sk(l);
-      const cplx a0 = X[LS + sl], a1 = X[2 * LS + sl];
-      qg[l] = X[sl];
-      sgp[l] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
-    }
-    __syncthreads();
-  }
-}
-
 
 #ifndef SLSE_GRID_MINB
 #define SLSE_GRID_MINB 3
@@ -677,251 +609,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fus
   }
 }
 
-// Persistent v3: the same pass plan as grid_fused_kernel, but each CTA walks
-// problems p = blockIdx.x, + gridDim.x, ... and the next problem's (w, rho)
-// are prefetched with cp.async into a double-buffered shared stage while the
-// current one is transformed, so pass 1 reads shared memory instead of
-// waiting on HBM; q^G / s^G leave with streaming (evict-first) stores.
-template <int NT, int LG, int Q>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fused_persist_kernel(
-    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int B,
-    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* tw, int twlog) {
-  constexpr int L = 1 << LG;
-  constexpr int LS = L + (L >> 4);
-  constexpr int LGRL = (LG - 4) % 4;
-  constexpr int RL = 1 << LGRL;
-  constexpr int PER = L / RL;
-  constexpr int NZ = 16 >> Q;
-  constexpr int P1 = L / 16;
-  static_assert(LGRL >= 1 && PER == NT, "grid_fused_persist_kernel: plan needs NT = L / RL");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x;
-  cplx* X = (cplx*)(smem_raw + head_bytes(NT));
-  cplx* stage = X + 3 * LS;  // [2 buffers][w | rho][n]
-  const auto prefetch = [=](int prob, int buf) {
-    const cplx* wp = w + (size_t)prob * n;
-    const cplx* rp = rho + (size_t)prob * n;
-    cplx* sw = stage + (size_t)buf * 2 * n;
-    for (int i = tid; i < n; i += NT) {
-      cp_async16(sw + i, wp + i);
-      cp_async16(sw + n + i, rp + i);
-    }
-    cp_async_commit();
-  };
-  int p = blockIdx.x;
-  if (p < B) prefetch(p, 0);
-  for (int it = 0; p < B; ++it, p += gridDim.x) {
-    const int nxt = p + gridDim.x;
-    if (nxt < B) {
-      prefetch(nxt, (it + 1) & 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const cplx* sw = stage + (size_t)(it & 1) * 2 * n;
-    const cplx* sr = sw + n;
-    // ---- pass 1: pruned radix-16 from the stage
-    for (int t = tid; t < 3 * P1; t += NT) {
-      const int c = t / P1, j = t - c * P1;
-      cplx v[16];
-#pragma unroll
-      for (int r = 0; r < NZ; ++r) {
-        const int i = j + r * P1;
-        cplx x = mk(0.0, 0.0);
-        if (i < n) {
-          if (c == 0) x = sw[i];
-          else if (c == 1) x = sr[i];
-          else x = cscale(sr[i], (double)i);
-        }
-        v[r] = x;
-      }
-      DifPrunedStage<16, NZ, 8>::run(v, -1.0);
-      cplx* xc = X + (size_t)c * LS;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) xc[sk(j * 16 + r)] = v[brev_const(r, 16)];
-    }
-    __syncthreads();
-    FixedPlanMid<LG, 4, LG - LGRL, (3 * (L / 16) + NT - 1) / NT>::run(X, 3, -1.0, tw, twlog, tid, NT);
-    const int j = tid;
-    constexpr int NS = L / RL;
-    cplx* qg = q_grid + (size_t)p * L;
-    double* sgp = s_grid + (size_t)p * L;
-    {
-      cplx v0[RL];
-#pragma unroll
-      for (int r = 0; r < RL; ++r) v0[r] = X[sk(j + r * PER)];
-#pragma unroll
-      for (int r = 1; r < RL; ++r) v0[r] = cmul(v0[r], twid_tab(tw, twlog, j * r, LG, -1.0));
-      dft_dif<RL>(v0, -1.0);
-#pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        const cplx o = v0[brev_const(r, RL)];
-        __stcs((double2*)&qg[j + r * NS], make_double2(o.re, o.im));
-      }
-    }
-    const double inv_d = 1.0 / delta_last[p];
-    const double c2n = 2.0 - (double)n;
-    cplx v1[RL], v2[RL];
-#pragma unroll
-    for (int r = 0; r < RL; ++r) {
-      v1[r] = X[LS + sk(j + r * PER)];
-      v2[r] = X[2 * LS + sk(j + r * PER)];
-    }
-#pragma unroll
-    for (int r = 1; r < RL; ++r) {
-      const cplx t = twid_tab(tw, twlog, j * r, LG, -1.0);
-      v1[r] = cmul(v1[r], t);
-      v2[r] = cmul(v2[r], t);
-    }
-    dft_dif<RL>(v1, -1.0);
-    dft_dif<RL>(v2, -1.0);
-#pragma unroll
-    for (int r = 0; r < RL; ++r) {
-      const cplx a0 = v1[brev_const(r, RL)], a1 = v2[brev_const(r, RL)];
-      __stcs(&sgp[j + r * NS], (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d);
-    }
-    __syncthreads();  // X and this stage buffer are reused by the next problem
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Row 9 standalone, v4 ("warp per residue"), for 2^ceil(log2 N) = 256:
-// with R = L / 256, grid point l = 256-point DFT bin m of the twiddled signal
-// x_r[i] = s[i] W_L^{i r} at l = m R + r.  A CTA of R warps handles one
-// problem; warp r runs the three 256-point transforms of residue r (w, rho,
-// i rho) entirely in registers and one 4.6 KB shared buffer:
-//   256 = 32 lanes x 8:  radix-8 over each lane's stride-32 points,
-//   twiddle W_256^{lane k2}, shared transpose, radix-8 over 8 of the 32
-//   lane-points, twiddle W_32^{s k1a}, shared transpose, radix-4 --
-// no CTA barriers, conflict-free 16-byte shared accesses (skews 36 / 9),
-// then q^G and s^G straight to HBM (the R warps of a CTA fill each other's
-// sectors).  Twiddles come from the launch's table (L1-resident).
 SLSE_D cplx ldg_c(const cplx* p) {
   const double2 d = __ldg((const double2*)p);
   return mk(d.x, d.y);
-}
-SLSE_D cplx twl(const cplx* __restrict__ tw, int twlog, int k, int lg) {
-  (void)twlog;
-  return ldg_c(&tw[tw_index(k, lg)]);
-}
-
-// in: v[t] = x[lane + 32 t]; out: v[4 j + k1b] = X[k2 + 8 (q + 4 j) + 64 k1b],
-// k2 = lane / 4, q = lane % 4.  S: 288 complex of shared memory; T256: the
-// CTA's shared table W_256^k at T256[k + k / 8] (skewed: the strided
-// lookups below hit distinct banks).
-SLSE_D int sk8(int k) { return k + (k >> 3); }
-SLSE_D void warp_fft256(cplx* v, cplx* S, unsigned lane, const cplx* T256) {
-  dft_dif<8>(v, -1.0);  // Y[k2] = v[brev(k2)]
-#pragma unroll
-  for (int k2 = 0; k2 < 8; ++k2) {
-    cplx y = v[brev_const(k2, 8)];
-    if (k2) y = cmul(y, T256[sk8((lane * k2) & 255)]);
-    S[36 * k2 + lane] = y;
-  }
-  __syncwarp();
-  const unsigned k2 = lane >> 2, sq = lane & 3;
-#pragma unroll
-  for (int u = 0; u < 8; ++u) v[u] = S[36 * k2 + sq + 4 * u];
-  __syncwarp();
-  dft_dif<8>(v, -1.0);  // over u: V[k1a] = v[brev(k1a)]
-#pragma unroll
-  for (int k1a = 0; k1a < 8; ++k1a) {
-    cplx y = v[brev_const(k1a, 8)];
-    if (k1a) y = cmul(y, T256[sk8(((sq * k1a) & 31) << 3)]);  // W_32^{q k1a}
-    S[36 * k2 + 9 * sq + k1a] = y;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    cplx z[4];
-#pragma unroll
-    for (int s2 = 0; s2 < 4; ++s2) z[s2] = S[36 * k2 + 9 * s2 + sq + 4 * j];
-    dft_dif<4>(z, -1.0);
-#pragma unroll
-    for (int k1b = 0; k1b < 4; ++k1b) v[4 * j + k1b] = z[brev_const(k1b, 4)];
-  }
-  __syncwarp();
-}
-
-#ifndef SLSE_GRIDW_MINB
-#define SLSE_GRIDW_MINB 4
-#endif
-template <int LG>
-__global__ void __launch_bounds__(32 * (1 << (LG - 8)), (LG <= 10 ? SLSE_GRIDW_MINB : 4)) grid_warp_kernel(
-    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n,
-    cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* __restrict__ tw, int twlog) {
-  constexpr int L = 1 << LG;
-  constexpr int R = L / 256;
-  constexpr int NT = 32 * R;
-  // per-warp transpose buffers, then (after the transforms) the s^G staging;
-  // q^G is staged separately so the w transform's bins need not stay live
-  __shared__ __align__(16) cplx Sall[R][288];
-  __shared__ __align__(16) cplx Qst[L];
-  __shared__ __align__(16) cplx T256[288];    // W_256^k at sk8(k)
-  __shared__ __align__(16) cplx TL[32 * R];   // W_L^k, k < 32 R (pre-twiddle heads)
-  const int p = blockIdx.x;
-  const unsigned lane = threadIdx.x & 31;
-  const int r = threadIdx.x >> 5;
-  const cplx* wp = w + (size_t)p * n;
-  const cplx* rp = rho + (size_t)p * n;
-  // issue the problem's input loads before the table fill so both latencies overlap
-  cplx v[8], a0[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int i = lane + 32 * t;
-    v[t] = i < n ? ldg_c(&wp[i]) : mk(0.0, 0.0);
-    a0[t] = i < n ? ldg_c(&rp[i]) : mk(0.0, 0.0);
-  }
-  for (int k = threadIdx.x; k < 256; k += NT) T256[sk8(k)] = twl(tw, twlog, k, 8);
-  for (int k = threadIdx.x; k < 32 * R; k += NT) TL[k] = twl(tw, twlog, k, LG);
-  __syncthreads();
-  cplx* S = Sall[r];
-  const unsigned k2 = lane >> 2, sq = lane & 3;
-  // pre-twiddle W_L^{(lane + 32 t) r} = W_L^{lane r} W_{256/R... }: W_L^{32 t r} = W_256^{(32/R... )}
-  // with L = 256 R:  W_L^{32 t r} = W_256^{(32 t r) / R} when R | 32 t r -- use W_L^{32 t r} =
-  // W_{L/32}^{t r} = W_256^{(t r) * (256 / (L / 32))} = T256[(t r * 8 / R) & 255]
-  const cplx base = TL[lane * r];
-  // ---- q^G = FFT_L(w) at residue r
-  if (r) {
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const cplx tw_t = cmul(base, T256[sk8(((t * r * 32) / R) & 255)]);
-      v[t] = cmul(v[t], tw_t);
-      a0[t] = cmul(a0[t], tw_t);  // rho pre-twiddled too (kept for A0 and A1)
-    }
-  }
-  warp_fft256(v, S, lane, T256);
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-#pragma unroll
-    for (int k1b = 0; k1b < 4; ++k1b) Qst[(k2 + 8 * (sq + 4 * j) + 64 * k1b) * R + r] = v[4 * j + k1b];
-  // ---- A1 = FFT_L(i rho), then A0 = FFT_L(rho), at residue r
-#pragma unroll
-  for (int t = 0; t < 8; ++t) v[t] = cscale(a0[t], (double)(lane + 32 * t));
-  warp_fft256(v, S, lane, T256);
-  warp_fft256(a0, S, lane, T256);
-  const double inv_d = 1.0 / delta_last[p];
-  const double c2n = 2.0 - (double)n;
-  __syncthreads();  // every warp is done with its transpose buffer
-  double* Sst = (double*)&Sall[0][0];  // L doubles (R * 288 * 2 >= L)
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-#pragma unroll
-    for (int k1b = 0; k1b < 4; ++k1b) {
-      const cplx b0 = a0[4 * j + k1b], b1 = v[4 * j + k1b];  // A0, A1
-      Sst[(k2 + 8 * (sq + 4 * j) + 64 * k1b) * R + r] =
-          (c2n * cabs2(b0) + 2.0 * (b1.re * b0.re + b1.im * b0.im)) * inv_d;
-    }
-  __syncthreads();
-  // coalesced write-out of the problem's L bins
-  double2* qg = (double2*)(q_grid + (size_t)p * L);
-  double* sgp = s_grid + (size_t)p * L;
-#pragma unroll 4
-  for (int l = threadIdx.x; l < L; l += NT) {
-    __stcs(&qg[l], make_double2(Qst[l].re, Qst[l].im));
-    __stcs(&sgp[l], Sst[l]);
-  }
 }
 
 }  // namespace slse_k
@@ -944,4 +634,4 @@ SLSE_DECL_SOLVE(1024)
 cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t st, const slse::SolveParams& P,
                                     const slse::CfTable& cft, const slse::cplx* ys, int B, const slse_outputs& out,
                                     char* ws, size_t slab, int* queue, const slse::cplx* tw, int twlog, int fft_cap,
-                                    int rec_smem, int warp_smem, int tw_smem);
+                                    int rec_smem, int warp_smem);

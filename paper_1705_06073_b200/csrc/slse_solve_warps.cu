@@ -10,26 +10,26 @@
 cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t st, const slse::SolveParams& P,
                                     const slse::CfTable& cft, const slse::cplx* ys, int B, const slse_outputs& out,
                                     char* ws, size_t slab, int* queue, const slse::cplx* tw, int twlog, int fft_cap,
-                                    int rec_smem, int warp_smem, int tw_smem) {
+                                    int rec_smem, int warp_smem) {
   cudaError_t e;
   switch (W) {
     case 16:
       e = cudaFuncSetAttribute(slse_k::solve_kernel_warps<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       slse_k::solve_kernel_warps<16><<<ctas, 32 * 16, smem, st>>>(P, cft, ys, B, out, ws, slab, queue, tw, twlog,
-                                                                    fft_cap, rec_smem, warp_smem, tw_smem);
+                                                                    fft_cap, rec_smem, warp_smem);
       break;
     case 8:
       e = cudaFuncSetAttribute(slse_k::solve_kernel_warps<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       slse_k::solve_kernel_warps<8><<<ctas, 32 * 8, smem, st>>>(P, cft, ys, B, out, ws, slab, queue, tw, twlog,
-                                                                  fft_cap, rec_smem, warp_smem, tw_smem);
+                                                                  fft_cap, rec_smem, warp_smem);
       break;
     case 4:
       e = cudaFuncSetAttribute(slse_k::solve_kernel_warps<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       slse_k::solve_kernel_warps<4><<<ctas, 32 * 4, smem, st>>>(P, cft, ys, B, out, ws, slab, queue, tw, twlog,
-                                                                  fft_cap, rec_smem, warp_smem, tw_smem);
+                                                                  fft_cap, rec_smem, warp_smem);
       break;
     default:
       return cudaErrorInvalidValue;

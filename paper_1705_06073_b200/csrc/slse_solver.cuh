@@ -82,6 +82,15 @@ struct SolveParams {
   int dnc_direct;    // superfast nodes up to this many steps use direct products
 };
 
+// Superfast divide-and-conquer factorisation: decomp_method 2 ("schur",
+// toeplitz.generalized_schur), or "auto" from kDncMinN up (the measured
+// crossover of the two device factorisations; the reference's own auto
+// switches at N > 256, toeplitz.py:36,263-276 -- both agree to ~1e-12).
+constexpr int kDncMinN = 4096;
+SLSE_HD bool use_dnc(int n, int decomp_method) {
+  return decomp_method == 2 || (decomp_method == 0 && n >= kDncMinN);
+}
+
 // Launch-uniform parameters from the C-ABI options (estimator.py:34-50).
 SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   SolveParams P;
@@ -101,7 +110,7 @@ SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   P.tau = o.tau;
   P.conv_tol_scale = o.convergence_tol_scale;
   P.dec_tol_scale = o.newton_decrement_tol_scale;
-  P.dnc = 0;
+  P.dnc = use_dnc(n, o.decomp_method) ? 1 : 0;
   P.dnc_stockham = 0;
   P.grid_fused = 1;
   P.dnc_direct = SLSE_DNC_DIRECT;
@@ -208,6 +217,7 @@ struct ProbOut {
   int* nevents;
   long long* counters;  // [4] builds, grids, stats, backtracks
   double* stage_s;      // [6] seconds per stage (estimator.py:106-114 buckets)
+  double* iter_s;       // [max_outer] seconds per outer iteration (estimator.py:165,247), or nullptr
 };
 
 SLSE_D double prior_zeta(double zeta, int kmax) {  // model_core.py:230-234
@@ -1125,6 +1135,7 @@ struct Solver {
     int iterations = 0;
     for (int it = 1; it <= P.max_outer; ++it) {
       iterations = it;
+      const unsigned long long t_iter = now_ns();
       // 1) activation
       if (it <= P.sweep_iters) {
         status = ensure_cur();
@@ -1224,6 +1235,7 @@ struct Solver {
         if (status != kOk) break;
       }
       lap(kTmRefine);
+      if (o.iter_s && b.leader()) o.iter_s[it - 1] = (double)(now_ns() - t_iter) * 1e-9;  // estimator.py:247
       const double current = last_trace;
       if (fabs(previous - current) < (double)n * P.conv_tol_scale) {
         converged = 1;

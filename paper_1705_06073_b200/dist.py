@@ -5,6 +5,12 @@ tests).  Problems are independent, so the data path has no collective:
 each rank solves a contiguous slice of the batch; the only communication is
 one gather of the per-problem results at the end (and, in bench.py, a MAX
 reduction of the elapsed time).
+
+Public entry point: :func:`estimate_batch_distributed` -- every rank passes
+the same (B, N) batch (the reference solves one problem per call,
+estimator.py:117; this shards a named batch of them), solves its slice on
+its own GPU through :func:`estimate_batch`, and receives the whole batch's
+results in problem order.
 """
 
 from __future__ import annotations
@@ -94,3 +100,82 @@ def gather_results(local: np.ndarray, total: int, group=None) -> np.ndarray:
         a, z = shard_range(total, r, world)
         out[a:z] = parts[r][: z - a].cpu().numpy()
     return out
+
+
+class GatheredResult:
+    """The whole batch's results after :func:`estimate_batch_distributed`:
+    SoA arrays in problem order (k_hat, status, iterations, converged, beta,
+    zeta (B,); theta, gamma, slot (B, K); alpha (B, K) complex, zero-padded
+    past k_hat) plus per-problem dicts via indexing."""
+
+    def __init__(self, m: np.ndarray, kmax: int, shard: tuple):
+        self.kmax = kmax
+        self.shard = shard  # this rank's [lo, hi)
+        self._m = m
+        o = 6
+        self.k_hat = m[:, 0].astype(np.int64)
+        self.status = m[:, 1].astype(np.int64)
+        self.iterations = m[:, 2].astype(np.int64)
+        self.converged = (m[:, 3].astype(np.int64) & 1) != 0
+        self.beta = m[:, 4].copy()
+        self.zeta = m[:, 5].copy()
+        self.theta = m[:, o:o + kmax]
+        self.gamma = m[:, o + kmax:o + 2 * kmax]
+        self.alpha = m[:, o + 2 * kmax:o + 3 * kmax] + 1j * m[:, o + 3 * kmax:o + 4 * kmax]
+        self.slot = m[:, o + 4 * kmax:o + 5 * kmax].astype(np.int64)
+        self._items = None
+
+    def __len__(self):
+        return self._m.shape[0]
+
+    def __getitem__(self, i):
+        if self._items is None:
+            self._items = unpack_results(self._m, self.kmax)
+        return self._items[i]
+
+
+def estimate_batch_distributed(y, opts=None, group=None, device=None, solve=None) -> GatheredResult:
+    """Solve a batch of independent problems on every rank's GPU.
+
+    Every rank of ``group`` calls this with the same ``y`` ((B, N) complex,
+    numpy or a CPU torch tensor -- pinned input uploads asynchronously).
+    Rank r solves problems ``shard_range(B, r, world)`` with
+    :func:`paper_1705_06073_b200.estimate_batch` on ``device`` (default: the
+    current CUDA device); the packed per-problem estimates are then
+    all-gathered (one NCCL collective on GPUs, gloo on CPU) so every rank
+    returns the full batch in problem order.  No collective runs on the
+    data path.  ``solve`` replaces the per-rank solver (tests: the host
+    emulation of the device program stands in for a GPU under gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    from .estimator import estimate_batch
+
+    solve = solve or (lambda ys: estimate_batch(ys, opts, device=device))
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    total = int(y.shape[0])
+    lo, hi = shard_range(total, rank, world)
+    n = int(y.shape[-1])
+    kmax = n if opts is None or getattr(opts, "k_max", None) is None else int(opts.k_max)
+    if hi > lo:
+        res = solve(y[lo:hi])
+        kk = max(1, int(np.max(res.k_hat, initial=0)))
+        h = {name: res.h[name] for name in _SCALARS}
+        for name in _VECTORS:
+            h[name] = res.h[name]
+    else:
+        kk = 1
+        h = None
+    # width of the gathered rows: the largest model order over all ranks
+    dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
+           else torch.device("cpu"))
+    kt = torch.tensor([kk], dtype=torch.int64, device=dev)
+    dist.all_reduce(kt, op=dist.ReduceOp.MAX, group=group)
+    kk = min(int(kt.item()), kmax)
+    if h is None:
+        local = np.zeros((0, 6 + 5 * kk))
+    else:
+        local = pack_results(h, kk)
+    return GatheredResult(gather_results(local, total, group), kk, (lo, hi))

@@ -33,6 +33,8 @@ STAGE_NAMES = ("init", "beta", "activate", "zeta", "refine", "deactivate")
 TIMER_NAMES = ("activate", "objective", "beta", "refine", "deactivate", "total")
 FLAG_CONVERGED, FLAG_KMAX_CAP, FLAG_TRACE_FULL, FLAG_EVENTS_FULL = 1, 2, 4, 8
 STATUS_OK, STATUS_NOT_PD, STATUS_BAD_DIAGONAL = 0, 1, 2
+DECOMP_METHODS = {"auto": 0, "levinson": 1, "schur": 2}  # slse_options.decomp_method
+STEER_METHODS = ("auto", "direct", "nufft")
 
 
 @dataclass
@@ -76,6 +78,7 @@ class LseResult:
     slots: np.ndarray = None
     counters: dict = field(default_factory=dict)
     status: int = STATUS_OK
+    algorithms: dict = field(default_factory=dict)
 
 
 def _validate(opts: EstimatorOptions):
@@ -83,9 +86,9 @@ def _validate(opts: EstimatorOptions):
         raise ValueError(f"backend must be one of {BACKENDS}")
     if opts.backend == "semifast":
         raise NotImplementedError("the semifast (Woodbury) backend is outside this build's scope")
-    if opts.decomp_method not in ("auto", "levinson", "schur"):
+    if opts.decomp_method not in DECOMP_METHODS:  # toeplitz.py:263-276
         raise ValueError(f"unknown decomposition method {opts.decomp_method!r}")
-    if opts.steer_method not in ("auto", "direct", "nufft"):
+    if opts.steer_method not in STEER_METHODS:  # nufft.py:118-123
         raise ValueError(f"unknown method {opts.steer_method!r}")
     if not 1 <= opts.lbfgs_memory <= 16:
         raise ValueError("lbfgs_memory must lie in 1..16 on the GPU path")
@@ -104,14 +107,32 @@ def c_options(opts: EstimatorOptions, n: int) -> _native.SlseOptions:
     o.k_max = int(opts.k_max) if opts.k_max is not None else n
     o.trace_capacity = 2 + 13 * int(opts.max_outer_iterations)
     o.event_capacity = 4 * o.k_max + 64
+    o.decomp_method = DECOMP_METHODS[opts.decomp_method]
     return o
+
+
+def algorithms(opts: EstimatorOptions, n: int) -> dict:
+    """The algorithms the device runs for these options (reported in
+    LseResult.algorithms).  decomp_method selects the Toeplitz factorisation
+    exactly as toeplitz.decompose does (:263-276; "auto" switches to the
+    superfast divide-and-conquer Schur from N = 4096, the device crossover).
+    Every off-grid Fourier sum (nufft.steer_forward / steer_adjoint /
+    fourier_sum_two_sided) is evaluated EXACTLY on the device -- the values
+    the reference's "direct" method computes (nufft.py:139-141,156-158), in
+    the product form of SURVEY.md 8(a) rows 8-9 -- whatever steer_method
+    says; the reference's "nufft" approximates the same sums to ~1e-10
+    (SURVEY.md 8(c)), so it is accepted and served by the exact sums."""
+    dm = opts.decomp_method
+    schur = dm == "schur" or (dm == "auto" and n >= 4096)
+    return {"decomp": "generalized_schur (superfast D&C)" if schur else "levinson (Schur-Levinson)",
+            "steer": "direct (exact, product form)", "steer_requested": opts.steer_method}
 
 
 class BatchOutputs:
     """Output arrays of one batched solve (torch tensors on one device, or
     numpy arrays for host-side consumers), laid out as slse_outputs."""
 
-    def __init__(self, xp_empty, B, kmax, tcap, ecap, g=1):
+    def __init__(self, xp_empty, B, kmax, tcap, ecap, g=1, max_outer=200):
         e = xp_empty
         self.k_hat = e((B,), "i32")
         self.status = e((B,), "i32")
@@ -131,6 +152,7 @@ class BatchOutputs:
         self.n_events = e((B,), "i32")
         self.counters = e((B, 4), "i64")
         self.stage_seconds = e((B, 6), "f64")
+        self.iter_seconds = e((B, max(1, max_outer)), "f64")
 
     def struct(self, ptr_of) -> _native.SlseOutputs:
         s = _native.SlseOutputs()
@@ -164,9 +186,11 @@ def decode_events(rows: np.ndarray):
 _STAGE_ARR = np.array(STAGE_NAMES, dtype=object)
 
 
-def unpack_all(h: dict):
+def unpack_all(h: dict, algos: dict = None):
     """LseResult per problem from host (numpy) copies of the batch outputs.
-    Per-batch vectorised preparation; per-problem arrays are views."""
+    Per-problem arrays are fresh copies (the caller owns them, as the
+    reference's results, estimator.py:262-275; they do not keep the batch's
+    host block alive)."""
     B = h["k_hat"].shape[0]
     khat = h["k_hat"].tolist()
     ntr = h["n_trace"].tolist()
@@ -182,6 +206,7 @@ def unpack_all(h: dict):
     ctr = h["counters"].tolist()
     theta, gamma, slot, trace, trace_k, events = (h["theta"], h["gamma"], h["slot"], h["trace"], h["trace_k"],
                                                   h["events"])
+    iter_s = h.get("iter_seconds")
     out = []
     for b in range(B):
         k, nt, fl = khat[b], ntr[b], flags[b]
@@ -194,34 +219,36 @@ def unpack_all(h: dict):
             if fl & FLAG_EVENTS_FULL:
                 warns.append("active-set history truncated (event capacity)")
         times = dict(zip(TIMER_NAMES, secs[b]))
-        times["per_iteration"] = []
+        times["per_iteration"] = (iter_s[b, :min(iters[b], iter_s.shape[1])].tolist()
+                                  if iter_s is not None else [])
         c = ctr[b]
         out.append(LseResult(
             k_hat=k,
-            theta_hat=theta[b, :k],
+            theta_hat=theta[b, :k].copy(),
             alpha_hat=alpha[b, :, :k].copy(),
             beta_hat=beta[b],
-            gamma_hat=gamma[b, :k],
+            gamma_hat=gamma[b, :k].copy(),
             zeta_hat=zeta[b],
-            objective_trace=trace[b, :nt],
+            objective_trace=trace[b, :nt].copy(),
             iterations=iters[b],
             wall_time_per_stage=times,
             converged=bool(fl & FLAG_CONVERGED),
             trace_stages=names[b, :nt].tolist(),
             warnings=warns,
             events=decode_events(events[b, :nev[b]].tolist()),
-            trace_k=trace_k[b, :nt],
-            slots=slot[b, :k],
+            trace_k=trace_k[b, :nt].copy(),
+            slots=slot[b, :k].copy(),
             counters=dict(builds=c[0], grids=c[1], stats=c[2], line_search_trials=c[3]),
             status=status[b],
+            algorithms=dict(algos) if algos else {},
         ))
     return out
 
 
-def unpack(h: dict, b: int) -> LseResult:
+def unpack(h: dict, b: int, algos: dict = None) -> LseResult:
     """LseResult of problem b alone (see unpack_all)."""
     sub = {k: v[b:b + 1] for k, v in h.items()}
-    return unpack_all(sub)[0]
+    return unpack_all(sub, algos)[0]
 
 
 # ------------------------------------------------------------------ GPU path
@@ -267,8 +294,10 @@ class BatchSolver:
                 return torch.empty(shape, dtype=getattr(torch, _TORCH_DT[dt]), device=self.device)
 
             self.out = BatchOutputs(empty, batch, self.kmax, self.copts.trace_capacity, self.copts.event_capacity,
-                                    g=self.g)
+                                    g=self.g, max_outer=self.copts.max_outer_iterations)
         self.cout = self.out.struct(lambda t: t.data_ptr())
+        self.algorithms = algorithms(self.opts, n)
+        self._stream = None
 
     def solve(self, y_dev, stream=None):
         torch = _torch()
@@ -276,6 +305,7 @@ class BatchSolver:
         if y_dev.dtype != torch.complex128 or not y_dev.is_contiguous() or tuple(y_dev.shape) != want:
             raise DimensionMismatch(f"y must be a contiguous complex128 tensor of shape {want}")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._stream = st
         rc = self.lib.slse_estimate_batch_mmv(
             ctypes.c_void_p(y_dev.data_ptr()), self.n, self.g, self.batch, ctypes.byref(self.copts),
             ctypes.byref(self.cout), ctypes.c_void_p(self.workspace.data_ptr()),
@@ -289,18 +319,20 @@ class BatchSolver:
         block to the next call, so steady-state calls neither pin new memory
         nor copy (or page-fault) the outputs a second time on the host."""
         torch = _torch()
-        st = torch.cuda.current_stream(self.device)
-        ts = {name: t.contiguous() for name, t in tensors.items()}
-        span = {name: (t.numel() * t.element_size() + 63) // 64 * 64 for name, t in ts.items()}
-        buf = torch.empty(max(64, sum(span.values())), dtype=torch.uint8, pin_memory=True)
-        off = 0
-        host = {}
-        for name, t in ts.items():
-            nb = t.numel() * t.element_size()
-            hb = buf[off:off + nb].view(t.dtype).view(t.shape)
-            hb.copy_(t, non_blocking=True)
-            host[name] = hb
-            off += span[name]
+        # copy on the stream the last solve() ran on (stream-ordered after it)
+        st = self._stream if self._stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            ts = {name: t.contiguous() for name, t in tensors.items()}
+            span = {name: (t.numel() * t.element_size() + 63) // 64 * 64 for name, t in ts.items()}
+            buf = torch.empty(max(64, sum(span.values())), dtype=torch.uint8, pin_memory=True)
+            off = 0
+            host = {}
+            for name, t in ts.items():
+                nb = t.numel() * t.element_size()
+                hb = buf[off:off + nb].view(t.dtype).view(t.shape)
+                hb.copy_(t, non_blocking=True)
+                host[name] = hb
+                off += span[name]
         st.synchronize()
         return {name: hb.numpy() for name, hb in host.items()}
 
@@ -315,14 +347,15 @@ class BatchSolver:
         tt = max(1, int(h["n_trace"].max(initial=0)))
         ee = max(1, int(h["n_events"].max(initial=0)))
         o = self.out
+        ii = max(1, min(int(h["iterations"].max(initial=0)), o.iter_seconds.shape[1]))
         big = {"theta": o.theta[:, :kk], "gamma": o.gamma[:, :kk], "alpha": o.alpha[:, :, :kk], "slot": o.slot[:, :kk],
                "trace": o.trace[:, :tt], "stage": o.stage[:, :tt], "trace_k": o.trace_k[:, :tt],
-               "events": o.events[:, :ee]}
+               "events": o.events[:, :ee], "iter_seconds": o.iter_seconds[:, :ii]}
         h.update(self._d2h(big))
         return h
 
     def results(self):
-        return unpack_all(self.host_outputs())
+        return unpack_all(self.host_outputs(), self.algorithms)
 
 
 class BatchResult:
@@ -333,10 +366,14 @@ class BatchResult:
     SoA fields (problem-major): k_hat, status, iterations, converged, beta,
     zeta (B,); theta, gamma, slot (B, K) zero-padded past k_hat; alpha
     complex (B, K), or (B, G, K) with G > 1 snapshots; trace (B, T) padded
-    past n_trace."""
+    past n_trace.  The SoA arrays are zero-copy views of one pinned host
+    block (no second host copy of the outputs); the block returns to torch's
+    pinned-memory cache when the last of them is dropped.  The per-problem
+    LseResult arrays are independent copies."""
 
-    def __init__(self, h: dict):
+    def __init__(self, h: dict, algos: dict = None):
         self.h = h
+        self.algorithms = algos or {}
         self.k_hat = h["k_hat"]
         self.status = h["status"]
         self.iterations = h["iterations"]
@@ -357,7 +394,7 @@ class BatchResult:
 
     def _all(self):
         if self._items is None:
-            self._items = unpack_all(self.h)
+            self._items = unpack_all(self.h, self.algorithms)
         return self._items
 
     def __getitem__(self, i):
@@ -412,7 +449,7 @@ def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=
     pinned = yt.device.type == "cpu" and yt.is_pinned()
     ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=pinned).contiguous()
     solver.solve(ydev)
-    res = BatchResult(solver.host_outputs())
+    res = BatchResult(solver.host_outputs(), solver.algorithms)
     return (res, solver) if return_solver else res
 
 

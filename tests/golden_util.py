@@ -10,7 +10,9 @@ STAGES = ("init", "beta", "activate", "zeta", "refine", "deactivate")
 
 
 def load(cfg):
-    return np.load(os.path.join(GOLDEN_DIR, f"golden_cfg{cfg}.npz"))
+    """golden_cfg{cfg}.npz (cfg may be "4x"), or golden_deact.npz for cfg="deact"."""
+    name = "golden_deact.npz" if cfg == "deact" else f"golden_cfg{cfg}.npz"
+    return np.load(os.path.join(GOLDEN_DIR, name))
 
 
 def encode_events(events):
@@ -53,4 +55,5 @@ def near_ties(cfg, b):
     """Near-tie decisions of golden trajectory (cfg, b): [[trace_pos, kind, margin], ...]."""
     import json
     with open(os.path.join(GOLDEN_DIR, "margins.json")) as f:
-        return json.load(f)[f"cfg{cfg}_p{b}"]["near_ties"]
+        tag = "deact" if cfg == "deact" else f"cfg{cfg}"
+        return json.load(f)[f"{tag}_p{b}"]["near_ties"]

@@ -29,9 +29,7 @@ static std::vector<cplx> make_twiddles(int lg) {
 }
 
 extern "C" int emu_estimate_batch(const double* y, int N, int B, const slse_options* opts, const slse_outputs* out) {
-  SolveParams P = make_params(N, *opts);
-  const char* dm = getenv("SLSE_DNC_MIN");
-  P.dnc = (dm && N >= atoi(dm)) ? 1 : 0;
+  SolveParams P = make_params(N, *opts);  // P.dnc from opts->decomp_method
   const int fmax = P.L > 2 * N ? P.L : 2 * N;
   std::vector<cplx> tw = make_twiddles(ilog2(fmax));
   CfTable cf;
@@ -64,6 +62,7 @@ extern "C" int emu_estimate_batch(const double* y, int N, int B, const slse_opti
     o.nevents = out->n_events + p;
     o.counters = (long long*)out->counters + (size_t)p * 4;
     o.stage_s = out->stage_seconds + (size_t)p * 6;
+    o.iter_s = out->iter_seconds ? out->iter_seconds + (size_t)p * P.max_outer : nullptr;
     Solver S(b, P, &cf, (const cplx*)y + (size_t)p * N, o, base, lay, nullptr, f);
     S.run();
   }

@@ -41,18 +41,24 @@ def build():
 _NP = {"i32": np.int32, "f64": np.float64, "i64": np.int64}
 
 
-def estimate_batch(Y, opts=None):
+def estimate_batch_raw(Y, opts=None):
+    """Host-output dict of the emulated batch (the layout of
+    BatchSolver.host_outputs)."""
     lib = build()
     opts = opts or EstimatorOptions()
     Y = np.ascontiguousarray(np.atleast_2d(np.asarray(Y, dtype=np.complex128)))
     B, n = Y.shape
     co = c_options(opts, n)
     out = BatchOutputs(lambda shape, dt: np.zeros(shape, dtype=_NP[dt]), B, co.k_max, co.trace_capacity,
-                       co.event_capacity)
+                       co.event_capacity, max_outer=co.max_outer_iterations)
     st = out.struct(lambda a: a.ctypes.data)
     lib.emu_estimate_batch(Y.ctypes.data, n, B, ctypes.byref(co), ctypes.byref(st))
-    h = {name: getattr(out, name) for name in _native.OUTPUT_FIELDS}
-    return [unpack(h, b) for b in range(B)]
+    return {name: getattr(out, name) for name in _native.OUTPUT_FIELDS}
+
+
+def estimate_batch(Y, opts=None):
+    h = estimate_batch_raw(Y, opts)
+    return [unpack(h, b) for b in range(h["k_hat"].shape[0])]
 
 
 def bundle(y, thetas, gammas, beta, L):

@@ -90,3 +90,57 @@ def test_two_rank_gloo_shard_and_gather():
         assert np.array_equal(g["theta_hat"], r.theta_hat)
         assert np.array_equal(g["alpha_hat"], r.alpha_hat)
         assert g["beta_hat"] == r.beta_hat
+
+
+def _worker_api(rank, world, port, Y, q):
+    import torch.distributed as dist
+
+    import hostemu_util as H
+    from paper_1705_06073_b200.estimator import EstimatorOptions
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        opts = EstimatorOptions(grid_factor=4)
+
+        class _Res:  # the BatchResult surface estimate_batch_distributed reads
+            def __init__(self, h):
+                self.h = h
+                self.k_hat = h["k_hat"]
+
+        out = D.estimate_batch_distributed(Y, opts, solve=lambda ys: _Res(H.estimate_batch_raw(ys, opts)))
+        q.put((rank, out.shard, out.k_hat, out.theta, out.alpha, out.beta))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_public_distributed_entry():
+    """paper_1705_06073_b200.dist.estimate_batch_distributed at world size 2:
+    every rank returns the whole batch (problem order) equal to solving it
+    in one process."""
+    import hostemu_util as H
+    from oracle import superlse_oracle as O
+    from paper_1705_06073_b200.estimator import EstimatorOptions
+
+    H.build()
+    Y = O.generate_batch(5, 1, 7)  # 7 problems: shards of 4 + 3
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_api, args=(r, 2, port, Y, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=240) for _ in range(2)], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = H.estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    assert outs[0][1] == (0, 4) and outs[1][1] == (4, 7)
+    for rank, shard, k_hat, theta, alpha, beta in outs:
+        for b, r in enumerate(ref):
+            assert k_hat[b] == r.k_hat
+            assert np.array_equal(theta[b, : r.k_hat], r.theta_hat)
+            assert np.array_equal(alpha[b, : r.k_hat], r.alpha_hat[0])
+            assert beta[b] == r.beta_hat

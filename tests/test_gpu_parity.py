@@ -153,9 +153,12 @@ def test_default_grid_factor_and_small_sizes():
         assert np.max(wrap_distance(r.theta_hat, o.theta_hat), initial=0) < THETA_TOL
         # a decision that sat within roundoff of its threshold (e.g. an Armijo
         # test on a 1e-12 objective change at convergence) may legitimately
-        # go either way; the history is compared only when none did.
-        if o.min_margin > 0.05:
-            assert r.trace_stages == o.trace_stages, n
+        # go either way: the stage trace is held to the oracle's up to its
+        # first near tie
+        ties = oracle_ties(o)
+        upto = min((t[0] for t in ties), default=len(o.trace_stages))
+        assert r.trace_stages[:upto] == o.trace_stages[:upto], n
+        assert encode_events(r.events).tolist() == encode_events(o.events).tolist(), n
 
 
 def test_pure_noise_and_zero_signal():
@@ -174,27 +177,20 @@ def test_pure_noise_and_zero_signal():
 
 
 @pytest.mark.parametrize("cfg", [2, 3])
-def test_trajectories_superfast_forced(cfg, monkeypatch):
+def test_trajectories_superfast_forced(cfg):
     """Golden histories with the superfast (divide-and-conquer) factorisation
-    forced on inside the solver kernel."""
+    forced on inside the solver kernel (decomp_method="schur",
+    toeplitz.py:263-276): identical history, the stage trace held to the
+    golden one up to the first near tie the oracle records at L = 4N."""
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
 
-    monkeypatch.setenv("SLSE_DNC_MIN", "64")
     z = load(cfg)
     count = int(z["count"])
     Y = np.stack([z[f"p{b}_y"] for b in range(count)])
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, decomp_method="schur"))
     for b in range(count):
-        p = f"p{b}_"
-        r = res[b]
-        # identical model order and active-set history; the L-BFGS step count
-        # of the converged tail may differ (Armijo tests on 1e-12 objective
-        # changes sit at roundoff), so the stage sequence is not compared
-        assert r.status == 0 and r.k_hat == int(z[p + "k_hat"])
-        assert np.array_equal(encode_events(r.events), z[p + "events"])
-        assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
-        assert rel(r.alpha_hat[0], z[p + "alpha_hat"]) < AMP_TOL
-        assert abs(r.beta_hat - float(z[p + "beta_hat"])) / float(z[p + "beta_hat"]) < AMP_TOL
+        assert "schur" in res[b].algorithms["decomp"]
+        _check_traj(res[b], z, f"p{b}_", near_ties(cfg, b))
 
 
 # ---- rows 7, 10, 11, 12 as separate operators (the solver runs them fused)
@@ -416,22 +412,42 @@ def test_per_call_size_sweep(n, monkeypatch):
         assert rel(sg.cpu().numpy()[b], s_ref) < CALL_TOL
 
 
+def oracle_ties(o):
+    """Near-tie decisions of an oracle run, as golden_util.near_ties."""
+    from golden_util import NEAR_TIE
+
+    return [[int(pos), kind, float(mg)] for kind, mg, pos in o.margins if mg < NEAR_TIE]
+
+
+def check_vs_oracle(r, o):
+    """GPU result vs oracle run on the same input: identical model order and
+    active-set history, stage trace identical up to the oracle's first near
+    tie (all of it when there is none), estimates within the bars."""
+    ties = oracle_ties(o)
+    assert r.status == 0
+    assert r.k_hat == o.k_hat
+    assert encode_events(r.events).tolist() == encode_events(o.events).tolist()
+    upto = min((t[0] for t in ties), default=None)
+    if upto is None:
+        assert r.trace_stages == o.trace_stages
+    else:
+        assert r.trace_stages[:upto] == o.trace_stages[:upto]
+    m = min(len(r.objective_trace), len(o.objective_trace), upto if upto is not None else 1 << 30)
+    assert rel(np.asarray(r.objective_trace)[:m], np.asarray(o.objective_trace)[:m]) < CALL_TOL
+    assert np.max(wrap_distance(r.theta_hat, o.theta_hat), initial=0) < THETA_TOL
+    assert rel(r.alpha_hat[0], o.alpha_hat[0]) < AMP_TOL
+    assert abs(r.beta_hat - o.beta_hat) / o.beta_hat < AMP_TOL
+
+
 @pytest.mark.parametrize("n,k", [(100, 6), (300, 12), (513, 16)])
 def test_trajectories_ragged_sizes_vs_oracle(n, k):
     """Whole estimates at sizes between the configs (one-warp with 8 warps
     per CTA at N = 300, 256-thread blocks at N = 513) vs the oracle: same
-    model order, active-set history and estimates.  (The stage trace may end
-    one refine step apart: the Newton-decrement stopping test at
-    |g^T d| ~ M 1e-8 sits on a cancelling quantity.)"""
+    model order, active-set history, estimates, and the stage trace up to
+    the oracle's first near-tie decision."""
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
 
     Y = O.generate_batch(31, 2, 3, n=n, k=k)
     res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
     for b in range(Y.shape[0]):
-        o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
-        r = res[b]
-        assert r.status == 0
-        assert r.k_hat == o.k_hat, (n, b)
-        assert np.max(wrap_distance(r.theta_hat, o.theta_hat), initial=0) < THETA_TOL
-        assert rel(r.alpha_hat[0], o.alpha_hat[0]) < AMP_TOL
-        assert encode_events(r.events).tolist() == encode_events(o.events).tolist(), (n, b)
+        check_vs_oracle(res[b], O.estimate(Y[b], O.OracleOptions(grid_factor=4)))

@@ -140,12 +140,12 @@ def test_emulated_superfast_factor(cfg):
 
 
 @pytest.mark.parametrize("cfg,b", [(1, 0), (2, 0), (2, 2), (3, 0)])
-def test_emulated_trajectory_superfast(cfg, b, monkeypatch):
-    """Whole estimator with the superfast factorisation forced on."""
-    monkeypatch.setenv("SLSE_DNC_MIN", "32")
+def test_emulated_trajectory_superfast(cfg, b):
+    """Whole estimator with the superfast factorisation forced on
+    (decomp_method="schur", toeplitz.py:263-276)."""
     z = load(cfg)
     p = f"p{b}_"
-    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4))[0]
+    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4, decomp_method="schur"))[0]
     assert r.k_hat == int(z[p + "k_hat"])
     assert np.array_equal(np.array([STAGES.index(s) for s in r.trace_stages]), z[p + "stages"])
     assert np.array_equal(encode_events(r.events), z[p + "events"])

@@ -33,6 +33,62 @@ def test_trajectory_matches_reference(cfg, b):
     assert np.max(np.abs(r.objective_trace - z[p + "trace"]) / np.abs(z[p + "trace"])) < 1e-9
 
 
+@pytest.mark.parametrize("b", range(4))
+def test_deactivation_trajectory_matches_reference(b):
+    """The oracle reproduces the reference's deactivating runs
+    (golden_deact.npz: removals, lowest-free-slot reuse afterwards)."""
+    from golden_util import near_ties
+
+    z = load("deact")
+    p = f"p{b}_"
+    r = O.estimate(z[p + "y"], O.OracleOptions(grid_factor=4))
+    assert r.k_hat == int(z[p + "k_hat"])
+    assert np.array_equal(encode_events(r.events), z[p + "events"])
+    assert any(ev[0] == "deactivate" for ev in r.events)
+    stages = np.array([STAGES.index(s) for s in r.trace_stages])
+    ties = near_ties("deact", b)
+    upto = min((t[0] for t in ties), default=stages.size)
+    assert np.array_equal(stages[:upto], z[p + "stages"][:upto])
+    assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
+    assert rel(r.alpha_hat[0], z[p + "alpha_hat"]) < AMP_TOL
+
+
+def test_deactivation_margins_match_reference():
+    """smlr.deactivation_margins at the reference state before its first
+    removal (golden_deact.npz, case 0)."""
+    z = load("deact")
+    p = "p0_call_predeact_"
+
+    class _S:
+        pass
+
+    sv = _S()
+    ga = z[p + "gammas"]
+    sv.gamma, sv.z, sv.zeta, sv.k_max = ga, np.ones(ga.size, bool), float(z[p + "zeta"]), int(z[p + "kmax"])
+    st = {k: z[p + "st_" + k] for k in "qrustvx"}
+    assert rel(O.deactivation_margins(sv, st), z[p + "margins"]) < CALL_TOL
+
+
+def test_cfg5_per_call_final_matches_reference():
+    """The oracle's bundle at the cfg5 shape (N = 16384) against the
+    reference's (final state of problem 0; decimated grid / omega vectors)."""
+    z = load(5)
+    dec = int(z["decim"])
+    p = "p0_call_final_"
+    y = z["p0_y"]
+    th, ga, be = z[p + "thetas"], z[p + "gammas"], float(z[p + "beta"])
+    bd = O.Bundle(y, th, ga, be)
+    assert rel(bd.rho, z[p + "rho"]) < CALL_TOL
+    assert rel(bd.delta, z[p + "delta"]) < CALL_TOL
+    assert rel(bd.w, z[p + "w"]) < CALL_TOL
+    qg, sg = bd.grid(4 * y.size)
+    assert rel(qg[::dec], z[p + "q_grid_dec"]) < CALL_TOL
+    assert rel(sg[::dec], z[p + "s_grid_dec"]) < CALL_TOL
+    st = bd.stats()
+    for k in "qrustvx":
+        assert rel(st[k], z[p + "st_" + k]) < CALL_TOL, k
+
+
 CALL_CASES = [(cfg, b, st) for cfg, nb in ((1, 2), (2, 2), (3, 1)) for b in range(nb)
               for st in ("empty", "truth", "final")]
 
