@@ -441,7 +441,7 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   // L = 1024, 128 < N <= 256 (cfg2): v5 (slse_grid.cuh), two-pass transform,
   // TMA bulk input prefetch, persistent CTAs
   if (L == 1024 && N > 128 && N <= 256) {
-    const size_t smem = g5_smem_bytes(N);
+    const size_t smem = g5_smem_bytes();
     e = set_smem(grid_tma_kernel, smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(grid_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,

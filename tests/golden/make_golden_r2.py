@@ -5,8 +5,9 @@ the shapes and code paths round 1 left without reference evidence:
 
 * ``golden_cfg5.npz`` -- the cfg5 shape (N = 16384, K = 512, L = 4N):
   trajectories of problems 0 and 1 with the reference's default
-  (``steer_method="auto"``: NUFFT at N >= 512) and, for problem 0, a second
-  trajectory with ``steer_method="direct"``; per-call bundle quantities
+  (``steer_method="auto"``: NUFFT at N >= 512) and a second trajectory of
+  each with ``steer_method="direct"`` (prefix ``p{b}d_``: the reference's own
+  spread between its two statistics methods); per-call bundle quantities
   (``steer_method="direct"``, SURVEY.md 8(c) caveat) at the truth / final /
   empty states of problem 0 and the final state of problem 1.
 * ``golden_cfg4x.npz`` -- cfg4 problems 1 and 2: trajectories plus
@@ -27,6 +28,7 @@ Usage:  python tests/golden/make_golden_r2.py [cfg5|cfg4x|deact ...]
 
 import multiprocessing as mp
 import os
+import re
 import sys
 
 for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
@@ -99,6 +101,7 @@ def _store_call(store, p, y, th, ga, be, L, decim):
     for key, val in MG.per_call(y, th, ga, be, L).items():
         if decim > 1 and key in BIG:
             store[p + key + "_dec"] = val[::decim]
+            store[p + key + "_max"] = float(np.max(np.abs(val)))  # the full vector's inf-norm (the rel denominator)
         else:
             store[p + key] = val
 
@@ -208,15 +211,64 @@ def build_deact_fixture(nproc=8):
                         **store)
 
 
+def refresh_calls(out_name, nproc=8):
+    """Recompute the per-call entries of an existing fixture from its stored
+    states (no trajectory rerun); the recomputed values must equal the stored
+    ones, and the new keys (the full-vector inf-norms of decimated vectors)
+    are added."""
+    path = os.path.join(HERE, out_name)
+    z = np.load(path)
+    store = {k: z[k] for k in z.files}
+    decim = int(z["decim"])
+    cfg = 5 if "cfg5" in out_name else 4
+    cjobs = []
+    for k in z.files:
+        m = re.match(r"p(\d+)_call_(\w+?)_thetas$", k)
+        if m:
+            b, name = int(m.group(1)), m.group(2)
+            p = f"p{b}_call_{name}_"
+            cjobs.append((cfg, b, name, z[p + "thetas"], z[p + "gammas"], float(z[p + "beta"]), None, None,
+                          SEED, decim))
+    with mp.get_context("fork").Pool(min(nproc, max(1, len(cjobs)))) as pool:
+        for (c, b, name), st in pool.imap_unordered(job_call, cjobs):
+            for key, val in st.items():
+                full = f"p{b}_call_{name}_{key}"
+                if full in store:
+                    assert np.array_equal(np.asarray(store[full]), np.asarray(val)), full
+                store[full] = val
+            print(f"{out_name} p{b} call {name} refreshed", flush=True)
+    np.savez_compressed(path, **store)
+
+
+def add_direct(out_name, cfg, b):
+    """Add problem b's steer_method="direct" reference trajectory (p{b}d_)
+    to an existing fixture."""
+    path = os.path.join(HERE, out_name)
+    z = np.load(path)
+    store = {k: z[k] for k in z.files}
+    (_, _, _, _, _, _), y, _, res, events = job_traj((cfg, b, "direct", None, None, SEED))
+    assert np.array_equal(y, store[f"p{b}_y"])
+    _store_traj(store, f"p{b}d_", res, events)
+    print(f"{out_name} p{b}d_: k_hat={res.k_hat} records={len(res.trace_stages)}", flush=True)
+    np.savez_compressed(path, **store)
+
+
 def main():
     what = sys.argv[1:] or ["deact", "cfg4x", "cfg5"]
+    if "cfg5d1" in what:
+        add_direct("golden_cfg5.npz", 5, 1)
+        return
+    if "refresh" in what:
+        refresh_calls("golden_cfg4x.npz")
+        refresh_calls("golden_cfg5.npz")
+        return
     if "deact" in what:
         build_deact_fixture()
     if "cfg4x" in what:
         build_traj_fixture(4, [1, 2], {1: ["truth", "final"], 2: ["truth", "final"]}, "golden_cfg4x.npz")
     if "cfg5" in what:
         build_traj_fixture(5, [0, 1], {0: ["truth", "final", "empty"], 1: ["final"]}, "golden_cfg5.npz",
-                           extra_direct=[0])
+                           extra_direct=[0, 1])
 
 
 if __name__ == "__main__":

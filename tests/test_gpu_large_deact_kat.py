@@ -66,10 +66,15 @@ def check_estimates(r, z, p):
 
 
 # objective-trace bar per shape: 1e-9 relative (north_star per-call bar)
-# except at N = 16384, where log det sums 16384 terms of a cancellation-prone
-# difference and the reference's OWN algorithm switches (LD vs Schur) already
-# differ by up to 2.7e-9; there the bar is 1e-8.
-TRACE_TOL = {"4x": CALL_TOL, 5: 1e-8, "deact": CALL_TOL}
+# except at N = 16384.  There the reference's OWN algorithm switches move the
+# trace by more than 1e-9: LD vs Schur by up to 2.7e-9, and
+# its default NUFFT statistics vs exact direct sums (steer_method "auto" vs
+# "direct", both stored in golden_cfg5.npz) by 5.2e-8 on problem 1 (records
+# 23-24, L-BFGS refine steps: the step is accepted on an objective change
+# near roundoff).  The bar is ~2x that spread, 1e-7; the events, model
+# order and final estimates keep the north-star bars.
+TRACE_TOL = {"4x": CALL_TOL, 5: 1e-7, "deact": CALL_TOL}
+
 
 
 @pytest.mark.parametrize("cfg", ["4x", 5])
@@ -90,11 +95,12 @@ def test_large_trajectories_against_reference(cfg):
         if same:
             assert r.iterations == int(z[p + "iterations"])
         check_estimates(r, z, p)
-        if cfg == 5 and b == 0:
+        if cfg == 5:
             # the reference run with exact direct sums (steer_method="direct")
             # gives the same history; the GPU matches it too
-            check_traj(r, z, "p0d_", near_ties(cfg, b))
-            check_estimates(r, z, "p0d_")
+            trd, gtd, _ = check_traj(r, z, f"p{b}d_", near_ties(cfg, b))
+            assert np.max(np.abs(trd - gtd) / np.abs(gtd), initial=0) < TRACE_TOL[cfg]
+            check_estimates(r, z, f"p{b}d_")
 
 
 def test_cfg5_levinson_inside_solver():
@@ -118,12 +124,16 @@ LARGE_CALLS = [("4x", 1, "truth"), ("4x", 1, "final"), ("4x", 2, "truth"), ("4x"
 
 
 def _golden_vec(z, key, n_full, decim):
-    """(values, indices) of a possibly decimated golden vector."""
+    """(values, indices, inf-norm of the FULL golden vector) of a possibly
+    decimated golden vector: the relative error is always taken against the
+    full vector's inf-norm (north_star "relative" = ||d||/||ref||), which the
+    fixture stores beside the decimated values (at the empty state the only
+    nonzero omega lag, i = 0, is not on the decimated index set)."""
     if key in z.files:
         v = z[key]
-        return v, np.arange(v.size)
+        return v, np.arange(v.size), float(np.max(np.abs(v)))
     v = z[key + "_dec"]
-    return v, np.arange(0, n_full, decim)[: v.size]
+    return v, np.arange(0, n_full, decim)[: v.size], float(z[key + "_max"])
 
 
 @pytest.mark.parametrize("method", ["levinson", "schur"])
@@ -167,13 +177,16 @@ def test_large_per_call_against_reference(cfg, b, state, method):
     w_r = _dev(z[p + "w"][None, :])
     qg, sg = ops.grid_eval(rho_r, dl_r, w_r, L)
     for key, got in (("q_grid", _np(qg)[0]), ("s_grid", _np(sg)[0])):
-        want, idx = _golden_vec(z, p + key, L, decim)
-        assert rel(got[idx], want) < CALL_TOL, key
+        want, idx, den = _golden_vec(z, p + key, L, decim)
+        assert np.max(np.abs(got[idx] - want)) / den < CALL_TOL, key
+        assert abs(np.max(np.abs(got)) - den) <= CALL_TOL * den, key
     # row 7
     om = ops.omegas(rho_r, dl_r)
     for kind in "stvx":
-        want, idx = _golden_vec(z, p + "om_" + kind, 2 * n - 1, decim)
-        assert rel(_np(om[kind])[0][idx], want) < CALL_TOL, kind
+        want, idx, den = _golden_vec(z, p + "om_" + kind, 2 * n - 1, decim)
+        got = _np(om[kind])[0]
+        assert np.max(np.abs(got[idx] - want)) / den < CALL_TOL, kind
+        assert abs(np.max(np.abs(got)) - den) <= CALL_TOL * den, kind
     # row 8 (reference stats evaluated with exact direct sums)
     if k:
         st = ops.component_stats(tht, kc, rho_r, dl_r, w_r)
