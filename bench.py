@@ -342,7 +342,7 @@ def solve_rate(torch, dev, stream, flush, cfg, steps, warmup, B=None, start=0):
     n = simdata.CONFIGS[cfg][1]
     Y = simdata.batch(SEED, cfg, B, start=start)
     ydev = torch.from_numpy(Y).to(dev)
-    solver = BatchSolver(n, B, EstimatorOptions(grid_factor=4), device=dev)
+    solver = BatchSolver(n, B, EstimatorOptions(grid_factor=4, backend="superfast"), device=dev)
     ms = time_steps(torch, stream, lambda: solver.solve(ydev), steps, warmup, flush)
     h = solver.host_outputs()
     return Y, solver, ms, h
@@ -363,7 +363,7 @@ def run_ours(args):
     cfg = args.config
     B = args.batch or simdata.CONFIGS[cfg][0]
     n = simdata.CONFIGS[cfg][1]
-    opts = EstimatorOptions(grid_factor=4)
+    opts = EstimatorOptions(grid_factor=4, backend="superfast")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream(dev)
 

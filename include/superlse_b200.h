@@ -29,6 +29,11 @@
  *   slse_estimate_batch    <- estimator.estimate :117-275 (complete data, G = 1,
  *                             backend "superfast"), one problem per batch row
  *   slse_estimate_batch_mmv <- estimator.estimate_mmv :278-283 (G >= 1 snapshots)
+ *   slse_estimate_batch_semifast <- estimator.estimate :117-275 with backend "semifast"
+ *                             (SemifastEngine, model_core.py:456-460; complete or
+ *                             incomplete data, Observation :43-130)
+ *   slse_semifast_bundle   <- model_core._SemifastBundle :316-409 (data_term, stats, grid)
+ *                             with nufft.gram :184-210
  */
 #ifndef SUPERLSE_B200_H
 #define SUPERLSE_B200_H
@@ -40,7 +45,7 @@
 extern "C" {
 #endif
 
-#define SLSE_ABI_VERSION 2
+#define SLSE_ABI_VERSION 3
 
 /* EstimatorOptions (estimator.py:34-50), superfast fields. */
 typedef struct slse_options {
@@ -59,13 +64,18 @@ typedef struct slse_options {
                                     0 "auto" (superfast from N >= 4096), 1 "levinson"
                                     (Schur-Levinson, O(N^2)), 2 "schur" (superfast
                                     divide-and-conquer generalized Schur, O(N log^2 N)) */
+  int k_cap;                     /* semifast backend only: K x K matrices are sized k_cap
+                                    (<= 0: min(k_max, 64)); a problem whose active set
+                                    outgrows it stops with status 3 (rerun it with a
+                                    larger k_cap; estimator.py does so automatically) */
 } slse_options;
 
 /* Outputs of slse_estimate_batch (device pointers, per problem b at offset
  * b * stride).  K = k_max, T = trace_capacity, E = event_capacity. */
 typedef struct slse_outputs {
   int32_t* k_hat;        /* [B] */
-  int32_t* status;       /* [B] 0 ok, 1 not PD, 2 invalid diagonal */
+  int32_t* status;       /* [B] 0 ok, 1 not PD, 2 invalid diagonal, 3 semifast
+                                  active set outgrew k_cap */
   int32_t* iterations;   /* [B] */
   int32_t* flags;        /* [B] bit0 converged, bit1 K_max-cap warning,
                                   bit2 trace truncated, bit3 events truncated */
@@ -173,6 +183,31 @@ size_t slse_estimate_workspace_bytes_mmv(int N, int G, int B, const slse_options
 int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_options* opts,
                             const slse_outputs* out, void* workspace, size_t workspace_bytes,
                             void* stream);
+
+/* Semifast (Woodbury) backend, complete or incomplete data: the whole
+ * estimate() per problem with _SemifastBundle (model_core.py:316-409).
+ * y: [B, G, M] complex observed samples; the observation pattern is
+ * idx[M] (0-based positions, sorted, unique, < N) and scales[M] complex
+ * (NULL = ones), shared by the batch (pattern_stride 0) or given per problem
+ * (pattern_stride M: idx [B, M], scales [B, M]).  Outputs as slse_estimate_batch
+ * with K = k_max (default M). */
+size_t slse_estimate_workspace_bytes_semifast(int N, int M, int G, int B, const slse_options* opts);
+int slse_estimate_batch_semifast(const double* y, int N, int M, int G, int B, const int32_t* idx,
+                                 const double* scales, int pattern_stride, const slse_options* opts,
+                                 const slse_outputs* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* One semifast bundle per problem at (theta, gamma)[b, :kcount[b]] (rows of
+ * stride kstride) and beta[b] on the pattern above (grid length L): data_term
+ * [B] (G ln|C| + sum_g y_g^H C^-1 y_g), e [B, G, N] complex (Phi^H C^-1 y),
+ * q, r, u [B, G, kstride] complex, s, x [B, kstride], t, v [B, kstride] complex,
+ * q_grid [B, G, L] complex, s_grid [B, L], status [B]; workspace from
+ * slse_semifast_bundle_workspace_bytes. */
+size_t slse_semifast_bundle_workspace_bytes(int N, int M, int G, int B, int L, int kstride);
+int slse_semifast_bundle(const double* theta, const double* gamma, const int32_t* kcount, int kstride,
+                         const double* beta, const double* y, int N, int M, int G, int B, const int32_t* idx,
+                         const double* scales, int pattern_stride, int L, double* data_term, double* e, double* q,
+                         double* r, double* u, double* s, double* t, double* v, double* x, double* q_grid,
+                         double* s_grid, int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ from .errors import SuperLseError
 
 _LIB_PATH = os.environ.get("SLSE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
                                                      "libsuperlse_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 c_int_p = ctypes.POINTER(ctypes.c_int32)
 
@@ -35,6 +35,7 @@ class SlseOptions(ctypes.Structure):
         ("trace_capacity", ctypes.c_int),
         ("event_capacity", ctypes.c_int),
         ("decomp_method", ctypes.c_int),
+        ("k_cap", ctypes.c_int),
     ]
 
 
@@ -86,6 +87,11 @@ def load():
         "slse_estimate_workspace_bytes_mmv": ([i, i, i, ctypes.POINTER(SlseOptions)], sz),
         "slse_estimate_batch_mmv": ([vp, i, i, i, ctypes.POINTER(SlseOptions), ctypes.POINTER(SlseOutputs), vp, sz,
                                      vp], i),
+        "slse_estimate_workspace_bytes_semifast": ([i, i, i, i, ctypes.POINTER(SlseOptions)], sz),
+        "slse_estimate_batch_semifast": ([vp, i, i, i, i, vp, vp, i, ctypes.POINTER(SlseOptions),
+                                          ctypes.POINTER(SlseOutputs), vp, sz, vp], i),
+        "slse_semifast_bundle_workspace_bytes": ([i, i, i, i, i, i], sz),
+        "slse_semifast_bundle": ([vp, vp, vp, i, vp, vp, i, i, i, i, vp, vp, i, i] + [vp] * 13 + [sz, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -223,6 +223,7 @@ void slse_default_options(slse_options* o) {
   o->trace_capacity = 0;
   o->event_capacity = 0;
   o->decomp_method = 0;
+  o->k_cap = 0;
 }
 
 int slse_cov_column(const double* theta, const double* gamma, const int32_t* kcount, int kstride, const double* beta,
@@ -605,6 +606,132 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
   }
 #undef SLSE_SOLVE_ARGS
   return e == cudaSuccess ? 0 : fail("solve_kernel", e);
+}
+
+// ------------------------------------------------------------ semifast
+}  // extern "C"
+
+namespace {
+// Launch geometry of the semifast solver (slse_solve_sf.cu).
+struct SfSetup {
+  SolveParams P;
+  size_t slab, smem;
+  int fft_cap, grid;
+};
+
+int sf_setup(int N, int M, int G, int B, const slse_options& o, SfSetup* S) {
+  if (N < 1 || M < 2 || M > N || G < 1 || B < 0) return fail_arg("semifast: need 2 <= M <= N, G >= 1, B >= 0");
+  SolveParams P = make_params(N, o);
+  P.g = G;
+  P.m = M;
+  P.semifast = 1;
+  P.dnc = 0;
+  P.kmax = o.k_max > 0 ? o.k_max : M;  // EstimationState K_max = M (estimator.py:126)
+  if (o.event_capacity <= 0) P.ecap = 4 * P.kmax + 64;
+  const int cap = o.k_cap > 0 ? o.k_cap : 64;
+  P.kcap = cap < P.kmax ? cap : P.kmax;
+  if (P.kcap < 1) P.kcap = 1;
+  SmemPlan plan = smem_plan(N, P.L, kSfThreads, false);
+  S->fft_cap = plan.fft_cap;
+  S->smem = red_bytes(kSfThreads) + 16 * (size_t)plan.fft_cap;
+  S->slab = make_layout(N, P.L, P.kmax, P.lbfgs_mem, false, false, G, 1, M, P.kcap).total;
+  int occ = 1;
+  cudaError_t e = slse_solve_sf_occupancy(S->smem, &occ);
+  if (e != cudaSuccess) return fail("semifast occupancy", e);
+  if (occ < 1) occ = 1;
+  int g = sm_count() * occ;
+  if (g > B) g = B;
+  if (g < 1) g = 1;
+  S->grid = g;
+  S->P = P;
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+size_t slse_estimate_workspace_bytes_semifast(int N, int M, int G, int B, const slse_options* opts) {
+  slse_options o;
+  if (opts) o = *opts; else slse_default_options(&o);
+  SfSetup S;
+  if (sf_setup(N, M, G, B, o, &S)) return 0;
+  return 256 + (size_t)S.grid * S.slab;
+}
+
+int slse_estimate_batch_semifast(const double* y, int N, int M, int G, int B, const int32_t* idx,
+                                 const double* scales, int pattern_stride, const slse_options* opts,
+                                 const slse_outputs* out, void* workspace, size_t workspace_bytes, void* stream) {
+  slse_options o;
+  if (opts) o = *opts; else slse_default_options(&o);
+  if (o.lbfgs_memory < 1 || o.lbfgs_memory > 16) return fail_arg("semifast: lbfgs_memory must be 1..16");
+  if (out == nullptr || idx == nullptr || (pattern_stride != 0 && pattern_stride != M))
+    return fail_arg("semifast: bad pattern arguments (pattern_stride must be 0 or M)");
+  if (B == 0) return 0;
+  SfSetup S;
+  int rc = sf_setup(N, M, G, B, o, &S);
+  if (rc) return rc;
+  const size_t need = 256 + (size_t)S.grid * S.slab;
+  if (workspace_bytes < need) {
+    snprintf(g_err, sizeof(g_err), "semifast: workspace %zu < required %zu bytes", workspace_bytes, need);
+    return -2;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const cplx* tw;
+  int twlog;
+  rc = twiddles(ilog2(S.P.L), st, &tw, &twlog);
+  if (rc) return rc;
+  int* queue = (int*)workspace;
+  cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(int), st);
+  if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
+  e = slse_solve_sf_launch(S.grid, S.smem, st, S.P, (const cplx*)y, idx, (const cplx*)scales, pattern_stride, B,
+                           *out, (char*)workspace + 256, S.slab, queue, tw, twlog, S.fft_cap);
+  return e == cudaSuccess ? 0 : fail("solve_sf_kernel", e);
+}
+
+size_t slse_semifast_bundle_workspace_bytes(int N, int M, int G, int B, int L, int kstride) {
+  if (!pow2(L) || L < N || kstride < 1) return 0;
+  slse_options o;
+  slse_default_options(&o);
+  o.k_max = kstride;
+  o.k_cap = kstride;
+  SfSetup S;
+  if (sf_setup(N, M, G, 1, o, &S)) return 0;
+  SolveParams P = S.P;
+  P.L = L;
+  return (size_t)B * make_layout(N, L, P.kmax, P.lbfgs_mem, false, false, G, 1, M, P.kcap).total;
+}
+
+int slse_semifast_bundle(const double* theta, const double* gamma, const int32_t* kcount, int kstride,
+                         const double* beta, const double* y, int N, int M, int G, int B, const int32_t* idx,
+                         const double* scales, int pattern_stride, int L, double* data_term, double* e, double* q,
+                         double* r, double* u, double* s, double* t, double* v, double* x, double* q_grid,
+                         double* s_grid, int32_t* status, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!pow2(L) || L < N || kstride < 1 || idx == nullptr || (pattern_stride != 0 && pattern_stride != M))
+    return fail_arg("slse_semifast_bundle: L must be a power of two >= N, kstride >= 1, pattern_stride 0 or M");
+  if (B == 0) return 0;
+  slse_options o;
+  slse_default_options(&o);
+  o.k_max = kstride;
+  o.k_cap = kstride;
+  SfSetup S;
+  int rc = sf_setup(N, M, G, 1, o, &S);
+  if (rc) return rc;
+  SolveParams P = S.P;
+  P.L = L;
+  SmemPlan plan = smem_plan(N, L, kSfThreads, false);
+  const size_t smem = red_bytes(kSfThreads) + 16 * (size_t)plan.fft_cap;
+  const size_t slab = make_layout(N, L, P.kmax, P.lbfgs_mem, false, false, G, 1, M, P.kcap).total;
+  if (workspace_bytes < (size_t)B * slab) return fail_arg("slse_semifast_bundle: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const cplx* tw;
+  int twlog;
+  rc = twiddles(ilog2(L), st, &tw, &twlog);
+  if (rc) return rc;
+  cudaError_t err = slse_sf_bundle_launch(
+      smem, st, P, theta, gamma, kcount, kstride, beta, (const cplx*)y, idx, (const cplx*)scales, pattern_stride, B,
+      (char*)workspace, slab, tw, twlog, plan.fft_cap, data_term, (cplx*)e, (cplx*)q, (cplx*)r, (cplx*)u, s, (cplx*)t,
+      (cplx*)v, x, (cplx*)q_grid, s_grid, status);
+  return err == cudaSuccess ? 0 : fail("sf_bundle_kernel", err);
 }
 
 }  // extern "C"

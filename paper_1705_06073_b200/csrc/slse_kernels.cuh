@@ -609,6 +609,113 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fus
   }
 }
 
+#ifdef SLSE_SEMIFAST
+// Semifast solver (slse_solve_sf.cu): the same persistent estimate() loop
+// with semifast bundles on an observation pattern (model_core.py:316-409);
+// y rows hold G x M observed samples, the pattern (idx, scales) is shared
+// by the batch (pstride 0) or given per problem (pstride M).
+template <int NT>
+__global__ void __launch_bounds__(NT) solve_sf_kernel(SolveParams P, const cplx* __restrict__ ys,
+                                                      const int* __restrict__ pidx, const cplx* __restrict__ psc,
+                                                      int pstride, int B, slse_outputs out, char* ws,
+                                                      size_t slab_bytes, int* queue, const cplx* tw, int twlog,
+                                                      int fft_cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* red = (double*)smem_raw;
+  cplx* region = (cplx*)(smem_raw + red_bytes(NT));
+  __shared__ int s_prob;
+  Blk b;
+  b.tid = threadIdx.x;
+  b.nt = NT;
+  b.red = red;
+  b.bank = 0;
+  FftCtx f;
+  f.tw = tw;
+  f.twlog = twlog;
+  f.smem = region;
+  f.smem_cap = fft_cap;
+  char* slab = ws + (size_t)blockIdx.x * slab_bytes;
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, false, false, P.g, 1, P.m, P.kcap);
+  for (;;) {
+    if (threadIdx.x == 0) s_prob = atomicAdd(queue, 1);
+    __syncthreads();
+    const int p = s_prob;
+    __syncthreads();
+    if (p >= B) break;
+    const ProbOut o = prob_out(out, P, p);
+    Solver S(b, P, nullptr, ys + (size_t)p * P.m * P.g, o, slab, lay, nullptr, f);
+    S.obs.idx = pidx + (size_t)p * pstride;
+    S.obs.sc = psc ? psc + (size_t)p * pstride : nullptr;
+    S.run();
+    b.bank = S.b.bank;
+    __syncthreads();
+  }
+}
+
+// Per-call semifast bundle (the parity tests' view of one bundle): one CTA
+// per problem builds the bundle of (theta, gamma, beta) and writes its data
+// term, e = Phi^H C^{-1} y, the component statistics and the grid.
+template <int NT>
+__global__ void __launch_bounds__(NT) sf_bundle_kernel(SolveParams P, const double* theta, const double* gamma,
+                                                       const int* kcount, int kstride, const double* beta,
+                                                       const cplx* __restrict__ ys, const int* __restrict__ pidx,
+                                                       const cplx* __restrict__ psc, int pstride, char* ws,
+                                                       size_t slab_bytes, const cplx* tw, int twlog, int fft_cap,
+                                                       double* data_term, cplx* e, cplx* q, cplx* r, cplx* u,
+                                                       double* s, cplx* t, cplx* v, double* x, cplx* q_grid,
+                                                       double* s_grid, int* status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Blk b;
+  b.tid = threadIdx.x;
+  b.nt = NT;
+  b.red = (double*)smem_raw;
+  b.bank = 0;
+  FftCtx f;
+  f.tw = tw;
+  f.twlog = twlog;
+  f.smem = (cplx*)(smem_raw + red_bytes(NT));
+  f.smem_cap = fft_cap;
+  const int p = blockIdx.x;
+  char* slab = ws + (size_t)p * slab_bytes;
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, false, false, P.g, 1, P.m, P.kcap);
+  ProbOut o = {};
+  Solver S(b, P, nullptr, ys + (size_t)p * P.m * P.g, o, slab, lay, nullptr, f);
+  S.obs.idx = pidx + (size_t)p * pstride;
+  S.obs.sc = psc ? psc + (size_t)p * pstride : nullptr;
+  const int kk = kcount[p];
+  for (int i = threadIdx.x; i < kk; i += NT) {
+    S.act_theta[i] = theta[(size_t)p * kstride + i];
+    S.act_gamma[i] = gamma[(size_t)p * kstride + i];
+  }
+  __syncthreads();
+  S.k = kk;
+  Bundle& B = S.bun[0];
+  const int st = S.sf_build(B, S.act_theta, S.act_gamma, kk, beta[p]);
+  if (threadIdx.x == 0) status[p] = st;
+  if (st != kOk) return;
+  if (threadIdx.x == 0) data_term[p] = B.data_term;
+  for (int i = threadIdx.x; i < P.n * P.g; i += NT) e[(size_t)p * P.n * P.g + i] = B.w[i];
+  if (kk) {
+    S.sf_stats(B, S.act_theta, kk);
+    for (int i = threadIdx.x; i < kk; i += NT) {
+      for (int g = 0; g < P.g; ++g) {
+        const size_t o_ = ((size_t)p * P.g + g) * kstride + i;
+        q[o_] = B.q[(size_t)g * P.kmax + i];
+        r[o_] = B.r[(size_t)g * P.kmax + i];
+        u[o_] = B.u[(size_t)g * P.kmax + i];
+      }
+      s[(size_t)p * kstride + i] = B.s[i];
+      t[(size_t)p * kstride + i] = B.t[i];
+      v[(size_t)p * kstride + i] = B.v[i];
+      x[(size_t)p * kstride + i] = B.x[i];
+    }
+  }
+  S.cur = 0;
+  S.sf_grid(B, 1.0, 0.0, q_grid + (size_t)p * P.g * P.L);
+  for (int l = threadIdx.x; l < P.L; l += NT) s_grid[(size_t)p * P.L + l] = S.sg[l];
+}
+#endif
+
 SLSE_D cplx ldg_c(const cplx* p) {
   const double2 d = __ldg((const double2*)p);
   return mk(d.x, d.y);
@@ -629,6 +736,21 @@ SLSE_DECL_SOLVE(128)
 SLSE_DECL_SOLVE(256)
 SLSE_DECL_SOLVE(512)
 SLSE_DECL_SOLVE(1024)
+
+// semifast solver (slse_solve_sf.cu, 128 threads per problem)
+constexpr int kSfThreads = 128;
+cudaError_t slse_solve_sf_occupancy(size_t smem, int* occ);
+cudaError_t slse_solve_sf_launch(int grid, size_t smem, cudaStream_t st, const slse::SolveParams& P,
+                                 const slse::cplx* ys, const int* idx, const slse::cplx* sc, int pstride, int B,
+                                 const slse_outputs& out, char* ws, size_t slab, int* queue, const slse::cplx* tw,
+                                 int twlog, int fft_cap);
+cudaError_t slse_sf_bundle_launch(size_t smem, cudaStream_t st, const slse::SolveParams& P, const double* theta,
+                                  const double* gamma, const int* kcount, int kstride, const double* beta,
+                                  const slse::cplx* ys, const int* idx, const slse::cplx* sc, int pstride, int B,
+                                  char* ws, size_t slab, const slse::cplx* tw, int twlog, int fft_cap,
+                                  double* data_term, slse::cplx* e, slse::cplx* q, slse::cplx* r, slse::cplx* u,
+                                  double* s, slse::cplx* t, slse::cplx* v, double* x, slse::cplx* q_grid,
+                                  double* s_grid, int* status);
 
 // warp-mode solver (slse_solve_warps.cu): W one-warp solvers per CTA
 cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t st, const slse::SolveParams& P,

@@ -1,0 +1,167 @@
+// slse_semifast.cuh -- the semifast (Woodbury) bundle: complete OR incomplete
+// data.
+//
+// Reference: _SemifastBundle (pkg/src/superlse/model_core.py:316-409), the
+// engine it serves (SemifastEngine :456-460, make_engine "auto" :466-472),
+// nufft.gram (nufft.py:184-210, direct evaluation) and the observation
+// operator Phi of Observation (model_core.py:43-130: scatter :109-117,
+// sample :119-123).
+//
+// With P the components of positive variance, E_ip = e^{j 2 pi n_i theta_p}
+// at the M observed positions n_i (scales a_i, weights w0_i = |a_i|^2,
+// d_i = 2 pi n_i):
+//   G_j        = E^H diag(w0 d^j) E                  (K x K, j = 0, 1, 2)
+//   Sigma^{-1} = G_0[P,P] / beta + diag(1 / gamma_P) = L L^H   (Cholesky)
+//   ln|C|      = M ln beta + sum_P ln gamma + 2 sum ln L_jj
+//   C^{-1} y   = y / beta - a . (E_P Sigma E_P^H Phi^H y) / beta^2
+//   e          = Phi^H C^{-1} y  (length N, zero off the pattern)
+//   stats      q, r, u = Psi^H [e, D e, D^2 e];  s, t, v, x = diag(G) / beta
+//              minus the Woodbury corrections (G Sigma G)_kk / beta^2
+//   grid       q^G = FFT_L(e);  s^G_l = sum w0 / beta - |L^{-1} b(l)|^2 / beta^2,
+//              b_p(l) = sum_i w0_i e^{-j 2 pi n_i theta_p} e^{+j 2 pi n_i l / L}
+// Everything is CTA-cooperative (Blk) on K x K matrices of leading dimension
+// kcap stored in the solver's workspace slab.
+#pragma once
+#include "slse_stats.cuh"
+
+#define SLSE_CTRL_LOOP_SF _Pragma("unroll 1")
+
+namespace slse {
+
+// Observation pattern of one problem (model_core.Observation): M observed
+// 0-based positions (sorted, < N) and their complex scales (nullptr = ones).
+struct SfObs {
+  const int* idx;
+  const cplx* sc;
+  int m;
+};
+
+SLSE_D cplx sf_scale(const SfObs& o, int i) { return o.sc ? o.sc[i] : mk(1.0, 0.0); }
+SLSE_D double sf_w0(const SfObs& o, int i) { return o.sc ? cabs2(o.sc[i]) : 1.0; }
+
+// E[i * ld + p] = e^{j 2 pi n_i theta_p}, i < m, p < kk (exactly reduced phases)
+SLSE_D void sf_phases(cplx* E, int ld, const SfObs& o, const double* th, int kk, Blk& b) {
+  const int tot = o.m * kk;
+  SLSE_CTRL_LOOP_SF
+  for (int t = b.tid; t < tot; t += b.nt) {
+    const int i = t / kk, p = t - i * kk;
+    E[(size_t)i * ld + p] = expj2pi((double)o.idx[i], th[p], 1.0);
+  }
+  b.sync();
+}
+
+// Weighted steering Gram matrices (nufft.gram, direct; model_core.py:331-333)
+// G_j[r, c] = sum_i w0_i d_i^j conj(E_ir) E_ic, Hermitian by construction
+// (the reference symmetrises, _hermitize :412-413: real diagonal).
+SLSE_D void sf_gram(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde, const SfObs& o, int kk, Blk& b) {
+  const int tot = kk * kk;
+  SLSE_CTRL_LOOP_SF
+  for (int t = b.tid; t < tot; t += b.nt) {
+    const int r = t / kk, c = t - r * kk;
+    if (r > c) continue;
+    cplx a0 = mk(0.0, 0.0), a1 = a0, a2 = a0;
+    SLSE_CTRL_LOOP_SF
+    for (int i = 0; i < o.m; ++i) {
+      const cplx e = cmulc(E[(size_t)i * lde + c], E[(size_t)i * lde + r]);  // E_ic conj(E_ir)
+      const double w0 = sf_w0(o, i);
+      const double d = 2.0 * kPi * (double)o.idx[i];
+      const double wd = w0 * d, wd2 = w0 * (d * d);
+      a0 = mk(fma(w0, e.re, a0.re), fma(w0, e.im, a0.im));
+      a1 = mk(fma(wd, e.re, a1.re), fma(wd, e.im, a1.im));
+      a2 = mk(fma(wd2, e.re, a2.re), fma(wd2, e.im, a2.im));
+    }
+    if (r == c) {
+      a0.im = 0.0;
+      a1.im = 0.0;
+      a2.im = 0.0;
+    }
+    G0[r * ld + c] = a0;
+    G1[r * ld + c] = a1;
+    G2[r * ld + c] = a2;
+    G0[c * ld + r] = conjg(a0);
+    G1[c * ld + r] = conjg(a1);
+    G2[c * ld + r] = conjg(a2);
+  }
+  b.sync();
+}
+
+// Cholesky (lower, scipy cho_factor(lower=True) role) of
+// A = G0[P,P] / beta + diag(1 / gamma_P) into Lc (strict lower part; the
+// diagonal of Lc keeps A_jj) and the real diagonal ld_[j] = L_jj.
+// Returns kNotPD if a pivot is not positive (scipy raises LinAlgError).
+SLSE_D int sf_cholesky(cplx* Lc, double* ldg, int ld, const cplx* G0, int ldg0, const int* P, const double* ga,
+                       int kp, double be, Blk& b) {
+  const int tot = kp * kp;
+  SLSE_CTRL_LOOP_SF
+  for (int t = b.tid; t < tot; t += b.nt) {
+    const int i = t / kp, j = t - i * kp;
+    if (j > i) continue;
+    const cplx g = G0[P[i] * ldg0 + P[j]];
+    Lc[i * ld + j] = i == j ? mk(g.re / be + 1.0 / ga[P[i]], 0.0) : mk(g.re / be, g.im / be);
+  }
+  b.sync();
+  SLSE_CTRL_LOOP_SF
+  for (int j = 0; j < kp; ++j) {
+    // every thread forms the pivot itself (identical bits, no broadcast)
+    double d = Lc[j * ld + j].re;
+    SLSE_CTRL_LOOP_SF
+    for (int k = 0; k < j; ++k) d -= cabs2(Lc[j * ld + k]);
+    if (!(d > 0.0)) return kNotPD;
+    const double ljj = sqrt(d);
+    if (b.tid == 0) ldg[j] = ljj;
+    SLSE_CTRL_LOOP_SF
+    for (int i = j + 1 + b.tid; i < kp; i += b.nt) {
+      cplx a = Lc[i * ld + j];
+      SLSE_CTRL_LOOP_SF
+      for (int k = 0; k < j; ++k) a = csub(a, cmulc(Lc[i * ld + k], Lc[j * ld + k]));  // L_ik conj(L_jk)
+      Lc[i * ld + j] = mk(a.re / ljj, a.im / ljj);
+    }
+    b.sync();
+  }
+  return kOk;
+}
+
+// X <- (L L^H)^{-1} X in place (scipy cho_solve), X: kp rows of nrhs
+// (row stride ldx).  Column-oriented substitutions, one barrier per pivot.
+SLSE_D void sf_cho_solve(const cplx* Lc, const double* ldg, int ld, int kp, cplx* X, int ldx, int nrhs, Blk& b) {
+  // forward: L z = x
+  SLSE_CTRL_LOOP_SF
+  for (int j = 0; j < kp; ++j) {
+    const double inv = 1.0 / ldg[j];
+    const int tot = (kp - j - 1) * nrhs;
+    SLSE_CTRL_LOOP_SF
+    for (int t = b.tid; t < tot; t += b.nt) {
+      const int i = j + 1 + t / nrhs, c = t % nrhs;
+      const cplx xj = cscale(X[j * ldx + c], inv);
+      X[i * ldx + c] = csub(X[i * ldx + c], cmul(Lc[i * ld + j], xj));
+    }
+    b.sync();
+  }
+  SLSE_CTRL_LOOP_SF
+  for (int t = b.tid; t < kp * nrhs; t += b.nt) {
+    const int i = t / nrhs, c = t % nrhs;
+    X[i * ldx + c] = cscale(X[i * ldx + c], 1.0 / ldg[i]);
+  }
+  b.sync();
+  // backward: L^H x = z
+  SLSE_CTRL_LOOP_SF
+  for (int j = kp - 1; j >= 0; --j) {
+    const double inv = 1.0 / ldg[j];
+    const int tot = j * nrhs;
+    SLSE_CTRL_LOOP_SF
+    for (int t = b.tid; t < tot; t += b.nt) {
+      const int i = t / nrhs, c = t % nrhs;
+      const cplx xj = cscale(X[j * ldx + c], inv);
+      X[i * ldx + c] = csub(X[i * ldx + c], cmul(conjg(Lc[j * ld + i]), xj));  // conj(L_ji) x_j
+    }
+    b.sync();
+  }
+  SLSE_CTRL_LOOP_SF
+  for (int t = b.tid; t < kp * nrhs; t += b.nt) {
+    const int i = t / nrhs, c = t % nrhs;
+    X[i * ldx + c] = cscale(X[i * ldx + c], 1.0 / ldg[i]);
+  }
+  b.sync();
+}
+
+}  // namespace slse

@@ -11,6 +11,7 @@
 #pragma once
 #include "slse_stats.cuh"
 #include "slse_dnc.cuh"
+#include "slse_semifast.cuh"
 #include "superlse_b200.h"
 
 #ifdef SLSE_HOST_EMU
@@ -80,6 +81,9 @@ struct SolveParams {
   int dnc_stockham;  // product transforms with the register Stockham passes
   int grid_fused;    // activation grid via the zero-padding-aware R x M decomposition
   int dnc_direct;    // superfast nodes up to this many steps use direct products
+  int m;             // observed samples per snapshot (Observation.m; = n for complete data)
+  int semifast;      // 1: semifast (Woodbury) bundles, slse_semifast.cuh (SLSE_SEMIFAST builds)
+  int kcap;          // semifast: K x K matrices sized kcap (active sets beyond it stop, status 3)
 };
 
 // Superfast divide-and-conquer factorisation: decomp_method 2 ("schur",
@@ -114,6 +118,9 @@ SLSE_HD SolveParams make_params(int n, const slse_options& o) {
   P.dnc_stockham = 0;
   P.grid_fused = 1;
   P.dnc_direct = SLSE_DNC_DIRECT;
+  P.m = n;
+  P.semifast = 0;
+  P.kcap = 0;
   return P;
 }
 
@@ -124,13 +131,17 @@ struct Layout {
   size_t dtmp, dl, q2, sg, theta, gamma, act_theta, act_gamma, st_s[2], st_x[2];
   size_t lbS, lbY, lbR, diag, g0, gnew, dir, pt, cand, cth, cga, marg, cflist_d;
   size_t z, act_slot, cidx, csort;
+  // semifast bundles (model_core.py:316-409): per bundle the Gram matrices,
+  // the Cholesky factor (kcap x kcap) and the positive-variance list; shared
+  // phases (m x kcap), solve scratch, A^H y and the grid's b(l) rows
+  size_t sfG0[2], sfG1[2], sfG2[2], sfL[2], sfLd[2], sfP[2], sfE, sfX, sfAhy, sfBb;
   size_t total;
 };
 
 SLSE_HD size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion_in_smem, bool dnc = false,
-                           int g = 1) {
+                           int g = 1, int semifast = 0, int m = 0, int kcap = 0) {
   Layout l;
   size_t o = 0;
   const size_t C = 16, D = 8, I = 4;
@@ -193,6 +204,23 @@ SLSE_HD Layout make_layout(int n, int L, int kmax, int lbfgs_mem, bool recursion
   l.act_slot = o; o = al(o + I * K);
   l.cidx = o; o = al(o + I * L);
   l.csort = o; o = al(o + I * L);
+  for (int i = 0; i < 2; ++i) l.sfG0[i] = l.sfG1[i] = l.sfG2[i] = l.sfL[i] = l.sfLd[i] = l.sfP[i] = 0;
+  l.sfE = l.sfX = l.sfAhy = l.sfBb = 0;
+  if (semifast) {
+    const size_t KC = (size_t)kcap, K2c = KC * KC;
+    for (int i = 0; i < 2; ++i) {
+      l.sfG0[i] = o; o = al(o + C * K2c);
+      l.sfG1[i] = o; o = al(o + C * K2c);
+      l.sfG2[i] = o; o = al(o + C * K2c);
+      l.sfL[i] = o; o = al(o + C * K2c);
+      l.sfLd[i] = o; o = al(o + D * KC);
+      l.sfP[i] = o; o = al(o + I * KC);
+    }
+    l.sfE = o; o = al(o + C * (size_t)m * KC);
+    l.sfX = o; o = al(o + C * KC * (KC > G ? KC : G));
+    l.sfAhy = o; o = al(o + C * KC * G);
+    l.sfBb = o; o = al(o + C * KC * (size_t)L);
+  }
   l.total = o;
   return l;
 }
@@ -317,11 +345,18 @@ SLSE_D unsigned long long now_ns() {
 
 struct Bundle {
   cplx* rho;
-  cplx* w;
+  cplx* w;  // C^{-1} y (superfast); e = Phi^H C^{-1} y (semifast), G rows of n
   cplx *q, *r, *u, *t, *v;
   double *s, *x;
   double data_term, delta_last, logdet;
   int stats_valid;
+  // semifast (model_core.py:316-409): Gram matrices, Cholesky factor of
+  // Sigma^{-1} (strict lower part + real diagonal sLd), positive list sP
+  cplx *sG0, *sG1, *sG2, *sL;
+  double* sLd;
+  int* sP;
+  int kp;
+  double sbeta;
 };
 
 struct Solver {
@@ -341,6 +376,10 @@ struct Solver {
   int cur_valid;
   // scalar state (identical in every thread)
   int n, L, kmax, k;
+  int m;  // observed samples per snapshot (P.m): y holds G rows of m
+  SfObs obs;
+  cplx *sfE, *sfX, *sfAhy, *sfBb;
+  int kcap;
   int G;  // snapshots (P.g): y, yhat and w hold G rows of n / nf; q, r, u, mu G rows of kmax
   double beta, zeta, energy, floor_beta;
   int status;
@@ -361,6 +400,13 @@ struct Solver {
                 char* slab, const Layout& lay, cplx* rec_smem, const FftCtx& fc)
       : b(blk), f(fc), P(p), cf(cf_), y(y_), o(out) {
     n = p.n; L = p.L; kmax = p.kmax; G = p.g;
+    m = p.m;
+    kcap = p.kcap;
+    obs.idx = nullptr;
+    obs.sc = nullptr;
+    obs.m = m;
+    sfE = (cplx*)(slab + lay.sfE); sfX = (cplx*)(slab + lay.sfX);
+    sfAhy = (cplx*)(slab + lay.sfAhy); sfBb = (cplx*)(slab + lay.sfBb);
     yhat = (cplx*)(slab + lay.yhat);
     c = (cplx*)(slab + lay.c);
     if (rec_smem) {
@@ -382,6 +428,14 @@ struct Solver {
       bun[i].x = (double*)(slab + lay.st_x[i]);
       bun[i].stats_valid = 0;
       bun[i].data_term = bun[i].delta_last = bun[i].logdet = 0.0;
+      bun[i].sG0 = (cplx*)(slab + lay.sfG0[i]);
+      bun[i].sG1 = (cplx*)(slab + lay.sfG1[i]);
+      bun[i].sG2 = (cplx*)(slab + lay.sfG2[i]);
+      bun[i].sL = (cplx*)(slab + lay.sfL[i]);
+      bun[i].sLd = (double*)(slab + lay.sfLd[i]);
+      bun[i].sP = (int*)(slab + lay.sfP[i]);
+      bun[i].kp = 0;
+      bun[i].sbeta = 0.0;
     }
     PP = (cplx*)(slab + lay.P); U = (cplx*)(slab + lay.U); V = (cplx*)(slab + lay.V);
     G0 = (cplx*)(slab + lay.G0); G1 = (cplx*)(slab + lay.G1); G2 = (cplx*)(slab + lay.G2);
@@ -470,6 +524,9 @@ struct Solver {
 
   SLSE_NIM int build(Bundle& B, const double* th, const double* ga, int kk, double be) {
     ++n_builds;
+#ifdef SLSE_SEMIFAST
+    return sf_build(B, th, ga, kk, be);
+#endif
     if (kk == 0) return build_white(B, be);
 #ifdef SLSE_WARP_MODE
     SLSE_PROF_T0(w0);
@@ -540,6 +597,10 @@ struct Solver {
   SLSE_NIM void stats(Bundle& B, const double* th, int kk) {
     if (B.stats_valid) return;
     ++n_stats;
+#ifdef SLSE_SEMIFAST
+    sf_stats(B, th, kk);
+    return;
+#endif
 #if defined(SLSE_WARP_MODE) && defined(SLSE_STATS_RV)
     SLSE_PROF_T0(w0);
     rv_arrive(0);
@@ -596,6 +657,248 @@ struct Solver {
   }
   double last_trace;
 
+#ifdef SLSE_SEMIFAST
+  // ---- semifast bundle (model_core._SemifastBundle :316-409) ----
+  // Bundle for (th[0..kk), ga[0..kk), be) on the observation pattern `obs`:
+  // Gram matrices, Cholesky of Sigma^{-1} over the positive-variance
+  // components, ln|C|, y^H C^{-1} y and e = Phi^H C^{-1} y (:320-363).
+  SLSE_NIM int sf_build(Bundle& B, const double* th, const double* ga, int kk, double be) {
+    const int tid_ = b.tid, nt_ = b.nt;
+    if (!(be > 0.0)) return kBadColumn;
+    if (kk > kcap) return kCapacity;
+    int kp = 0;
+    SLSE_CTRL_LOOP
+    for (int p = 0; p < kk; ++p) kp += ga[p] > 0.0 ? 1 : 0;  // self.pos (:325)
+    if (tid_ == 0) {
+      int j = 0;
+      for (int p = 0; p < kk; ++p)
+        if (ga[p] > 0.0) B.sP[j++] = p;
+    }
+    B.kp = kp;
+    B.sbeta = be;
+    // y^H y over the pattern, and A^H Phi^H y (steer_adjoint of scatter(y), :338)
+    double yy = 0.0;
+    SLSE_CTRL_LOOP
+    for (int i = tid_; i < m * G; i += nt_) yy += cabs2(y[i]);
+    const double quad_y = b.sum(yy);
+    double ln_c = (double)m * log(be);  // :339
+    double quad = quad_y / be;
+    if (kk) {
+      sf_phases(sfE, kcap, obs, th, kk, b);
+      sf_gram(B.sG0, B.sG1, B.sG2, kcap, sfE, kcap, obs, kk, b);
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kk * G; t += nt_) {
+        const int p = t / G, g = t - p * G;
+        const cplx* yg = y + (size_t)g * m;
+        cplx acc = mk(0.0, 0.0);
+        SLSE_CTRL_LOOP
+        for (int i = 0; i < m; ++i) {
+          const cplx ys = cmulc(yg[i], sf_scale(obs, i));           // scatter: conj(a_i) y_i
+          const cplx e = sfE[(size_t)i * kcap + p];
+          acc = mk(acc.re + e.re * ys.re + e.im * ys.im, acc.im + e.re * ys.im - e.im * ys.re);  // conj(E_ip) ys
+        }
+        sfAhy[t] = acc;
+      }
+      b.sync();
+    }
+    if (kp) {
+      const int st = sf_cholesky(B.sL, B.sLd, kcap, B.sG0, kcap, B.sP, ga, kp, be, b);  // :342-343
+      if (st != kOk) return st;
+      double lg = 0.0, ll = 0.0;
+      SLSE_CTRL_LOOP
+      for (int j = 0; j < kp; ++j) {
+        lg += log(ga[B.sP[j]]);
+        ll += log(B.sLd[j]);
+      }
+      ln_c += lg;         // :344
+      ln_c += 2.0 * ll;   // :345
+      // wp = Sigma A_P^H y (:346), kp x G
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kp * G; t += nt_) {
+        const int j = t / G, g = t - j * G;
+        sfX[t] = sfAhy[B.sP[j] * G + g];
+      }
+      b.sync();
+      sf_cho_solve(B.sL, B.sLd, kcap, kp, sfX, G, G, b);
+      double cr = 0.0;
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kp * G; t += nt_) {
+        const int j = t / G, g = t - j * G;
+        const cplx a = sfAhy[B.sP[j] * G + g], w = sfX[t];
+        cr += a.re * w.re + a.im * w.im;  // Re(conj(A^H y) wp)
+      }
+      const double corr = b.sum(cr);
+      quad = quad_y / be - corr / (be * be);  // :347-349
+    }
+    // e = scatter(y / beta - sample(A_P wp) / beta^2) (:350-351, :358)
+    SLSE_CTRL_LOOP
+    for (int i = tid_; i < n * G; i += nt_) B.w[i] = mk(0.0, 0.0);
+    b.sync();
+    SLSE_CTRL_LOOP
+    for (int t = tid_; t < m * G; t += nt_) {
+      const int g = t / m, i = t - g * m;
+      const cplx a = sf_scale(obs, i);
+      cplx cy = mk(y[t].re / be, y[t].im / be);
+      if (kp) {
+        cplx zs = mk(0.0, 0.0);
+        SLSE_CTRL_LOOP
+        for (int j = 0; j < kp; ++j) zs = cadd(zs, cmul(sfE[(size_t)i * kcap + B.sP[j]], sfX[j * G + g]));
+        const cplx az = cmul(a, zs);
+        const double b2 = be * be;
+        cy = csub(cy, mk(az.re / b2, az.im / b2));
+      }
+      B.w[(size_t)g * n + obs.idx[i]] = cmulc(cy, a);  // conj(a_i) (C^{-1} y)_i
+    }
+    b.sync();
+    B.data_term = (G == 1 ? ln_c : (double)G * ln_c) + quad;  // :355
+    B.stats_valid = 0;
+    return kOk;
+  }
+
+  // stats (:368-390): q, r, u = Psi^H [e, D e, D^2 e]; s, t, v, x from the
+  // Gram diagonals minus the Woodbury terms diag(G_a[:,P] Sigma G_b[P,:])
+  SLSE_NIM void sf_stats(Bundle& B, const double* th, int kk) {
+    const int tid_ = b.tid, nt_ = b.nt;
+    const double be = B.sbeta, b2 = be * be;
+    sf_phases(sfE, kcap, obs, th, kk, b);
+    SLSE_CTRL_LOOP
+    for (int t = tid_; t < kk * G; t += nt_) {
+      const int g = t / kk, p = t - g * kk;
+      const cplx* eg = B.w + (size_t)g * n;
+      cplx aq = mk(0.0, 0.0), ar = aq, au = aq;
+      SLSE_CTRL_LOOP
+      for (int i = 0; i < m; ++i) {
+        const int ni = obs.idx[i];
+        const double d = 2.0 * kPi * (double)ni;
+        const cplx ph = conjg(sfE[(size_t)i * kcap + p]);
+        const cplx e0 = eg[ni];
+        aq = cadd(aq, cmul(ph, e0));
+        ar = cadd(ar, cmul(ph, cscale(e0, d)));
+        au = cadd(au, cmul(ph, cscale(e0, d * d)));
+      }
+      B.q[(size_t)g * kmax + p] = aq;
+      B.r[(size_t)g * kmax + p] = ar;
+      B.u[(size_t)g * kmax + p] = au;
+    }
+    SLSE_CTRL_LOOP
+    for (int p = tid_; p < kk; p += nt_) {
+      B.s[p] = B.sG0[p * kcap + p].re / be;
+      B.t[p] = mk(B.sG1[p * kcap + p].re / be, B.sG1[p * kcap + p].im / be);
+      B.v[p] = mk(B.sG2[p * kcap + p].re / be, B.sG2[p * kcap + p].im / be);
+      B.x[p] = B.sG2[p * kcap + p].re / be;
+    }
+    b.sync();
+    const int kp = B.kp;
+    if (kp) {
+      // W00 = Sigma G0[P, :] (:381)
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kp * kk; t += nt_) {
+        const int j = t / kk, c = t - j * kk;
+        sfX[t] = B.sG0[B.sP[j] * kcap + c];
+      }
+      b.sync();
+      sf_cho_solve(B.sL, B.sLd, kcap, kp, sfX, kk, kk, b);
+      SLSE_CTRL_LOOP
+      for (int c = tid_; c < kk; c += nt_) {
+        double as = 0.0;
+        cplx at = mk(0.0, 0.0), av = at;
+        SLSE_CTRL_LOOP
+        for (int j = 0; j < kp; ++j) {
+          const cplx w = sfX[j * kk + c];
+          const int pj = B.sP[j];
+          const cplx g0 = B.sG0[c * kcap + pj], g1 = B.sG1[c * kcap + pj], g2 = B.sG2[c * kcap + pj];
+          as += g0.re * w.re - g0.im * w.im;
+          at = cadd(at, cmul(g1, w));
+          av = cadd(av, cmul(g2, w));
+        }
+        B.s[c] -= as / b2;                                    // :382
+        B.t[c] = csub(B.t[c], mk(at.re / b2, at.im / b2));   // :383
+        B.v[c] = csub(B.v[c], mk(av.re / b2, av.im / b2));   // :384
+      }
+      b.sync();
+      // W11 = Sigma G1[:, P]^H (:385), G1 Hermitian: rows G1[P, :]
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kp * kk; t += nt_) {
+        const int j = t / kk, c = t - j * kk;
+        sfX[t] = conjg(B.sG1[c * kcap + B.sP[j]]);
+      }
+      b.sync();
+      sf_cho_solve(B.sL, B.sLd, kcap, kp, sfX, kk, kk, b);
+      SLSE_CTRL_LOOP
+      for (int c = tid_; c < kk; c += nt_) {
+        double ax = 0.0;
+        SLSE_CTRL_LOOP
+        for (int j = 0; j < kp; ++j) {
+          const cplx w = sfX[j * kk + c], g1 = B.sG1[c * kcap + B.sP[j]];
+          ax += g1.re * w.re - g1.im * w.im;
+        }
+        B.x[c] -= ax / b2;  // :386
+      }
+      b.sync();
+    }
+    B.stats_valid = 1;
+  }
+
+  // grid (:392-409): q2 = sum_g |FFT_L(e_g)|^2, s^G = sum w0 / beta -
+  // |L^{-1} b(l)|^2 / beta^2 with b_p = L IFFT_L(scatter(w0 e^{-j 2 pi n theta_p}))
+  SLSE_NIM void sf_grid(Bundle& B, double gb, double lr, cplx* qg_out = nullptr) {
+    const int tid_ = b.tid, nt_ = b.nt;
+    const double be = B.sbeta, b2 = be * be;
+    for (int g = 0; g < G; ++g) {
+      const cplx* eg = B.w + (size_t)g * n;
+      const int nn = n;
+      double* q2_ = q2;
+      const int first = g == 0;
+      cplx* qo = qg_out ? qg_out + (size_t)g * L : nullptr;
+      fft(G0, L, -1.0, [=](int i) { return i < nn ? eg[i] : mk(0.0, 0.0); },
+          [=](int l, cplx v) {
+            q2_[l] = (first ? 0.0 : q2_[l]) + cabs2(v);
+            if (qo) qo[l] = v;
+          }, f, b);
+    }
+    double w0s = 0.0;
+    SLSE_CTRL_LOOP
+    for (int i = 0; i < m; ++i) w0s += sf_w0(obs, i);
+    const double base = w0s / be;  // :397
+    const int kp = B.kp;
+    if (kp) {
+      sf_phases(sfE, kcap, obs, act_theta, k, b);
+      for (int j = 0; j < kp; ++j) {  // b_p(l), p in P (:400-403)
+        cplx* row = sfBb + (size_t)j * L;
+        SLSE_CTRL_LOOP
+        for (int l = tid_; l < L; l += nt_) row[l] = mk(0.0, 0.0);
+        b.sync();
+        const int pj = B.sP[j];
+        SLSE_CTRL_LOOP
+        for (int i = tid_; i < m; i += nt_) row[obs.idx[i]] = cscale(conjg(sfE[(size_t)i * kcap + pj]), sf_w0(obs, i));
+        b.sync();
+        fft(G1, L, +1.0, [=](int i) { return row[i]; }, [=](int l, cplx v) { row[l] = v; }, f, b);
+      }
+      // |L^{-1} b(l)|^2 per grid point (b^H Sigma b, :404-405), in place
+      SLSE_CTRL_LOOP
+      for (int l = tid_; l < L; l += nt_) {
+        double acc = 0.0;
+        SLSE_CTRL_LOOP
+        for (int j = 0; j < kp; ++j) {
+          cplx a = sfBb[(size_t)j * L + l];
+          SLSE_CTRL_LOOP
+          for (int c = 0; c < j; ++c) a = csub(a, cmul(B.sL[j * kcap + c], sfBb[(size_t)c * L + l]));
+          a = mk(a.re / B.sLd[j], a.im / B.sLd[j]);
+          sfBb[(size_t)j * L + l] = a;
+          acc += cabs2(a);
+        }
+        sg[l] = base - acc / b2;
+      }
+    } else {
+      SLSE_CTRL_LOOP
+      for (int l = tid_; l < L; l += nt_) sg[l] = base;
+    }
+    SLSE_CTRL_LOOP
+    for (int l = tid_; l < L; l += nt_) dl[l] = gain_g(q2[l], sg[l], gb, lr, G);
+    b.sync();
+  }
+#endif
+
   // ---- activation (smlr.py:53-171) ----
   SLSE_NIM double gamma_bar() {
     const int tid_ = b.tid, nt_ = b.nt;  // smlr.py:53-59
@@ -606,7 +909,7 @@ struct Solver {
       double bar = b.sum(part) / (double)k;
       if (bar > 0.0) return bar;
     }
-    double g = energy / ((double)n * kGammaBarKInit);
+    double g = energy / ((double)m * kGammaBarKInit);  // obs.m (smlr.py:59)
     return g > kTiny ? g : kTiny;
   }
 
@@ -629,6 +932,10 @@ struct Solver {
     const int tid_ = b.tid, nt_ = b.nt;
     Bundle& B = bun[cur];
     const double lr = log((1.0 - ze) / ze);
+#ifdef SLSE_SEMIFAST
+    sf_grid(B, gb, lr);
+    return;
+#endif
     SLSE_PROF_T0(t0);
     if (G == 1 && P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) {
       SLSE_PROF_ADD(4, t0);
@@ -1099,29 +1406,31 @@ struct Solver {
     t_mark = t_start;
     // energy, floor, beta0 (model_core.py:125-130; estimator.py:135-137)
     double part = 0.0;
-    for (int i = b.tid; i < n * G; i += b.nt) {
+    for (int i = b.tid; i < m * G; i += b.nt) {
       part += cabs2(y[i]);
     }
     energy = b.sum(part);
     if (G != 1) energy /= (double)G;  // mean per-snapshot energy (model_core.py:125-127)
-    floor_beta = kBetaFloorScale * energy / (double)n;
-    const double b0 = kInitialBetaFrac * energy / (double)n;
+    floor_beta = kBetaFloorScale * energy / (double)m;
+    const double b0 = kInitialBetaFrac * energy / (double)m;
     beta = b0 > floor_beta ? b0 : floor_beta;
     zeta = kInitialZeta;
     for (int i = b.tid; i < kmax; i += b.nt) { z[i] = 0; theta[i] = 0.0; gamma[i] = 0.0; }
     k = 0;
-    // cached spectrum of y for every GS apply
+    // cached spectrum of y for every GS apply (superfast)
+#ifndef SLSE_SEMIFAST
     for (int g = 0; g < G; ++g) {
       const cplx* yg = y + (size_t)g * n;
       cplx* yh = yhat + ((size_t)g << ilog2(2 * n));
       fft(yh, 1 << ilog2(2 * n), -1.0, [=](int i) { return i < n ? yg[i] : mk(0.0, 0.0); },
           [=](int i, cplx v) { yh[i] = v; }, f, b);
     }
+#endif
     status = ensure_cur();
     if (status != kOk) { finish(0, 0); return; }
     record(kStInit);
     {  // warm-up beta (estimator.py:153)
-      const double v = energy / (double)n;
+      const double v = energy / (double)m;
       beta = floor_beta > v ? floor_beta : v;
       cur_valid = 0;
     }
@@ -1176,7 +1485,7 @@ struct Solver {
         const double tr = beta * b.sum(tr_part);
         value = residual_value(tr);
       } else {
-        value = energy / (double)n;
+        value = energy / (double)m;
       }
       const double bc = floor_beta > value ? floor_beta : value;
       {
@@ -1230,14 +1539,14 @@ struct Solver {
             lap(kTmObjective);
             if (k == 0) break;
           }
-          if (dec < (double)n * P.dec_tol_scale) break;
+          if (dec < (double)m * P.dec_tol_scale) break;
         }
         if (status != kOk) break;
       }
       lap(kTmRefine);
       if (o.iter_s && b.leader()) o.iter_s[it - 1] = (double)(now_ns() - t_iter) * 1e-9;  // estimator.py:247
       const double current = last_trace;
-      if (fabs(previous - current) < (double)n * P.conv_tol_scale) {
+      if (fabs(previous - current) < (double)m * P.conv_tol_scale) {
         converged = 1;
         break;
       }
@@ -1269,13 +1578,19 @@ struct Solver {
       else
 #endif
         steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
-      const cplx* yg = y + (size_t)g * n;
+      const cplx* yg = y + (size_t)g * m;
+#ifdef SLSE_SEMIFAST
+      // y - Phi Psi mu over the observed samples (estimator.py:86-87, Observation.sample)
+      SLSE_CTRL_LOOP
+      for (int i = tid_; i < m; i += nt_) part += cabs2(csub(yg[i], cmul(sf_scale(obs, i), c[obs.idx[i]])));
+#else
       SLSE_CTRL_LOOP
       for (int i = tid_; i < n; i += nt_) part += cabs2(csub(yg[i], c[i]));
+#endif
       b.sync();
     }
     const double resid = b.sum(part);
-    return (tr + (G == 1 ? resid : resid / (double)G)) / (double)n;
+    return (tr + (G == 1 ? resid : resid / (double)G)) / (double)m;
   }
 
   SLSE_NIM void finish(int iterations, int converged) {

@@ -7,12 +7,13 @@ and this module only packs inputs, launches ``slse_estimate_batch`` through
 the C ABI and unpacks results.  ``estimate_batch`` is the batched entry
 point (one problem per row).
 
-Scope: complete data, G >= 1 snapshots (MMV), the
-superfast backend.  ``backend="auto"`` runs superfast for complete data
-(the reference's auto picks its semifast backend below N = 512; both agree
-to ~1e-13 per call and give the same trajectories).
-``backend="semifast"`` and incomplete patterns are outside this
-build's scope and raise.
+Backends (model_core.make_engine :466-472): "superfast" (complete data,
+Toeplitz / Gohberg-Semencul bundles, the north-star path) and "semifast"
+(Woodbury bundles with a K x K Cholesky; complete or incomplete data,
+``Observation.incomplete``); "auto" picks superfast for complete data with
+N >= 512 and semifast otherwise, exactly as the reference.  Both run the
+whole loop on the device (csrc/slse_solver.cuh; semifast bundles in
+csrc/slse_semifast.cuh).  G >= 1 snapshots (MMV) on both.
 """
 
 from __future__ import annotations
@@ -32,7 +33,11 @@ DEFAULT_TAU = 5.0  # smlr.py:28
 STAGE_NAMES = ("init", "beta", "activate", "zeta", "refine", "deactivate")
 TIMER_NAMES = ("activate", "objective", "beta", "refine", "deactivate", "total")
 FLAG_CONVERGED, FLAG_KMAX_CAP, FLAG_TRACE_FULL, FLAG_EVENTS_FULL = 1, 2, 4, 8
-STATUS_OK, STATUS_NOT_PD, STATUS_BAD_DIAGONAL = 0, 1, 2
+STATUS_OK, STATUS_NOT_PD, STATUS_BAD_DIAGONAL, STATUS_KCAP = 0, 1, 2, 3
+SUPERFAST_MIN_N = 512  # model_core.py:469-470 ("auto": superfast for complete data from N = 512)
+# First-attempt K capacity of semifast solves (0: the library default,
+# min(K_max, 64)); problems whose active set outgrows it are re-solved at K_max.
+SEMIFAST_FIRST_KCAP = 0
 DECOMP_METHODS = {"auto": 0, "levinson": 1, "schur": 2}  # slse_options.decomp_method
 STEER_METHODS = ("auto", "direct", "nufft")
 
@@ -81,11 +86,21 @@ class LseResult:
     algorithms: dict = field(default_factory=dict)
 
 
+def resolve_backend(opts: EstimatorOptions, n: int, complete: bool = True) -> str:
+    """make_engine's choice (model_core.py:463-472)."""
+    if opts.backend not in BACKENDS:
+        raise ValueError(f"backend must be one of {BACKENDS}")
+    b = opts.backend
+    if b == "auto":
+        b = "superfast" if (complete and n >= SUPERFAST_MIN_N) else "semifast"
+    if b == "superfast" and not complete:
+        raise InvalidPattern("superfast backend requires the complete observation pattern")
+    return b
+
+
 def _validate(opts: EstimatorOptions):
     if opts.backend not in BACKENDS:
         raise ValueError(f"backend must be one of {BACKENDS}")
-    if opts.backend == "semifast":
-        raise NotImplementedError("the semifast (Woodbury) backend is outside this build's scope")
     if opts.decomp_method not in DECOMP_METHODS:  # toeplitz.py:263-276
         raise ValueError(f"unknown decomposition method {opts.decomp_method!r}")
     if opts.steer_method not in STEER_METHODS:  # nufft.py:118-123
@@ -94,7 +109,7 @@ def _validate(opts: EstimatorOptions):
         raise ValueError("lbfgs_memory must lie in 1..16 on the GPU path")
 
 
-def c_options(opts: EstimatorOptions, n: int) -> _native.SlseOptions:
+def c_options(opts: EstimatorOptions, n: int, k_cap: int = 0) -> _native.SlseOptions:
     o = _native.SlseOptions()
     o.grid_factor = int(opts.grid_factor)
     o.tau = float(opts.tau)
@@ -108,10 +123,11 @@ def c_options(opts: EstimatorOptions, n: int) -> _native.SlseOptions:
     o.trace_capacity = 2 + 13 * int(opts.max_outer_iterations)
     o.event_capacity = 4 * o.k_max + 64
     o.decomp_method = DECOMP_METHODS[opts.decomp_method]
+    o.k_cap = int(k_cap)
     return o
 
 
-def algorithms(opts: EstimatorOptions, n: int) -> dict:
+def algorithms(opts: EstimatorOptions, n: int, backend: str = "superfast") -> dict:
     """The algorithms the device runs for these options (reported in
     LseResult.algorithms).  decomp_method selects the Toeplitz factorisation
     exactly as toeplitz.decompose does (:263-276; "auto" switches to the
@@ -122,9 +138,13 @@ def algorithms(opts: EstimatorOptions, n: int) -> dict:
     the product form of SURVEY.md 8(a) rows 8-9 -- whatever steer_method
     says; the reference's "nufft" approximates the same sums to ~1e-10
     (SURVEY.md 8(c)), so it is accepted and served by the exact sums."""
+    if backend == "semifast":
+        return {"backend": "semifast", "decomp": "cholesky (Woodbury, K x K)",
+                "steer": "direct (exact Gram / Fourier sums)", "steer_requested": opts.steer_method}
     dm = opts.decomp_method
     schur = dm == "schur" or (dm == "auto" and n >= 4096)
-    return {"decomp": "generalized_schur (superfast D&C)" if schur else "levinson (Schur-Levinson)",
+    return {"backend": "superfast",
+            "decomp": "generalized_schur (superfast D&C)" if schur else "levinson (Schur-Levinson)",
             "steer": "direct (exact, product form)", "steer_requested": opts.steer_method}
 
 
@@ -268,26 +288,34 @@ class BatchSolver:
     contiguous complex128 (B, N) CUDA tensor.  ``results()`` copies back and
     unpacks.  No host synchronisation happens inside ``solve``."""
 
-    def __init__(self, n: int, batch: int, opts: EstimatorOptions = None, device=None, g: int = 1):
+    def __init__(self, n: int, batch: int, opts: EstimatorOptions = None, device=None, g: int = 1, m: int = None,
+                 backend: str = None, k_cap: int = 0):
         torch = _torch()
         self.opts = opts or EstimatorOptions()
         _validate(self.opts)
-        if n < 2:
+        self.m = int(m) if m is not None else n
+        if self.m < 2:
             raise ValueError("need at least two observed samples")
+        self.backend = backend or resolve_backend(self.opts, n, self.m == n)
+        if self.backend == "superfast" and self.m != n:
+            raise InvalidPattern("superfast backend requires the complete observation pattern")
         self.lib = _native.load()
         if not torch.cuda.is_available():
-            raise SuperLseError("no CUDA device: the superfast GPU path has no CPU fallback")
+            raise SuperLseError("no CUDA device: the GPU estimator has no CPU fallback")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.n, self.batch, self.g = n, batch, int(g)
         if self.g < 1:
             raise ValueError("need at least one snapshot")
-        self.copts = c_options(self.opts, n)
+        self.copts = c_options(self.opts, self.m, k_cap)
         self.kmax = self.copts.k_max
         self.L = default_grid_size(n, self.opts.grid_factor)
         with torch.cuda.device(self.device):
-            ws = self.lib.slse_estimate_workspace_bytes_mmv(n, self.g, batch, ctypes.byref(self.copts))
+            if self.backend == "semifast":
+                ws = self.lib.slse_estimate_workspace_bytes_semifast(n, self.m, self.g, batch, ctypes.byref(self.copts))
+            else:
+                ws = self.lib.slse_estimate_workspace_bytes_mmv(n, self.g, batch, ctypes.byref(self.copts))
             if ws == 0:
-                _native.check(-1, "slse_estimate_workspace_bytes_mmv")
+                _native.check(-1, "slse_estimate_workspace_bytes")
             self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
 
             def empty(shape, dt):
@@ -296,16 +324,44 @@ class BatchSolver:
             self.out = BatchOutputs(empty, batch, self.kmax, self.copts.trace_capacity, self.copts.event_capacity,
                                     g=self.g, max_outer=self.copts.max_outer_iterations)
         self.cout = self.out.struct(lambda t: t.data_ptr())
-        self.algorithms = algorithms(self.opts, n)
+        self.algorithms = algorithms(self.opts, n, self.backend)
         self._stream = None
+        self._pattern = None
+
+    def set_pattern(self, idx0, scales=None):
+        """Observation pattern of the semifast solve: 0-based positions
+        (M,) shared by the batch or (B, M) per problem, and complex scales of
+        the same shape (None = ones)."""
+        torch = _torch()
+        idx = torch.as_tensor(np.ascontiguousarray(idx0, dtype=np.int32)).to(self.device)
+        if idx.shape[-1] != self.m or idx.dim() not in (1, 2) or (idx.dim() == 2 and idx.shape[0] != self.batch):
+            raise DimensionMismatch("observed_indices must have shape (M,) or (B, M)")
+        sc = None
+        if scales is not None:
+            sc = torch.as_tensor(np.ascontiguousarray(scales, dtype=np.complex128)).to(self.device)
+            if tuple(sc.shape) != tuple(idx.shape):
+                raise DimensionMismatch("scales must have the shape of observed_indices")
+        self._pattern = (idx, sc, 0 if idx.dim() == 1 else self.m)
 
     def solve(self, y_dev, stream=None):
         torch = _torch()
-        want = (self.batch, self.n) if self.g == 1 else (self.batch, self.g, self.n)
+        w = self.m if self.backend == "semifast" else self.n
+        want = (self.batch, w) if self.g == 1 else (self.batch, self.g, w)
         if y_dev.dtype != torch.complex128 or not y_dev.is_contiguous() or tuple(y_dev.shape) != want:
             raise DimensionMismatch(f"y must be a contiguous complex128 tensor of shape {want}")
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         self._stream = st
+        if self.backend == "semifast":
+            if self._pattern is None:  # complete data: the identity pattern
+                self.set_pattern(np.arange(self.n, dtype=np.int32))
+            idx, sc, stride = self._pattern
+            rc = self.lib.slse_estimate_batch_semifast(
+                ctypes.c_void_p(y_dev.data_ptr()), self.n, self.m, self.g, self.batch,
+                ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(sc.data_ptr() if sc is not None else None), stride,
+                ctypes.byref(self.copts), ctypes.byref(self.cout), ctypes.c_void_p(self.workspace.data_ptr()),
+                ctypes.c_size_t(self.workspace.numel()), ctypes.c_void_p(st.cuda_stream))
+            _native.check(rc, "slse_estimate_batch_semifast")
+            return
         rc = self.lib.slse_estimate_batch_mmv(
             ctypes.c_void_p(y_dev.data_ptr()), self.n, self.g, self.batch, ctypes.byref(self.copts),
             ctypes.byref(self.cout), ctypes.c_void_p(self.workspace.data_ptr()),
@@ -407,14 +463,14 @@ class BatchResult:
 _SOLVERS = threading.local()
 
 
-def _cached_solver(n, batch, opts, device, g):
+def _cached_solver(n, batch, opts, device, g, m=None, backend=None, k_cap=0):
     """BatchSolver reuse across calls of one thread (device buffers and the
-    workspace are sized by (N, B, G, options, device)); results are host
-    copies, so reuse by sequential calls is safe."""
+    workspace are sized by (N, M, B, G, options, backend, device)); results
+    are host copies, so reuse by sequential calls is safe."""
     torch = _torch()
     opts = opts or EstimatorOptions()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    key = (n, batch, g, dataclasses.astuple(opts), str(dev))
+    key = (n, m, batch, g, dataclasses.astuple(opts), backend, k_cap, str(dev))
     cache = getattr(_SOLVERS, "cache", None)
     if cache is None:
         cache = _SOLVERS.cache = {}
@@ -422,34 +478,81 @@ def _cached_solver(n, batch, opts, device, g):
     if s is None:
         if len(cache) >= 4:
             cache.pop(next(iter(cache)))
-        s = cache[key] = BatchSolver(n, batch, opts, device=dev, g=g)
+        s = cache[key] = BatchSolver(n, batch, opts, device=dev, g=g, m=m, backend=backend, k_cap=k_cap)
     return s
 
 
-def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False) -> BatchResult:
-    """Solve B independent complete-data problems, y: (B, N) complex, or
-    (B, G, N) for G snapshots per problem sharing the frequencies (MMV).
-    Accepts numpy or torch input; returns a BatchResult (SoA arrays + a
-    sequence of LseResult in problem order).  Problems that hit a non-PD
-    covariance carry ``status`` 1 instead of raising."""
+def _check_pattern(n, m, observed_indices, scales, batch):
+    """Observation's pattern contract (model_core.py:66-81) for a shared (M,)
+    or per-problem (B, M) pattern: 1-based, sorted, unique, within 1..n.
+    Returns 0-based int32 positions and complex scales (or None)."""
+    idx = np.asarray(observed_indices, dtype=np.int64)
+    if idx.ndim not in (1, 2) or idx.shape[-1] != m or (idx.ndim == 2 and idx.shape[0] != batch):
+        raise DimensionMismatch("observed_indices must have length M (shape (M,) or (B, M))")
+    if np.any(np.diff(idx, axis=-1) <= 0):
+        raise ValueError("observed_indices must be sorted and unique")
+    if idx.min() < 1 or idx.max() > n:
+        raise ValueError("observed_indices must lie in 1..n")
+    sc = None
+    if scales is not None:
+        sc = np.asarray(scales, dtype=np.complex128)
+        if sc.shape != idx.shape:
+            raise DimensionMismatch("scales must have length M")
+    return (idx - 1).astype(np.int32), sc
+
+
+def estimate_batch(y, opts: EstimatorOptions = None, device=None, return_solver=False, n: int = None,
+                   observed_indices=None, scales=None) -> BatchResult:
+    """Solve B independent problems, y: (B, M) complex, or (B, G, M) for G
+    snapshots per problem sharing the frequencies (MMV).  Complete data
+    (default): M = N.  Incomplete data (the semifast backend,
+    model_core.Observation.incomplete): ``n`` and the 1-based
+    ``observed_indices`` (M,) shared by the batch or (B, M) per problem, with
+    optional complex ``scales`` of the same shape.  Accepts numpy or torch
+    input; returns a BatchResult (SoA arrays + a sequence of LseResult in
+    problem order).  Problems that hit a non-PD covariance carry ``status`` 1
+    instead of raising."""
     torch = _torch()
+    opts = opts or EstimatorOptions()
     if isinstance(y, torch.Tensor):
         yt = y
     else:
         yt = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(np.asarray(y, dtype=np.complex128))))
     if yt.dim() not in (2, 3):
-        raise DimensionMismatch("y must have shape (B, N) or (B, G, N)")
+        raise DimensionMismatch("y must have shape (B, M) or (B, G, M)")
     g = 1 if yt.dim() == 2 else int(yt.shape[1])
     if yt.dim() == 3 and g == 1:
         yt = yt[:, 0]
-    solver = _cached_solver(int(yt.shape[-1]), int(yt.shape[0]), opts, device, g)
+    m = int(yt.shape[-1])
+    B = int(yt.shape[0])
+    complete = observed_indices is None
+    if complete:
+        if n is not None and int(n) != m:
+            raise DimensionMismatch(f"complete data needs M == n, got {m} != {n}")
+        n = m
+    n = int(n)
+    backend = resolve_backend(opts, n, complete)
+    pattern = None if complete else _check_pattern(n, m, observed_indices, scales, B)
     # pinned input (e.g. a torch.Tensor from pin_memory()) goes up
     # asynchronously; pageable numpy memory is copied by the driver directly
     # (cheaper than page-locking it for one transfer)
     pinned = yt.device.type == "cpu" and yt.is_pinned()
-    ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=pinned).contiguous()
-    solver.solve(ydev)
-    res = BatchResult(solver.host_outputs(), solver.algorithms)
+    k_cap = SEMIFAST_FIRST_KCAP
+    while True:
+        solver = _cached_solver(n, B, opts, device, g, m=m, backend=backend, k_cap=k_cap)
+        ydev = yt.to(device=solver.device, dtype=torch.complex128, non_blocking=pinned).contiguous()
+        if pattern is not None:
+            solver.set_pattern(*pattern)
+        else:
+            solver._pattern = None
+        solver.solve(ydev)
+        h = solver.host_outputs()
+        if backend != "semifast" or not np.any(h["status"] == STATUS_KCAP) or k_cap >= solver.kmax:
+            break
+        # a semifast active set outgrew the K capacity: rerun at full K_max
+        # (whole batch; results are deterministic per problem)
+        k_cap = solver.kmax
+    res = BatchResult(h, solver.algorithms)
     return (res, solver) if return_solver else res
 
 
@@ -459,10 +562,13 @@ def estimate(obs: Observation, opts: EstimatorOptions = None) -> LseResult:
     if obs.m < 2:
         raise ValueError("need at least two observed samples")
     _validate(opts)
-    if not obs.is_complete:
-        raise InvalidPattern("superfast backend requires the complete observation pattern")
+    resolve_backend(opts, obs.n, obs.is_complete)  # InvalidPattern for superfast on incomplete data
     y = np.asarray(obs.y, dtype=np.complex128)
-    res = estimate_batch(y if obs.g == 1 else y[None], opts)[0]
+    if obs.is_complete:
+        res = estimate_batch(y if obs.g == 1 else y[None], opts)[0]
+    else:
+        res = estimate_batch(y if obs.g == 1 else y[None], opts, n=obs.n, observed_indices=obs.observed_indices,
+                             scales=obs.scales)[0]
     if res.status == STATUS_NOT_PD:
         raise NotPositiveDefinite("covariance lost positive definiteness during the fit")
     if res.status == STATUS_BAD_DIAGONAL:

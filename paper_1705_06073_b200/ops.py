@@ -156,3 +156,42 @@ def gradient_hessian(stats, gamma, kcount, n):
                                             _p(st["v"]), _p(st["x"]), _p(gamma), _p(kcount), K, n, B, _p(g), _p(d),
                                             _stream()), "slse_gradient_hessian")
     return g, d
+
+
+def semifast_bundle(theta, gamma, kcount, beta, y, n, L, idx0=None, scales=None):
+    """One semifast bundle per problem (model_core._SemifastBundle, :316-409):
+    theta/gamma (B, K) float64 with kcount (B,) int32 active entries, beta
+    (B,), y (B, M) or (B, G, M) complex observed samples, observation pattern
+    idx0 (M,) or (B, M) 0-based int32 (None: complete, M = n) and complex
+    scales of the same shape (None: ones), grid length L.  Returns a dict of
+    data_term (B,), e (B, G, n), q, r, u (B, G, K), s, t, v, x (B, K),
+    q_grid (B, G, L), s_grid (B, L), status (B,)."""
+    lib = _native.load()
+    _c128(y)
+    dev = y.device
+    B, K = theta.shape
+    K = max(K, 1)
+    g = 1 if y.dim() == 2 else int(y.shape[1])
+    m = int(y.shape[-1])
+    if idx0 is None:
+        idx0 = torch.arange(n, dtype=torch.int32, device=dev)
+    stride = 0 if idx0.dim() == 1 else m
+    ws_bytes = lib.slse_semifast_bundle_workspace_bytes(n, m, g, B, L, K)
+    if ws_bytes == 0:
+        _native.check(-1, "slse_semifast_bundle_workspace_bytes")
+    ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=dev)
+    c, f = torch.complex128, torch.float64
+    out = dict(data_term=torch.empty(B, dtype=f, device=dev), e=torch.empty((B, g, n), dtype=c, device=dev),
+               q=torch.zeros((B, g, K), dtype=c, device=dev), r=torch.zeros((B, g, K), dtype=c, device=dev),
+               u=torch.zeros((B, g, K), dtype=c, device=dev), s=torch.zeros((B, K), dtype=f, device=dev),
+               t=torch.zeros((B, K), dtype=c, device=dev), v=torch.zeros((B, K), dtype=c, device=dev),
+               x=torch.zeros((B, K), dtype=f, device=dev), q_grid=torch.empty((B, g, L), dtype=c, device=dev),
+               s_grid=torch.empty((B, L), dtype=f, device=dev), status=torch.empty(B, dtype=torch.int32, device=dev))
+    th = theta if theta.shape[1] else torch.zeros((B, 1), dtype=f, device=dev)
+    ga = gamma if gamma.shape[1] else torch.zeros((B, 1), dtype=f, device=dev)
+    _native.check(lib.slse_semifast_bundle(
+        _p(th.contiguous()), _p(ga.contiguous()), _p(kcount), K, _p(beta), _p(y), n, m, g, B, _p(idx0.contiguous()),
+        _p(scales.contiguous() if scales is not None else None), stride, L,
+        *[_p(out[k]) for k in ("data_term", "e", "q", "r", "u", "s", "t", "v", "x", "q_grid", "s_grid", "status")],
+        _p(ws), ws_bytes, _stream()), "slse_semifast_bundle")
+    return out

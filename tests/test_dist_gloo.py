@@ -42,7 +42,7 @@ def _worker(rank, world, port, Y, kmax, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         lo, hi = D.shard_range(Y.shape[0], rank, world)
-        res = H.estimate_batch(Y[lo:hi], EstimatorOptions(grid_factor=4))
+        res = H.estimate_batch(Y[lo:hi], EstimatorOptions(grid_factor=4, backend="superfast"))
         h = {"k_hat": np.array([r.k_hat for r in res]), "status": np.array([r.status for r in res]),
              "iterations": np.array([r.iterations for r in res]),
              "flags": np.array([int(r.converged) for r in res]), "beta": np.array([r.beta_hat for r in res]),
@@ -84,7 +84,7 @@ def test_two_rank_gloo_shard_and_gather():
         p.join(timeout=60)
         assert p.exitcode == 0
     got = D.unpack_results(full, kmax)
-    ref = H.estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    ref = H.estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for g, r in zip(got, ref):
         assert g["k_hat"] == r.k_hat
         assert np.array_equal(g["theta_hat"], r.theta_hat)
@@ -102,7 +102,7 @@ def _worker_api(rank, world, port, Y, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        opts = EstimatorOptions(grid_factor=4)
+        opts = EstimatorOptions(grid_factor=4, backend="superfast")
 
         class _Res:  # the BatchResult surface estimate_batch_distributed reads
             def __init__(self, h):
@@ -136,7 +136,7 @@ def test_two_rank_gloo_public_distributed_entry():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ref = H.estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    ref = H.estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     assert outs[0][1] == (0, 4) and outs[1][1] == (4, 7)
     for rank, shard, k_hat, theta, alpha, beta in outs:
         for b, r in enumerate(ref):

@@ -86,7 +86,7 @@ def test_large_trajectories_against_reference(cfg):
     z = load(cfg)
     probs = [int(b) for b in z["problems"]]
     Y = np.stack([z[f"p{b}_y"] for b in probs])
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for i, b in enumerate(probs):
         r = res[i]
         p = f"p{b}_"
@@ -111,7 +111,7 @@ def test_cfg5_levinson_inside_solver():
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
 
     z = load(5)
-    res = estimate_batch(z["p0_y"][None, :], EstimatorOptions(grid_factor=4, decomp_method="levinson"))
+    res = estimate_batch(z["p0_y"][None, :], EstimatorOptions(grid_factor=4, backend="superfast", decomp_method="levinson"))
     r = res[0]
     assert "levinson" in r.algorithms["decomp"]
     tr, gt, _ = check_traj(r, z, "p0_", near_ties(5, 0))
@@ -230,7 +230,7 @@ def test_deactivation_trajectories_against_reference():
     # ragged N across the cases: one batch per problem
     for b in range(count):
         p = f"p{b}_"
-        r = estimate_batch(z[p + "y"][None, :], EstimatorOptions(grid_factor=4))[0]
+        r = estimate_batch(z[p + "y"][None, :], EstimatorOptions(grid_factor=4, backend="superfast"))[0]
         assert any(ev[0] == "deactivate" for ev in r.events)
         tr, gt, same = check_traj(r, z, p, near_ties("deact", b))
         assert np.max(np.abs(tr - gt) / np.abs(gt), initial=0) < TRACE_TOL["deact"]
@@ -269,7 +269,7 @@ def test_deactivation_batch_vs_oracle():
     from test_gpu_parity import check_vs_oracle
 
     Y = O.generate_batch(99, 5, 24, n=128, k=16)
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     n_deact = 0
     for b in range(Y.shape[0]):
         o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
@@ -455,6 +455,6 @@ def test_kat_activation_on_grid_sinusoid():
     gbar = energy / (n * 4)  # smlr._gamma_bar fallback (:53-59)
     _, idx = ops.activation_curve(qg, sg, _dev(np.array([gbar])), _dev(np.array([0.2])), kmax)
     assert int(idx.item()) == 24
-    r = estimate(Observation.complete(y), EstimatorOptions(grid_factor=4))
+    r = estimate(Observation.complete(y), EstimatorOptions(grid_factor=4, backend="superfast"))
     assert r.k_hat >= 1
     assert np.min(wrap_distance(r.theta_hat, theta_true)) < 1e-6

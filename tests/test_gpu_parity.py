@@ -104,7 +104,7 @@ def test_trajectories_against_reference(cfg):
     z = load(cfg)
     count = int(z["count"])
     Y = np.stack([z[f"p{b}_y"] for b in range(count)])
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(count):
         _check_traj(res[b], z, f"p{b}_", near_ties(cfg, b))
 
@@ -114,7 +114,7 @@ def test_drop_in_estimate_single():
     from paper_1705_06073_b200 import EstimatorOptions, Observation, estimate
 
     z = load(1)
-    r = estimate(Observation.complete(z["p0_y"]), EstimatorOptions(grid_factor=4))
+    r = estimate(Observation.complete(z["p0_y"]), EstimatorOptions(grid_factor=4, backend="superfast"))
     _check_traj(r, z, "p0_", near_ties(1, 0))
     assert r.alpha_hat.shape == (1, r.k_hat)
     assert set(r.wall_time_per_stage) >= {"activate", "objective", "beta", "refine", "deactivate", "total"}
@@ -126,7 +126,7 @@ def test_batch_vs_oracle_cfg2_shape():
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
 
     Y = O.generate_batch(7, 2, 48)
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(Y.shape[0]):
         o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
         r = res[b]
@@ -146,7 +146,7 @@ def test_default_grid_factor_and_small_sizes():
     rng = np.random.default_rng(11)
     for n in (2, 3, 17, 64, 100):
         y = np.exp(2j * np.pi * 0.3 * np.arange(n)) + 0.1 * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
-        r = estimate_batch(y[None, :], EstimatorOptions())[0]
+        r = estimate_batch(y[None, :], EstimatorOptions(backend="superfast"))[0]
         o = O.estimate(y, O.OracleOptions())
         assert r.status == 0
         assert r.k_hat == o.k_hat, n
@@ -166,14 +166,14 @@ def test_pure_noise_and_zero_signal():
 
     rng = np.random.default_rng(5)
     Y = (rng.standard_normal((8, 128)) + 1j * rng.standard_normal((8, 128))) / np.sqrt(2)
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(8):
         o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
         assert res[b].k_hat == o.k_hat
         assert res[b].trace_stages == o.trace_stages
     # all-zero data: beta0 = 0 -> c_0 = 0 -> NotPositiveDefinite (toeplitz.py:55-57)
     with pytest.raises(NotPositiveDefinite):
-        estimate(Observation.complete(np.zeros(32, complex)), EstimatorOptions(grid_factor=4))
+        estimate(Observation.complete(np.zeros(32, complex)), EstimatorOptions(grid_factor=4, backend="superfast"))
 
 
 @pytest.mark.parametrize("cfg", [2, 3])
@@ -187,7 +187,7 @@ def test_trajectories_superfast_forced(cfg):
     z = load(cfg)
     count = int(z["count"])
     Y = np.stack([z[f"p{b}_y"] for b in range(count)])
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, decomp_method="schur"))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast", decomp_method="schur"))
     for b in range(count):
         assert "schur" in res[b].algorithms["decomp"]
         _check_traj(res[b], z, f"p{b}_", near_ties(cfg, b))
@@ -284,7 +284,7 @@ def test_mmv_trajectories_against_reference(cfg, g):
     z = _mmv()
     count = int(dict((int(c), int(n)) for c, gg, n in z["cases"] if int(gg) == g)[cfg])
     Y = np.stack([z[f"c{cfg}g{g}_p{b}_y"] for b in range(count)])  # (B, G, N)
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     assert res.alpha.shape[:2] == (count, g)
     for b in range(count):
         p = f"c{cfg}g{g}_p{b}_"
@@ -303,7 +303,7 @@ def test_mmv_drop_in_estimate():
     p = "c1g3_p2_"  # no near ties
     y = z[p + "y"]
     for fn in (estimate, estimate_mmv):
-        r = fn(Observation.complete(y), EstimatorOptions(grid_factor=4))
+        r = fn(Observation.complete(y), EstimatorOptions(grid_factor=4, backend="superfast"))
         _check_traj(r, z, p, [])
         assert r.alpha_hat.shape == (3, r.k_hat)
 
@@ -322,7 +322,7 @@ def test_paired_residency_batch(cfg):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     B = sms + 12
     Y = np.repeat(z["p0_y"][None, :], B, axis=0)
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in (0, B // 2, B - 1):
         _check_traj(res[b], z, "p0_", near_ties(cfg, 0))
     assert np.all(res.status == 0)
@@ -448,6 +448,6 @@ def test_trajectories_ragged_sizes_vs_oracle(n, k):
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
 
     Y = O.generate_batch(31, 2, 3, n=n, k=k)
-    res = estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(Y.shape[0]):
         check_vs_oracle(res[b], O.estimate(Y[b], O.OracleOptions(grid_factor=4)))

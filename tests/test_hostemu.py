@@ -18,7 +18,7 @@ CASES = [(1, b) for b in range(6)] + [(2, b) for b in range(4)] + [(3, 0)]
 def test_emulated_trajectory_matches_reference(cfg, b):
     z = load(cfg)
     p = f"p{b}_"
-    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4))[0]
+    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4, backend="superfast"))[0]
     assert r.status == 0
     assert r.k_hat == int(z[p + "k_hat"])
     assert np.array_equal(np.array([STAGES.index(s) for s in r.trace_stages]), z[p + "stages"])
@@ -55,7 +55,7 @@ def test_emulated_small_and_odd_sizes():
     rng = np.random.default_rng(11)
     for n in (2, 3, 17, 64, 100):
         y = np.exp(2j * np.pi * 0.3 * np.arange(n)) + 0.1 * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
-        r = H.estimate_batch(y[None, :], EstimatorOptions())[0]
+        r = H.estimate_batch(y[None, :], EstimatorOptions(backend="superfast"))[0]
         o = O.estimate(y, O.OracleOptions())
         assert r.k_hat == o.k_hat and r.trace_stages == o.trace_stages
         assert np.max(wrap_distance(r.theta_hat, o.theta_hat), initial=0) < THETA_TOL
@@ -64,16 +64,16 @@ def test_emulated_small_and_odd_sizes():
 def test_emulated_noise_and_zero():
     rng = np.random.default_rng(5)
     Y = (rng.standard_normal((4, 128)) + 1j * rng.standard_normal((4, 128))) / np.sqrt(2)
-    res = H.estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = H.estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(4):
         o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
         assert res[b].k_hat == o.k_hat and res[b].trace_stages == o.trace_stages
-    assert H.estimate_batch(np.zeros((1, 32), complex), EstimatorOptions(grid_factor=4))[0].status == 2
+    assert H.estimate_batch(np.zeros((1, 32), complex), EstimatorOptions(grid_factor=4, backend="superfast"))[0].status == 2
 
 
 def test_emulated_batch_vs_oracle_cfg2_shape():
     Y = O.generate_batch(7, 2, 12)
-    res = H.estimate_batch(Y, EstimatorOptions(grid_factor=4))
+    res = H.estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(Y.shape[0]):
         o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
         assert res[b].k_hat == o.k_hat
@@ -145,7 +145,7 @@ def test_emulated_trajectory_superfast(cfg, b):
     (decomp_method="schur", toeplitz.py:263-276)."""
     z = load(cfg)
     p = f"p{b}_"
-    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4, decomp_method="schur"))[0]
+    r = H.estimate_batch(z[p + "y"], EstimatorOptions(grid_factor=4, backend="superfast", decomp_method="schur"))[0]
     assert r.k_hat == int(z[p + "k_hat"])
     assert np.array_equal(np.array([STAGES.index(s) for s in r.trace_stages]), z[p + "stages"])
     assert np.array_equal(encode_events(r.events), z[p + "events"])

@@ -27,7 +27,7 @@ def gpu_rate(cfg, steps=2):
 
     B, n = simdata.CONFIGS[cfg][0], simdata.CONFIGS[cfg][1]
     Y = torch.from_numpy(simdata.batch(bench.SEED, cfg, B)).cuda()
-    s = BatchSolver(n, B, EstimatorOptions(grid_factor=4))
+    s = BatchSolver(n, B, EstimatorOptions(grid_factor=4, backend="superfast"))
     s.solve(Y)
     torch.cuda.synchronize()
     ms = []

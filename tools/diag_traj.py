@@ -14,7 +14,7 @@ z = load(cfg)
 probs = [int(b) for b in z["problems"]] if "problems" in z.files else list(range(int(z["count"])))
 for b in probs:
     p = f"p{b}_"
-    r = estimate_batch(z[p + "y"][None, :], EstimatorOptions(grid_factor=4, decomp_method=method))[0]
+    r = estimate_batch(z[p + "y"][None, :], EstimatorOptions(grid_factor=4, backend="superfast", decomp_method=method))[0]
     st = np.array([STAGES.index(s) for s in r.trace_stages]); gs = z[p + "stages"]
     tr = np.asarray(r.objective_trace); gt = z[p + "trace"]
     m = min(tr.size, gt.size)

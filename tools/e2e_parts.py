@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1705_06073_b200 import EstimatorOptions, simdata  # noqa: E402
 from paper_1705_06073_b200.estimator import BatchResult, _cached_solver, estimate_batch  # noqa: E402
 Y = simdata.batch(20261019, 2, 4096)
-opts = EstimatorOptions(grid_factor=4)
+opts = EstimatorOptions(grid_factor=4, backend="superfast")
 Yp = torch.from_numpy(Y).pin_memory()
 for it in range(4):
     torch.cuda.synchronize()

@@ -22,7 +22,7 @@ cfg = a.config
 B = a.batch or simdata.CONFIGS[cfg][0]
 n = simdata.CONFIGS[cfg][1]
 Y = torch.from_numpy(simdata.batch(20261019, cfg, B)).cuda()
-s = BatchSolver(n, B, EstimatorOptions(grid_factor=4))
+s = BatchSolver(n, B, EstimatorOptions(grid_factor=4, backend="superfast"))
 ev = []
 for i in range(a.solves):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -31,7 +31,7 @@ a = ap.parse_args()
 n = simdata.CONFIGS[a.config][1]
 B = a.batch or simdata.CONFIGS[a.config][0]
 Y = torch.from_numpy(simdata.batch(20261019, a.config, B)).cuda()
-s = BatchSolver(n, B, EstimatorOptions(grid_factor=4))
+s = BatchSolver(n, B, EstimatorOptions(grid_factor=4, backend="superfast"))
 s.solve(Y)  # warm-up
 lib = _native.load()
 out = (ctypes.c_ulonglong * 16)()

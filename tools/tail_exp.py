@@ -8,7 +8,7 @@ from paper_1705_06073_b200 import EstimatorOptions, simdata  # noqa: E402
 from paper_1705_06073_b200.estimator import BatchSolver  # noqa: E402
 for B in (2368, 4096, 4736, 8192):
     Y = torch.from_numpy(simdata.batch(20261019, 2, B)).cuda()
-    s = BatchSolver(256, B, EstimatorOptions(grid_factor=4))
+    s = BatchSolver(256, B, EstimatorOptions(grid_factor=4, backend="superfast"))
     s.solve(Y); torch.cuda.synchronize()
     ms = []
     for _ in range(3):
