@@ -1,8 +1,10 @@
 """CPU oracle for the Superfast LSE inner loop -- TEST INFRASTRUCTURE ONLY.
 
 This module is a plain-numpy restatement of the reference algorithm
-(`superlse`, /root/reference/pkg/src/superlse) for the complete-data,
-single-snapshot (G = 1) superfast path.  It exists for three purposes only:
+(`superlse`, /root/reference/pkg/src/superlse): the superfast bundle
+(complete data) and the semifast (Woodbury) bundle (complete or incomplete
+data), G >= 1 snapshots, and the estimator loop.  It exists for three
+purposes only:
 
 * the checker in ``tests/`` (parity of the CUDA path against it),
 * ``__graft_entry__.smoke()`` (one small check on cuda:0),
@@ -340,6 +342,121 @@ class Bundle:
         return self._grid[length]
 
 
+# --- semifast bundle ----------------------------------------
+def gram(t_rows, t_cols, weights, idx):
+    """nufft.gram direct branch (nufft.py:184-210): entry (i, k) =
+    sum_m w_m e^{j 2 pi (I(m) - 1)(theta_k - theta_i)}, I 1-based."""
+    er = np.exp(2j * np.pi * np.outer(idx - 1, t_rows))
+    ec = np.exp(2j * np.pi * np.outer(idx - 1, t_cols))
+    return (np.conj(er) * weights[:, None]).T @ ec
+
+
+def _chol_solve(lower, rhs):
+    """scipy cho_solve(lower=True): (L L^H)^{-1} rhs by two triangular solves."""
+    z = np.linalg.solve(lower, rhs)
+    return np.linalg.solve(np.conj(lower).T, z)
+
+
+class SemifastBundle:
+    """_SemifastBundle (model_core.py:316-409): Woodbury form of C on an
+    observation pattern (Observation, model_core.py:43-130; scatter :109-117,
+    sample :119-123).  y is (G, M) observed samples, idx 1-based positions,
+    scales complex (ones for complete data)."""
+
+    def __init__(self, y, n, idx, scales, thetas, gammas, beta):
+        y2 = np.atleast_2d(np.asarray(y, dtype=np.complex128))
+        self.y, self.n, self.idx, self.sc = y2, n, np.asarray(idx), np.asarray(scales, dtype=np.complex128)
+        self.g, m = y2.shape
+        self.thetas = np.asarray(thetas, dtype=np.float64)
+        self.gammas = np.asarray(gammas, dtype=np.float64)
+        self.beta = beta
+        self.pos = self.gammas > 0.0  # :325
+        w0 = np.abs(self.sc) ** 2
+        d1 = 2.0 * np.pi * (self.idx - 1)
+        self.w0 = w0
+        herm = lambda a: 0.5 * (a + np.conj(a).T)  # _hermitize :412-413
+        self.g0 = herm(gram(self.thetas, self.thetas, w0, self.idx))
+        self.g1 = herm(gram(self.thetas, self.thetas, w0 * d1, self.idx))
+        self.g2 = herm(gram(self.thetas, self.thetas, w0 * d1 ** 2, self.idx))
+        pos = self.pos
+        kp = int(np.count_nonzero(pos))
+        ycols = y2.T  # (M, G)
+        ys = self._scatter(ycols)
+        self.ahy = steer_adjoint(self.thetas, ys) if self.thetas.size else np.zeros((0, self.g), complex)
+        ln_c = m * np.log(beta)
+        if kp:
+            sigma_inv = self.g0[np.ix_(pos, pos)] / beta + np.diag(1.0 / self.gammas[pos])
+            self.chol = np.linalg.cholesky(sigma_inv)
+            ln_c += float(np.sum(np.log(self.gammas[pos])))
+            ln_c += 2.0 * float(np.sum(np.log(np.diag(self.chol).real)))
+            wp = _chol_solve(self.chol, self.ahy[pos])
+            quad = float(np.sum(np.abs(ycols) ** 2)) / beta - float(
+                np.sum(np.conj(self.ahy[pos]) * wp).real) / beta ** 2
+            z1 = steer_forward(self.thetas[pos], wp, n)
+            cinv_y = ycols / beta - self._sample(z1) / beta ** 2
+        else:
+            self.chol = None
+            quad = float(np.sum(np.abs(ycols) ** 2)) / beta
+            cinv_y = ycols / beta
+        self.ln_c = ln_c
+        self.data_term = self.g * ln_c + quad
+        self.e = self._scatter(cinv_y)  # (N, G)
+        self.w = self.e.T if self.g > 1 else self.e[:, 0]
+        self._stats = None
+        self._grid = {}
+
+    def _scatter(self, w):
+        out = np.zeros((self.n,) + w.shape[1:], dtype=np.complex128)
+        out[self.idx - 1] = np.conj(self.sc).reshape((-1,) + (1,) * (w.ndim - 1)) * w
+        return out
+
+    def _sample(self, z):
+        return self.sc.reshape((-1,) + (1,) * (z.ndim - 1)) * z[self.idx - 1]
+
+    def stats(self):
+        """:368-390."""
+        if self._stats is None:
+            beta = self.beta
+            d = 2.0 * np.pi * np.arange(self.n)
+            stack = np.concatenate((self.e, d[:, None] * self.e, (d ** 2)[:, None] * self.e), axis=1)
+            adj = steer_adjoint(self.thetas, stack)
+            g = self.g
+            q, r, u = adj[:, :g].T, adj[:, g:2 * g].T, adj[:, 2 * g:].T
+            pos = self.pos
+            s = np.diag(self.g0).real / beta
+            t = np.diag(self.g1).astype(np.complex128) / beta
+            v = np.diag(self.g2).astype(np.complex128) / beta
+            x = np.diag(self.g2).real / beta
+            if self.chol is not None:
+                w00 = _chol_solve(self.chol, self.g0[pos])
+                s = s - np.einsum("kp,pk->k", self.g0[:, pos], w00).real / beta ** 2
+                t = t - np.einsum("kp,pk->k", self.g1[:, pos], w00) / beta ** 2
+                v = v - np.einsum("kp,pk->k", self.g2[:, pos], w00) / beta ** 2
+                w11 = _chol_solve(self.chol, np.conj(self.g1[:, pos]).T)
+                x = x - np.einsum("kp,pk->k", self.g1[:, pos], w11).real / beta ** 2
+            one = g == 1
+            self._stats = dict(q=q[0] if one else q, r=r[0] if one else r, u=u[0] if one else u,
+                               s=s, t=t, v=v, x=x)
+        return self._stats
+
+    def grid(self, length):
+        """:392-409; q_grid is (G, L) for G > 1 snapshots."""
+        if length not in self._grid:
+            beta = self.beta
+            q_grid = np.fft.fft(self.e, n=length, axis=0).T
+            s_grid = np.full(length, float(np.sum(self.w0)) / beta)
+            pos = self.pos
+            if self.chol is not None and np.any(pos):
+                phases = np.exp(-2j * np.pi * np.outer(self.idx - 1, self.thetas[pos]))
+                scat = np.zeros((length, int(np.count_nonzero(pos))), dtype=np.complex128)
+                np.add.at(scat, self.idx - 1, self.w0[:, None] * phases)
+                b = (length * np.fft.ifft(scat, axis=0)).T
+                wb = _chol_solve(self.chol, b)
+                s_grid = s_grid - np.einsum("pl,pl->l", np.conj(b), wb).real / beta ** 2
+            self._grid[length] = (q_grid[0] if self.g == 1 else q_grid, s_grid)
+        return self._grid[length]
+
+
 # --- Row 10: activation -----------------------------------------------------------
 def gamma_bar(active_gamma, energy, m):
     """smlr.py:53-59."""
@@ -493,6 +610,7 @@ class OracleOptions:
     initial_sweep_iterations: int = 3
     lbfgs_memory: int = 10
     k_max: int = None
+    backend: str = "superfast"  # or "semifast" (model_core.py:456-472)
 
 
 class _State:
@@ -525,9 +643,10 @@ class _State:
 class _Engine:
     """LRU(4) bundle cache keyed on the exact state bytes (model_core.py:416-444)."""
 
-    def __init__(self, y, grid_size):
+    def __init__(self, y, grid_size, pattern=None):
         self.y = y
         self.grid_size = grid_size
+        self.pattern = pattern  # None: superfast bundles; (n, idx 1-based, scales): semifast
         self._b = {}
         self._order = []
         self.builds = 0
@@ -539,7 +658,10 @@ class _Engine:
         hit = self._b.get(key)
         if hit is not None:
             return hit
-        b = Bundle(self.y, th, ga, float(st.beta))
+        if self.pattern is None:
+            b = Bundle(self.y, th, ga, float(st.beta))
+        else:
+            b = SemifastBundle(self.y, *self.pattern, th, ga, float(st.beta))
         self.builds += 1
         self._b[key] = b
         self._order.append(key)
@@ -681,9 +803,11 @@ class OracleResult:
     margins: list = None  # every decision: (kind, margin, trace position)
 
 
-def estimate(y, opts: OracleOptions = None) -> OracleResult:
-    """estimator.py:117-275, complete data, superfast backend; y is one
-    snapshot (N,) or G snapshots (G, N) sharing the frequencies (MMV).
+def estimate(y, opts: OracleOptions = None, n=None, observed_indices=None, scales=None) -> OracleResult:
+    """estimator.py:117-275; y is one snapshot (M,) or G snapshots (G, M)
+    sharing the frequencies (MMV).  opts.backend "superfast" (complete data)
+    or "semifast" (complete, or incomplete with n, 1-based observed_indices
+    and complex scales: Observation.incomplete, model_core.py:43-130).
 
     `events` is the active-set history: ("sweep", [(slot, idx)...]),
     ("activate", slot, idx), ("deactivate", [slots]) in order."""
@@ -695,12 +819,21 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
     if y.ndim != 2:
         y = y.ravel()
     g = 1 if y.ndim == 1 else y.shape[0]
-    n = m = y.shape[-1]
+    m = y.shape[-1]
+    if observed_indices is None:
+        n = m
+        obs_idx, obs_sc = np.arange(1, m + 1), np.ones(m, dtype=np.complex128)
+    else:
+        obs_idx = np.asarray(observed_indices, dtype=np.int64)
+        obs_sc = np.ones(m, dtype=np.complex128) if scales is None else np.asarray(scales, dtype=np.complex128)
     if m < 2:
         raise ValueError("need at least two observed samples")
     k_max = opts.k_max if opts.k_max is not None else m
     L = default_grid_size(n, opts.grid_factor)
-    eng = _Engine(y, L)
+    semifast = opts.backend == "semifast"
+    if not semifast and observed_indices is not None:
+        raise ValueError("superfast backend requires the complete observation pattern")
+    eng = _Engine(y, L, (n, obs_idx, obs_sc) if semifast else None)
     energy = float(np.mean(np.sum(np.abs(np.atleast_2d(y)) ** 2, axis=1)))
     floor = BETA_FLOOR_SCALE * energy / m
     beta0 = max(INITIAL_BETA_ENERGY_FRACTION * energy / m, floor)
@@ -756,6 +889,8 @@ def estimate(y, opts: OracleOptions = None) -> OracleResult:
             mu = ga * stt["q"]  # (K,) or (G, K)
             tr = float(st.beta * np.sum(stt["s"] * ga))
             fitted = steer_forward(st.theta[st.z], mu if g == 1 else mu.T, n)
+            if semifast:  # y - sample(fitted) (estimator.py:86-87)
+                fitted = (obs_sc[:, None] * fitted[obs_idx - 1]) if g > 1 else obs_sc * fitted[obs_idx - 1]
             resid = y - fitted if g == 1 else y.T - fitted
             value = (tr + float(np.sum(np.abs(resid) ** 2)) / g) / m
         else:

@@ -194,3 +194,30 @@ def test_semifast_batched_patterns():
         assert rb.k_hat == r1.k_hat
         assert np.array_equal(rb.objective_trace, r1.objective_trace)
         assert np.array_equal(rb.theta_hat, r1.theta_hat)
+
+
+@pytest.mark.parametrize("n,k,m", [(64, 4, 40), (200, 8, 120), (512, 10, 300)])
+def test_semifast_incomplete_batch_vs_oracle(n, k, m):
+    """Seeded problems with per-problem random patterns and complex scales at
+    sizes between the fixtures (N = 512 runs 128-thread CTAs over an
+    L = 2048 grid): every CUDA trajectory vs the oracle's semifast
+    restatement on the same input."""
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
+    from oracle import superlse_oracle as O
+    from test_gpu_parity import check_vs_oracle
+
+    rng = np.random.default_rng([7, n, m])
+    Y, I, S = [], [], []
+    for b in range(6):
+        yf, _ = O.generate_problem(41, 2, b, n=n, k=k)
+        idx = np.sort(rng.choice(n, size=m, replace=False)) + 1
+        sc = rng.uniform(0.5, 1.5, m) * np.exp(2j * np.pi * rng.random(m))
+        Y.append(sc * yf[idx - 1])
+        I.append(idx)
+        S.append(sc)
+    Y, I, S = np.stack(Y), np.stack(I), np.stack(S)
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="semifast"), n=n, observed_indices=I, scales=S)
+    for b in range(Y.shape[0]):
+        o = O.estimate(Y[b], O.OracleOptions(grid_factor=4, backend="semifast"), n=n, observed_indices=I[b],
+                       scales=S[b])
+        check_vs_oracle(res[b], o)

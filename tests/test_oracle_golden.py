@@ -240,3 +240,60 @@ def test_cfg5_reference_self_spread():
         m = min(a.size, d.size)
         spread = max(spread, float(np.max(np.abs(a[:m] - d[:m]) / np.abs(a[:m]))))
     assert CALL_TOL < spread < CFG5_TRACE_TOL
+
+
+# ------------------------------------------------------------ semifast backend
+def _sf():
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_sf.npz"))
+
+
+SF_NAMES = ["c1a", "c1b", "c1c", "c2a", "c2b", "i1a", "i1b", "i2a", "i2b", "m1a", "d1a", "d1b"]
+
+
+def _sf_case(z, name):
+    p = name + "_"
+    idx = z[p + "idx"] if p + "idx" in z.files else None
+    sc = z[p + "scales"] if p + "scales" in z.files else None
+    return p, z[p + "y"], int(z[p + "n"]), idx, sc
+
+
+@pytest.mark.parametrize("name", SF_NAMES)
+def test_oracle_semifast_trajectory(name):
+    """The oracle's semifast restatement (SemifastBundle, model_core.py:316-409,
+    incomplete data included) reproduces the real reference's semifast runs:
+    same model order, stages and history; trace within 1e-12."""
+    z = _sf()
+    p, y, n, idx, sc = _sf_case(z, name)
+    r = O.estimate(y[0] if y.shape[0] == 1 else y, O.OracleOptions(grid_factor=4, backend="semifast"), n=n,
+                   observed_indices=idx, scales=sc)
+    assert r.k_hat == int(z[p + "k_hat"])
+    assert [STAGES.index(s) for s in r.trace_stages] == z[p + "stages"].tolist()
+    assert np.array_equal(encode_events(r.events), z[p + "events"])
+    gt = z[p + "trace"]
+    assert np.max(np.abs(r.objective_trace - gt) / np.abs(gt)) < 1e-12
+    assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
+    assert rel(r.alpha_hat, z[p + "alpha_hat"]) < AMP_TOL
+
+
+@pytest.mark.parametrize("name", ["c1a", "c2a", "i1b", "i2a", "m1a", "d1a"])
+def test_oracle_semifast_bundle(name):
+    """Per-call semifast bundle (data term, e, stats, grid) vs the reference
+    at every recorded state, to 1e-12."""
+    z = _sf()
+    p, y, n, idx, sc = _sf_case(z, name)
+    if idx is None:
+        idx, sc = np.arange(1, n + 1), np.ones(n, complex)
+    for state in [str(s) for s in z[p + "states"]]:
+        q = f"{p}call_{state}_"
+        b = O.SemifastBundle(y, n, idx, sc, z[q + "thetas"], z[q + "gammas"], float(z[q + "beta"]))
+        assert abs(b.data_term - float(z[q + "data_term"])) <= 1e-12 * abs(float(z[q + "data_term"]))
+        assert rel(b.e.T, z[q + "e"]) < 1e-12
+        qg, sg = b.grid(z[q + "q_grid"].shape[-1])
+        assert rel(np.atleast_2d(qg), z[q + "q_grid"]) < 1e-12
+        assert rel(sg, z[q + "s_grid"]) < 1e-12
+        if z[q + "thetas"].size:
+            st = b.stats()
+            for key in "qru":
+                assert rel(np.atleast_2d(st[key]), z[q + "st_" + key]) < 1e-11, key
+            for key in "stvx":
+                assert rel(st[key], z[q + "st_" + key]) < 1e-11, key
