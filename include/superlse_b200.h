@@ -34,6 +34,10 @@
  *                             incomplete data, Observation :43-130)
  *   slse_semifast_bundle   <- model_core._SemifastBundle :316-409 (data_term, stats, grid)
  *                             with nufft.gram :184-210
+ *   slse_sim_generate      <- simdata.generate :109-122 / generate_pairs :125-149 (on-device
+ *                             scenes, counter-based Philox stream)
+ *   slse_sim_metrics       <- simdata.nmse :160-169, csr :196-205 (+ nearest distances for
+ *                             bsr_trial :185-193, whose Hungarian assignment stays on the host)
  */
 #ifndef SUPERLSE_B200_H
 #define SUPERLSE_B200_H
@@ -208,6 +212,27 @@ int slse_semifast_bundle(const double* theta, const double* gamma, const int32_t
                          const double* scales, int pattern_stride, int L, double* data_term, double* e, double* q,
                          double* r, double* u, double* s, double* t, double* v, double* x, double* q_grid,
                          double* s_grid, int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/* On-device synthetic scenes (simdata.generate laws): trials independent
+ * scenes of n samples, m observed (first and last always; m = n: complete),
+ * k frequencies (pairs != 0: k / 2 pairs at intra_sep, generate_pairs), G
+ * snapshots, SNR snr_db, from the Philox stream keyed by (seed, point) with
+ * the trial index as counter.  Outputs: y [trials, G, m] complex, idx
+ * [trials, m] 0-based observed positions, theta [trials, k], alpha
+ * [trials, G, k] complex, beta [trials], status [trials] (0 ok, 1 infeasible
+ * separation).  workspace: slse_sim_workspace_bytes(n, trials). */
+size_t slse_sim_workspace_bytes(int n, int trials);
+int slse_sim_generate(unsigned long long seed, unsigned point, int trials, int n, int m, int k, int G, double snr_db,
+                      double min_sep, int pairs, double intra_sep, double* y, int32_t* idx, double* theta,
+                      double* alpha, double* beta, int32_t* status, void* workspace, void* stream);
+
+/* Metrics per trial (simdata.nmse, csr): nmse [trials], csr [trials] and
+ * mind [trials, k] (wrap distance of each true frequency to its nearest
+ * estimate, for the host's block-success check).  theta_est/alpha_est rows
+ * of stride kstride with k_hat[t] valid entries; alpha_est [trials, G, kstride]. */
+int slse_sim_metrics(int trials, int n, int G, const double* theta_true, const double* alpha_true, int k,
+                     const double* theta_est, const double* alpha_est, const int32_t* k_hat, int kstride,
+                     double* nmse, double* csr, double* mind, void* stream);
 
 #ifdef __cplusplus
 }

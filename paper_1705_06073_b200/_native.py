@@ -92,6 +92,9 @@ def load():
                                           ctypes.POINTER(SlseOutputs), vp, sz, vp], i),
         "slse_semifast_bundle_workspace_bytes": ([i, i, i, i, i, i], sz),
         "slse_semifast_bundle": ([vp, vp, vp, i, vp, vp, i, i, i, i, vp, vp, i, i] + [vp] * 13 + [sz, vp], i),
+        "slse_sim_workspace_bytes": ([i, i], sz),
+        "slse_sim_generate": ([ctypes.c_ulonglong, ctypes.c_uint, i, i, i, i, i, d, d, i, d] + [vp] * 8, i),
+        "slse_sim_metrics": ([i, i, i, vp, vp, i, vp, vp, vp, i, vp, vp, vp, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

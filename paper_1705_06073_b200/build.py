@@ -48,6 +48,7 @@ def _sources():
         units.append((f"slse_solve_{nt}", os.path.join(CSRC, "slse_solve_inst.cu"), [f"-DSLSE_NT={nt}"]))
     units.append(("slse_solve_warps", os.path.join(CSRC, "slse_solve_warps.cu"), ["-DSLSE_WARP_MODE"]))
     units.append(("slse_solve_sf", os.path.join(CSRC, "slse_solve_sf.cu"), ["-DSLSE_SEMIFAST"]))
+    units.append(("slse_sim", os.path.join(CSRC, "slse_sim.cu"), []))
     return hdrs, units
 
 
