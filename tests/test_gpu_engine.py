@@ -1,0 +1,63 @@
+"""Engine-level seam: the REFERENCE's own outer
+loop (superlse.estimator.estimate, installed unmodified in baseline/_ref by
+tools/install_reference.sh) driving GPU bundles through
+paper_1705_06073_b200.engine.make_engine, against the real-reference golden
+trajectories.  Skipped when baseline/_ref is absent."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from golden_util import AMP_TOL, CALL_TOL, STAGES, THETA_TOL, load, rel, wrap_distance
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+@pytest.fixture()
+def ref_superlse(monkeypatch):
+    if not os.path.isdir(os.path.join(REF, "superlse")):
+        pytest.skip("reference not installed (tools/install_reference.sh)")
+    monkeypatch.syspath_prepend(REF)
+    import superlse
+    from superlse import estimator as ref_est
+
+    from paper_1705_06073_b200 import engine
+
+    monkeypatch.setattr(ref_est, "make_engine", engine.make_engine)
+    return superlse
+
+
+def _compare(r, z, p, tol=CALL_TOL):
+    assert r.k_hat == int(z[p + "k_hat"])
+    assert [STAGES.index(s) for s in r.trace_stages] == z[p + "stages"].tolist()
+    gt = z[p + "trace"]
+    assert np.max(np.abs(r.objective_trace - gt) / np.abs(gt)) < tol
+    assert np.max(wrap_distance(r.theta_hat, z[p + "theta_hat"]), initial=0) < THETA_TOL
+    assert rel(r.alpha_hat[0], np.atleast_2d(z[p + "alpha_hat"])[0]) < AMP_TOL
+
+
+@pytest.mark.parametrize("cfg,b", [(1, 0), (1, 3), (2, 0)])
+def test_reference_loop_on_gpu_superfast_bundles(ref_superlse, cfg, b):
+    z = load(cfg)
+    p = f"p{b}_"
+    S = ref_superlse
+    r = S.estimate(S.Observation.complete(z[p + "y"]), S.EstimatorOptions(backend="superfast", grid_factor=4))
+    _compare(r, z, p)
+
+
+@pytest.mark.parametrize("name", ["c1a", "i1b", "i2a"])
+def test_reference_loop_on_gpu_semifast_bundles(ref_superlse, name):
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_sf.npz"))
+    p = name + "_"
+    S = ref_superlse
+    y = z[p + "y"]
+    n = int(z[p + "n"])
+    obs = (S.Observation.complete(y) if p + "idx" not in z.files
+           else S.Observation.incomplete(y, n, z[p + "idx"], z[p + "scales"]))
+    r = S.estimate(obs, S.EstimatorOptions(backend="semifast", grid_factor=4))
+    _compare(r, z, p)
