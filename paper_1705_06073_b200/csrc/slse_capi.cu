@@ -459,6 +459,39 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
     }
     if (e != cudaSuccess) return fail("grid_tma_kernel setup", e);
   }
+  if (L >= 8192 && N >= 64 && !slse_knob("SLSE_GRID_OLD")) {
+    // residue decomposition (slse_grid.cuh): R transforms of M <= 2048 points
+    // per signal, three per task staged in shared memory.  Measured at the
+    // cfg4 / cfg5 shapes (batches > 2x L2): 402 us (13.4 % of HBM) vs 2208 us
+    // for the generic passes through global scratch, 743 vs 4076 us; at
+    // L = 4096 (cfg3) the register-Stockham kernel below stays faster (243 vs 283 us)
+    const int lgM = ilog2(N) < 11 ? ilog2(N) : 11;
+#define SLSE_GRID_RES(NTV, LGMV)                                                                            \
+  case LGMV: {                                                                                              \
+    const size_t smem = 3 * 16 * (size_t)sk_len(1 << LGMV);                                                 \
+    e = set_smem(grid_res_kernel<NTV, LGMV>, smem);                                                         \
+    int occ = 0;                                                                                            \
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_res_kernel<NTV, LGMV>, NTV, smem); \
+    if (e != cudaSuccess || occ < 1) return fail("grid_res_kernel setup", e);                               \
+    long long g = (long long)sm_count() * occ;                                                              \
+    const long long tasks = (long long)B << (ilog2(L) - LGMV);                                              \
+    if (g > tasks) g = tasks;                                                                               \
+    grid_res_kernel<NTV, LGMV><<<(int)g, NTV, smem, st>>>((const cplx*)rho, delta_last, (const cplx*)w, N,   \
+                                                          ilog2(L), B, (cplx*)q_grid, s_grid, tw, twlog);   \
+    e = cudaGetLastError();                                                                                 \
+    return e == cudaSuccess ? 0 : fail("grid_res_kernel", e);                                               \
+  }
+    switch (lgM) {
+      SLSE_GRID_RES(128, 6)
+      SLSE_GRID_RES(128, 7)
+      SLSE_GRID_RES(128, 8)
+      SLSE_GRID_RES(128, 9)
+      SLSE_GRID_RES(192, 10)
+      SLSE_GRID_RES(384, 11)
+      default: break;
+    }
+#undef SLSE_GRID_RES
+  }
   {
     const int lg = ilog2(L);
     int q = 0;

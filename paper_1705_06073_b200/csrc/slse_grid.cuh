@@ -334,4 +334,81 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Residue-decomposed grid for the other large shapes (L >= 2048): with
+// L = R M and l = r + R m,
+//   X[r + R m] = sum_{i<M} z_r(i) W_M^{i m},
+//   z_r(i)     = W_L^{i r} sum_{j : i + j M < n} x_{i + j M} W_R^{j r}
+// (W_L^{j M r} = W_R^{j r}), i.e. R independent M-point transforms of
+// folded, twiddled inputs, M <= 2048 so the three of one residue (w, rho,
+// n rho) stay in shared memory together and run the compile-time Stockham
+// schedule of the cfg1/cfg3 kernels.  One task = (problem, residue); tasks
+// are problem-major, so the R residue tasks that fill one problem's output
+// lines run together and their interleaved writes merge in L2.  Persistent
+// CTAs, one barrier between tasks.
+#ifndef SLSE_GRES_MINB
+#define SLSE_GRES_MINB 2
+#endif
+template <int NT, int LGM>
+__global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res_kernel(
+    const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int lgL,
+    int B, cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* __restrict__ tw, int twlog) {
+  constexpr int M = 1 << LGM;
+  constexpr int MS = M + (M >> 4);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* X = (cplx*)smem_raw;
+  const int L = 1 << lgL;
+  const int lgR = lgL - LGM;
+  const int T = B << lgR;
+  const int J = (n + M - 1) >> LGM;  // folds
+  const double c2n = 2.0 - (double)n;
+  for (int task = blockIdx.x; task < T; task += gridDim.x) {
+    const int r = task & ((1 << lgR) - 1);
+    const int p = task >> lgR;
+    const cplx* wp = w + (size_t)p * n;
+    const cplx* rp = rho + (size_t)p * n;
+    for (int i = threadIdx.x; i < M; i += NT) {
+      cplx z0 = mk(0.0, 0.0), z1 = z0, z2 = z0;
+      for (int j = 0; j < J; ++j) {
+        const int m = i + (j << LGM);
+        if (m >= n) break;
+        const cplx a = wp[m], b = rp[m];
+        const cplx bm = cscale(b, (double)m);
+        if (j == 0 || r == 0) {
+          z0 = cadd(z0, a);
+          z1 = cadd(z1, b);
+          z2 = cadd(z2, bm);
+        } else {
+          const cplx t = tw[tw_index((j * r) & ((1 << lgR) - 1), lgR)];  // W_R^{j r}
+          z0 = cadd(z0, cmul(a, t));
+          z1 = cadd(z1, cmul(b, t));
+          z2 = cadd(z2, cmul(bm, t));
+        }
+      }
+      if (r) {
+        const cplx t = tw[tw_index(i * r, lgL)];  // W_L^{i r}, i r < M R = L
+        z0 = cmul(z0, t);
+        z1 = cmul(z1, t);
+        z2 = cmul(z2, t);
+      }
+      const int si = sk(i);
+      X[si] = z0;
+      X[MS + si] = z1;
+      X[2 * MS + si] = z2;
+    }
+    __syncthreads();
+    fft_fixed_pruned<LGM, 0>(X, 3, -1.0, tw, twlog, threadIdx.x, NT);
+    const double inv_d = 1.0 / delta_last[p];
+    cplx* qg = q_grid + (size_t)p * L + r;
+    double* sg = s_grid + (size_t)p * L + r;
+    for (int k = threadIdx.x; k < M; k += NT) {
+      const int sk_ = sk(k);
+      const cplx a0 = X[MS + sk_], a1 = X[2 * MS + sk_];
+      qg[(size_t)k << lgR] = X[sk_];
+      sg[(size_t)k << lgR] = (c2n * cabs2(a0) + 2.0 * (a1.re * a0.re + a1.im * a0.im)) * inv_d;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace slse_k

@@ -331,7 +331,11 @@ def test_paired_residency_batch(cfg):
 
 
 @pytest.mark.parametrize("n,L,B", [(256, 1024, 300), (200, 1024, 37), (129, 1024, 5), (256, 2048, 7), (64, 256, 9),
-                                   (1000, 4096, 3)])
+                                   (1000, 4096, 3),
+                                   # residue kernel (L >= 8192): M = N (no fold), folded (N > 2048),
+                                   # ragged N, small N with many residues, more tasks than CTAs
+                                   (2048, 8192, 5), (3000, 16384, 4), (4096, 16384, 300), (5000, 32768, 3),
+                                   (16384, 65536, 2), (100, 8192, 3), (2049, 8192, 2)])
 def test_grid_eval_shapes_against_fft(n, L, B):
     """Row 9 on every kernel family (the TMA two-pass kernel serves L = 1024,
     128 < N <= 256, including ragged N and batches that are not a multiple
