@@ -154,10 +154,24 @@ int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem) {
   return 0;
 }
 
+// One problem per 2-CTA cluster (slse_split.cuh) when the superfast batch
+// leaves at least half the SMs idle (cfg5: 64 problems on 148 SMs).
+bool solver_pair(int n, int B, bool dnc) {
+  if (slse_knob("SLSE_NO_CTA_PAIR")) return false;
+  return dnc && solver_threads(n, B, dnc) == 512 && 2 * B <= sm_count();
+}
+
 int grid_size_for_solver(int n, int G, int B, const slse_options& o, size_t* slab_out, SmemPlan* plan_out) {
   SolveParams P = make_params(n, o);
   const bool dnc = P.dnc != 0;
   const int nt = solver_threads(n, B, dnc);
+  if (solver_pair(n, B, dnc)) {  // B clusters, one slab each (+ one job slot, see slse_estimate_batch_mmv)
+    SmemPlan plan = smem_plan(n, P.L, nt, dnc, 0);
+    Layout lay = make_layout(n, P.L, P.kmax, P.lbfgs_mem, false, true, G);
+    *slab_out = lay.total + sizeof(SplitJob);
+    if (plan_out) *plan_out = plan;
+    return B < 1 ? 1 : B;
+  }
   SmemPlan plan = smem_plan(n, P.L, nt, dnc, (nt == 256 && solver_paired(n, B, dnc)) ? kPairRegion : 0);
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {  // one slab per warp of every CTA
@@ -620,6 +634,14 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
   if (e != cudaSuccess) return fail("cudaMemsetAsync", e);
   char* ws = (char*)workspace + 256;
   const int nt = solver_threads(N, B, P.dnc != 0);
+  if (solver_pair(N, B, P.dnc != 0)) {
+    // g clusters; the job slots follow the slabs (slab includes one slot's bytes)
+    const size_t lay_total = slab - sizeof(SplitJob);
+    SplitJob* jobs = (SplitJob*)(ws + (size_t)g * lay_total);
+    e = slse_solve_pair_launch_512(g, plan.bytes, st, P, cft, (const cplx*)y, B, *out, ws, lay_total, queue, tw,
+                                   twlog, plan.fft_cap, jobs);
+    return e == cudaSuccess ? 0 : fail("solve_kernel_pair", e);
+  }
   int wsm = 0;
   if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {
     const size_t smem = kCfBytes + (size_t)W * wsm;

@@ -22,6 +22,7 @@
 //             a cyclic convolution of length F = 2^ceil(log2(s+1)), done
 //             with the block FFT (shared-memory staged when it fits).
 #pragma once
+#include "slse_split.cuh"
 #include "slse_toeplitz.cuh"
 
 namespace slse {
@@ -54,7 +55,98 @@ struct DncCtx {
   int direct_max;     // nodes with s <= direct_max use direct products
   int leaf_max;       // subtrees with s <= leaf_max run as one leaf (dnc_leaf_block above 32)
   long long* prof;    // optional: clock64 per phase (leaf, direct1, direct2, fft1, fft2, total)
+  Split* sp;          // CTA pair (slse_split.cuh): node transforms shared with the helper CTA, or null
 };
+
+// Node transforms of one FFT node site, transforms [qlo, qhi) of the site's
+// batch (dnc_split below; the helper CTA of a pair runs the other half).
+// site 0: forward T11, T12, E, Bw -> S[0..1], SE, SB      (phase 1)
+// site 1: inverse of the E2 / B2 window products           (phase 1)
+// site 2: forward rows of T2 -> A                           (phase 2)
+// site 3: inverse of row 1 of T2 T1 -> T                    (phase 2)
+struct DncFftArgs {
+  int site, F, h, s, l1, l2, ld;
+  double invF;
+  const cplx *T1, *E, *Bw, *T2;
+  cplx *S, *SE, *SB, *E2, *B2, *A, *T, *work;
+};
+SLSE_HD constexpr int dnc_fft_count(int site) { return site == 0 ? 4 : 2; }
+// transforms of at least this size are shared by the two CTAs of a pair
+constexpr int kDncSplitMinF = 1024;
+
+SLSE_D void dnc_fft_site(const DncFftArgs& a, int qlo, int qhi, const FftCtx& f, Blk& b) {
+  const int F = a.F, h = a.h, s = a.s, l1 = a.l1, l2 = a.l2, ld = a.ld;
+  const double invF = a.invF;
+  const int cnt = qhi - qlo;
+  if (cnt <= 0) return;
+  cplx* work = a.work + (size_t)qlo * F;
+  if (a.site == 0) {
+    const cplx *T1 = a.T1, *E = a.E, *Bw = a.Bw;
+    cplx *S = a.S, *SEw = a.SE;
+    fft_multi(work, cnt, F, -1.0,
+              [=](int q, int i) {
+                q += qlo;
+                if (q < 2) return i < l1 ? T1[q * l1 + i] : mk(0.0, 0.0);
+                if (q == 2) return i <= s ? E[i] : mk(0.0, 0.0);
+                return i < s ? Bw[i] : mk(0.0, 0.0);
+              },
+              [=](int q, int i, cplx v) {
+                q += qlo;
+                (q < 2 ? S + (size_t)q * F : SEw + (size_t)(q - 2) * F)[i] = v;
+              },
+              f, b);
+  } else if (a.site == 1) {
+    const cplx *S = a.S, *SE = a.SE, *SB = a.SB;
+    cplx *E2 = a.E2, *B2 = a.B2;
+    fft_multi(work, cnt, F, 1.0,
+              [=](int q, int k) {
+                q += qlo;
+                return q == 0 ? cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k]))
+                              : cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k]));
+              },
+              [=](int q, int i, cplx v) {
+                q += qlo;
+                if (q == 0) {
+                  if (i >= h && i <= s) E2[i - h] = cscale(v, invF);
+                } else if (i >= h && i < s) {
+                  B2[i - h] = cscale(v, invF);
+                }
+              },
+              f, b);
+  } else if (a.site == 2) {
+    const cplx* T2 = a.T2;
+    cplx* A = a.A;
+    fft_multi(work, cnt, F, -1.0, [=](int q, int i) { q += qlo; return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
+              [=](int q, int i, cplx v) { q += qlo; A[(size_t)q * F + i] = v; }, f, b);
+  } else {
+    const cplx *A = a.A, *S = a.S;
+    cplx* T = a.T;
+    // T_rc = A_r1 S_1c + A_r2 S_2c ; output q = 2 r + c
+    fft_multi(work, cnt, F, 1.0,
+              [=](int q, int k) {
+                q += qlo;
+                const int r = q >> 1, c = q & 1;
+                return cadd(cmul(A[(size_t)(2 * r) * F + k], S[(size_t)c * F + k]),
+                            cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
+              },
+              [=](int q, int i, cplx v) { q += qlo; if (i < ld) T[q * ld + i] = cscale(v, invF); }, f, b);
+  }
+}
+
+// All transforms of a site: shared with the helper CTA when the pair is
+// active and the transforms are large enough, else on this CTA alone.
+SLSE_D void dnc_fft_run(DncCtx& X, const DncFftArgs& a, Blk& b) {
+  const int cnt = dnc_fft_count(a.site);
+  if (X.sp && a.F >= kDncSplitMinF) {
+    SplitJob j;
+    j.set(kJobDncFft, a);
+    X.sp->post(j, b);
+    dnc_fft_site(a, 0, cnt / 2, X.f, b);
+    X.sp->done();
+  } else {
+    dnc_fft_site(a, 0, cnt, X.f, b);
+  }
+}
 
 SLSE_D long long dnc_clock() {
 #ifdef SLSE_HOST_EMU
@@ -762,15 +854,13 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       cplx* S = d.S;  // S[0..3] = spectra of T1, S[4] = E, S[5] = Bw (contiguous: S, SE, SB)
       // four forward transforms in one batch (T11, T12, E, Bw); the spectra
       // of T21 = T12^#, T22 = T11^# (degree h) follow as W^{h k} conj(.)
-      const cplx* SEw = d.SE;
-      fft_multi(d.work_multi, 4, F, -1.0,
-                [=](int q, int i) {
-                  if (q < 2) return i < l1 ? T1[q * l1 + i] : mk(0.0, 0.0);
-                  if (q == 2) return i <= s ? E[i] : mk(0.0, 0.0);
-                  return i < s ? Bw[i] : mk(0.0, 0.0);
-                },
-                [=](int q, int i, cplx v) { (q < 2 ? S + (size_t)q * F : (cplx*)SEw + (size_t)(q - 2) * F)[i] = v; },
-                X.f, b);
+      DncFftArgs fa{};
+      fa.F = F; fa.h = h; fa.s = s; fa.l1 = l1; fa.invF = invF;
+      fa.T1 = T1; fa.E = E; fa.Bw = Bw;
+      fa.S = S; fa.SE = d.SE; fa.SB = d.SB; fa.E2 = d.E2; fa.B2 = d.B2;
+      fa.work = d.work_multi;
+      fa.site = 0;
+      dnc_fft_run(X, fa, b);
       {
         const int lgF = ilog2(F);
         for (int k = b.tid; k < F; k += b.nt) {
@@ -780,24 +870,9 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
         }
         fft_barrier();
       }
-      const cplx* SE = d.SE;
-      const cplx* SB = d.SB;
-      cplx* E2 = d.E2;
-      cplx* B2 = d.B2;
       // E2 = (T11 E + T12 Bw)[h..s], B2 = (T21 E + T22 Bw)[h..s-1]
-      fft_multi(d.work_multi, 2, F, 1.0,
-                [=](int q, int k) {
-                  return q == 0 ? cadd(cmul(S[k], SE[k]), cmul(S[F + k], SB[k]))
-                                : cadd(cmul(S[2 * F + k], SE[k]), cmul(S[3 * F + k], SB[k]));
-                },
-                [=](int q, int i, cplx v) {
-                  if (q == 0) {
-                    if (i >= h && i <= s) E2[i - h] = cscale(v, invF);
-                  } else if (i >= h && i < s) {
-                    B2[i - h] = cscale(v, invF);
-                  }
-                },
-                X.f, b);
+      fa.site = 1;
+      dnc_fft_run(X, fa, b);
       if (prof) {
         const long long dt = dnc_clock() - t0;
         X.prof[3] += dt;
@@ -816,20 +891,15 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       cplx* wk = d.above + 4 * (size_t)F;  // 4 F global work
       // only row 1 of the product is transformed (2 + 2 transforms instead
       // of 4 + 4); row 2 follows by symmetry, skipped on the right spine
-      const int nq = 2;  // row 1 of T2 and of the product; row 2 by dnc_fill_row2
-      fft_multi(wk, nq, F, -1.0, [=](int q, int i) { return i < l2 ? T2[q * l2 + i] : mk(0.0, 0.0); },
-                [=](int q, int i, cplx v) { A[(size_t)q * F + i] = v; }, X.f, b);
-      const cplx* S = d.S;
+      // (row 1 of T2 and of the product; row 2 by dnc_fill_row2)
       cplx* T = cf.T;
-      const int ld = s + 1;
-      // T_rc = A_r1 S_1c + A_r2 S_2c ; output q = 2 r + c
-      fft_multi(wk, nq, F, 1.0,
-                [=](int q, int k) {
-                  const int r = q >> 1, c = q & 1;
-                  return cadd(cmul(A[(size_t)(2 * r) * F + k], S[(size_t)c * F + k]),
-                              cmul(A[(size_t)(2 * r + 1) * F + k], S[(size_t)(2 + c) * F + k]));
-                },
-                [=](int q, int i, cplx v) { if (i < ld) T[q * ld + i] = cscale(v, invF); }, X.f, b);
+      DncFftArgs fa{};
+      fa.F = F; fa.h = h; fa.s = s; fa.l2 = l2; fa.ld = s + 1; fa.invF = invF;
+      fa.T2 = T2; fa.A = A; fa.S = d.S; fa.T = T; fa.work = wk;
+      fa.site = 2;
+      dnc_fft_run(X, fa, b);
+      fa.site = 3;
+      dnc_fft_run(X, fa, b);
       if (!cf.row1) dnc_fill_row2(T, s, b);
       if (prof) {
         const long long dt = dnc_clock() - t0;
@@ -866,7 +936,7 @@ SLSE_HD size_t dnc_arena_elems(int s) {
 SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, cplx* arena, double* delta_out,
                                    double* delta_tmp, cplx* SLSE_RESTRICT rho, const FftCtx& f, Blk& b,
                                    int dnc_stockham = 0, int direct_max = SLSE_DNC_DIRECT,
-                                   long long* prof = nullptr) {
+                                   long long* prof = nullptr, Split* sp = nullptr) {
   Factor F;
   F.logdet = 0.0;
   F.status = kOk;
@@ -903,6 +973,7 @@ SLSE_NI Factor toeplitz_factor_dnc(const cplx* SLSE_RESTRICT c, int n, cplx* T, 
   }
 #endif
   X.prof = prof;
+  X.sp = sp;
   b.sync();
   // the root window is the column itself: e = b = c (c_0 forced real)
   // (E[0] and Bw[0] are c_0; E[j] = Bw[j] = c_j)

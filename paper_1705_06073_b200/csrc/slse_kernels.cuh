@@ -168,6 +168,67 @@ __global__ void __launch_bounds__(NT, (NT <= 32 ? SLSE_SOLVER_MINB32 : SLSE_SOLV
   }
 }
 
+// One problem per 2-CTA cluster (slse_split.cuh): rank 0 runs the solver
+// (problems from the atomic queue), rank 1 executes the jobs rank 0 posts
+// until it posts kJobQuit.  Launched with cluster dimension 2.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) solve_kernel_pair(SolveParams P, CfTable cft, const cplx* __restrict__ ys,
+                                                            int B, slse_outputs out, char* ws, size_t slab_bytes,
+                                                            int* queue, const cplx* tw, int twlog, int fft_cap,
+                                                            SplitJob* jobs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* red = (double*)smem_raw;
+  CfTable* cf = (CfTable*)(smem_raw + red_bytes(NT));
+  cplx* region = (cplx*)(smem_raw + head_bytes(NT));
+  __shared__ int s_prob;
+  if (threadIdx.x == 0) *cf = cft;
+  Blk b;
+  b.tid = threadIdx.x;
+  b.nt = NT;
+  b.red = red;
+  b.bank = 0;
+  FftCtx f;
+  f.tw = tw;
+  f.twlog = twlog;
+  f.smem = region;
+  f.smem_cap = fft_cap;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int cid = blockIdx.x >> 1;
+  Split sp;
+  sp.job = jobs + cid;
+  sp.rank = (int)rank;
+  __syncthreads();
+  if (rank != 0) {  // helper
+    for (;;) {
+      cluster_sync_all();  // rank 0 posted a job
+      const SplitJob j = *sp.job;  // visible: the barrier acquired it
+      if (j.kind == kJobQuit) break;
+      run_split_job(j, 1, cf, f, b);
+      cluster_sync_all();  // both halves done
+    }
+    return;
+  }
+  char* slab = ws + (size_t)cid * slab_bytes;
+  const Layout lay = make_layout(P.n, P.L, P.kmax, P.lbfgs_mem, false, P.dnc != 0, P.g);
+  for (;;) {
+    if (threadIdx.x == 0) s_prob = atomicAdd(queue, 1);
+    __syncthreads();
+    const int p = s_prob;
+    __syncthreads();
+    if (p >= B) break;
+    const ProbOut o = prob_out(out, P, p);
+    Solver S(b, P, cf, ys + (size_t)p * P.n * P.g, o, slab, lay, nullptr, f);
+    S.sp = &sp;
+    S.run();
+    b.bank = S.b.bank;
+    __syncthreads();
+  }
+  SplitJob q;
+  q.kind = kJobQuit;
+  sp.post(q, b);
+}
+
 #ifdef SLSE_WARP_MODE
 // W independent one-warp solvers per CTA (one CTA per SM), meeting at a
 // CTA-wide rendezvous for every heavy operation (Solver::build / stats /
@@ -751,6 +812,12 @@ cudaError_t slse_sf_bundle_launch(size_t smem, cudaStream_t st, const slse::Solv
                                   double* data_term, slse::cplx* e, slse::cplx* q, slse::cplx* r, slse::cplx* u,
                                   double* s, slse::cplx* t, slse::cplx* v, double* x, slse::cplx* q_grid,
                                   double* s_grid, int* status);
+
+// CTA-pair solver (slse_solve_inst.cu): one problem per 2-CTA cluster
+cudaError_t slse_solve_pair_launch_512(int clusters, size_t smem, cudaStream_t st, const slse::SolveParams& P,
+                                       const slse::CfTable& cft, const slse::cplx* ys, int B,
+                                       const slse_outputs& out, char* ws, size_t slab, int* queue,
+                                       const slse::cplx* tw, int twlog, int fft_cap, slse::SplitJob* jobs);
 
 // warp-mode solver (slse_solve_warps.cu): W one-warp solvers per CTA
 cudaError_t slse_solve_warps_launch(int W, int ctas, size_t smem, cudaStream_t st, const slse::SolveParams& P,

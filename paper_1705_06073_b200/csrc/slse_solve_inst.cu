@@ -28,6 +28,31 @@ cudaError_t SLSE_CAT(slse_solve_launch_, SLSE_NT)(int grid, size_t smem, cudaStr
   return cudaGetLastError();
 }
 
+#if SLSE_NT == 512
+// one problem per 2-CTA cluster (slse_split.cuh)
+cudaError_t slse_solve_pair_launch_512(int clusters, size_t smem, cudaStream_t st, const slse::SolveParams& P,
+                                       const slse::CfTable& cft, const slse::cplx* ys, int B,
+                                       const slse_outputs& out, char* ws, size_t slab, int* queue,
+                                       const slse::cplx* tw, int twlog, int fft_cap, slse::SplitJob* jobs) {
+  auto kern = slse_k::solve_kernel_pair<512>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters, 1, 1);
+  cfg.blockDim = dim3(512, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, P, cft, ys, B, out, ws, slab, queue, tw, twlog, fft_cap, jobs);
+}
+#endif
+
 #ifdef SLSE_SOLVER_PROF
 // Read (and optionally reset) the solver phase-cycle accumulators of this
 // instantiation (see slse_solver.cuh, SLSE_SOLVER_PROF).

@@ -343,6 +343,41 @@ SLSE_D unsigned long long now_ns() {
 #endif
 }
 
+// ---- CTA-pair jobs (slse_split.cuh) ----
+struct SteerArgs {
+  cplx* out;
+  const double *th, *cre, *cim;
+  int n, k, column;
+  double beta0;
+};
+struct StatsArgs {
+  const double* th;
+  const cplx *rho, *w;
+  cplx *q, *r, *u, *t, *v;
+  double *s, *x;
+  int K, n;
+  double delta_last;
+};
+
+// One half (rank) of a job: the same device function as the single-CTA
+// path, on this CTA's share of the work.
+SLSE_D void run_split_job(const SplitJob& j, int rank, const CfTable* cf, const FftCtx& f, Blk& b) {
+  if (j.kind == kJobSteer) {
+    const SteerArgs a = j.get<SteerArgs>();
+    steer_forward(a.out, a.n, a.th, a.cre, a.cim, a.k, a.beta0, a.column != 0, b, rank, 2);
+  } else if (j.kind == kJobStats) {
+    const StatsArgs a = j.get<StatsArgs>();
+    Blk v = b;
+    v.tid = b.tid + rank * b.nt;  // one warp per frequency: warps of both CTAs
+    v.nt = 2 * b.nt;
+    component_stats(a.th, a.K, a.rho, a.w, a.n, a.delta_last, cf, a.q, a.r, a.u, a.s, a.t, a.v, a.x, v);
+  } else if (j.kind == kJobDncFft) {
+    const DncFftArgs a = j.get<DncFftArgs>();
+    const int cnt = dnc_fft_count(a.site);
+    dnc_fft_site(a, rank ? cnt / 2 : 0, rank ? cnt : cnt / 2, f, b);
+  }
+}
+
 struct Bundle {
   cplx* rho;
   cplx* w;  // C^{-1} y (superfast); e = Phi^H C^{-1} y (semifast), G rows of n
@@ -376,6 +411,7 @@ struct Solver {
   int cur_valid;
   // scalar state (identical in every thread)
   int n, L, kmax, k;
+  Split* sp = nullptr;  // CTA pair (solve_kernel_pair): data-parallel jobs shared with the helper CTA
   int m;  // observed samples per snapshot (P.m): y holds G rows of m
   SfObs obs;
   cplx *sfE, *sfX, *sfAhy, *sfBb;
@@ -510,6 +546,21 @@ struct Solver {
     if (nevents < P.ecap) ++nevents; else flags |= kFlEventsFull;
   }
 
+  // steer_forward on this CTA, or split with the helper CTA of a pair
+  SLSE_NIM void steer(cplx* out, const double* th, const double* cre, const double* cim, int kk, double be,
+                      bool column) {
+    if (sp) {
+      SteerArgs a{out, th, cre, cim, n, kk, column ? 1 : 0, be};
+      SplitJob j;
+      j.set(kJobSteer, a);
+      sp->post(j, b);
+      steer_forward(out, n, th, cre, cim, kk, be, column, b, 0, 2);
+      sp->done();
+    } else {
+      steer_forward(out, n, th, cre, cim, kk, be, column, b);
+    }
+  }
+
   // ---- model evaluation ----
   // Bundle for (th[0..kk), ga[0..kk), beta): model_core.py:257-274
   // Warp mode (several one-warp solvers per CTA, SLSE_WARP_MODE): every heavy
@@ -548,10 +599,11 @@ struct Solver {
     if (b.nt == 32 && n <= 512) steer_forward_warp(c, n, th, ga, nullptr, kk, be, true, b.tid);
     else
 #endif
-      steer_forward(c, n, th, ga, nullptr, kk, be, true, b);
+      steer(c, th, ga, nullptr, kk, be, true);
     SLSE_PROF_ADD(0, t0);
     SLSE_PROF_T0(t1);
-    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham, P.dnc_direct)
+    Factor F = P.dnc ? toeplitz_factor_dnc(c, n, dT, darena, nullptr, dtmp, B.rho, f, b, P.dnc_stockham, P.dnc_direct,
+                                           nullptr, sp)
                      : toeplitz_factor(c, n, e, bg, a, nullptr, dtmp, B.rho, b);
     SLSE_PROF_ADD(1, t1);
     if (F.status != kOk) return F.status;
@@ -624,7 +676,18 @@ struct Solver {
         component_stats_warp(th, kk, B.rho, wg, n, B.delta_last, cf, qg, rg, ug, B.s, B.t, B.v, B.x, b.tid);
       else
 #endif
-        component_stats(th, kk, B.rho, wg, n, B.delta_last, cf, qg, rg, ug, B.s, B.t, B.v, B.x, b);
+      {
+        if (sp) {
+          StatsArgs a{th, B.rho, wg, qg, rg, ug, B.t, B.v, B.s, B.x, kk, n, B.delta_last};
+          SplitJob j;
+          j.set(kJobStats, a);
+          sp->post(j, b);
+          run_split_job(j, 0, cf, f, b);
+          sp->done();
+        } else {
+          component_stats(th, kk, B.rho, wg, n, B.delta_last, cf, qg, rg, ug, B.s, B.t, B.v, B.x, b);
+        }
+      }
     }
     SLSE_PROF_ADD(3, t0);
     B.stats_valid = 1;
@@ -1577,7 +1640,7 @@ struct Solver {
       if (b.nt == 32 && n <= 512) steer_forward_warp(c, n, act_theta, mre, mim, k, 0.0, false, b.tid);
       else
 #endif
-        steer_forward(c, n, act_theta, mre, mim, k, 0.0, false, b);
+        steer(c, act_theta, mre, mim, k, 0.0, false);
       const cplx* yg = y + (size_t)g * m;
 #ifdef SLSE_SEMIFAST
       // y - Phi Psi mu over the observed samples (estimator.py:86-87, Observation.sample)

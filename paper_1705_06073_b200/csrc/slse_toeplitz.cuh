@@ -27,11 +27,13 @@ enum Status : int {
 // column=true: covariance-column convention, c_0 <- Re(c_0) + beta0.
 SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RESTRICT thetas,
                           const double* SLSE_RESTRICT coef_re, const double* SLSE_RESTRICT coef_im,
-                          int k, double beta0, bool column, Blk& b) {
+                          int k, double beta0, bool column, Blk& b, int chunk0 = 0, int chunks = 1) {
   const int tid_ = b.tid, nt_ = b.nt;
   // accumulate in registers chunk-wise: each thread handles up to 16 owned m
-  // values per sweep over k.
-  for (int m0 = tid_; m0 < n; m0 += 16 * nt_) {
+  // values per sweep over k.  (chunk0, chunks): this block computes chunks
+  // chunk0, chunk0 + chunks, ... of 16 nt outputs (a CTA pair splits the
+  // chunks; every output's arithmetic is the same either way)
+  for (int m0 = tid_ + chunk0 * 16 * nt_; m0 < n; m0 += chunks * 16 * nt_) {
     const int J = (n - m0 + nt_ - 1) / nt_;  // owned values in this chunk (<= 16 used)
     cplx acc[16];
 #pragma unroll
