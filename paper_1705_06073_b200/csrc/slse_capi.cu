@@ -120,6 +120,8 @@ namespace {
 // measured on B200 (tools/occ_exp.sh) cfg3 181 -> 130 ms, cfg4 1.00 -> 0.82 s;
 // with B <= SMs (cfg5) one 512-thread CTA per problem stays faster.
 constexpr size_t kPairRegion = 100 * 1024;
+constexpr int kWideMaxPerSM = 5;       // N <= 512: 128-thread CTA per problem up to 5 problems per SM
+constexpr int kWarpModeMinPerSM = 10;  // N <= 512: warp mode from 10 problems per SM
 bool solver_paired(int n, int B, bool dnc) {
   if (slse_knob("SLSE_NO_PAIR")) return false;
   if (n <= 512 || B <= sm_count()) return false;
@@ -132,7 +134,13 @@ int solver_threads(int n, int B, bool dnc) {
     int v = atoi(env);
     if (v == 32 || v == 64 || v == 128 || v == 256 || v == 512 || v == 1024) return v;
   }
-  if (n <= 512) return 32;    // cfg1-2: measured 68 ms (32) vs 113 ms (256) per 4096 x N=256 batch
+  // N <= 512: by batch size (measured, N = 256, tools/small_batch.sh): up to
+  // 5 problems per SM one 128-thread CTA per problem is fastest (B = 148:
+  // 4.4 ms vs 14.3 ms in warp mode, which packs 16 problems on 10 SMs);
+  // one-warp CTAs (classic, several per SM) up to 10 per SM; warp mode
+  // (16 one-warp solvers per CTA, operation windows) from there (B = 4096:
+  // 30.9 ms vs 68 ms classic)
+  if (n <= 512) return B <= kWideMaxPerSM * sm_count() ? 128 : 32;
   if (solver_paired(n, B, dnc)) return 256;
   if (n <= 2048) return 256;  // cfg3: 167 ms (256) vs 205 (128) / 236 (512) per 1024 x N=1024
   return 512;                 // cfg4/5 with B <= SMs (superfast): 8.8 s (512) vs 13.1 (1024) / 12 (128) at cfg5
@@ -142,8 +150,9 @@ int solver_threads(int n, int B, bool dnc) {
 // CTA-wide rendezvous per heavy operation (slse_solve_warps.cu).  Returns
 // W (16, 8 or 4 -- as many as the per-warp shared memory allows), or 0 when
 // the classic one-problem-per-CTA kernel is used (nt > 32, SLSE_NO_WARPS).
-int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem) {
+int warps_per_cta(int nt, bool dnc, const SmemPlan& plan, int* warp_smem, int B) {
   if (nt != 32 || dnc || slse_knob("SLSE_NO_WARPS")) return 0;  // (the superfast factor keeps CTA-static scratch)
+  if (B < kWarpModeMinPerSM * sm_count()) return 0;  // classic one-warp CTAs (see solver_threads)
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -174,7 +183,7 @@ int grid_size_for_solver(int n, int G, int B, const slse_options& o, size_t* sla
   }
   SmemPlan plan = smem_plan(n, P.L, nt, dnc, (nt == 256 && solver_paired(n, B, dnc)) ? kPairRegion : 0);
   int wsm = 0;
-  if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {  // one slab per warp of every CTA
+  if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm, B)) {  // one slab per warp of every CTA
     int ctas = (B + W - 1) / W;
     if (ctas > sm_count()) ctas = sm_count();
     if (ctas < 1) ctas = 1;
@@ -643,7 +652,7 @@ int slse_estimate_batch_mmv(const double* y, int N, int G, int B, const slse_opt
     return e == cudaSuccess ? 0 : fail("solve_kernel_pair", e);
   }
   int wsm = 0;
-  if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm)) {
+  if (const int W = warps_per_cta(nt, P.dnc != 0, plan, &wsm, B)) {
     const size_t smem = kCfBytes + (size_t)W * wsm;
     e = slse_solve_warps_launch(W, g / W, smem, st, P, cft, (const cplx*)y, B, *out, ws, slab, queue, tw, twlog,
                                 plan.fft_cap, plan.rec_in_smem, wsm);
