@@ -137,7 +137,7 @@ SLSE_D void dnc_fft_site(const DncFftArgs& a, int qlo, int qhi, const FftCtx& f,
 // active and the transforms are large enough, else on this CTA alone.
 SLSE_D void dnc_fft_run(DncCtx& X, const DncFftArgs& a, Blk& b) {
   const int cnt = dnc_fft_count(a.site);
-  if (X.sp && a.F >= kDncSplitMinF) {
+  if (SLSE_PAIR && X.sp && a.F >= kDncSplitMinF) {
     SplitJob j;
     j.set(kJobDncFft, a);
     X.sp->post(j, b);

@@ -385,6 +385,7 @@ struct Bundle {
   double *s, *x;
   double data_term, delta_last, logdet;
   int stats_valid;
+#ifdef SLSE_SEMIFAST
   // semifast (model_core.py:316-409): Gram matrices, Cholesky factor of
   // Sigma^{-1} (strict lower part + real diagonal sLd), positive list sP
   cplx *sG0, *sG1, *sG2, *sL;
@@ -392,6 +393,7 @@ struct Bundle {
   int* sP;
   int kp;
   double sbeta;
+#endif
 };
 
 struct Solver {
@@ -413,9 +415,11 @@ struct Solver {
   int n, L, kmax, k;
   Split* sp = nullptr;  // CTA pair (solve_kernel_pair): data-parallel jobs shared with the helper CTA
   int m;  // observed samples per snapshot (P.m): y holds G rows of m
+#ifdef SLSE_SEMIFAST
   SfObs obs;
   cplx *sfE, *sfX, *sfAhy, *sfBb;
   int kcap;
+#endif
   int G;  // snapshots (P.g): y, yhat and w hold G rows of n / nf; q, r, u, mu G rows of kmax
   double beta, zeta, energy, floor_beta;
   int status;
@@ -437,12 +441,14 @@ struct Solver {
       : b(blk), f(fc), P(p), cf(cf_), y(y_), o(out) {
     n = p.n; L = p.L; kmax = p.kmax; G = p.g;
     m = p.m;
+#ifdef SLSE_SEMIFAST
     kcap = p.kcap;
     obs.idx = nullptr;
     obs.sc = nullptr;
     obs.m = m;
     sfE = (cplx*)(slab + lay.sfE); sfX = (cplx*)(slab + lay.sfX);
     sfAhy = (cplx*)(slab + lay.sfAhy); sfBb = (cplx*)(slab + lay.sfBb);
+#endif
     yhat = (cplx*)(slab + lay.yhat);
     c = (cplx*)(slab + lay.c);
     if (rec_smem) {
@@ -464,6 +470,7 @@ struct Solver {
       bun[i].x = (double*)(slab + lay.st_x[i]);
       bun[i].stats_valid = 0;
       bun[i].data_term = bun[i].delta_last = bun[i].logdet = 0.0;
+#ifdef SLSE_SEMIFAST
       bun[i].sG0 = (cplx*)(slab + lay.sfG0[i]);
       bun[i].sG1 = (cplx*)(slab + lay.sfG1[i]);
       bun[i].sG2 = (cplx*)(slab + lay.sfG2[i]);
@@ -472,6 +479,7 @@ struct Solver {
       bun[i].sP = (int*)(slab + lay.sfP[i]);
       bun[i].kp = 0;
       bun[i].sbeta = 0.0;
+#endif
     }
     PP = (cplx*)(slab + lay.P); U = (cplx*)(slab + lay.U); V = (cplx*)(slab + lay.V);
     G0 = (cplx*)(slab + lay.G0); G1 = (cplx*)(slab + lay.G1); G2 = (cplx*)(slab + lay.G2);
@@ -547,9 +555,9 @@ struct Solver {
   }
 
   // steer_forward on this CTA, or split with the helper CTA of a pair
-  SLSE_NIM void steer(cplx* out, const double* th, const double* cre, const double* cim, int kk, double be,
+  SLSE_D void steer(cplx* out, const double* th, const double* cre, const double* cim, int kk, double be,
                       bool column) {
-    if (sp) {
+    if (SLSE_PAIR && sp) {
       SteerArgs a{out, th, cre, cim, n, kk, column ? 1 : 0, be};
       SplitJob j;
       j.set(kJobSteer, a);
@@ -677,7 +685,7 @@ struct Solver {
       else
 #endif
       {
-        if (sp) {
+        if (SLSE_PAIR && sp) {
           StatsArgs a{th, B.rho, wg, qg, rg, ug, B.t, B.v, B.s, B.x, kk, n, B.delta_last};
           SplitJob j;
           j.set(kJobStats, a);

@@ -28,6 +28,14 @@
 
 namespace slse {
 
+// The pair kernel exists only in the 512-thread solver unit; every other
+// instantiation compiles the split branches away.
+#if defined(SLSE_NT) && SLSE_NT == 512 && !defined(SLSE_HOST_EMU)
+#define SLSE_PAIR 1
+#else
+#define SLSE_PAIR 0
+#endif
+
 enum SplitKind : int { kJobQuit = 0, kJobSteer = 1, kJobStats = 2, kJobDncFft = 3 };
 
 struct SplitJob {
