@@ -359,6 +359,13 @@ struct StatsArgs {
   double delta_last;
 };
 
+struct GridArgs {
+  const cplx *rho, *w;
+  double *dl, *q2, *sg;
+  int n, L;
+  double delta_last, gb, lr;
+};
+
 // One half (rank) of a job: the same device function as the single-CTA
 // path, on this CTA's share of the work.
 SLSE_D void run_split_job(const SplitJob& j, int rank, const CfTable* cf, const FftCtx& f, Blk& b) {
@@ -371,6 +378,9 @@ SLSE_D void run_split_job(const SplitJob& j, int rank, const CfTable* cf, const 
     v.tid = b.tid + rank * b.nt;  // one warp per frequency: warps of both CTAs
     v.nt = 2 * b.nt;
     component_stats(a.th, a.K, a.rho, a.w, a.n, a.delta_last, cf, a.q, a.r, a.u, a.s, a.t, a.v, a.x, v);
+  } else if (j.kind == kJobGrid) {
+    const GridArgs a = j.get<GridArgs>();
+    grid_gain_fused(a.rho, a.w, a.n, a.delta_last, a.L, a.gb, a.lr, a.dl, a.q2, a.sg, f, b, rank, 2);
   } else if (j.kind == kJobDncFft) {
     const DncFftArgs a = j.get<DncFftArgs>();
     const int cnt = dnc_fft_count(a.site);
@@ -1008,7 +1018,18 @@ struct Solver {
     return;
 #endif
     SLSE_PROF_T0(t0);
-    if (G == 1 && P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) {
+    if (SLSE_PAIR && sp && G == 1 && P.grid_fused) {
+      GridArgs a{B.rho, B.w, dl, q2, sg, n, L, B.delta_last, gb, lr};
+      SplitJob j;
+      j.set(kJobGrid, a);
+      sp->post(j, b);
+      const bool ok = grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b, 0, 2);
+      sp->done();
+      if (ok) {
+        SLSE_PROF_ADD(4, t0);
+        return;
+      }
+    } else if (G == 1 && P.grid_fused && grid_gain_fused(B.rho, B.w, n, B.delta_last, L, gb, lr, dl, q2, sg, f, b)) {
       SLSE_PROF_ADD(4, t0);
       return;
     }

@@ -9,7 +9,8 @@
 //   * the covariance column / Psi mu steering sums (steer_forward),
 //   * the component statistics (component_stats, one warp per frequency),
 //   * the superfast factor's batched node transforms (dnc_split: the 4 / 2
-//     transforms of an FFT node are shared between the two CTAs).
+//     transforms of an FFT node are shared between the two CTAs),
+//   * the activation grid's residue batches (grid_gain_fused: even / odd r).
 // Every job is the same device function on this CTA's share of the work
 // (alternate output chunks, alternate frequencies, half of a node's
 // transforms), so each output is computed by the same source arithmetic as
@@ -36,7 +37,7 @@ namespace slse {
 #define SLSE_PAIR 0
 #endif
 
-enum SplitKind : int { kJobQuit = 0, kJobSteer = 1, kJobStats = 2, kJobDncFft = 3 };
+enum SplitKind : int { kJobQuit = 0, kJobSteer = 1, kJobStats = 2, kJobDncFft = 3, kJobGrid = 4 };
 
 struct SplitJob {
   int kind;

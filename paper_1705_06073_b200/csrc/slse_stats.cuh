@@ -285,12 +285,15 @@ SLSE_NI void grid_eval(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT 
 // length-M transforms -- no work on the zero tail, each batch staged in
 // shared memory (needs 3 M <= f.smem_cap) -- and every output is combined
 // straight into s^G, |q^G|^2 and the gain curve (no L-sized complex
-// buffers).  Returns false when the staging does not fit (caller falls
-// back to grid_eval).
+// buffers).  When 3 M does not fit the staging (large N) M is capped and the
+// input folded: X[m R + r] = sum_{i<M} (sum_j x_{i+jM} W_L^{(i+jM) r}) W_M^{i m}.
+// Residues r0, r0 + rstep, ... only (a CTA pair splits them).  Returns false
+// when not even a 64-point batch fits (caller falls back to grid_eval).
 SLSE_NI bool grid_gain_fused(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RESTRICT w, int n, double delta_last,
                              int L, double gb, double log_ratio, double* dl, double* q2, double* sg,
-                             const FftCtx& f, Blk& b) {
-  const int M = 1 << ilog2(n);
+                             const FftCtx& f, Blk& b, int r0 = 0, int rstep = 1) {
+  int M = 1 << ilog2(n);
+  while (M > 64 && 3 * M > f.smem_cap) M >>= 1;
   if (3 * M > f.smem_cap || M > L) return false;
   const int tid = b.tid, nt = b.nt;
   const int R = L / M;
@@ -306,16 +309,16 @@ SLSE_NI bool grid_gain_fused(const cplx* SLSE_RESTRICT rho, const cplx* SLSE_RES
 #else
   const auto gz = [](int i) { return i; };
 #endif
-  for (int r = 0; r < R; ++r) {
+  for (int r = r0; r < R; r += rstep) {
     for (int t = tid; t < 3 * M; t += nt) {
-      const int c = t >> p, i = t & (M - 1);
+      const int c = t >> p, i0 = t & (M - 1);
       cplx v = mk(0.0, 0.0);
-      if (i < n) {
+      for (int i = i0; i < n; i += M) {  // one term unless the input is folded
         const cplx tw = twid_tab(f.tw, f.twlog, (int)(((long long)i * r) & (L - 1)), lgL, -1.0);
         const cplx src = c == 0 ? w[i] : (c == 1 ? rho[i] : cscale(rho[i], (double)i));
-        v = r ? cmul(src, tw) : src;
+        v = cadd(v, r ? cmul(src, tw) : src);
       }
-      x[(size_t)c * M + gz(brev_bits((unsigned)i, p))] = v;
+      x[(size_t)c * M + gz(brev_bits((unsigned)i0, p))] = v;
     }
     fft_barrier();
 #ifndef SLSE_HOST_EMU
