@@ -378,6 +378,9 @@ SLSE_D void run_split_job(const SplitJob& j, int rank, const CfTable* cf, const 
     v.tid = b.tid + rank * b.nt;  // one warp per frequency: warps of both CTAs
     v.nt = 2 * b.nt;
     component_stats(a.th, a.K, a.rho, a.w, a.n, a.delta_last, cf, a.q, a.r, a.u, a.s, a.t, a.v, a.x, v);
+  } else if (j.kind == kJobGsChain) {
+    const GsChainArgs a = j.get<GsChainArgs>();
+    gs_chain((cplx*)a.Y, a.n, a.nf, f, b);
   } else if (j.kind == kJobGrid) {
     const GridArgs a = j.get<GridArgs>();
     grid_gain_fused(a.rho, a.w, a.n, a.delta_last, a.L, a.gb, a.lr, a.dl, a.q2, a.sg, f, b, rank, 2);
@@ -629,10 +632,10 @@ struct Solver {
     B.logdet = F.logdet;
     SLSE_PROF_T0(t2);
     const int nf = 1 << ilog2(2 * n);
-    double quad = gs_apply_any(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b);
+    double quad = gs_apply_any(B.rho, n, F.delta_last, y, yhat, PP, U, V, B.w, f, b, sp);
     for (int g = 1; g < G; ++g)  // MMV: one C^{-1} y_g per snapshot (model_core.py:267-269)
       quad += gs_apply_any(B.rho, n, F.delta_last, y + (size_t)g * n, yhat + (size_t)g * nf, PP, U, V,
-                           B.w + (size_t)g * n, f, b);
+                           B.w + (size_t)g * n, f, b, sp);
     SLSE_PROF_ADD(2, t2);
     B.data_term = (G == 1 ? F.logdet : (double)G * F.logdet) + quad;
     B.stats_valid = 0;

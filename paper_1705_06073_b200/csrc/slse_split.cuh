@@ -10,7 +10,8 @@
 //   * the component statistics (component_stats, one warp per frequency),
 //   * the superfast factor's batched node transforms (dnc_split: the 4 / 2
 //     transforms of an FFT node are shared between the two CTAs),
-//   * the activation grid's residue batches (grid_gain_fused: even / odd r).
+//   * the activation grid's residue batches (grid_gain_fused: even / odd r),
+//   * the GS apply's two independent transform chains (gs_chain on U / V).
 // Every job is the same device function on this CTA's share of the work
 // (alternate output chunks, alternate frequencies, half of a node's
 // transforms), so each output is computed by the same source arithmetic as
@@ -37,7 +38,7 @@ namespace slse {
 #define SLSE_PAIR 0
 #endif
 
-enum SplitKind : int { kJobQuit = 0, kJobSteer = 1, kJobStats = 2, kJobDncFft = 3, kJobGrid = 4 };
+enum SplitKind : int { kJobQuit = 0, kJobSteer = 1, kJobStats = 2, kJobDncFft = 3, kJobGrid = 4, kJobGsChain = 5 };
 
 struct SplitJob {
   int kind;
@@ -62,6 +63,11 @@ SLSE_D void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 #endif
 }
+
+struct GsChainArgs {
+  void* Y;
+  int n, nf;
+};
 
 struct Split {
   SplitJob* job;  // this cluster's descriptor slot (global memory)

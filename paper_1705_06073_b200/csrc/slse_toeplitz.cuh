@@ -6,6 +6,7 @@
 // log_det :312-314); model_core.py:242-249, 256-274.
 #pragma once
 #include "slse_fft.cuh"
+#include "slse_split.cuh"
 
 namespace slse {
 
@@ -876,9 +877,27 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
 //   P0h_k = FFT(conj(rev v0))_k = W^{(N-1)k} conj(P0_k).
 // Xhat = FFT_nf(x) is cached by the caller (x = y is fixed per problem).
 // Buffers P, U, V: nf complex each (global).
+// One of GS apply's two independent chains: Y <- FFT(shift_{N-1}(IFFT(Y)) / nf)
+// (U and V below; a CTA pair runs one each, slse_split.cuh).
+SLSE_NI void gs_chain(cplx* Y, int n, int nf, const FftCtx& f, Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
+  const double inv = 1.0 / (double)nf;
+  fft_inplace(Y, nf, 1.0, f, b);
+  // shift down by N-1 through registers (barrier between read and write)
+  for (int i0 = 0; i0 < nf; i0 += nt_) {
+    const int i = i0 + tid_;
+    cplx u = mk(0.0, 0.0);
+    if (i < n) u = cscale(Y[n - 1 + i], inv);
+    b.sync();
+    if (i < nf) Y[i] = u;
+    b.sync();
+  }
+  fft_inplace(Y, nf, -1.0, f, b);
+}
+
 SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
                        const cplx* SLSE_RESTRICT x, const cplx* SLSE_RESTRICT Xhat, cplx* P, cplx* U,
-                       cplx* V, cplx* SLSE_RESTRICT w, const FftCtx& f, Blk& b) {
+                       cplx* V, cplx* SLSE_RESTRICT w, const FftCtx& f, Blk& b, Split* sp = nullptr) {
   const int tid_ = b.tid, nt_ = b.nt;
   const int lg = ilog2(2 * n);  // nf = next power of two >= 2N
   const int nf = 1 << lg;
@@ -900,20 +919,19 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
   }
   b.sync();
   const double inv = 1.0 / (double)nf;
-  // t1x = IFFT(U)[N-1 : 2N-1] and t0hx = IFFT(V)[N-1 : 2N-1], zero padded
-  fft_inplace(U, nf, 1.0, f, b);
-  fft_inplace(V, nf, 1.0, f, b);
-  // shift down by N-1 through registers (barrier between read and write)
-  for (int i0 = 0; i0 < nf; i0 += nt_) {
-    const int i = i0 + tid_;
-    cplx u = mk(0.0, 0.0), v = mk(0.0, 0.0);
-    if (i < n) { u = cscale(U[n - 1 + i], inv); v = cscale(V[n - 1 + i], inv); }
-    b.sync();
-    if (i < nf) { U[i] = u; V[i] = v; }
-    b.sync();
+  // t1x = IFFT(U)[N-1 : 2N-1] and t0hx = IFFT(V)[N-1 : 2N-1], zero padded,
+  // transformed back: two independent chains
+  if (SLSE_PAIR && sp) {
+    GsChainArgs a{V, n, nf};
+    SplitJob j;
+    j.set(kJobGsChain, a);
+    sp->post(j, b);
+    gs_chain(U, n, nf, f, b);
+    sp->done();
+  } else {
+    gs_chain(U, n, nf, f, b);
+    gs_chain(V, n, nf, f, b);
   }
-  fft_inplace(U, nf, -1.0, f, b);
-  fft_inplace(V, nf, -1.0, f, b);
   // Z = F1 * P1h - F0 * P0  -> U
   for (int k = tid_; k < nf; k += nt_) {
     const cplx p1 = P[k];
@@ -1110,7 +1128,7 @@ static __device__ __noinline__ double gs_apply_warp(const cplx* SLSE_RESTRICT rh
 // when the staging fits, else the general block version.
 SLSE_NI double gs_apply_any(const cplx* SLSE_RESTRICT rho, int n, double delta_last, const cplx* SLSE_RESTRICT x,
                            const cplx* SLSE_RESTRICT Xhat, cplx* P, cplx* U, cplx* V, cplx* SLSE_RESTRICT w,
-                           const FftCtx& f, Blk& b) {
+                           const FftCtx& f, Blk& b, Split* sp = nullptr) {
 #if !defined(SLSE_HOST_EMU) && !defined(SLSE_GS_BLOCK)
   if (b.nt == 32 && __isShared(f.smem)) {
     const int lg = ilog2(2 * n);
@@ -1119,7 +1137,7 @@ SLSE_NI double gs_apply_any(const cplx* SLSE_RESTRICT rho, int n, double delta_l
     }
   }
 #endif
-  return gs_apply(rho, n, delta_last, x, Xhat, P, U, V, w, f, b);
+  return gs_apply(rho, n, delta_last, x, Xhat, P, U, V, w, f, b, sp);
 }
 
 }  // namespace slse
