@@ -139,6 +139,27 @@ def test_batch_vs_oracle_cfg2_shape():
         assert abs(r.beta_hat - o.beta_hat) / o.beta_hat < AMP_TOL
 
 
+@pytest.mark.parametrize("per_sm", [7, 12])
+def test_batch_layouts_vs_oracle_cfg2_shape(per_sm):
+    """The N <= 512 solver layout depends on the batch size (solver_threads /
+    warps_per_cta): 128-thread CTAs up to 5 problems per SM, classic one-warp
+    CTAs up to 10, warp mode (16 one-warp solvers per CTA, operation
+    windows: the bench's cfg2 path) above.  A batch of per_sm x SMs seeded
+    cfg2 problems runs the classic (7) or the warp-mode (12) kernel; 24 of
+    its problems, spread over the batch, match the oracle's histories."""
+    import torch
+
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    B = per_sm * sms
+    Y = O.generate_batch(11, 2, B)
+    res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
+    assert np.all(res.status == 0)
+    for b in np.linspace(0, B - 1, 24).astype(int):
+        check_vs_oracle(res[int(b)], O.estimate(Y[b], O.OracleOptions(grid_factor=4)))
+
+
 def test_default_grid_factor_and_small_sizes():
     """Reference defaults (grid_factor=8) and the smallest / odd sizes."""
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
