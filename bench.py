@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU legs")
     ap.add_argument("--no-per-config", action="store_true", help="skip the per_config block")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--per-config-cpu", default="1,2,3",
                     help="configs whose real-reference CPU rate goes into per_config (cfg4/5 take minutes)")
     return ap.parse_args()
@@ -352,12 +353,18 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per rank; --dist-backend gloo (ranks sharing a GPU) only
+    # exercises the multi-rank code path on a one-GPU box, timings meaningless
+    local_dev = local % torch.cuda.device_count() if args.dist_backend == "gloo" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     from paper_1705_06073_b200 import EstimatorOptions, dist as D, estimate_batch, simdata
 
     cfg = args.config

@@ -160,6 +160,24 @@ def test_batch_layouts_vs_oracle_cfg2_shape(per_sm):
         check_vs_oracle(res[int(b)], O.estimate(Y[b], O.OracleOptions(grid_factor=4)))
 
 
+def test_work_counts_vs_oracle():
+    """The device keeps two bundles (current, trial) where the reference
+    keeps an LRU(4) cache (model_core.py:416-444): on the same inputs it may
+    never build MORE bundles than the oracle's LRU(4) engine (a rebuild the
+    reference would have served from its cache is wasted work), and the
+    histories it builds them for are the same."""
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
+
+    for cfg, n, k in ((2, None, None), (3, 512, 24)):
+        Y = O.generate_batch(5, cfg, 4, n=n, k=k)
+        res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
+        for b in range(Y.shape[0]):
+            o = O.estimate(Y[b], O.OracleOptions(grid_factor=4))
+            r = res[b]
+            assert r.trace_stages == o.trace_stages
+            assert 0 < r.counters["builds"] <= o.builds, (cfg, b, r.counters, o.builds)
+
+
 def test_default_grid_factor_and_small_sizes():
     """Reference defaults (grid_factor=8) and the smallest / odd sizes."""
     from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
