@@ -675,8 +675,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? SLSE_GRID_MINB : 1)) grid_fus
 // with semifast bundles on an observation pattern (model_core.py:316-409);
 // y rows hold G x M observed samples, the pattern (idx, scales) is shared
 // by the batch (pstride 0) or given per problem (pstride M).
+#ifndef SLSE_SF_MINB
+#define SLSE_SF_MINB 6  // 80 registers: cfg2-shape semifast 149 -> 94 ms per 4096 problems (2 -> 6 CTAs per SM)
+#endif
 template <int NT>
-__global__ void __launch_bounds__(NT) solve_sf_kernel(SolveParams P, const cplx* __restrict__ ys,
+__global__ void __launch_bounds__(NT, SLSE_SF_MINB) solve_sf_kernel(SolveParams P, const cplx* __restrict__ ys,
                                                       const int* __restrict__ pidx, const cplx* __restrict__ psc,
                                                       int pstride, int B, slse_outputs out, char* ws,
                                                       size_t slab_bytes, int* queue, const cplx* tw, int twlog,

@@ -947,16 +947,22 @@ struct Solver {
     const int kp = B.kp;
     if (kp) {
       sf_phases(sfE, kcap, obs, act_theta, k, b);
-      for (int j = 0; j < kp; ++j) {  // b_p(l), p in P (:400-403)
-        cplx* row = sfBb + (size_t)j * L;
-        SLSE_CTRL_LOOP
-        for (int l = tid_; l < L; l += nt_) row[l] = mk(0.0, 0.0);
-        b.sync();
-        const int pj = B.sP[j];
-        SLSE_CTRL_LOOP
-        for (int i = tid_; i < m; i += nt_) row[obs.idx[i]] = cscale(conjg(sfE[(size_t)i * kcap + pj]), sf_w0(obs, i));
-        b.sync();
-        fft(G1, L, +1.0, [=](int i) { return row[i]; }, [=](int l, cplx v) { row[l] = v; }, f, b);
+      // b_p(l), p in P (:400-403): scatter every row, then one batched
+      // inverse transform of the kp rows (in place)
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kp * L; t += nt_) sfBb[t] = mk(0.0, 0.0);
+      b.sync();
+      SLSE_CTRL_LOOP
+      for (int t = tid_; t < kp * m; t += nt_) {
+        const int j = t / m, i = t - j * m;
+        sfBb[(size_t)j * L + obs.idx[i]] = cscale(conjg(sfE[(size_t)i * kcap + B.sP[j]]), sf_w0(obs, i));
+      }
+      b.sync();
+      {
+        cplx* bb = sfBb;
+        const int LL = L;
+        fft_multi(G1, kp, L, +1.0, [=](int c, int i) { return bb[(size_t)c * LL + i]; },
+                  [=](int c, int l, cplx v) { bb[(size_t)c * LL + l] = v; }, f, b);
       }
       // |L^{-1} b(l)|^2 per grid point (b^H Sigma b, :404-405), in place
       SLSE_CTRL_LOOP
