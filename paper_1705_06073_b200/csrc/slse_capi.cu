@@ -485,8 +485,8 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   if (L >= 8192 && N >= 64 && !slse_knob("SLSE_GRID_OLD")) {
     // residue decomposition (slse_grid.cuh): R transforms of M <= 2048 points
     // per signal, three per task staged in shared memory.  Measured at the
-    // cfg4 / cfg5 shapes (batches > 2x L2): 402 us (13.4 % of HBM) vs 2208 us
-    // for the generic passes through global scratch, 743 vs 4076 us; at
+    // cfg4 / cfg5 shapes (batches > 2x L2): 374 us (14.4 % of HBM) vs 2208 us
+    // for the generic passes through global scratch, 608 vs 4076 us; at
     // L = 4096 (cfg3) the register-Stockham kernel below stays faster (243 vs 283 us)
     const int lgM = ilog2(N) < 11 ? ilog2(N) : 11;
 #define SLSE_GRID_RES(NTV, LGMV)                                                                            \

@@ -349,6 +349,9 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
 #ifndef SLSE_GRES_MINB
 #define SLSE_GRES_MINB 2
 #endif
+#ifndef SLSE_GRES_U
+#define SLSE_GRES_U 2
+#endif
 template <int NT, int LGM>
 __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res_kernel(
     const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int lgL,
@@ -367,34 +370,54 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res
     const int p = task >> lgR;
     const cplx* wp = w + (size_t)p * n;
     const cplx* rp = rho + (size_t)p * n;
-    for (int i = threadIdx.x; i < M; i += NT) {
-      cplx z0 = mk(0.0, 0.0), z1 = z0, z2 = z0;
+    // U items per thread per round, their loads issued together (the fold
+    // reads L2: one load round trip per fold step instead of per item)
+    constexpr int U = SLSE_GRES_U;
+    for (int i0 = threadIdx.x; i0 < M; i0 += U * NT) {
+      cplx z0[U], z1[U], z2[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) z0[u] = z1[u] = z2[u] = mk(0.0, 0.0);
       for (int j = 0; j < J; ++j) {
-        const int m = i + (j << LGM);
-        if (m >= n) break;
-        const cplx a = wp[m], b = rp[m];
-        const cplx bm = cscale(b, (double)m);
-        if (j == 0 || r == 0) {
-          z0 = cadd(z0, a);
-          z1 = cadd(z1, b);
-          z2 = cadd(z2, bm);
-        } else {
-          const cplx t = tw[tw_index((j * r) & ((1 << lgR) - 1), lgR)];  // W_R^{j r}
-          z0 = cadd(z0, cmul(a, t));
-          z1 = cadd(z1, cmul(b, t));
-          z2 = cadd(z2, cmul(bm, t));
+        cplx a[U], bb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int m = i0 + u * NT + (j << LGM);
+          const bool ok = i0 + u * NT < M && m < n;
+          a[u] = ok ? wp[m] : mk(0.0, 0.0);
+          bb[u] = ok ? rp[m] : mk(0.0, 0.0);
+        }
+        const cplx t = (j == 0 || r == 0) ? mk(1.0, 0.0) : tw[tw_index((j * r) & ((1 << lgR) - 1), lgR)];  // W_R^{j r}
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int m = i0 + u * NT + (j << LGM);
+          const cplx bm = cscale(bb[u], (double)m);
+          if (j == 0 || r == 0) {
+            z0[u] = cadd(z0[u], a[u]);
+            z1[u] = cadd(z1[u], bb[u]);
+            z2[u] = cadd(z2[u], bm);
+          } else {
+            z0[u] = cadd(z0[u], cmul(a[u], t));
+            z1[u] = cadd(z1[u], cmul(bb[u], t));
+            z2[u] = cadd(z2[u], cmul(bm, t));
+          }
         }
       }
-      if (r) {
-        const cplx t = tw[tw_index(i * r, lgL)];  // W_L^{i r}, i r < M R = L
-        z0 = cmul(z0, t);
-        z1 = cmul(z1, t);
-        z2 = cmul(z2, t);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * NT;
+        if (i >= M) break;
+        cplx y0 = z0[u], y1 = z1[u], y2 = z2[u];
+        if (r) {
+          const cplx t = tw[tw_index(i * r, lgL)];  // W_L^{i r}, i r < M R = L
+          y0 = cmul(y0, t);
+          y1 = cmul(y1, t);
+          y2 = cmul(y2, t);
+        }
+        const int si = sk(i);
+        X[si] = y0;
+        X[MS + si] = y1;
+        X[2 * MS + si] = y2;
       }
-      const int si = sk(i);
-      X[si] = z0;
-      X[MS + si] = z1;
-      X[2 * MS + si] = z2;
     }
     __syncthreads();
     fft_fixed_pruned<LGM, 0>(X, 3, -1.0, tw, twlog, threadIdx.x, NT);
