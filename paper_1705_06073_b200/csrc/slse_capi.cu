@@ -482,7 +482,8 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
     }
     if (e != cudaSuccess) return fail("grid_tma_kernel setup", e);
   }
-  if (L >= 8192 && N >= 64 && !slse_knob("SLSE_GRID_OLD")) {
+  const char* gmin = slse_knob("SLSE_GRES_MIN_L");  // experiment override of the residue-kernel threshold
+  if (L >= (gmin ? atoi(gmin) : 8192) && N >= 64 && !slse_knob("SLSE_GRID_OLD")) {
     // residue decomposition (slse_grid.cuh): R transforms of M <= 2048 points
     // per signal, three per task staged in shared memory.  Measured at the
     // cfg4 / cfg5 shapes (batches > 2x L2): 374 us (14.4 % of HBM) vs 2208 us
