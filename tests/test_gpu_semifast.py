@@ -221,3 +221,29 @@ def test_semifast_incomplete_batch_vs_oracle(n, k, m):
         o = O.estimate(Y[b], O.OracleOptions(grid_factor=4, backend="semifast"), n=n, observed_indices=I[b],
                        scales=S[b])
         check_vs_oracle(res[b], o)
+
+
+def test_semifast_edge_patterns():
+    """Edge cases of the observation pattern against the oracle's semifast
+    restatement: the minimum M = 2 (first and last sample), an incomplete
+    call whose pattern is every sample (== complete semifast), and unit vs
+    explicit unit scales."""
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch
+    from oracle import superlse_oracle as O
+
+    opts = EstimatorOptions(grid_factor=4, backend="semifast")
+    yf, _ = O.generate_problem(13, 1, 0)
+    n = yf.size
+    # M = 2
+    idx = np.array([1, n])
+    r = estimate_batch(yf[idx - 1][None], opts, n=n, observed_indices=idx)[0]
+    o = O.estimate(yf[idx - 1], O.OracleOptions(grid_factor=4, backend="semifast"), n=n, observed_indices=idx)
+    assert r.status == 0 and r.k_hat == o.k_hat
+    assert r.trace_stages == o.trace_stages
+    # full pattern through the incomplete API == complete data
+    full = np.arange(1, n + 1)
+    ri = estimate_batch(yf[None], opts, n=n, observed_indices=full, scales=np.ones(n, complex))[0]
+    rc = estimate_batch(yf[None], opts)[0]
+    assert ri.k_hat == rc.k_hat and ri.trace_stages == rc.trace_stages
+    assert rel(ri.objective_trace, rc.objective_trace) < CALL_TOL
+    assert np.max(wrap_distance(ri.theta_hat, rc.theta_hat), initial=0) < THETA_TOL
