@@ -208,9 +208,10 @@ _STAGE_ARR = np.array(STAGE_NAMES, dtype=object)
 
 def unpack_all(h: dict, algos: dict = None):
     """LseResult per problem from host (numpy) copies of the batch outputs.
-    Per-problem arrays are fresh copies (the caller owns them, as the
-    reference's results, estimator.py:262-275; they do not keep the batch's
-    host block alive)."""
+    Per-problem arrays are views of ONE pageable copy per field (the caller
+    owns them, as the reference's results, estimator.py:262-275; they do not
+    keep the batch's pinned host block alive, and the batch is copied in a
+    few large copies instead of six small ones per problem)."""
     B = h["k_hat"].shape[0]
     khat = h["k_hat"].tolist()
     ntr = h["n_trace"].tolist()
@@ -220,12 +221,12 @@ def unpack_all(h: dict, algos: dict = None):
     iters = h["iterations"].tolist()
     beta = h["beta"].tolist()
     zeta = h["zeta"].tolist()
-    alpha = np.ascontiguousarray(h["alpha"]).view(np.complex128)[..., 0]  # (B, G, K)
+    alpha = np.array(h["alpha"]).view(np.complex128)[..., 0]  # (B, G, K), pageable copy
     names = _STAGE_ARR[np.clip(h["stage"], 0, len(STAGE_NAMES) - 1)]
     secs = h["stage_seconds"].tolist()
     ctr = h["counters"].tolist()
-    theta, gamma, slot, trace, trace_k, events = (h["theta"], h["gamma"], h["slot"], h["trace"], h["trace_k"],
-                                                  h["events"])
+    theta, gamma, slot, trace, trace_k = (np.array(h[k]) for k in ("theta", "gamma", "slot", "trace", "trace_k"))
+    events = h["events"]
     iter_s = h.get("iter_seconds")
     out = []
     for b in range(B):
@@ -244,20 +245,20 @@ def unpack_all(h: dict, algos: dict = None):
         c = ctr[b]
         out.append(LseResult(
             k_hat=k,
-            theta_hat=theta[b, :k].copy(),
-            alpha_hat=alpha[b, :, :k].copy(),
+            theta_hat=theta[b, :k],
+            alpha_hat=alpha[b, :, :k],
             beta_hat=beta[b],
-            gamma_hat=gamma[b, :k].copy(),
+            gamma_hat=gamma[b, :k],
             zeta_hat=zeta[b],
-            objective_trace=trace[b, :nt].copy(),
+            objective_trace=trace[b, :nt],
             iterations=iters[b],
             wall_time_per_stage=times,
             converged=bool(fl & FLAG_CONVERGED),
             trace_stages=names[b, :nt].tolist(),
             warnings=warns,
             events=decode_events(events[b, :nev[b]].tolist()),
-            trace_k=trace_k[b, :nt].copy(),
-            slots=slot[b, :k].copy(),
+            trace_k=trace_k[b, :nt],
+            slots=slot[b, :k],
             counters=dict(builds=c[0], grids=c[1], stats=c[2], line_search_trials=c[3]),
             status=status[b],
             algorithms=dict(algos) if algos else {},
