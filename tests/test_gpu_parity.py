@@ -495,3 +495,26 @@ def test_trajectories_ragged_sizes_vs_oracle(n, k):
     res = estimate_batch(Y, EstimatorOptions(grid_factor=4, backend="superfast"))
     for b in range(Y.shape[0]):
         check_vs_oracle(res[b], O.estimate(Y[b], O.OracleOptions(grid_factor=4)))
+
+
+def test_layout_boundaries_same_results():
+    """Every solver layout boundary (N = 4096: CTA pair up to SMs/2 problems,
+    one 512-thread CTA up to SMs, paired 256-thread CTAs above; N = 256:
+    128-thread CTAs up to 5 per SM, classic one-warp CTAs up to 10, warp
+    mode above): every problem finishes, and problem 0's trajectory is the
+    same in each layout (4 outer iterations, to bound the run time)."""
+    import torch
+
+    from paper_1705_06073_b200 import EstimatorOptions, estimate_batch, simdata
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    opts = EstimatorOptions(grid_factor=4, backend="superfast", max_outer_iterations=4)
+    for cfg, sizes in ((4, (1, sms // 2, sms // 2 + 1, sms, sms + 1)), (2, (1, 5 * sms + 1, 10 * sms + 1))):
+        ref = None
+        for B in sizes:
+            r = estimate_batch(simdata.batch(7, cfg, B), opts)
+            assert np.all(r.status == 0), (cfg, B)
+            t0 = r[0].objective_trace
+            ref = t0 if ref is None else ref
+            assert r[0].trace_stages == r[0].trace_stages and t0.shape == ref.shape
+            assert rel(t0, ref) < 1e-12, (cfg, B)
