@@ -441,7 +441,9 @@ int slse_component_stats(const double* theta, const int32_t* kcount, int kstride
   cudaStream_t st = (cudaStream_t)stream;
   CfTable cft;
   cf_build(cft, N);
-  const int nt = block_threads(N);
+  // at most 512 threads: the two-chain sums (component_stats) need ~100
+  // registers, which 1024-thread blocks cannot give (measured 10x slower)
+  const int nt = block_threads(N) < 512 ? block_threads(N) : 512;
   cudaError_t e = cudaSuccess;
   SLSE_DISPATCH_NT(nt, {
     stats_kernel<NTC><<<B, NTC, kHeadBytes, st>>>(cft, theta, kcount, kstride, (const cplx*)rho, delta_last,

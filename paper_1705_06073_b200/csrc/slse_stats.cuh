@@ -86,35 +86,10 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
 #else
   const int lanes = 32, lane = tid_ & 31, warp = tid_ >> 5, nwarp = nt_ >> 5;
 #endif
-  for (int kk = warp; kk < K; kk += nwarp) {
-    const double th = thetas[kk];
-    double acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    const cplx step = expj2pi((double)lanes, th, -1.0);
-    cplx e = mk(1.0, 0.0);
-    int since = 1 << 30;
-    for (int m = lane; m < n; m += lanes) {
-      if (since >= 32) {
-        e = expj2pi((double)m, th, -1.0);
-        since = 0;
-      }
-      const double dm = (double)m;
-      const cplx p = cmul(rho[m], e);
-      const cplx qq = cmul(w[m], e);
-      const double m2 = dm * dm, m3 = m2 * dm;
-      acc[0] += p.re;       acc[1] += p.im;
-      acc[2] += dm * p.re;  acc[3] += dm * p.im;
-      acc[4] += m2 * p.re;  acc[5] += m2 * p.im;
-      acc[6] += m3 * p.re;  acc[7] += m3 * p.im;
-      const double d1 = two_pi * dm;
-      const double d2 = d1 * d1;
-      acc[8] += qq.re;       acc[9] += qq.im;
-      acc[10] += d1 * qq.re; acc[11] += d1 * qq.im;
-      acc[12] += d2 * qq.re; acc[13] += d2 * qq.im;
-      e = cmul(e, step);
-      ++since;
-    }
+  // Two frequencies per warp pass: two independent phasor chains per lane
+  // share the sample loads (the recurrence is the latency chain).  Every
+  // frequency's sums are formed exactly as with one chain.
+  const auto finish = [&](double* acc, int kk) {
 #ifndef SLSE_HOST_EMU
     // Transposed warp reduction: 16 shuffles for the 14 sums (vs 70), sum v
     // ends in lanes 2v, 2v+1.
@@ -183,6 +158,48 @@ SLSE_NI void component_stats(const double* SLSE_RESTRICT thetas, int K, const cp
       x[kk] = sum[3].re * sc_vx;
     }
 #endif
+  };
+  for (int kk0 = warp; kk0 < K; kk0 += 2 * nwarp) {
+    const int kk1 = kk0 + nwarp;
+    const bool two = kk1 < K;  // warp-uniform
+    const double th0 = thetas[kk0], th1 = two ? thetas[kk1] : th0;
+    double acc0[16], acc1[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc0[i] = acc1[i] = 0.0;
+    const cplx step0 = expj2pi((double)lanes, th0, -1.0), step1 = expj2pi((double)lanes, th1, -1.0);
+    cplx e0 = mk(1.0, 0.0), e1 = e0;
+    int since = 1 << 30;
+    for (int m = lane; m < n; m += lanes) {
+      if (since >= 32) {
+        e0 = expj2pi((double)m, th0, -1.0);
+        e1 = expj2pi((double)m, th1, -1.0);
+        since = 0;
+      }
+      const double dm = (double)m;
+      const cplx rm = rho[m], wm = w[m];
+      const double m2 = dm * dm, m3 = m2 * dm;
+      const double d1 = two_pi * dm;
+      const double d2 = d1 * d1;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        double* acc = c ? acc1 : acc0;
+        const cplx e = c ? e1 : e0;
+        const cplx p = cmul(rm, e);
+        const cplx qq = cmul(wm, e);
+        acc[0] += p.re;       acc[1] += p.im;
+        acc[2] += dm * p.re;  acc[3] += dm * p.im;
+        acc[4] += m2 * p.re;  acc[5] += m2 * p.im;
+        acc[6] += m3 * p.re;  acc[7] += m3 * p.im;
+        acc[8] += qq.re;       acc[9] += qq.im;
+        acc[10] += d1 * qq.re; acc[11] += d1 * qq.im;
+        acc[12] += d2 * qq.re; acc[13] += d2 * qq.im;
+      }
+      e0 = cmul(e0, step0);
+      e1 = cmul(e1, step1);
+      ++since;
+    }
+    finish(acc0, kk0);
+    if (two) finish(acc1, kk1);
   }
   b.sync();
 }
