@@ -39,7 +39,28 @@ SLSE_NI void steer_forward(cplx* SLSE_RESTRICT out, int n, const double* SLSE_RE
     cplx acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = mk(0.0, 0.0);
-    for (int kk = 0; kk < k; ++kk) {
+    // frequencies in pairs: two independent phasor chains (the recurrence
+    // is the latency chain); acc[j] still adds them in slot order
+    int kk = 0;
+    for (; kk + 1 < k; kk += 2) {
+      const double tha = thetas[kk], thb = thetas[kk + 1];
+      const double cra = coef_re[kk], crb = coef_re[kk + 1];
+      const double cia = coef_im ? coef_im[kk] : 0.0, cib = coef_im ? coef_im[kk + 1] : 0.0;
+      cplx ea = expj2pi((double)m0, tha, 1.0), eb = expj2pi((double)m0, thb, 1.0);
+      const cplx sa = expj2pi((double)nt_, tha, 1.0), sb = expj2pi((double)nt_, thb, 1.0);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < J) {
+          acc[j].re += ea.re * cra - ea.im * cia;
+          acc[j].im += ea.re * cia + ea.im * cra;
+          acc[j].re += eb.re * crb - eb.im * cib;
+          acc[j].im += eb.re * cib + eb.im * crb;
+          ea = cmul(ea, sa);
+          eb = cmul(eb, sb);
+        }
+      }
+    }
+    for (; kk < k; ++kk) {
       const double th = thetas[kk];
       const double cr = coef_re[kk];
       const double ci = coef_im ? coef_im[kk] : 0.0;
