@@ -898,6 +898,9 @@ SLSE_NI Factor toeplitz_factor(const cplx* SLSE_RESTRICT c, int n, cplx* e, cplx
 //   P0h_k = FFT(conj(rev v0))_k = W^{(N-1)k} conj(P0_k).
 // Xhat = FFT_nf(x) is cached by the caller (x = y is fixed per problem).
 // Buffers P, U, V: nf complex each (global).
+#ifndef SLSE_GS_CHAIN2
+#define SLSE_GS_CHAIN2 1
+#endif
 // One of GS apply's two independent chains: Y <- FFT(shift_{N-1}(IFFT(Y)) / nf)
 // (U and V below; a CTA pair runs one each, slse_split.cuh).
 SLSE_NI void gs_chain(cplx* Y, int n, int nf, const FftCtx& f, Blk& b) {
@@ -914,6 +917,25 @@ SLSE_NI void gs_chain(cplx* Y, int n, int nf, const FftCtx& f, Blk& b) {
     b.sync();
   }
   fft_inplace(Y, nf, -1.0, f, b);
+}
+
+// Both chains at once: the transforms of U and V batched (one barrier
+// sequence for two transforms in flight).
+SLSE_NI void gs_chain2(cplx* U, cplx* V, cplx* work, int n, int nf, const FftCtx& f, Blk& b) {
+  const int tid_ = b.tid, nt_ = b.nt;
+  const double inv = 1.0 / (double)nf;
+  fft_multi(work, 2, nf, 1.0, [=](int c, int i) { return c ? V[i] : U[i]; },
+            [=](int c, int i, cplx v) { (c ? V : U)[i] = v; }, f, b);
+  for (int i0 = 0; i0 < nf; i0 += nt_) {
+    const int i = i0 + tid_;
+    cplx u = mk(0.0, 0.0), v = mk(0.0, 0.0);
+    if (i < n) { u = cscale(U[n - 1 + i], inv); v = cscale(V[n - 1 + i], inv); }
+    b.sync();
+    if (i < nf) { U[i] = u; V[i] = v; }
+    b.sync();
+  }
+  fft_multi(work, 2, nf, -1.0, [=](int c, int i) { return c ? V[i] : U[i]; },
+            [=](int c, int i, cplx v) { (c ? V : U)[i] = v; }, f, b);
 }
 
 SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
@@ -949,6 +971,8 @@ SLSE_NI double gs_apply(const cplx* SLSE_RESTRICT rho, int n, double delta_last,
     sp->post(j, b);
     gs_chain(U, n, nf, f, b);
     sp->done();
+  } else if (SLSE_GS_CHAIN2 && 2 * nf <= f.smem_cap) {
+    gs_chain2(U, V, nullptr, n, nf, f, b);
   } else {
     gs_chain(U, n, nf, f, b);
     gs_chain(V, n, nf, f, b);
