@@ -16,8 +16,10 @@ between steps.  The JSON line also carries:
                at N > 1 GPUs the public multi-GPU entry
                dist.estimate_batch_distributed (shard, solve, all-gather);
   roofline     the activation-grid kernel (BASELINE metric "grid-eval HBM
-               GB/s vs peak") timed live at the config's shape, on a batch
-               whose outputs exceed L2 (so DRAM traffic = algorithmic bytes);
+               GB/s vs peak") timed live at the config's shape in both
+               forms (reference (w, om_s) and product (w, rho); the faster
+               one, the other under `alt`), on a batch whose outputs are 8x
+               the L2 (so DRAM traffic ~ algorithmic bytes);
   per_config   every BASELINE config (cfg1-5) solved in full on this GPU:
                problems/s, ms per batch, its grid roofline, and the real
                reference's CPU rate on a bounded sample (N = 1 only);
@@ -235,55 +237,85 @@ def time_steps(torch, stream, fn, steps, warmup, flush):
     return [a.elapsed_time(b) for a, b in ev]
 
 
-def grid_roofline(torch, dev, stream, flush, n, launches=10):
-    """Row 9 (model_core.py:303-313) standalone at the config's shape, on a
-    batch whose q^G / s^G outputs (24 L bytes per problem) exceed 2x the L2,
-    so every byte reaches DRAM inside the launch; CUDA events on the
-    launching stream, L2 flushed before each launch."""
+def _grid_form(torch, dev, stream, flush, n, L, B, form, launches):
+    """Time one form of row 9 standalone (CUDA events on the launching
+    stream, L2 flushed before each launch); returns (ms, kernel name)."""
     from paper_1705_06073_b200 import ops
 
-    L = 4 * n
-    per = 32 * n + 24 * L  # SURVEY 8(d): 16N (w) + 16N (rho) in, 16L (q^G) + 8L (s^G) out
-    B = max(1, -(-2 * L2_BYTES // (24 * L)))
-    B = max(B, 148)  # at least one problem per SM
     g = torch.Generator(device=dev).manual_seed(1)
-    rho = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
     w = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
-    dl = torch.rand(B, dtype=torch.float64, device=dev, generator=g) + 0.5
     qg = torch.empty((B, L), dtype=torch.complex128, device=dev)
     sg = torch.empty((B, L), dtype=torch.float64, device=dev)
-    ms = time_steps(torch, stream, lambda: ops.grid_eval(rho, dl, w, L, out=(qg, sg)), launches, 3, flush)
-    del rho, w, qg, sg
-    grid_ms = float(np.mean(ms))
-    alg = B * per
-    achieved = alg / (grid_ms / 1000.0) / 1e9
-    peaks, peak_src = measured_peaks()
-    flops = B * 15 * L * int(np.log2(L))  # SURVEY 8(d): 3 complex FFTs of L at 5 L log2 L
-    fp64_tf = flops / (grid_ms / 1000.0) / 1e12
-    fp64_peak, fp64_src = fp64_peak_tflops()
-    attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
-    if L == 1024 and 128 < n <= 256:
-        kname = "grid_tma_kernel"
-    elif L == 1024:
-        kname = "grid_fused_kernel"
-    elif L <= 4096:
-        kname = "grid_stockham_kernel"
+    if form == "omega":
+        # om_s rows as all_diagonal_sums()["s"] returns them: Hermitian, (2N - 1) wide
+        half = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
+        half[:, 0] = half[:, 0].real.to(torch.complex128)
+        om = torch.cat([torch.flip(half[:, 1:], dims=[1]).conj(), half], dim=1).contiguous()
+        del half
+        ms = time_steps(torch, stream, lambda: ops.grid_eval_omega(w, om, L, out=(qg, sg)), launches, 3, flush)
+        del om
+        kname = "grid_coef_kernel" if (L == 1024 and 128 < n <= 256) else "grid_res_kernel<omega>"
     else:
-        kname = "grid_kernel"
-    traffic = None
-    tf = os.path.join(REPO, "profiles", f"r2_{kname}_n{n}.json")
-    if os.path.exists(tf):  # DRAM bytes per launch from the committed ncu --set full capture of this shape
-        with open(tf) as fh:
-            t = json.load(fh)
-        if int(t.get("batch", -1)) == B:
-            traffic = int(t["traffic_bytes_per_launch"])
-    return {"bound": "hbm", "kernel": f"{kname} (activation grid, SURVEY 8(a) row 9)",
-            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-            "traffic": traffic, "peak_source": peak_src, "batch": B, "alg_bytes_per_problem": per,
-            "alg_bytes_per_launch": alg, "launch_ms": grid_ms, "flops_per_launch": flops,
-            "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "peak_source": fp64_src,
-                     "frac": fp64_tf / fp64_peak, "attainable_tflops": attainable,
-                     "frac_of_min_roofline": fp64_tf / attainable}}
+        rho = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
+        dl = torch.rand(B, dtype=torch.float64, device=dev, generator=g) + 0.5
+        ms = time_steps(torch, stream, lambda: ops.grid_eval(rho, dl, w, L, out=(qg, sg)), launches, 3, flush)
+        del rho, dl
+        if L == 1024 and 128 < n <= 256:
+            kname = "grid_tma_kernel"
+        elif L == 1024:
+            kname = "grid_fused_kernel"
+        elif L <= 4096:
+            kname = "grid_stockham_kernel"
+        else:
+            kname = "grid_res_kernel"
+    del w, qg, sg
+    torch.cuda.empty_cache()
+    return float(np.mean(ms)), kname
+
+
+def grid_roofline(torch, dev, stream, flush, n, launches=10):
+    """Row 9 (model_core.py:303-313) standalone at the config's shape, on a
+    batch whose q^G / s^G outputs (24 L bytes per problem) are 8x the L2, so
+    all but the last ~L2 of the writes reach DRAM inside the launch (ncu
+    traffic within a few % of the algorithmic bytes).  Both forms are timed:
+      omega -- the reference's grid() literally: q^G = FFT_L(w), s^G from the
+               om_s diagonal sums (slse_grid_eval_omega), 2 transforms;
+      rho   -- s^G from the GS vector by the product form (slse_grid_eval,
+               what the solver fuses), 3 transforms.
+    Same algorithmic bytes (16N w + 16N om_s half or rho in, 24L out); the
+    faster form is `roofline`, the other is `alt`."""
+    L = 4 * n
+    per = 32 * n + 24 * L  # SURVEY 8(d): 16N (w) + 16N (om_s / rho) in, 16L (q^G) + 8L (s^G) out
+    B = max(148, -(-8 * L2_BYTES // (24 * L)))
+    peaks, peak_src = measured_peaks()
+    fp64_peak, fp64_src = fp64_peak_tflops()
+    out = {}
+    for form, ntr in (("omega", 2), ("rho", 3)):
+        grid_ms, kname = _grid_form(torch, dev, stream, flush, n, L, B, form, launches)
+        alg = B * per
+        achieved = alg / (grid_ms / 1000.0) / 1e9
+        flops = B * 5 * ntr * L * int(np.log2(L))  # SURVEY 8(d): ntr complex FFTs of L at 5 L log2 L
+        fp64_tf = flops / (grid_ms / 1000.0) / 1e12
+        attainable = min(peaks["hbm_gbs"] * 1e9 * flops / alg, fp64_peak * 1e12) / 1e12  # min(BW*AI, FP64)
+        traffic = None
+        tf = os.path.join(REPO, "profiles", f"r2_{kname.replace('<omega>', '_omega')}_n{n}.json")
+        if os.path.exists(tf):  # DRAM bytes per launch from the committed ncu --set full capture of this shape
+            with open(tf) as fh:
+                t = json.load(fh)
+            if int(t.get("batch", -1)) == B:
+                traffic = int(t["traffic_bytes_per_launch"])
+        out[form] = {"bound": "hbm", "kernel": f"{kname} (activation grid, SURVEY 8(a) row 9, {form} form)",
+                     "form": form, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peak_src, "batch": B,
+                     "alg_bytes_per_problem": per, "alg_bytes_per_launch": alg, "launch_ms": grid_ms,
+                     "flops_per_launch": flops,
+                     "fp64": {"achieved_tflops": fp64_tf, "peak_tflops": fp64_peak, "peak_source": fp64_src,
+                              "frac": fp64_tf / fp64_peak, "attainable_tflops": attainable,
+                              "frac_of_min_roofline": fp64_tf / attainable}}
+    best, other = ("omega", "rho") if out["omega"]["launch_ms"] <= out["rho"]["launch_ms"] else ("rho", "omega")
+    r = dict(out[best])
+    r["alt"] = out[other]
+    return r
 
 
 # ------------------------------------------------------------------ reference arm

@@ -148,6 +148,14 @@ int slse_component_stats(const double* theta, const int32_t* kcount, int kstride
 int slse_grid_eval(const double* rho, const double* delta_last, const double* w, int N, int L, int B,
                    double* q_grid, double* s_grid, void* stream);
 
+/* Row 9, the reference's own form (model_core._SuperfastBundle.grid :303-313
+ * literally): q_grid = FFT_L(w), s_grid = L IFFT_L(buf).real with
+ * buf[i mod L] = om_s(i), |i| < N.  om_s: [B, 2N-1] complex, index i + N - 1
+ * (the slse_omegas "s" output; Hermitian, toeplitz.py:428-430, so only its
+ * i >= 0 half is read).  Same outputs as slse_grid_eval. */
+int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int B, double* q_grid, double* s_grid,
+                         void* stream);
+
 /* Row 10: activation curve Delta L_l = log1p(gbar s_l) + ln((1-ze)/ze)
  * - |q_l|^2 / (1/gbar + s_l) over the grid (G = 1; ze = clamp(zeta[b],
  * 1/(2 kmax), 1/2)) and its argmin, lowest index on ties.  curve [B, L]

@@ -78,6 +78,7 @@ def load():
         "slse_gs_apply": ([vp, vp, vp, i, i, vp, vp, vp], i),
         "slse_component_stats": ([vp, vp, i, vp, vp, vp, i, i, vp, vp, vp, vp, vp, vp, vp, vp], i),
         "slse_grid_eval": ([vp, vp, vp, i, i, i, vp, vp, vp], i),
+        "slse_grid_eval_omega": ([vp, vp, i, i, i, vp, vp, vp], i),
         "slse_omegas": ([vp, vp, i, i, vp, vp, vp, vp, vp], i),
         "slse_activation_curve": ([vp, vp, vp, vp, i, i, i, vp, vp, vp], i),
         "slse_deactivation_margins": ([vp, vp, vp, vp, i, vp, i, i, vp, vp, vp], i),

@@ -591,6 +591,78 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
   return e == cudaSuccess ? 0 : fail("grid_kernel", e);
 }
 
+int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int B, double* q_grid, double* s_grid,
+                         void* stream) {
+  // the reference's grid length is a power of two >= 2N (model_core.py:224-227);
+  // below 2N - 1 its buffer placement would alias om_s(i) and om_s(i - L)
+  if (N < 1 || !pow2(L) || L < 2 * N - 1 || B < 0)
+    return fail_arg("slse_grid_eval_omega: L must be a power of two >= 2N - 1");
+  if (B == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const cplx* tw;
+  int twlog;
+  int rc = twiddles(ilog2(L), st, &tw, &twlog);
+  if (rc) return rc;
+  cudaError_t e = cudaSuccess;
+  if (L == 1024 && N > 128 && N <= 256) {
+    // cfg2 shape: two-pass exchange, TMA bulk input stages, persistent CTAs
+    const size_t smem = gc_smem_bytes();
+    e = set_smem(grid_coef_kernel, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_coef_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_coef_kernel, kGCThreads, smem);
+    if (e != cudaSuccess || occ < 1) return fail("grid_coef_kernel setup", e);
+    int g = sm_count() * occ;
+    if (g > B) g = B;
+    grid_coef_kernel<<<g, kGCThreads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, B, (cplx*)q_grid, s_grid, tw);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : fail("grid_coef_kernel", e);
+  }
+  const int lgL = ilog2(L);
+  if (L < 16) {
+    const long long items = (long long)B * L;
+    grid_coef_direct_kernel<<<(unsigned)((items + 127) / 128), 128, 0, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL,
+                                                                            B, (cplx*)q_grid, s_grid, tw);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : fail("grid_coef_direct_kernel", e);
+  }
+  // residue decomposition with two transforms per (problem, residue)
+  int lgM = ilog2(N);
+  if (lgM < 4) lgM = 4;
+  if (lgM > 11) lgM = 11;
+#define SLSE_GRID_RES_OM(NTV, LGMV)                                                                         \
+  case LGMV: {                                                                                              \
+    const size_t smem = 2 * 16 * (size_t)sk_len(1 << LGMV);                                                 \
+    e = set_smem(grid_res_kernel<NTV, LGMV, true>, smem);                                                   \
+    int occ = 0;                                                                                            \
+    if (e == cudaSuccess)                                                                                   \
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_res_kernel<NTV, LGMV, true>, NTV, smem); \
+    if (e != cudaSuccess || occ < 1) return fail("grid_res_kernel (omega) setup", e);                       \
+    long long g = (long long)sm_count() * occ;                                                              \
+    const long long tasks = (long long)B << (lgL - LGMV);                                                   \
+    if (g > tasks) g = tasks;                                                                               \
+    grid_res_kernel<NTV, LGMV, true><<<(int)g, NTV, smem, st>>>((const cplx*)om_s, nullptr, (const cplx*)w, N, \
+                                                                lgL, B, (cplx*)q_grid, s_grid, tw, twlog);  \
+    e = cudaGetLastError();                                                                                 \
+    return e == cudaSuccess ? 0 : fail("grid_res_kernel (omega)", e);                                       \
+  }
+  switch (lgM) {
+    SLSE_GRID_RES_OM(64, 4)
+    SLSE_GRID_RES_OM(64, 5)
+    SLSE_GRID_RES_OM(128, 6)
+    SLSE_GRID_RES_OM(128, 7)
+    SLSE_GRID_RES_OM(128, 8)
+    SLSE_GRID_RES_OM(128, 9)
+    SLSE_GRID_RES_OM(192, 10)
+    SLSE_GRID_RES_OM(384, 11)
+    default: break;
+  }
+#undef SLSE_GRID_RES_OM
+  return fail_arg("slse_grid_eval_omega: unsupported shape");
+}
+
 size_t slse_estimate_workspace_bytes_mmv(int N, int G, int B, const slse_options* opts) {
   slse_options o;
   if (opts) o = *opts; else slse_default_options(&o);

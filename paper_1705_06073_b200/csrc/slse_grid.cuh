@@ -335,6 +335,151 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Coefficient form, the reference's own grid() (model_core.py:303-313):
+//   q^G = FFT_L(w),   s^G = L IFFT_L(buf).real,  buf[i mod L] = om_s(i), |i| < N,
+// with om_s = all_diagonal_sums()["s"] (toeplitz.py:415-432), Hermitian by
+// construction (toeplitz.py:428-430).  So with d_0 = om_s(0), d_k = 2 om_s(k):
+//   s^G_l = Re sum_{k<N} d_k e^{+j 2 pi k l / L} = Re FFT_L(conj d)[l],
+// one forward N-point-supported transform per output, the real part kept
+// (the last radix-4 stage's imaginary halves are dead code).  Inputs: the
+// w row and the non-negative half of the om_s row (16 N bytes each, the same
+// algorithmic bytes as the (w, rho) form); 2 transforms instead of 3.
+//
+// L = 1024, 128 < N <= 256 (cfg2).  Same two-pass exchange as grid_tma_kernel,
+// 128 threads per CTA, every role warp-uniform:
+//   inner: warp r = residue, lanes 0-15 w, 16-31 conj d (t = lane & 15): the
+//          W64^{s r} pre-twiddles are compile-time for the whole warp;
+//   outer: warps 0-1 q^G (a = tid), warps 2-3 s^G (a = tid - 64).
+// Inputs by TMA bulk copy into NS stages; persistent CTAs; one barrier per
+// problem, plus the xfree mbarrier guarding the exchange buffer.
+constexpr int kGCThreads = 128;
+constexpr int kGCWarps = kGCThreads / 32;
+#ifndef SLSE_GC_STAGES
+#define SLSE_GC_STAGES 2  // measured at B = 43008: 2 stages 250 us, 3: 261 us, 4: 262 us (4 vs 3 CTAs per SM)
+#endif
+constexpr int kGCStages = SLSE_GC_STAGES;
+SLSE_HD constexpr size_t gc_smem_bytes() {
+  // mbarriers (128 B) | NS stages of (w, om) rows | X (2 exchange buffers)
+  return 128 + (size_t)kGCStages * 2 * 16 * kG5Rows + 2 * 16 * (size_t)kG5Buf;
+}
+
+__global__ void __launch_bounds__(kGCThreads) grid_coef_kernel(const cplx* __restrict__ w,
+                                                                 const cplx* __restrict__ om_s, int n, int B,
+                                                                 cplx* __restrict__ q_grid,
+                                                                 double* __restrict__ s_grid,
+                                                                 const cplx* __restrict__ tw) {
+  constexpr int L = 1024;
+  constexpr int NS = kGCStages;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* full = (uint64_t*)smem_raw;  // [NS]
+  uint64_t* xfree = full + NS;
+  cplx* stage = (cplx*)(smem_raw + 128);  // [NS][w | om], kG5Rows each (zero past n)
+  cplx* X = stage + NS * 2 * kG5Rows;     // 2 exchange buffers
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const unsigned row_bytes = 16u * (unsigned)n;
+  const int G = gridDim.x;
+  const size_t om_stride = 2 * (size_t)n - 1;
+
+  const auto issue = [&](int prob, int st) {
+    mbar_expect_tx(&full[st], 2 * row_bytes);
+    tma_load_1d(stage + st * 2 * kG5Rows, w + (size_t)prob * n, row_bytes, &full[st]);
+    tma_load_1d(stage + st * 2 * kG5Rows + kG5Rows, om_s + (size_t)prob * om_stride + (n - 1), row_bytes,
+                &full[st]);
+  };
+  for (int i = tid; i < NS * 2 * kG5Rows; i += kGCThreads)  // zero tails (the copies never touch them)
+    if ((i & (kG5Rows - 1)) >= n) stage[i] = mk(0.0, 0.0);
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    mbar_init(xfree, kGCWarps);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if ((int)blockIdx.x + s * G < B) issue(blockIdx.x + s * G, s);
+  }
+  const int h = lane >> 4, t = lane & 15;
+  cplx* Xi = X + h * kG5Buf;
+  const bool oq = warp < 2;
+  const int oa = tid & 63;
+  const cplx* Xo = X + (oq ? 0 : 1) * kG5Buf + oa * kG5Row;
+  const cplx* twa = tw + tw_index(oa, 10);
+  // om half: conj, doubled except om_s(0)
+  const double sc0 = (h && t) ? 2.0 : 1.0;
+
+  int p = blockIdx.x;
+  unsigned st = 0, ph = 0;
+  for (unsigned k = 0; p < B; ++k, p += G) {
+    mbar_wait(&full[st], ph);
+    const cplx* src = stage + st * 2 * kG5Rows + h * kG5Rows;
+    cplx v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = src[t + 16 * s];
+    if (h) {
+      v[0] = mk(sc0 * v[0].re, -sc0 * v[0].im);
+#pragma unroll
+      for (int s = 1; s < 16; ++s) v[s] = mk(2.0 * v[s].re, -2.0 * v[s].im);
+    }
+    switch (warp) {  // Y(t, r + 4 a') = v[g5_pos(a')], r = warp
+      case 0: dft16_t<0>(v); break;
+      case 1: dft16_t<1>(v); break;
+      case 2: dft16_t<2>(v); break;
+      default: dft16_t<3>(v); break;
+    }
+    if (k) mbar_wait(xfree, (k - 1) & 1);  // everyone has read problem k-1's X
+#pragma unroll
+    for (int a2 = 0; a2 < 16; ++a2) Xi[(warp + 4 * a2) * kG5Row + t] = v[g5_pos(a2)];
+    __syncthreads();
+    if (tid == 0 && p + NS * G < B) issue(p + NS * G, st);
+    if (++st == NS) { st = 0; ph ^= 1u; }
+#pragma unroll
+    for (int tt = 0; tt < 16; ++tt) v[tt] = Xo[tt];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xfree);
+    g5_outer_twiddles(v, twa, oa);
+    dft16_t<0>(v);  // bin l = a + 64 b is v[g5_pos(b)]
+    if (oq) {
+      double2* qg = (double2*)(q_grid + (size_t)p * L);
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const cplx o = v[g5_pos(b)];
+        __stcs(&qg[oa + 64 * b], make_double2(o.re, o.im));
+      }
+    } else {
+      double* sg = s_grid + (size_t)p * L;
+#pragma unroll
+      for (int b = 0; b < 16; ++b) __stcs(&sg[oa + 64 * b], v[g5_pos(b)].re);
+    }
+  }
+}
+
+// Coefficient form for tiny grids (L < 16): one thread per (problem, bin),
+// direct sums with the table's exact twiddles W_L^{(m l) mod L}.
+__global__ void grid_coef_direct_kernel(const cplx* __restrict__ w, const cplx* __restrict__ om_s, int n, int lgL,
+                                        int B, cplx* __restrict__ q_grid, double* __restrict__ s_grid,
+                                        const cplx* __restrict__ tw) {
+  const int L = 1 << lgL;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)B * L) return;
+  const int p = (int)(i >> lgL), l = (int)(i & (L - 1));
+  const cplx* wp = w + (size_t)p * n;
+  const cplx* op = om_s + (size_t)p * (2 * (size_t)n - 1) + (n - 1);
+  cplx q = mk(0.0, 0.0);
+  double s = 0.0;
+  for (int m = 0; m < n; ++m) {
+    const cplx e = tw[tw_index((m * l) & (L - 1), lgL)];  // e^{-j 2 pi m l / L}
+    q = cadd(q, cmul(wp[m], e));
+    const double f = m ? 2.0 : 1.0;
+    s += f * (op[m].re * e.re + op[m].im * e.im);  // Re(om conj(e))
+  }
+  q_grid[i] = q;
+  s_grid[i] = s;
+}
+
+// ---------------------------------------------------------------------------
 // Residue-decomposed grid for the other large shapes (L >= 2048): with
 // L = R M and l = r + R m,
 //   X[r + R m] = sum_{i<M} z_r(i) W_M^{i m},
@@ -352,7 +497,12 @@ __global__ void SLSE_G5_BOUNDS grid_tma_kernel(
 #ifndef SLSE_GRES_U
 #define SLSE_GRES_U 2
 #endif
-template <int NT, int LGM>
+//
+// OMEGA = true: the coefficient form (grid_coef_kernel above): `rho` is the
+// om_s array ([B, 2N-1], row p's om_s(0) at p (2N-1) + N-1) and the second
+// signal is conj d (d_0 = om_s(0), d_k = 2 om_s(k)); two transforms per
+// residue, s^G = Re of the second; `delta_last` is unused.
+template <int NT, int LGM, bool OMEGA = false>
 __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res_kernel(
     const cplx* __restrict__ rho, const double* __restrict__ delta_last, const cplx* __restrict__ w, int n, int lgL,
     int B, cplx* __restrict__ q_grid, double* __restrict__ s_grid, const cplx* __restrict__ tw, int twlog) {
@@ -369,7 +519,7 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res
     const int r = task & ((1 << lgR) - 1);
     const int p = task >> lgR;
     const cplx* wp = w + (size_t)p * n;
-    const cplx* rp = rho + (size_t)p * n;
+    const cplx* rp = OMEGA ? rho + (size_t)p * (2 * (size_t)n - 1) + (n - 1) : rho + (size_t)p * n;
     // U items per thread per round, their loads issued together (the fold
     // reads L2: one load round trip per fold step instead of per item)
     constexpr int U = SLSE_GRES_U;
@@ -385,6 +535,10 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res
           const bool ok = i0 + u * NT < M && m < n;
           a[u] = ok ? wp[m] : mk(0.0, 0.0);
           bb[u] = ok ? rp[m] : mk(0.0, 0.0);
+          if (OMEGA) {
+            const double f = m ? 2.0 : 1.0;
+            bb[u] = mk(f * bb[u].re, -f * bb[u].im);
+          }
         }
         const cplx t = (j == 0 || r == 0) ? mk(1.0, 0.0) : tw[tw_index((j * r) & ((1 << lgR) - 1), lgR)];  // W_R^{j r}
 #pragma unroll
@@ -394,11 +548,11 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res
           if (j == 0 || r == 0) {
             z0[u] = cadd(z0[u], a[u]);
             z1[u] = cadd(z1[u], bb[u]);
-            z2[u] = cadd(z2[u], bm);
+            if (!OMEGA) z2[u] = cadd(z2[u], bm);
           } else {
             z0[u] = cadd(z0[u], cmul(a[u], t));
             z1[u] = cadd(z1[u], cmul(bb[u], t));
-            z2[u] = cadd(z2[u], cmul(bm, t));
+            if (!OMEGA) z2[u] = cadd(z2[u], cmul(bm, t));
           }
         }
       }
@@ -411,16 +565,29 @@ __global__ void __launch_bounds__(NT, (NT <= 192 ? 3 : SLSE_GRES_MINB)) grid_res
           const cplx t = tw[tw_index(i * r, lgL)];  // W_L^{i r}, i r < M R = L
           y0 = cmul(y0, t);
           y1 = cmul(y1, t);
-          y2 = cmul(y2, t);
+          if (!OMEGA) y2 = cmul(y2, t);
         }
         const int si = sk(i);
         X[si] = y0;
         X[MS + si] = y1;
-        X[2 * MS + si] = y2;
+        if (!OMEGA) X[2 * MS + si] = y2;
       }
     }
     __syncthreads();
-    fft_fixed_pruned<LGM, 0>(X, 3, -1.0, tw, twlog, threadIdx.x, NT);
+    // (the signal count stays a run-time value: a compile-time 2 made nvcc
+    // unroll the plan's count loops into a 656-byte stack frame)
+    fft_fixed_pruned<LGM, 0>(X, OMEGA ? 2 + (lgL < 0) : 3, -1.0, tw, twlog, threadIdx.x, NT);
+    if (OMEGA) {
+      cplx* qg = q_grid + (size_t)p * L + r;
+      double* sg = s_grid + (size_t)p * L + r;
+      for (int k = threadIdx.x; k < M; k += NT) {
+        const int sk_ = sk(k);
+        qg[(size_t)k << lgR] = X[sk_];
+        sg[(size_t)k << lgR] = X[MS + sk_].re;
+      }
+      __syncthreads();
+      continue;
+    }
     const double inv_d = 1.0 / delta_last[p];
     cplx* qg = q_grid + (size_t)p * L + r;
     double* sg = s_grid + (size_t)p * L + r;

@@ -108,6 +108,25 @@ def grid_eval(rho, delta_last, w, L, out=None):
     return qg, sg
 
 
+def grid_eval_omega(w, om_s, L, out=None):
+    """Row 9 in the reference's own form (model_core._SuperfastBundle.grid,
+    :303-313): q_grid = FFT_L(w), s_grid = L IFFT_L(om_s wrapped).real, from
+    w (B, N) and om_s (B, 2N-1) (the omegas() "s" diagonal sums); returns
+    (q_grid (B, L) complex, s_grid (B, L) real)."""
+    lib = _native.load()
+    B, n = w.shape
+    if om_s.shape != (B, 2 * n - 1):
+        raise ValueError(f"om_s must be (B, 2N-1) = ({B}, {2 * n - 1}), got {tuple(om_s.shape)}")
+    if out is None:
+        qg = torch.empty((B, L), dtype=torch.complex128, device=w.device)
+        sg = torch.empty((B, L), dtype=torch.float64, device=w.device)
+    else:
+        qg, sg = out
+    _native.check(lib.slse_grid_eval_omega(_p(w), _p(om_s), n, L, B, _p(qg), _p(sg), _stream()),
+                  "slse_grid_eval_omega")
+    return qg, sg
+
+
 def omegas(rho, delta_last):
     """Row 7: dict s, t, v, x of the diagonal sums omega(i), i = -(N-1)..N-1,
     each (B, 2N-1) complex (toeplitz.all_diagonal_sums, :415-432)."""

@@ -398,6 +398,49 @@ def test_grid_eval_shapes_against_fft(n, L, B):
         assert rel(s[b], S[b]) < CALL_TOL, b
 
 
+@pytest.mark.parametrize("cfg,b,state", ROW_CASES)
+def test_grid_eval_omega_against_reference(cfg, b, state):
+    """Row 9 in the reference's own form: the golden w and om_s (the
+    reference's all_diagonal_sums) in, q^G and s^G against the reference's
+    grid() output (model_core.py:303-313) at the per-call bar."""
+    from paper_1705_06073_b200 import ops
+
+    z = load(cfg)
+    p = f"p{b}_call_{state}_"
+    n = z[p + "w"].size
+    L = O.default_grid_size(n, 4)
+    qg, sg = ops.grid_eval_omega(_dev(z[p + "w"][None, :]), _dev(z[p + "om_s"][None, :]), L)
+    assert rel(qg.cpu().numpy()[0], z[p + "q_grid"]) < CALL_TOL
+    assert rel(sg.cpu().numpy()[0], z[p + "s_grid"]) < CALL_TOL
+
+
+@pytest.mark.parametrize("n,L,B", [(256, 1024, 300), (200, 1024, 37), (129, 1024, 5), (256, 1024, 1),
+                                   # every residue-kernel M (2^4 .. 2^11), folds, ragged N, the direct kernel
+                                   (2, 4, 3), (2, 8, 3), (4, 8, 2), (3, 16, 4), (17, 64, 5), (64, 256, 9), (100, 512, 6),
+                                   (128, 1024, 4), (257, 1024, 3), (256, 2048, 7), (1000, 4096, 3),
+                                   (2048, 8192, 5), (3000, 16384, 4), (4096, 16384, 300), (16384, 65536, 2)])
+def test_grid_eval_omega_shapes_against_fft(n, L, B):
+    """Row 9 coefficient form on every kernel family vs the reference's
+    literal formula in numpy (q^G = fft(w, L), s^G = L ifft(buf).real with
+    buf[i mod L] = om_s(i)) on seeded Hermitian om_s rows."""
+    from paper_1705_06073_b200 import ops
+
+    rng = np.random.default_rng(n * 11 + L + B)
+    w = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    half = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    half[:, 0] = half[:, 0].real
+    om = np.concatenate([np.conj(half[:, :0:-1]), half], axis=1)
+    qg, sg = ops.grid_eval_omega(_dev(w), _dev(om), L)
+    Q = np.fft.fft(w, L, axis=1)
+    buf = np.zeros((B, L), dtype=np.complex128)
+    buf[:, np.arange(-(n - 1), n) % L] = om
+    S = (L * np.fft.ifft(buf, axis=1)).real
+    q, s = qg.cpu().numpy(), sg.cpu().numpy()
+    for b in range(B):
+        assert rel(q[b], Q[b]) < CALL_TOL, b
+        assert rel(s[b], S[b]) < CALL_TOL, b
+
+
 SWEEP_N = [2, 3, 17, 64, 100, 255, 256, 257, 300, 512, 513, 1000, 2048, 3000, 4096]
 
 
