@@ -11,6 +11,7 @@
 //   tw_fill_kernel        twiddle table exp(-2 pi i k / TW).
 #include "slse_kernels.cuh"
 #include "slse_grid.cuh"
+#include "slse_grid3.cuh"
 
 #include <cstdlib>
 
@@ -621,6 +622,29 @@ int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int 
     return e == cudaSuccess ? 0 : fail("grid_coef_kernel", e);
   }
   const int lgL = ilog2(L);
+  if (lgL >= 12 && !slse_knob("SLSE_GRID_NO_R3")) {
+    // register transforms of 4096 points per (problem, signal, residue) task (slse_grid3.cuh)
+    const bool pruned = lgL == 12 && N <= 1024;
+    const void* fn = pruned ? (const void*)grid_r3_kernel<0> : (const void*)grid_r3_kernel<1>;
+    const size_t smem = r3_smem_bytes();
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kR3Threads, smem);
+    if (e != cudaSuccess || occ < 1) return fail("grid_r3_kernel setup", e);
+    long long g = (long long)sm_count() * occ;
+    const long long tasks = ((long long)B * 2) << (lgL - 12);
+    if (g > tasks) g = tasks;
+    if (pruned)
+      grid_r3_kernel<0><<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL, B, (cplx*)q_grid,
+                                                          s_grid, tw);
+    else
+      grid_r3_kernel<1><<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL, B, (cplx*)q_grid,
+                                                          s_grid, tw);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : fail("grid_r3_kernel", e);
+  }
   if (L < 16) {
     const long long items = (long long)B * L;
     grid_coef_direct_kernel<<<(unsigned)((items + 127) / 128), 128, 0, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL,
