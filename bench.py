@@ -254,7 +254,14 @@ def _grid_form(torch, dev, stream, flush, n, L, B, form, launches):
         del half
         ms = time_steps(torch, stream, lambda: ops.grid_eval_omega(w, om, L, out=(qg, sg)), launches, 3, flush)
         del om
-        kname = "grid_coef_kernel" if (L == 1024 and 128 < n <= 256) else "grid_res_kernel<omega>"
+        if L == 1024 and 128 < n <= 256:
+            kname = "grid_coef_kernel"
+        elif 16384 <= L <= 32768 and 4 * n <= L:
+            kname = "grid_r3s_kernel"  # residue pairs of 4096-point register transforms, s^G at half length
+        elif L >= 4096:
+            kname = "grid_r3_kernel"   # 4096-point register transforms (three DFT16 passes)
+        else:
+            kname = "grid_res_kernel<omega>"
     else:
         rho = torch.randn((B, n), dtype=torch.complex128, device=dev, generator=g)
         dl = torch.rand(B, dtype=torch.float64, device=dev, generator=g) + 0.5

@@ -622,6 +622,26 @@ int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int 
     return e == cudaSuccess ? 0 : fail("grid_coef_kernel", e);
   }
   const int lgL = ilog2(L);
+  if (lgL >= 14 && lgL <= 15 && 4LL * N <= L && !slse_knob("SLSE_GRID_NO_R3P")) {
+    // residue pairs (whole-sector stores), s^G at half length (slse_grid3.cuh).  From L = 65536 the
+    // folds (4 for q^G, 8 for the half-length s^G, re-read per residue) outweigh the store savings:
+    // cfg5 shape 1.82 ms here vs 1.40 ms on the single-residue tasks below.
+    const long long tasks = (long long)B * (3 << (lgL - 14));
+    const size_t smem = r3s_smem_bytes();
+    e = set_smem(grid_r3s_kernel, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_r3s_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_r3s_kernel, kR3Threads, smem);
+    if (e != cudaSuccess || occ < 1) return fail("grid_r3s_kernel setup", e);
+    long long g = (long long)sm_count() * occ;
+    if (g > tasks) g = tasks;
+    grid_r3s_kernel<<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL, B, (cplx*)q_grid,
+                                                      s_grid, tw);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : fail("grid_r3s_kernel", e);
+  }
   if (lgL >= 12 && !slse_knob("SLSE_GRID_NO_R3")) {
     // register transforms of 4096 points per (problem, signal, residue) task (slse_grid3.cuh)
     const bool pruned = lgL == 12 && N <= 1024;

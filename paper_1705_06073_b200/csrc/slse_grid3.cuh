@@ -45,7 +45,7 @@ constexpr int kR3StrideHi = 273, kR3StrideLo = 17;
 constexpr int kR3Buf = 16 * kR3StrideHi;  // 4368 complex
 SLSE_HD constexpr size_t r3_smem_bytes() { return 16 * (size_t)kR3Buf; }
 #ifndef SLSE_R3_MINB
-#define SLSE_R3_MINB 3
+#define SLSE_R3_MINB 2  // 128 registers: 3 CTAs at 80 registers spill (cfg3 shape 0.48 vs 0.585 of HBM)
 #endif
 
 // pruned DFT16: inputs x0..x3 at n2 = 0..3, zero beyond; A[r + 4 k] for the
@@ -75,7 +75,50 @@ SLSE_D void r3_chain_twiddles(cplx* v, cplx base, cplx step) {
   }
 }
 
-// MODE 0: R = 1 pruned (N <= 1024);  MODE 1: R >= 4, J = R / 4 folds
+// v[t] *= w^t, t = 1..15, from w and w^2 (two interleaved chains)
+SLSE_D void r3_pow_twiddles(cplx* v, cplx wa, cplx wa2) {
+  cplx pe = wa2, po = wa;
+  v[1] = cmul(v[1], wa);
+#pragma unroll
+  for (int tt = 2; tt < 16; tt += 2) {
+    if (tt > 2) pe = cmul(pe, wa2);
+    po = cmul(po, wa2);
+    v[tt] = cmul(v[tt], pe);
+    v[tt + 1] = cmul(v[tt + 1], po);
+  }
+}
+
+// SLSE_R3_TWREG: 0 = the two table entries of each pass's twiddle chain are
+// loaded before the barrier that precedes the pass (their latency hides
+// behind the barrier); 1 = they stay in registers for the kernel's lifetime;
+// 2 = all 15 + 15 twiddles stay in registers (no chains).
+// Measured (B200, 2 CTAs per SM): pruned mode 1 (cfg3 shape 0.585 of HBM vs
+// 0.552 with 0, 0.421 with 2: spills); dense mode 0 (1 spills there).
+#ifndef SLSE_R3_TWREG_PRUNED
+#define SLSE_R3_TWREG_PRUNED 1
+#endif
+#ifndef SLSE_R3_TWREG_DENSE
+#define SLSE_R3_TWREG_DENSE 0
+#endif
+// SLSE_R3_PREFETCH: the pruned mode loads the next task's four inputs into
+// registers before pass B of the current task.
+#ifndef SLSE_R3_PREFETCH
+#define SLSE_R3_PREFETCH 1
+#endif
+
+// Streaming (evict-first) stores only when a task writes whole lines (R = 1):
+// with R > 1 a line is completed by the R residue tasks of its problem, and
+// an evict-first partial line leaves L2 before they arrive.
+#ifndef SLSE_R3_STORE
+#define SLSE_R3_STORE 1
+#endif
+template <typename V>
+SLSE_D void r3_store(V* p, V x, int lgR) {
+  if (SLSE_R3_STORE == 0 || (SLSE_R3_STORE == 1 && lgR == 0)) __stcs(p, x);
+  else *p = x;
+}
+
+// MODE 0: R = 1 pruned (N <= 1024);  MODE 1: R >= 1 dense, J = ceil(N / 4096) folds
 template <int MODE>
 __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const cplx* __restrict__ w,
                                                                           const cplx* __restrict__ om_s, int n,
@@ -93,31 +136,56 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
   const long long T = ((long long)B * 2) << lgR;
   const size_t om_stride = 2 * (size_t)n - 1;
   const int J = (n + M - 1) >> 12;
-  // fixed per thread: pass B twiddle step W256^{b}, pass C step W4096^{tid}
+  // fixed per thread: pass B twiddles (W256^{b})^t, pass C twiddles (W4096^{tid})^t
   const cplx* twb = tw + tw_index(b, 8);
   const cplx* twc = tw + tw_index(tid, 12);
+  constexpr int TWR = MODE == 0 ? SLSE_R3_TWREG_PRUNED : SLSE_R3_TWREG_DENSE;
+  cplx wb1, wb2, wc1, wc2;
+  if (TWR == 1) {
+    wb1 = ldg_c(twb), wb2 = ldg_c(twb + b), wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+  }
+  cplx tB[16], tC[16];
+  if (TWR == 2) {
+#pragma unroll
+    for (int t = 1; t < 16; ++t) {
+      tB[t] = ldg_c(tw + tw_index((b * t) & 255, 8));
+      tC[t] = ldg_c(tw + tw_index(tid * t, 12));
+    }
+  }
   int sP = kR3StrideHi, sQ = kR3StrideLo;
+
+  const auto row_of = [&](long long task) {
+    const int sig = (int)(task >> lgR) & 1;
+    const int p = (int)(task >> (lgR + 1));
+    return sig ? om_s + (size_t)p * om_stride + (n - 1) : w + (size_t)p * n;
+  };
+  cplx xn[4];  // pruned mode: the next task's raw inputs
+  if (MODE == 0 && SLSE_R3_PREFETCH && (long long)blockIdx.x < T) {
+    const cplx* src = row_of(blockIdx.x);
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) xn[n2] = tid + 256 * n2 < n ? ldg_c(src + tid + 256 * n2) : mk(0.0, 0.0);
+  }
 
   for (long long task = blockIdx.x; task < T; task += gridDim.x) {
     const int r = (int)(task & (R - 1));
     const int sig = (int)(task >> lgR) & 1;
     const int p = (int)(task >> (lgR + 1));
-    const cplx* src = sig ? om_s + (size_t)p * om_stride + (n - 1) : w + (size_t)p * n;
+    const cplx* src = row_of(task);
     cplx v[16];
     // ---- pass A
     // signal 1 is conj d, d_0 = om_s(0), d_m = 2 om_s(m)
-    const auto ld = [&](int m) {
-      cplx xv = m < n ? ldg_c(src + m) : mk(0.0, 0.0);
+    const auto fix = [&](cplx xv, int m) {
       if (sig) {
         const double f = m ? 2.0 : 1.0;
         xv = mk(f * xv.re, -f * xv.im);
       }
       return xv;
     };
+    const auto ld = [&](int m) { return fix(m < n ? ldg_c(src + m) : mk(0.0, 0.0), m); };
     if (MODE == 0) {
       cplx x[4];
 #pragma unroll
-      for (int n2 = 0; n2 < 4; ++n2) x[n2] = ld(tid + 256 * n2);
+      for (int n2 = 0; n2 < 4; ++n2) x[n2] = SLSE_R3_PREFETCH ? fix(xn[n2], tid + 256 * n2) : ld(tid + 256 * n2);
       r3_pruned4<0>(x, v);
       r3_pruned4<1>(x, v);
       r3_pruned4<2>(x, v);
@@ -125,6 +193,11 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
       // v[k0] = A(k0)
 #pragma unroll
       for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[k0];
+      if (SLSE_R3_PREFETCH && task + gridDim.x < T) {
+        const cplx* nsrc = row_of(task + gridDim.x);
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) xn[n2] = tid + 256 * n2 < n ? ldg_c(nsrc + tid + 256 * n2) : mk(0.0, 0.0);
+      }
     } else {
 #pragma unroll
       for (int n2 = 0; n2 < 16; ++n2) v[n2] = ld(tid + 256 * n2);
@@ -143,17 +216,24 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
 #pragma unroll
       for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[g5_pos(k0)];
     }
+    if (TWR == 0) wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
     __syncthreads();
     // ---- pass B: thread (n0 = a, k0 = b)
     {
       cplx* row = X + b * sP + a * sQ;
 #pragma unroll
       for (int n1 = 0; n1 < 16; ++n1) v[n1] = row[n1];
-      g5_outer_twiddles(v, twb, b);
+      if (TWR == 2) {
+#pragma unroll
+        for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], tB[t]);
+      } else {
+        r3_pow_twiddles(v, wb1, wb2);
+      }
       dft16_t<0>(v);
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) row[k1] = v[g5_pos(k1)];
     }
+    if (TWR == 0) wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
     __syncthreads();
     // ---- pass C: thread (k0 = a, k1 = b)
     {
@@ -161,23 +241,196 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
 #pragma unroll
       for (int n0 = 0; n0 < 16; ++n0) v[n0] = col[n0 * sQ];
     }
-    g5_outer_twiddles(v, twc, tid);
+    if (TWR == 2) {
+#pragma unroll
+      for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], tC[t]);
+    } else {
+      r3_pow_twiddles(v, wc1, wc2);
+    }
     dft16_t<0>(v);
     if (sig == 0) {
       double2* qg = (double2*)(q_grid + (size_t)p * L) + r + ((size_t)tid << lgR);
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) {
         const cplx o = v[g5_pos(k2)];
-        __stcs(&qg[(size_t)(256 * k2) << lgR], make_double2(o.re, o.im));
+        r3_store(&qg[(size_t)(256 * k2) << lgR], make_double2(o.re, o.im), lgR);
       }
     } else {
       double* sg = s_grid + (size_t)p * L + r + ((size_t)tid << lgR);
 #pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) __stcs(&sg[(size_t)(256 * k2) << lgR], v[g5_pos(k2)].re);
+      for (int k2 = 0; k2 < 16; ++k2) r3_store(&sg[(size_t)(256 * k2) << lgR], v[g5_pos(k2)].re, lgR);
     }
     const int tmp = sP;
     sP = sQ;
     sQ = tmp;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Residue PAIRS for L >= 16384, N <= L / 4 (cfg4 / cfg5 shapes).  A residue
+// task above writes 16-byte (q^G) or 8-byte (s^G) pieces at stride 16 R
+// bytes: partial 32-byte sectors.  Every partial piece costs a whole sector
+// on the SM -> L2 path and a sector operation in L2, and L2 completes evicted
+// partial sectors by read-modify-write against DRAM (ncu at the cfg4 shape:
+// DRAM reads 4.3x, writes 1.7x the algorithmic bytes).  Here one task is a
+// PAIR of residues r = 2 pair, r + 1 of a problem, and every store is one
+// whole 32-byte sector (bins r, r + 1 of one m; STG.256).
+//
+// s^G additionally runs at HALF length: with h_k = conj om_s(k) (all |k| < N)
+//   s_l = sum_k h_k W_L^{k l},   z_m = s_{2m} + i s_{2m+1} = FFT_{L/2}(g)[m],
+//   g[k mod L/2] = h_k (1 + i W_L^k),
+// (2N - 1 <= L / 2, no aliasing), a complex transform of L / 2 points whose
+// output IS the s^G row (re, im interleaved = consecutive doubles): R / 4
+// pair tasks instead of R / 2, their 32-byte pieces at stride 16 R bytes
+// like q^G's pairs (contiguous rows at cfg4, where R / 2 = 2).
+//
+// The pair runs SEQUENTIALLY in one 256-thread CTA: residue r, whose 16
+// outputs per thread are parked (10 in shared memory, 6 in registers), then
+// residue r + 1, then the stores.  Two CTAs per SM (110.8 KB each) overlap
+// each other's barriers and loads.  (A lock-step variant -- 512 threads,
+// lanes 0-15 / 16-31 of every warp on the two residues, outputs paired by
+// shuffle -- measured the same 0.28 of HBM at the cfg4 shape as this one
+// before the 32-byte stores, with one CTA per SM and nothing to overlap its
+// load latency; removed.)
+// one 32-byte store (sm_100: STG.256), p 32-byte aligned
+SLSE_D void r3_store32(double2* p, cplx lo, cplx hi) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(lo.re), "d"(lo.im), "d"(hi.re), "d"(hi.im)
+               : "memory");
+}
+// L2 prefetch of `bytes` (multiple of 16) at a 16-byte aligned address
+SLSE_D void r3_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+#ifndef SLSE_R3_L2PF
+#define SLSE_R3_L2PF 1
+#endif
+constexpr int kR3SaveSmem = 10;  // outputs per thread parked in shared memory
+SLSE_HD constexpr size_t r3s_smem_bytes() { return 16 * ((size_t)kR3Buf + kR3SaveSmem * kR3Threads); }
+
+__global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __restrict__ w,
+                                                                 const cplx* __restrict__ om_s, int n, int lgL, int B,
+                                                                 cplx* __restrict__ q_grid, double* __restrict__ s_grid,
+                                                                 const cplx* __restrict__ tw) {
+  constexpr int M = 4096;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* X = (cplx*)smem_raw;
+  cplx* S = X + kR3Buf;
+  const int tid = threadIdx.x;
+  const int a = tid & 15, b = tid >> 4;
+  const int lgR = lgL - 12;
+  const int R = 1 << lgR;
+  const size_t L = (size_t)1 << lgL;
+  const int TPq = R >> 1, TP = TPq + (R >> 2);
+  const long long T = (long long)B * TP;
+  const size_t om_stride = 2 * (size_t)n - 1;
+  const int Jq = (n + M - 1) >> 12;
+  const cplx* twb = tw + tw_index(b, 8);
+  const cplx* twc = tw + tw_index(tid, 12);
+  const cplx* twL = tw + tw_index(0, lgL);
+  const cplx wg = ldg_c(twL + tid);  // W_L^{tid}
+  int sP = kR3StrideHi, sQ = kR3StrideLo;
+  int p = (int)(blockIdx.x / TP), t = (int)(blockIdx.x - (long long)p * TP);
+  const int dp = (int)(gridDim.x / TP), dt = (int)(gridDim.x - (long long)dp * TP);
+
+  for (long long task = blockIdx.x; task < T; task += gridDim.x) {
+    const int sig = t >= TPq;
+    const int pair = sig ? t - TPq : t;
+    const int lgLe = lgL - sig, lgRe = lgLe - 12;
+    const int Re = 1 << lgRe;
+    const int Le = 1 << lgLe;
+    const cplx* src = sig ? om_s + (size_t)p * om_stride + (n - 1) : w + (size_t)p * n;
+    const int J = sig ? Re : Jq;
+    if (SLSE_R3_L2PF && task + gridDim.x < T) {
+      // the next task's input row towards L2 (16 KB pieces, one per thread)
+      int pn = p + dp, tn = t + dt;
+      if (tn >= TP) tn -= TP, ++pn;
+      const cplx* nsrc = tn >= TPq ? om_s + (size_t)pn * om_stride + (n - 1) : w + (size_t)pn * n;
+      const int piece = tid << 10;
+      if (piece < n) r3_prefetch_l2(nsrc + piece, 16u * (unsigned)(n - piece < 1024 ? n - piece : 1024));
+    }
+    // element kap of the length-Le input: w (zero past n), or g.  W_L^k comes
+    // from the thread's W_L^{tid} times a warp-uniform table entry:
+    // k = kap: W_L^{kap - tid} W_L^{tid};  k = Le - kap: W_L^{k + tid} conj W_L^{tid}
+    const auto ld = [&](int kap) {
+      if (!sig) return kap < n ? ldg_c(src + kap) : mk(0.0, 0.0);
+      const bool pos = kap < n;
+      const int k = pos ? kap : Le - kap;
+      if (k >= n) return mk(0.0, 0.0);
+      const cplx o = ldg_c(src + k), U = ldg_c(twL + (pos ? kap - tid : k + tid));
+      const cplx W = pos ? cmul(U, wg) : cmulc(U, wg);
+      // k = kap: conj(om) (1 + i W);  k = Le - kap: om (1 + i conj W)
+      const double ur = pos ? 1.0 - W.im : 1.0 + W.im;
+      const double oi = pos ? -o.im : o.im;
+      return mk(o.re * ur - oi * W.re, o.re * W.re + oi * ur);
+    };
+    cplx sv[16 - kR3SaveSmem];
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int r = 2 * pair + h;
+      cplx v[16];
+#pragma unroll
+      for (int n2 = 0; n2 < 16; ++n2) v[n2] = ld(tid + 256 * n2);
+      for (int j = 1; j < J; ++j) {
+        const cplx tj = ldg_c(tw + tw_index((j * r) & (Re - 1), lgRe));  // W_Re^{j r}
+#pragma unroll
+        for (int n2 = 0; n2 < 16; ++n2) v[n2] = cadd(v[n2], cmul(ld(tid + 256 * n2 + (j << 12)), tj));
+      }
+      if (r) {
+        const cplx base = ldg_c(tw + tw_index(tid * r, lgLe));
+        const cplx step = ldg_c(tw + tw_index(r, lgLe - 8));
+        r3_chain_twiddles(v, base, step);
+      }
+      dft16_t<0>(v);
+#pragma unroll
+      for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[g5_pos(k0)];
+      const cplx wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
+      __syncthreads();
+      {
+        cplx* row = X + b * sP + a * sQ;
+#pragma unroll
+        for (int n1 = 0; n1 < 16; ++n1) v[n1] = row[n1];
+        r3_pow_twiddles(v, wb1, wb2);
+        dft16_t<0>(v);
+#pragma unroll
+        for (int k1 = 0; k1 < 16; ++k1) row[k1] = v[g5_pos(k1)];
+      }
+      const cplx wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+      __syncthreads();
+      {
+        const cplx* col = X + a * sP + b;
+#pragma unroll
+        for (int n0 = 0; n0 < 16; ++n0) v[n0] = col[n0 * sQ];
+      }
+      r3_pow_twiddles(v, wc1, wc2);
+      dft16_t<0>(v);
+      if (h == 0) {
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+          if (k2 < kR3SaveSmem) S[k2 * kR3Threads + tid] = v[g5_pos(k2)];
+          else sv[k2 - kR3SaveSmem] = v[g5_pos(k2)];
+        }
+      } else {
+        // bins l = 2 pair + {0, 1} + Re m, m = tid + 256 k2, in 16-byte units
+        double2* out = sig ? (double2*)(s_grid + (size_t)p * L) : (double2*)(q_grid + (size_t)p * L);
+        out += 2 * pair + ((size_t)tid << lgRe);
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+          const cplx lo = k2 < kR3SaveSmem ? S[k2 * kR3Threads + tid] : sv[k2 < kR3SaveSmem ? 0 : k2 - kR3SaveSmem];
+          const cplx hi = v[g5_pos(k2)];
+          double2* dst = out + ((size_t)(256 * k2) << lgRe);
+          r3_store32(dst, lo, hi);
+        }
+      }
+      const int tmp = sP;
+      sP = sQ;
+      sQ = tmp;
+    }
+    p += dp;
+    t += dt;
+    if (t >= TP) {
+      t -= TP;
+      ++p;
+    }
   }
 }
 

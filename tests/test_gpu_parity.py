@@ -418,7 +418,13 @@ def test_grid_eval_omega_against_reference(cfg, b, state):
                                    # every residue-kernel M (2^4 .. 2^11), folds, ragged N, the direct kernel
                                    (2, 4, 3), (2, 8, 3), (4, 8, 2), (3, 16, 4), (17, 64, 5), (64, 256, 9), (100, 512, 6),
                                    (128, 1024, 4), (257, 1024, 3), (256, 2048, 7), (1000, 4096, 3),
-                                   (2048, 8192, 5), (3000, 16384, 4), (4096, 16384, 300), (16384, 65536, 2)])
+                                   (2048, 8192, 5), (3000, 16384, 4), (4096, 16384, 300), (16384, 65536, 2),
+                                   # register-transform kernels (slse_grid3.cuh): pruned / dense, several tasks
+                                   # per CTA (the exchange layout alternates), folds, residue pairs, ragged N,
+                                   # 4N > L (no half-length s^G)
+                                   (1024, 4096, 700), (513, 4096, 3), (1500, 4096, 5), (2048, 4096, 2),
+                                   (2048, 8192, 400), (4096, 8192, 3), (5000, 16384, 3), (8192, 16384, 2),
+                                   (9000, 65536, 3), (16384, 65536, 30), (20000, 65536, 2), (32768, 131072, 2)])
 def test_grid_eval_omega_shapes_against_fft(n, L, B):
     """Row 9 coefficient form on every kernel family vs the reference's
     literal formula in numpy (q^G = fft(w, L), s^G = L ifft(buf).real with
