@@ -256,7 +256,7 @@ def _grid_form(torch, dev, stream, flush, n, L, B, form, launches):
         del om
         if L == 1024 and 128 < n <= 256:
             kname = "grid_coef_kernel"
-        elif 16384 <= L <= 32768 and 4 * n <= L:
+        elif L >= 16384 and 4 * n <= L:
             kname = "grid_r3s_kernel"  # residue pairs of 4096-point register transforms, s^G at half length
         elif L >= 4096:
             kname = "grid_r3_kernel"   # 4096-point register transforms (three DFT16 passes)

@@ -12,6 +12,9 @@
 #include "slse_kernels.cuh"
 #include "slse_grid.cuh"
 #include "slse_grid3.cuh"
+#ifndef SLSE_R3S_MAXLG
+#define SLSE_R3S_MAXLG 30
+#endif
 
 #include <cstdlib>
 
@@ -622,7 +625,7 @@ int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int 
     return e == cudaSuccess ? 0 : fail("grid_coef_kernel", e);
   }
   const int lgL = ilog2(L);
-  if (lgL >= 14 && lgL <= 15 && 4LL * N <= L && !slse_knob("SLSE_GRID_NO_R3P")) {
+  if (lgL >= 14 && lgL <= SLSE_R3S_MAXLG && 4LL * N <= L && !slse_knob("SLSE_GRID_NO_R3P")) {
     // residue pairs (whole-sector stores), s^G at half length (slse_grid3.cuh).  From L = 65536 the
     // folds (4 for q^G, 8 for the half-length s^G, re-read per residue) outweigh the store savings:
     // cfg5 shape 1.82 ms here vs 1.40 ms on the single-residue tasks below.

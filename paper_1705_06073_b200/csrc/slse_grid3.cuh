@@ -328,6 +328,7 @@ __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __r
   const cplx* twc = tw + tw_index(tid, 12);
   const cplx* twL = tw + tw_index(0, lgL);
   const cplx wg = ldg_c(twL + tid);  // W_L^{tid}
+  const cplx w256 = ldg_c(twL + 256);
   int sP = kR3StrideHi, sQ = kR3StrideLo;
   int p = (int)(blockIdx.x / TP), t = (int)(blockIdx.x - (long long)p * TP);
   const int dp = (int)(gridDim.x / TP), dt = (int)(gridDim.x - (long long)dp * TP);
@@ -348,34 +349,60 @@ __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __r
       const int piece = tid << 10;
       if (piece < n) r3_prefetch_l2(nsrc + piece, 16u * (unsigned)(n - piece < 1024 ? n - piece : 1024));
     }
-    // element kap of the length-Le input: w (zero past n), or g.  W_L^k comes
-    // from the thread's W_L^{tid} times a warp-uniform table entry:
-    // k = kap: W_L^{kap - tid} W_L^{tid};  k = Le - kap: W_L^{k + tid} conj W_L^{tid}
-    const auto ld = [&](int kap) {
-      if (!sig) return kap < n ? ldg_c(src + kap) : mk(0.0, 0.0);
-      const bool pos = kap < n;
-      const int k = pos ? kap : Le - kap;
-      if (k >= n) return mk(0.0, 0.0);
-      const cplx o = ldg_c(src + k), U = ldg_c(twL + (pos ? kap - tid : k + tid));
-      const cplx W = pos ? cmul(U, wg) : cmulc(U, wg);
-      // k = kap: conj(om) (1 + i W);  k = Le - kap: om (1 + i conj W)
-      const double ur = pos ? 1.0 - W.im : 1.0 + W.im;
-      const double oi = pos ? -o.im : o.im;
-      return mk(o.re * ur - oi * W.re, o.re * W.re + oi * ur);
+    // fold j of the length-Le input at i = tid + 256 n2, n2 = 8 h8 .. 8 h8 + 7:
+    // w (zero past n), or g.  A fold of g lies wholly on one side (Le / 2 is
+    // a multiple of M): kap = i + j M < n (k = kap) or k = Le - kap.  Eight
+    // loads are issued before the arithmetic; W_L^k runs as a chain from
+    // W_L^{tid} (wg) times a uniform table entry, step W_L^{+-256}.
+    const auto load_fold = [&](int j, int h8, cplx* x) {
+      const int kap0 = tid + 2048 * h8 + (j << 12);
+      if (!sig) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = kap0 + 256 * u < n ? ldg_c(src + kap0 + 256 * u) : mk(0.0, 0.0);
+        return;
+      }
+      const bool pos = (j << 12) < n;
+      const int k0 = pos ? kap0 : Le - kap0, dk = pos ? 256 : -256;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + dk * u;
+        x[u] = ldg_c(src + (k < n ? k : 0));
+      }
+      const double sg = pos ? 1.0 : -1.0;
+      // W_L^{k0} = W_L^{k0 -+ tid} (W_L^{tid})^{+-1}
+      cplx W = cmul(ldg_c(twL + (pos ? kap0 - tid : k0 + tid)), mk(wg.re, sg * wg.im));
+      const cplx st = mk(w256.re, sg * w256.im);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        // k = kap: conj(om) (1 + i W);  k = Le - kap: om (1 + i conj W)
+        const double ur = 1.0 - sg * W.im, oi = -sg * x[u].im, orr = x[u].re;
+        x[u] = k0 + dk * u < n ? mk(orr * ur - oi * W.re, orr * W.re + oi * ur) : mk(0.0, 0.0);
+        W = cmul(W, st);
+      }
     };
+    // (Both residues' pass A from ONE pass over the input -- the second one's
+    // outputs parked in S / sv until the first one's pass C has read the
+    // buffer -- measured no faster: 550 vs 542 us at the cfg4 shape, 1100 vs
+    // 1016 us at cfg5; its two accumulators spill.)
     cplx sv[16 - kR3SaveSmem];
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       const int r = 2 * pair + h;
       cplx v[16];
-#pragma unroll
-      for (int n2 = 0; n2 < 16; ++n2) v[n2] = ld(tid + 256 * n2);
+      load_fold(0, 0, v);
+      load_fold(0, 1, v + 8);
       for (int j = 1; j < J; ++j) {
         const cplx tj = ldg_c(tw + tw_index((j * r) & (Re - 1), lgRe));  // W_Re^{j r}
 #pragma unroll
-        for (int n2 = 0; n2 < 16; ++n2) v[n2] = cadd(v[n2], cmul(ld(tid + 256 * n2 + (j << 12)), tj));
+        for (int h8 = 0; h8 < 2; ++h8) {
+          cplx x[8];
+          load_fold(j, h8, x);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[8 * h8 + u] = cadd(v[8 * h8 + u], cmul(x[u], tj));
+        }
       }
       if (r) {
+        // W_Le^{(tid + 256 n2) r} = W_Le^{tid r} (W_{Le/256}^{r})^{n2}
         const cplx base = ldg_c(tw + tw_index(tid * r, lgLe));
         const cplx step = ldg_c(tw + tw_index(r, lgLe - 8));
         r3_chain_twiddles(v, base, step);
@@ -417,8 +444,7 @@ __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __r
         for (int k2 = 0; k2 < 16; ++k2) {
           const cplx lo = k2 < kR3SaveSmem ? S[k2 * kR3Threads + tid] : sv[k2 < kR3SaveSmem ? 0 : k2 - kR3SaveSmem];
           const cplx hi = v[g5_pos(k2)];
-          double2* dst = out + ((size_t)(256 * k2) << lgRe);
-          r3_store32(dst, lo, hi);
+          r3_store32(out + ((size_t)(256 * k2) << lgRe), lo, hi);
         }
       }
       const int tmp = sP;
