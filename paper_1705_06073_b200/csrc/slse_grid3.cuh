@@ -60,21 +60,6 @@ SLSE_D void r3_pruned4(const cplx* x, cplx* v) {
   v[R16 + 12] = d;
 }
 
-// v[t] *= base * step^t, t = 0..15 (two interleaved chains)
-SLSE_D void r3_chain_twiddles(cplx* v, cplx base, cplx step) {
-  const cplx step2 = cmul(step, step);
-  cplx pe = base, po = cmul(base, step);
-  v[0] = cmul(v[0], pe);
-  v[1] = cmul(v[1], po);
-#pragma unroll
-  for (int t = 2; t < 16; t += 2) {
-    pe = cmul(pe, step2);
-    po = cmul(po, step2);
-    v[t] = cmul(v[t], pe);
-    v[t + 1] = cmul(v[t + 1], po);
-  }
-}
-
 // v[t] *= w^t, t = 1..15, from w and w^2 (two interleaved chains)
 SLSE_D void r3_pow_twiddles(cplx* v, cplx wa, cplx wa2) {
   cplx pe = wa2, po = wa;
@@ -85,6 +70,31 @@ SLSE_D void r3_pow_twiddles(cplx* v, cplx wa, cplx wa2) {
     po = cmul(po, wa2);
     v[tt] = cmul(v[tt], pe);
     v[tt + 1] = cmul(v[tt + 1], po);
+  }
+}
+
+// Residue pre-twiddle W_Le^{i r}, i = n0 + 16 n1 + 256 n2, folded into the
+// three passes at no per-element cost:
+//   n2: (W_{Le/256}^r)^{n2} is W64^{n2 e}, e = 16384 r / Le, whenever that is
+//       an integer below 4 (every cfg4 task, a quarter of cfg5's): dft16_t<e>
+//       carries it in its compile-time twiddles; otherwise a chain;
+//   n1: (W_{Le/16}^r)^{n1} joins pass B's chain: its step W256^{k0} is
+//       multiplied by W_{Le/16}^r once;
+//   n0: (W_Le^r)^{n0} joins pass C's chain the same way.
+SLSE_D void r3_pass_a_dft(cplx* v, int r, int lgLe, const cplx* __restrict__ tw) {
+  const int num = r << 14;
+  const int e = num >> lgLe;
+  if ((num & ((1 << lgLe) - 1)) == 0 && e < 4) {
+    switch (e) {
+      case 0: dft16_t<0>(v); break;
+      case 1: dft16_t<1>(v); break;
+      case 2: dft16_t<2>(v); break;
+      default: dft16_t<3>(v); break;
+    }
+  } else {
+    const cplx step = ldg_c(tw + tw_index(r, lgLe - 8));
+    r3_pow_twiddles(v, step, cmul(step, step));
+    dft16_t<0>(v);
   }
 }
 
@@ -140,6 +150,7 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
   const cplx* twb = tw + tw_index(b, 8);
   const cplx* twc = tw + tw_index(tid, 12);
   constexpr int TWR = MODE == 0 ? SLSE_R3_TWREG_PRUNED : SLSE_R3_TWREG_DENSE;
+  static_assert(MODE == 0 || TWR == 0, "the dense mode rewrites the chain steps per task");
   cplx wb1, wb2, wc1, wc2;
   if (TWR == 1) {
     wb1 = ldg_c(twb), wb2 = ldg_c(twb + b), wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
@@ -206,17 +217,15 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
 #pragma unroll
         for (int n2 = 0; n2 < 16; ++n2) v[n2] = cadd(v[n2], cmul(ld(tid + 256 * n2 + (j << 12)), t));
       }
-      if (r) {
-        // W_L^{(tid + 256 n2) r} = W_L^{tid r} (W_{L/256}^{r})^{n2}
-        const cplx base = ldg_c(tw + tw_index(tid * r, lgL));
-        const cplx step = ldg_c(tw + tw_index(r, lgL - 8));
-        r3_chain_twiddles(v, base, step);
-      }
-      dft16_t<0>(v);
+      r3_pass_a_dft(v, r, lgL, tw);
 #pragma unroll
       for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[g5_pos(k0)];
     }
     if (TWR == 0) wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
+    if (MODE == 1 && r) {  // the residue pre-twiddle's n1 part (r3_pass_a_dft)
+      wb1 = cmul(ldg_c(twb), ldg_c(tw + tw_index(r, lgL - 4)));
+      wb2 = cmul(wb1, wb1);
+    }
     __syncthreads();
     // ---- pass B: thread (n0 = a, k0 = b)
     {
@@ -234,6 +243,10 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
       for (int k1 = 0; k1 < 16; ++k1) row[k1] = v[g5_pos(k1)];
     }
     if (TWR == 0) wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+    if (MODE == 1 && r) {
+      wc1 = cmul(ldg_c(twc), ldg_c(tw + tw_index(r, lgL)));
+      wc2 = cmul(wc1, wc1);
+    }
     __syncthreads();
     // ---- pass C: thread (k0 = a, k1 = b)
     {
@@ -401,16 +414,14 @@ __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __r
           for (int u = 0; u < 8; ++u) v[8 * h8 + u] = cadd(v[8 * h8 + u], cmul(x[u], tj));
         }
       }
-      if (r) {
-        // W_Le^{(tid + 256 n2) r} = W_Le^{tid r} (W_{Le/256}^{r})^{n2}
-        const cplx base = ldg_c(tw + tw_index(tid * r, lgLe));
-        const cplx step = ldg_c(tw + tw_index(r, lgLe - 8));
-        r3_chain_twiddles(v, base, step);
-      }
-      dft16_t<0>(v);
+      r3_pass_a_dft(v, r, lgLe, tw);
 #pragma unroll
       for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[g5_pos(k0)];
-      const cplx wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
+      cplx wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
+      if (r) {
+        wb1 = cmul(wb1, ldg_c(tw + tw_index(r, lgLe - 4)));
+        wb2 = cmul(wb1, wb1);
+      }
       __syncthreads();
       {
         cplx* row = X + b * sP + a * sQ;
@@ -421,7 +432,11 @@ __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __r
 #pragma unroll
         for (int k1 = 0; k1 < 16; ++k1) row[k1] = v[g5_pos(k1)];
       }
-      const cplx wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+      cplx wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+      if (r) {
+        wc1 = cmul(wc1, ldg_c(tw + tw_index(r, lgLe)));
+        wc2 = cmul(wc1, wc1);
+      }
       __syncthreads();
       {
         const cplx* col = X + a * sP + b;
