@@ -258,8 +258,10 @@ def _grid_form(torch, dev, stream, flush, n, L, B, form, launches):
             kname = "grid_coef_kernel"
         elif L >= 16384 and 4 * n <= L:
             kname = "grid_r3s_kernel"  # residue pairs of 4096-point register transforms, s^G at half length
+        elif L == 4096 and n <= 1024:
+            kname = "grid_r3c_kernel"  # pruned 4096-point register transforms, s^G of two problems per transform
         elif L >= 4096:
-            kname = "grid_r3_kernel"   # 4096-point register transforms (three DFT16 passes)
+            kname = "grid_r3_kernel"   # dense 4096-point register transforms (three DFT16 passes)
         else:
             kname = "grid_res_kernel<omega>"
     else:

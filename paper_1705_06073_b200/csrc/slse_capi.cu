@@ -645,26 +645,39 @@ int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int 
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : fail("grid_r3s_kernel", e);
   }
-  if (lgL >= 12 && !slse_knob("SLSE_GRID_NO_R3")) {
-    // register transforms of 4096 points per (problem, signal, residue) task (slse_grid3.cuh)
-    const bool pruned = lgL == 12 && N <= 1024;
-    const void* fn = pruned ? (const void*)grid_r3_kernel<0> : (const void*)grid_r3_kernel<1>;
+  if (lgL == 12 && N <= 1024 && !slse_knob("SLSE_GRID_NO_R3C")) {
+    // cfg3 shape: pruned 4096-point register transforms, s^G of two problems per transform
     const size_t smem = r3_smem_bytes();
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = set_smem(grid_r3c_kernel, smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+      e = cudaFuncSetAttribute(grid_r3c_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
     int occ = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kR3Threads, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_r3c_kernel, kR3Threads, smem);
+    if (e != cudaSuccess || occ < 1) return fail("grid_r3c_kernel setup", e);
+    long long g = (long long)sm_count() * occ;
+    const long long tasks = 3LL * ((B + 1) / 2);
+    if (g > tasks) g = tasks;
+    grid_r3c_kernel<<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, B, (cplx*)q_grid, s_grid,
+                                                      tw);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : fail("grid_r3c_kernel", e);
+  }
+  if (lgL >= 12 && !slse_knob("SLSE_GRID_NO_R3")) {
+    // dense 4096-point register transforms per (problem, signal, residue) task (slse_grid3.cuh)
+    const size_t smem = r3_smem_bytes();
+    e = set_smem(grid_r3_kernel, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_r3_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
+    int occ = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_r3_kernel, kR3Threads, smem);
     if (e != cudaSuccess || occ < 1) return fail("grid_r3_kernel setup", e);
     long long g = (long long)sm_count() * occ;
     const long long tasks = ((long long)B * 2) << (lgL - 12);
     if (g > tasks) g = tasks;
-    if (pruned)
-      grid_r3_kernel<0><<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL, B, (cplx*)q_grid,
-                                                          s_grid, tw);
-    else
-      grid_r3_kernel<1><<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL, B, (cplx*)q_grid,
-                                                          s_grid, tw);
+    grid_r3_kernel<<<(int)g, kR3Threads, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, lgL, B, (cplx*)q_grid,
+                                                     s_grid, tw);
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : fail("grid_r3_kernel", e);
   }

@@ -10,13 +10,14 @@
 // N <= L / 4 point signal is R independent M-point transforms
 //   X[r + R m] = sum_{i<M} z_r(i) W_M^{i m},
 //   z_r(i)     = W_L^{i r} sum_{j : i + j M < N} x_{i + j M} W_R^{j r}.
-// One task = (problem, signal, residue); tasks are problem-major so the R
-// residue tasks that interleave into one problem's output rows run at the
-// same time on neighbouring CTAs and their partial sectors merge in L2.
-//   R = 1  (cfg3, N <= 1024): z = x, zero past M / 4: the first pass is four
-//          radix-4 butterflies per thread (pruned DFT16);
-//   R = 4  (cfg4, N <= 4096): z_r(i) = W_L^{i r} x_i, no fold;
-//   R = 16 (cfg5, N <= 16384): four folds.
+// Three kernels share the transform below:
+//   grid_r3c_kernel  L = 4096, N <= 1024 (cfg3): R = 1, z = x, zero past
+//                    M / 4: the first pass is four radix-4 butterflies per
+//                    thread (pruned DFT16); s^G of TWO problems per transform;
+//   grid_r3s_kernel  L >= 16384, N <= L / 4 (cfg4, cfg5): tasks are residue
+//                    PAIRS stored as whole 32-byte sectors, s^G at half length;
+//   grid_r3_kernel   every other L >= 4096 shape: one (problem, signal,
+//                    residue) per task, dense input, J = ceil(N / M) folds.
 //
 // The M-point transform, i = n0 + 16 n1 + 256 n2, m = k0 + 16 k1 + 256 k2:
 //   pass A  thread (n0, n1): DFT16 over n2            -> A(n0, n1, k0)
@@ -25,8 +26,7 @@
 // so the loads (i = tid + 256 n2) and the stores (m = tid + 256 k2) are
 // coalesced, 16 bytes per lane.  256 threads; every thread holds 16 points.
 //
-// Exchanges are in place in ONE 4368-complex buffer (69.9 KB: three CTAs per
-// SM), slot (p, q, x) = p sP + q sQ + x:
+// Exchanges are in place in ONE 4368-complex buffer (69.9 KB), slot (p, q, x) = p sP + q sQ + x:
 //   A writes (k0, n0, n1);  B reads (k0, n0, *) and overwrites its own 16
 //   slots with its outputs (k0, n0, k1);  C reads (k0, *, k1);
 // the NEXT task's pass A of the same thread then writes exactly the slots
@@ -98,38 +98,20 @@ SLSE_D void r3_pass_a_dft(cplx* v, int r, int lgLe, const cplx* __restrict__ tw)
   }
 }
 
-// SLSE_R3_TWREG: 0 = the two table entries of each pass's twiddle chain are
-// loaded before the barrier that precedes the pass (their latency hides
-// behind the barrier); 1 = they stay in registers for the kernel's lifetime;
-// 2 = all 15 + 15 twiddles stay in registers (no chains).
-// Measured (B200, 2 CTAs per SM): pruned mode 1 (cfg3 shape 0.585 of HBM vs
-// 0.552 with 0, 0.421 with 2: spills); dense mode 0 (1 spills there).
-#ifndef SLSE_R3_TWREG_PRUNED
-#define SLSE_R3_TWREG_PRUNED 1
-#endif
-#ifndef SLSE_R3_TWREG_DENSE
-#define SLSE_R3_TWREG_DENSE 0
-#endif
-// SLSE_R3_PREFETCH: the pruned mode loads the next task's four inputs into
-// registers before pass B of the current task.
-#ifndef SLSE_R3_PREFETCH
-#define SLSE_R3_PREFETCH 1
-#endif
-
 // Streaming (evict-first) stores only when a task writes whole lines (R = 1):
 // with R > 1 a line is completed by the R residue tasks of its problem, and
 // an evict-first partial line leaves L2 before they arrive.
-#ifndef SLSE_R3_STORE
-#define SLSE_R3_STORE 1
-#endif
 template <typename V>
 SLSE_D void r3_store(V* p, V x, int lgR) {
-  if (SLSE_R3_STORE == 0 || (SLSE_R3_STORE == 1 && lgR == 0)) __stcs(p, x);
+  if (lgR == 0) __stcs(p, x);
   else *p = x;
 }
 
-// MODE 0: R = 1 pruned (N <= 1024);  MODE 1: R >= 1 dense, J = ceil(N / 4096) folds
-template <int MODE>
+// Dense single-residue tasks: any N <= L, L >= 4096 (the shapes the pruned
+// and the pair kernels below do not take: N > L / 4, or L = 4096 / 8192 with
+// N > 1024).  J = ceil(N / 4096) folds.  Two CTAs per SM at 128 registers
+// (three at 80 registers spill).  The two table entries of each pass's
+// twiddle chain are loaded before the barrier that precedes the pass.
 __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const cplx* __restrict__ w,
                                                                           const cplx* __restrict__ om_s, int n,
                                                                           int lgL, int B, cplx* __restrict__ q_grid,
@@ -149,81 +131,36 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
   // fixed per thread: pass B twiddles (W256^{b})^t, pass C twiddles (W4096^{tid})^t
   const cplx* twb = tw + tw_index(b, 8);
   const cplx* twc = tw + tw_index(tid, 12);
-  constexpr int TWR = MODE == 0 ? SLSE_R3_TWREG_PRUNED : SLSE_R3_TWREG_DENSE;
-  static_assert(MODE == 0 || TWR == 0, "the dense mode rewrites the chain steps per task");
-  cplx wb1, wb2, wc1, wc2;
-  if (TWR == 1) {
-    wb1 = ldg_c(twb), wb2 = ldg_c(twb + b), wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
-  }
-  cplx tB[16], tC[16];
-  if (TWR == 2) {
-#pragma unroll
-    for (int t = 1; t < 16; ++t) {
-      tB[t] = ldg_c(tw + tw_index((b * t) & 255, 8));
-      tC[t] = ldg_c(tw + tw_index(tid * t, 12));
-    }
-  }
   int sP = kR3StrideHi, sQ = kR3StrideLo;
-
-  const auto row_of = [&](long long task) {
-    const int sig = (int)(task >> lgR) & 1;
-    const int p = (int)(task >> (lgR + 1));
-    return sig ? om_s + (size_t)p * om_stride + (n - 1) : w + (size_t)p * n;
-  };
-  cplx xn[4];  // pruned mode: the next task's raw inputs
-  if (MODE == 0 && SLSE_R3_PREFETCH && (long long)blockIdx.x < T) {
-    const cplx* src = row_of(blockIdx.x);
-#pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2) xn[n2] = tid + 256 * n2 < n ? ldg_c(src + tid + 256 * n2) : mk(0.0, 0.0);
-  }
 
   for (long long task = blockIdx.x; task < T; task += gridDim.x) {
     const int r = (int)(task & (R - 1));
     const int sig = (int)(task >> lgR) & 1;
     const int p = (int)(task >> (lgR + 1));
-    const cplx* src = row_of(task);
+    const cplx* src = sig ? om_s + (size_t)p * om_stride + (n - 1) : w + (size_t)p * n;
     cplx v[16];
-    // ---- pass A
-    // signal 1 is conj d, d_0 = om_s(0), d_m = 2 om_s(m)
-    const auto fix = [&](cplx xv, int m) {
+    // ---- pass A; signal 1 is conj d, d_0 = om_s(0), d_m = 2 om_s(m)
+    const auto ld = [&](int m) {
+      cplx xv = m < n ? ldg_c(src + m) : mk(0.0, 0.0);
       if (sig) {
         const double f = m ? 2.0 : 1.0;
         xv = mk(f * xv.re, -f * xv.im);
       }
       return xv;
     };
-    const auto ld = [&](int m) { return fix(m < n ? ldg_c(src + m) : mk(0.0, 0.0), m); };
-    if (MODE == 0) {
-      cplx x[4];
 #pragma unroll
-      for (int n2 = 0; n2 < 4; ++n2) x[n2] = SLSE_R3_PREFETCH ? fix(xn[n2], tid + 256 * n2) : ld(tid + 256 * n2);
-      r3_pruned4<0>(x, v);
-      r3_pruned4<1>(x, v);
-      r3_pruned4<2>(x, v);
-      r3_pruned4<3>(x, v);
-      // v[k0] = A(k0)
+    for (int n2 = 0; n2 < 16; ++n2) v[n2] = ld(tid + 256 * n2);
+    for (int j = 1; j < J; ++j) {
+      const cplx t = ldg_c(tw + tw_index((j * r) & (R - 1), lgR));  // W_R^{j r}
 #pragma unroll
-      for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[k0];
-      if (SLSE_R3_PREFETCH && task + gridDim.x < T) {
-        const cplx* nsrc = row_of(task + gridDim.x);
-#pragma unroll
-        for (int n2 = 0; n2 < 4; ++n2) xn[n2] = tid + 256 * n2 < n ? ldg_c(nsrc + tid + 256 * n2) : mk(0.0, 0.0);
-      }
-    } else {
-#pragma unroll
-      for (int n2 = 0; n2 < 16; ++n2) v[n2] = ld(tid + 256 * n2);
-      for (int j = 1; j < J; ++j) {
-        const cplx t = ldg_c(tw + tw_index((j * r) & (R - 1), lgR));  // W_R^{j r}
-#pragma unroll
-        for (int n2 = 0; n2 < 16; ++n2) v[n2] = cadd(v[n2], cmul(ld(tid + 256 * n2 + (j << 12)), t));
-      }
-      r3_pass_a_dft(v, r, lgL, tw);
-#pragma unroll
-      for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[g5_pos(k0)];
+      for (int n2 = 0; n2 < 16; ++n2) v[n2] = cadd(v[n2], cmul(ld(tid + 256 * n2 + (j << 12)), t));
     }
-    if (TWR == 0) wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
-    if (MODE == 1 && r) {  // the residue pre-twiddle's n1 part (r3_pass_a_dft)
-      wb1 = cmul(ldg_c(twb), ldg_c(tw + tw_index(r, lgL - 4)));
+    r3_pass_a_dft(v, r, lgL, tw);
+#pragma unroll
+    for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[g5_pos(k0)];
+    cplx wb1 = ldg_c(twb), wb2 = ldg_c(twb + b);
+    if (r) {  // the residue pre-twiddle's n1 part (r3_pass_a_dft)
+      wb1 = cmul(wb1, ldg_c(tw + tw_index(r, lgL - 4)));
       wb2 = cmul(wb1, wb1);
     }
     __syncthreads();
@@ -232,19 +169,14 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
       cplx* row = X + b * sP + a * sQ;
 #pragma unroll
       for (int n1 = 0; n1 < 16; ++n1) v[n1] = row[n1];
-      if (TWR == 2) {
-#pragma unroll
-        for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], tB[t]);
-      } else {
-        r3_pow_twiddles(v, wb1, wb2);
-      }
+      r3_pow_twiddles(v, wb1, wb2);
       dft16_t<0>(v);
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) row[k1] = v[g5_pos(k1)];
     }
-    if (TWR == 0) wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
-    if (MODE == 1 && r) {
-      wc1 = cmul(ldg_c(twc), ldg_c(tw + tw_index(r, lgL)));
+    cplx wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+    if (r) {
+      wc1 = cmul(wc1, ldg_c(tw + tw_index(r, lgL)));
       wc2 = cmul(wc1, wc1);
     }
     __syncthreads();
@@ -254,12 +186,7 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
 #pragma unroll
       for (int n0 = 0; n0 < 16; ++n0) v[n0] = col[n0 * sQ];
     }
-    if (TWR == 2) {
-#pragma unroll
-      for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], tC[t]);
-    } else {
-      r3_pow_twiddles(v, wc1, wc2);
-    }
+    r3_pow_twiddles(v, wc1, wc2);
     dft16_t<0>(v);
     if (sig == 0) {
       double2* qg = (double2*)(q_grid + (size_t)p * L) + r + ((size_t)tid << lgR);
@@ -272,6 +199,136 @@ __global__ void __launch_bounds__(kR3Threads, SLSE_R3_MINB) grid_r3_kernel(const
       double* sg = s_grid + (size_t)p * L + r + ((size_t)tid << lgR);
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) r3_store(&sg[(size_t)(256 * k2) << lgR], v[g5_pos(k2)].re, lgR);
+    }
+    const int tmp = sP;
+    sP = sQ;
+    sQ = tmp;
+  }
+}
+
+// L2 prefetch of `bytes` (multiple of 16) at a 16-byte aligned address
+SLSE_D void r3_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+// ---------------------------------------------------------------------------
+// cfg3 shape (L = 4096, N <= 1024), s^G of TWO problems in one transform.
+// With h_k = conj om_s(k) for all |k| < N (om_s Hermitian), s^G = FFT_L(h) is
+// real, so for problems p0, p1
+//   FFT_L(h^{p0} + i h^{p1})[l] = s^{p0}_l + i s^{p1}_l :
+// three tasks per problem pair (q^G of p0, q^G of p1, the shared s^G) instead
+// of four.  The input c = h^{p0} + i h^{p1} is two-sided: c[k] = conj om^{p0}(k)
+// + i conj om^{p1}(k) for 0 <= k < N and c[L - k] = om^{p0}(k) + i om^{p1}(k)
+// for 0 < k < N, i.e. i = tid + 256 n2 is non-zero for n2 in {0..3} and
+// {12..15} = {n2a - 4}: the pruned pass A folds the second group in with the
+// trivial factor W16^{-4 k0} = i^{k0} before its radix-4 butterflies.
+// The q^G tasks are grid_r3_kernel<0>'s (inputs prefetched into registers).
+__global__ void __launch_bounds__(kR3Threads, 2) grid_r3c_kernel(const cplx* __restrict__ w,
+                                                                 const cplx* __restrict__ om_s, int n, int B,
+                                                                 cplx* __restrict__ q_grid, double* __restrict__ s_grid,
+                                                                 const cplx* __restrict__ tw) {
+  constexpr int L = 4096;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* X = (cplx*)smem_raw;
+  const int tid = threadIdx.x;
+  const int a = tid & 15, b = tid >> 4;
+  const int T = 3 * ((B + 1) >> 1);
+  const size_t om_stride = 2 * (size_t)n - 1;
+  const cplx* twb = tw + tw_index(b, 8);
+  const cplx* twc = tw + tw_index(tid, 12);
+  const cplx wb1 = ldg_c(twb), wb2 = ldg_c(twb + b), wc1 = ldg_c(twc), wc2 = ldg_c(twc + tid);
+  int sP = kR3StrideHi, sQ = kR3StrideLo;
+  cplx xn[4];  // the next q^G task's inputs
+  const auto prefetch = [&](int task) {
+    const int role = task % 3, p = 2 * (task / 3) + role;
+    if (task < T && role < 2 && p < B) {
+      const cplx* src = w + (size_t)p * n;
+#pragma unroll
+      for (int n2 = 0; n2 < 4; ++n2) xn[n2] = tid + 256 * n2 < n ? ldg_c(src + tid + 256 * n2) : mk(0.0, 0.0);
+    } else if (task < T && role == 2 && tid < 2 && p - 2 + tid < B) {
+      // the s^G task's two om_s half rows towards L2 (its 16 loads per thread are not prefetched)
+      r3_prefetch_l2(om_s + (size_t)(p - 2 + tid) * om_stride + (n - 1), 16u * (unsigned)n);
+    }
+  };
+  prefetch(blockIdx.x);
+
+  for (int task = blockIdx.x; task < T; task += gridDim.x) {
+    const int role = task % 3, p0 = 2 * (task / 3);
+    const int p = role < 2 ? p0 + role : p0;
+    if (p >= B) {  // odd batch: the last pair has no second q^G task
+      prefetch(task + gridDim.x);
+      continue;
+    }
+    cplx v[16];
+    if (role < 2) {
+      r3_pruned4<0>(xn, v);
+      r3_pruned4<1>(xn, v);
+      r3_pruned4<2>(xn, v);
+      r3_pruned4<3>(xn, v);
+    } else {
+      const bool two = p0 + 1 < B;
+      const cplx* o0 = om_s + (size_t)p0 * om_stride + (n - 1);
+      const cplx* o1 = o0 + (two ? om_stride : 0);
+      const double f1 = two ? 1.0 : 0.0;
+      cplx xp[4], xm[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int kp = tid + 256 * j;        // i = kp            (n2 = j)
+        const int km = 256 * (4 - j) - tid;  // i = L - km        (n2 = 12 + j)
+        const cplx a0 = kp < n ? ldg_c(o0 + kp) : mk(0.0, 0.0), a1 = kp < n ? ldg_c(o1 + kp) : mk(0.0, 0.0);
+        const cplx b0 = km < n ? ldg_c(o0 + km) : mk(0.0, 0.0), b1 = km < n ? ldg_c(o1 + km) : mk(0.0, 0.0);
+        xp[j] = mk(a0.re + f1 * a1.im, f1 * a1.re - a0.im);  // conj a0 + i conj a1
+        xm[j] = mk(b0.re - f1 * b1.im, b0.im + f1 * b1.re);  // b0 + i b1
+      }
+      cplx y[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = cadd(xp[j], xm[j]);
+      r3_pruned4<0>(y, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = mk(xp[j].re - xm[j].im, xp[j].im + xm[j].re);  // + i xm
+      r3_pruned4<1>(y, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = csub(xp[j], xm[j]);
+      r3_pruned4<2>(y, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) y[j] = mk(xp[j].re + xm[j].im, xp[j].im - xm[j].re);  // - i xm
+      r3_pruned4<3>(y, v);
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < 16; ++k0) X[k0 * sP + a * sQ + b] = v[k0];
+    prefetch(task + gridDim.x);
+    __syncthreads();
+    {
+      cplx* row = X + b * sP + a * sQ;
+#pragma unroll
+      for (int n1 = 0; n1 < 16; ++n1) v[n1] = row[n1];
+      r3_pow_twiddles(v, wb1, wb2);
+      dft16_t<0>(v);
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) row[k1] = v[g5_pos(k1)];
+    }
+    __syncthreads();
+    {
+      const cplx* col = X + a * sP + b;
+#pragma unroll
+      for (int n0 = 0; n0 < 16; ++n0) v[n0] = col[n0 * sQ];
+    }
+    r3_pow_twiddles(v, wc1, wc2);
+    dft16_t<0>(v);
+    if (role < 2) {
+      double2* qg = (double2*)(q_grid + (size_t)p * L) + tid;
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) {
+        const cplx o = v[g5_pos(k2)];
+        __stcs(&qg[256 * k2], make_double2(o.re, o.im));
+      }
+    } else {
+      double* s0 = s_grid + (size_t)p0 * L + tid;
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) __stcs(&s0[256 * k2], v[g5_pos(k2)].re);
+      if (p0 + 1 < B) {
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) __stcs(&s0[L + 256 * k2], v[g5_pos(k2)].im);
+      }
     }
     const int tmp = sP;
     sP = sQ;
@@ -310,14 +367,13 @@ SLSE_D void r3_store32(double2* p, cplx lo, cplx hi) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(lo.re), "d"(lo.im), "d"(hi.re), "d"(hi.im)
                : "memory");
 }
-// L2 prefetch of `bytes` (multiple of 16) at a 16-byte aligned address
-SLSE_D void r3_prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
 #ifndef SLSE_R3_L2PF
 #define SLSE_R3_L2PF 1
 #endif
-constexpr int kR3SaveSmem = 10;  // outputs per thread parked in shared memory
+#ifndef SLSE_R3_SAVE_SMEM
+#define SLSE_R3_SAVE_SMEM 10
+#endif
+constexpr int kR3SaveSmem = SLSE_R3_SAVE_SMEM;  // outputs per thread parked in shared memory
 SLSE_HD constexpr size_t r3s_smem_bytes() { return 16 * ((size_t)kR3Buf + kR3SaveSmem * kR3Threads); }
 
 __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __restrict__ w,

@@ -4,7 +4,7 @@
 # shapes) at the bench's roofline batches, then the default bench line and its launch list.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-for spec in 1024:4096:10752:grid_r3_kernel 4096:16384:2688:grid_r3s_kernel 16384:65536:672:grid_r3s_kernel; do
+for spec in 1024:4096:10752:grid_r3c_kernel 4096:16384:2688:grid_r3s_kernel 16384:65536:672:grid_r3s_kernel; do
   IFS=: read n L B k <<< "$spec"
   timeout 300 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 \
     -o gpurun_out/${k}_n$n -f python tools/grid_omega_bench.py --shapes $n:$L:$B --reps 1 > gpurun_out/r3_ncu_n$n.log 2>&1
