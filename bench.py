@@ -258,6 +258,8 @@ def _grid_form(torch, dev, stream, flush, n, L, B, form, launches):
             kname = "grid_coef_kernel"
         elif L >= 16384 and 4 * n <= L:
             kname = "grid_r3s_kernel"  # residue pairs of 4096-point register transforms, s^G at half length
+        elif L == 256 and n <= 64:
+            kname = "grid_c1_kernel"   # one warp per problem, two DFT16 passes
         elif L == 4096 and n <= 1024:
             kname = "grid_r3c_kernel"  # pruned 4096-point register transforms, s^G of two problems per transform
         elif L >= 4096:

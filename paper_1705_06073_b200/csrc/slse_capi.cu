@@ -645,6 +645,22 @@ int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int 
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : fail("grid_r3s_kernel", e);
   }
+  if (L == 256 && N <= 64 && !slse_knob("SLSE_GRID_NO_C1")) {
+    // cfg1 shape: one warp per problem, two DFT16 passes through a warp-local exchange
+    const size_t smem = c1_smem_bytes();
+    e = set_smem(grid_c1_kernel, smem);
+    int occ = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_c1_kernel, 32 * kC1Warps, smem);
+    if (e != cudaSuccess || occ < 1) return fail("grid_c1_kernel setup", e);
+    long long g = (long long)sm_count() * occ;
+    const long long ctas = ((long long)B + kC1Warps - 1) / kC1Warps;
+    if (g > ctas) g = ctas;
+    grid_c1_kernel<<<(int)g, 32 * kC1Warps, smem, st>>>((const cplx*)w, (const cplx*)om_s, N, B, (cplx*)q_grid, s_grid,
+                                                        tw);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : fail("grid_c1_kernel", e);
+  }
   if (lgL == 12 && N <= 1024 && !slse_knob("SLSE_GRID_NO_R3C")) {
     // cfg3 shape: pruned 4096-point register transforms, s^G of two problems per transform
     const size_t smem = r3_smem_bytes();

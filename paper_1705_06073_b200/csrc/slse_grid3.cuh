@@ -531,4 +531,76 @@ __global__ void __launch_bounds__(kR3Threads, 2) grid_r3s_kernel(const cplx* __r
   }
 }
 
+// ---------------------------------------------------------------------------
+// cfg1 shape (L = 256, N <= 64): one warp per problem, no CTA barrier.
+// i = t + 16 n1 (n1 < 4 non-zero), l = k0 + 16 k1:
+//   pass A  lane t:  pruned DFT16 over n1                      -> A(t, k0)
+//   pass B  lane k0: W256^{t k0}, DFT16 over t                 -> X[k0 + 16 k1]
+// lanes 0-15 run q^G = FFT_L(w), lanes 16-31 s^G = Re FFT_L(conj d); the
+// exchange is a 16 x 17 complex tile per half-warp (__syncwarp only); the two
+// table entries of the twiddle chain stay in registers and the next
+// problem's four inputs are loaded before the exchange.
+constexpr int kC1Warps = 4;
+#ifndef SLSE_C1_MINB
+#define SLSE_C1_MINB 4  // 128 registers, 16 warps per SM: 0.83 of HBM (5: 96 registers spill, 0.74; 6: 0.46)
+#endif
+SLSE_HD constexpr size_t c1_smem_bytes() { return 16 * (size_t)kC1Warps * 2 * 16 * 17; }
+
+__global__ void __launch_bounds__(32 * kC1Warps, SLSE_C1_MINB) grid_c1_kernel(const cplx* __restrict__ w,
+                                                                const cplx* __restrict__ om_s, int n, int B,
+                                                                cplx* __restrict__ q_grid, double* __restrict__ s_grid,
+                                                                const cplx* __restrict__ tw) {
+  constexpr int L = 256;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = lane >> 4, t = lane & 15;
+  cplx* X = (cplx*)smem_raw + (warp * 2 + h) * (16 * 17);
+  const size_t om_stride = 2 * (size_t)n - 1;
+  const cplx w1 = ldg_c(tw + tw_index(t, 8)), w2 = ldg_c(tw + tw_index(2 * t, 8));  // W256^{t}, W256^{2t}
+  const int stride = gridDim.x * kC1Warps;
+  const auto load = [&](int p, cplx* x) {
+    if (p >= B) return;
+    const cplx* src = h ? om_s + (size_t)p * om_stride + (n - 1) : w + (size_t)p * n;
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) x[n1] = t + 16 * n1 < n ? ldg_c(src + t + 16 * n1) : mk(0.0, 0.0);
+  };
+  int p = blockIdx.x * kC1Warps + warp;
+  cplx xn[4];
+  load(p, xn);
+  for (; p < B; p += stride) {
+    cplx x[4], v[16];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+      // signal 1 is conj d, d_0 = om_s(0), d_m = 2 om_s(m)
+      const double f = (t + 16 * n1) ? 2.0 : 1.0;
+      x[n1] = h ? mk(f * xn[n1].re, -f * xn[n1].im) : xn[n1];
+    }
+    r3_pruned4<0>(x, v);
+    r3_pruned4<1>(x, v);
+    r3_pruned4<2>(x, v);
+    r3_pruned4<3>(x, v);
+#pragma unroll
+    for (int k0 = 0; k0 < 16; ++k0) X[k0 * 17 + t] = v[k0];
+    load(p + stride, xn);
+    __syncwarp();
+#pragma unroll
+    for (int tt = 0; tt < 16; ++tt) v[tt] = X[t * 17 + tt];
+    __syncwarp();
+    r3_pow_twiddles(v, w1, w2);  // lane k0 = t: input tt times W256^{tt k0}
+    dft16_t<0>(v);
+    if (h == 0) {
+      double2* qg = (double2*)(q_grid + (size_t)p * L) + t;
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) {
+        const cplx o = v[g5_pos(k1)];
+        __stcs(&qg[16 * k1], make_double2(o.re, o.im));
+      }
+    } else {
+      double* sg = s_grid + (size_t)p * L + t;
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) __stcs(&sg[16 * k1], v[g5_pos(k1)].re);
+    }
+  }
+}
+
 }  // namespace slse_k

@@ -424,7 +424,9 @@ def test_grid_eval_omega_against_reference(cfg, b, state):
                                    # 4N > L (no half-length s^G)
                                    (1024, 4096, 700), (513, 4096, 3), (1500, 4096, 5), (2048, 4096, 2),
                                    (2048, 8192, 400), (4096, 8192, 3), (5000, 16384, 3), (8192, 16384, 2),
-                                   (9000, 65536, 3), (16384, 65536, 30), (20000, 65536, 2), (32768, 131072, 2)])
+                                   (9000, 65536, 3), (16384, 65536, 30), (20000, 65536, 2), (32768, 131072, 2),
+                                   # the cfg1 warp-per-problem kernel: several problems per warp, ragged N
+                                   (64, 256, 20000), (64, 256, 1), (33, 256, 7), (50, 256, 130)])
 def test_grid_eval_omega_shapes_against_fft(n, L, B):
     """Row 9 coefficient form on every kernel family vs the reference's
     literal formula in numpy (q^G = fft(w, L), s^G = L ifft(buf).real with
