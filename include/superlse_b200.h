@@ -152,7 +152,10 @@ int slse_grid_eval(const double* rho, const double* delta_last, const double* w,
  * literally): q_grid = FFT_L(w), s_grid = L IFFT_L(buf).real with
  * buf[i mod L] = om_s(i), |i| < N.  om_s: [B, 2N-1] complex, index i + N - 1
  * (the slse_omegas "s" output; Hermitian, toeplitz.py:428-430, so only its
- * i >= 0 half is read).  Same outputs as slse_grid_eval. */
+ * i >= 0 half is read).  Same outputs as slse_grid_eval.  Kernels by shape
+ * (DESIGN.md 4): L = 256 / 1024 / 4096 with N <= L / 4 and every L >= 16384
+ * have register-transform kernels (cfg1-cfg5 shapes), other shapes the
+ * residue kernel. */
 int slse_grid_eval_omega(const double* w, const double* om_s, int N, int L, int B, double* q_grid, double* s_grid,
                          void* stream);
 
