@@ -373,14 +373,38 @@ SLSE_NI void dnc_leaf_block(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cp
 #endif
 }
 
+// c + a * b.  SLSE_LEAF_CFMA = 1: four fused multiply-adds (two levels deep)
+// instead of multiply, fused multiply-add and add (three levels, six
+// instructions); 0 keeps the arithmetic of dnc_leaf / dnc_leaf_block bit for bit.
+#ifndef SLSE_LEAF_CFMA
+#define SLSE_LEAF_CFMA 1
+#endif
+SLSE_D cplx lf_fma(cplx a, cplx b, cplx c) {
+#if SLSE_LEAF_CFMA
+  return mk(fma(-a.im, b.im, fma(a.re, b.re, c.re)), fma(a.im, b.re, fma(a.re, b.im, c.im)));
+#else
+  return cadd(c, cmul(a, b));
+#endif
+}
+template <class P>
+SLSE_D void lf_swap(P& a, P& b) {
+  const P t = a;
+  a = b;
+  b = t;
+}
+
 // Block leaf, two Schur steps per barrier.  The same recursion as
 // dnc_leaf_block (identical arithmetic), but each item also computes the
 // step-t value of its right-hand neighbour (generator slot j + 1, or Theta
 // coefficient i - 1 of row 2) from the pre-pair state, so it can apply step
 // t + 1 without waiting for that neighbour.  All state is ping-ponged
-// between two buffers per pair; thread 1 additionally carries slot 2 so it
-// can form k_{t+2} and k_{t+3} for the next pair.  Needs s <= nt (a few
-// threads then also hold the top Theta coefficients, s + 3 > nt).
+// between two buffers per pair.  The next pair's coefficients k_{t+2},
+// k_{t+3} (slots 1..3 of the pre-pair state, two reciprocals: the longest
+// dependent chain of the pair) are formed by a dedicated "chain warp" before
+// its own items, not by item 1 after its update: as item 1's divergent tail
+// the chain ran after warp 0's generator work and every other warp waited
+// at the barrier for it.  Needs s <= nt (a few threads then also hold the
+// top Theta coefficients, s + 3 > nt).
 SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T, Blk& b) {
 #ifdef SLSE_HOST_EMU
   dnc_leaf(X, E1, Bw, s, T, b);
@@ -405,11 +429,13 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
   double d = X.d;
   double* dtmp = X.delta_tmp + X.step;
   const double floor_ = X.floor_;
+  double* dsh = (double*)(kb + 4);  // the chain warp's running prediction error (read after the loop)
   if (tid == 0) {  // k_0, and k_1 from the pre-update pair (e_1, b_1)
     const double inv = 1.0 / d;
     const cplx e0 = E1[0];
     const cplx k0 = mk(-e0.re * inv, -e0.im * inv);
     kb[0] = k0;
+    dsh[0] = d;
     if (s > 1) {
       const double d1 = d * (1.0 - (k0.re * k0.re + k0.im * k0.im));
       const cplx en = cadd(E1[1], cmul(k0, Bw[1]));
@@ -420,99 +446,108 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
   b.sync();
   int st = 0;
   const int ci = nt - 1 - tid;  // Theta coefficient of this thread
-  int P = 0;
+  const int cw = nt >> 6;       // chain warp: a middle warp (the fewest own items over the leaf)
+  const bool chain = (tid >> 5) == cw;
+  // current / next buffers of the pair, swapped after every pair
+  cplx *ec = eb, *en_ = eb + le, *bc = bbuf, *bn_ = bbuf + le;
+  cplx *r1c = r1, *r1n = r1 + 2 * l1, *r2c = r2, *r2n = r2 + 2 * l2;
+  cplx *kc_ = kb, *kn_ = kb + 2;
   int t = 0;
-  for (; t + 1 < s; t += 2, P ^= 1) {
-    const int Q = P ^ 1;
-    const cplx ka = kb[2 * P], kk = kb[2 * P + 1];
+  for (; t + 1 < s; t += 2) {
+    const cplx ka = kc_[0], kk = kc_[1];
+    if (ka.re != ka.re) {  // uniform: the chain warp's not-positive-definite marker
+      st = kNotPD;
+      break;
+    }
     const cplx kac = conjg(ka), kkc = conjg(kk);
-    const double d1 = d * (1.0 - (ka.re * ka.re + ka.im * ka.im));
-    const double d2 = d1 * (1.0 - (kk.re * kk.re + kk.im * kk.im));
-    const cplx* ec = eb + P * le;
-    const cplx* bc = bbuf + P * le;
-    cplx* en_ = eb + Q * le;
-    cplx* bn_ = bbuf + Q * le;
-    const int j = tid;
-    if (j < s - t) {
-      const cplx ej = ec[t + j], bj = bc[j];
-      const cplx e1 = cadd(ej, cmul(ka, bj));  // step t, own slot (index t + j; superseded)
-      const cplx b1 = cadd(bj, cmul(kac, ej));
-      (void)e1;
-      if (j < s - t - 1) {
-        const cplx ej1 = ec[t + 1 + j], bj1 = bc[j + 1];
-        const cplx e1h = cadd(ej1, cmul(ka, bj1));  // step t, slot j + 1 (index t + 1 + j)
-        const cplx e2 = cadd(e1h, cmul(kk, b1));    // step t + 1, own slot
-        const cplx b2 = cadd(b1, cmul(kkc, e1h));
-        en_[t + 1 + j] = e2;
-        bn_[j] = b2;
-        if (j == 1 && t + 2 < s) {  // next pair's coefficients
-          const cplx e2s = ec[t + 2], e3s = ec[t + 3], b2s = bc[2], b3s = bc[3];
-          const cplx b1_2 = cadd(b2s, cmul(kac, e2s));
-          const cplx e1h_3 = cadd(e3s, cmul(ka, b3s));
-          const cplx e2_2 = cadd(e1h_3, cmul(kk, b1_2));  // e^{(t+2)}_{t+3}
-          const double inv2 = rcp_pos(d2);
-          const cplx kn0 = mk(-e2.re * inv2, -e2.im * inv2);
-          const double d3 = d2 * (1.0 - (kn0.re * kn0.re + kn0.im * kn0.im));
-          const cplx e3n = cadd(e2_2, cmul(kn0, b2));  // e^{(t+3)}_{t+3}
-          const double inv3 = rcp_pos(d3);
-          kb[2 * Q] = kn0;
-          kb[2 * Q + 1] = mk(-e3n.re * inv3, -e3n.im * inv3);
-        }
+    if (chain) {
+      // Chain warp: the prediction errors of this pair, the check that they
+      // stay above the floor, and the next pair's coefficients from slots
+      // 1..3 of the pre-pair state, all before this warp's own items (every
+      // lane computes them, lane 0 publishes).  The other warps only read
+      // (k_t, k_{t+1}); a failed check reaches them as a NaN coefficient.
+      const double d1 = d * (1.0 - (ka.re * ka.re + ka.im * ka.im));
+      const double d2 = d1 * (1.0 - (kk.re * kk.re + kk.im * kk.im));
+      const bool ok = (d1 > floor_) && (d2 > floor_);
+      cplx kn0 = mk(0.0, 0.0), kn1 = kn0;
+      if (t + 2 < s) {
+        const cplx e1s = ec[t + 1], e2s = ec[t + 2], e3s = ec[t + 3];
+        const cplx b1s = bc[1], b2s = bc[2], b3s = bc[3];
+        const cplx b1 = lf_fma(kac, e1s, b1s);
+        const cplx e1h = lf_fma(ka, b2s, e2s);
+        const cplx e2 = lf_fma(kk, b1, e1h);        // e^{(t+2)}_{t+2}
+        const cplx b2 = lf_fma(kkc, e1h, b1);
+        const cplx b1_2 = lf_fma(kac, e2s, b2s);
+        const cplx e1h_3 = lf_fma(ka, b3s, e3s);
+        const cplx e2_2 = lf_fma(kk, b1_2, e1h_3);  // e^{(t+2)}_{t+3}
+        const double inv2 = rcp_pos(d2);
+        kn0 = mk(-e2.re * inv2, -e2.im * inv2);
+        const double d3 = d2 * (1.0 - (kn0.re * kn0.re + kn0.im * kn0.im));
+        const cplx e3n = lf_fma(kn0, b2, e2_2);     // e^{(t+3)}_{t+3}
+        const double inv3 = rcp_pos(d3);
+        kn1 = mk(-e3n.re * inv3, -e3n.im * inv3);
       }
+      if (!ok) kn0.re = __longlong_as_double(0x7ff8000000000000LL);
+      if ((tid & 31) == 0) {
+        kn_[0] = kn0;
+        kn_[1] = kn1;
+        dsh[0] = d2;
+        dtmp[t + 1] = d1;
+        dtmp[t + 2] = d2;
+      }
+      d = d2;
+    }
+    const int j = tid;
+    if (j < s - t - 1) {
+      const cplx ej = ec[t + j], bj = bc[j];
+      const cplx ej1 = ec[t + 1 + j], bj1 = bc[j + 1];
+      const cplx b1 = lf_fma(kac, ej, bj);        // step t, own slot
+      const cplx e1h = lf_fma(ka, bj1, ej1);      // step t, slot j + 1 (index t + 1 + j)
+      en_[t + 1 + j] = lf_fma(kk, b1, e1h);       // step t + 1, own slot
+      bn_[j] = lf_fma(kkc, e1h, b1);
     }
     // Theta coefficient ci (and ci + nt when s >= nt: only the top one)
     for (int cq = ci; cq <= t + 2; cq += nt) {
-      const cplx* r1c = r1 + P * 2 * l1;
-      const cplx* r2c = r2 + P * 2 * l2;
-      cplx* r1n = r1 + Q * 2 * l1;
-      cplx* r2n = r2 + Q * 2 * l2;
       const cplx a11 = r1c[cq + 1], a12 = r1c[l1 + cq + 1];
       const cplx h11 = r1c[cq], h12 = r1c[l1 + cq];            // coefficient cq - 1, row 1
       const cplx p21 = r2c[cq + 1], p22 = r2c[l2 + cq + 1];    // coefficient cq - 1, row 2
       const cplx q21 = r2c[cq], q22 = r2c[l2 + cq];            // coefficient cq - 2, row 2
-      const cplx A1 = cadd(a11, cmul(ka, p21)), A2 = cadd(a12, cmul(ka, p22));
-      const cplx H1 = cadd(cmul(kac, h11), q21), H2 = cadd(cmul(kac, h12), q22);
-      r1n[cq + 1] = cadd(A1, cmul(kk, H1));
-      r1n[l1 + cq + 1] = cadd(A2, cmul(kk, H2));
-      r2n[cq + 2] = cadd(cmul(kkc, A1), H1);
-      r2n[l2 + cq + 2] = cadd(cmul(kkc, A2), H2);
-    }
-    if (tid == 0) {
-      dtmp[t + 1] = d1;
-      dtmp[t + 2] = d2;
-    }
-    d = d2;
-    if (!(d1 > floor_) || !(d2 > floor_)) {  // uniform
-      st = kNotPD;
-      break;
+      const cplx A1 = lf_fma(ka, p21, a11), A2 = lf_fma(ka, p22, a12);
+      const cplx H1 = lf_fma(kac, h11, q21), H2 = lf_fma(kac, h12, q22);
+      r1n[cq + 1] = lf_fma(kk, H1, A1);
+      r1n[l1 + cq + 1] = lf_fma(kk, H2, A2);
+      r2n[cq + 2] = lf_fma(kkc, A1, H1);
+      r2n[l2 + cq + 2] = lf_fma(kkc, A2, H2);
     }
     b.sync();
+    lf_swap(ec, en_);
+    lf_swap(bc, bn_);
+    lf_swap(r1c, r1n);
+    lf_swap(r2c, r2n);
+    lf_swap(kc_, kn_);
   }
+  // every thread: the chain warp's prediction error, and a failure in the last pair
+  d = dsh[0];
+  if (!st && kc_[0].re != kc_[0].re) st = kNotPD;
   if (!st && t < s) {  // odd s: one last single step with k_{s-1}
-    const int Q = P ^ 1;
-    const cplx ka = kb[2 * P], kac = conjg(ka);
+    const cplx ka = kc_[0], kac = conjg(ka);
     const double d1 = d * (1.0 - (ka.re * ka.re + ka.im * ka.im));
     for (int cq = ci; cq <= t + 1; cq += nt) {
-      const cplx* r1c = r1 + P * 2 * l1;
-      const cplx* r2c = r2 + P * 2 * l2;
-      cplx* r1n = r1 + Q * 2 * l1;
-      cplx* r2n = r2 + Q * 2 * l2;
       const cplx a11 = r1c[cq + 1], a12 = r1c[l1 + cq + 1];
       const cplx p21 = r2c[cq + 1], p22 = r2c[l2 + cq + 1];
-      r1n[cq + 1] = cadd(a11, cmul(ka, p21));
-      r1n[l1 + cq + 1] = cadd(a12, cmul(ka, p22));
-      r2n[cq + 2] = cadd(cmul(kac, a11), p21);
-      r2n[l2 + cq + 2] = cadd(cmul(kac, a12), p22);
+      r1n[cq + 1] = lf_fma(ka, p21, a11);
+      r1n[l1 + cq + 1] = lf_fma(ka, p22, a12);
+      r2n[cq + 2] = lf_fma(kac, a11, p21);
+      r2n[l2 + cq + 2] = lf_fma(kac, a12, p22);
     }
     if (tid == 0) dtmp[t + 1] = d1;
     d = d1;
     if (!(d1 > floor_)) st = kNotPD;
-    P ^= 1;
+    lf_swap(r1c, r1n);
+    lf_swap(r2c, r2n);
   }
   b.sync();
   if (!st) {
-    const cplx* r1c = r1 + P * 2 * l1;
-    const cplx* r2c = r2 + P * 2 * l2;
     for (int i = tid; i < ld; i += nt) {
       T[i] = r1c[i + 1];
       T[ld + i] = r1c[l1 + i + 1];
@@ -725,7 +760,7 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
       else if (2 * s <= b.nt) dnc_leaf_regs(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #endif
 #if SLSE_DNC_LEAF2
-      else if (s <= b.nt && 12 * s + 48 <= X.f.smem_cap) dnc_leaf_block2(X, cf.E + 1, cf.Bw, s, cf.T, b);
+      else if (s <= b.nt && 12 * s + 50 <= X.f.smem_cap) dnc_leaf_block2(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #endif
       else dnc_leaf_block(X, cf.E + 1, cf.Bw, s, cf.T, b);
       if (prof) X.prof[0] += dnc_clock() - t0;
