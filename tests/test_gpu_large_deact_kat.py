@@ -365,6 +365,26 @@ def test_kat_not_positive_definite():
         assert int(st.item()) == 2, method
 
 
+@pytest.mark.parametrize("n,where", [(600, 254), (600, 255), (600, 256), (600, 257), (600, 511), (600, 512),
+                                      (600, 598), (600, 599), (513, 511), (513, 512), (515, 513), (1030, 1027)])
+def test_kat_not_positive_definite_at_leaf_boundaries(n, where):
+    """The pivot fails at a chosen step of the superfast recursion: first /
+    last pair of a 256-step block leaf, the single odd step that ends a leaf,
+    the last step of the whole factorisation.  Both factorisations return
+    status 1 (toeplitz.py:129-134), and the same column without the
+    perturbation factors with status 0."""
+    rng = np.random.default_rng(1000 + where)
+    c = _random_pd_toeplitz(n, rng)
+    for method in ("levinson", "schur"):
+        _, _, _, st = _factor(c, method)
+        assert int(st.item()) == 0, method
+    bad = c.copy()
+    bad[where] += 50.0 * abs(c[0])
+    for method in ("levinson", "schur"):
+        _, _, _, st = _factor(bad, method)
+        assert int(st.item()) == 1, (method, where)
+
+
 def test_kat_apply_inverse_and_logdet():
     """test_toeplitz.py:150-159 (identity; C^-1 [1,0] = [2/3, -1/3] for
     C = [[2,1],[1,2]]) and :184-190 (log det 0, ln 3, N ln beta)."""
