@@ -39,48 +39,96 @@ struct SfObs {
 SLSE_D cplx sf_scale(const SfObs& o, int i) { return o.sc ? o.sc[i] : mk(1.0, 0.0); }
 SLSE_D double sf_w0(const SfObs& o, int i) { return o.sc ? cabs2(o.sc[i]) : 1.0; }
 
-// E[i * ld + p] = e^{j 2 pi n_i theta_p}, i < m, p < kk (exactly reduced phases)
+// Sums over the observed positions are split over groups of `nch` adjacent
+// lanes (chunk ch of an item takes i = ch, ch + nch, ...) and combined by
+// shuffles, so every thread of the CTA works on them (K items alone would
+// occupy K of the 128 threads).  Every lane of a warp must call sf_group_sum.
+// lane groups need whole warps (and do not exist in the serial host emulation)
+SLSE_D bool sf_lanes_ok(int nt) {
+#ifdef SLSE_HOST_EMU
+  (void)nt;
+  return false;
+#else
+  return (nt & 31) == 0;
+#endif
+}
+// lanes per item: the smallest power of two that gives every thread a chunk (at most cap <= 32)
+SLSE_D int sf_chunks(int items, int nt, int cap) {
+  if (!sf_lanes_ok(nt)) return 1;
+  int nch = 1;
+  while (nch < cap && items * nch < nt) nch *= 2;
+  return nch;
+}
+SLSE_D double sf_group_sum(double v, int nch) {
+#ifndef SLSE_HOST_EMU
+  for (int o = nch >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+#else
+  (void)nch;
+#endif
+  return v;
+}
+SLSE_D cplx sf_group_sum(cplx v, int nch) { return mk(sf_group_sum(v.re, nch), sf_group_sum(v.im, nch)); }
+
+// E[p * ld + i] = e^{j 2 pi n_i theta_p}, i < m, p < kk (exactly reduced
+// phases), component-major: the sums over i below read consecutive
+// addresses, per thread and across the lanes of a group.
 SLSE_D void sf_phases(cplx* E, int ld, const SfObs& o, const double* th, int kk, Blk& b) {
   const int tot = o.m * kk;
   SLSE_CTRL_LOOP_SF
   for (int t = b.tid; t < tot; t += b.nt) {
-    const int i = t / kk, p = t - i * kk;
-    E[(size_t)i * ld + p] = expj2pi((double)o.idx[i], th[p], 1.0);
+    const int p = t / o.m, i = t - p * o.m;
+    E[(size_t)p * ld + i] = expj2pi((double)o.idx[i], th[p], 1.0);
   }
   b.sync();
 }
 
 // Weighted steering Gram matrices (nufft.gram, direct; model_core.py:331-333)
 // G_j[r, c] = sum_i w0_i d_i^j conj(E_ir) E_ic, Hermitian by construction
-// (the reference symmetrises, _hermitize :412-413: real diagonal).
+// (the reference symmetrises, _hermitize :412-413: real diagonal).  One
+// (r <= c) pair per group of 8 lanes.
 SLSE_D void sf_gram(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde, const SfObs& o, int kk, Blk& b) {
-  const int tot = kk * kk;
+  const int npairs = kk * (kk + 1) / 2;
+  const int nch = sf_lanes_ok(b.nt) ? 8 : 1;  // 8 lanes per pair on the device
+  const int tot = npairs * nch;
   SLSE_CTRL_LOOP_SF
-  for (int t = b.tid; t < tot; t += b.nt) {
-    const int r = t / kk, c = t - r * kk;
-    if (r > c) continue;
+  for (int base = 0; base < tot; base += b.nt) {
+    const int t = base + b.tid;
+    const bool act = t < tot;
+    const int q = act ? t / nch : 0, ch = t - (t / nch) * nch;
+    int c = 0;  // pair q -> (r, c), r <= c, column-major over the upper triangle
+    while ((c + 1) * (c + 2) / 2 <= q) ++c;
+    const int r = q - c * (c + 1) / 2;
     cplx a0 = mk(0.0, 0.0), a1 = a0, a2 = a0;
-    SLSE_CTRL_LOOP_SF
-    for (int i = 0; i < o.m; ++i) {
-      const cplx e = cmulc(E[(size_t)i * lde + c], E[(size_t)i * lde + r]);  // E_ic conj(E_ir)
-      const double w0 = sf_w0(o, i);
-      const double d = 2.0 * kPi * (double)o.idx[i];
-      const double wd = w0 * d, wd2 = w0 * (d * d);
-      a0 = mk(fma(w0, e.re, a0.re), fma(w0, e.im, a0.im));
-      a1 = mk(fma(wd, e.re, a1.re), fma(wd, e.im, a1.im));
-      a2 = mk(fma(wd2, e.re, a2.re), fma(wd2, e.im, a2.im));
+    if (act) {
+      const cplx* Ec = E + (size_t)c * lde;
+      const cplx* Er = E + (size_t)r * lde;
+#pragma unroll 4
+      for (int i = ch; i < o.m; i += nch) {
+        const cplx e = cmulc(Ec[i], Er[i]);  // E_ic conj(E_ir)
+        const double w0 = sf_w0(o, i);
+        const double d = 2.0 * kPi * (double)o.idx[i];
+        const double wd = w0 * d, wd2 = w0 * (d * d);
+        a0 = mk(fma(w0, e.re, a0.re), fma(w0, e.im, a0.im));
+        a1 = mk(fma(wd, e.re, a1.re), fma(wd, e.im, a1.im));
+        a2 = mk(fma(wd2, e.re, a2.re), fma(wd2, e.im, a2.im));
+      }
     }
-    if (r == c) {
-      a0.im = 0.0;
-      a1.im = 0.0;
-      a2.im = 0.0;
+    a0 = sf_group_sum(a0, nch);
+    a1 = sf_group_sum(a1, nch);
+    a2 = sf_group_sum(a2, nch);
+    if (act && ch == 0) {
+      if (r == c) {
+        a0.im = 0.0;
+        a1.im = 0.0;
+        a2.im = 0.0;
+      }
+      G0[r * ld + c] = a0;
+      G1[r * ld + c] = a1;
+      G2[r * ld + c] = a2;
+      G0[c * ld + r] = conjg(a0);
+      G1[c * ld + r] = conjg(a1);
+      G2[c * ld + r] = conjg(a2);
     }
-    G0[r * ld + c] = a0;
-    G1[r * ld + c] = a1;
-    G2[r * ld + c] = a2;
-    G0[c * ld + r] = conjg(a0);
-    G1[c * ld + r] = conjg(a1);
-    G2[c * ld + r] = conjg(a2);
   }
   b.sync();
 }

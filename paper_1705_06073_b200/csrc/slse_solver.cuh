@@ -768,20 +768,31 @@ struct Solver {
     double ln_c = (double)m * log(be);  // :339
     double quad = quad_y / be;
     if (kk) {
-      sf_phases(sfE, kcap, obs, th, kk, b);
-      sf_gram(B.sG0, B.sG1, B.sG2, kcap, sfE, kcap, obs, kk, b);
-      SLSE_CTRL_LOOP
-      for (int t = tid_; t < kk * G; t += nt_) {
-        const int p = t / G, g = t - p * G;
-        const cplx* yg = y + (size_t)g * m;
-        cplx acc = mk(0.0, 0.0);
+      sf_phases(sfE, m, obs, th, kk, b);
+      sf_gram(B.sG0, B.sG1, B.sG2, kcap, sfE, m, obs, kk, b);
+      {
+        // one (component, snapshot) item per group of lanes, the positions split over the group
+        const int items = kk * G, nch = sf_chunks(items, nt_, 32), tot = items * nch;
         SLSE_CTRL_LOOP
-        for (int i = 0; i < m; ++i) {
-          const cplx ys = cmulc(yg[i], sf_scale(obs, i));           // scatter: conj(a_i) y_i
-          const cplx e = sfE[(size_t)i * kcap + p];
-          acc = mk(acc.re + e.re * ys.re + e.im * ys.im, acc.im + e.re * ys.im - e.im * ys.re);  // conj(E_ip) ys
+        for (int base = 0; base < tot; base += nt_) {
+          const int t = base + tid_;
+          const bool act = t < tot;
+          const int it = act ? t / nch : 0, ch = t - (t / nch) * nch;
+          const int p = it / G, g = it - p * G;
+          const cplx* yg = y + (size_t)g * m;
+          const cplx* Ep = sfE + (size_t)p * m;
+          cplx acc = mk(0.0, 0.0);
+          if (act) {
+#pragma unroll 4
+            for (int i = ch; i < m; i += nch) {
+              const cplx ys = cmulc(yg[i], sf_scale(obs, i));           // scatter: conj(a_i) y_i
+              const cplx e = Ep[i];
+              acc = mk(acc.re + e.re * ys.re + e.im * ys.im, acc.im + e.re * ys.im - e.im * ys.re);  // conj(E_ip) ys
+            }
+          }
+          acc = sf_group_sum(acc, nch);
+          if (act && ch == 0) sfAhy[it] = acc;
         }
-        sfAhy[t] = acc;
       }
       b.sync();
     }
@@ -826,7 +837,7 @@ struct Solver {
       if (kp) {
         cplx zs = mk(0.0, 0.0);
         SLSE_CTRL_LOOP
-        for (int j = 0; j < kp; ++j) zs = cadd(zs, cmul(sfE[(size_t)i * kcap + B.sP[j]], sfX[j * G + g]));
+        for (int j = 0; j < kp; ++j) zs = cadd(zs, cmul(sfE[(size_t)B.sP[j] * m + i], sfX[j * G + g]));
         const cplx az = cmul(a, zs);
         const double b2 = be * be;
         cy = csub(cy, mk(az.re / b2, az.im / b2));
@@ -844,25 +855,39 @@ struct Solver {
   SLSE_NIM void sf_stats(Bundle& B, const double* th, int kk) {
     const int tid_ = b.tid, nt_ = b.nt;
     const double be = B.sbeta, b2 = be * be;
-    sf_phases(sfE, kcap, obs, th, kk, b);
-    SLSE_CTRL_LOOP
-    for (int t = tid_; t < kk * G; t += nt_) {
-      const int g = t / kk, p = t - g * kk;
-      const cplx* eg = B.w + (size_t)g * n;
-      cplx aq = mk(0.0, 0.0), ar = aq, au = aq;
+    sf_phases(sfE, m, obs, th, kk, b);
+    {
+      const int items = kk * G, nch = sf_chunks(items, nt_, 32), tot = items * nch;
       SLSE_CTRL_LOOP
-      for (int i = 0; i < m; ++i) {
-        const int ni = obs.idx[i];
-        const double d = 2.0 * kPi * (double)ni;
-        const cplx ph = conjg(sfE[(size_t)i * kcap + p]);
-        const cplx e0 = eg[ni];
-        aq = cadd(aq, cmul(ph, e0));
-        ar = cadd(ar, cmul(ph, cscale(e0, d)));
-        au = cadd(au, cmul(ph, cscale(e0, d * d)));
+      for (int base = 0; base < tot; base += nt_) {
+        const int t = base + tid_;
+        const bool act = t < tot;
+        const int it = act ? t / nch : 0, ch = t - (t / nch) * nch;
+        const int g = it / kk, p = it - g * kk;
+        const cplx* eg = B.w + (size_t)g * n;
+        const cplx* Ep = sfE + (size_t)p * m;
+        cplx aq = mk(0.0, 0.0), ar = aq, au = aq;
+        if (act) {
+#pragma unroll 4
+          for (int i = ch; i < m; i += nch) {
+            const int ni = obs.idx[i];
+            const double d = 2.0 * kPi * (double)ni;
+            const cplx ph = conjg(Ep[i]);
+            const cplx e0 = eg[ni];
+            aq = cadd(aq, cmul(ph, e0));
+            ar = cadd(ar, cmul(ph, cscale(e0, d)));
+            au = cadd(au, cmul(ph, cscale(e0, d * d)));
+          }
+        }
+        aq = sf_group_sum(aq, nch);
+        ar = sf_group_sum(ar, nch);
+        au = sf_group_sum(au, nch);
+        if (act && ch == 0) {
+          B.q[(size_t)g * kmax + p] = aq;
+          B.r[(size_t)g * kmax + p] = ar;
+          B.u[(size_t)g * kmax + p] = au;
+        }
       }
-      B.q[(size_t)g * kmax + p] = aq;
-      B.r[(size_t)g * kmax + p] = ar;
-      B.u[(size_t)g * kmax + p] = au;
     }
     SLSE_CTRL_LOOP
     for (int p = tid_; p < kk; p += nt_) {
@@ -946,7 +971,7 @@ struct Solver {
     const double base = w0s / be;  // :397
     const int kp = B.kp;
     if (kp) {
-      sf_phases(sfE, kcap, obs, act_theta, k, b);
+      sf_phases(sfE, m, obs, act_theta, k, b);
       // b_p(l), p in P (:400-403): scatter every row, then one batched
       // inverse transform of the kp rows (in place)
       SLSE_CTRL_LOOP
@@ -955,7 +980,7 @@ struct Solver {
       SLSE_CTRL_LOOP
       for (int t = tid_; t < kp * m; t += nt_) {
         const int j = t / m, i = t - j * m;
-        sfBb[(size_t)j * L + obs.idx[i]] = cscale(conjg(sfE[(size_t)i * kcap + B.sP[j]]), sf_w0(obs, i));
+        sfBb[(size_t)j * L + obs.idx[i]] = cscale(conjg(sfE[(size_t)B.sP[j] * m + i]), sf_w0(obs, i));
       }
       b.sync();
       {
