@@ -431,6 +431,8 @@ struct Solver {
 #ifdef SLSE_SEMIFAST
   SfObs obs;
   cplx *sfE, *sfX, *sfAhy, *sfBb;
+  const Bundle* sfE_of = nullptr;  // the bundle whose (theta, kk) the steering matrix sfE currently holds
+  int sfE_kk = 0;
   int kcap;
 #endif
   int G;  // snapshots (P.g): y, yhat and w hold G rows of n / nf; q, r, u, mu G rows of kmax
@@ -769,6 +771,8 @@ struct Solver {
     double quad = quad_y / be;
     if (kk) {
       sf_phases(sfE, m, obs, th, kk, b);
+      sfE_of = &B;
+      sfE_kk = kk;
       sf_gram(B.sG0, B.sG1, B.sG2, kcap, sfE, m, obs, kk, b);
       {
         // one (component, snapshot) item per group of lanes, the positions split over the group
@@ -855,7 +859,13 @@ struct Solver {
   SLSE_NIM void sf_stats(Bundle& B, const double* th, int kk) {
     const int tid_ = b.tid, nt_ = b.nt;
     const double be = B.sbeta, b2 = be * be;
-    sf_phases(sfE, m, obs, th, kk, b);
+    // (a bundle's statistics and grid use the theta it was built from: its steering matrix is still
+    // in sfE unless another bundle was built since)
+    if (sfE_of != &B || sfE_kk != kk) {
+      sf_phases(sfE, m, obs, th, kk, b);
+      sfE_of = &B;
+      sfE_kk = kk;
+    }
     {
       const int items = kk * G, nch = sf_chunks(items, nt_, 32), tot = items * nch;
       SLSE_CTRL_LOOP
@@ -971,7 +981,11 @@ struct Solver {
     const double base = w0s / be;  // :397
     const int kp = B.kp;
     if (kp) {
-      sf_phases(sfE, m, obs, act_theta, k, b);
+      if (sfE_of != &B || sfE_kk != k) {
+        sf_phases(sfE, m, obs, act_theta, k, b);
+        sfE_of = &B;
+        sfE_kk = k;
+      }
       // b_p(l), p in P (:400-403): scatter every row, then one batched
       // inverse transform of the kp rows (in place)
       SLSE_CTRL_LOOP
