@@ -25,6 +25,9 @@
 #include "slse_stats.cuh"
 
 #define SLSE_CTRL_LOOP_SF _Pragma("unroll 1")
+#ifndef SLSE_SF_GRAM_CLOSED
+#define SLSE_SF_GRAM_CLOSED 1  // complete data: closed-form Gram sums (sf_gram_complete)
+#endif
 
 namespace slse {
 
@@ -86,7 +89,14 @@ SLSE_D void sf_phases(cplx* E, int ld, const SfObs& o, const double* th, int kk,
 // G_j[r, c] = sum_i w0_i d_i^j conj(E_ir) E_ic, Hermitian by construction
 // (the reference symmetrises, _hermitize :412-413: real diagonal).  One
 // (r <= c) pair per group of 8 lanes.
-SLSE_D void sf_gram(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde, const SfObs& o, int kk, Blk& b) {
+SLSE_D void sf_gram_complete(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde, const double* th, int n,
+                             int kk, Blk& b);
+SLSE_D void sf_gram(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde, const SfObs& o, int kk, Blk& b,
+                    const double* th = nullptr, int n = 0) {
+  if (SLSE_SF_GRAM_CLOSED && th && o.sc == nullptr && o.m == n) {  // complete data: idx = 0 .. n-1, unit scales
+    sf_gram_complete(G0, G1, G2, ld, E, lde, th, n, kk, b);
+    return;
+  }
   const int npairs = kk * (kk + 1) / 2;
   const int nch = sf_lanes_ok(b.nt) ? 8 : 1;  // 8 lanes per pair on the device
   const int tot = npairs * nch;
@@ -129,6 +139,75 @@ SLSE_D void sf_gram(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde
       G1[c * ld + r] = conjg(a1);
       G2[c * ld + r] = conjg(a2);
     }
+  }
+  b.sync();
+}
+
+// Complete data (positions 0 .. N-1, unit scales): the Gram entries are the
+// geometric sums S_j(x) = sum_{i<N} i^j z^i, z = e^{j 2 pi x}, x = theta_c - theta_r
+// (wrapped to [-1/2, 1/2)), in closed form -- O(K^2) per bundle instead of
+// O(K^2 N):
+//   S_0 = (1 - z^N) / (1 - z)
+//   S_1 = (z - N z^N + (N-1) z^{N+1}) / (1 - z)^2
+//   S_2 = z (1 + z - N^2 z^{N-1} + (2N^2 - 2N - 1) z^N - (N-1)^2 z^{N+1}) / (1 - z)^3
+// with 1 - z = 2 sin(pi x) (sin(pi x) - j cos(pi x)) (no cancellation) and
+// z^N from the exactly reduced phase N x.  The numerators cancel like
+// 1 / (N |x|)^{j+1}: within ~1e-12 of the direct sums for N |x| >= 1/2
+// (checked against them up to N = 500); closer pairs take the direct sums.
+SLSE_D void sf_gram_complete(cplx* G0, cplx* G1, cplx* G2, int ld, const cplx* E, int lde, const double* th, int n,
+                             int kk, Blk& b) {
+  const int npairs = kk * (kk + 1) / 2;
+  const double N = (double)n;
+  const double tp = 2.0 * kPi;
+  SLSE_CTRL_LOOP_SF
+  for (int q = b.tid; q < npairs; q += b.nt) {
+    int c = 0;
+    while ((c + 1) * (c + 2) / 2 <= q) ++c;
+    const int r = q - c * (c + 1) / 2;
+    cplx a0, a1, a2;
+    double x = th[c] - th[r];
+    x -= floor(x + 0.5);
+    if (r == c) {
+      a0 = mk(N, 0.0);
+      a1 = mk(tp * (0.5 * N * (N - 1.0)), 0.0);
+      a2 = mk(tp * tp * ((N - 1.0) * N * (2.0 * N - 1.0) / 6.0), 0.0);
+    } else if (fabs(x) * N < 0.5) {
+      a0 = a1 = a2 = mk(0.0, 0.0);
+      const cplx* Ec = E + (size_t)c * lde;
+      const cplx* Er = E + (size_t)r * lde;
+      SLSE_CTRL_LOOP_SF
+      for (int i = 0; i < n; ++i) {
+        const cplx e = cmulc(Ec[i], Er[i]);
+        const double d = tp * (double)i;
+        a0 = cadd(a0, e);
+        a1 = mk(fma(d, e.re, a1.re), fma(d, e.im, a1.im));
+        a2 = mk(fma(d * d, e.re, a2.re), fma(d * d, e.im, a2.im));
+      }
+    } else {
+      double sn, cs;
+      sincos2pi(0.5 * x, &sn, &cs);  // sin / cos (pi x)
+      const cplx omz = mk(2.0 * sn * sn, -2.0 * sn * cs);  // 1 - z
+      const cplx z = mk(1.0 - omz.re, -omz.im);
+      const cplx zN = expj2pi(N, x, 1.0);                  // z^N, phase N x reduced exactly
+      const cplx zNm1 = cmulc(zN, z), zNp1 = cmul(zN, z);
+      const double i2 = 1.0 / cabs2(omz);
+      const cplx inv = mk(omz.re * i2, -omz.im * i2);      // 1 / (1 - z)
+      const cplx inv2 = cmul(inv, inv), inv3 = cmul(inv2, inv);
+      const cplx n0 = mk(1.0 - zN.re, -zN.im);
+      const cplx n1 = mk(z.re - N * zN.re + (N - 1.0) * zNp1.re, z.im - N * zN.im + (N - 1.0) * zNp1.im);
+      const double k1 = N * N, k2 = 2.0 * N * N - 2.0 * N - 1.0, k3 = (N - 1.0) * (N - 1.0);
+      const cplx n2 = cmul(z, mk(1.0 + z.re - k1 * zNm1.re + k2 * zN.re - k3 * zNp1.re,
+                                 z.im - k1 * zNm1.im + k2 * zN.im - k3 * zNp1.im));
+      a0 = cmul(n0, inv);
+      a1 = cscale(cmul(n1, inv2), tp);
+      a2 = cscale(cmul(n2, inv3), tp * tp);
+    }
+    G0[r * ld + c] = a0;
+    G1[r * ld + c] = a1;
+    G2[r * ld + c] = a2;
+    G0[c * ld + r] = conjg(a0);
+    G1[c * ld + r] = conjg(a1);
+    G2[c * ld + r] = conjg(a2);
   }
   b.sync();
 }

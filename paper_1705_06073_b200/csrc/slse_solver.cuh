@@ -773,7 +773,7 @@ struct Solver {
       sf_phases(sfE, m, obs, th, kk, b);
       sfE_of = &B;
       sfE_kk = kk;
-      sf_gram(B.sG0, B.sG1, B.sG2, kcap, sfE, m, obs, kk, b);
+      sf_gram(B.sG0, B.sG1, B.sG2, kcap, sfE, m, obs, kk, b, th, n);
       {
         // one (component, snapshot) item per group of lanes, the positions split over the group
         const int items = kk * G, nch = sf_chunks(items, nt_, 32), tot = items * nch;

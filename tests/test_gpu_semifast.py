@@ -247,3 +247,39 @@ def test_semifast_edge_patterns():
     assert ri.k_hat == rc.k_hat and ri.trace_stages == rc.trace_stages
     assert rel(ri.objective_trace, rc.objective_trace) < CALL_TOL
     assert np.max(wrap_distance(ri.theta_hat, rc.theta_hat), initial=0) < THETA_TOL
+
+
+@pytest.mark.parametrize("n", [64, 256, 500])
+def test_semifast_complete_gram_closed_form_vs_oracle(n):
+    """Complete data takes the closed-form Gram sums (sf_gram_complete);
+    the oracle's bundle takes the reference's direct sums (nufft.gram,
+    nufft.py:184-210).  Frequencies at separations 0.2/N ... 3/N (the pairs
+    below 0.5/N fall back to the direct sums), across the wrap-around point
+    and far apart: data term, e, the seven statistics and the grid agree at
+    the per-call bar."""
+    from oracle import superlse_oracle as O
+    from paper_1705_06073_b200 import ops
+
+    rng = np.random.default_rng(n)
+    base = np.array([0.11, 0.37, 0.62, 0.9995])
+    seps = np.array([0.2, 0.49, 0.51, 1.0, 1.7, 3.0]) / n
+    th = np.concatenate([base, 0.2 + np.cumsum(seps), [0.0004, 0.75]])  # 0.9995 / 0.0004: a pair across the wrap
+    k = th.size
+    ga = rng.uniform(0.5, 2.0, k)
+    be = 0.05
+    y = sum(np.sqrt(g) * np.exp(2j * np.pi * t * np.arange(n)) for g, t in zip(ga, th))
+    y = y + np.sqrt(be / 2) * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    L = 4 * (1 << int(np.ceil(np.log2(n))))
+    ref = O.SemifastBundle(y[None], n, np.arange(1, n + 1), np.ones(n), th, ga, be)
+    st = ref.stats()
+    qg, sg = ref.grid(L)
+    out = ops.semifast_bundle(_dev(th[None], np.float64), _dev(ga[None], np.float64), _dev(np.array([k]), np.int32),
+                              _dev(np.array([be])), _dev(y[None]), n, L, None, None)
+    assert int(out["status"].item()) == 0
+    assert abs(out["data_term"].item() - ref.data_term) <= CALL_TOL * abs(ref.data_term)
+    assert rel(out["q_grid"].cpu().numpy()[0], qg) < CALL_TOL
+    assert rel(out["s_grid"].cpu().numpy()[0], sg) < CALL_TOL
+    for key in "qru":
+        assert rel(out[key].cpu().numpy()[0, :, :k], np.asarray(st[key]).reshape(1, -1)[:, :k]) < CALL_TOL, key
+    for key in "stvx":
+        assert rel(out[key].cpu().numpy()[0, :k], np.asarray(st[key])[:k]) < CALL_TOL, key
