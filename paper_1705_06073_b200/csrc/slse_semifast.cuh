@@ -235,13 +235,14 @@ SLSE_D int sf_cholesky(cplx* Lc, double* ldg, int ld, const cplx* G0, int ldg0, 
     for (int k = 0; k < j; ++k) d -= cabs2(Lc[j * ld + k]);
     if (!(d > 0.0)) return kNotPD;
     const double ljj = sqrt(d);
+    const double rjj = 1.0 / ljj;
     if (b.tid == 0) ldg[j] = ljj;
     SLSE_CTRL_LOOP_SF
     for (int i = j + 1 + b.tid; i < kp; i += b.nt) {
       cplx a = Lc[i * ld + j];
       SLSE_CTRL_LOOP_SF
       for (int k = 0; k < j; ++k) a = csub(a, cmulc(Lc[i * ld + k], Lc[j * ld + k]));  // L_ik conj(L_jk)
-      Lc[i * ld + j] = mk(a.re / ljj, a.im / ljj);
+      Lc[i * ld + j] = mk(a.re * rjj, a.im * rjj);
     }
     b.sync();
   }

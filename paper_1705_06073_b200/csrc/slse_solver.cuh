@@ -1010,9 +1010,15 @@ struct Solver {
         SLSE_CTRL_LOOP
         for (int j = 0; j < kp; ++j) {
           cplx a = sfBb[(size_t)j * L + l];
-          SLSE_CTRL_LOOP
-          for (int c = 0; c < j; ++c) a = csub(a, cmul(B.sL[j * kcap + c], sfBb[(size_t)c * L + l]));
-          a = mk(a.re / B.sLd[j], a.im / B.sLd[j]);
+          const cplx* Lj = B.sL + j * kcap;
+          const cplx* bl = sfBb + l;
+#pragma unroll 4
+          for (int c = 0; c < j; ++c) {  // (the solved entries a_c are final: independent loads)
+            const cplx lc = Lj[c], ac = bl[(size_t)c * L];
+            a = mk(fma(lc.im, ac.im, fma(-lc.re, ac.re, a.re)), fma(-lc.im, ac.re, fma(-lc.re, ac.im, a.im)));
+          }
+          const double inv = 1.0 / B.sLd[j];  // uniform: one reciprocal per pivot, not two divisions per point
+          a = mk(a.re * inv, a.im * inv);
           sfBb[(size_t)j * L + l] = a;
           acc += cabs2(a);
         }
