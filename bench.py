@@ -21,8 +21,10 @@ between steps.  The JSON line also carries:
                one, the other under `alt`), on a batch whose outputs are 8x
                the L2 (so DRAM traffic ~ algorithmic bytes);
   per_config   every BASELINE config (cfg1-5) solved in full on this GPU:
-               problems/s, ms per batch, its grid roofline, and the real
-               reference's CPU rate on a bounded sample (N = 1 only);
+               problems/s, ms per batch, its grid roofline, the real
+               reference's CPU rate on a bounded sample (N = 1 only), and for
+               N < 512 the same batch through the semifast backend the
+               reference's "auto" picks there (`auto_backend`);
   cpu_baseline the REAL reference (baseline/_ref, installed by
                tools/install_reference.sh) on a bounded sample on this
                host's cores (rank 0, N = 1 only); the oracle port if absent.
@@ -382,7 +384,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-def solve_rate(torch, dev, stream, flush, cfg, steps, warmup, B=None, start=0):
+def solve_rate(torch, dev, stream, flush, cfg, steps, warmup, B=None, start=0, backend="superfast"):
     from paper_1705_06073_b200 import EstimatorOptions, simdata
     from paper_1705_06073_b200.estimator import BatchSolver
 
@@ -390,7 +392,7 @@ def solve_rate(torch, dev, stream, flush, cfg, steps, warmup, B=None, start=0):
     n = simdata.CONFIGS[cfg][1]
     Y = simdata.batch(SEED, cfg, B, start=start)
     ydev = torch.from_numpy(Y).to(dev)
-    solver = BatchSolver(n, B, EstimatorOptions(grid_factor=4, backend="superfast"), device=dev)
+    solver = BatchSolver(n, B, EstimatorOptions(grid_factor=4, backend=backend), device=dev)
     ms = time_steps(torch, stream, lambda: solver.solve(ydev), steps, warmup, flush)
     h = solver.host_outputs()
     return Y, solver, ms, h
@@ -532,6 +534,16 @@ def run_ours(args):
                           "k_hat_mean": float(np.mean(hc["k_hat"])),
                           "roofline": grid_roofline(torch, dev, stream, flush, simdata.CONFIGS[c][1])}
                 pc["config"] = config_dict(c, 1, simdata.CONFIGS[c][0])
+                if simdata.CONFIGS[c][1] < 512:
+                    # the reference's backend="auto" picks the semifast (Woodbury) engine below
+                    # N = 512 (model_core.py:466-472): the same batch through that backend
+                    _, s, ms, hc = solve_rate(torch, dev, stream, flush, c, 3, 3, backend="semifast")
+                    del s
+                    mps = float(np.mean(ms))
+                    pc["auto_backend"] = {"backend": "semifast", "value": simdata.CONFIGS[c][0] / (mps / 1000.0),
+                                          "ms_per_step": mps, "steps": 3,
+                                          "status_nonzero": int(np.count_nonzero(hc["status"])),
+                                          "k_hat_mean": float(np.mean(hc["k_hat"]))}
                 if pool is not None and c in cpu_cfgs:
                     pc["cpu_baseline"] = cpu if c == cfg else cpu_sample(pool, c, args.cpu_seconds,
                                                                           simdata.CONFIGS[c][0])
