@@ -31,9 +31,6 @@ constexpr int kDncLeaf = 32;
 #ifndef SLSE_DNC_LEAF2
 #define SLSE_DNC_LEAF2 1  // block leaves take two Schur steps per barrier (dnc_leaf_block2)
 #endif
-#ifndef SLSE_DNC_REG_LEAF
-#define SLSE_DNC_REG_LEAF 0  // 1: leaves of s <= nt / 2 steps in registers (dnc_leaf_regs; measured 11.9 M vs 10.4 M cycles at N = 16384: off)
-#endif
 #ifndef SLSE_DNC_BLOCK_LEAF
 #define SLSE_DNC_BLOCK_LEAF 256  // CTA-wide leaves up to this many steps (0 / 32: one-warp leaves only)
 #endif
@@ -562,133 +559,6 @@ SLSE_NI void dnc_leaf_block2(DncCtx& X, const cplx* E1, const cplx* Bw, int s, c
 #endif
 }
 
-// Register leaf: s <= nt / 2 steps, the block-leaf recursion with every
-// value in registers.  Threads [0, G), G = nt / 2, hold one generator slot
-// each in the shifted frame (thread j: e_{t+j}, b_j; E moves down one slot
-// per step by shuffle, lane 31 taking the next warp's first slot through a
-// double-buffered boundary cell); thread 1 forms the next reflection
-// coefficient.  Threads [G, nt) hold Theta coefficient i = tid - G of all
-// four polynomials (the last thread also coefficient G); coefficient i
-// needs coefficient i - 1 of Theta_21 / Theta_22 from the previous step:
-// shuffle up, lane 0 through a boundary cell.  One barrier per step and no
-// shared-memory round trip on any item.
-SLSE_NI void dnc_leaf_regs(DncCtx& X, const cplx* E1, const cplx* Bw, int s, cplx* T, Blk& b) {
-#ifdef SLSE_HOST_EMU
-  dnc_leaf(X, E1, Bw, s, T, b);
-#else
-  const int tid = b.tid, nt = b.nt, G = nt >> 1;
-  const int lane = tid & 31, warp = tid >> 5, nwg = G >> 5;  // warps per half
-  const bool gen = tid < G;
-  const int j = gen ? tid : tid - G;  // generator slot / Theta coefficient
-  const int wh = gen ? warp : warp - nwg;  // warp index within the half
-  const int ld = s + 1;
-  __builtin_assume(__isShared(X.f.smem));
-  cplx* kb = X.f.smem;        // [2]
-  cplx* bnd = kb + 2;         // [2][nwg] generator boundary (first slot of warp w, post-update)
-  cplx* bth = bnd + 2 * nwg;  // [2][nwg][2] Theta_21 / Theta_22 of each warp's lane 31
-  const cplx z = mk(0.0, 0.0);
-  cplx ej = z, bj = z, t11 = z, t12 = z, t21 = z, t22 = z, x11 = z, x12 = z, x21 = z, x22 = z;
-  if (gen) {
-    if (j < s) {
-      ej = E1[j];
-      bj = Bw[j];
-    }
-  } else if (j == 0) {
-    t11 = mk(1.0, 0.0);
-    t22 = mk(1.0, 0.0);
-  }
-  const bool xtra = tid == nt - 1;  // also holds Theta coefficient G
-  double d = X.d;
-  double* dtmp = X.delta_tmp + X.step;
-  const double floor_ = X.floor_;
-  double kr, ki;
-  {
-    const cplx e0 = E1[0];
-    const double inv = 1.0 / d;
-    kr = -e0.re * inv;
-    ki = -e0.im * inv;
-  }
-  if (!gen && lane == 31) {  // coefficient j of Theta_21 / 22 for the next warp's lane 0 (step 0)
-    bth[(0 * nwg + wh) * 2] = t21;
-    bth[(0 * nwg + wh) * 2 + 1] = t22;
-  }
-  b.sync();
-  int st = 0;
-  for (int t = 0; t < s; ++t) {
-    const int q = t & 1;
-    const double dn = d * (1.0 - (kr * kr + ki * ki));
-    if (gen) {
-      const cplx en = mk(fma(kr, bj.re, fma(-ki, bj.im, ej.re)), fma(kr, bj.im, fma(ki, bj.re, ej.im)));
-      bj = mk(fma(kr, ej.re, fma(ki, ej.im, bj.re)), fma(kr, ej.im, fma(-ki, ej.re, bj.im)));
-      if (tid == 1) {
-        const double invn = rcp_pos(dn);
-        kb[(t + 1) & 1] = mk(-en.re * invn, -en.im * invn);
-      }
-      if (lane == 0 && wh > 0) bnd[q * nwg + wh] = en;
-      const double sr = __shfl_down_sync(0xffffffffu, en.re, 1);
-      const double si = __shfl_down_sync(0xffffffffu, en.im, 1);
-      ej = mk(sr, si);  // lane 31 fixed after the barrier
-    } else {
-      // coefficient j - 1 of the old Theta_21 / Theta_22
-      const double ar = __shfl_up_sync(0xffffffffu, t21.re, 1), ai = __shfl_up_sync(0xffffffffu, t21.im, 1);
-      const double cr = __shfl_up_sync(0xffffffffu, t22.re, 1), ci = __shfl_up_sync(0xffffffffu, t22.im, 1);
-      cplx p21 = mk(ar, ai), p22 = mk(cr, ci);
-      if (lane == 0) {
-        if (wh > 0) {
-          p21 = bth[(q * nwg + wh - 1) * 2];
-          p22 = bth[(q * nwg + wh - 1) * 2 + 1];
-        } else {
-          p21 = z;
-          p22 = z;
-        }
-      }
-      const cplx kk = mk(kr, ki), kc = mk(kr, -ki);
-      if (xtra) {  // coefficient G reads this thread's own old coefficient G - 1
-        const cplx m11 = cadd(x11, cmul(kk, t21)), m12 = cadd(x12, cmul(kk, t22));
-        const cplx m21 = cadd(cmul(kc, x11), t21), m22 = cadd(cmul(kc, x12), t22);
-        x11 = m11; x12 = m12; x21 = m21; x22 = m22;
-      }
-      const cplx n11 = cadd(t11, cmul(kk, p21)), n12 = cadd(t12, cmul(kk, p22));
-      const cplx n21 = cadd(cmul(kc, t11), p21), n22 = cadd(cmul(kc, t12), p22);
-      t11 = n11; t12 = n12; t21 = n21; t22 = n22;
-      if (lane == 31) {
-        bth[(((t + 1) & 1) * nwg + wh) * 2] = t21;
-        bth[(((t + 1) & 1) * nwg + wh) * 2 + 1] = t22;
-      }
-    }
-    d = dn;
-    if (tid == 0) dtmp[t + 1] = d;
-    if (!(d > floor_)) {  // uniform: every thread holds the same d
-      st = kNotPD;
-      break;
-    }
-    b.sync();
-    if (gen && lane == 31) ej = (wh + 1 < nwg) ? bnd[q * nwg + wh + 1] : z;
-    const cplx kn = kb[(t + 1) & 1];
-    kr = kn.re;
-    ki = kn.im;
-  }
-  if (!st && !gen) {
-    if (j < ld) {
-      T[j] = t11;
-      T[ld + j] = t12;
-      T[2 * ld + j] = t21;
-      T[3 * ld + j] = t22;
-    }
-    if (xtra && G < ld) {
-      T[G] = x11;
-      T[ld + G] = x12;
-      T[2 * ld + G] = x21;
-      T[3 * ld + G] = x22;
-    }
-  }
-  b.sync();
-  X.d = d;
-  X.step += s;
-  if (st) X.status = st;
-#endif
-}
-
 // forward transform of src[0..len) zero padded to F -> dst[0..F)
 SLSE_D void dnc_fwd(cplx* dst, const cplx* src, int len, int F, cplx* work, const FftCtx& f, Blk& b) {
   fft(work, F, -1.0, [=](int i) { return i < len ? src[i] : mk(0.0, 0.0); },
@@ -756,9 +626,6 @@ SLSE_NI void dnc_split(DncCtx& X, const cplx* E0, const cplx* Bw0, int s0, cplx*
     const long long t0 = prof ? dnc_clock() : 0;
     if (s <= X.leaf_max) {
       if (s <= kDncLeaf && X.leaf_max <= kDncLeaf) dnc_leaf(X, cf.E + 1, cf.Bw, s, cf.T, b);
-#if SLSE_DNC_REG_LEAF
-      else if (2 * s <= b.nt) dnc_leaf_regs(X, cf.E + 1, cf.Bw, s, cf.T, b);
-#endif
 #if SLSE_DNC_LEAF2
       else if (s <= b.nt && 12 * s + 50 <= X.f.smem_cap) dnc_leaf_block2(X, cf.E + 1, cf.Bw, s, cf.T, b);
 #endif
